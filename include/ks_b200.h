@@ -1,0 +1,195 @@
+/* ks_b200.h -- the drop-in C-ABI of the B200 constrained-beam-decode engine.
+ *
+ * Plain C types only (no torch, no C++).  Everything the reference's
+ * `kernelseer` C++/Python API needs for the hot path -- model load, encode,
+ * greedy / beam / constrained beam search over a batch of problem
+ * descriptors, predicate registration -- crosses this boundary.  The C++
+ * host layer (include/kernelseer_b200/*.hpp) and the Python module are
+ * written on top of it; INTEGRATION.md shows the bindings a maintainer of
+ * the reference would add.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj):
+ *   ks_checkpoint_*            load_checkpoint          src/data.cpp:513-665, include/kernelseer/data.hpp:77
+ *   ks_engine_create           SequencePredictor ctor   src/models.cpp:377-379, include/kernelseer/models.hpp:80-98
+ *   ks_encode_problems         encode_problem           src/encoding.cpp:87-113, include/kernelseer/encoding.hpp:80-81
+ *   ks_beam_search_batch       beam_search /            src/decoding.cpp:27-103, 126-135
+ *                              constrained_beam_search  include/kernelseer/decoding.hpp:28-36
+ *   ks_greedy_batch            greedy_decode            src/decoding.cpp:107-124, include/kernelseer/decoding.hpp:23-24
+ *   ks_pred (typed programs)   ConstraintPredicate +    include/kernelseer/constraints.hpp:45-63,
+ *                              membership_predicate /   src/constraints.cpp:198-242
+ *                              resource_budget_predicate
+ *   ks_status                  exception taxonomy       include/kernelseer/errors.hpp:10-87
+ *   the batch entry points     parallel_stripes fan-out include/kernelseer/parallel.hpp:14-27 as used
+ *                              in topk_metrics          src/eval.cpp:105-137
+ */
+#ifndef KS_B200_H
+#define KS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One status code per reference exception class (errors.hpp). */
+typedef enum {
+    KS_OK = 0,
+    KS_ERR_SHAPE = 1,          /* ShapeError */
+    KS_ERR_PARAMETER = 2,      /* ParameterError (beam width < 1, bad sizes, ...) */
+    KS_ERR_INDEX = 3,          /* IndexError (token id out of range) */
+    KS_ERR_STATE = 4,          /* StateError (missing tensor, stepping past the end) */
+    KS_ERR_VALIDATION = 5,     /* ValidationError (out-of-vocabulary descriptor field) */
+    KS_ERR_CHECKPOINT = 6,     /* CheckpointError; see ks_checkpoint_error_kind */
+    KS_ERR_BEAM_EXHAUSTED = 7, /* BeamExhaustedError (single-config calls only; batch calls
+                                  report exhaustion per row in out_status) */
+    KS_ERR_CUDA = 8,           /* device / driver failure */
+    KS_ERR_UNSUPPORTED = 9     /* model variant or shape this engine does not implement */
+} ks_status;
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+const char* ks_last_error(void);
+/* For KS_ERR_VALIDATION: the offending field name (ValidationError::field). */
+const char* ks_last_error_field(void);
+
+/* ------------------------------------------------------------------------- */
+/* Checkpoint: kernelseer-checkpoint/1 (docs/formats.md:53-93)                */
+/* ------------------------------------------------------------------------- */
+typedef struct ks_checkpoint ks_checkpoint;
+
+/* CheckpointError kinds (errors.hpp:66-74): 0 version, 1 truncated, 2 shape,
+ * 3 malformed, 4 io. */
+ks_status ks_checkpoint_load(const char* path, ks_checkpoint** out);
+int32_t ks_checkpoint_error_kind(void);
+void ks_checkpoint_free(ks_checkpoint* ck);
+/* Header value by key ("variant", "kernel", "post_attention_size", ...); NULL if absent. */
+const char* ks_checkpoint_header(const ks_checkpoint* ck, const char* key);
+int32_t ks_checkpoint_num_tensors(const ks_checkpoint* ck);
+/* i-th tensor in payload (= alphabetical) order: name, rank, dims[3], fp32 data. */
+ks_status ks_checkpoint_tensor(const ks_checkpoint* ck, int32_t i, const char** name,
+                               int32_t* rank, int32_t* dims, const float** data);
+
+/* ------------------------------------------------------------------------- */
+/* Model description for engine creation (the fields of ModelParams,         */
+/* models.hpp:45-53, flattened).                                              */
+/* ------------------------------------------------------------------------- */
+enum { KS_VARIANT_ENC_DEC = 0, KS_VARIANT_ATTN = 1, KS_VARIANT_ATTN2 = 2,
+       KS_VARIANT_HYBRID = 3, KS_VARIANT_HYBRID2 = 4 };
+
+typedef struct {
+    int32_t variant;              /* KS_VARIANT_* (ModelVariant, models.hpp:16) */
+    int32_t encoder_state_size;   /* |e| */
+    int32_t pre_attention_size;   /* n_a (per direction) */
+    int32_t post_attention_size;  /* n_s */
+    int32_t attention_dense_nodes;/* n_d */
+    int32_t num_positions;        /* T_out */
+    const int32_t* input_sizes;   /* 7 input-field vocabulary sizes (order n,c,h,w,k,y,x) */
+    const int64_t* input_values;  /* concatenated input values, ascending per field */
+    const int32_t* vocab_sizes;   /* T_out output-parameter vocabulary sizes */
+    const int64_t* output_values; /* concatenated output values in spec order */
+    int32_t num_tensors;
+    const char* const* tensor_names; /* reference names: "post.w_input", "head.3.bias", ... */
+    const int32_t* tensor_numel;
+    const float* const* tensor_data; /* fp32 (checkpoints are fp32, data.cpp:447-460) */
+} ks_model_desc;
+
+/* Arithmetic of the gate GEMMs (the 99.6% of FLOPs):
+ *   KS_PREC_F16X3: tcgen05 tensor cores, fp16 hi/lo operand split with three
+ *                  MMAs (hi*hi + hi*lo + lo*hi), fp32 accumulate in TMEM --
+ *                  fp32-grade accuracy; the default and the parity path.
+ *   KS_PREC_FP32:  CUDA-core fp32 FFMA (exact fp32 GEMM); a second parity path.
+ *   KS_PREC_BF16:  tcgen05 single bf16 MMA, fp32 accumulate -- reduced precision,
+ *                  reported as decoded-sequence agreement. */
+enum { KS_PREC_F16X3 = 0, KS_PREC_FP32 = 1, KS_PREC_BF16 = 2 };
+
+typedef struct ks_engine ks_engine;
+
+ks_status ks_engine_create(const ks_model_desc* model, int32_t device, int32_t precision,
+                           ks_engine** out);
+ks_status ks_engine_create_from_checkpoint(const char* path, int32_t device, int32_t precision,
+                                           ks_engine** out);
+void ks_engine_destroy(ks_engine* eng);
+
+int32_t ks_engine_num_positions(const ks_engine* eng);
+int32_t ks_engine_vocab_size(const ks_engine* eng, int32_t position);
+int32_t ks_engine_precision(const ks_engine* eng);
+/* Number of kernel launches issued by the last decode call (evidence for bench). */
+int64_t ks_engine_last_launch_count(const ks_engine* eng);
+/* Configs per internal chunk (device workspace is sized for it); 0 = default. */
+ks_status ks_engine_set_chunk(ks_engine* eng, int64_t configs_per_chunk);
+
+/* encode_problem for B descriptors (B x 7 int64, field order n,c,h,w,k,y,x):
+ * writes B x 7 token ids.  allow_nearest snaps unknown values (FieldVocab::nearest,
+ * encoding.cpp:26-34).  On an unknown value returns KS_ERR_VALIDATION naming
+ * the field of the first failing row; *bad_row receives its index. */
+ks_status ks_encode_problems(const ks_engine* eng, const int64_t* desc, int64_t B,
+                             int32_t allow_nearest, int32_t* tok, int64_t* bad_row);
+
+/* ------------------------------------------------------------------------- */
+/* Typed predicate programs.  ConstraintPredicate::fn is an opaque callable in  */
+/* the reference (constraints.hpp:49); the engine evaluates these typed forms */
+/* on the device.  Registration order = evaluation order; the first rejecting */
+/* predicate discards the candidate (decoding.cpp:69-76).                     */
+/* ------------------------------------------------------------------------- */
+enum {
+    KS_PRED_MASK = 1,     /* allowed[value_offset(p) + token] for every assigned position:
+                             membership_predicate and other per-value tables */
+    KS_PRED_BUDGET = 2,   /* resource_budget_predicate: cost = sum over terms (ALPHABETICAL
+                             parameter-name order) of w * value for assigned params, fp64
+                             with separate multiply and add; accept iff cost <= budget */
+    KS_PRED_PRODUCT = 3,  /* scale * prod(values of assigned listed params) <= limit
+                             (workgroup size, LDS bytes); no reference counterpart */
+    KS_PRED_DIVIDES = 4   /* each assigned listed param value v > 0 divides the descriptor
+                             field term_field[i] (tile divisibility); no reference counterpart */
+};
+
+typedef struct {
+    int32_t kind;
+    int32_t full_sequence_only;   /* evaluate only at the last position (decoding.cpp:67-70) */
+    const uint8_t* allowed;       /* MASK: sum_p vocab_size(p) entries */
+    int32_t n_terms;
+    const int32_t* term_pos;      /* output position per term; -1 = never assigned */
+    const double* term_w;         /* BUDGET weights, terms in alphabetical name order */
+    const int32_t* term_field;    /* DIVIDES descriptor field per term (0..6) */
+    double budget;                /* BUDGET */
+    int64_t scale;                /* PRODUCT */
+    int64_t limit;                /* PRODUCT */
+} ks_pred;
+
+/* ------------------------------------------------------------------------- */
+/* Decode.  Host-pointer entry points (the reference-facing call; copies are  */
+/* part of the call).  tok: B x 7 token ids; desc: B x 7 descriptor values,   */
+/* only read by KS_PRED_DIVIDES (may be NULL otherwise).                      */
+/* Outputs: out_tok B x k x T (rank order, -1 padded), out_lp B x k (fp64),   */
+/* out_count B (beams returned), out_status B (0 ok, 1 exhausted),            */
+/* out_fail_pred / out_fail_step B (BeamExhaustedError::predicate index and   */
+/* step, -1 when ok).  Any output pointer except out_tok may be NULL.          */
+/* ------------------------------------------------------------------------- */
+ks_status ks_beam_search_batch(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                               int64_t B, int32_t beam_width, const ks_pred* preds,
+                               int32_t n_preds, int32_t* out_tok, double* out_lp,
+                               int32_t* out_count, int32_t* out_status,
+                               int32_t* out_fail_pred, int32_t* out_fail_step);
+
+/* greedy_decode: out_tok B x T. */
+ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok);
+
+/* Device-resident variant: every pointer is device memory; runs on `stream`
+ * (a cudaStream_t, NULL = legacy default) and returns without synchronising. */
+ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok, const int64_t* d_desc,
+                                int64_t B, int32_t beam_width, const ks_pred* preds,
+                                int32_t n_preds, int32_t* d_out_tok, double* d_out_lp,
+                                int32_t* d_out_count, int32_t* d_out_status,
+                                int32_t* d_out_fail_pred, int32_t* d_out_fail_step,
+                                void* stream);
+
+/* Kernel-level timing hook for bench.py: accumulated device milliseconds of
+ * the gate-GEMM launches (CUDA events on the launching stream) since the last
+ * reset, and their count. */
+void ks_engine_profile_reset(ks_engine* eng, int32_t enable);
+double ks_engine_profile_gemm_ms(const ks_engine* eng, int64_t* launches, double* useful_flops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_B200_H */

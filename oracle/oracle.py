@@ -1,0 +1,355 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes view of the CPU checkers in oracle/_ref.
+
+* ``OracleModel``: our plain-C fp64 restatement (ks_oracle.c) of the
+  reference hot path (proj/src/models.cpp:387-493, proj/src/decoding.cpp:27-135,
+  proj/src/constraints.cpp:198-242, proj/src/data.cpp:513-665).
+* ``RefModel``: the unmodified reference core compiled from
+  /root/reference/proj/src (oracle/Makefile), driven through ref_shim.cpp.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline/reference
+legs may import this module, and only as the checker.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_DIR = os.path.join(HERE, "_ref")
+
+PRED_MASK, PRED_BUDGET, PRED_PRODUCT, PRED_DIVIDES = 1, 2, 3, 4
+
+
+class _Pred(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int),
+        ("full_sequence_only", C.c_int),
+        ("allowed", C.POINTER(C.c_uint8)),
+        ("n_terms", C.c_int),
+        ("term_pos", C.POINTER(C.c_int32)),
+        ("term_w", C.POINTER(C.c_double)),
+        ("term_field", C.POINTER(C.c_int32)),
+        ("budget", C.c_double),
+        ("scale", C.c_int64),
+        ("limit", C.c_int64),
+    ]
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct)) if a is not None else None
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(REF_DIR, "libks_oracle.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle oracle`")
+        L = C.CDLL(path)
+        L.kso_load.restype = C.c_void_p
+        L.kso_load.argtypes = [C.c_char_p]
+        L.kso_free.argtypes = [C.c_void_p]
+        L.kso_last_error.restype = C.c_char_p
+        for fn in ("kso_variant", "kso_num_positions"):
+            getattr(L, fn).argtypes = [C.c_void_p]
+        L.kso_vocab_size.argtypes = [C.c_void_p, C.c_int]
+        L.kso_output_name.argtypes = [C.c_void_p, C.c_int]
+        L.kso_output_name.restype = C.c_char_p
+        L.kso_input_vocab_size.argtypes = [C.c_void_p, C.c_int]
+        L.kso_input_value.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.kso_input_value.restype = C.c_int64
+        L.kso_output_value.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.kso_output_value.restype = C.c_int64
+        L.kso_tensor.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_int)]
+        L.kso_tensor.restype = C.POINTER(C.c_double)
+        L.kso_encode_problem.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        L.kso_beam_batch.argtypes = [
+            C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.c_int64, C.c_int,
+            C.POINTER(_Pred), C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+            C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+            C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+        L.kso_greedy.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.kso_forward.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_double)]
+        L.kso_encode.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+        _lib = L
+    return _lib
+
+
+class OracleModel:
+    """A checkpoint loaded into the fp64 C restatement."""
+
+    def __init__(self, path: str):
+        L = lib()
+        self._h = L.kso_load(path.encode())
+        if not self._h:
+            raise RuntimeError("oracle load failed: " + L.kso_last_error().decode())
+        self.T = L.kso_num_positions(self._h)
+        self.vsizes = [L.kso_vocab_size(self._h, p) for p in range(self.T)]
+        self.names = [L.kso_output_name(self._h, p).decode() for p in range(self.T)]
+        self.values = [[L.kso_output_value(self._h, p, i) for i in range(v)]
+                       for p, v in enumerate(self.vsizes)]
+        self.input_values = [[L.kso_input_value(self._h, f, i)
+                              for i in range(L.kso_input_vocab_size(self._h, f))]
+                             for f in range(7)]
+        self.variant = L.kso_variant(self._h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().kso_free(self._h)
+            self._h = None
+
+    def tensor(self, name: str) -> np.ndarray:
+        n = C.c_int(0)
+        ptr = lib().kso_tensor(self._h, name.encode(), C.byref(n))
+        if not ptr:
+            raise KeyError(name)
+        return np.ctypeslib.as_array(ptr, shape=(n.value,))
+
+    # -- predicate programs -------------------------------------------------
+    def membership(self, spec_values=None, full_sequence_only=False):
+        """membership_predicate (constraints.cpp:198-218) as a static token mask.
+        spec_values: {name: [legal values]} (defaults to the model's own spec)."""
+        allowed = []
+        for p in range(self.T):
+            legal = self.values[p] if spec_values is None else spec_values[self.names[p]]
+            allowed += [1 if v in legal else 0 for v in self.values[p]]
+        return {"kind": PRED_MASK, "allowed": np.array(allowed, np.uint8),
+                "full": full_sequence_only}
+
+    def mask(self, allowed_by_pos, full_sequence_only=False):
+        flat = np.concatenate([np.asarray(a, np.uint8) for a in allowed_by_pos])
+        return {"kind": PRED_MASK, "allowed": flat, "full": full_sequence_only}
+
+    def budget(self, weights: dict, budget: float, full_sequence_only=False):
+        """resource_budget_predicate (constraints.cpp:220-242): std::map order."""
+        names = sorted(weights)
+        pos = [self.names.index(n) if n in self.names else -1 for n in names]
+        return {"kind": PRED_BUDGET, "term_pos": np.array(pos, np.int32),
+                "term_w": np.array([weights[n] for n in names], np.float64),
+                "budget": float(budget), "full": full_sequence_only}
+
+    def product(self, names, scale, limit, full_sequence_only=False):
+        pos = [self.names.index(n) if n in self.names else -1 for n in names]
+        return {"kind": PRED_PRODUCT, "term_pos": np.array(pos, np.int32),
+                "scale": int(scale), "limit": int(limit), "full": full_sequence_only}
+
+    def divides(self, pairs, full_sequence_only=False):
+        """pairs: [(param name, descriptor field index)]"""
+        pos = [self.names.index(n) if n in self.names else -1 for n, _ in pairs]
+        return {"kind": PRED_DIVIDES, "term_pos": np.array(pos, np.int32),
+                "term_field": np.array([f for _, f in pairs], np.int32),
+                "full": full_sequence_only}
+
+    def _pack(self, preds):
+        arr = (_Pred * max(1, len(preds)))()
+        keep = []
+        for i, d in enumerate(preds):
+            a = arr[i]
+            a.kind = d["kind"]
+            a.full_sequence_only = int(bool(d.get("full", False)))
+            for key, field, ct in (("allowed", "allowed", C.c_uint8),
+                                   ("term_pos", "term_pos", C.c_int32),
+                                   ("term_w", "term_w", C.c_double),
+                                   ("term_field", "term_field", C.c_int32)):
+                if key in d:
+                    v = np.ascontiguousarray(d[key])
+                    keep.append(v)
+                    setattr(a, field, _p(v, ct))
+            if "term_pos" in d:
+                a.n_terms = len(d["term_pos"])
+            a.budget = d.get("budget", 0.0)
+            a.scale = d.get("scale", 1)
+            a.limit = d.get("limit", 0)
+        return arr, keep
+
+    # -- decode ---------------------------------------------------------------
+    def encode_problem(self, desc):
+        desc = np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
+        tok = np.zeros(desc.shape, np.int32)
+        bad = np.zeros(len(desc), np.int32)
+        for b in range(len(desc)):
+            bad[b] = lib().kso_encode_problem(self._h, _p(desc[b], C.c_int64), _p(tok[b], C.c_int32))
+        return tok, bad
+
+    def beam(self, tok, k, desc=None, preds=(), threads=1):
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        B = len(tok)
+        desc = (np.ascontiguousarray(desc, np.int64).reshape(-1, 7) if desc is not None
+                else np.zeros((B, 7), np.int64))
+        out_tok = np.full((B, k, self.T), -1, np.int32)
+        out_lp = np.full((B, k), -np.inf, np.float64)
+        cnt = np.zeros(B, np.int32)
+        st = np.zeros(B, np.int32)
+        fp = np.full(B, -1, np.int32)
+        fs = np.full(B, -1, np.int32)
+        gap = np.zeros(B, np.float64)
+        arr, keep = self._pack(list(preds))
+        lib().kso_beam_batch(self._h, _p(tok, C.c_int32), _p(desc, C.c_int64), B, k, arr,
+                             len(preds), threads, _p(out_tok, C.c_int32), _p(out_lp, C.c_double),
+                             _p(cnt, C.c_int32), _p(st, C.c_int32), _p(fp, C.c_int32),
+                             _p(fs, C.c_int32), _p(gap, C.c_double))
+        return {"tokens": out_tok, "log_prob": out_lp, "count": cnt, "status": st,
+                "fail_pred": fp, "fail_step": fs, "min_gap": gap}
+
+    def greedy(self, tok):
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        out = np.zeros((len(tok), self.T), np.int32)
+        for b in range(len(tok)):
+            rc = lib().kso_greedy(self._h, _p(tok[b], C.c_int32), _p(out[b], C.c_int32))
+            if rc:
+                raise ValueError("bad input tokens")
+        return out
+
+    def forward(self, tok7, teacher=None):
+        tok7 = np.ascontiguousarray(tok7, np.int32)
+        out = np.zeros(sum(self.vsizes), np.float64)
+        t = None if teacher is None else np.ascontiguousarray(teacher, np.int32)
+        lib().kso_forward(self._h, _p(tok7, C.c_int32), _p(t, C.c_int32), _p(out, C.c_double))
+        res, o = [], 0
+        for v in self.vsizes:
+            res.append(out[o:o + v].copy())
+            o += v
+        return res
+
+    def score(self, tok7, seq):
+        """Teacher-forced sequence score (decoding_test.cpp:38-46)."""
+        import math
+        d = self.forward(tok7, seq)
+        return sum(math.log(max(d[i][s], 1e-300)) for i, s in enumerate(seq))
+
+    def encode(self, tok7):
+        out = np.zeros(7 * 2 * 4096, np.float64)
+        rc = lib().kso_encode(self._h, _p(np.ascontiguousarray(tok7, np.int32), C.c_int32),
+                              _p(out, C.c_double))
+        if rc:
+            raise ValueError("encode failed")
+        return out
+
+
+# ---------------------------------------------------------------------------
+# The unmodified reference, compiled from its sources (oracle/Makefile `ref`)
+# ---------------------------------------------------------------------------
+_rlib = None
+
+
+def ref_available() -> bool:
+    return os.path.exists(os.path.join(REF_DIR, "libkernelseer_ref.so"))
+
+
+def rlib():
+    global _rlib
+    if _rlib is None:
+        L = C.CDLL(os.path.join(REF_DIR, "libkernelseer_ref.so"))
+        L.ksref_last_error.restype = C.c_char_p
+        L.ksref_load.restype = C.c_void_p
+        L.ksref_load.argtypes = [C.c_char_p]
+        L.ksref_free.argtypes = [C.c_void_p]
+        L.ksref_num_positions.argtypes = [C.c_void_p]
+        L.ksref_vocab_size.argtypes = [C.c_void_p, C.c_int]
+        L.ksref_encode.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_int32)]
+        L.ksref_beam_batch.argtypes = [
+            C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.c_int64, C.c_int,
+            C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+            C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_char_p]
+        L.ksref_greedy_batch.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64, C.c_int,
+                                         C.POINTER(C.c_int32)]
+        L.ksref_forward.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_double)]
+        L.ksref_init_save.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.c_char_p, C.c_int, C.c_uint64, C.c_char_p, C.c_uint64,
+                                      C.c_char_p]
+        L.ksref_init_save_spec.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_uint64, C.c_char_p]
+        L.ksref_synthetic.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_char_p,
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        _rlib = L
+    return _rlib
+
+
+def ref_init_save(path, variant="attn", e_size=256, n_a=256, n_s=512, n_d=2, cell=256,
+                  kernel="ConvAsm1x1U", synth_count=5000, synth_seed=7,
+                  difficulty="moderate", init_seed=1):
+    rc = rlib().ksref_init_save(variant.encode(), e_size, n_a, n_s, n_d, cell, kernel.encode(),
+                                synth_count, synth_seed, difficulty.encode(), init_seed,
+                                path.encode())
+    if rc:
+        raise RuntimeError(rlib().ksref_last_error().decode())
+
+
+def ref_init_save_spec(path, variant, spec_line, seed, cell=6):
+    """tiny_model (proj/tests/test_util.hpp:74-88) over a custom spec line."""
+    rc = rlib().ksref_init_save_spec(variant.encode(), cell, spec_line.encode(), seed, path.encode())
+    if rc:
+        raise RuntimeError(rlib().ksref_last_error().decode())
+
+
+def ref_synthetic(kernel, count, seed, difficulty="moderate", T=None):
+    desc = np.zeros((count, 7), np.int64)
+    params = np.zeros((count, T), np.int32) if T else None
+    rc = rlib().ksref_synthetic(kernel.encode(), count, seed, difficulty.encode(),
+                                _p(desc, C.c_int64), _p(params, C.c_int32))
+    if rc:
+        raise RuntimeError(rlib().ksref_last_error().decode())
+    return desc, params
+
+
+class RefModel:
+    def __init__(self, path: str):
+        self._h = rlib().ksref_load(path.encode())
+        if not self._h:
+            raise RuntimeError(rlib().ksref_last_error().decode())
+        self.T = rlib().ksref_num_positions(self._h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            rlib().ksref_free(self._h)
+            self._h = None
+
+    def encode(self, desc):
+        desc = np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
+        tok = np.zeros(desc.shape, np.int32)
+        bad = rlib().ksref_encode(self._h, _p(desc, C.c_int64), len(desc), _p(tok, C.c_int32))
+        return tok, bad
+
+    def beam(self, tok, k, desc=None, preds_text="", threads=1):
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        B = len(tok)
+        desc = (np.ascontiguousarray(desc, np.int64).reshape(-1, 7) if desc is not None
+                else np.zeros((B, 7), np.int64))
+        out_tok = np.full((B, k, self.T), -1, np.int32)
+        out_lp = np.full((B, k), -np.inf, np.float64)
+        cnt = np.zeros(B, np.int32)
+        st = np.zeros(B, np.int32)
+        fs = np.zeros(B, np.int32)
+        names = C.create_string_buffer(64 * B)
+        rc = rlib().ksref_beam_batch(self._h, _p(tok, C.c_int32), _p(desc, C.c_int64), B, k,
+                                     preds_text.encode(), threads, _p(out_tok, C.c_int32),
+                                     _p(out_lp, C.c_double), _p(cnt, C.c_int32), _p(st, C.c_int32),
+                                     _p(fs, C.c_int32), names)
+        if rc:
+            raise RuntimeError(rlib().ksref_last_error().decode())
+        raw = names.raw
+        fail_names = [raw[64 * b:64 * b + 64].split(b"\0", 1)[0].decode() for b in range(B)]
+        return {"tokens": out_tok, "log_prob": out_lp, "count": cnt, "status": st,
+                "fail_step": fs, "fail_name": fail_names}
+
+    def greedy(self, tok, threads=1):
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        out = np.zeros((len(tok), self.T), np.int32)
+        rc = rlib().ksref_greedy_batch(self._h, _p(tok, C.c_int32), len(tok), threads,
+                                       _p(out, C.c_int32))
+        if rc:
+            raise RuntimeError(rlib().ksref_last_error().decode())
+        return out
+
+    def forward(self, tok7, teacher=None, total=None):
+        out = np.zeros(total or 4096, np.float64)
+        t = None if teacher is None else np.ascontiguousarray(teacher, np.int32)
+        rlib().ksref_forward(self._h, _p(np.ascontiguousarray(tok7, np.int32), C.c_int32),
+                             _p(t, C.c_int32), _p(out, C.c_double))
+        return out

@@ -1,0 +1,232 @@
+"""ctypes view of the engine's C-ABI (include/ks_b200.h).
+
+This is the thin host binding used by tests and bench.py; the reference-style
+API (``predict``, ``topk_metrics`` ...) lives in ``paper_2404_10162_b200.api``
+and the C++ host library.  The shared library is built in-tree by
+``__graft_entry__.build()``; importing without it raises, there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libks_b200.so")
+
+KS_OK = 0
+STATUS_NAMES = {
+    1: "ShapeError", 2: "ParameterError", 3: "IndexError", 4: "StateError",
+    5: "ValidationError", 6: "CheckpointError", 7: "BeamExhaustedError", 8: "CudaError",
+    9: "UnsupportedError",
+}
+PREC = {"f16x3": 0, "fp32": 1, "bf16": 2}
+PRED_MASK, PRED_BUDGET, PRED_PRODUCT, PRED_DIVIDES = 1, 2, 3, 4
+
+
+class KsError(RuntimeError):
+    """Carries the C-ABI status code (one per reference exception class)."""
+
+    def __init__(self, code: int, msg: str, field: str = ""):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.field = field
+
+
+class KsPred(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("full_sequence_only", C.c_int32),
+        ("allowed", C.POINTER(C.c_uint8)),
+        ("n_terms", C.c_int32),
+        ("term_pos", C.POINTER(C.c_int32)),
+        ("term_w", C.POINTER(C.c_double)),
+        ("term_field", C.POINTER(C.c_int32)),
+        ("budget", C.c_double),
+        ("scale", C.c_int64),
+        ("limit", C.c_int64),
+    ]
+
+
+class KsModelDesc(C.Structure):
+    _fields_ = [
+        ("variant", C.c_int32),
+        ("encoder_state_size", C.c_int32),
+        ("pre_attention_size", C.c_int32),
+        ("post_attention_size", C.c_int32),
+        ("attention_dense_nodes", C.c_int32),
+        ("num_positions", C.c_int32),
+        ("input_sizes", C.POINTER(C.c_int32)),
+        ("input_values", C.POINTER(C.c_int64)),
+        ("vocab_sizes", C.POINTER(C.c_int32)),
+        ("output_values", C.POINTER(C.c_int64)),
+        ("num_tensors", C.c_int32),
+        ("tensor_names", C.POINTER(C.c_char_p)),
+        ("tensor_numel", C.POINTER(C.c_int32)),
+        ("tensor_data", C.POINTER(C.POINTER(C.c_float))),
+    ]
+
+
+_lib = None
+
+EXPORTS = [
+    "ks_last_error", "ks_last_error_field", "ks_checkpoint_load", "ks_checkpoint_error_kind",
+    "ks_checkpoint_free", "ks_checkpoint_header", "ks_checkpoint_num_tensors",
+    "ks_checkpoint_tensor", "ks_engine_create", "ks_engine_create_from_checkpoint",
+    "ks_engine_destroy", "ks_engine_num_positions", "ks_engine_vocab_size",
+    "ks_engine_precision", "ks_engine_last_launch_count", "ks_engine_set_chunk",
+    "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
+    "ks_engine_profile_reset", "ks_engine_profile_gemm_ms",
+]
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct)) if a is not None else None
+
+
+def lib():
+    """Loads libks_b200.so (raises if the extension was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(the engine has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    L.ks_last_error.restype = C.c_char_p
+    L.ks_last_error_field.restype = C.c_char_p
+    L.ks_checkpoint_load.argtypes = [C.c_char_p, P(vp)]
+    L.ks_checkpoint_error_kind.restype = i32
+    L.ks_checkpoint_free.argtypes = [vp]
+    L.ks_checkpoint_header.argtypes = [vp, C.c_char_p]
+    L.ks_checkpoint_header.restype = C.c_char_p
+    L.ks_checkpoint_num_tensors.argtypes = [vp]
+    L.ks_checkpoint_tensor.argtypes = [vp, i32, P(C.c_char_p), P(i32), P(i32), P(P(C.c_float))]
+    L.ks_engine_create.argtypes = [P(KsModelDesc), i32, i32, P(vp)]
+    L.ks_engine_create_from_checkpoint.argtypes = [C.c_char_p, i32, i32, P(vp)]
+    L.ks_engine_destroy.argtypes = [vp]
+    L.ks_engine_num_positions.argtypes = [vp]
+    L.ks_engine_vocab_size.argtypes = [vp, i32]
+    L.ks_engine_precision.argtypes = [vp]
+    L.ks_engine_last_launch_count.argtypes = [vp]
+    L.ks_engine_last_launch_count.restype = i64
+    L.ks_engine_set_chunk.argtypes = [vp, i64]
+    L.ks_encode_problems.argtypes = [vp, P(i64), i64, i32, P(i32), P(i64)]
+    L.ks_beam_search_batch.argtypes = [vp, P(i32), P(i64), i64, i32, P(KsPred), i32, P(i32),
+                                       P(dbl), P(i32), P(i32), P(i32), P(i32)]
+    L.ks_greedy_batch.argtypes = [vp, P(i32), i64, P(i32)]
+    L.ks_beam_search_device.argtypes = [vp, vp, vp, i64, i32, P(KsPred), i32, vp, vp, vp, vp, vp,
+                                        vp, vp]
+    L.ks_engine_profile_reset.argtypes = [vp, i32]
+    L.ks_engine_profile_gemm_ms.argtypes = [vp, P(i64), P(dbl)]
+    L.ks_engine_profile_gemm_ms.restype = dbl
+    _lib = L
+    return L
+
+
+def check(code: int):
+    if code != KS_OK:
+        L = lib()
+        raise KsError(code, L.ks_last_error().decode(), L.ks_last_error_field().decode())
+
+
+def pack_preds(preds):
+    """preds: list of dicts {kind, full, allowed | term_pos/term_w/term_field, budget, scale, limit}."""
+    arr = (KsPred * max(1, len(preds)))()
+    keep = []
+    for i, d in enumerate(preds):
+        a = arr[i]
+        a.kind = d["kind"]
+        a.full_sequence_only = int(bool(d.get("full", False)))
+        for key, ct in (("allowed", C.c_uint8), ("term_pos", C.c_int32), ("term_w", C.c_double),
+                        ("term_field", C.c_int32)):
+            if key in d and d[key] is not None:
+                v = np.ascontiguousarray(d[key])
+                keep.append(v)
+                setattr(a, key, _p(v, ct))
+        if "term_pos" in d:
+            a.n_terms = len(d["term_pos"])
+        a.budget = float(d.get("budget", 0.0))
+        a.scale = int(d.get("scale", 1))
+        a.limit = int(d.get("limit", 0))
+    return arr, keep
+
+
+class Engine:
+    """One engine per GPU; immutable weights, reusable workspace."""
+
+    def __init__(self, checkpoint: str, device: int = 0, precision: str = "f16x3"):
+        L = lib()
+        h = C.c_void_p()
+        check(L.ks_engine_create_from_checkpoint(checkpoint.encode(), device, PREC[precision],
+                                                 C.byref(h)))
+        self._h = h
+        self.T = L.ks_engine_num_positions(h)
+        self.vsizes = [L.ks_engine_vocab_size(h, p) for p in range(self.T)]
+        self.precision = precision
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ks_engine_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_chunk(self, n: int):
+        check(lib().ks_engine_set_chunk(self._h, n))
+
+    def launches(self) -> int:
+        return lib().ks_engine_last_launch_count(self._h)
+
+    def encode(self, desc, allow_nearest=False):
+        desc = np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
+        tok = np.zeros(desc.shape, np.int32)
+        bad = C.c_int64(-1)
+        check(lib().ks_encode_problems(self._h, _p(desc, C.c_int64), len(desc), int(allow_nearest),
+                                       _p(tok, C.c_int32), C.byref(bad)))
+        return tok
+
+    def beam(self, tok, k, desc=None, preds=()):
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        B = len(tok)
+        d = None if desc is None else np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
+        out_tok = np.empty((B, k, self.T), np.int32)
+        out_lp = np.empty((B, k), np.float64)
+        cnt = np.empty(B, np.int32)
+        st = np.empty(B, np.int32)
+        fp = np.empty(B, np.int32)
+        fs = np.empty(B, np.int32)
+        arr, keep = pack_preds(list(preds))
+        check(lib().ks_beam_search_batch(self._h, _p(tok, C.c_int32), _p(d, C.c_int64), B, k, arr,
+                                         len(preds), _p(out_tok, C.c_int32), _p(out_lp, C.c_double),
+                                         _p(cnt, C.c_int32), _p(st, C.c_int32), _p(fp, C.c_int32),
+                                         _p(fs, C.c_int32)))
+        return {"tokens": out_tok, "log_prob": out_lp, "count": cnt, "status": st,
+                "fail_pred": fp, "fail_step": fs}
+
+    def greedy(self, tok):
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        out = np.empty((len(tok), self.T), np.int32)
+        check(lib().ks_greedy_batch(self._h, _p(tok, C.c_int32), len(tok), _p(out, C.c_int32)))
+        return out
+
+    def beam_device(self, d_tok, d_desc, B, k, preds, d_out, stream=0):
+        """All buffers are device pointers (ints); d_out = dict of pointers."""
+        arr, keep = pack_preds(list(preds))
+        check(lib().ks_beam_search_device(self._h, d_tok, d_desc, B, k, arr, len(preds),
+                                          d_out["tokens"], d_out["log_prob"], d_out["count"],
+                                          d_out.get("status"), d_out.get("fail_pred"),
+                                          d_out.get("fail_step"), stream))
+
+    def profile_reset(self, enable=True):
+        lib().ks_engine_profile_reset(self._h, int(enable))
+
+    def profile(self):
+        n = C.c_int64(0)
+        useful = C.c_double(0.0)
+        ms = lib().ks_engine_profile_gemm_ms(self._h, C.byref(n), C.byref(useful))
+        return ms, n.value, useful.value

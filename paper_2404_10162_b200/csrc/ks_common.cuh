@@ -1,0 +1,150 @@
+// ks_common.cuh -- shared device-side types for the B200 beam-decode engine.
+//
+// HBM layout (one decode chunk of C configs, beam width k, padded hidden
+// sizes NA = roundup(n_a, 64), NS = roundup(n_s, 64)):
+//
+//   tok      [C][7]          int32   input token ids
+//   act      [C][7][2NA]     fp32    encoder activations a_t = [fwd_h ; bwd_h]
+//   uatt     [C][7][n_d]     fp32    per-config attention term b_h + a_t.W_a
+//   A        [C*k][2NA+NS]   fp32    (FP32 mode) decoder GEMM operand [ctx ; h_prev]
+//   A_hi/lo  [C*k][2NA+NS]   fp16    (F16X3 / BF16 modes) the same operand, split
+//   h, c     2 x [C*k][NS]   fp32    decoder state, ping-pong by position parity
+//   beam     2 x {live u8, lp f64, key u64, parent i32, slot i32} per slot
+//
+// Rows of position p are r = b * H_p + j (H_p = static live-hypothesis bound,
+// H_0 = 1, H_{p+1} = min(k, H_p * V_p)), so the GEMM M dimension carries no
+// padding beyond the reference's own live counts in the unconstrained case.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+
+namespace ksb {
+
+constexpr int kTin = 7;        // input fields n,c,h,w,k,y,x (problem.hpp:36-38)
+constexpr int kMaxT = 16;      // output positions supported (builtin specs use <= 10)
+constexpr int kMaxV = 32;      // vocabulary per position (lane-per-token in the beam kernel)
+constexpr int kMaxNd = 8;      // attention dense nodes
+
+// Per-position metadata passed by value to the beam kernel.
+struct PosMeta {
+    int T;
+    int vsize[kMaxT];
+    int value_offset[kMaxT];   // into the concatenated output-value table
+    int fb_offset[kMaxT];      // feedback one-hot slot offset (GO = slot 0)
+    int shift[kMaxT];          // packed-prefix key bit offset (position 0 in the MSBs)
+    int bits[kMaxT];
+};
+
+// Device predicate program (see ks_pred in include/ks_b200.h).
+struct DevPred {
+    int kind;
+    int full;
+    int n_terms;
+    int allowed_off;   // into the predicate byte table
+    int terms_off;     // into the term arrays
+    double budget;
+    long long scale;
+    long long limit;
+};
+
+// Fused LSTM step: gates = G[slot(r)] + A[r] . W, then the cell update
+// (nn.cpp:88-128) with gate order i, f, o, cand.
+struct LstmArgs {
+    int M;             // rows
+    int H;             // hidden units (padded, multiple of 64)
+    int K;             // dense reduction length (multiple of 64, may be 0)
+    // FP32 operand
+    const float* A;
+    long long lda;
+    // split operand planes (row stride K)
+    const __half* A_hi;
+    const __half* A_lo;
+    const float* W;    // FP32 mode: [K][4H], column u*4+g
+    const float* G;    // [slots][4][H] = bias + one-hot weight row
+    const int* slot_ptr;
+    long long slot_stride;
+    int slot_base;
+    const float* c_prev;   // may be null -> zero state
+    long long ldc_prev;
+    const int* parent;     // row -> c_prev row; null -> identity; <0 -> zero state
+    float* h_out;
+    long long ldh;
+    float* c_out;
+    long long ldc;
+    __half* hA_hi;         // optional split copy of h_out for the next GEMM
+    __half* hA_lo;
+    long long ldha;
+};
+
+struct AttnArgs {
+    int M;             // rows of this position
+    int H_rows;        // rows per config at this position
+    int NS;            // decoder hidden (padded)
+    int NA2;           // 2 * NA
+    int nd;
+    const float* h_prev;   // previous-position h rows
+    long long ldh;
+    const int* parent;     // row -> h_prev row (<0 or null -> zero state)
+    const float* act;      // [C][7][NA2]
+    const float* uatt;     // [C][7][nd]
+    const float* Ws;       // [NS][nd]  (attn.hidden rows for s_prev)
+    const float* wo;       // [nd]
+    float bo;
+    float* A;              // FP32 operand out [M][NA2+NS]
+    __half* A_hi;          // split operand out
+    __half* A_lo;
+    int split_mode;        // 0 fp32, 1 fp16 hi/lo (F16X3), 2 bf16 hi only (BF16)
+};
+
+struct BeamArgs {
+    int B;
+    int H_cur;
+    int H_next;
+    int pos;
+    int k;
+    int greedy;
+    int final_step;
+    int NS;
+    const float* h;        // [B*H_cur][NS]
+    const float* Wh;       // head weights [NS][V] (padded rows zero)
+    const float* bh;       // [V]
+    const unsigned char* live_cur;
+    const double* lp_cur;
+    const unsigned long long* key_cur;
+    unsigned char* live_next;
+    double* lp_next;
+    unsigned long long* key_next;
+    int* parent_next;
+    int* slot_next;
+    int* status;
+    int* fail_pred;
+    int* fail_step;
+    const DevPred* preds;
+    int n_preds;
+    const unsigned char* pred_bytes;
+    const int* term_pos;
+    const double* term_w;
+    const int* term_field;
+    const long long* values;   // concatenated output values
+    const long long* desc;     // [B][7] or null
+    int* out_tok;              // [B][k][T]
+    double* out_lp;            // [B][k]
+    int* out_count;            // [B]
+    int* out_fail_pred;
+    int* out_fail_step;
+    int* out_status;
+    int cands_per_warp;        // smem capacity per warp (entries)
+};
+
+// fp16 split with an exact power-of-two scale on the residual so that it
+// stays in the normal fp16 range: x ~= hi + lo * 2^-kSplitShift.
+constexpr int kSplitShift = 11;
+
+__device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
+    hi = __float2half_rn(x);
+    const float r = x - __half2float(hi);          // exact in fp32
+    lo = __float2half_rn(r * 2048.0f);
+}
+
+}  // namespace ksb

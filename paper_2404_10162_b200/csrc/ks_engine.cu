@@ -1,0 +1,1006 @@
+// ks_engine.cu -- the C-ABI (include/ks_b200.h): engine creation (weight
+// packing into device layouts), workspace management, and the per-chunk
+// decode schedule:
+//
+//   encoder   7 x lstm_step (both directions in one launch)   nn.cpp:130-165
+//   uatt      a_t . W_a + b_h once per config                  models.cpp:265-281
+//   for each output position p:                                decoding.cpp:45-94
+//     attention_pack  rows B*H_p  -> [ctx ; h_prev] operand    models.cpp:466-478
+//     lstm_step       gate GEMM + fused cell                   models.cpp:479-480
+//     beam_step       head, log-softmax, predicates, top-k     models.cpp:490-492,
+//                                                              decoding.cpp:49-93
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ks_b200.h"
+#include "ks_common.cuh"
+#include "ks_internal.h"
+
+namespace ksb {
+__global__ void lstm_step_simt(LstmArgs a0, LstmArgs a1);
+__global__ void attention_pack(AttnArgs p);
+__global__ void uatt_kernel(int C, int NA2, int nd, const float* act, const float* Wa,
+                            const float* bh, float* uatt);
+__global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long long* key,
+                          int* status, int* fail_pred, int* fail_step);
+__global__ void beam_step(BeamArgs a, PosMeta m);
+// tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
+bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
+                    const __half* W_lo0, const __half* W_hi1, const __half* W_lo1,
+                    cudaStream_t stream, int* launches);
+}  // namespace ksb
+
+using namespace ksb;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_msg;
+thread_local std::string g_field;
+}  // namespace
+
+namespace ksb_host {
+ks_status set_error(ks_status code, const std::string& msg, const std::string& field) {
+    g_msg = msg;
+    g_field = field;
+    return code;
+}
+}  // namespace ksb_host
+using ksb_host::set_error;
+
+extern "C" const char* ks_last_error(void) { return g_msg.c_str(); }
+extern "C" const char* ks_last_error_field(void) { return g_field.c_str(); }
+
+#define KS_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t err_ = (call);                                                      \
+        if (err_ != cudaSuccess)                                                        \
+            return set_error(KS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(err_)); \
+    } while (0)
+
+namespace {
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+constexpr int SB_M_HOST = 64;
+
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevMem() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+    template <class T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct HostMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~HostMem() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMallocHost(&p, n);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+    template <class T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// One packed LSTM cell on the device.
+struct DevLstm {
+    int H = 0, K = 0, slots = 0;
+    DevMem W;       // FP32: [K][4H] (u*4+g)
+    DevMem Whi;     // TC: [4H][K] gate-interleaved per 64-unit tile
+    DevMem Wlo;
+    DevMem G;       // [slots][4][H]
+};
+
+}  // namespace
+
+struct ks_engine {
+    int device = 0;
+    int precision = KS_PREC_F16X3;
+    int variant = 1;
+    int n_a = 0, n_s = 0, n_d = 0, e = 0;
+    int NA = 0, NS = 0, NE = 0;
+    int T = 0;
+    int d_in = 0, d_fb = 0;
+    std::vector<int> vsize, in_sizes, in_offset;
+    std::vector<int64_t> in_values, out_values;
+    PosMeta meta{};
+    DevLstm enc[2], dec;
+    DevMem attWs, attWa, attBh, attWo;
+    float attBo = 0.0f;
+    std::vector<std::unique_ptr<DevMem>> headW, headB;
+    DevMem values;
+    // workspace
+    int64_t chunk = 65536;
+    DevMem tok, desc, act, uatt, encc, encA, Abuf, Ahi, Alo, hbuf, cbuf;
+    DevMem live[2], lp[2], key[2], parent[2], slot[2], status, fpred, fstep;
+    DevMem otok, olp, ocount, ostatus, ofpred, ofstep;
+    DevMem preds, pbytes, tpos, tw, tfield;
+    HostMem h_in, h_out;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    int beam_smem_max = 0;
+    // profiling of the gate GEMM launches
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+    std::vector<double> prof_flops;
+    double prof_ms = 0.0, prof_useful = 0.0;
+    int64_t prof_n = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// weight packing
+// ---------------------------------------------------------------------------
+struct HostTensors {
+    std::map<std::string, std::pair<const float*, int>> m;
+    const float* get(const std::string& n, int numel_expect, std::string& err) const {
+        auto it = m.find(n);
+        if (it == m.end()) {
+            err = "model tensor '" + n + "' is missing";
+            return nullptr;
+        }
+        if (numel_expect >= 0 && it->second.second != numel_expect) {
+            err = "tensor '" + n + "' has " + std::to_string(it->second.second) + " values, expected " +
+                  std::to_string(numel_expect);
+            return nullptr;
+        }
+        return it->second.first;
+    }
+};
+
+// Packs a reference LSTM cell (4 gate matrices (rows x H) + 4 biases) whose
+// rows split into a dense part (device k -> reference row, -1 = zero) and a
+// one-hot part (slot -> reference row, -1 = bias only).
+ks_status pack_lstm(const HostTensors& ht, const std::string& prefix, int rows, int H, int Hp,
+                    const std::vector<int>& dense_rows, const std::vector<int>& slot_rows,
+                    DevLstm& out) {
+    static const char* gates[4] = {"input", "forget", "output", "cand"};
+    std::string err;
+    const float* W[4];
+    const float* Bv[4];
+    for (int g = 0; g < 4; ++g) {
+        W[g] = ht.get(prefix + ".w_" + gates[g], rows * H, err);
+        if (!W[g]) return set_error(KS_ERR_STATE, err);
+        Bv[g] = ht.get(prefix + ".b_" + gates[g], H, err);
+        if (!Bv[g]) return set_error(KS_ERR_STATE, err);
+    }
+    const int K = (int)dense_rows.size();
+    const int S = (int)slot_rows.size();
+    out.H = Hp;
+    out.K = K;
+    out.slots = S;
+    std::vector<float> Wf((size_t)K * 4 * Hp, 0.0f);
+    std::vector<__half> Whi((size_t)4 * Hp * K), Wlo((size_t)4 * Hp * K);
+    std::vector<float> G((size_t)S * 4 * Hp, 0.0f);
+    for (int k = 0; k < K; ++k) {
+        const int r = dense_rows[(size_t)k];
+        for (int u = 0; u < Hp; ++u)
+            for (int g = 0; g < 4; ++g) {
+                const float w = (r >= 0 && u < H) ? W[g][(size_t)r * H + u] : 0.0f;
+                if (std::fabs(w) > 60000.0f)
+                    return set_error(KS_ERR_UNSUPPORTED, "weight magnitude exceeds the fp16 split range");
+                Wf[(size_t)k * 4 * Hp + u * 4 + g] = w;
+                // tensor-core layout: N index n = tile*256 + g*64 + u%64 (tile = u/64), K-major
+                const size_t n = (size_t)(u / 64) * 256 + (size_t)g * 64 + (u % 64);
+                const __half hi = __float2half_rn(w);
+                const float res = w - __half2float(hi);
+                Whi[n * K + k] = hi;
+                Wlo[n * K + k] = __float2half_rn(res * 2048.0f);
+            }
+    }
+    for (int s = 0; s < S; ++s) {
+        const int r = slot_rows[(size_t)s];
+        for (int g = 0; g < 4; ++g)
+            for (int u = 0; u < H; ++u) {
+                float v = Bv[g][u];
+                if (r >= 0) v += W[g][(size_t)r * H + u];
+                G[(size_t)s * 4 * Hp + (size_t)g * Hp + u] = v;
+            }
+    }
+    cudaError_t e = cudaSuccess;
+    if (K > 0) {
+        if ((e = out.W.ensure(Wf.size() * 4)) != cudaSuccess) goto fail;
+        if ((e = cudaMemcpy(out.W.p, Wf.data(), Wf.size() * 4, cudaMemcpyHostToDevice))) goto fail;
+        if ((e = out.Whi.ensure(Whi.size() * 2)) != cudaSuccess) goto fail;
+        if ((e = out.Wlo.ensure(Wlo.size() * 2)) != cudaSuccess) goto fail;
+        if ((e = cudaMemcpy(out.Whi.p, Whi.data(), Whi.size() * 2, cudaMemcpyHostToDevice))) goto fail;
+        if ((e = cudaMemcpy(out.Wlo.p, Wlo.data(), Wlo.size() * 2, cudaMemcpyHostToDevice))) goto fail;
+    }
+    if ((e = out.G.ensure(G.size() * 4)) != cudaSuccess) goto fail;
+    if ((e = cudaMemcpy(out.G.p, G.data(), G.size() * 4, cudaMemcpyHostToDevice))) goto fail;
+    return KS_OK;
+fail:
+    return set_error(KS_ERR_CUDA, std::string("weight upload: ") + cudaGetErrorString(e));
+}
+
+ks_status upload(DevMem& m, const void* src, size_t bytes) {
+    if (m.ensure(bytes ? bytes : 4) != cudaSuccess) return set_error(KS_ERR_CUDA, "cudaMalloc failed");
+    if (bytes && cudaMemcpy(m.p, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        return set_error(KS_ERR_CUDA, "cudaMemcpy failed");
+    return KS_OK;
+}
+
+}  // namespace
+
+extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, int32_t precision,
+                                      ks_engine** out) {
+    if (!d || !out) return set_error(KS_ERR_PARAMETER, "null argument");
+    if (precision < 0 || precision > 2) return set_error(KS_ERR_PARAMETER, "unknown precision mode");
+    if (d->variant != KS_VARIANT_ATTN && d->variant != KS_VARIANT_ATTN2 &&
+        d->variant != KS_VARIANT_ENC_DEC)
+        return set_error(KS_ERR_UNSUPPORTED,
+                         "the B200 engine implements the enc-dec, attn and attn-2 variants");
+    if (d->num_positions < 1 || d->num_positions > kMaxT)
+        return set_error(KS_ERR_UNSUPPORTED, "number of output positions must be in [1, 16]");
+    if (d->attention_dense_nodes < 1 || d->attention_dense_nodes > kMaxNd)
+        return set_error(KS_ERR_UNSUPPORTED, "attention_dense_nodes must be in [1, 8]");
+    if (cudaSetDevice(device) != cudaSuccess) return set_error(KS_ERR_CUDA, "cudaSetDevice failed");
+    auto eng = std::make_unique<ks_engine>();
+    ks_engine& E = *eng;
+    E.device = device;
+    E.precision = precision;
+    E.variant = d->variant;
+    E.n_a = d->pre_attention_size;
+    E.n_s = d->post_attention_size;
+    E.n_d = d->attention_dense_nodes;
+    E.e = d->encoder_state_size;
+    E.NA = round_up(E.n_a, 64);
+    E.NS = round_up(E.n_s, 64);
+    E.NE = round_up(E.e, 64);
+    E.T = d->num_positions;
+    E.in_sizes.assign(d->input_sizes, d->input_sizes + 7);
+    E.in_offset.resize(7);
+    int w = 0, nin = 0;
+    for (int f = 0; f < 7; ++f) {
+        if (E.in_sizes[f] < 1) return set_error(KS_ERR_CHECKPOINT, "empty input vocabulary");
+        E.in_offset[f] = w;
+        w += E.in_sizes[f];
+    }
+    nin = w;
+    E.d_in = w;
+    E.in_values.assign(d->input_values, d->input_values + nin);
+    E.vsize.assign(d->vocab_sizes, d->vocab_sizes + E.T);
+    int nout = 0, fb = 1, bits_total = 0;
+    E.meta.T = E.T;
+    for (int p = 0; p < E.T; ++p) {
+        const int V = E.vsize[p];
+        if (V < 1 || V > kMaxV)
+            return set_error(KS_ERR_UNSUPPORTED, "output vocabularies must have 1..32 values");
+        E.meta.vsize[p] = V;
+        E.meta.value_offset[p] = nout;
+        E.meta.fb_offset[p] = fb;
+        int b = 1;
+        while ((1 << b) < V) ++b;
+        E.meta.bits[p] = b;
+        bits_total += b;
+        nout += V;
+        fb += V;
+    }
+    if (bits_total > 64) return set_error(KS_ERR_UNSUPPORTED, "packed prefix key exceeds 64 bits");
+    int sh = 0;
+    for (int p = E.T - 1; p >= 0; --p) {
+        E.meta.shift[p] = sh;
+        sh += E.meta.bits[p];
+    }
+    E.d_fb = fb;
+    E.out_values.assign(d->output_values, d->output_values + nout);
+
+    HostTensors ht;
+    for (int i = 0; i < d->num_tensors; ++i)
+        ht.m[d->tensor_names[i]] = {d->tensor_data[i], d->tensor_numel[i]};
+    std::string err;
+    ks_status st;
+    if (E.variant == KS_VARIANT_ENC_DEC) {
+        std::vector<int> dense, slots;
+        for (int k = 0; k < E.NE; ++k) dense.push_back(k < E.e ? E.d_in + k : -1);
+        for (int s = 0; s < E.d_in; ++s) slots.push_back(s);
+        if ((st = pack_lstm(ht, "encoder", E.d_in + E.e, E.e, E.NE, dense, slots, E.enc[0]))) return st;
+        dense.clear();
+        slots.clear();
+        for (int k = 0; k < E.NE; ++k) dense.push_back(k < E.e ? E.d_fb + k : -1);
+        for (int s = 0; s < E.d_fb; ++s) slots.push_back(s);
+        if ((st = pack_lstm(ht, "decoder", E.d_fb + E.e, E.e, E.NE, dense, slots, E.dec))) return st;
+    } else {
+        std::vector<int> dense, slots;
+        for (int k = 0; k < E.NA; ++k) dense.push_back(k < E.n_a ? E.d_in + k : -1);
+        for (int s = 0; s < E.d_in; ++s) slots.push_back(s);
+        if ((st = pack_lstm(ht, "pre.fwd", E.d_in + E.n_a, E.n_a, E.NA, dense, slots, E.enc[0]))) return st;
+        if ((st = pack_lstm(ht, "pre.bwd", E.d_in + E.n_a, E.n_a, E.NA, dense, slots, E.enc[1]))) return st;
+        // decoder rows: [ctx (2 n_a) | fb one-hot (d_fb, attn only) | h (n_s)]  (models.cpp:215-219)
+        const bool fbk = E.variant == KS_VARIANT_ATTN;
+        const int hbase = 2 * E.n_a + (fbk ? E.d_fb : 0);
+        const int rows = hbase + E.n_s;
+        dense.clear();
+        slots.clear();
+        for (int k = 0; k < 2 * E.NA; ++k) {
+            const int half = k / E.NA, i = k % E.NA;
+            dense.push_back(i < E.n_a ? half * E.n_a + i : -1);
+        }
+        for (int k = 0; k < E.NS; ++k) dense.push_back(k < E.n_s ? hbase + k : -1);
+        if (fbk)
+            for (int s = 0; s < E.d_fb; ++s) slots.push_back(2 * E.n_a + s);
+        else
+            slots.push_back(-1);
+        if ((st = pack_lstm(ht, "post", rows, E.n_s, E.NS, dense, slots, E.dec))) return st;
+        // attention energy network: attn.hidden (n_s + 2 n_a) x n_d, attn.out n_d x 1
+        const float* Wh = ht.get("attn.hidden.weights", (E.n_s + 2 * E.n_a) * E.n_d, err);
+        const float* bh = ht.get("attn.hidden.bias", E.n_d, err);
+        const float* wo = ht.get("attn.out.weights", E.n_d, err);
+        const float* bo = ht.get("attn.out.bias", 1, err);
+        if (!Wh || !bh || !wo || !bo) return set_error(KS_ERR_STATE, err);
+        std::vector<float> Ws((size_t)E.NS * E.n_d, 0.0f), Wa((size_t)2 * E.NA * E.n_d, 0.0f);
+        for (int i = 0; i < E.n_s; ++i)
+            for (int dd = 0; dd < E.n_d; ++dd) Ws[(size_t)i * E.n_d + dd] = Wh[(size_t)i * E.n_d + dd];
+        for (int k = 0; k < 2 * E.NA; ++k) {
+            const int half = k / E.NA, i = k % E.NA;
+            if (i >= E.n_a) continue;
+            const int r = E.n_s + half * E.n_a + i;
+            for (int dd = 0; dd < E.n_d; ++dd) Wa[(size_t)k * E.n_d + dd] = Wh[(size_t)r * E.n_d + dd];
+        }
+        if ((st = upload(E.attWs, Ws.data(), Ws.size() * 4))) return st;
+        if ((st = upload(E.attWa, Wa.data(), Wa.size() * 4))) return st;
+        if ((st = upload(E.attBh, bh, (size_t)E.n_d * 4))) return st;
+        if ((st = upload(E.attWo, wo, (size_t)E.n_d * 4))) return st;
+        E.attBo = bo[0];
+    }
+    const int Hd = E.variant == KS_VARIANT_ENC_DEC ? E.e : E.n_s;
+    const int HdP = E.variant == KS_VARIANT_ENC_DEC ? E.NE : E.NS;
+    for (int p = 0; p < E.T; ++p) {
+        const int V = E.vsize[p];
+        const float* W = ht.get("head." + std::to_string(p) + ".weights", Hd * V, err);
+        const float* b = ht.get("head." + std::to_string(p) + ".bias", V, err);
+        if (!W || !b) return set_error(KS_ERR_STATE, err);
+        std::vector<float> Wp((size_t)HdP * V, 0.0f);
+        std::memcpy(Wp.data(), W, sizeof(float) * (size_t)Hd * V);
+        E.headW.emplace_back(new DevMem());
+        E.headB.emplace_back(new DevMem());
+        if ((st = upload(*E.headW.back(), Wp.data(), Wp.size() * 4))) return st;
+        if ((st = upload(*E.headB.back(), b, (size_t)V * 4))) return st;
+    }
+    std::vector<long long> vals(E.out_values.begin(), E.out_values.end());
+    if ((st = upload(E.values, vals.data(), vals.size() * 8))) return st;
+    if (cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking) != cudaSuccess)
+        return set_error(KS_ERR_CUDA, "stream creation failed");
+    cudaFuncSetAttribute(beam_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    E.beam_smem_max = 227 * 1024;
+    *out = eng.release();
+    return KS_OK;
+}
+
+extern "C" ks_status ks_engine_create_from_checkpoint(const char* path, int32_t device,
+                                                      int32_t precision, ks_engine** out) {
+    ks_checkpoint* ck = nullptr;
+    ks_status st = ks_checkpoint_load(path, &ck);
+    if (st) return st;
+    ksb_host::DescStore store;
+    ks_model_desc d;
+    st = ksb_host::desc_from_checkpoint(ck, store, d);
+    if (!st) st = ks_engine_create(&d, device, precision, out);
+    ks_checkpoint_free(ck);
+    return st;
+}
+
+extern "C" void ks_engine_destroy(ks_engine* eng) {
+    if (!eng) return;
+    cudaSetDevice(eng->device);
+    for (auto& ev : eng->prof_ev) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    if (eng->stream) cudaStreamDestroy(eng->stream);
+    delete eng;
+}
+
+extern "C" int32_t ks_engine_num_positions(const ks_engine* eng) { return eng ? eng->T : 0; }
+extern "C" int32_t ks_engine_vocab_size(const ks_engine* eng, int32_t p) {
+    return (eng && p >= 0 && p < eng->T) ? eng->vsize[(size_t)p] : 0;
+}
+extern "C" int32_t ks_engine_precision(const ks_engine* eng) { return eng ? eng->precision : -1; }
+extern "C" int64_t ks_engine_last_launch_count(const ks_engine* eng) { return eng ? eng->launches : 0; }
+extern "C" ks_status ks_engine_set_chunk(ks_engine* eng, int64_t c) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    eng->chunk = c > 0 ? c : 65536;
+    return KS_OK;
+}
+
+extern "C" ks_status ks_encode_problems(const ks_engine* eng, const int64_t* desc, int64_t B,
+                                        int32_t allow_nearest, int32_t* tok, int64_t* bad_row) {
+    static const char* names[7] = {"n", "c", "h", "w", "k", "y", "x"};
+    if (!eng || (!desc && B) || (!tok && B)) return set_error(KS_ERR_PARAMETER, "null argument");
+    for (int64_t b = 0; b < B; ++b) {
+        for (int f = 0; f < 7; ++f) {
+            const int64_t v = desc[b * 7 + f];
+            if (v < 1) {
+                if (bad_row) *bad_row = b;
+                return set_error(KS_ERR_VALIDATION,
+                                 std::string("descriptor field ") + names[f] + " must be >= 1, got " +
+                                     std::to_string(v),
+                                 names[f]);
+            }
+            const int64_t* vals = eng->in_values.data() + eng->in_offset[(size_t)f];
+            const int n = eng->in_sizes[(size_t)f];
+            int id = -1;
+            for (int i = 0; i < n; ++i)
+                if (vals[i] == v) { id = i; break; }
+            // FieldVocab::nearest (encoding.cpp:26-34): closest, smaller value on ties
+            int64_t best = vals[0];
+            for (int i = 0; i < n; ++i) {
+                const int64_t dv = vals[i] > v ? vals[i] - v : v - vals[i];
+                const int64_t db = best > v ? best - v : v - best;
+                if (dv < db || (dv == db && vals[i] < best)) best = vals[i];
+            }
+            if (id < 0 && allow_nearest)
+                for (int i = 0; i < n; ++i)
+                    if (vals[i] == best) { id = i; break; }
+            if (id < 0) {
+                if (bad_row) *bad_row = b;
+                return set_error(KS_ERR_VALIDATION,
+                                 "value " + std::to_string(v) + " of field " + names[f] +
+                                     " is not in the vocabulary (nearest known: " +
+                                     std::to_string(best) + ")",
+                                 names[f]);
+            }
+            tok[b * 7 + f] = id;
+        }
+    }
+    return KS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// decode schedule
+// ---------------------------------------------------------------------------
+namespace {
+
+struct PredDev {
+    int n = 0;
+    bool needs_desc = false;
+};
+
+ks_status upload_preds(ks_engine& E, const ks_pred* preds, int n, PredDev& pd) {
+    std::vector<DevPred> dp;
+    std::vector<unsigned char> bytes;
+    std::vector<int> tpos, tfield;
+    std::vector<double> tw;
+    int total_v = 0;
+    for (int p = 0; p < E.T; ++p) total_v += E.vsize[(size_t)p];
+    for (int i = 0; i < n; ++i) {
+        const ks_pred& q = preds[i];
+        DevPred d{};
+        d.kind = q.kind;
+        d.full = q.full_sequence_only ? 1 : 0;
+        if (q.kind == KS_PRED_MASK) {
+            if (!q.allowed) return set_error(KS_ERR_PARAMETER, "mask predicate without table");
+            d.allowed_off = (int)bytes.size();
+            bytes.insert(bytes.end(), q.allowed, q.allowed + total_v);
+        } else if (q.kind == KS_PRED_BUDGET || q.kind == KS_PRED_PRODUCT || q.kind == KS_PRED_DIVIDES) {
+            if (q.n_terms < 0 || (q.n_terms > 0 && !q.term_pos))
+                return set_error(KS_ERR_PARAMETER, "predicate terms missing");
+            d.n_terms = q.n_terms;
+            d.terms_off = (int)tpos.size();
+            for (int t = 0; t < q.n_terms; ++t) {
+                const int pp = q.term_pos[t];
+                if (pp < -1 || pp >= E.T) return set_error(KS_ERR_INDEX, "predicate term position out of range");
+                tpos.push_back(pp);
+                tw.push_back(q.kind == KS_PRED_BUDGET ? (q.term_w ? q.term_w[t] : 0.0) : 0.0);
+                int f = 0;
+                if (q.kind == KS_PRED_DIVIDES) {
+                    if (!q.term_field) return set_error(KS_ERR_PARAMETER, "divisibility predicate without fields");
+                    f = q.term_field[t];
+                    if (f < 0 || f > 6) return set_error(KS_ERR_INDEX, "descriptor field out of range");
+                    pd.needs_desc = true;
+                }
+                tfield.push_back(f);
+            }
+            if (q.kind == KS_PRED_BUDGET) {
+                for (int t = 0; t < q.n_terms; ++t)
+                    if (q.term_w && q.term_w[t] < 0.0)
+                        return set_error(KS_ERR_PARAMETER, "resource budget weight must be nonnegative");
+                if (q.budget < 0.0) return set_error(KS_ERR_PARAMETER, "resource budget must be nonnegative");
+            }
+            d.budget = q.budget;
+            d.scale = q.scale;
+            d.limit = q.limit;
+        } else {
+            return set_error(KS_ERR_PARAMETER, "unknown predicate kind " + std::to_string(q.kind));
+        }
+        dp.push_back(d);
+    }
+    pd.n = n;
+    ks_status st;
+    if ((st = upload(E.preds, dp.data(), dp.size() * sizeof(DevPred)))) return st;
+    if ((st = upload(E.pbytes, bytes.data(), bytes.size()))) return st;
+    if ((st = upload(E.tpos, tpos.data(), tpos.size() * 4))) return st;
+    if ((st = upload(E.tw, tw.data(), tw.size() * 8))) return st;
+    if ((st = upload(E.tfield, tfield.data(), tfield.size() * 4))) return st;
+    return KS_OK;
+}
+
+ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
+    const int64_t R = C * k;
+    const bool enc_dec = E.variant == KS_VARIANT_ENC_DEC;
+    const int Hd = enc_dec ? E.NE : E.NS;
+    const int NA2 = enc_dec ? 0 : 2 * E.NA;
+    const int Kd = NA2 + Hd;
+    const int He = enc_dec ? E.NE : E.NA;
+    cudaError_t e = cudaSuccess;
+#define ENS(buf, n) if ((e = (buf).ensure((size_t)(n))) != cudaSuccess) goto fail
+    ENS(E.tok, C * 7 * 4);
+    ENS(E.desc, C * 7 * 8);
+    ENS(E.act, C * 7 * (enc_dec ? E.NE : NA2) * 4);
+    ENS(E.uatt, C * 7 * E.n_d * 4 + 16);
+    ENS(E.encc, 2 * 2 * C * He * 4);
+    ENS(E.encA, 2 * 2 * 2 * C * He * 2);   // [dir][pingpong][hi/lo][C][He] fp16
+    if (E.precision == KS_PREC_FP32) {
+        ENS(E.Abuf, R * Kd * 4);
+    } else {
+        ENS(E.Ahi, R * Kd * 2);
+        ENS(E.Alo, R * Kd * 2);
+    }
+    ENS(E.hbuf, 2 * R * Hd * 4);
+    ENS(E.cbuf, 2 * R * Hd * 4);
+    for (int i = 0; i < 2; ++i) {
+        ENS(E.live[i], R);
+        ENS(E.lp[i], R * 8);
+        ENS(E.key[i], R * 8);
+        ENS(E.parent[i], R * 4);
+        ENS(E.slot[i], R * 4);
+    }
+    ENS(E.status, C * 4);
+    ENS(E.fpred, C * 4);
+    ENS(E.fstep, C * 4);
+#undef ENS
+    return KS_OK;
+fail:
+    return set_error(KS_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+}
+
+ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevLstm& L0,
+                      DevLstm* L1, double useful_flops) {
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    const bool timed = E.prof && a0.K > 0;
+    if (timed) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, E.stream);
+    }
+    int n = 0;
+    bool done = false;
+    if (E.precision != KS_PREC_FP32 && a0.K > 0) {
+        done = launch_lstm_tc(a0, a1, E.precision, L0.Whi.as<__half>(), L0.Wlo.as<__half>(),
+                              L1 ? L1->Whi.as<__half>() : nullptr, L1 ? L1->Wlo.as<__half>() : nullptr,
+                              E.stream, &n);
+    }
+    if (!done) {
+        dim3 grid((unsigned)((a0.M + SB_M_HOST - 1) / SB_M_HOST), (unsigned)(a0.H / 32), a1 ? 2u : 1u);
+        lstm_step_simt<<<grid, 256, 0, E.stream>>>(a0, a1 ? *a1 : a0);
+        n = 1;
+    }
+    E.launches += n;
+    if (timed) {
+        cudaEventRecord(ev1, E.stream);
+        E.prof_ev.emplace_back(ev0, ev1);
+        E.prof_flops.push_back(useful_flops);
+    }
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("lstm launch: ") + cudaGetErrorString(err));
+    return KS_OK;
+}
+
+// Decodes one chunk of C configs already resident on the device.
+ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_tok,
+                    const long long* d_desc, const PredDev& pd, int* o_tok, double* o_lp,
+                    int* o_count, int* o_status, int* o_fpred, int* o_fstep) {
+    ks_status st;
+    if ((st = ensure_workspace(E, C, k))) return st;
+    cudaStream_t s = E.stream;
+    const bool enc_dec = E.variant == KS_VARIANT_ENC_DEC;
+    const bool split = E.precision != KS_PREC_FP32;
+    const int He = enc_dec ? E.NE : E.NA;
+    const int NA2 = enc_dec ? 0 : 2 * E.NA;
+    const int Hd = enc_dec ? E.NE : E.NS;
+    const int Kd = NA2 + Hd;
+    const long long act_ld = enc_dec ? 0 : 7LL * NA2;
+    float* act = E.act.as<float>();
+    float* encc = E.encc.as<float>();
+    __half* encA = E.encA.as<__half>();
+    auto encc_at = [&](int dir, int pp) { return encc + ((size_t)dir * 2 + pp) * C * He; };
+    auto encA_at = [&](int dir, int pp, int lo) { return encA + (((size_t)dir * 2 + pp) * 2 + lo) * C * He; };
+
+    // ---- encoder (bi-LSTM over the 7 one-hot input steps, zero initial state)
+    const int dirs = enc_dec ? 1 : 2;
+    for (int sidx = 0; sidx < 7; ++sidx) {
+        LstmArgs a[2];
+        for (int dir = 0; dir < dirs; ++dir) {
+            const int t = dir == 0 ? sidx : 6 - sidx;
+            const int tprev = dir == 0 ? t - 1 : t + 1;
+            LstmArgs& p = a[dir];
+            std::memset(&p, 0, sizeof p);
+            p.M = (int)C;
+            p.H = He;
+            p.K = sidx == 0 ? 0 : He;
+            if (enc_dec) {
+                // hidden state ping-pongs through the split planes and a scratch fp32 copy
+                p.A = act + (size_t)((sidx + 1) & 1) * C * He;
+                p.lda = He;
+                p.h_out = act + (size_t)(sidx & 1) * C * He;
+                p.ldh = He;
+            } else {
+                p.A = act + (size_t)tprev * NA2 + dir * E.NA;
+                p.lda = act_ld;
+                p.h_out = act + (size_t)t * NA2 + dir * E.NA;
+                p.ldh = act_ld;
+            }
+            p.A_hi = encA_at(dir, (sidx + 1) & 1, 0);
+            p.A_lo = encA_at(dir, (sidx + 1) & 1, 1);
+            p.W = E.enc[dir].W.as<float>();
+            p.G = E.enc[dir].G.as<float>();
+            p.slot_ptr = d_tok + t;
+            p.slot_stride = 7;
+            p.slot_base = E.in_offset[(size_t)t];
+            p.c_prev = sidx == 0 ? nullptr : encc_at(dir, (sidx + 1) & 1);
+            p.ldc_prev = He;
+            p.parent = nullptr;
+            p.c_out = encc_at(dir, sidx & 1);
+            p.ldc = He;
+            if (split) {
+                p.hA_hi = encA_at(dir, sidx & 1, 0);
+                p.hA_lo = encA_at(dir, sidx & 1, 1);
+                p.ldha = He;
+            }
+        }
+        const double fl = sidx == 0 ? 0.0 : 2.0 * dirs * (double)C * He * 4.0 * He;
+        if ((st = launch_lstm(E, a[0], dirs == 2 ? &a[1] : nullptr, E.enc[0], dirs == 2 ? &E.enc[1] : nullptr, fl)))
+            return st;
+    }
+    if (!enc_dec) {
+        const long long n = C * 7;
+        uatt_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>((int)C, NA2, E.n_d, act, E.attWa.as<float>(),
+                                                            E.attBh.as<float>(), E.uatt.as<float>());
+        E.launches++;
+    }
+    beam_init<<<(unsigned)((C + 255) / 256), 256, 0, s>>>((int)C, E.live[0].as<unsigned char>(),
+                                                          E.lp[0].as<double>(),
+                                                          E.key[0].as<unsigned long long>(),
+                                                          E.status.as<int>(), E.fpred.as<int>(),
+                                                          E.fstep.as<int>());
+    E.launches++;
+
+    // ---- decoder positions
+    float* hb = E.hbuf.as<float>();
+    float* cb = E.cbuf.as<float>();
+    const int64_t R = C * k;
+    int H = 1;
+    int maxc = 8;
+    {
+        int h = 1;
+        for (int p = 0; p < E.T; ++p) {
+            maxc = std::max(maxc, h * E.vsize[(size_t)p]);
+            h = std::min<int64_t>(k, (int64_t)h * E.vsize[(size_t)p]);
+        }
+    }
+    const int cpw = (maxc + 7) / 8 * 8;
+    for (int pos = 0; pos < E.T; ++pos) {
+        const int cur = pos & 1, nxt = cur ^ 1;
+        const int M = (int)(C * H);
+        // previous position's state (or the initial state at position 0)
+        const float* h_prev = nullptr;
+        const float* c_prev = nullptr;
+        const int* par = nullptr;
+        if (pos > 0) {
+            h_prev = hb + (size_t)((pos - 1) & 1) * R * Hd;
+            c_prev = cb + (size_t)((pos - 1) & 1) * R * Hd;
+            par = E.parent[cur].as<int>();
+        } else if (enc_dec) {
+            h_prev = act + (size_t)(6 & 1) * C * He;   // encoder final state (thought vector)
+            c_prev = encc_at(0, 6 & 1);
+            par = nullptr;                              // H_0 = 1: row r = config r
+        }
+        AttnArgs aa{};
+        aa.M = M;
+        aa.H_rows = H;
+        aa.NS = Hd;
+        aa.NA2 = NA2;
+        aa.nd = E.n_d;
+        aa.h_prev = h_prev;
+        aa.ldh = Hd;
+        aa.parent = par;
+        aa.act = act;
+        aa.uatt = E.uatt.as<float>();
+        aa.Ws = enc_dec ? nullptr : E.attWs.as<float>();
+        aa.wo = enc_dec ? nullptr : E.attWo.as<float>();
+        aa.bo = E.attBo;
+        aa.A = E.Abuf.as<float>();
+        aa.A_hi = E.Ahi.as<__half>();
+        aa.A_lo = E.Alo.as<__half>();
+        aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
+        if (enc_dec) aa.nd = 0;
+        attention_pack<<<(unsigned)((M + 7) / 8), 256, 0, s>>>(aa);
+        E.launches++;
+
+        LstmArgs p{};
+        p.M = M;
+        p.H = Hd;
+        p.K = Kd;
+        p.A = E.Abuf.as<float>();
+        p.lda = Kd;
+        p.A_hi = E.Ahi.as<__half>();
+        p.A_lo = E.Alo.as<__half>();
+        p.W = E.dec.W.as<float>();
+        p.G = E.dec.G.as<float>();
+        if (E.variant == KS_VARIANT_ATTN2) {
+            p.slot_ptr = nullptr;
+            p.slot_base = 0;
+        } else if (pos == 0) {
+            p.slot_ptr = nullptr;
+            p.slot_base = 0;     // GO token, feedback slot 0 (encoding.cpp:192-199)
+        } else {
+            p.slot_ptr = E.slot[cur].as<int>();
+            p.slot_stride = 1;
+            p.slot_base = 0;
+        }
+        p.c_prev = c_prev;
+        p.ldc_prev = Hd;
+        p.parent = par;
+        p.h_out = hb + (size_t)cur * R * Hd;
+        p.ldh = Hd;
+        p.c_out = cb + (size_t)cur * R * Hd;
+        p.ldc = Hd;
+        if (enc_dec && pos == 0) p.ldc_prev = He;
+        const double useful = 2.0 * (double)M * (double)(2 * E.n_a * (enc_dec ? 0 : 1) + (enc_dec ? E.e : E.n_s)) *
+                              4.0 * (enc_dec ? E.e : E.n_s);
+        if ((st = launch_lstm(E, p, nullptr, E.dec, nullptr, useful))) return st;
+
+        const int V = E.vsize[(size_t)pos];
+        const bool fin = pos == E.T - 1;
+        const int Hn = fin ? 0 : (int)std::min<int64_t>(k, (int64_t)H * V);
+        BeamArgs b{};
+        b.B = (int)C;
+        b.H_cur = H;
+        b.H_next = Hn;
+        b.pos = pos;
+        b.k = k;
+        b.greedy = greedy ? 1 : 0;
+        b.final_step = fin ? 1 : 0;
+        b.NS = Hd;
+        b.h = hb + (size_t)cur * R * Hd;
+        b.Wh = E.headW[(size_t)pos]->as<float>();
+        b.bh = E.headB[(size_t)pos]->as<float>();
+        b.live_cur = E.live[cur].as<unsigned char>();
+        b.lp_cur = E.lp[cur].as<double>();
+        b.key_cur = E.key[cur].as<unsigned long long>();
+        b.live_next = E.live[nxt].as<unsigned char>();
+        b.lp_next = E.lp[nxt].as<double>();
+        b.key_next = E.key[nxt].as<unsigned long long>();
+        b.parent_next = E.parent[nxt].as<int>();
+        b.slot_next = E.slot[nxt].as<int>();
+        b.status = E.status.as<int>();
+        b.fail_pred = E.fpred.as<int>();
+        b.fail_step = E.fstep.as<int>();
+        b.preds = E.preds.as<DevPred>();
+        b.n_preds = pd.n;
+        b.pred_bytes = E.pbytes.as<unsigned char>();
+        b.term_pos = E.tpos.as<int>();
+        b.term_w = E.tw.as<double>();
+        b.term_field = E.tfield.as<int>();
+        b.values = E.values.as<long long>();
+        b.desc = d_desc;
+        b.out_tok = o_tok;
+        b.out_lp = o_lp;
+        b.out_count = o_count;
+        b.out_status = o_status;
+        b.out_fail_pred = o_fpred;
+        b.out_fail_step = o_fstep;
+        b.cands_per_warp = cpw;
+        const size_t wsm = ((size_t)Hd * (V | 1) * 4 + 15) & ~(size_t)15;
+        int warps = 8;
+        while (warps > 1 && wsm + (size_t)warps * cpw * 28 > (size_t)E.beam_smem_max) --warps;
+        const size_t smem = wsm + (size_t)warps * cpw * 28;
+        if (smem > (size_t)E.beam_smem_max)
+            return set_error(KS_ERR_UNSUPPORTED, "beam width x vocabulary too large for the beam kernel");
+        beam_step<<<(unsigned)((C + warps - 1) / warps), warps * 32, smem, s>>>(b, E.meta);
+        E.launches++;
+        const cudaError_t err = cudaGetLastError();
+        if (err != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("beam launch: ") + cudaGetErrorString(err));
+        H = Hn;
+    }
+    return KS_OK;
+}
+
+ks_status check_common(ks_engine* eng, int64_t B, int32_t k, const ks_pred* preds, int32_t n) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    if (k < 1) return set_error(KS_ERR_PARAMETER, "beam width must be >= 1, got " + std::to_string(k));
+    if (B < 0) return set_error(KS_ERR_PARAMETER, "negative batch size");
+    if (n < 0 || (n > 0 && !preds)) return set_error(KS_ERR_PARAMETER, "bad predicate list");
+    if (cudaSetDevice(eng->device) != cudaSuccess) return set_error(KS_ERR_CUDA, "cudaSetDevice failed");
+    return KS_OK;
+}
+
+ks_status collect_profile(ks_engine& E) {
+    for (size_t i = 0; i < E.prof_ev.size(); ++i) {
+        float ms = 0.0f;
+        cudaEventSynchronize(E.prof_ev[i].second);
+        cudaEventElapsedTime(&ms, E.prof_ev[i].first, E.prof_ev[i].second);
+        E.prof_ms += ms;
+        E.prof_useful += E.prof_flops[i];
+        E.prof_n++;
+        cudaEventDestroy(E.prof_ev[i].first);
+        cudaEventDestroy(E.prof_ev[i].second);
+    }
+    E.prof_ev.clear();
+    E.prof_flops.clear();
+    return KS_OK;
+}
+
+ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, int64_t B, int32_t k,
+                      bool greedy, const ks_pred* preds, int32_t n_preds, int32_t* out_tok,
+                      double* out_lp, int32_t* out_count, int32_t* out_status, int32_t* out_fpred,
+                      int32_t* out_fstep) {
+    ks_engine& E = *eng;
+    const int T = E.T;
+    for (int64_t b = 0; b < B; ++b)
+        for (int f = 0; f < 7; ++f) {
+            const int t = tok[b * 7 + f];
+            if (t < 0 || t >= E.in_sizes[(size_t)f])
+                return set_error(KS_ERR_INDEX, "input token " + std::to_string(t) + " out of range for field " +
+                                                   std::to_string(f) + " (row " + std::to_string(b) + ")");
+        }
+    PredDev pd;
+    ks_status st;
+    if ((st = upload_preds(E, preds, n_preds, pd))) return st;
+    if (pd.needs_desc && !desc) return set_error(KS_ERR_PARAMETER, "divisibility predicates need descriptors");
+    E.launches = 0;
+    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
+    const size_t in_bytes = (size_t)C * 7 * 4 + (size_t)C * 7 * 8;
+    const size_t out_bytes = (size_t)C * k * T * 4 + (size_t)C * k * 8 + (size_t)C * 4 * 4;
+    if (E.h_in.ensure(in_bytes) != cudaSuccess || E.h_out.ensure(out_bytes) != cudaSuccess)
+        return set_error(KS_ERR_CUDA, "pinned staging allocation failed");
+    if (E.otok.ensure((size_t)C * k * T * 4) || E.olp.ensure((size_t)C * k * 8) ||
+        E.ocount.ensure((size_t)C * 4) || E.ostatus.ensure((size_t)C * 4) ||
+        E.ofpred.ensure((size_t)C * 4) || E.ofstep.ensure((size_t)C * 4))
+        return set_error(KS_ERR_CUDA, "output allocation failed");
+    if ((st = ensure_workspace(E, C, k))) return st;
+    for (int64_t c0 = 0; c0 < B; c0 += C) {
+        const int64_t n = std::min<int64_t>(C, B - c0);
+        int32_t* htok = E.h_in.as<int32_t>();
+        int64_t* hdesc = reinterpret_cast<int64_t*>(E.h_in.as<char>() + (size_t)C * 7 * 4);
+        std::memcpy(htok, tok + c0 * 7, (size_t)n * 7 * 4);
+        KS_CUDA(cudaMemcpyAsync(E.tok.p, htok, (size_t)n * 7 * 4, cudaMemcpyHostToDevice, E.stream));
+        const long long* ddesc = nullptr;
+        if (desc && pd.needs_desc) {
+            std::memcpy(hdesc, desc + c0 * 7, (size_t)n * 7 * 8);
+            KS_CUDA(cudaMemcpyAsync(E.desc.p, hdesc, (size_t)n * 7 * 8, cudaMemcpyHostToDevice, E.stream));
+            ddesc = E.desc.as<long long>();
+        }
+        if ((st = run_chunk(E, n, k, greedy, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
+                            E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>())))
+            return st;
+        char* ho = E.h_out.as<char>();
+        int32_t* h_tok = reinterpret_cast<int32_t*>(ho);
+        double* h_lp = reinterpret_cast<double*>(ho + (size_t)C * k * T * 4);
+        int32_t* h_misc = reinterpret_cast<int32_t*>(ho + (size_t)C * k * T * 4 + (size_t)C * k * 8);
+        KS_CUDA(cudaMemcpyAsync(h_tok, E.otok.p, (size_t)n * k * T * 4, cudaMemcpyDeviceToHost, E.stream));
+        if (!greedy) {
+            KS_CUDA(cudaMemcpyAsync(h_lp, E.olp.p, (size_t)n * k * 8, cudaMemcpyDeviceToHost, E.stream));
+            KS_CUDA(cudaMemcpyAsync(h_misc, E.ocount.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+            KS_CUDA(cudaMemcpyAsync(h_misc + C, E.ostatus.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+            KS_CUDA(cudaMemcpyAsync(h_misc + 2 * C, E.ofpred.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+            KS_CUDA(cudaMemcpyAsync(h_misc + 3 * C, E.ofstep.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+        }
+        KS_CUDA(cudaStreamSynchronize(E.stream));
+        std::memcpy(out_tok + c0 * k * T, h_tok, (size_t)n * k * T * 4);
+        if (!greedy) {
+            if (out_lp) std::memcpy(out_lp + c0 * k, h_lp, (size_t)n * k * 8);
+            if (out_count) std::memcpy(out_count + c0, h_misc, (size_t)n * 4);
+            if (out_status) std::memcpy(out_status + c0, h_misc + C, (size_t)n * 4);
+            if (out_fpred) std::memcpy(out_fpred + c0, h_misc + 2 * C, (size_t)n * 4);
+            if (out_fstep) std::memcpy(out_fstep + c0, h_misc + 3 * C, (size_t)n * 4);
+        }
+    }
+    if (E.prof) collect_profile(E);
+    return KS_OK;
+}
+
+}  // namespace
+
+extern "C" ks_status ks_beam_search_batch(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                                          int64_t B, int32_t k, const ks_pred* preds, int32_t n_preds,
+                                          int32_t* out_tok, double* out_lp, int32_t* out_count,
+                                          int32_t* out_status, int32_t* out_fpred, int32_t* out_fstep) {
+    ks_status st = check_common(eng, B, k, preds, n_preds);
+    if (st) return st;
+    if (B == 0) return KS_OK;
+    if (!tok || !out_tok) return set_error(KS_ERR_PARAMETER, "null token buffer");
+    return decode_host(eng, tok, desc, B, k, false, preds, n_preds, out_tok, out_lp, out_count, out_status,
+                       out_fpred, out_fstep);
+}
+
+extern "C" ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok) {
+    ks_status st = check_common(eng, B, 1, nullptr, 0);
+    if (st) return st;
+    if (B == 0) return KS_OK;
+    if (!tok || !out_tok) return set_error(KS_ERR_PARAMETER, "null token buffer");
+    return decode_host(eng, tok, nullptr, B, 1, true, nullptr, 0, out_tok, nullptr, nullptr, nullptr, nullptr,
+                       nullptr);
+}
+
+extern "C" ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok, const int64_t* d_desc,
+                                           int64_t B, int32_t k, const ks_pred* preds, int32_t n_preds,
+                                           int32_t* d_out_tok, double* d_out_lp, int32_t* d_out_count,
+                                           int32_t* d_out_status, int32_t* d_out_fpred,
+                                           int32_t* d_out_fstep, void* stream) {
+    ks_status st = check_common(eng, B, k, preds, n_preds);
+    if (st) return st;
+    if (B == 0) return KS_OK;
+    if (!d_tok || !d_out_tok || !d_out_lp || !d_out_count)
+        return set_error(KS_ERR_PARAMETER, "null device buffer");
+    ks_engine& E = *eng;
+    PredDev pd;
+    if ((st = upload_preds(E, preds, n_preds, pd))) return st;
+    if (pd.needs_desc && !d_desc) return set_error(KS_ERR_PARAMETER, "divisibility predicates need descriptors");
+    E.launches = 0;
+    cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, user);
+    cudaStreamWaitEvent(E.stream, ev, 0);
+    const int T = E.T;
+    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
+    for (int64_t c0 = 0; c0 < B; c0 += C) {
+        const int64_t n = std::min<int64_t>(C, B - c0);
+        st = run_chunk(E, n, k, false, d_tok + c0 * 7, d_desc ? reinterpret_cast<const long long*>(d_desc) + c0 * 7 : nullptr,
+                       pd, d_out_tok + c0 * k * T, d_out_lp + c0 * k, d_out_count + c0,
+                       d_out_status ? d_out_status + c0 : nullptr, d_out_fpred ? d_out_fpred + c0 : nullptr,
+                       d_out_fstep ? d_out_fstep + c0 : nullptr);
+        if (st) break;
+    }
+    cudaEventRecord(ev, E.stream);
+    cudaStreamWaitEvent(user, ev, 0);
+    cudaEventDestroy(ev);
+    if (!st && E.prof) collect_profile(E);
+    return st;
+}
+
+extern "C" void ks_engine_profile_reset(ks_engine* eng, int32_t enable) {
+    if (!eng) return;
+    collect_profile(*eng);
+    eng->prof = enable != 0;
+    eng->prof_ms = 0.0;
+    eng->prof_useful = 0.0;
+    eng->prof_n = 0;
+}
+
+extern "C" double ks_engine_profile_gemm_ms(const ks_engine* eng, int64_t* launches, double* useful) {
+    if (!eng) return 0.0;
+    if (launches) *launches = eng->prof_n;
+    if (useful) *useful = eng->prof_useful;
+    return eng->prof_ms;
+}

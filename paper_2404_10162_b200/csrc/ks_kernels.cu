@@ -1,0 +1,491 @@
+// ks_kernels.cu -- CUDA-core kernels of the B200 beam-decode engine:
+//   * lstm_step_simt   fp32 gate GEMM + fused LSTM cell (FP32 precision mode,
+//                      and the encoder's first step in every mode)
+//   * attention_pack   additive attention + context, writes the decoder GEMM
+//                      operand [ctx ; h_prev] (fp32 or fp16 hi/lo split)
+//   * uatt_kernel      per-config attention term b_h + a_t . W_a
+//   * beam_step        head GEMV + fp64 log-softmax + typed predicate mask +
+//                      warp top-k with the reference tie-break
+//   * beam_init        position-0 beam state
+//
+// Reference semantics restated (paths under /root/reference/proj):
+//   lstm_cell_step        src/nn.cpp:88-128
+//   attention_weights     src/models.cpp:265-281
+//   context_vector        src/models.cpp:283-294
+//   SequencePredictor::step src/models.cpp:448-493
+//   beam_search_impl      src/decoding.cpp:27-103 (children, 1e-300 floor, predicate
+//                         order, BeamExhaustedError, sort by (lp desc, prefix asc))
+//   greedy_decode         src/decoding.cpp:107-124 (strict '>' argmax)
+#include <cfloat>
+#include <cmath>
+
+#include "ks_common.cuh"
+
+namespace ksb {
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Fused LSTM cell epilogue shared by the SIMT and tensor-core GEMMs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void lstm_cell_store(const LstmArgs& p, int row, int u, float gi,
+                                                float gf, float go, float gc, int slot,
+                                                int crow) {
+    const float* G = p.G + (long long)slot * 4 * p.H;
+    gi += G[u];
+    gf += G[p.H + u];
+    go += G[2 * p.H + u];
+    gc += G[3 * p.H + u];
+    float cprev = 0.0f;
+    if (p.c_prev != nullptr && crow >= 0) cprev = p.c_prev[(long long)crow * p.ldc_prev + u];
+    const float ig = sigmoidf_(gi);
+    const float fg = sigmoidf_(gf);
+    const float og = sigmoidf_(go);
+    const float cg = tanhf(gc);
+    const float c = fg * cprev + ig * cg;
+    const float h = og * tanhf(c);
+    p.c_out[(long long)row * p.ldc + u] = c;
+    p.h_out[(long long)row * p.ldh + u] = h;
+    if (p.hA_hi != nullptr) {
+        __half hi, lo;
+        split_f16(h, hi, lo);
+        p.hA_hi[(long long)row * p.ldha + u] = hi;
+        p.hA_lo[(long long)row * p.ldha + u] = lo;
+    }
+}
+
+__device__ __forceinline__ int row_slot(const LstmArgs& p, int row) {
+    return p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0);
+}
+__device__ __forceinline__ int row_crow(const LstmArgs& p, int row) {
+    return p.parent ? p.parent[row] : row;
+}
+
+// ---------------------------------------------------------------------------
+// lstm_step_simt: tile 64 rows x 32 hidden units (x4 gates), 256 threads,
+// K chunks of 32 through shared memory, 4x(2 units x 4 gates) per thread.
+// ---------------------------------------------------------------------------
+constexpr int SB_M = 64, SB_U = 32, SB_K = 32;
+
+__global__ void __launch_bounds__(256) lstm_step_simt(LstmArgs a0, LstmArgs a1) {
+    const LstmArgs& p = blockIdx.z == 0 ? a0 : a1;
+    __shared__ float As[SB_K][SB_M + 1];
+    __shared__ __align__(16) float Ws[SB_K][SB_U * 4];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int row0 = blockIdx.x * SB_M;
+    const int ublk = blockIdx.y * SB_U;
+    if (ublk >= p.H) return;
+    float acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+
+    for (int k0 = 0; k0 < p.K; k0 += SB_K) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int idx = tid + 256 * i;
+            const int r = idx >> 5, kk = idx & 31;
+            const int row = row0 + r;
+            As[kk][r] = row < p.M ? p.A[(long long)row * p.lda + k0 + kk] : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int idx = tid + 256 * i;          // float4 index within 32 x 128
+            const int kk = idx >> 5, c4 = idx & 31;
+            const float4 v = *reinterpret_cast<const float4*>(
+                p.W + (long long)(k0 + kk) * 4 * p.H + ublk * 4 + c4 * 4);
+            *reinterpret_cast<float4*>(&Ws[kk][c4 * 4]) = v;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < SB_K; ++kk) {
+            float a[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+            const float4 w0 = *reinterpret_cast<const float4*>(&Ws[kk][tx * 8]);
+            const float4 w1 = *reinterpret_cast<const float4*>(&Ws[kk][tx * 8 + 4]);
+            const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = row0 + ty * 4 + i;
+        if (row >= p.M) continue;
+        const int slot = row_slot(p, row);
+        const int crow = row_crow(p, row);
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu) {
+            const int u = ublk + tx * 2 + uu;
+            lstm_cell_store(p, row, u, acc[i][uu * 4 + 0], acc[i][uu * 4 + 1], acc[i][uu * 4 + 2],
+                            acc[i][uu * 4 + 3], slot, crow);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// attention_pack: one warp per decoder row.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void store_operand(const AttnArgs& p, long long idx, float v) {
+    if (p.split_mode == 0) {
+        p.A[idx] = v;
+    } else if (p.split_mode == 1) {
+        __half hi, lo;
+        split_f16(v, hi, lo);
+        p.A_hi[idx] = hi;
+        p.A_lo[idx] = lo;
+    } else {
+        reinterpret_cast<__nv_bfloat16*>(p.A_hi)[idx] = __float2bfloat16_rn(v);
+    }
+}
+
+__global__ void __launch_bounds__(256) attention_pack(AttnArgs p) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (r >= p.M) return;
+    const int b = r / p.H_rows;
+    const int par = p.parent ? p.parent[r] : r;
+    const float* s = (p.h_prev != nullptr && par >= 0) ? p.h_prev + (long long)par * p.ldh : nullptr;
+    const int Kd = p.NA2 + p.NS;
+    const long long base = (long long)r * Kd;
+    float sd[kMaxNd];
+#pragma unroll
+    for (int d = 0; d < kMaxNd; ++d) sd[d] = 0.0f;
+    for (int i = lane; i < p.NS; i += 32) {
+        const float si = s ? s[i] : 0.0f;
+        for (int d = 0; d < p.nd; ++d) sd[d] = fmaf(si, p.Ws[i * p.nd + d], sd[d]);
+        store_operand(p, base + p.NA2 + i, si);
+    }
+    if (p.NA2 == 0) return;  // enc-dec: operand is h_prev only
+    for (int d = 0; d < p.nd; ++d) sd[d] = warp_sum_f(sd[d]);
+    // energies e_t = b_o + sum_d tanh(s.W_s + a_t.W_a + b_h)_d * w_o[d]; softmax over 7
+    float e[kTin];
+    float mx = -FLT_MAX;
+#pragma unroll
+    for (int t = 0; t < kTin; ++t) {
+        float v = p.bo;
+        const float* u = p.uatt + ((long long)b * kTin + t) * p.nd;
+        for (int d = 0; d < p.nd; ++d) v = fmaf(tanhf(sd[d] + u[d]), p.wo[d], v);
+        e[t] = v;
+        mx = fmaxf(mx, v);
+    }
+    float sum = 0.0f;
+#pragma unroll
+    for (int t = 0; t < kTin; ++t) {
+        e[t] = expf(e[t] - mx);
+        sum += e[t];
+    }
+    const float inv = 1.0f / sum;
+#pragma unroll
+    for (int t = 0; t < kTin; ++t) e[t] *= inv;
+    const float* act = p.act + (long long)b * kTin * p.NA2;
+    for (int j = lane; j < p.NA2; j += 32) {
+        float c = 0.0f;
+#pragma unroll
+        for (int t = 0; t < kTin; ++t) c = fmaf(e[t], act[t * p.NA2 + j], c);
+        store_operand(p, base + j, c);
+    }
+}
+
+// uatt[b][t][d] = b_h[d] + a_t . W_a[:, d]  (the s-independent half of the
+// attention energy network, computed once per config instead of per step).
+__global__ void __launch_bounds__(256) uatt_kernel(int C, int NA2, int nd, const float* act,
+                                                   const float* Wa, const float* bh, float* uatt) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long bt = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (bt >= (long long)C * kTin) return;
+    const float* a = act + bt * NA2;
+    float acc[kMaxNd];
+#pragma unroll
+    for (int d = 0; d < kMaxNd; ++d) acc[d] = 0.0f;
+    for (int i = lane; i < NA2; i += 32) {
+        const float ai = a[i];
+        for (int d = 0; d < nd; ++d) acc[d] = fmaf(ai, Wa[i * nd + d], acc[d]);
+    }
+    for (int d = 0; d < nd; ++d) {
+        const float v = warp_sum_f(acc[d]);
+        if (lane == 0) uatt[bt * nd + d] = v + bh[d];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// beam_init: position 0 has one live hypothesis per config (decoding.cpp:41-43).
+// ---------------------------------------------------------------------------
+__global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long long* key,
+                          int* status, int* fail_pred, int* fail_step) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    live[b] = 1;
+    lp[b] = 0.0;
+    key[b] = 0ull;
+    status[b] = 0;
+    fail_pred[b] = -1;
+    fail_step[b] = -1;
+}
+
+// ---------------------------------------------------------------------------
+// beam_step: one warp per config.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int key_token(unsigned long long key, const PosMeta& m, int i) {
+    return (int)((key >> m.shift[i]) & ((1ull << m.bits[i]) - 1ull));
+}
+
+__device__ bool pred_accepts(const BeamArgs& a, const PosMeta& m, const DevPred& q,
+                             unsigned long long key, int pos, const long long* desc_b) {
+    switch (q.kind) {
+        case 1: {  // MASK
+            const unsigned char* allowed = a.pred_bytes + q.allowed_off;
+            for (int i = 0; i <= pos; ++i)
+                if (!allowed[m.value_offset[i] + key_token(key, m, i)]) return false;
+            return true;
+        }
+        case 2: {  // BUDGET: alphabetical terms, separate fp64 mul and add (constraints.cpp:234-239)
+            double cost = 0.0;
+            for (int t = 0; t < q.n_terms; ++t) {
+                const int pp = a.term_pos[q.terms_off + t];
+                if (pp < 0 || pp > pos) continue;
+                const double v = (double)a.values[m.value_offset[pp] + key_token(key, m, pp)];
+                cost = __dadd_rn(cost, __dmul_rn(a.term_w[q.terms_off + t], v));
+            }
+            return cost <= q.budget;
+        }
+        case 3: {  // PRODUCT
+            __int128 prod = q.scale;
+            const __int128 cap = (__int128)1 << 100;
+            for (int t = 0; t < q.n_terms; ++t) {
+                const int pp = a.term_pos[q.terms_off + t];
+                if (pp < 0 || pp > pos) continue;
+                prod *= (__int128)a.values[m.value_offset[pp] + key_token(key, m, pp)];
+                if (prod > cap) prod = cap;
+                if (prod < -cap) prod = -cap;
+            }
+            return prod <= (__int128)q.limit;
+        }
+        case 4: {  // DIVIDES
+            for (int t = 0; t < q.n_terms; ++t) {
+                const int pp = a.term_pos[q.terms_off + t];
+                if (pp < 0 || pp > pos) continue;
+                const long long v = a.values[m.value_offset[pp] + key_token(key, m, pp)];
+                if (v <= 0 || desc_b == nullptr) return false;
+                if (desc_b[a.term_field[q.terms_off + t]] % v != 0) return false;
+            }
+            return true;
+        }
+        default:
+            return true;
+    }
+}
+
+// Candidate order: higher score first, exact ties to the smaller packed
+// prefix key (= lexicographically smaller prefix; Candidate::operator<,
+// decoding.cpp:21-24).
+__device__ __forceinline__ bool better(double s1, unsigned long long k1, double s2,
+                                       unsigned long long k2) {
+    return s1 > s2 || (s1 == s2 && k1 < k2);
+}
+
+__global__ void __launch_bounds__(256) beam_step(BeamArgs a, PosMeta m) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int V = m.vsize[a.pos];
+    const int Vs = V | 1;  // odd row stride: conflict-free lane-strided head reads
+    float* Wsh = reinterpret_cast<float*>(smem);
+    const int nW = a.NS * Vs;
+    for (int i = threadIdx.x; i < a.NS * V; i += blockDim.x) {
+        const int row = i / V, v = i - row * V;
+        Wsh[row * Vs + v] = a.Wh[i];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const int b = blockIdx.x * nwarps + warp;
+    if (b >= a.B) return;
+    unsigned char* cbase = smem + ((nW * 4 + 15) & ~15) + (size_t)warp * a.cands_per_warp * 28;
+    double* c_score = reinterpret_cast<double*>(cbase);
+    double* c_lp = c_score + a.cands_per_warp;
+    unsigned long long* c_key = reinterpret_cast<unsigned long long*>(c_lp + a.cands_per_warp);
+    int* c_meta = reinterpret_cast<int*>(c_key + a.cands_per_warp);
+
+    const int nc = a.H_cur * V;
+    const long long* desc_b = a.desc ? a.desc + (long long)b * kTin : nullptr;
+    const int T = m.T;
+
+    auto write_dead_next = [&](int from) {
+        if (a.final_step) return;
+        for (int i = from + lane; i < a.H_next; i += 32) {
+            const long long s = (long long)b * a.H_next + i;
+            a.live_next[s] = 0;
+            a.lp_next[s] = -INFINITY;
+            a.key_next[s] = 0ull;
+            a.parent_next[s] = b * a.H_cur;
+            a.slot_next[s] = m.fb_offset[a.pos];
+        }
+    };
+
+    if (a.status[b] != 0) {  // exhausted earlier: nothing left to extend
+        write_dead_next(0);
+        return;
+    }
+    const float bias = lane < V ? a.bh[lane] : 0.0f;
+    int n_alive = 0;
+    int last_live = -1;
+    for (int j = 0; j < a.H_cur; ++j) {
+        const long long r = (long long)b * a.H_cur + j;
+        const bool live = a.live_cur[r] != 0;
+        if (!live) {
+            for (int v = lane; v < V; v += 32) c_meta[j * V + v] = -1;
+            continue;
+        }
+        last_live = j;
+        // head: logits[v] = b[v] + sum_i h[i] W[i][v]   (models.cpp:490-491)
+        float part[kMaxV];
+#pragma unroll
+        for (int v = 0; v < kMaxV; ++v) part[v] = 0.0f;
+        const float* hr = a.h + r * a.NS;
+        for (int i = lane; i < a.NS; i += 32) {
+            const float hv = hr[i];
+            const float* wrow = Wsh + i * Vs;
+#pragma unroll
+            for (int v = 0; v < kMaxV; ++v)
+                if (v < V) part[v] = fmaf(hv, wrow[v], part[v]);
+        }
+        float logit = 0.0f;
+#pragma unroll
+        for (int v = 0; v < kMaxV; ++v) {
+            if (v < V) {
+                const float t = warp_sum_f(part[v]);
+                if (lane == v) logit = t;
+            }
+        }
+        // softmax in fp64 then log(max(p, 1e-300)) (nn.cpp:215-226, decoding.cpp:57-58)
+        const double l = lane < V ? (double)(logit + bias) : -INFINITY;
+        const double mx = warp_max_d(l);
+        const double ex = lane < V ? exp(l - mx) : 0.0;
+        const double sum = warp_sum_d(ex);
+        const double pr = ex / sum;
+        const double clp = a.lp_cur[r] + log(fmax(pr, 1e-300));
+        const unsigned long long key = a.key_cur[r] | ((unsigned long long)lane << m.shift[a.pos]);
+        int rej = -1;
+        if (lane < V) {
+            for (int q = 0; q < a.n_preds; ++q) {
+                const DevPred pq = a.preds[q];
+                if (pq.full && !a.final_step) continue;
+                if (!pred_accepts(a, m, pq, key, a.pos, desc_b)) {
+                    rej = q;
+                    break;
+                }
+            }
+            const int c = j * V + lane;
+            c_score[c] = a.greedy ? pr : clp;
+            c_lp[c] = clp;
+            c_key[c] = key;
+            c_meta[c] = rej < 0 ? ((j << 8) | lane) : -2 - rej;
+        }
+        n_alive += __popc(__ballot_sync(0xffffffffu, lane < V && rej < 0));
+    }
+    __syncwarp();
+    if (n_alive == 0) {
+        // BeamExhaustedError(last_rejecting, pos): every child was rejected, so the
+        // last rejecting predicate is that of the last child (last live hyp, last token).
+        if (lane == 0) {
+            int fp = -1;
+            if (last_live >= 0) {
+                const int mm = c_meta[last_live * V + V - 1];
+                fp = mm <= -2 ? -2 - mm : -1;
+            }
+            a.status[b] = 1;
+            a.fail_pred[b] = fp;
+            a.fail_step[b] = a.pos;
+            a.out_count[b] = 0;
+            if (a.out_status) a.out_status[b] = 1;
+            if (a.out_fail_pred) a.out_fail_pred[b] = fp;
+            if (a.out_fail_step) a.out_fail_step[b] = a.pos;
+        }
+        for (int i = lane; i < a.k * T; i += 32) a.out_tok[(long long)b * a.k * T + i] = -1;
+        for (int i = lane; i < a.k; i += 32) a.out_lp[(long long)b * a.k + i] = -INFINITY;
+        write_dead_next(0);
+        return;
+    }
+    const int ksel = n_alive < a.k ? n_alive : a.k;
+    for (int i = 0; i < ksel; ++i) {
+        double bs = -INFINITY;
+        unsigned long long bk = ~0ull;
+        int bc = -1;
+        for (int c = lane; c < nc; c += 32) {
+            if (c_meta[c] < 0) continue;
+            if (bc < 0 || better(c_score[c], c_key[c], bs, bk)) {
+                bs = c_score[c];
+                bk = c_key[c];
+                bc = c;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            if (oc >= 0 && (bc < 0 || better(os, ok, bs, bk))) {
+                bs = os;
+                bk = ok;
+                bc = oc;
+            }
+        }
+        if (lane == 0) {
+            const int meta = c_meta[bc];
+            const int j = meta >> 8, v = meta & 255;
+            const double clp = c_lp[bc];
+            if (a.final_step) {
+                const long long o = (long long)b * a.k + i;
+                a.out_lp[o] = clp;
+                for (int t = 0; t < T; ++t) a.out_tok[o * T + t] = key_token(bk, m, t);
+            } else {
+                const long long s = (long long)b * a.H_next + i;
+                a.live_next[s] = 1;
+                a.lp_next[s] = clp;
+                a.key_next[s] = bk;
+                a.parent_next[s] = b * a.H_cur + j;
+                a.slot_next[s] = m.fb_offset[a.pos] + v;
+            }
+            c_meta[bc] = -1;
+        }
+        __syncwarp();
+    }
+    if (a.final_step) {
+        for (int i = ksel + lane; i < a.k; i += 32) {
+            const long long o = (long long)b * a.k + i;
+            a.out_lp[o] = -INFINITY;
+            for (int t = 0; t < T; ++t) a.out_tok[o * T + t] = -1;
+        }
+        if (lane == 0) {
+            a.out_count[b] = ksel;
+            if (a.out_status) a.out_status[b] = 0;
+            if (a.out_fail_pred) a.out_fail_pred[b] = -1;
+            if (a.out_fail_step) a.out_fail_step[b] = -1;
+        }
+    } else {
+        write_dead_next(ksel);
+    }
+}
+
+}  // namespace ksb

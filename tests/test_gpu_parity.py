@@ -1,0 +1,144 @@
+"""GPU parity: the CUDA engine, called through its C-ABI, against the pinned
+fp64 oracle on the same inputs and checkpoints.
+
+Bar: decoded token sequences, their rank order, beam
+counts, exhaustion status / step / predicate identical on every config the
+oracle does not flag tie-adjacent (relative lp gap < 1e-4 between candidates
+deciding top-k membership or rank); log-probs within 1e-4 relative.
+"""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleModel
+from tests import ckpt_util
+from tests.golden.make_fixtures import TINY_MODELS
+from tests.util import BIG_CKPT, compare_beams, golden_path, have_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a GPU")]
+
+PRECISIONS = ["fp32", "f16x3"]
+
+
+def engine(path, precision):
+    from paper_2404_10162_b200._cabi import Engine
+    return Engine(path, 0, precision)
+
+
+def oracle_preds(o, spec):
+    out = []
+    for kind, arg in spec:
+        if kind == "membership":
+            out.append(o.membership())
+        elif kind == "budget":
+            out.append(o.budget(*arg))
+        elif kind == "mask":
+            out.append(o.mask(arg))
+        elif kind == "product":
+            out.append(o.product(*arg))
+        elif kind == "divides":
+            out.append(o.divides(arg))
+    return out
+
+
+def random_tokens(o, B, seed):
+    rng = np.random.default_rng(seed)
+    return np.stack([rng.integers(0, len(o.input_values[f]), B) for f in range(7)], 1).astype(np.int32)
+
+
+def random_desc(o, tok):
+    return np.array([[o.input_values[f][t] for f, t in enumerate(row)] for row in tok], np.int64)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("stem", [m[0] for m in TINY_MODELS])
+def test_tiny_models_all_k(stem, precision):
+    path = golden_path(stem + ".ckpt")
+    o, e = OracleModel(path), engine(path, precision)
+    tok = random_tokens(o, 128, 1)
+    for k in (1, 2, 3, 8, 64):
+        a, g = o.beam(tok, k), e.beam(tok, k)
+        n, ties, bad = compare_beams(g, a)
+        assert not bad, f"k={k}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+    assert (e.greedy(tok)[o.beam(tok, 1)["min_gap"] >= 1e-4] ==
+            o.greedy(tok)[o.beam(tok, 1)["min_gap"] >= 1e-4]).all()
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_small_trained_constrained(precision):
+    path = golden_path("attn_small_trained.ckpt")
+    o, e = OracleModel(path), engine(path, precision)
+    tok = random_tokens(o, 2048, 2)
+    desc = random_desc(o, tok)
+    for preds in ([], [("membership", None)],
+                  [("membership", None), ("budget", ({n: 1.0 for n in o.names}, 28.0))],
+                  [("budget", ({"chunk_size": 1.0, "k_mult": 2.0, "n_mult": 0.5}, 40.0)),
+                   ("product", (["read_size", "chunk_size", "n_mult"], 4, 512)),
+                   ("divides", [("c_mult", 1), ("k_mult", 4)])]):
+        po = oracle_preds(o, preds)
+        a = o.beam(tok, 5, desc, po, threads=8)
+        g = e.beam(tok, 5, desc, po)
+        n, ties, bad = compare_beams(g, a)
+        assert n > 0.9 * len(tok)
+        assert not bad, f"{preds}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_exact_tie_order(precision):
+    with tempfile.TemporaryDirectory() as tmp:
+        path = ckpt_util.modified(golden_path("tiny_attn_s232.ckpt"), os.path.join(tmp, "z.ckpt"),
+                                  lambda t: [t[n].fill(0) for n in t if n.startswith("head.")])
+        g = engine(path, precision).beam(np.array([[0, 1, 0, 1, 0, 1, 0]]), 5)
+        assert g["tokens"][0].tolist() == [[0, 0, 0], [0, 0, 1], [0, 1, 0], [0, 1, 1], [0, 2, 0]]
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_exhaustion_names_predicate_and_step(precision):
+    """decoding_test.cpp:300-318: a predicate rejecting every non-empty map
+    exhausts at step 0 and is named."""
+    path = golden_path("tiny_attn_s22.ckpt")
+    o, e = OracleModel(path), engine(path, precision)
+    never = o.mask([[0, 0], [0, 0]])
+    always = o.mask([[1, 1], [1, 1]])
+    g = e.beam(np.zeros((3, 7), np.int32), 4, preds=[always, never])
+    assert (g["status"] == 1).all() and (g["fail_step"] == 0).all() and (g["fail_pred"] == 1).all()
+    assert (g["count"] == 0).all() and (g["tokens"] == -1).all()
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_full_sequence_only_predicate(precision):
+    path = golden_path("tiny_attn_s3423.ckpt")
+    o, e = OracleModel(path), engine(path, precision)
+    tok = random_tokens(o, 64, 3)
+    preds = [o.budget({"p0": 1.0, "p1": 1.0, "p2": 1.0, "p3": 1.0}, 3.0, full_sequence_only=True)]
+    a, g = o.beam(tok, 6, preds=preds), e.beam(tok, 6, preds=preds)
+    n, ties, bad = compare_beams(g, a)
+    assert not bad
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_chunking_is_transparent(precision):
+    path = golden_path("attn_small_trained.ckpt")
+    e = engine(path, precision)
+    tok = random_tokens(OracleModel(path), 1000, 4)
+    full = e.beam(tok, 5)
+    e.set_chunk(97)
+    part = e.beam(tok, 5)
+    for key in ("tokens", "log_prob", "count"):
+        np.testing.assert_array_equal(full[key], part[key])
+
+
+@pytest.mark.skipif(not os.path.exists(BIG_CKPT), reason="default-size trained checkpoint absent")
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_default_size_trained_parity(precision):
+    o, e = OracleModel(BIG_CKPT), engine(BIG_CKPT, precision)
+    tok = random_tokens(o, 256, 7)
+    desc = random_desc(o, tok)
+    preds = oracle_preds(o, [("membership", None), ("budget", ({n: 1.0 for n in o.names}, 60.0))])
+    a = o.beam(tok, 5, desc, preds, threads=os.cpu_count() or 8)
+    g = e.beam(tok, 5, desc, preds)
+    n, ties, bad = compare_beams(g, a)
+    assert n >= 0.9 * len(tok)
+    assert not bad, f"{len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
