@@ -1,0 +1,365 @@
+"""Benchmark: constrained beam-search decode (beam = 5) of synthetic ConvFwd
+problem configs -- BASELINE.json config 2 (65,536 configs per GPU, default
+attn model n_a=256, n_s=512, n_d=2, ConvAsm1x1U, membership + resource-budget
+predicates).  Prints ONE JSON line.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--precision f16x3]
+
+* value: whole-job configs/s with tokens already resident in HBM; each step
+  is one device-resident ks_beam_search_device call over the GPU's 65,536
+  configs, timed with CUDA events on the launching stream; L2 is flushed
+  (a 512 MiB write) before every timed step; max over ranks.
+* e2e: the same workload through the reference-facing host C-ABI
+  (ks_beam_search_batch) with host buffers; H2D of tokens and D2H of beams
+  and log-probs are inside the timed region.
+* roofline: the gate GEMM (dominant kernel), useful FLOPs per launch
+  (reference live-hypothesis counts) / its CUDA-event time,
+  against MEASURED_PEAKS.json bf16 dense.
+* cpu_baseline: the unmodified reference (oracle/_ref, compiled from its own
+  sources) on a bounded sample, all host threads, rank 0 only.
+* --impl reference: the reference arm itself (same metric/config/unit).
+Multi-GPU: one process per GPU (torchrun), configs sharded by rank, no
+collective on the data path ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "problem-configs/sec, constrained beam decode (beam=5)"
+UNIT = "configs/s"
+KERNEL = "ConvAsm1x1U"
+BEAM = 5
+CONFIGS_PER_GPU = 65536
+BUDGET = 60.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="f16x3", choices=["f16x3", "fp32", "bf16"])
+    ap.add_argument("--configs", type=int, default=CONFIGS_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def model_path():
+    from paper_2404_10162_b200.synth import write_checkpoint
+
+    path = os.path.join(tempfile.gettempdir(), "ks_bench_attn_default.ckpt")
+    if not os.path.exists(path):
+        tmp = path + f".{os.getpid()}"
+        write_checkpoint(tmp, KERNEL, "attn", 256, 512, 2, seed=1)
+        os.replace(tmp, path)
+    return path
+
+
+def predicates(param_names, values):
+    """membership_predicate(spec) + resource_budget_predicate({p: 1.0}, 60)."""
+    from paper_2404_10162_b200._cabi import PRED_BUDGET, PRED_MASK
+
+    allowed = np.ones(sum(len(v) for v in values), np.uint8)
+    names = sorted(param_names)
+    return [{"kind": PRED_MASK, "allowed": allowed},
+            {"kind": PRED_BUDGET, "term_pos": np.array([param_names.index(n) for n in names], np.int32),
+             "term_w": np.ones(len(names)), "budget": BUDGET}]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("hbm_gbs"), "measured"
+    except Exception:
+        return 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def reference_rate(path, tok, threads, seconds_target=15.0, max_configs=None):
+    """Times the reference's own constrained_beam_search (oracle/_ref) on host cores."""
+    from oracle.oracle import RefModel
+
+    r = RefModel(path)
+    names = None
+    line = "membership\nbudget bud %g " % BUDGET
+    # param names from the checkpoint header
+    with open(path, "rb") as f:
+        head = f.read(8192).split(b"\n\n")[0].decode().split("\n")
+    names = [l.split(": ", 1)[1].split(" = ")[0] for l in head if l.startswith("param.")]
+    line += ",".join(f"{n}=1.0" for n in names)
+    n0 = max(threads, 8)
+    t0 = time.perf_counter()
+    r.beam(tok[:n0], BEAM, None, line, threads)
+    dt = time.perf_counter() - t0
+    rate0 = n0 / dt
+    n = int(min(len(tok), max(n0, rate0 * seconds_target)))
+    if max_configs:
+        n = min(n, max_configs)
+    t0 = time.perf_counter()
+    r.beam(tok[:n], BEAM, None, line, threads)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2404_10162_b200.synth import descriptors
+    from oracle.oracle import RefModel
+
+    path = model_path()
+    desc = descriptors(args.configs * max(1, args.gpus), KERNEL)
+    tok, bad = RefModel(path).encode(desc)
+    threads = os.cpu_count() or 1
+    # one step = a bounded sample sized so the whole W+K run ends within minutes
+    rate, n, dt = reference_rate(path, tok, threads, seconds_target=6.0)
+    step_n = max(threads, int(rate * 6.0))
+    times = []
+    for i in range(args.warmup + args.steps):
+        r_, n_, dt_ = reference_rate(path, tok[(i * step_n) % max(1, len(tok) - step_n):], threads,
+                                     seconds_target=6.0, max_configs=step_n)
+        if i >= args.warmup:
+            times.append((n_, dt_))
+    tot_n = sum(t[0] for t in times)
+    tot_t = sum(t[1] for t in times)
+    value = tot_n / tot_t
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1000.0 * tot_t / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"constrained beam search beam={BEAM}, {KERNEL} synthetic configs, "
+                                  "attn n_a=256 n_s=512 n_d=2 (bounded sample per step)",
+                      "configs_per_step": int(tot_n / args.steps), "beam": BEAM,
+                      "predicates": f"membership + resource_budget(sum values <= {BUDGET:g})"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": f"{int(tot_n / args.steps)} configs per step, "
+                                      f"constrained_beam_search via parallel_stripes({threads})"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_10162_b200 import _cabi
+    from paper_2404_10162_b200.synth import descriptors
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    path = model_path()
+    eng = _cabi.Engine(path, local, args.precision)
+    B = args.configs
+    desc_all = descriptors(B * world, KERNEL)
+    desc = desc_all[rank * B:(rank + 1) * B]
+    tok = eng.encode(desc)
+    with open(path, "rb") as f:
+        head = f.read(8192).split(b"\n\n")[0].decode().split("\n")
+    names = [l.split(": ", 1)[1].split(" = ")[0] for l in head if l.startswith("param.")]
+    values = [[int(x) for x in l.split(" = ")[1].split(",")] for l in head if l.startswith("param.")]
+    preds = predicates(names, values)
+    T = eng.T
+    stream = torch.cuda.current_stream()
+    d_tok = torch.from_numpy(tok).cuda()
+    d_out = {"tokens": torch.empty((B, BEAM, T), dtype=torch.int32, device="cuda"),
+             "log_prob": torch.empty((B, BEAM), dtype=torch.float64, device="cuda"),
+             "count": torch.empty(B, dtype=torch.int32, device="cuda"),
+             "status": torch.empty(B, dtype=torch.int32, device="cuda"),
+             "fail_pred": torch.empty(B, dtype=torch.int32, device="cuda"),
+             "fail_step": torch.empty(B, dtype=torch.int32, device="cuda")}
+    ptrs = {k: v.data_ptr() for k, v in d_out.items()}
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        eng.beam_device(d_tok.data_ptr(), 0, B, BEAM, preds, ptrs, stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            step()
+            s1.record(stream)
+            evs.append((s0, s1))
+        torch.cuda.synchronize()
+    launches_per_step = eng.launches()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = B * world * args.steps / (ms / 1000.0)
+
+    # roofline of the dominant kernel (gate GEMM), timed on the engine stream
+    eng.profile_reset(True)
+    step()
+    torch.cuda.synchronize()
+    gemm_ms, gemm_n, useful = eng.profile()
+    eng.profile_reset(False)
+    bf16_peak, hbm_peak, peak_kind = peaks()
+    achieved = useful / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            traffic = json.load(f).get(args.precision)
+    except Exception:
+        pass
+
+    # end to end through the host C-ABI (pinned staging, copies in the timed region)
+    for _ in range(max(1, args.warmup // 2)):
+        eng.beam(tok, BEAM, None, preds)
+    e2e_t = []
+    for _ in range(max(2, args.steps // 2)):
+        t0 = time.perf_counter()
+        eng.beam(tok, BEAM, None, preds)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = B * world * len(e2e_t) / e2e_s
+    h2d = B * 7 * 4
+    d2h = B * BEAM * T * 4 + B * BEAM * 8 + 4 * B * 4
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import ref_available
+
+            if ref_available():
+                threads = os.cpu_count() or 1
+                rate, n, dt = reference_rate(path, tok, threads, seconds_target=15.0)
+                cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"{n} configs of the same workload in {dt:.1f} s "
+                                 f"(reference constrained_beam_search, parallel_stripes({threads}))"}
+        except Exception as ex:  # reported, never fatal for the GPU number
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+    if rank == 0:
+        mma_factor = 3.0 if args.precision == "f16x3" else 1.0
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": {"f16x3": "f16x3 (fp16 hi/lo split, 3 MMAs, fp32 accumulate; fp32-grade)",
+                      "fp32": "fp32", "bf16": "bf16 (fp32 accumulate)"}[args.precision],
+            "data": "synthetic",
+            "config": {"workload": f"BASELINE config 2: constrained beam search beam={BEAM}, "
+                                   f"{B} synthetic {KERNEL} problem configs per GPU",
+                       "model": "attn n_a=256 n_s=512 n_d=2 (random init, reference checkpoint format)",
+                       "configs_per_gpu": B, "beam": BEAM,
+                       "predicates": f"membership + resource_budget(sum values <= {BUDGET:g})",
+                       "l2": "flushed (512 MiB write) before every timed step",
+                       "parallelism": f"dp{world} (configs sharded by rank, no collective)"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "ks_beam_search_batch (host buffers)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
+                         "frac": achieved / bf16_peak, "traffic": traffic,
+                         "kernel": "lstm_gemm_tc (gate GEMM + fused cell)" if args.precision != "fp32"
+                         else "lstm_step_simt",
+                         "peak_kind": f"{peak_kind} bf16 dense (burst)",
+                         "useful_flops_per_step": useful, "gemm_launches_per_step": gemm_n,
+                         "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / (ms / args.steps),
+                         "mma_issued_tflops": achieved * mma_factor},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

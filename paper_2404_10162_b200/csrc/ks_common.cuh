@@ -75,6 +75,7 @@ struct LstmArgs {
     __half* hA_hi;         // optional split copy of h_out for the next GEMM
     __half* hA_lo;
     long long ldha;
+    int ha_bf16;           // split copy as bf16 (BF16 mode) instead of fp16 hi/lo
 };
 
 struct AttnArgs {
@@ -145,6 +146,17 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
     hi = __float2half_rn(x);
     const float r = x - __half2float(hi);          // exact in fp32
     lo = __float2half_rn(r * 2048.0f);
+}
+
+__device__ __forceinline__ void store_split_h(const LstmArgs& p, long long idx, float h) {
+    if (p.ha_bf16) {
+        reinterpret_cast<__nv_bfloat16*>(p.hA_hi)[idx] = __float2bfloat16_rn(h);
+    } else {
+        __half hi, lo;
+        split_f16(h, hi, lo);
+        p.hA_hi[idx] = hi;
+        p.hA_lo[idx] = lo;
+    }
 }
 
 }  // namespace ksb

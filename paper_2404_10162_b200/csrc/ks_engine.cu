@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -35,7 +36,7 @@ __global__ void beam_step(BeamArgs a, PosMeta m);
 // tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
                     const __half* W_lo0, const __half* W_hi1, const __half* W_lo1,
-                    cudaStream_t stream, int* launches);
+                    cudaStream_t stream, int* launches, int units);
 }  // namespace ksb
 
 using namespace ksb;
@@ -153,6 +154,7 @@ struct ks_engine {
     std::vector<double> prof_flops;
     double prof_ms = 0.0, prof_useful = 0.0;
     int64_t prof_n = 0;
+    int tc_units = 32;
 };
 
 namespace {
@@ -182,7 +184,7 @@ struct HostTensors {
 // one-hot part (slot -> reference row, -1 = bias only).
 ks_status pack_lstm(const HostTensors& ht, const std::string& prefix, int rows, int H, int Hp,
                     const std::vector<int>& dense_rows, const std::vector<int>& slot_rows,
-                    DevLstm& out) {
+                    DevLstm& out, int precision, int units) {
     static const char* gates[4] = {"input", "forget", "output", "cand"};
     std::string err;
     const float* W[4];
@@ -209,12 +211,18 @@ ks_status pack_lstm(const HostTensors& ht, const std::string& prefix, int rows, 
                 if (std::fabs(w) > 60000.0f)
                     return set_error(KS_ERR_UNSUPPORTED, "weight magnitude exceeds the fp16 split range");
                 Wf[(size_t)k * 4 * Hp + u * 4 + g] = w;
-                // tensor-core layout: N index n = tile*256 + g*64 + u%64 (tile = u/64), K-major
-                const size_t n = (size_t)(u / 64) * 256 + (size_t)g * 64 + (u % 64);
-                const __half hi = __float2half_rn(w);
-                const float res = w - __half2float(hi);
-                Whi[n * K + k] = hi;
-                Wlo[n * K + k] = __float2half_rn(res * 2048.0f);
+                // tensor-core layout: N index n = blk*4U + g*U + u%U (blk = u/U), K-major
+                const size_t n = (size_t)(u / units) * 4 * units + (size_t)g * units + (u % units);
+                if (precision == KS_PREC_BF16) {
+                    const __nv_bfloat16 hb = __float2bfloat16_rn(w);
+                    std::memcpy(&Whi[n * K + k], &hb, 2);
+                    Wlo[n * K + k] = __float2half_rn(0.0f);
+                } else {
+                    const __half hi = __float2half_rn(w);
+                    const float res = w - __half2float(hi);
+                    Whi[n * K + k] = hi;
+                    Wlo[n * K + k] = __float2half_rn(res * 2048.0f);
+                }
             }
     }
     for (int s = 0; s < S; ++s) {
@@ -276,6 +284,7 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
     E.NA = round_up(E.n_a, 64);
     E.NS = round_up(E.n_s, 64);
     E.NE = round_up(E.e, 64);
+    if (const char* u = std::getenv("KS_TC_UNITS")) E.tc_units = std::atoi(u) == 64 ? 64 : 32;
     E.T = d->num_positions;
     E.in_sizes.assign(d->input_sizes, d->input_sizes + 7);
     E.in_offset.resize(7);
@@ -323,18 +332,18 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         std::vector<int> dense, slots;
         for (int k = 0; k < E.NE; ++k) dense.push_back(k < E.e ? E.d_in + k : -1);
         for (int s = 0; s < E.d_in; ++s) slots.push_back(s);
-        if ((st = pack_lstm(ht, "encoder", E.d_in + E.e, E.e, E.NE, dense, slots, E.enc[0]))) return st;
+        if ((st = pack_lstm(ht, "encoder", E.d_in + E.e, E.e, E.NE, dense, slots, E.enc[0], E.precision, E.tc_units))) return st;
         dense.clear();
         slots.clear();
         for (int k = 0; k < E.NE; ++k) dense.push_back(k < E.e ? E.d_fb + k : -1);
         for (int s = 0; s < E.d_fb; ++s) slots.push_back(s);
-        if ((st = pack_lstm(ht, "decoder", E.d_fb + E.e, E.e, E.NE, dense, slots, E.dec))) return st;
+        if ((st = pack_lstm(ht, "decoder", E.d_fb + E.e, E.e, E.NE, dense, slots, E.dec, E.precision, E.tc_units))) return st;
     } else {
         std::vector<int> dense, slots;
         for (int k = 0; k < E.NA; ++k) dense.push_back(k < E.n_a ? E.d_in + k : -1);
         for (int s = 0; s < E.d_in; ++s) slots.push_back(s);
-        if ((st = pack_lstm(ht, "pre.fwd", E.d_in + E.n_a, E.n_a, E.NA, dense, slots, E.enc[0]))) return st;
-        if ((st = pack_lstm(ht, "pre.bwd", E.d_in + E.n_a, E.n_a, E.NA, dense, slots, E.enc[1]))) return st;
+        if ((st = pack_lstm(ht, "pre.fwd", E.d_in + E.n_a, E.n_a, E.NA, dense, slots, E.enc[0], E.precision, E.tc_units))) return st;
+        if ((st = pack_lstm(ht, "pre.bwd", E.d_in + E.n_a, E.n_a, E.NA, dense, slots, E.enc[1], E.precision, E.tc_units))) return st;
         // decoder rows: [ctx (2 n_a) | fb one-hot (d_fb, attn only) | h (n_s)]  (models.cpp:215-219)
         const bool fbk = E.variant == KS_VARIANT_ATTN;
         const int hbase = 2 * E.n_a + (fbk ? E.d_fb : 0);
@@ -350,7 +359,7 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
             for (int s = 0; s < E.d_fb; ++s) slots.push_back(2 * E.n_a + s);
         else
             slots.push_back(-1);
-        if ((st = pack_lstm(ht, "post", rows, E.n_s, E.NS, dense, slots, E.dec))) return st;
+        if ((st = pack_lstm(ht, "post", rows, E.n_s, E.NS, dense, slots, E.dec, E.precision, E.tc_units))) return st;
         // attention energy network: attn.hidden (n_s + 2 n_a) x n_d, attn.out n_d x 1
         const float* Wh = ht.get("attn.hidden.weights", (E.n_s + 2 * E.n_a) * E.n_d, err);
         const float* bh = ht.get("attn.hidden.bias", E.n_d, err);
@@ -597,7 +606,8 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
     if (E.precision != KS_PREC_FP32 && a0.K > 0) {
         done = launch_lstm_tc(a0, a1, E.precision, L0.Whi.as<__half>(), L0.Wlo.as<__half>(),
                               L1 ? L1->Whi.as<__half>() : nullptr, L1 ? L1->Wlo.as<__half>() : nullptr,
-                              E.stream, &n);
+                              E.stream, &n, E.tc_units);
+        if (!done) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
     }
     if (!done) {
         dim3 grid((unsigned)((a0.M + SB_M_HOST - 1) / SB_M_HOST), (unsigned)(a0.H / 32), a1 ? 2u : 1u);
@@ -675,6 +685,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
                 p.hA_hi = encA_at(dir, sidx & 1, 0);
                 p.hA_lo = encA_at(dir, sidx & 1, 1);
                 p.ldha = He;
+                p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
             }
         }
         const double fl = sidx == 0 ? 0.0 : 2.0 * dirs * (double)C * He * 4.0 * He;

@@ -1,8 +1,476 @@
-// ks_gemm_tc.cu -- tcgen05 gate GEMM (placeholder until the tensor-core path lands).
+// ks_gemm_tc.cu -- the LSTM gate GEMM on the 5th-generation tensor cores
+// (tcgen05 + TMEM + TMA), with the LSTM cell fused into the epilogue.
+//
+//   gates[M x 4H] = A[M x K] . W^T + G[slot(row)]         (nn.cpp:88-128)
+//   c' = sig(f) c_prev[parent(row)] + sig(i) tanh(g);  h' = sig(o) tanh(c')
+//
+// Precision modes (include/ks_b200.h):
+//   F16X3: A = A_hi + 2^-11 A_lo and W = W_hi + 2^-11 W_lo (fp16 planes). Two
+//          TMEM accumulators per tile: D1 = A_hi.W_hi, D2 = A_hi.W_lo + A_lo.W_hi;
+//          gates = D1 + 2^-11 D2 (the dropped A_lo.W_lo term is 2^-22 relative).
+//   BF16:  one bf16 MMA per K step (A_hi / W_hi planes hold bf16).
+//
+// Structure: persistent CTAs (one per SM), 256 threads:
+//   warp 0      TMA producer (A and W tiles, 128B swizzle, mbarrier ring)
+//   warp 1      MMA issuer (one elected thread, tcgen05.mma.cta_group::1)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld -> cell update -> h, c (+ split h) stores
+// Tile: 128 rows x (4 gates x UNITS hidden units); the weight packing
+// interleaves the gates per UNITS-unit block so one N tile holds i,f,o,g of the
+// same units and the cell update needs no cross-CTA exchange.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
 #include "ks_common.cuh"
+
 namespace ksb {
-bool launch_lstm_tc(const LstmArgs&, const LstmArgs*, int, const __half*, const __half*,
-                    const __half*, const __half*, cudaStream_t, int*) {
-    return false;
+
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    while (!mbar_try_wait(bar, phase)) {
+    }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// K-major, 128B-swizzled operand tile: rows of 64 fp16 (128 B), 8-row atoms of
+// 1024 B (SBO), LBO unused (1), descriptor version 1, layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+}  // namespace tc
+
+struct TcProblem {
+    LstmArgs p;
+    int m_tiles;
+    int n_tiles;
+    int k_blocks;
+    int tile_begin;  // first global tile index of this problem
+};
+
+struct TcParams {
+    TcProblem prob[2];
+    int n_prob;
+    int total_tiles;
+};
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;
+
+template <int UNITS, bool SPLIT>
+struct TcCfg {
+    static constexpr int BN = 4 * UNITS;                       // gate columns per tile
+    static constexpr int PLANES = SPLIT ? 2 : 1;
+    static constexpr int A_BYTES = TC_BM * TC_BK * 2;          // one plane
+    static constexpr int B_BYTES = BN * TC_BK * 2;
+    static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
+    static constexpr int ACC_COLS = (SPLIT ? 2 : 1) * BN;      // fp32 TMEM columns per accumulator set
+    static constexpr int ACC_STAGES = 512 / ACC_COLS >= 2 ? 2 : 1;
+    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+    // instruction descriptor: fp32 accumulate (bits 4-5 = 1), A/B fp16 (0) or bf16 (1) at
+    // bits 7-9 / 10-12, both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
+    static constexpr uint32_t IDESC = (1u << 4) | ((SPLIT ? 0u : 1u) << 7) | ((SPLIT ? 0u : 1u) << 10) |
+                                      ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+};
+
+__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+template <int UNITS, bool SPLIT>
+__global__ void __launch_bounds__(256, 1)
+    lstm_gemm_tc(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap mA0,
+                 const __grid_constant__ CUtensorMap mAl0, const __grid_constant__ CUtensorMap mB0,
+                 const __grid_constant__ CUtensorMap mBl0, const __grid_constant__ CUtensorMap mA1,
+                 const __grid_constant__ CUtensorMap mAl1, const __grid_constant__ CUtensorMap mB1,
+                 const __grid_constant__ CUtensorMap mBl1) {
+    using Cfg = TcCfg<UNITS, SPLIT>;
+    constexpr int S = Cfg::STAGES;
+    constexpr int AS = Cfg::ACC_STAGES;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
+    // bars: full[S], empty[S], tfull[AS], tempty[AS]; then the TMEM base slot
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * AS);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            tc::mbar_init(tc::smem_u32(&bars[s]), 1);
+            tc::mbar_init(tc::smem_u32(&bars[S + s]), 1);
+        }
+        for (int a = 0; a < AS; ++a) {
+            tc::mbar_init(tc::smem_u32(&bars[2 * S + a]), 1);
+            tc::mbar_init(tc::smem_u32(&bars[2 * S + AS + a]), 4);  // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&mA0);
+        tc::tma_prefetch(&mB0);
+        if (SPLIT) {
+            tc::tma_prefetch(&mAl0);
+            tc::tma_prefetch(&mBl0);
+        }
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         tc::smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+                const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
+                const TcProblem& pr = P.prob[pi];
+                const int lt = t - pr.tile_begin;
+                const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
+                const CUtensorMap* ma = pi ? &mA1 : &mA0;
+                const CUtensorMap* mal = pi ? &mAl1 : &mAl0;
+                const CUtensorMap* mb = pi ? &mB1 : &mB0;
+                const CUtensorMap* mbl = pi ? &mBl1 : &mBl0;
+                for (int kb = 0; kb < pr.k_blocks; ++kb) {
+                    tc::mbar_wait(tc::smem_u32(&bars[S + stage]), phase ^ 1);
+                    const uint32_t full = tc::smem_u32(&bars[stage]);
+                    tc::mbar_expect_tx(full, Cfg::STAGE_BYTES);
+                    unsigned char* st = smem + stage * Cfg::STAGE_BYTES;
+                    const int kx = kb * TC_BK;
+                    tc::tma_load_2d(tc::smem_u32(st), ma, full, kx, mt * TC_BM);
+                    tc::tma_load_2d(tc::smem_u32(st + Cfg::A_BYTES), mb, full, kx, nt * Cfg::BN);
+                    if (SPLIT) {
+                        tc::tma_load_2d(tc::smem_u32(st + Cfg::A_BYTES + Cfg::B_BYTES), mal, full, kx,
+                                        mt * TC_BM);
+                        tc::tma_load_2d(tc::smem_u32(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES), mbl, full,
+                                        kx, nt * Cfg::BN);
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+                const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
+                const TcProblem& pr = P.prob[pi];
+                tc::mbar_wait(tc::smem_u32(&bars[2 * S + AS + acc]), acc_phase ^ 1);
+                tc::fence_after();
+                const uint32_t d1 = tmem_base + acc * Cfg::ACC_COLS;
+                const uint32_t d2 = d1 + Cfg::BN;
+                for (int kb = 0; kb < pr.k_blocks; ++kb) {
+                    tc::mbar_wait(tc::smem_u32(&bars[stage]), phase);
+                    tc::fence_after();
+                    const uint32_t a0 = tc::smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                    const uint32_t b0 = a0 + Cfg::A_BYTES;
+                    const uint32_t al = b0 + Cfg::B_BYTES;
+                    const uint32_t bl = al + Cfg::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k) {
+                        const uint32_t acc_flag = (kb > 0 || k > 0) ? 1u : 0u;
+                        const uint32_t koff = k * 32;  // 16 fp16 = 32 bytes along the swizzled row
+                        tc::mma_f16(d1, tc::smem_desc(a0 + koff), tc::smem_desc(b0 + koff), Cfg::IDESC,
+                                    acc_flag);
+                        if (SPLIT) {
+                            tc::mma_f16(d2, tc::smem_desc(a0 + koff), tc::smem_desc(bl + koff),
+                                        Cfg::IDESC, acc_flag);
+                            tc::mma_f16(d2, tc::smem_desc(al + koff), tc::smem_desc(b0 + koff),
+                                        Cfg::IDESC, 1u);
+                        }
+                    }
+                    tc::mma_commit(tc::smem_u32(&bars[S + stage]));  // frees the smem stage
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc::mma_commit(tc::smem_u32(&bars[2 * S + acc]));  // accumulator ready
+                if (++acc == AS) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+            const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
+            const TcProblem& pr = P.prob[pi];
+            const LstmArgs& p = pr.p;
+            const int lt = t - pr.tile_begin;
+            const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
+            tc::mbar_wait(tc::smem_u32(&bars[2 * S + acc]), acc_phase);
+            tc::fence_after();
+            const int row = mt * TC_BM + q * 32 + lane;
+            const bool valid = row < p.M;
+            const int slot = valid ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0) : 0;
+            const int crow = valid ? (p.parent ? p.parent[row] : row) : -1;
+            const float* G = p.G + (long long)slot * 4 * p.H;
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
+#pragma unroll 1
+            for (int c = 0; c < UNITS / 8; ++c) {
+                float g[4][8];
+                float g2[4][8];
+#pragma unroll
+                for (int gt = 0; gt < 4; ++gt) {
+                    tc::tmem_ld8(tbase + gt * UNITS + c * 8, g[gt]);
+                    if (SPLIT) tc::tmem_ld8(tbase + Cfg::BN + gt * UNITS + c * 8, g2[gt]);
+                }
+                tc::tmem_wait_ld();
+                if (valid) {
+                    const int u0 = nt * UNITS + c * 8;
+                    float hv[8], cv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int u = u0 + j;
+                        float gi = g[0][j], gf = g[1][j], go = g[2][j], gc = g[3][j];
+                        if (SPLIT) {
+                            gi = fmaf(g2[0][j], 1.0f / 2048.0f, gi);
+                            gf = fmaf(g2[1][j], 1.0f / 2048.0f, gf);
+                            go = fmaf(g2[2][j], 1.0f / 2048.0f, go);
+                            gc = fmaf(g2[3][j], 1.0f / 2048.0f, gc);
+                        }
+                        gi += G[u];
+                        gf += G[p.H + u];
+                        go += G[2 * p.H + u];
+                        gc += G[3 * p.H + u];
+                        const float cp =
+                            (p.c_prev != nullptr && crow >= 0) ? p.c_prev[(long long)crow * p.ldc_prev + u] : 0.0f;
+                        const float cn = sigm(gf) * cp + sigm(gi) * tanhf(gc);
+                        cv[j] = cn;
+                        hv[j] = sigm(go) * tanhf(cn);
+                    }
+                    float4* hd = reinterpret_cast<float4*>(p.h_out + (long long)row * p.ldh + u0);
+                    float4* cd = reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u0);
+                    hd[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                    hd[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                    cd[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+                    cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+                    if (p.hA_hi != nullptr && p.ha_bf16) {
+                        __align__(16) __nv_bfloat16 hb[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) hb[j] = __float2bfloat16_rn(hv[j]);
+                        *reinterpret_cast<uint4*>(p.hA_hi + (long long)row * p.ldha + u0) =
+                            *reinterpret_cast<const uint4*>(hb);
+                    } else if (p.hA_hi != nullptr) {
+                        __align__(16) __half hh[8], hl[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) split_f16(hv[j], hh[j], hl[j]);
+                        *reinterpret_cast<uint4*>(p.hA_hi + (long long)row * p.ldha + u0) =
+                            *reinterpret_cast<const uint4*>(hh);
+                        *reinterpret_cast<uint4*>(p.hA_lo + (long long)row * p.ldha + u0) =
+                            *reinterpret_cast<const uint4*>(hl);
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&bars[2 * S + AS + acc]));
+            if (++acc == AS) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc::fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 2D fp16/bf16 row-major [rows][cols] tensor, box [box_rows][64], 128B swizzle.
+bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, long long row_stride_elems,
+              int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)row_stride_elems * 2};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+template <int UNITS, bool SPLIT>
+bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, const __half* Wl0,
+                 const __half* Wh1, const __half* Wl1, cudaStream_t stream) {
+    using Cfg = TcCfg<UNITS, SPLIT>;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::SMEM) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    TcParams P{};
+    CUtensorMap maps[8];
+    const LstmArgs* args[2] = {&a0, a1};
+    const __half* wh[2] = {Wh0, Wh1};
+    const __half* wl[2] = {Wl0, Wl1};
+    P.n_prob = a1 ? 2 : 1;
+    int tiles = 0;
+    for (int i = 0; i < P.n_prob; ++i) {
+        const LstmArgs& a = *args[i];
+        if (a.K % TC_BK != 0 || a.H % UNITS != 0) return false;
+        TcProblem& pr = P.prob[i];
+        pr.p = a;
+        pr.m_tiles = (a.M + TC_BM - 1) / TC_BM;
+        pr.n_tiles = a.H / UNITS;
+        pr.k_blocks = a.K / TC_BK;
+        pr.tile_begin = tiles;
+        tiles += pr.m_tiles * pr.n_tiles;
+        // A planes: [M][K] with row stride K (decoder operand / encoder split h)
+        const long long lda = a.K;
+        if (!make_map(&maps[4 * i + 0], a.A_hi, a.M, a.K, lda, TC_BM)) return false;
+        if (!make_map(&maps[4 * i + 1], SPLIT ? a.A_lo : a.A_hi, a.M, a.K, lda, TC_BM)) return false;
+        if (!make_map(&maps[4 * i + 2], wh[i], 4LL * a.H, a.K, a.K, Cfg::BN)) return false;
+        if (!make_map(&maps[4 * i + 3], SPLIT ? wl[i] : wh[i], 4LL * a.H, a.K, a.K, Cfg::BN)) return false;
+    }
+    if (P.n_prob == 1)
+        for (int j = 4; j < 8; ++j) maps[j] = maps[j - 4];
+    P.total_tiles = tiles;
+    const int grid = tiles < sm_count() ? tiles : sm_count();
+    lstm_gemm_tc<UNITS, SPLIT><<<grid, 256, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3], maps[4],
+                                                                 maps[5], maps[6], maps[7]);
+    return cudaGetLastError() == cudaSuccess;
+}
+
+}  // namespace
+
+int tc_units_default() { return 32; }
+
+bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
+                    const __half* W_lo0, const __half* W_hi1, const __half* W_lo1, cudaStream_t stream,
+                    int* launches, int units) {
+    bool ok;
+    if (mode == 0)
+        ok = units == 64 ? launch_impl<64, true>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream)
+                         : launch_impl<32, true>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream);
+    else
+        ok = units == 64 ? launch_impl<64, false>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream)
+                         : launch_impl<32, false>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream);
+    if (ok && launches) *launches = 1;
+    return ok;
+}
+
 }  // namespace ksb

@@ -62,12 +62,7 @@ __device__ __forceinline__ void lstm_cell_store(const LstmArgs& p, int row, int 
     const float h = og * tanhf(c);
     p.c_out[(long long)row * p.ldc + u] = c;
     p.h_out[(long long)row * p.ldh + u] = h;
-    if (p.hA_hi != nullptr) {
-        __half hi, lo;
-        split_f16(h, hi, lo);
-        p.hA_hi[(long long)row * p.ldha + u] = hi;
-        p.hA_lo[(long long)row * p.ldha + u] = lo;
-    }
+    if (p.hA_hi != nullptr) store_split_h(p, (long long)row * p.ldha + u, h);
 }
 
 __device__ __forceinline__ int row_slot(const LstmArgs& p, int row) {
