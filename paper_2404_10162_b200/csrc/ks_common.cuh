@@ -90,6 +90,9 @@ struct AttnArgs {
     const float* act;      // [C][7][NA2]
     const float* uatt;     // [C][7][nd]
     const float* Ws;       // [NS][nd]  (attn.hidden rows for s_prev)
+    const float* Wa;       // [NA2][nd] (attn.hidden rows for a_t), position 0 only
+    const float* bh;       // [nd], position 0 only
+    float* uatt_out;       // [C][7][nd] written at position 0
     const float* wo;       // [nd]
     float bo;
     float* A;              // FP32 operand out [M][NA2+NS]

@@ -27,12 +27,11 @@
 
 namespace ksb {
 __global__ void lstm_step_simt(LstmArgs a0, LstmArgs a1);
-__global__ void attention_pack(AttnArgs p);
-__global__ void uatt_kernel(int C, int NA2, int nd, const float* act, const float* Wa,
-                            const float* bh, float* uatt);
+bool launch_attention(const AttnArgs& p, bool first, cudaStream_t s);
 __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long long* key,
                           int* status, int* fail_pred, int* fail_step);
-__global__ void beam_step(BeamArgs a, PosMeta m);
+size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp);
+bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s);
 // tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
                     const __half* W_lo0, const __half* W_hi1, const __half* W_lo1,
@@ -155,6 +154,7 @@ struct ks_engine {
     double prof_ms = 0.0, prof_useful = 0.0;
     int64_t prof_n = 0;
     int tc_units = 32;
+    int num_sms = 148;
 };
 
 namespace {
@@ -399,8 +399,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
     if ((st = upload(E.values, vals.data(), vals.size() * 8))) return st;
     if (cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking) != cudaSuccess)
         return set_error(KS_ERR_CUDA, "stream creation failed");
-    cudaFuncSetAttribute(beam_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     E.beam_smem_max = 227 * 1024;
+    cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device);
     *out = eng.release();
     return KS_OK;
 }
@@ -692,12 +692,6 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
         if ((st = launch_lstm(E, a[0], dirs == 2 ? &a[1] : nullptr, E.enc[0], dirs == 2 ? &E.enc[1] : nullptr, fl)))
             return st;
     }
-    if (!enc_dec) {
-        const long long n = C * 7;
-        uatt_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>((int)C, NA2, E.n_d, act, E.attWa.as<float>(),
-                                                            E.attBh.as<float>(), E.uatt.as<float>());
-        E.launches++;
-    }
     beam_init<<<(unsigned)((C + 255) / 256), 256, 0, s>>>((int)C, E.live[0].as<unsigned char>(),
                                                           E.lp[0].as<double>(),
                                                           E.key[0].as<unsigned long long>(),
@@ -748,13 +742,17 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
         aa.uatt = E.uatt.as<float>();
         aa.Ws = enc_dec ? nullptr : E.attWs.as<float>();
         aa.wo = enc_dec ? nullptr : E.attWo.as<float>();
+        aa.Wa = enc_dec ? nullptr : E.attWa.as<float>();
+        aa.bh = enc_dec ? nullptr : E.attBh.as<float>();
+        aa.uatt_out = E.uatt.as<float>();
         aa.bo = E.attBo;
         aa.A = E.Abuf.as<float>();
         aa.A_hi = E.Ahi.as<__half>();
         aa.A_lo = E.Alo.as<__half>();
         aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
         if (enc_dec) aa.nd = 0;
-        attention_pack<<<(unsigned)((M + 7) / 8), 256, 0, s>>>(aa);
+        if (!launch_attention(aa, pos == 0 && !enc_dec, s))
+            return set_error(KS_ERR_UNSUPPORTED, "attention_dense_nodes outside 1..8");
         E.launches++;
 
         LstmArgs p{};
@@ -831,13 +829,16 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
         b.out_fail_pred = o_fpred;
         b.out_fail_step = o_fstep;
         b.cands_per_warp = cpw;
-        const size_t wsm = ((size_t)Hd * (V | 1) * 4 + 15) & ~(size_t)15;
         int warps = 8;
-        while (warps > 1 && wsm + (size_t)warps * cpw * 28 > (size_t)E.beam_smem_max) --warps;
-        const size_t smem = wsm + (size_t)warps * cpw * 28;
+        while (warps > 1 && beam_smem_bytes(Hd, V, warps, cpw) > (size_t)E.beam_smem_max) --warps;
+        const size_t smem = beam_smem_bytes(Hd, V, warps, cpw);
         if (smem > (size_t)E.beam_smem_max)
             return set_error(KS_ERR_UNSUPPORTED, "beam width x vocabulary too large for the beam kernel");
-        beam_step<<<(unsigned)((C + warps - 1) / warps), warps * 32, smem, s>>>(b, E.meta);
+        // persistent: the head weights are staged into shared memory once per CTA
+        const int per_sm = std::max(1, std::min(8, (int)((228 * 1024) / (smem + 1024))));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((C + warps - 1) / warps, (int64_t)E.num_sms * per_sm));
+        if (!launch_beam(b, E.meta, warps, smem, grid, s))
+            return set_error(KS_ERR_CUDA, "beam kernel launch failed");
         E.launches++;
         const cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("beam launch: ") + cudaGetErrorString(err));

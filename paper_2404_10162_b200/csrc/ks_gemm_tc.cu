@@ -10,11 +10,11 @@
 //          gates = D1 + 2^-11 D2 (the dropped A_lo.W_lo term is 2^-22 relative).
 //   BF16:  one bf16 MMA per K step (A_hi / W_hi planes hold bf16).
 //
-// Structure: persistent CTAs (one per SM), 256 threads:
+// Structure: persistent CTAs (one per SM), 384 threads:
 //   warp 0      TMA producer (A and W tiles, 128B swizzle, mbarrier ring)
 //   warp 1      MMA issuer (one elected thread, tcgen05.mma.cta_group::1)
 //   warp 2      TMEM allocator
-//   warps 4..7  epilogue: tcgen05.ld -> cell update -> h, c (+ split h) stores
+//   warps 4..11 epilogue: tcgen05.ld -> cell update -> h, c (+ split h) stores
 // Tile: 128 rows x (4 gates x UNITS hidden units); the weight packing
 // interleaves the gates per UNITS-unit block so one N tile holds i,f,o,g of the
 // same units and the cell update needs no cross-CTA exchange.
@@ -143,10 +143,13 @@ struct TcCfg {
                                       ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 };
 
-__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
+// Cell nonlinearities with MUFU exp2 + fast reciprocal: absolute error ~1e-7,
+// far below the fp32-grade GEMM tolerance (the FP32 mode keeps libm expf/tanhf).
+__device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanh_fast(float x) { return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x)); }
 
 template <int UNITS, bool SPLIT>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     lstm_gemm_tc(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap mA0,
                  const __grid_constant__ CUtensorMap mAl0, const __grid_constant__ CUtensorMap mB0,
                  const __grid_constant__ CUtensorMap mBl0, const __grid_constant__ CUtensorMap mA1,
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         for (int a = 0; a < AS; ++a) {
             tc::mbar_init(tc::smem_u32(&bars[2 * S + a]), 1);
-            tc::mbar_init(tc::smem_u32(&bars[2 * S + AS + a]), 4);  // one arrive per epilogue warp
+            tc::mbar_init(tc::smem_u32(&bars[2 * S + AS + a]), 8);  // one arrive per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -277,7 +280,11 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        // 8 warps: warp%4 selects the TMEM lane quarter (hardware access rule),
+        // (warp-4)/4 selects which half of the tile's UNITS hidden units.
+        const int q = warp & 3;
+        const int half = (warp - 4) >> 2;
+        constexpr int HU = UNITS / 2;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
@@ -286,30 +293,49 @@ __global__ void __launch_bounds__(256, 1)
             const LstmArgs& p = pr.p;
             const int lt = t - pr.tile_begin;
             const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
-            tc::mbar_wait(tc::smem_u32(&bars[2 * S + acc]), acc_phase);
-            tc::fence_after();
             const int row = mt * TC_BM + q * 32 + lane;
             const bool valid = row < p.M;
+            // per-row gathers issued before waiting on the accumulator
             const int slot = valid ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0) : 0;
             const int crow = valid ? (p.parent ? p.parent[row] : row) : -1;
             const float* G = p.G + (long long)slot * 4 * p.H;
+            tc::mbar_wait(tc::smem_u32(&bars[2 * S + acc]), acc_phase);
+            tc::fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
 #pragma unroll 1
-            for (int c = 0; c < UNITS / 8; ++c) {
+            for (int c = 0; c < HU / 8; ++c) {
+                const int uc = half * HU + c * 8;  // unit offset within the tile
                 float g[4][8];
                 float g2[4][8];
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt) {
-                    tc::tmem_ld8(tbase + gt * UNITS + c * 8, g[gt]);
-                    if (SPLIT) tc::tmem_ld8(tbase + Cfg::BN + gt * UNITS + c * 8, g2[gt]);
+                    tc::tmem_ld8(tbase + gt * UNITS + uc, g[gt]);
+                    if (SPLIT) tc::tmem_ld8(tbase + Cfg::BN + gt * UNITS + uc, g2[gt]);
                 }
                 tc::tmem_wait_ld();
                 if (valid) {
-                    const int u0 = nt * UNITS + c * 8;
+                    const int u0 = nt * UNITS + uc;
+                    float gb[4][8];
+#pragma unroll
+                    for (int gt = 0; gt < 4; ++gt) {
+                        const float4 b0 = *reinterpret_cast<const float4*>(G + gt * p.H + u0);
+                        const float4 b1 = *reinterpret_cast<const float4*>(G + gt * p.H + u0 + 4);
+                        gb[gt][0] = b0.x; gb[gt][1] = b0.y; gb[gt][2] = b0.z; gb[gt][3] = b0.w;
+                        gb[gt][4] = b1.x; gb[gt][5] = b1.y; gb[gt][6] = b1.z; gb[gt][7] = b1.w;
+                    }
+                    float cp[8];
+                    if (p.c_prev != nullptr && crow >= 0) {
+                        const float4 c0 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0);
+                        const float4 c1 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0 + 4);
+                        cp[0] = c0.x; cp[1] = c0.y; cp[2] = c0.z; cp[3] = c0.w;
+                        cp[4] = c1.x; cp[5] = c1.y; cp[6] = c1.z; cp[7] = c1.w;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) cp[j] = 0.0f;
+                    }
                     float hv[8], cv[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int u = u0 + j;
                         float gi = g[0][j], gf = g[1][j], go = g[2][j], gc = g[3][j];
                         if (SPLIT) {
                             gi = fmaf(g2[0][j], 1.0f / 2048.0f, gi);
@@ -317,15 +343,13 @@ __global__ void __launch_bounds__(256, 1)
                             go = fmaf(g2[2][j], 1.0f / 2048.0f, go);
                             gc = fmaf(g2[3][j], 1.0f / 2048.0f, gc);
                         }
-                        gi += G[u];
-                        gf += G[p.H + u];
-                        go += G[2 * p.H + u];
-                        gc += G[3 * p.H + u];
-                        const float cp =
-                            (p.c_prev != nullptr && crow >= 0) ? p.c_prev[(long long)crow * p.ldc_prev + u] : 0.0f;
-                        const float cn = sigm(gf) * cp + sigm(gi) * tanhf(gc);
+                        gi += gb[0][j];
+                        gf += gb[1][j];
+                        go += gb[2][j];
+                        gc += gb[3][j];
+                        const float cn = sigm_fast(gf) * cp[j] + sigm_fast(gi) * tanh_fast(gc);
                         cv[j] = cn;
-                        hv[j] = sigm(go) * tanhf(cn);
+                        hv[j] = sigm_fast(go) * tanh_fast(cn);
                     }
                     float4* hd = reinterpret_cast<float4*>(p.h_out + (long long)row * p.ldh + u0);
                     float4* cd = reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u0);
@@ -450,7 +474,7 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         for (int j = 4; j < 8; ++j) maps[j] = maps[j - 4];
     P.total_tiles = tiles;
     const int grid = tiles < sm_count() ? tiles : sm_count();
-    lstm_gemm_tc<UNITS, SPLIT><<<grid, 256, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3], maps[4],
+    lstm_gemm_tc<UNITS, SPLIT><<<grid, 384, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3], maps[4],
                                                                  maps[5], maps[6], maps[7]);
     return cudaGetLastError() == cudaSuccess;
 }

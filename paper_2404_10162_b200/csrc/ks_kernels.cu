@@ -3,7 +3,7 @@
 //                      and the encoder's first step in every mode)
 //   * attention_pack   additive attention + context, writes the decoder GEMM
 //                      operand [ctx ; h_prev] (fp32 or fp16 hi/lo split)
-//   * uatt_kernel      per-config attention term b_h + a_t . W_a
+//   (uatt = b_h + a_t . W_a is computed by the position-0 attention launch)
 //   * beam_step        head GEMV + fp64 log-softmax + typed predicate mask +
 //                      warp top-k with the reference tie-break
 //   * beam_init        position-0 beam state
@@ -141,22 +141,42 @@ __global__ void __launch_bounds__(256) lstm_step_simt(LstmArgs a0, LstmArgs a1) 
 }
 
 // ---------------------------------------------------------------------------
-// attention_pack: one warp per decoder row.
+// attention_pack: one warp per decoder row (models.cpp:265-294, 466-478).
+//   s = h_prev[parent(row)] (zero state at position 0)
+//   e_t = b_o + sum_d tanh(s.W_s[:,d] + u[t][d]) * w_o[d],  u[t][d] = b_h[d] + a_t.W_a[:,d]
+//   alpha = softmax_t(e);  ctx = sum_t alpha_t a_t
+//   A[row] = [ctx ; s]  (fp32, fp16 hi/lo split, or bf16)
+// FIRST (position 0, one row per config): also computes and stores u.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void store_operand(const AttnArgs& p, long long idx, float v) {
-    if (p.split_mode == 0) {
-        p.A[idx] = v;
-    } else if (p.split_mode == 1) {
-        __half hi, lo;
-        split_f16(v, hi, lo);
-        p.A_hi[idx] = hi;
-        p.A_lo[idx] = lo;
+template <int SPLIT>
+__device__ __forceinline__ void store4(const AttnArgs& p, long long idx, float4 v) {
+    if (SPLIT == 0) {
+        *reinterpret_cast<float4*>(p.A + idx) = v;
+    } else if (SPLIT == 1) {
+        __half hi[4], lo[4];
+        split_f16(v.x, hi[0], lo[0]);
+        split_f16(v.y, hi[1], lo[1]);
+        split_f16(v.z, hi[2], lo[2]);
+        split_f16(v.w, hi[3], lo[3]);
+        uint2 h, l;
+        h.x = (uint32_t)__half_as_ushort(hi[0]) | ((uint32_t)__half_as_ushort(hi[1]) << 16);
+        h.y = (uint32_t)__half_as_ushort(hi[2]) | ((uint32_t)__half_as_ushort(hi[3]) << 16);
+        l.x = (uint32_t)__half_as_ushort(lo[0]) | ((uint32_t)__half_as_ushort(lo[1]) << 16);
+        l.y = (uint32_t)__half_as_ushort(lo[2]) | ((uint32_t)__half_as_ushort(lo[3]) << 16);
+        *reinterpret_cast<uint2*>(p.A_hi + idx) = h;
+        *reinterpret_cast<uint2*>(p.A_lo + idx) = l;
     } else {
-        reinterpret_cast<__nv_bfloat16*>(p.A_hi)[idx] = __float2bfloat16_rn(v);
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
+        __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
+        uint2 h;
+        h.x = *reinterpret_cast<uint32_t*>(&a);
+        h.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(p.A_hi + idx) = h;
     }
 }
 
-__global__ void __launch_bounds__(256) attention_pack(AttnArgs p) {
+template <int ND, int SPLIT, bool FIRST>
+__global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x >> 5) + warp;
     if (r >= p.M) return;
@@ -165,24 +185,58 @@ __global__ void __launch_bounds__(256) attention_pack(AttnArgs p) {
     const float* s = (p.h_prev != nullptr && par >= 0) ? p.h_prev + (long long)par * p.ldh : nullptr;
     const int Kd = p.NA2 + p.NS;
     const long long base = (long long)r * Kd;
-    float sd[kMaxNd];
+    float sd[ND > 0 ? ND : 1];
 #pragma unroll
-    for (int d = 0; d < kMaxNd; ++d) sd[d] = 0.0f;
-    for (int i = lane; i < p.NS; i += 32) {
-        const float si = s ? s[i] : 0.0f;
-        for (int d = 0; d < p.nd; ++d) sd[d] = fmaf(si, p.Ws[i * p.nd + d], sd[d]);
-        store_operand(p, base + p.NA2 + i, si);
+    for (int d = 0; d < ND; ++d) sd[d] = 0.0f;
+    for (int c = lane; c < p.NS / 4; c += 32) {
+        const float4 v = s ? *reinterpret_cast<const float4*>(s + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ND > 0 && s) {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+#pragma unroll
+                for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], p.Ws[(4 * c + e) * ND + d], sd[d]);
+        }
+        store4<SPLIT>(p, base + p.NA2 + 4 * c, v);
     }
-    if (p.NA2 == 0) return;  // enc-dec: operand is h_prev only
-    for (int d = 0; d < p.nd; ++d) sd[d] = warp_sum_f(sd[d]);
-    // energies e_t = b_o + sum_d tanh(s.W_s + a_t.W_a + b_h)_d * w_o[d]; softmax over 7
+    if (ND == 0) return;  // enc-dec: the operand is h_prev only
+#pragma unroll
+    for (int d = 0; d < ND; ++d) sd[d] = warp_sum_f(sd[d]);
+    const float* act = p.act + (long long)b * kTin * p.NA2;
+    float u[kTin][ND > 0 ? ND : 1];
+    if (FIRST) {
+#pragma unroll
+        for (int t = 0; t < kTin; ++t) {
+            float acc[ND > 0 ? ND : 1];
+#pragma unroll
+            for (int d = 0; d < ND; ++d) acc[d] = 0.0f;
+            for (int c = lane; c < p.NA2 / 4; c += 32) {
+                const float4 a4 = *reinterpret_cast<const float4*>(act + t * p.NA2 + 4 * c);
+                const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) acc[d] = fmaf(av[e], p.Wa[(4 * c + e) * ND + d], acc[d]);
+            }
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                u[t][d] = warp_sum_f(acc[d]) + p.bh[d];
+                if (lane == 0) p.uatt_out[((long long)b * kTin + t) * ND + d] = u[t][d];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < kTin; ++t)
+#pragma unroll
+            for (int d = 0; d < ND; ++d) u[t][d] = p.uatt[((long long)b * kTin + t) * ND + d];
+    }
     float e[kTin];
     float mx = -FLT_MAX;
 #pragma unroll
     for (int t = 0; t < kTin; ++t) {
         float v = p.bo;
-        const float* u = p.uatt + ((long long)b * kTin + t) * p.nd;
-        for (int d = 0; d < p.nd; ++d) v = fmaf(tanhf(sd[d] + u[d]), p.wo[d], v);
+#pragma unroll
+        for (int d = 0; d < ND; ++d) v = fmaf(tanhf(sd[d] + u[t][d]), p.wo[d], v);
         e[t] = v;
         mx = fmaxf(mx, v);
     }
@@ -195,34 +249,49 @@ __global__ void __launch_bounds__(256) attention_pack(AttnArgs p) {
     const float inv = 1.0f / sum;
 #pragma unroll
     for (int t = 0; t < kTin; ++t) e[t] *= inv;
-    const float* act = p.act + (long long)b * kTin * p.NA2;
-    for (int j = lane; j < p.NA2; j += 32) {
-        float c = 0.0f;
+    for (int c = lane; c < p.NA2 / 4; c += 32) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int t = 0; t < kTin; ++t) c = fmaf(e[t], act[t * p.NA2 + j], c);
-        store_operand(p, base + j, c);
+        for (int t = 0; t < kTin; ++t) {
+            const float4 a4 = *reinterpret_cast<const float4*>(act + t * p.NA2 + 4 * c);
+            acc.x = fmaf(e[t], a4.x, acc.x);
+            acc.y = fmaf(e[t], a4.y, acc.y);
+            acc.z = fmaf(e[t], a4.z, acc.z);
+            acc.w = fmaf(e[t], a4.w, acc.w);
+        }
+        store4<SPLIT>(p, base + 4 * c, acc);
     }
 }
 
-// uatt[b][t][d] = b_h[d] + a_t . W_a[:, d]  (the s-independent half of the
-// attention energy network, computed once per config instead of per step).
-__global__ void __launch_bounds__(256) uatt_kernel(int C, int NA2, int nd, const float* act,
-                                                   const float* Wa, const float* bh, float* uatt) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long bt = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (bt >= (long long)C * kTin) return;
-    const float* a = act + bt * NA2;
-    float acc[kMaxNd];
-#pragma unroll
-    for (int d = 0; d < kMaxNd; ++d) acc[d] = 0.0f;
-    for (int i = lane; i < NA2; i += 32) {
-        const float ai = a[i];
-        for (int d = 0; d < nd; ++d) acc[d] = fmaf(ai, Wa[i * nd + d], acc[d]);
+template <int ND, int SPLIT>
+void launch_attention_nd(const AttnArgs& p, bool first, cudaStream_t s) {
+    const unsigned grid = (unsigned)((p.M + 7) / 8);
+    if (first)
+        attention_pack_t<ND, SPLIT, true><<<grid, 256, 0, s>>>(p);
+    else
+        attention_pack_t<ND, SPLIT, false><<<grid, 256, 0, s>>>(p);
+}
+
+template <int SPLIT>
+bool launch_attention_split(const AttnArgs& p, bool first, cudaStream_t s) {
+    switch (p.nd) {
+        case 0: launch_attention_nd<0, SPLIT>(p, first, s); return true;
+        case 1: launch_attention_nd<1, SPLIT>(p, first, s); return true;
+        case 2: launch_attention_nd<2, SPLIT>(p, first, s); return true;
+        case 3: launch_attention_nd<3, SPLIT>(p, first, s); return true;
+        case 4: launch_attention_nd<4, SPLIT>(p, first, s); return true;
+        case 5: launch_attention_nd<5, SPLIT>(p, first, s); return true;
+        case 6: launch_attention_nd<6, SPLIT>(p, first, s); return true;
+        case 7: launch_attention_nd<7, SPLIT>(p, first, s); return true;
+        case 8: launch_attention_nd<8, SPLIT>(p, first, s); return true;
+        default: return false;
     }
-    for (int d = 0; d < nd; ++d) {
-        const float v = warp_sum_f(acc[d]);
-        if (lane == 0) uatt[bt * nd + d] = v + bh[d];
-    }
+}
+
+bool launch_attention(const AttnArgs& p, bool first, cudaStream_t s) {
+    if (p.split_mode == 0) return launch_attention_split<0>(p, first, s);
+    if (p.split_mode == 1) return launch_attention_split<1>(p, first, s);
+    return launch_attention_split<2>(p, first, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -293,6 +362,7 @@ __device__ bool pred_accepts(const BeamArgs& a, const PosMeta& m, const DevPred&
     }
 }
 
+
 // Candidate order: higher score first, exact ties to the smaller packed
 // prefix key (= lexicographically smaller prefix; Candidate::operator<,
 // decoding.cpp:21-24).
@@ -301,186 +371,272 @@ __device__ __forceinline__ bool better(double s1, unsigned long long k1, double 
     return s1 > s2 || (s1 == s2 && k1 < k2);
 }
 
-__global__ void __launch_bounds__(256) beam_step(BeamArgs a, PosMeta m) {
+// Reduce-scatter of VP per-lane partial sums over the warp: after it, the
+// lane src_lane<VP>(v) holds the full 32-lane sum for token v.  Costs
+// VP-1 + (5 - log2 VP) shuffles instead of 5*VP for independent reductions.
+template <int VP>
+struct RS {
+    static constexpr int L = VP == 32 ? 5 : VP == 16 ? 4 : VP == 8 ? 3 : 2;
+};
+template <int VP>
+__device__ __forceinline__ float reduce_scatter(float (&p)[VP], int lane) {
+    constexpr int L = RS<VP>::L;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        const int mask = 16 >> l;
+        const int half = VP >> (l + 1);
+        const bool hi = (lane & mask) != 0;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+            const float keep = hi ? p[half + j] : p[j];
+            const float send = hi ? p[j] : p[half + j];
+            p[j] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+        }
+    }
+    float v = p[0];
+#pragma unroll
+    for (int l = L; l < 5; ++l) v += __shfl_xor_sync(0xffffffffu, v, 16 >> l);
+    return v;
+}
+template <int VP>
+__device__ __forceinline__ int src_lane(int v) {
+    constexpr int L = RS<VP>::L;
+    int lane = 0;
+#pragma unroll
+    for (int l = 0; l < L; ++l) lane |= ((v >> (L - 1 - l)) & 1) << (4 - l);
+    return lane;
+}
+
+template <int VP>
+__global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int WS = VP == 4 ? 12 : VP + 4;  // padded W row: conflict-free 128-bit loads
     const int V = m.vsize[a.pos];
-    const int Vs = V | 1;  // odd row stride: conflict-free lane-strided head reads
     float* Wsh = reinterpret_cast<float*>(smem);
-    const int nW = a.NS * Vs;
-    for (int i = threadIdx.x; i < a.NS * V; i += blockDim.x) {
-        const int row = i / V, v = i - row * V;
-        Wsh[row * Vs + v] = a.Wh[i];
+    for (int i = threadIdx.x; i < a.NS * VP; i += blockDim.x) {
+        const int row = i / VP, v = i - row * VP;
+        Wsh[row * WS + v] = v < V ? a.Wh[row * V + v] : 0.0f;
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    const int b = blockIdx.x * nwarps + warp;
-    if (b >= a.B) return;
-    unsigned char* cbase = smem + ((nW * 4 + 15) & ~15) + (size_t)warp * a.cands_per_warp * 28;
+    unsigned char* cbase = smem + ((size_t)(a.NS * WS * 4 + 15) & ~(size_t)15) + (size_t)warp * a.cands_per_warp * 28;
     double* c_score = reinterpret_cast<double*>(cbase);
     double* c_lp = c_score + a.cands_per_warp;
     unsigned long long* c_key = reinterpret_cast<unsigned long long*>(c_lp + a.cands_per_warp);
     int* c_meta = reinterpret_cast<int*>(c_key + a.cands_per_warp);
-
     const int nc = a.H_cur * V;
-    const long long* desc_b = a.desc ? a.desc + (long long)b * kTin : nullptr;
     const int T = m.T;
-
-    auto write_dead_next = [&](int from) {
-        if (a.final_step) return;
-        for (int i = from + lane; i < a.H_next; i += 32) {
-            const long long s = (long long)b * a.H_next + i;
-            a.live_next[s] = 0;
-            a.lp_next[s] = -INFINITY;
-            a.key_next[s] = 0ull;
-            a.parent_next[s] = b * a.H_cur;
-            a.slot_next[s] = m.fb_offset[a.pos];
-        }
-    };
-
-    if (a.status[b] != 0) {  // exhausted earlier: nothing left to extend
-        write_dead_next(0);
-        return;
-    }
     const float bias = lane < V ? a.bh[lane] : 0.0f;
-    int n_alive = 0;
-    int last_live = -1;
-    for (int j = 0; j < a.H_cur; ++j) {
-        const long long r = (long long)b * a.H_cur + j;
-        const bool live = a.live_cur[r] != 0;
-        if (!live) {
-            for (int v = lane; v < V; v += 32) c_meta[j * V + v] = -1;
+    const int my_src = src_lane<VP>(lane < VP ? lane : 0);
+
+    for (int b = blockIdx.x * nwarps + warp; b < a.B; b += gridDim.x * nwarps) {
+        const long long* desc_b = a.desc ? a.desc + (long long)b * kTin : nullptr;
+        auto write_dead_next = [&](int from) {
+            if (a.final_step) return;
+            for (int i = from + lane; i < a.H_next; i += 32) {
+                const long long sl = (long long)b * a.H_next + i;
+                a.live_next[sl] = 0;
+                a.lp_next[sl] = -INFINITY;
+                a.key_next[sl] = 0ull;
+                a.parent_next[sl] = b * a.H_cur;
+                a.slot_next[sl] = m.fb_offset[a.pos];
+            }
+        };
+        if (a.status[b] != 0) {  // exhausted earlier: nothing left to extend
+            write_dead_next(0);
             continue;
         }
-        last_live = j;
-        // head: logits[v] = b[v] + sum_i h[i] W[i][v]   (models.cpp:490-491)
-        float part[kMaxV];
-#pragma unroll
-        for (int v = 0; v < kMaxV; ++v) part[v] = 0.0f;
-        const float* hr = a.h + r * a.NS;
-        for (int i = lane; i < a.NS; i += 32) {
-            const float hv = hr[i];
-            const float* wrow = Wsh + i * Vs;
-#pragma unroll
-            for (int v = 0; v < kMaxV; ++v)
-                if (v < V) part[v] = fmaf(hv, wrow[v], part[v]);
-        }
-        float logit = 0.0f;
-#pragma unroll
-        for (int v = 0; v < kMaxV; ++v) {
-            if (v < V) {
-                const float t = warp_sum_f(part[v]);
-                if (lane == v) logit = t;
+        int n_alive = 0;
+        int last_live = -1;
+        for (int j0 = 0; j0 < a.H_cur; j0 += 2) {
+            const long long r0 = (long long)b * a.H_cur + j0;
+            const bool two = j0 + 1 < a.H_cur;
+            const bool live0 = a.live_cur[r0] != 0;
+            const bool live1 = two && a.live_cur[r0 + 1] != 0;
+            if (!live0 && !live1) {
+                for (int c = lane; c < (two ? 2 : 1) * V; c += 32) c_meta[j0 * V + c] = -1;
+                continue;
             }
-        }
-        // softmax in fp64 then log(max(p, 1e-300)) (nn.cpp:215-226, decoding.cpp:57-58)
-        const double l = lane < V ? (double)(logit + bias) : -INFINITY;
-        const double mx = warp_max_d(l);
-        const double ex = lane < V ? exp(l - mx) : 0.0;
-        const double sum = warp_sum_d(ex);
-        const double pr = ex / sum;
-        const double clp = a.lp_cur[r] + log(fmax(pr, 1e-300));
-        const unsigned long long key = a.key_cur[r] | ((unsigned long long)lane << m.shift[a.pos]);
-        int rej = -1;
-        if (lane < V) {
-            for (int q = 0; q < a.n_preds; ++q) {
-                const DevPred pq = a.preds[q];
-                if (pq.full && !a.final_step) continue;
-                if (!pred_accepts(a, m, pq, key, a.pos, desc_b)) {
-                    rej = q;
-                    break;
+            // head logits for rows j0, j0+1: logits[v] = b[v] + sum_i h[i] W[i][v]  (models.cpp:490-491)
+            float p0[VP], p1[VP];
+#pragma unroll
+            for (int v = 0; v < VP; ++v) {
+                p0[v] = 0.0f;
+                p1[v] = 0.0f;
+            }
+            const float* h0 = a.h + r0 * a.NS;
+            const float* h1 = h0 + a.NS;
+            for (int i = lane; i < a.NS; i += 32) {
+                const float x0 = live0 ? h0[i] : 0.0f;
+                const float x1 = live1 ? h1[i] : 0.0f;
+                const float4* w4 = reinterpret_cast<const float4*>(Wsh + i * WS);
+#pragma unroll
+                for (int q = 0; q < VP / 4; ++q) {
+                    const float4 w = w4[q];
+                    p0[4 * q + 0] = fmaf(x0, w.x, p0[4 * q + 0]);
+                    p0[4 * q + 1] = fmaf(x0, w.y, p0[4 * q + 1]);
+                    p0[4 * q + 2] = fmaf(x0, w.z, p0[4 * q + 2]);
+                    p0[4 * q + 3] = fmaf(x0, w.w, p0[4 * q + 3]);
+                    p1[4 * q + 0] = fmaf(x1, w.x, p1[4 * q + 0]);
+                    p1[4 * q + 1] = fmaf(x1, w.y, p1[4 * q + 1]);
+                    p1[4 * q + 2] = fmaf(x1, w.z, p1[4 * q + 2]);
+                    p1[4 * q + 3] = fmaf(x1, w.w, p1[4 * q + 3]);
                 }
             }
-            const int c = j * V + lane;
-            c_score[c] = a.greedy ? pr : clp;
-            c_lp[c] = clp;
-            c_key[c] = key;
-            c_meta[c] = rej < 0 ? ((j << 8) | lane) : -2 - rej;
-        }
-        n_alive += __popc(__ballot_sync(0xffffffffu, lane < V && rej < 0));
-    }
-    __syncwarp();
-    if (n_alive == 0) {
-        // BeamExhaustedError(last_rejecting, pos): every child was rejected, so the
-        // last rejecting predicate is that of the last child (last live hyp, last token).
-        if (lane == 0) {
-            int fp = -1;
-            if (last_live >= 0) {
-                const int mm = c_meta[last_live * V + V - 1];
-                fp = mm <= -2 ? -2 - mm : -1;
-            }
-            a.status[b] = 1;
-            a.fail_pred[b] = fp;
-            a.fail_step[b] = a.pos;
-            a.out_count[b] = 0;
-            if (a.out_status) a.out_status[b] = 1;
-            if (a.out_fail_pred) a.out_fail_pred[b] = fp;
-            if (a.out_fail_step) a.out_fail_step[b] = a.pos;
-        }
-        for (int i = lane; i < a.k * T; i += 32) a.out_tok[(long long)b * a.k * T + i] = -1;
-        for (int i = lane; i < a.k; i += 32) a.out_lp[(long long)b * a.k + i] = -INFINITY;
-        write_dead_next(0);
-        return;
-    }
-    const int ksel = n_alive < a.k ? n_alive : a.k;
-    for (int i = 0; i < ksel; ++i) {
-        double bs = -INFINITY;
-        unsigned long long bk = ~0ull;
-        int bc = -1;
-        for (int c = lane; c < nc; c += 32) {
-            if (c_meta[c] < 0) continue;
-            if (bc < 0 || better(c_score[c], c_key[c], bs, bk)) {
-                bs = c_score[c];
-                bk = c_key[c];
-                bc = c;
-            }
-        }
+            const float s0 = reduce_scatter<VP>(p0, lane);
+            const float s1 = reduce_scatter<VP>(p1, lane);
+            const float lg[2] = {__shfl_sync(0xffffffffu, s0, my_src), __shfl_sync(0xffffffffu, s1, my_src)};
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double os = __shfl_xor_sync(0xffffffffu, bs, o);
-            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-            if (oc >= 0 && (bc < 0 || better(os, ok, bs, bk))) {
-                bs = os;
-                bk = ok;
-                bc = oc;
+            for (int jj = 0; jj < 2; ++jj) {
+                const int j = j0 + jj;
+                if (j >= a.H_cur) break;
+                const bool live = jj == 0 ? live0 : live1;
+                if (!live) {
+                    for (int v = lane; v < V; v += 32) c_meta[j * V + v] = -1;
+                    continue;
+                }
+                last_live = j;
+                const long long r = r0 + jj;
+                // softmax in fp64, then log(max(p, 1e-300)) (nn.cpp:215-226, decoding.cpp:57-58)
+                const double l = lane < V ? (double)(lg[jj] + bias) : -INFINITY;
+                const double mx = warp_max_d(l);
+                const double ex = lane < V ? exp(l - mx) : 0.0;
+                const double sum = warp_sum_d(ex);
+                const double pr = ex / sum;
+                const double clp = a.lp_cur[r] + log(fmax(pr, 1e-300));
+                const unsigned long long key = a.key_cur[r] | ((unsigned long long)lane << m.shift[a.pos]);
+                int rej = -1;
+                if (lane < V) {
+                    for (int q = 0; q < a.n_preds; ++q) {
+                        const DevPred pq = a.preds[q];
+                        if (pq.full && !a.final_step) continue;
+                        if (!pred_accepts(a, m, pq, key, a.pos, desc_b)) {
+                            rej = q;
+                            break;
+                        }
+                    }
+                    const int c = j * V + lane;
+                    c_score[c] = a.greedy ? pr : clp;
+                    c_lp[c] = clp;
+                    c_key[c] = key;
+                    c_meta[c] = rej < 0 ? ((j << 8) | lane) : -2 - rej;
+                }
+                n_alive += __popc(__ballot_sync(0xffffffffu, lane < V && rej < 0));
             }
         }
-        if (lane == 0) {
-            const int meta = c_meta[bc];
-            const int j = meta >> 8, v = meta & 255;
-            const double clp = c_lp[bc];
-            if (a.final_step) {
-                const long long o = (long long)b * a.k + i;
-                a.out_lp[o] = clp;
-                for (int t = 0; t < T; ++t) a.out_tok[o * T + t] = key_token(bk, m, t);
-            } else {
-                const long long s = (long long)b * a.H_next + i;
-                a.live_next[s] = 1;
-                a.lp_next[s] = clp;
-                a.key_next[s] = bk;
-                a.parent_next[s] = b * a.H_cur + j;
-                a.slot_next[s] = m.fb_offset[a.pos] + v;
+        __syncwarp();
+        if (n_alive == 0) {
+            // BeamExhaustedError(last_rejecting, pos): every child was rejected, so the
+            // last rejecting predicate is that of the last child (last live hyp, last token).
+            if (lane == 0) {
+                int fp = -1;
+                if (last_live >= 0) {
+                    const int mm = c_meta[last_live * V + V - 1];
+                    fp = mm <= -2 ? -2 - mm : -1;
+                }
+                a.status[b] = 1;
+                a.fail_pred[b] = fp;
+                a.fail_step[b] = a.pos;
+                a.out_count[b] = 0;
+                if (a.out_status) a.out_status[b] = 1;
+                if (a.out_fail_pred) a.out_fail_pred[b] = fp;
+                if (a.out_fail_step) a.out_fail_step[b] = a.pos;
             }
-            c_meta[bc] = -1;
+            for (int i = lane; i < a.k * T; i += 32) a.out_tok[(long long)b * a.k * T + i] = -1;
+            for (int i = lane; i < a.k; i += 32) a.out_lp[(long long)b * a.k + i] = -INFINITY;
+            write_dead_next(0);
+            __syncwarp();
+            continue;
+        }
+        const int ksel = n_alive < a.k ? n_alive : a.k;
+        for (int i = 0; i < ksel; ++i) {
+            double bs = -INFINITY;
+            unsigned long long bk = ~0ull;
+            int bc = -1;
+            for (int c = lane; c < nc; c += 32) {
+                if (c_meta[c] < 0) continue;
+                if (bc < 0 || better(c_score[c], c_key[c], bs, bk)) {
+                    bs = c_score[c];
+                    bk = c_key[c];
+                    bc = c;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+                const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                if (oc >= 0 && (bc < 0 || better(os, ok, bs, bk))) {
+                    bs = os;
+                    bk = ok;
+                    bc = oc;
+                }
+            }
+            if (lane == 0) {
+                const int meta = c_meta[bc];
+                const int j = meta >> 8, v = meta & 255;
+                const double clp = c_lp[bc];
+                if (a.final_step) {
+                    const long long o = (long long)b * a.k + i;
+                    a.out_lp[o] = clp;
+                    for (int t = 0; t < T; ++t) a.out_tok[o * T + t] = key_token(bk, m, t);
+                } else {
+                    const long long sl = (long long)b * a.H_next + i;
+                    a.live_next[sl] = 1;
+                    a.lp_next[sl] = clp;
+                    a.key_next[sl] = bk;
+                    a.parent_next[sl] = b * a.H_cur + j;
+                    a.slot_next[sl] = m.fb_offset[a.pos] + v;
+                }
+                c_meta[bc] = -1;
+            }
+            __syncwarp();
+        }
+        if (a.final_step) {
+            for (int i = ksel + lane; i < a.k; i += 32) {
+                const long long o = (long long)b * a.k + i;
+                a.out_lp[o] = -INFINITY;
+                for (int t = 0; t < T; ++t) a.out_tok[o * T + t] = -1;
+            }
+            if (lane == 0) {
+                a.out_count[b] = ksel;
+                if (a.out_status) a.out_status[b] = 0;
+                if (a.out_fail_pred) a.out_fail_pred[b] = -1;
+                if (a.out_fail_step) a.out_fail_step[b] = -1;
+            }
+        } else {
+            write_dead_next(ksel);
         }
         __syncwarp();
     }
-    if (a.final_step) {
-        for (int i = ksel + lane; i < a.k; i += 32) {
-            const long long o = (long long)b * a.k + i;
-            a.out_lp[o] = -INFINITY;
-            for (int t = 0; t < T; ++t) a.out_tok[o * T + t] = -1;
-        }
-        if (lane == 0) {
-            a.out_count[b] = ksel;
-            if (a.out_status) a.out_status[b] = 0;
-            if (a.out_fail_pred) a.out_fail_pred[b] = -1;
-            if (a.out_fail_step) a.out_fail_step[b] = -1;
-        }
-    } else {
-        write_dead_next(ksel);
+}
+
+size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp) {
+    const int VP = V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
+    const int WS = VP == 4 ? 12 : VP + 4;
+    return (((size_t)NS * WS * 4 + 15) & ~(size_t)15) + (size_t)warps * cands_per_warp * 28;
+}
+
+bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
+    const int V = m.vsize[a.pos];
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(beam_step_t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
     }
+    if (V <= 4)
+        beam_step_t<4><<<grid, warps * 32, smem, s>>>(a, m);
+    else if (V <= 8)
+        beam_step_t<8><<<grid, warps * 32, smem, s>>>(a, m);
+    else if (V <= 16)
+        beam_step_t<16><<<grid, warps * 32, smem, s>>>(a, m);
+    else
+        beam_step_t<32><<<grid, warps * 32, smem, s>>>(a, m);
+    return cudaGetLastError() == cudaSuccess;
 }
 
 }  // namespace ksb
