@@ -223,8 +223,10 @@ def run_b200(args):
     path = model_path()
     eng = _cabi.Engine(path, local, args.precision)
     B = args.configs
-    desc_all = descriptors(B * world, KERNEL)
-    desc = desc_all[rank * B:(rank + 1) * B]
+    from paper_2404_10162_b200.parallel import weak_shard
+
+    lo, hi = weak_shard(B, rank)
+    desc = descriptors(B * world, KERNEL)[lo:hi]
     tok = eng.encode(desc)
     with open(path, "rb") as f:
         head = f.read(8192).split(b"\n\n")[0].decode().split("\n")
