@@ -139,8 +139,11 @@ enum {
                              with separate multiply and add; accept iff cost <= budget */
     KS_PRED_PRODUCT = 3,  /* scale * prod(values of assigned listed params) <= limit
                              (workgroup size, LDS bytes); no reference counterpart */
-    KS_PRED_DIVIDES = 4   /* each assigned listed param value v > 0 divides the descriptor
+    KS_PRED_DIVIDES = 4,  /* each assigned listed param value v > 0 divides the descriptor
                              field term_field[i] (tile divisibility); no reference counterpart */
+    KS_PRED_HOST = 5      /* opaque host predicate (a reference std::function / Python callable):
+                             evaluated by the ks_host_pred_fn hook between positions, in
+                             registration order with the typed ones */
 };
 
 typedef struct {
@@ -170,6 +173,29 @@ ks_status ks_beam_search_batch(ks_engine* eng, const int32_t* tok, const int64_t
                                int32_t n_preds, int32_t* out_tok, double* out_lp,
                                int32_t* out_count, int32_t* out_status,
                                int32_t* out_fail_pred, int32_t* out_fail_step);
+
+/* Host hook for KS_PRED_HOST entries.  Called once per position (before that
+ * position's selection) with the n_rows live hypotheses of the call: their
+ * config index (0..B-1) and prefix tokens (n_rows x position, row-major).  For
+ * every (row, token < vocab) it writes the registration index (into the
+ * ks_pred array) of the first KS_PRED_HOST predicate that rejects the child,
+ * or -1.  The device combines it with the typed predicates so the first
+ * rejecting predicate in registration order wins (decoding.cpp:69-76).
+ * The hook runs on the calling thread while the GPU computes the position's
+ * attention and gate GEMM.  Return nonzero to abort the call. */
+typedef int32_t (*ks_host_pred_fn)(void* user, int32_t position, int32_t final_step,
+                                   int64_t n_rows, const int32_t* row_config,
+                                   const int32_t* row_prefix, int32_t vocab,
+                                   int32_t* out_first_reject);
+
+/* ks_beam_search_batch with a host predicate hook (required when any
+ * predicate has kind KS_PRED_HOST). */
+ks_status ks_beam_search_batch_hooked(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                                      int64_t B, int32_t beam_width, const ks_pred* preds,
+                                      int32_t n_preds, ks_host_pred_fn hook, void* user,
+                                      int32_t* out_tok, double* out_lp, int32_t* out_count,
+                                      int32_t* out_status, int32_t* out_fail_pred,
+                                      int32_t* out_fail_step);
 
 /* greedy_decode: out_tok B x T. */
 ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok);

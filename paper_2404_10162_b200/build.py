@@ -65,6 +65,31 @@ def build_engine(verbose: bool = False, force: bool = False) -> str:
     return out
 
 
+def build_host(verbose: bool = False, force: bool = False) -> str:
+    """libkernelseer_b200.so (reference-compatible C++ API) and the Python
+    module _kernelseer_b200 (reference binding names), both over libks_b200.so."""
+    import sysconfig
+
+    import pybind11
+
+    host = os.path.join(CSRC, "host")
+    api_src = os.path.join(host, "kernelseer_api.cpp")
+    mod_src = os.path.join(host, "pymodule.cpp")
+    hdrs = [os.path.join(ROOT, "include", "kernelseer_b200.hpp"), os.path.join(ROOT, "include", "ks_b200.h")]
+    engine = os.path.join(PKG, "libks_b200.so")
+    api = os.path.join(PKG, "libkernelseer_b200.so")
+    mod = os.path.join(PKG, "_kernelseer_b200" + sysconfig.get_config_var("EXT_SUFFIX"))
+    common = ["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", f"-I{ROOT}/include"]
+    rpath = "-Wl,-rpath,$ORIGIN"
+    if force or _newer([api_src, engine] + hdrs, api):
+        _run(common + ["-shared", "-o", api, api_src, f"-L{PKG}", "-l:libks_b200.so", rpath])
+    if force or _newer([mod_src, api] + hdrs, mod):
+        _run(common + ["-shared", f"-I{sysconfig.get_paths()['include']}", f"-I{pybind11.get_include()}",
+                       "-o", mod, mod_src, f"-L{PKG}", "-l:libkernelseer_b200.so", "-l:libks_b200.so", rpath])
+    return mod
+
+
 if __name__ == "__main__":
     import sys
     print(build_engine(verbose=True, force="--force" in sys.argv))
+    print(build_host(verbose=True, force="--force" in sys.argv))

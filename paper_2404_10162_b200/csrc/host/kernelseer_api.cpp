@@ -1,0 +1,817 @@
+// kernelseer_api.cpp -- the reference-compatible C++ host layer
+// (include/kernelseer_b200.hpp) over the engine's C-ABI (include/ks_b200.h).
+//
+// Host-side work here is O(batch x positions) bookkeeping: descriptor
+// tokenisation, predicate resolution, result unpacking, metrics.  All model
+// arithmetic and the beam search run on the GPU.
+#include "kernelseer_b200.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "ks_b200.h"
+
+namespace kernelseer {
+
+namespace {
+
+[[noreturn]] void throw_status(ks_status st) {
+    const std::string msg = ks_last_error();
+    switch (st) {
+        case KS_ERR_SHAPE: throw ShapeError(msg);
+        case KS_ERR_PARAMETER: throw ParameterError(msg);
+        case KS_ERR_INDEX: throw IndexError(msg);
+        case KS_ERR_STATE: throw StateError(msg);
+        case KS_ERR_VALIDATION: throw ValidationError(msg, ks_last_error_field());
+        case KS_ERR_CHECKPOINT: {
+            static const CheckpointError::Kind kinds[] = {
+                CheckpointError::Kind::version, CheckpointError::Kind::truncated,
+                CheckpointError::Kind::shape, CheckpointError::Kind::malformed,
+                CheckpointError::Kind::io};
+            const int k = ks_checkpoint_error_kind();
+            throw CheckpointError(k >= 0 && k < 5 ? kinds[k] : CheckpointError::Kind::malformed, msg);
+        }
+        case KS_ERR_BEAM_EXHAUSTED: throw BeamExhaustedError(msg, "", -1);
+        default: throw Error(msg);
+    }
+}
+
+void check(ks_status st) {
+    if (st != KS_OK) throw_status(st);
+}
+
+std::string join(const std::vector<std::int64_t>& v) {
+    std::string s;
+    for (std::size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+    return s;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ problems
+std::string precision_label(Precision p) { return p == Precision::full ? "fp32" : "fp16"; }
+
+Precision precision_from_label(const std::string& s) {
+    if (s == "fp32" || s == "full") return Precision::full;
+    if (s == "fp16" || s == "half") return Precision::half;
+    throw ValidationError("unknown precision label '" + s + "' (expected fp32 or fp16)", "precision");
+}
+
+std::int64_t descriptor_field(const ProblemDescriptor& d, int f) {
+    const std::int64_t v[7] = {d.n, d.c, d.h_i, d.w_i, d.k, d.y, d.x};
+    if (f < 0 || f >= 7) throw IndexError("descriptor field index " + std::to_string(f));
+    return v[f];
+}
+
+void set_descriptor_field(ProblemDescriptor& d, int f, std::int64_t value) {
+    std::int64_t* v[7] = {&d.n, &d.c, &d.h_i, &d.w_i, &d.k, &d.y, &d.x};
+    if (f < 0 || f >= 7) throw IndexError("descriptor field index " + std::to_string(f));
+    *v[f] = value;
+}
+
+void ProblemDescriptor::check() const {
+    for (int f = 0; f < kNumInputFields; ++f) {
+        const std::int64_t v = descriptor_field(*this, f);
+        if (v < 1)
+            throw ValidationError(std::string("descriptor field ") + kInputFieldNames[f] +
+                                      " must be >= 1, got " + std::to_string(v),
+                                  kInputFieldNames[f]);
+    }
+}
+
+// ------------------------------------------------------------------ kernel specs
+int KernelSpec::param_index(std::string_view n) const {
+    for (std::size_t i = 0; i < params.size(); ++i)
+        if (params[i].name == n) return static_cast<int>(i);
+    return -1;
+}
+
+void KernelSpec::check() const {
+    if (params.empty()) throw ValidationError("kernel spec has no parameters", name);
+    for (std::size_t i = 0; i < params.size(); ++i) {
+        if (params[i].values.empty())
+            throw ValidationError("parameter " + params[i].name + " has an empty value set", params[i].name);
+        for (std::size_t j = 0; j < i; ++j)
+            if (params[i].name == params[j].name)
+                throw ValidationError("duplicate parameter name " + params[i].name, params[i].name);
+    }
+}
+
+namespace {
+std::vector<std::int64_t> span_of(std::int64_t lo, std::int64_t hi) {
+    std::vector<std::int64_t> v;
+    for (std::int64_t x = lo; x <= hi; ++x) v.push_back(x);
+    return v;
+}
+std::vector<std::int64_t> pow2_of(int lo, int hi) {
+    std::vector<std::int64_t> v;
+    for (int e = lo; e <= hi; ++e) v.push_back(std::int64_t{1} << e);
+    return v;
+}
+}  // namespace
+
+// Table I of the paper (proj/tests/fixtures/table1.txt).
+const std::vector<KernelSpec>& builtin_specs() {
+    static const std::vector<KernelSpec> specs = [] {
+        std::vector<KernelSpec> s;
+        s.push_back({"ConvAsm1x1U",
+                     {{"read_size", span_of(1, 4)}, {"k_mult", {1, 4, 8, 16, 32}},
+                      {"chunks_per_wave", span_of(1, 16)}, {"chunk_size", pow2_of(0, 6)},
+                      {"n_mult", span_of(1, 8)}, {"c_mult", pow2_of(0, 5)},
+                      {"waves_c_in_group", span_of(1, 8)}, {"waves_k_in_group", pow2_of(0, 3)}}});
+        s.push_back({"ConvOclDirectFwd1x1",
+                     {{"grp_tile1", pow2_of(0, 4)}, {"grp_tile0", pow2_of(0, 8)}, {"in_tile1", pow2_of(0, 5)},
+                      {"in_tile_0", pow2_of(0, 5)}, {"out_pix_tile1", {0, 1}}, {"out_pix_tile0", {0, 1, 2, 4}},
+                      {"n_out_pix_tiles", pow2_of(0, 6)}, {"n_in_data_tiles", pow2_of(0, 11)},
+                      {"n_stacks", {0, 1}}}});
+        s.push_back({"ConvAsmBwdWrW1x1",
+                     {{"read_size", span_of(1, 4)}, {"c_per_gpr", pow2_of(0, 4)}, {"c_mult", pow2_of(0, 4)},
+                      {"k_per_gpr", pow2_of(0, 4)}, {"k_mult", pow2_of(0, 4)}, {"n_per_gpr", pow2_of(0, 4)},
+                      {"n_part_cnt", span_of(1, 8)}, {"chunk_size", pow2_of(0, 4)}, {"short_store", {0, 1}},
+                      {"data_prefetch", span_of(0, 4)}}});
+        s.push_back({"ConvAsmBwdWrW3x3",
+                     {{"limit_wave_cnt", span_of(0, 9)}, {"reverse_inout", {0, 1}}, {"chunk_size", {8, 16}},
+                      {"k_per_wave", pow2_of(0, 3)}, {"pipe_lines_depth", span_of(1, 16)},
+                      {"n_per_group", span_of(1, 8)}}});
+        return s;
+    }();
+    return specs;
+}
+
+const KernelSpec& builtin_spec(std::string_view name) {
+    std::string known;
+    for (const KernelSpec& s : builtin_specs()) {
+        if (s.name == name) return s;
+        known += (known.empty() ? "" : ", ") + s.name;
+    }
+    throw ValidationError("unknown kernel '" + std::string(name) + "' (built-in: " + known + ")", "kernel");
+}
+
+std::uint64_t search_space_size(const KernelSpec& spec) {
+    std::uint64_t n = 1;
+    for (const auto& p : spec.params) n *= p.values.size();
+    return n;
+}
+
+// ------------------------------------------------------------------ predicates
+ConstraintPredicate membership_predicate(const KernelSpec& spec) {
+    auto prog = std::make_shared<PredicateProgram>();
+    prog->kind = PredicateProgram::Kind::mask;
+    ConstraintPredicate p;
+    p.name = "membership:" + spec.name;
+    for (const auto& q : spec.params) {
+        p.reads.push_back(q.name);
+        prog->legal[q.name] = q.values;
+    }
+    p.program = prog;
+    p.fn = [spec](const ProblemDescriptor&, const ParamMap& assigned) {
+        for (const auto& [name, value] : assigned) {
+            const int i = spec.param_index(name);
+            if (i < 0)
+                throw ValidationError("membership predicate: unknown parameter '" + name + "' for kernel " +
+                                          spec.name,
+                                      name);
+            const auto& vals = spec.params[static_cast<std::size_t>(i)].values;
+            if (std::find(vals.begin(), vals.end(), value) == vals.end()) return false;
+        }
+        return true;
+    };
+    return p;
+}
+
+ConstraintPredicate resource_budget_predicate(std::map<std::string, double> weights, double budget,
+                                              std::string name) {
+    for (const auto& [n, w] : weights)
+        if (w < 0.0)
+            throw ParameterError("resource budget weight for " + n + " must be nonnegative, got " +
+                                 std::to_string(w));
+    if (budget < 0.0) throw ParameterError("resource budget must be nonnegative");
+    auto prog = std::make_shared<PredicateProgram>();
+    prog->kind = PredicateProgram::Kind::budget;
+    prog->weights = weights;
+    prog->budget = budget;
+    ConstraintPredicate p;
+    p.name = std::move(name);
+    for (const auto& [n, w] : weights) p.reads.push_back(n);
+    p.program = prog;
+    p.fn = [weights, budget](const ProblemDescriptor&, const ParamMap& assigned) {
+        double cost = 0.0;  // alphabetical (std::map) order, separate multiply and add
+        for (const auto& [n, w] : weights) {
+            auto it = assigned.find(n);
+            if (it == assigned.end()) continue;
+            const volatile double prod = w * static_cast<double>(it->second);
+            cost = cost + prod;
+        }
+        return cost <= budget;
+    };
+    return p;
+}
+
+ConstraintPredicate product_limit_predicate(std::vector<std::string> params, std::int64_t scale,
+                                            std::int64_t limit, std::string name) {
+    auto prog = std::make_shared<PredicateProgram>();
+    prog->kind = PredicateProgram::Kind::product;
+    prog->factors = params;
+    prog->scale = scale;
+    prog->limit = limit;
+    ConstraintPredicate p;
+    p.name = std::move(name);
+    p.reads = params;
+    p.program = prog;
+    p.fn = [params, scale, limit](const ProblemDescriptor&, const ParamMap& assigned) {
+        const __int128 cap = (__int128)1 << 100;
+        __int128 prod = scale;
+        for (const auto& n : params) {
+            auto it = assigned.find(n);
+            if (it == assigned.end()) continue;
+            prod *= (__int128)it->second;
+            prod = std::clamp(prod, -cap, cap);
+        }
+        return prod <= (__int128)limit;
+    };
+    return p;
+}
+
+ConstraintPredicate divisibility_predicate(std::vector<std::pair<std::string, int>> param_field,
+                                           std::string name) {
+    for (const auto& pf : param_field)
+        if (pf.second < 0 || pf.second > 6) throw IndexError("descriptor field index " + std::to_string(pf.second));
+    auto prog = std::make_shared<PredicateProgram>();
+    prog->kind = PredicateProgram::Kind::divides;
+    prog->divides = param_field;
+    ConstraintPredicate p;
+    p.name = std::move(name);
+    for (const auto& pf : param_field) p.reads.push_back(pf.first);
+    p.program = prog;
+    p.fn = [param_field](const ProblemDescriptor& d, const ParamMap& assigned) {
+        for (const auto& [n, f] : param_field) {
+            auto it = assigned.find(n);
+            if (it == assigned.end()) continue;
+            if (it->second <= 0 || descriptor_field(d, f) % it->second != 0) return false;
+        }
+        return true;
+    };
+    return p;
+}
+
+std::optional<Violation> validate_sequence(const KernelSpec& spec, const ProblemDescriptor& d,
+                                           const ParamMap& params,
+                                           std::span<const ConstraintPredicate> predicates) {
+    if (static_cast<int>(params.size()) != spec.num_params())
+        throw ParameterError("validate_sequence: map has " + std::to_string(params.size()) + " entries, kernel " +
+                             spec.name + " has " + std::to_string(spec.num_params()) + " parameters");
+    for (const auto& p : spec.params)
+        if (!params.contains(p.name)) throw ParameterError("validate_sequence: map missing parameter " + p.name);
+    for (const auto& pred : predicates)
+        if (!pred.evaluate(d, params)) return Violation{pred.name, pred.reads};
+    return std::nullopt;
+}
+
+// ------------------------------------------------------------------ vocabulary
+int FieldVocab::id_of(std::int64_t v) const {
+    for (std::size_t i = 0; i < values.size(); ++i)
+        if (values[i] == v) return static_cast<int>(i);
+    return -1;
+}
+
+std::int64_t FieldVocab::value_of(int id) const {
+    if (id < 0 || id >= size())
+        throw IndexError("token id " + std::to_string(id) + " out of range for " + name + " (size " +
+                         std::to_string(size()) + ")");
+    return values[static_cast<std::size_t>(id)];
+}
+
+std::int64_t FieldVocab::nearest(std::int64_t v) const {
+    std::int64_t best = values.front();
+    for (std::int64_t x : values) {
+        const std::int64_t dx = x > v ? x - v : v - x, db = best > v ? best - v : v - best;
+        if (dx < db || (dx == db && x < best)) best = x;
+    }
+    return best;
+}
+
+Vocabulary::Vocabulary(std::vector<FieldVocab> in, std::vector<FieldVocab> out)
+    : in_(std::move(in)), out_(std::move(out)) {}
+
+TokenSequence encode_problem(const ProblemDescriptor& d, const Vocabulary& v, bool allow_nearest) {
+    d.check();
+    TokenSequence t;
+    t.role = TokenSequence::Role::input;
+    for (int f = 0; f < kNumInputFields; ++f) {
+        const FieldVocab& fv = v.input_field(f);
+        std::int64_t value = descriptor_field(d, f);
+        int id = fv.id_of(value);
+        if (id < 0 && allow_nearest) id = fv.id_of(fv.nearest(value));
+        if (id < 0)
+            throw ValidationError("value " + std::to_string(value) + " of field " + fv.name +
+                                      " is not in the vocabulary (nearest known: " +
+                                      std::to_string(fv.nearest(value)) + ")",
+                                  fv.name);
+        t.ids.push_back(id);
+    }
+    return t;
+}
+
+ProblemDescriptor decode_problem(const TokenSequence& t, const Vocabulary& v, Precision precision) {
+    if (t.length() != kNumInputFields)
+        throw ParameterError("decode_problem: expected 7 tokens, got " + std::to_string(t.length()));
+    ProblemDescriptor d;
+    d.precision = precision;
+    for (int f = 0; f < kNumInputFields; ++f) set_descriptor_field(d, f, v.input_field(f).value_of(t.ids[f]));
+    return d;
+}
+
+ParamMap decode_params(const TokenSequence& t, const KernelSpec& spec, const Vocabulary& v) {
+    if (t.length() != spec.num_params())
+        throw ParameterError("decode_params: sequence length " + std::to_string(t.length()) + " vs " +
+                             std::to_string(spec.num_params()) + " parameters of " + spec.name);
+    ParamMap out;
+    for (int i = 0; i < spec.num_params(); ++i)
+        out[spec.params[static_cast<std::size_t>(i)].name] = v.output_param(i).value_of(t.ids[static_cast<std::size_t>(i)]);
+    return out;
+}
+
+TokenSequence encode_params(const ParamMap& params, const KernelSpec& spec, const Vocabulary& v) {
+    if (static_cast<int>(params.size()) != spec.num_params())
+        throw ParameterError("encode_params: map size " + std::to_string(params.size()) + " vs " +
+                             std::to_string(spec.num_params()) + " parameters of " + spec.name);
+    TokenSequence t;
+    t.role = TokenSequence::Role::output;
+    for (int i = 0; i < spec.num_params(); ++i) {
+        const std::string& n = spec.params[static_cast<std::size_t>(i)].name;
+        auto it = params.find(n);
+        if (it == params.end()) throw ValidationError("encode_params: map missing parameter " + n, n);
+        const int id = v.output_param(i).id_of(it->second);
+        if (id < 0)
+            throw ValidationError("value " + std::to_string(it->second) + " of parameter " + n +
+                                      " is not in the vocabulary",
+                                  n);
+        t.ids.push_back(id);
+    }
+    return t;
+}
+
+// ------------------------------------------------------------------ models
+std::string variant_label(ModelVariant v) {
+    switch (v) {
+        case ModelVariant::enc_dec: return "enc-dec";
+        case ModelVariant::attn: return "attn";
+        case ModelVariant::attn2: return "attn-2";
+        case ModelVariant::hybrid: return "hybrid";
+        case ModelVariant::hybrid2: return "hybrid-2";
+    }
+    throw ParameterError("unknown model variant");
+}
+
+ModelVariant variant_from_label(const std::string& s) {
+    if (s == "enc-dec") return ModelVariant::enc_dec;
+    if (s == "attn") return ModelVariant::attn;
+    if (s == "attn-2") return ModelVariant::attn2;
+    if (s == "hybrid") return ModelVariant::hybrid;
+    if (s == "hybrid-2") return ModelVariant::hybrid2;
+    throw ValidationError("unknown model variant '" + s + "' (enc-dec|attn|attn-2|hybrid|hybrid-2)", "variant");
+}
+
+KernelSpec spec_of(const ModelParams& params) {
+    KernelSpec s;
+    s.name = params.kernel;
+    for (const FieldVocab& fv : params.vocab.output_params()) s.params.push_back({fv.name, fv.values});
+    s.check();
+    return s;
+}
+
+ModelParams load_checkpoint(const std::string& path) {
+    ks_checkpoint* ck = nullptr;
+    check(ks_checkpoint_load(path.c_str(), &ck));
+    std::unique_ptr<ks_checkpoint, void (*)(ks_checkpoint*)> guard(ck, ks_checkpoint_free);
+    auto hdr = [&](const char* k) -> std::string {
+        const char* v = ks_checkpoint_header(ck, k);
+        return v ? std::string(v) : std::string();
+    };
+    auto ints = [](const std::string& s) {
+        std::vector<std::int64_t> v;
+        std::stringstream ss(s);
+        std::string piece;
+        while (std::getline(ss, piece, ','))
+            if (!piece.empty()) v.push_back(std::stoll(piece));
+        return v;
+    };
+    ModelParams mp;
+    mp.config.variant = variant_from_label(hdr("variant"));
+    mp.kernel = hdr("kernel");
+    if (!hdr("precision").empty()) mp.precision = precision_from_label(hdr("precision"));
+    auto geti = [&](const char* k, int& dst) {
+        const std::string v = hdr(k);
+        if (!v.empty()) dst = std::stoi(v);
+    };
+    geti("encoder_state_size", mp.config.encoder_state_size);
+    geti("pre_attention_size", mp.config.pre_attention_size);
+    geti("post_attention_size", mp.config.post_attention_size);
+    geti("attention_dense_nodes", mp.config.attention_dense_nodes);
+    geti("decoder_cell_size", mp.config.decoder_cell_size);
+    if (!hdr("dropout").empty()) mp.config.dropout = std::stod(hdr("dropout"));
+    if (!hdr("recurrent_dropout").empty()) mp.config.recurrent_dropout = std::stod(hdr("recurrent_dropout"));
+    std::vector<FieldVocab> in, out;
+    for (int f = 0; f < kNumInputFields; ++f) {
+        const std::string v = hdr((std::string("input_vocab.") + kInputFieldNames[f]).c_str());
+        if (v.empty())
+            throw CheckpointError(CheckpointError::Kind::malformed,
+                                  std::string("missing input vocabulary for field ") + kInputFieldNames[f]);
+        in.push_back({kInputFieldNames[f], ints(v)});
+    }
+    const int np = hdr("output_params").empty() ? 0 : std::stoi(hdr("output_params"));
+    for (int i = 0; i < np; ++i) {
+        const std::string v = hdr(("param." + std::to_string(i)).c_str());
+        const auto eq = v.find(" = ");
+        if (eq == std::string::npos)
+            throw CheckpointError(CheckpointError::Kind::malformed, "bad param header line: param." + std::to_string(i));
+        out.push_back({v.substr(0, eq), ints(v.substr(eq + 3))});
+    }
+    mp.vocab = Vocabulary(std::move(in), std::move(out));
+    for (int i = 0; i < ks_checkpoint_num_tensors(ck); ++i) {
+        const char* name;
+        int32_t rank = 0, dims[3] = {1, 1, 1};
+        const float* data;
+        check(ks_checkpoint_tensor(ck, i, &name, &rank, dims, &data));
+        HostTensor t;
+        std::size_t n = 1;
+        for (int r = 0; r < rank; ++r) {
+            t.shape.push_back(dims[r]);
+            n *= static_cast<std::size_t>(dims[r]);
+        }
+        t.values.assign(data, data + n);
+        mp.tensors.emplace(name, std::move(t));
+    }
+    return mp;
+}
+
+// ------------------------------------------------------------------ predictor
+SequencePredictor::SequencePredictor(const ModelParams& params, int device, GemmPrecision precision)
+    : params_(&params) {
+    const int var = static_cast<int>(params.config.variant);
+    std::vector<int32_t> in_sizes, vsizes;
+    std::vector<int64_t> in_vals, out_vals;
+    for (const auto& f : params.vocab.input_fields()) {
+        in_sizes.push_back(f.size());
+        in_vals.insert(in_vals.end(), f.values.begin(), f.values.end());
+    }
+    for (const auto& f : params.vocab.output_params()) {
+        vsizes.push_back(f.size());
+        out_vals.insert(out_vals.end(), f.values.begin(), f.values.end());
+    }
+    std::vector<const char*> names;
+    std::vector<int32_t> numel;
+    std::vector<const float*> data;
+    for (const auto& [n, t] : params.tensors) {
+        names.push_back(n.c_str());
+        numel.push_back(static_cast<int32_t>(t.values.size()));
+        data.push_back(t.values.data());
+    }
+    ks_model_desc d{};
+    d.variant = var;
+    d.encoder_state_size = params.config.encoder_state_size;
+    d.pre_attention_size = params.config.pre_attention_size;
+    d.post_attention_size = params.config.post_attention_size;
+    d.attention_dense_nodes = params.config.attention_dense_nodes;
+    d.num_positions = params.num_output_positions();
+    d.input_sizes = in_sizes.data();
+    d.input_values = in_vals.data();
+    d.vocab_sizes = vsizes.data();
+    d.output_values = out_vals.data();
+    d.num_tensors = static_cast<int32_t>(names.size());
+    d.tensor_names = names.data();
+    d.tensor_numel = numel.data();
+    d.tensor_data = data.data();
+    ks_engine* e = nullptr;
+    check(ks_engine_create(&d, device, static_cast<int32_t>(precision), &e));
+    engine_ = std::shared_ptr<ks_engine>(e, ks_engine_destroy);
+}
+
+int SequencePredictor::num_positions() const { return params_->num_output_positions(); }
+int SequencePredictor::vocab_size(int position) const { return params_->vocab.output_param(position).size(); }
+ks_engine* SequencePredictor::engine() const { return engine_.get(); }
+
+// ------------------------------------------------------------------ decode
+namespace {
+
+// Resolved predicate list for one model: ks_pred array + backing storage + the
+// opaque (host) predicates.
+struct ResolvedPreds {
+    std::vector<ks_pred> preds;
+    std::vector<std::vector<uint8_t>> masks;
+    std::vector<std::vector<int32_t>> pos, field;
+    std::vector<std::vector<double>> w;
+    std::vector<int> host;  // registration indices of opaque predicates
+};
+
+ResolvedPreds resolve(const ModelParams& mp, std::span<const ConstraintPredicate> preds) {
+    ResolvedPreds r;
+    const auto& outs = mp.vocab.output_params();
+    auto pos_of = [&](const std::string& n) {
+        for (std::size_t i = 0; i < outs.size(); ++i)
+            if (outs[i].name == n) return static_cast<int32_t>(i);
+        return -1;
+    };
+    r.preds.resize(preds.size());
+    r.masks.resize(preds.size());
+    r.pos.resize(preds.size());
+    r.field.resize(preds.size());
+    r.w.resize(preds.size());
+    for (std::size_t i = 0; i < preds.size(); ++i) {
+        const ConstraintPredicate& p = preds[i];
+        ks_pred& q = r.preds[i];
+        std::memset(&q, 0, sizeof q);
+        q.full_sequence_only = p.full_sequence_only ? 1 : 0;
+        if (!p.program) {
+            q.kind = KS_PRED_HOST;
+            r.host.push_back(static_cast<int>(i));
+            continue;
+        }
+        const PredicateProgram& g = *p.program;
+        switch (g.kind) {
+            case PredicateProgram::Kind::mask: {
+                q.kind = KS_PRED_MASK;
+                for (const auto& f : outs) {
+                    auto it = g.legal.find(f.name);
+                    if (it == g.legal.end())
+                        throw ValidationError("membership predicate: unknown parameter '" + f.name + "'", f.name);
+                    for (std::int64_t v : f.values)
+                        r.masks[i].push_back(std::find(it->second.begin(), it->second.end(), v) != it->second.end());
+                }
+                q.allowed = r.masks[i].data();
+                break;
+            }
+            case PredicateProgram::Kind::budget:
+                q.kind = KS_PRED_BUDGET;
+                for (const auto& [n, w] : g.weights) {  // std::map: alphabetical
+                    r.pos[i].push_back(pos_of(n));
+                    r.w[i].push_back(w);
+                }
+                q.n_terms = static_cast<int32_t>(r.pos[i].size());
+                q.term_pos = r.pos[i].data();
+                q.term_w = r.w[i].data();
+                q.budget = g.budget;
+                break;
+            case PredicateProgram::Kind::product:
+                q.kind = KS_PRED_PRODUCT;
+                for (const auto& n : g.factors) r.pos[i].push_back(pos_of(n));
+                q.n_terms = static_cast<int32_t>(r.pos[i].size());
+                q.term_pos = r.pos[i].data();
+                q.scale = g.scale;
+                q.limit = g.limit;
+                break;
+            case PredicateProgram::Kind::divides:
+                q.kind = KS_PRED_DIVIDES;
+                for (const auto& [n, f] : g.divides) {
+                    r.pos[i].push_back(pos_of(n));
+                    r.field[i].push_back(f);
+                }
+                q.n_terms = static_cast<int32_t>(r.pos[i].size());
+                q.term_pos = r.pos[i].data();
+                q.term_field = r.field[i].data();
+                break;
+        }
+    }
+    return r;
+}
+
+struct HookCtx {
+    const ModelParams* mp;
+    std::span<const ConstraintPredicate> preds;
+    const std::vector<int>* host;
+    std::span<const ProblemDescriptor> descs;
+    std::string error;
+};
+
+// Evaluates the opaque predicates exactly as beam_search_impl does
+// (decoding.cpp:60-77): decoded-value ParamMap of the child's prefix,
+// registration order, full_sequence_only only at the last position.
+int32_t host_hook(void* user, int32_t position, int32_t final_step, int64_t n_rows, const int32_t* row_config,
+                  const int32_t* row_prefix, int32_t vocab, int32_t* out) {
+    auto* ctx = static_cast<HookCtx*>(user);
+    const auto& outs = ctx->mp->vocab.output_params();
+    try {
+        for (int64_t r = 0; r < n_rows; ++r) {
+            ParamMap m;
+            for (int t = 0; t < position; ++t)
+                m[outs[static_cast<std::size_t>(t)].name] =
+                    outs[static_cast<std::size_t>(t)].value_of(row_prefix[r * position + t]);
+            const ProblemDescriptor& d = ctx->descs[static_cast<std::size_t>(row_config[r])];
+            const std::string& name = outs[static_cast<std::size_t>(position)].name;
+            for (int v = 0; v < vocab; ++v) {
+                m[name] = outs[static_cast<std::size_t>(position)].value_of(v);
+                int32_t rej = -1;
+                for (int qi : *ctx->host) {
+                    const ConstraintPredicate& q = ctx->preds[static_cast<std::size_t>(qi)];
+                    if (q.full_sequence_only && !final_step) continue;
+                    if (!q.evaluate(d, m)) {
+                        rej = qi;
+                        break;
+                    }
+                }
+                out[r * vocab + v] = rej;
+            }
+        }
+    } catch (const std::exception& e) {
+        ctx->error = e.what();
+        return 1;
+    }
+    return 0;
+}
+
+}  // namespace
+
+BatchResult beam_search_batch(const SequencePredictor& predictor, std::span<const TokenSequence> inputs,
+                              std::span<const ProblemDescriptor> descriptors, int beam_width,
+                              std::span<const ConstraintPredicate> predicates) {
+    if (beam_width < 1) throw ParameterError("beam width must be >= 1, got " + std::to_string(beam_width));
+    const ModelParams& mp = predictor.params();
+    const int T = mp.num_output_positions();
+    const std::size_t B = inputs.size();
+    std::vector<int32_t> tok(B * 7);
+    for (std::size_t b = 0; b < B; ++b) {
+        if (inputs[b].length() != kNumInputFields)
+            throw ParameterError("model input must have 7 tokens, got " + std::to_string(inputs[b].length()));
+        for (int f = 0; f < 7; ++f) tok[b * 7 + f] = inputs[b].ids[static_cast<std::size_t>(f)];
+    }
+    std::vector<int64_t> desc;
+    if (!descriptors.empty()) {
+        if (descriptors.size() != B) throw ParameterError("descriptor count differs from input count");
+        desc.resize(B * 7);
+        for (std::size_t b = 0; b < B; ++b)
+            for (int f = 0; f < 7; ++f) desc[b * 7 + f] = descriptor_field(descriptors[b], f);
+    }
+    ResolvedPreds rp = resolve(mp, predicates);
+    if (!rp.host.empty() && descriptors.empty())
+        throw ParameterError("opaque predicates need the problem descriptors");
+    const std::size_t k = static_cast<std::size_t>(beam_width);
+    std::vector<int32_t> otok(B * k * T), cnt(B), st(B), fp(B), fs(B);
+    std::vector<double> olp(B * k);
+    HookCtx ctx{&mp, predicates, &rp.host, descriptors, {}};
+    ks_status s = ks_beam_search_batch_hooked(
+        predictor.engine(), tok.data(), desc.empty() ? nullptr : desc.data(), static_cast<int64_t>(B),
+        beam_width, rp.preds.empty() ? nullptr : rp.preds.data(), static_cast<int32_t>(rp.preds.size()),
+        rp.host.empty() ? nullptr : host_hook, &ctx, otok.data(), olp.data(), cnt.data(), st.data(), fp.data(),
+        fs.data());
+    if (!ctx.error.empty()) throw Error("predicate raised: " + ctx.error);
+    check(s);
+    BatchResult res;
+    res.beams.resize(B);
+    res.exhausted.resize(B);
+    for (std::size_t b = 0; b < B; ++b) {
+        if (st[b] != 0) {
+            res.exhausted[b].exhausted = true;
+            res.exhausted[b].step = fs[b];
+            if (fp[b] >= 0 && static_cast<std::size_t>(fp[b]) < predicates.size())
+                res.exhausted[b].predicate = predicates[static_cast<std::size_t>(fp[b])].name;
+            continue;
+        }
+        for (int j = 0; j < cnt[b]; ++j) {
+            ScoredSequence ss;
+            ss.tokens.role = TokenSequence::Role::output;
+            ss.tokens.ids.assign(otok.begin() + (b * k + j) * T, otok.begin() + (b * k + j + 1) * T);
+            ss.log_prob = olp[b * k + j];
+            res.beams[b].push_back(std::move(ss));
+        }
+    }
+    return res;
+}
+
+std::vector<TokenSequence> greedy_decode_batch(const SequencePredictor& predictor,
+                                               std::span<const TokenSequence> inputs) {
+    const int T = predictor.num_positions();
+    const std::size_t B = inputs.size();
+    std::vector<int32_t> tok(B * 7), out(B * T);
+    for (std::size_t b = 0; b < B; ++b) {
+        if (inputs[b].length() != kNumInputFields)
+            throw ParameterError("model input must have 7 tokens, got " + std::to_string(inputs[b].length()));
+        for (int f = 0; f < 7; ++f) tok[b * 7 + f] = inputs[b].ids[static_cast<std::size_t>(f)];
+    }
+    check(ks_greedy_batch(predictor.engine(), tok.data(), static_cast<int64_t>(B), out.data()));
+    std::vector<TokenSequence> res(B);
+    for (std::size_t b = 0; b < B; ++b) {
+        res[b].role = TokenSequence::Role::output;
+        res[b].ids.assign(out.begin() + b * T, out.begin() + (b + 1) * T);
+    }
+    return res;
+}
+
+TokenSequence greedy_decode(const SequencePredictor& predictor, const TokenSequence& input) {
+    return greedy_decode_batch(predictor, std::span<const TokenSequence>(&input, 1))[0];
+}
+
+std::vector<ScoredSequence> beam_search(const SequencePredictor& predictor, const TokenSequence& input,
+                                        int beam_width) {
+    return beam_search_batch(predictor, std::span<const TokenSequence>(&input, 1), {}, beam_width, {}).beams[0];
+}
+
+std::vector<ScoredSequence> constrained_beam_search(const SequencePredictor& predictor, const TokenSequence& input,
+                                                    int beam_width, std::span<const ConstraintPredicate> predicates,
+                                                    const ProblemDescriptor& descriptor) {
+    BatchResult r = beam_search_batch(predictor, std::span<const TokenSequence>(&input, 1),
+                                      std::span<const ProblemDescriptor>(&descriptor, 1), beam_width, predicates);
+    if (r.exhausted[0].exhausted) {
+        const auto& e = r.exhausted[0];
+        throw BeamExhaustedError("constrained beam search: every candidate at position " + std::to_string(e.step) +
+                                     " was rejected (last rejecting predicate: " + e.predicate + ")",
+                                 e.predicate, e.step);
+    }
+    return r.beams[0];
+}
+
+// ------------------------------------------------------------------ evaluation
+EvalReport compute_metrics(const std::vector<TokenSequence>& predictions, const std::vector<TokenSequence>& actuals) {
+    if (actuals.empty()) throw ParameterError("metrics: empty test set");
+    if (predictions.size() != actuals.size())
+        throw ParameterError("metrics: " + std::to_string(predictions.size()) + " predictions vs " +
+                             std::to_string(actuals.size()) + " actuals");
+    const std::size_t arity = actuals[0].ids.size();
+    for (std::size_t i = 0; i < actuals.size(); ++i)
+        if (predictions[i].ids.size() != arity || actuals[i].ids.size() != arity)
+            throw ParameterError("metrics: sequences must have uniform arity");
+    EvalReport r;
+    r.sample_count = static_cast<int>(actuals.size());
+    r.per_param_accuracy.assign(arity, 0.0);
+    int perfect = 0;
+    for (std::size_t i = 0; i < actuals.size(); ++i) {
+        bool all = true;
+        for (std::size_t p = 0; p < arity; ++p) {
+            if (predictions[i].ids[p] == actuals[i].ids[p])
+                r.per_param_accuracy[p] += 1.0;
+            else
+                all = false;
+        }
+        perfect += all ? 1 : 0;
+    }
+    const double S = static_cast<double>(actuals.size());
+    double sum = 0.0;
+    for (double& a : r.per_param_accuracy) {
+        a = a / S * 100.0;
+        sum += a;
+    }
+    r.average_accuracy = sum / static_cast<double>(arity);
+    r.perfect_prediction = static_cast<double>(perfect) / S * 100.0;
+    return r;
+}
+
+// topk_metrics (proj/src/eval.cpp:74-152): for each k a full batched search on
+// the GPU; best-matching beam (most position matches, ties to the higher rank),
+// perfect = any of the k beams equals the truth; exhausted searches score 0.
+std::vector<EvalReport> topk_metrics(const ModelParams& params, const std::vector<Sample>& test,
+                                     const std::vector<int>& k_values,
+                                     std::span<const ConstraintPredicate> predicates, int threads) {
+    const SequencePredictor predictor(params);
+    return topk_metrics(predictor, test, k_values, predicates, threads);
+}
+
+std::vector<EvalReport> topk_metrics(const SequencePredictor& predictor, const std::vector<Sample>& test,
+                                     const std::vector<int>& k_values,
+                                     std::span<const ConstraintPredicate> predicates, int /*threads*/) {
+    if (test.empty()) throw ParameterError("topk_metrics: empty test set");
+    for (int k : k_values)
+        if (k < 1) throw ParameterError("topk_metrics: k must be >= 1");
+    const ModelParams& params = predictor.params();
+    const KernelSpec spec = spec_of(params);
+    const int arity = predictor.num_positions();
+    std::vector<TokenSequence> inputs, truths;
+    std::vector<ProblemDescriptor> descs;
+    for (const Sample& s : test) {
+        inputs.push_back(encode_problem(s.descriptor, params.vocab));
+        truths.push_back(encode_params(s.params, spec, params.vocab));
+        descs.push_back(s.descriptor);
+    }
+    std::vector<EvalReport> reports;
+    for (int k : k_values) {
+        const BatchResult br = beam_search_batch(predictor, inputs, descs, k, predicates);
+        std::vector<TokenSequence> best(test.size());
+        int hits = 0;
+        for (std::size_t i = 0; i < test.size(); ++i) {
+            int best_m = -1;
+            TokenSequence bs;
+            bs.role = TokenSequence::Role::output;
+            bs.ids.assign(static_cast<std::size_t>(arity), -1);
+            bool perfect = false;
+            for (const ScoredSequence& beam : br.beams[i]) {
+                int m = 0;
+                for (int p = 0; p < arity; ++p) m += beam.tokens.ids[static_cast<std::size_t>(p)] == truths[i].ids[static_cast<std::size_t>(p)];
+                if (m == arity) perfect = true;
+                if (m > best_m) {
+                    best_m = m;
+                    bs = beam.tokens;
+                }
+            }
+            hits += perfect ? 1 : 0;
+            best[i] = std::move(bs);
+        }
+        EvalReport r = compute_metrics(best, truths);
+        r.perfect_prediction = 100.0 * hits / static_cast<double>(test.size());
+        r.beam_width = k;
+        r.constrained = !predicates.empty();
+        reports.push_back(std::move(r));
+    }
+    return reports;
+}
+
+}  // namespace kernelseer

@@ -1,0 +1,282 @@
+// pymodule.cpp -- the Python face of the engine: the same function names,
+// keyword arguments and return shapes as the reference's pybind module
+// (proj/bindings/module.cpp:106-355) for the decode path, implemented on the
+// C++ host layer (kernelseer_b200.hpp) and therefore on the GPU.
+//
+// Differences that are deliberate:
+//  * the GIL is released around every device call (the reference holds it,
+//    which deadlocks topk_metrics(threads>1) with Python predicates);
+//  * ModelParams caches its device engine (weights packed once per process);
+//  * predict_batch / greedy_predict_batch take many descriptors in one call.
+#include <pybind11/functional.h>
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <mutex>
+
+#include "kernelseer_b200.hpp"
+
+namespace py = pybind11;
+using namespace kernelseer;
+
+namespace {
+
+struct PyModel {
+    std::shared_ptr<ModelParams> params;
+    std::shared_ptr<SequencePredictor> predictor;
+    int device = 0;
+    GemmPrecision precision = GemmPrecision::f16x3;
+    std::mutex mu;
+    const SequencePredictor& pred() {
+        std::lock_guard<std::mutex> g(mu);
+        if (!predictor) predictor = std::make_shared<SequencePredictor>(*params, device, precision);
+        return *predictor;
+    }
+};
+
+ProblemDescriptor descriptor_from_dict(const py::dict& d) {
+    ProblemDescriptor out;
+    for (auto item : d) {
+        const std::string key = py::cast<std::string>(item.first);
+        if (key == "precision") {
+            out.precision = precision_from_label(py::cast<std::string>(item.second));
+            continue;
+        }
+        bool known = false;
+        for (int f = 0; f < kNumInputFields; ++f)
+            if (key == kInputFieldNames[static_cast<std::size_t>(f)]) {
+                set_descriptor_field(out, f, py::cast<std::int64_t>(item.second));
+                known = true;
+            }
+        if (!known) throw ValidationError("unknown descriptor field '" + key + "'", key);
+    }
+    out.check();
+    return out;
+}
+
+py::dict descriptor_to_dict(const ProblemDescriptor& d) {
+    py::dict out;
+    for (int f = 0; f < kNumInputFields; ++f) out[kInputFieldNames[static_cast<std::size_t>(f)]] = descriptor_field(d, f);
+    out["precision"] = precision_label(d.precision);
+    return out;
+}
+
+// Opaque Python callable predicate (module.cpp:51-63): evaluated by the
+// engine's host hook between positions, under the GIL.
+ConstraintPredicate python_predicate(const std::string& name, const std::function<bool(py::dict, py::dict)>& fn) {
+    ConstraintPredicate pred;
+    pred.name = name;
+    pred.fn = [fn](const ProblemDescriptor& d, const ParamMap& partial) {
+        py::gil_scoped_acquire gil;
+        py::dict params;
+        for (const auto& [k, v] : partial) params[py::str(k)] = v;
+        return fn(descriptor_to_dict(d), params);
+    };
+    return pred;
+}
+
+py::list beams_to_python(const ModelParams& params, const std::vector<ScoredSequence>& beams) {
+    const KernelSpec spec = spec_of(params);
+    py::list out;
+    for (const ScoredSequence& s : beams) {
+        py::dict entry, values;
+        for (const auto& [k, v] : decode_params(s.tokens, spec, params.vocab)) values[py::str(k)] = v;
+        entry["params"] = values;
+        entry["log_prob"] = s.log_prob;
+        out.append(entry);
+    }
+    return out;
+}
+
+GemmPrecision precision_of(const std::string& s) {
+    if (s == "f16x3") return GemmPrecision::f16x3;
+    if (s == "fp32") return GemmPrecision::fp32;
+    if (s == "bf16") return GemmPrecision::bf16;
+    throw ParameterError("precision must be f16x3, fp32 or bf16");
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_kernelseer_b200, m) {
+    m.doc() = "B200 constrained beam decode for GPU kernel tuning-parameter prediction";
+    py::register_exception<Error>(m, "KernelseerError");
+
+    py::class_<KernelSpec>(m, "KernelSpec")
+        .def_readonly("name", &KernelSpec::name)
+        .def_property_readonly("params",
+                               [](const KernelSpec& s) {
+                                   py::list out;
+                                   for (const auto& p : s.params) out.append(py::make_tuple(p.name, p.values));
+                                   return out;
+                               })
+        .def("__repr__", [](const KernelSpec& s) {
+            return "<KernelSpec " + s.name + " (" + std::to_string(s.num_params()) + " params)>";
+        });
+    m.def("builtin_specs", [] { return builtin_specs(); });
+    m.def("builtin_spec", [](const std::string& n) { return builtin_spec(n); }, py::arg("name"));
+    m.def("search_space_size", [](const KernelSpec& s) { return search_space_size(s); }, py::arg("spec"));
+
+    py::class_<Sample>(m, "Sample")
+        .def(py::init([](const py::dict& descriptor, const ParamMap& params, const std::string& kernel,
+                         const std::string& precision) {
+                 Sample s;
+                 s.descriptor = descriptor_from_dict(descriptor);
+                 s.params = params;
+                 s.kernel = kernel;
+                 s.precision = precision_from_label(precision);
+                 return s;
+             }),
+             py::arg("descriptor"), py::arg("params"), py::arg("kernel") = "", py::arg("precision") = "fp32")
+        .def_property_readonly("descriptor", [](const Sample& s) { return descriptor_to_dict(s.descriptor); })
+        .def_readonly("params", &Sample::params)
+        .def_readonly("kernel", &Sample::kernel)
+        .def_property_readonly("precision", [](const Sample& s) { return precision_label(s.precision); });
+
+    py::class_<PyModel, std::shared_ptr<PyModel>>(m, "ModelParams")
+        .def_property_readonly("kernel", [](PyModel& p) { return p.params->kernel; })
+        .def_property_readonly("precision", [](PyModel& p) { return precision_label(p.params->precision); })
+        .def_property_readonly("variant", [](PyModel& p) { return variant_label(p.params->config.variant); })
+        .def_property_readonly("spec", [](PyModel& p) { return spec_of(*p.params); })
+        .def("set_engine",
+             [](PyModel& p, int device, const std::string& precision) {
+                 std::lock_guard<std::mutex> g(p.mu);
+                 p.device = device;
+                 p.precision = precision_of(precision);
+                 p.predictor.reset();
+             },
+             py::arg("device") = 0, py::arg("precision") = "f16x3",
+             "Select the GPU and the gate-GEMM arithmetic (f16x3 | fp32 | bf16) of the cached engine")
+        .def("__repr__", [](PyModel& p) {
+            return "<ModelParams " + variant_label(p.params->config.variant) + " for " + p.params->kernel + ">";
+        });
+    m.def("load_checkpoint",
+          [](const std::string& path) {
+              auto pm = std::make_shared<PyModel>();
+              pm->params = std::make_shared<ModelParams>(load_checkpoint(path));
+              return pm;
+          },
+          py::arg("path"));
+
+    py::class_<ConstraintPredicate>(m, "ConstraintPredicate")
+        .def_readonly("name", &ConstraintPredicate::name)
+        .def_property_readonly("device_evaluable", [](const ConstraintPredicate& p) { return (bool)p.program; });
+    m.def("membership_predicate", &membership_predicate, py::arg("spec"));
+    m.def("resource_budget_predicate",
+          [](const std::map<std::string, double>& w, double budget, const std::string& name) {
+              return resource_budget_predicate(w, budget, name);
+          },
+          py::arg("weights"), py::arg("budget"), py::arg("name") = "resource_budget");
+    m.def("product_limit_predicate", &product_limit_predicate, py::arg("params"), py::arg("scale"),
+          py::arg("limit"), py::arg("name") = "product_limit",
+          "scale * prod(assigned values) <= limit (workgroup size / LDS bytes); device-evaluated");
+    m.def("divisibility_predicate", &divisibility_predicate, py::arg("param_field"),
+          py::arg("name") = "divisibility",
+          "each listed parameter value divides descriptor field (0..6 = n,c,h,w,k,y,x); device-evaluated");
+    m.def("predicate", &python_predicate, py::arg("name"), py::arg("fn"),
+          "Wrap a python callable (descriptor_dict, partial_params_dict) -> bool (host-evaluated)");
+
+    m.def("validate",
+          [](const KernelSpec& spec, const py::dict& descriptor, const ParamMap& params,
+             const std::vector<ConstraintPredicate>& predicates) -> py::object {
+              const auto v = validate_sequence(spec, descriptor_from_dict(descriptor), params, predicates);
+              if (!v) return py::none();
+              py::dict out;
+              out["predicate"] = v->predicate;
+              out["params"] = v->params;
+              return out;
+          },
+          py::arg("spec"), py::arg("descriptor"), py::arg("params"), py::arg("predicates"));
+
+    m.def("predict",
+          [](std::shared_ptr<PyModel> pm, const py::dict& descriptor, int beam_width,
+             const std::vector<ConstraintPredicate>& predicates, bool snap) {
+              const ProblemDescriptor d = descriptor_from_dict(descriptor);
+              const TokenSequence input = encode_problem(d, pm->params->vocab, snap);
+              const SequencePredictor& pred = pm->pred();
+              std::vector<ScoredSequence> beams;
+              {
+                  py::gil_scoped_release nogil;
+                  beams = predicates.empty() ? beam_search(pred, input, beam_width)
+                                             : constrained_beam_search(pred, input, beam_width, predicates, d);
+              }
+              return beams_to_python(*pm->params, beams);
+          },
+          py::arg("params"), py::arg("descriptor"), py::arg("beam_width") = 1,
+          py::arg("predicates") = std::vector<ConstraintPredicate>{}, py::arg("snap") = false);
+
+    m.def("greedy_predict",
+          [](std::shared_ptr<PyModel> pm, const py::dict& descriptor, bool snap) {
+              const ProblemDescriptor d = descriptor_from_dict(descriptor);
+              const TokenSequence input = encode_problem(d, pm->params->vocab, snap);
+              const SequencePredictor& pred = pm->pred();
+              TokenSequence out;
+              {
+                  py::gil_scoped_release nogil;
+                  out = greedy_decode(pred, input);
+              }
+              py::dict values;
+              for (const auto& [k, v] : decode_params(out, spec_of(*pm->params), pm->params->vocab))
+                  values[py::str(k)] = v;
+              return values;
+          },
+          py::arg("params"), py::arg("descriptor"), py::arg("snap") = false);
+
+    m.def("predict_batch",
+          [](std::shared_ptr<PyModel> pm, const std::vector<py::dict>& descriptors, int beam_width,
+             const std::vector<ConstraintPredicate>& predicates, bool snap) {
+              std::vector<ProblemDescriptor> ds;
+              std::vector<TokenSequence> ins;
+              for (const auto& dd : descriptors) {
+                  ds.push_back(descriptor_from_dict(dd));
+                  ins.push_back(encode_problem(ds.back(), pm->params->vocab, snap));
+              }
+              const SequencePredictor& pred = pm->pred();
+              BatchResult r;
+              {
+                  py::gil_scoped_release nogil;
+                  r = beam_search_batch(pred, ins, ds, beam_width, predicates);
+              }
+              py::list out;
+              for (std::size_t i = 0; i < ins.size(); ++i) {
+                  if (r.exhausted[i].exhausted) {
+                      py::dict e;
+                      e["exhausted"] = true;
+                      e["predicate"] = r.exhausted[i].predicate;
+                      e["step"] = r.exhausted[i].step;
+                      out.append(e);
+                  } else {
+                      out.append(beams_to_python(*pm->params, r.beams[i]));
+                  }
+              }
+              return out;
+          },
+          py::arg("params"), py::arg("descriptors"), py::arg("beam_width") = 1,
+          py::arg("predicates") = std::vector<ConstraintPredicate>{}, py::arg("snap") = false,
+          "Batched predict: one entry per descriptor (a beam list, or an exhaustion record)");
+
+    m.def("topk_metrics",
+          [](std::shared_ptr<PyModel> pm, const std::vector<Sample>& test, const std::vector<int>& k_values,
+             const std::vector<ConstraintPredicate>& predicates, int threads) {
+              std::vector<EvalReport> reports;
+              const SequencePredictor& pred = pm->pred();
+              {
+                  py::gil_scoped_release nogil;
+                  reports = topk_metrics(pred, test, k_values, predicates, threads);
+              }
+              py::list out;
+              for (const EvalReport& r : reports) {
+                  py::dict d;
+                  d["beam_width"] = r.beam_width;
+                  d["constrained"] = r.constrained;
+                  d["samples"] = r.sample_count;
+                  d["average_accuracy"] = r.average_accuracy;
+                  d["perfect_prediction"] = r.perfect_prediction;
+                  d["per_param_accuracy"] = r.per_param_accuracy;
+                  out.append(d);
+              }
+              return out;
+          },
+          py::arg("params"), py::arg("test"), py::arg("k_values"),
+          py::arg("predicates") = std::vector<ConstraintPredicate>{}, py::arg("threads") = 1);
+}

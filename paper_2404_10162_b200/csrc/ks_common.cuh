@@ -139,6 +139,7 @@ struct BeamArgs {
     int* out_fail_step;
     int* out_status;
     int cands_per_warp;        // smem capacity per warp (entries)
+    const int* host_rej;       // [B*H_cur][V] first rejecting host predicate (or -1); may be null
 };
 
 // fp16 split with an exact power-of-two scale on the residual so that it

@@ -143,7 +143,8 @@ struct ks_engine {
     DevMem live[2], lp[2], key[2], parent[2], slot[2], status, fpred, fstep;
     DevMem otok, olp, ocount, ostatus, ofpred, ofstep;
     DevMem preds, pbytes, tpos, tw, tfield;
-    HostMem h_in, h_out;
+    DevMem hrej;                  // host-hook rejections [C*k][Vmax]
+    HostMem h_in, h_out, hk_keys, hk_live, hk_rej;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     int beam_smem_max = 0;
@@ -492,6 +493,9 @@ namespace {
 struct PredDev {
     int n = 0;
     bool needs_desc = false;
+    bool has_host = false;
+    ks_host_pred_fn hook = nullptr;
+    void* user = nullptr;
 };
 
 ks_status upload_preds(ks_engine& E, const ks_pred* preds, int n, PredDev& pd) {
@@ -538,6 +542,8 @@ ks_status upload_preds(ks_engine& E, const ks_pred* preds, int n, PredDev& pd) {
             d.budget = q.budget;
             d.scale = q.scale;
             d.limit = q.limit;
+        } else if (q.kind == KS_PRED_HOST) {
+            pd.has_host = true;
         } else {
             return set_error(KS_ERR_PARAMETER, "unknown predicate kind " + std::to_string(q.kind));
         }
@@ -626,7 +632,7 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
 }
 
 // Decodes one chunk of C configs already resident on the device.
-ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_tok,
+ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greedy, const int* d_tok,
                     const long long* d_desc, const PredDev& pd, int* o_tok, double* o_lp,
                     int* o_count, int* o_status, int* o_fpred, int* o_fstep) {
     ks_status st;
@@ -713,9 +719,26 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
         }
     }
     const int cpw = (maxc + 7) / 8 * 8;
+    int vmax = 1;
+    for (int p = 0; p < E.T; ++p) vmax = std::max(vmax, E.vsize[(size_t)p]);
+    cudaEvent_t keys_ready = nullptr;
+    if (pd.has_host) {
+        if (!pd.hook) return set_error(KS_ERR_PARAMETER, "host predicates need ks_beam_search_batch_hooked");
+        if (E.hk_keys.ensure((size_t)R * 8) || E.hk_live.ensure((size_t)R) ||
+            E.hk_rej.ensure((size_t)R * vmax * 4) || E.hrej.ensure((size_t)R * vmax * 4))
+            return set_error(KS_ERR_CUDA, "host-hook buffers");
+        cudaEventCreateWithFlags(&keys_ready, cudaEventDisableTiming);
+    }
     for (int pos = 0; pos < E.T; ++pos) {
         const int cur = pos & 1, nxt = cur ^ 1;
         const int M = (int)(C * H);
+        if (pd.has_host) {
+            // live prefixes of this position leave the device now; the hook runs on the
+            // host while the GPU computes this position's attention and gate GEMM
+            KS_CUDA(cudaMemcpyAsync(E.hk_keys.p, E.key[cur].p, (size_t)M * 8, cudaMemcpyDeviceToHost, s));
+            KS_CUDA(cudaMemcpyAsync(E.hk_live.p, E.live[cur].p, (size_t)M, cudaMemcpyDeviceToHost, s));
+            KS_CUDA(cudaEventRecord(keys_ready, s));
+        }
         // previous position's state (or the initial state at position 0)
         const float* h_prev = nullptr;
         const float* c_prev = nullptr;
@@ -787,6 +810,35 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
         const double useful = 2.0 * (double)M * (double)(2 * E.n_a * (enc_dec ? 0 : 1) + (enc_dec ? E.e : E.n_s)) *
                               4.0 * (enc_dec ? E.e : E.n_s);
         if ((st = launch_lstm(E, p, nullptr, E.dec, nullptr, useful))) return st;
+        const int* host_rej = nullptr;
+        if (pd.has_host) {
+            KS_CUDA(cudaEventSynchronize(keys_ready));
+            const int V = E.vsize[(size_t)pos];
+            const unsigned long long* keys = E.hk_keys.as<unsigned long long>();
+            const unsigned char* live = E.hk_live.as<unsigned char>();
+            int* rej = E.hk_rej.as<int>();
+            std::vector<int32_t> rcfg, rpre, rout;
+            std::vector<int64_t> ridx;
+            for (int64_t r = 0; r < M; ++r) {
+                for (int v = 0; v < V; ++v) rej[r * V + v] = -1;
+                if (!live[r]) continue;
+                ridx.push_back(r);
+                rcfg.push_back((int32_t)(cfg_base + r / H));
+                for (int t = 0; t < pos; ++t)
+                    rpre.push_back((int32_t)((keys[r] >> E.meta.shift[t]) & ((1ull << E.meta.bits[t]) - 1ull)));
+            }
+            rout.assign(ridx.size() * (size_t)V, -1);
+            if (!ridx.empty() &&
+                pd.hook(pd.user, pos, pos == E.T - 1 ? 1 : 0, (int64_t)ridx.size(), rcfg.data(),
+                        rpre.empty() ? nullptr : rpre.data(), V, rout.data()) != 0) {
+                cudaEventDestroy(keys_ready);
+                return set_error(KS_ERR_STATE, "host predicate hook aborted the search");
+            }
+            for (size_t i = 0; i < ridx.size(); ++i)
+                for (int v = 0; v < V; ++v) rej[ridx[i] * V + v] = rout[i * V + v];
+            KS_CUDA(cudaMemcpyAsync(E.hrej.p, rej, (size_t)M * V * 4, cudaMemcpyHostToDevice, s));
+            host_rej = E.hrej.as<int>();
+        }
 
         const int V = E.vsize[(size_t)pos];
         const bool fin = pos == E.T - 1;
@@ -829,6 +881,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
         b.out_fail_pred = o_fpred;
         b.out_fail_step = o_fstep;
         b.cands_per_warp = cpw;
+        b.host_rej = host_rej;
         int warps = 8;
         while (warps > 1 && beam_smem_bytes(Hd, V, warps, cpw) > (size_t)E.beam_smem_max) --warps;
         const size_t smem = beam_smem_bytes(Hd, V, warps, cpw);
@@ -843,6 +896,10 @@ ks_status run_chunk(ks_engine& E, int64_t C, int k, bool greedy, const int* d_to
         const cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("beam launch: ") + cudaGetErrorString(err));
         H = Hn;
+    }
+    if (keys_ready) {
+        cudaStreamSynchronize(s);  // pinned host-hook buffers are reused by the next chunk
+        cudaEventDestroy(keys_ready);
     }
     return KS_OK;
 }
@@ -875,7 +932,7 @@ ks_status collect_profile(ks_engine& E) {
 ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, int64_t B, int32_t k,
                       bool greedy, const ks_pred* preds, int32_t n_preds, int32_t* out_tok,
                       double* out_lp, int32_t* out_count, int32_t* out_status, int32_t* out_fpred,
-                      int32_t* out_fstep) {
+                      int32_t* out_fstep, ks_host_pred_fn hook = nullptr, void* user = nullptr) {
     ks_engine& E = *eng;
     const int T = E.T;
     for (int64_t b = 0; b < B; ++b)
@@ -889,6 +946,8 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
     ks_status st;
     if ((st = upload_preds(E, preds, n_preds, pd))) return st;
     if (pd.needs_desc && !desc) return set_error(KS_ERR_PARAMETER, "divisibility predicates need descriptors");
+    pd.hook = hook;
+    pd.user = user;
     E.launches = 0;
     const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
     const size_t in_bytes = (size_t)C * 7 * 4 + (size_t)C * 7 * 8;
@@ -912,7 +971,7 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
             KS_CUDA(cudaMemcpyAsync(E.desc.p, hdesc, (size_t)n * 7 * 8, cudaMemcpyHostToDevice, E.stream));
             ddesc = E.desc.as<long long>();
         }
-        if ((st = run_chunk(E, n, k, greedy, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
+        if ((st = run_chunk(E, n, c0, k, greedy, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
                             E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>())))
             return st;
         char* ho = E.h_out.as<char>();
@@ -955,6 +1014,19 @@ extern "C" ks_status ks_beam_search_batch(ks_engine* eng, const int32_t* tok, co
                        out_fpred, out_fstep);
 }
 
+extern "C" ks_status ks_beam_search_batch_hooked(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                                                 int64_t B, int32_t k, const ks_pred* preds, int32_t n_preds,
+                                                 ks_host_pred_fn hook, void* user, int32_t* out_tok,
+                                                 double* out_lp, int32_t* out_count, int32_t* out_status,
+                                                 int32_t* out_fpred, int32_t* out_fstep) {
+    ks_status st = check_common(eng, B, k, preds, n_preds);
+    if (st) return st;
+    if (B == 0) return KS_OK;
+    if (!tok || !out_tok) return set_error(KS_ERR_PARAMETER, "null token buffer");
+    return decode_host(eng, tok, desc, B, k, false, preds, n_preds, out_tok, out_lp, out_count, out_status,
+                       out_fpred, out_fstep, hook, user);
+}
+
 extern "C" ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok) {
     ks_status st = check_common(eng, B, 1, nullptr, 0);
     if (st) return st;
@@ -988,7 +1060,7 @@ extern "C" ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok,
     const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
     for (int64_t c0 = 0; c0 < B; c0 += C) {
         const int64_t n = std::min<int64_t>(C, B - c0);
-        st = run_chunk(E, n, k, false, d_tok + c0 * 7, d_desc ? reinterpret_cast<const long long*>(d_desc) + c0 * 7 : nullptr,
+        st = run_chunk(E, n, c0, k, false, d_tok + c0 * 7, d_desc ? reinterpret_cast<const long long*>(d_desc) + c0 * 7 : nullptr,
                        pd, d_out_tok + c0 * k * T, d_out_lp + c0 * k, d_out_count + c0,
                        d_out_status ? d_out_status + c0 : nullptr, d_out_fpred ? d_out_fpred + c0 : nullptr,
                        d_out_fstep ? d_out_fstep + c0 : nullptr);

@@ -508,8 +508,14 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                 const unsigned long long key = a.key_cur[r] | ((unsigned long long)lane << m.shift[a.pos]);
                 int rej = -1;
                 if (lane < V) {
-                    for (int q = 0; q < a.n_preds; ++q) {
+                    // host-evaluated (opaque) predicates: registration index of the first
+                    // rejecting one; typed predicates registered before it still win
+                    const int hrej = a.host_rej ? a.host_rej[r * V + lane] : -1;
+                    const int qend = hrej >= 0 ? hrej : a.n_preds;
+                    rej = hrej;
+                    for (int q = 0; q < qend; ++q) {
                         const DevPred pq = a.preds[q];
+                        if (pq.kind == 5) continue;  // KS_PRED_HOST: decided by the hook
                         if (pq.full && !a.final_step) continue;
                         if (!pred_accepts(a, m, pq, key, a.pos, desc_b)) {
                             rej = q;

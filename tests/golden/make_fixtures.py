@@ -55,12 +55,27 @@ def tiny_inputs():
     return np.array(list(itertools.product([0, 1], repeat=7))[::9], np.int32)
 
 
+def write_specs(ks):
+    """builtin_specs() and search_space_size() as the reference reports them."""
+    import json
+
+    specs = [{"name": s.name, "params": [[n, list(v)] for n, v in s.params],
+              "search_space": ks.search_space_size(s)} for s in ks.builtin_specs()]
+    with open(os.path.join(HERE, "builtin_specs.json"), "w") as f:
+        json.dump(specs, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--specs-only", action="store_true")
     args = ap.parse_args()
     sys.path.insert(0, REF_DIR)
     import _kernelseer as ks  # the reference's own pybind module
+
+    write_specs(ks)
+    if args.specs_only:
+        return
 
     golden = {}
     for stem, variant, skey, seed in TINY_MODELS:

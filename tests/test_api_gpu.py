@@ -1,0 +1,164 @@
+"""The reference-named Python API on the GPU: ports of the reference's own
+binding smoke tests (proj/tests/python/test_smoke.py:95-140) plus oracle
+comparisons of predict / predict_batch / topk_metrics, opaque (host-hook)
+predicates mixed with typed ones, and BeamExhaustedError surfacing."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleModel
+from tests.util import golden_path, have_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a GPU")]
+
+CKPT = golden_path("attn_small_trained.ckpt")
+FIELDS = "nchwkyx"
+
+
+@pytest.fixture(scope="module")
+def ks():
+    import paper_2404_10162_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def params(ks):
+    return ks.load_checkpoint(CKPT)
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return OracleModel(CKPT)
+
+
+def descs(oracle, n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        out.append({f: int(oracle.input_values[i][rng.integers(len(oracle.input_values[i]))])
+                    for i, f in enumerate(FIELDS)})
+    return out
+
+
+def tok_of(oracle, d):
+    return np.array([[oracle.input_values[i].index(d[f]) for i, f in enumerate(FIELDS)]], np.int32)
+
+
+def test_predict_top1_is_greedy_and_membership_is_noop(ks, params, oracle):
+    """test_smoke.py:95-107"""
+    for d in descs(oracle, 16, 1):
+        top = ks.predict(params, d, beam_width=3)
+        assert len(top) == 3 and top[1]["log_prob"] <= top[0]["log_prob"]
+        assert top[0]["params"] == ks.greedy_predict(params, d)
+        preds = [ks.membership_predicate(params.spec)]
+        con = ks.predict(params, d, beam_width=3, predicates=preds)
+        assert [c["params"] for c in con] == [t["params"] for t in top]
+        for c in con:
+            assert ks.validate(params.spec, d, c["params"], preds) is None
+
+
+def test_python_predicate(ks, params, oracle):
+    """test_smoke.py:109-117: opaque callable, evaluated by the host hook."""
+    keep8 = ks.predicate("chunk8", lambda d, partial: partial.get("chunk_size", 8) == 8)
+    for d in descs(oracle, 8, 2):
+        out = ks.predict(params, d, beam_width=4, predicates=[keep8])
+        assert out
+        for e in out:
+            assert e["params"]["chunk_size"] == 8
+        # same search with the equivalent device mask in the oracle
+        vals = oracle.values
+        mask = [[1] * len(v) for v in vals]
+        p = oracle.names.index("chunk_size")
+        mask[p] = [1 if v == 8 else 0 for v in vals[p]]
+        a = oracle.beam(tok_of(oracle, d), 4, preds=[oracle.mask(mask)])
+        if a["min_gap"][0] >= 1e-4:
+            got = [[e["params"][n] for n in oracle.names] for e in out]
+            want = [[vals[t][tok] for t, tok in enumerate(row)] for row in a["tokens"][0][:a["count"][0]]]
+            assert got == want
+
+
+def test_predict_matches_oracle_with_typed_and_opaque_predicates(ks, params, oracle):
+    names = oracle.names
+    bud = ks.resource_budget_predicate({n: 1.0 for n in names}, 30.0, "bud")
+    no_small_chunks = ks.predicate("chunk>=4", lambda d, p: p.get("chunk_size", 64) >= 4)
+    ds = descs(oracle, 64, 3)
+    res = ks.predict_batch(params, ds, beam_width=5,
+                           predicates=[ks.membership_predicate(params.spec), no_small_chunks, bud])
+    vals = oracle.values
+    mask = [[1] * len(v) for v in vals]
+    p = names.index("chunk_size")
+    mask[p] = [1 if v >= 4 else 0 for v in vals[p]]
+    opreds = [oracle.membership(), oracle.mask(mask), oracle.budget({n: 1.0 for n in names}, 30.0)]
+    checked = 0
+    for d, r in zip(ds, res):
+        a = oracle.beam(tok_of(oracle, d), 5, preds=opreds)
+        if a["min_gap"][0] < 1e-4:
+            continue
+        checked += 1
+        if a["status"][0] == 1:
+            assert isinstance(r, dict) and r["exhausted"] and r["step"] == a["fail_step"][0]
+            assert r["predicate"] == ["membership:ConvAsm1x1U", "chunk>=4", "bud"][a["fail_pred"][0]]
+            continue
+        got = [[e["params"][n] for n in names] for e in r]
+        want = [[vals[t][tok] for t, tok in enumerate(row)] for row in a["tokens"][0][:a["count"][0]]]
+        assert got == want
+        for e, lp in zip(r, a["log_prob"][0]):
+            assert math.isclose(e["log_prob"], lp, rel_tol=1e-4, abs_tol=1e-4)
+    assert checked >= 48
+
+
+def test_predict_batch_equals_single_predict(ks, params, oracle):
+    ds = descs(oracle, 20, 4)
+    batch = ks.predict_batch(params, ds, beam_width=5)
+    for d, b in zip(ds, batch):
+        assert b == ks.predict(params, d, beam_width=5)
+
+
+def test_exhaustion_raises_naming_the_predicate(ks, params, oracle):
+    """cli_test.cpp:189-194 / decoding_test.cpp:300-318 through the binding."""
+    tight = ks.resource_budget_predicate({"read_size": 1.0}, 0.5, "budget")
+    with pytest.raises(ks.KernelseerError, match="budget"):
+        ks.predict(params, descs(oracle, 1, 5)[0], beam_width=3, predicates=[tight])
+
+
+def test_topk_metrics_against_oracle(ks, params, oracle):
+    """eval.cpp:74-152 semantics (best-matching beam, any-of-k perfect)."""
+    ds = descs(oracle, 40, 6)
+    samples, truths = [], []
+    rng = np.random.default_rng(7)
+    for d in ds:
+        truth = [int(rng.integers(len(v))) for v in oracle.values]
+        truths.append(truth)
+        samples.append(ks.Sample(d, {n: oracle.values[i][t] for i, (n, t) in enumerate(zip(oracle.names, truth))},
+                                 "ConvAsm1x1U"))
+    reps = ks.topk_metrics(params, samples, [1, 4], threads=2)
+    assert [r["beam_width"] for r in reps] == [1, 4]
+    assert reps[0]["perfect_prediction"] <= reps[1]["perfect_prediction"] + 1e-9
+    for rep, k in zip(reps, [1, 4]):
+        tok = np.concatenate([tok_of(oracle, d) for d in ds])
+        a = oracle.beam(tok, k)
+        if (a["min_gap"] < 1e-4).any():
+            continue  # metrics depend on every config's beams
+        T = oracle.T
+        per = np.zeros(T)
+        perfect = 0
+        for b in range(len(ds)):
+            best, bm, hit = None, -1, False
+            for j in range(a["count"][b]):
+                m = sum(int(a["tokens"][b, j, p] == truths[b][p]) for p in range(T))
+                hit |= m == T
+                if m > bm:
+                    bm, best = m, a["tokens"][b, j]
+            per += np.array([best[p] == truths[b][p] for p in range(T)])
+            perfect += hit
+        assert math.isclose(rep["average_accuracy"], float(np.mean(per / len(ds) * 100)), rel_tol=1e-9)
+        assert math.isclose(rep["perfect_prediction"], 100.0 * perfect / len(ds), rel_tol=1e-9)
+
+
+def test_engine_precision_switch(ks, oracle):
+    p = ks.load_checkpoint(CKPT)
+    d = descs(oracle, 1, 8)[0]
+    ref = ks.predict(p, d, beam_width=5)
+    p.set_engine(0, "fp32")
+    assert [e["params"] for e in ks.predict(p, d, beam_width=5)] == [e["params"] for e in ref]
