@@ -142,14 +142,18 @@ struct BeamArgs {
     const int* host_rej;       // [B*H_cur][V] first rejecting host predicate (or -1); may be null
 };
 
-// fp16 split with an exact power-of-two scale on the residual so that it
-// stays in the normal fp16 range: x ~= hi + lo * 2^-kSplitShift.
-constexpr int kSplitShift = 11;
+// fp16 hi/lo split of an fp32 value, pre-scaled by 2^8 (exact) so that the
+// residual of values down to ~5e-4 stays in the normal fp16 range:
+//   x * 2^8 ~= hi + lo   (22 significant bits)
+// Weights are split the same way at pack time, so one fp32 accumulator
+// collects hi*hi + hi*lo + lo*hi = 2^16 * x.w and the epilogue scales by 2^-16.
+constexpr float kSplitScale = 256.0f;
+constexpr float kSplitUnscale = 1.0f / 65536.0f;
 
 __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
-    hi = __float2half_rn(x);
-    const float r = x - __half2float(hi);          // exact in fp32
-    lo = __float2half_rn(r * 2048.0f);
+    const float xs = x * kSplitScale;
+    hi = __float2half_rn(xs);
+    lo = __float2half_rn(xs - __half2float(hi));   // residual exact in fp32
 }
 
 __device__ __forceinline__ void store_split_h(const LstmArgs& p, long long idx, float h) {

@@ -154,7 +154,7 @@ struct ks_engine {
     std::vector<double> prof_flops;
     double prof_ms = 0.0, prof_useful = 0.0;
     int64_t prof_n = 0;
-    int tc_units = 32;
+    int tc_units = 64;
     int num_sms = 148;
 };
 
@@ -209,7 +209,7 @@ ks_status pack_lstm(const HostTensors& ht, const std::string& prefix, int rows, 
         for (int u = 0; u < Hp; ++u)
             for (int g = 0; g < 4; ++g) {
                 const float w = (r >= 0 && u < H) ? W[g][(size_t)r * H + u] : 0.0f;
-                if (std::fabs(w) > 60000.0f)
+                if (std::fabs(w) > 200.0f)
                     return set_error(KS_ERR_UNSUPPORTED, "weight magnitude exceeds the fp16 split range");
                 Wf[(size_t)k * 4 * Hp + u * 4 + g] = w;
                 // tensor-core layout: N index n = blk*4U + g*U + u%U (blk = u/U), K-major
@@ -218,11 +218,11 @@ ks_status pack_lstm(const HostTensors& ht, const std::string& prefix, int rows, 
                     const __nv_bfloat16 hb = __float2bfloat16_rn(w);
                     std::memcpy(&Whi[n * K + k], &hb, 2);
                     Wlo[n * K + k] = __float2half_rn(0.0f);
-                } else {
-                    const __half hi = __float2half_rn(w);
-                    const float res = w - __half2float(hi);
+                } else {  // same 2^8-scaled split as split_f16 (ks_common.cuh)
+                    const float ws = w * 256.0f;
+                    const __half hi = __float2half_rn(ws);
                     Whi[n * K + k] = hi;
-                    Wlo[n * K + k] = __float2half_rn(res * 2048.0f);
+                    Wlo[n * K + k] = __float2half_rn(ws - __half2float(hi));
                 }
             }
     }

@@ -5,9 +5,10 @@
 //   c' = sig(f) c_prev[parent(row)] + sig(i) tanh(g);  h' = sig(o) tanh(c')
 //
 // Precision modes (include/ks_b200.h):
-//   F16X3: A = A_hi + 2^-11 A_lo and W = W_hi + 2^-11 W_lo (fp16 planes). Two
-//          TMEM accumulators per tile: D1 = A_hi.W_hi, D2 = A_hi.W_lo + A_lo.W_hi;
-//          gates = D1 + 2^-11 D2 (the dropped A_lo.W_lo term is 2^-22 relative).
+//   F16X3: 2^8 A = A_hi + A_lo and 2^8 W = W_hi + W_lo (fp16 planes, ~22-bit
+//          operands).  One TMEM accumulator collects A_hi.W_hi + A_hi.W_lo +
+//          A_lo.W_hi (three MMAs per K step); gates = 2^-16 D.  The dropped
+//          A_lo.W_lo term is ~2^-22 relative.
 //   BF16:  one bf16 MMA per K step (A_hi / W_hi planes hold bf16).
 //
 // Structure: persistent CTAs (one per SM), 384 threads:
@@ -133,7 +134,7 @@ struct TcCfg {
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;          // one plane
     static constexpr int B_BYTES = BN * TC_BK * 2;
     static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
-    static constexpr int ACC_COLS = (SPLIT ? 2 : 1) * BN;      // fp32 TMEM columns per accumulator set
+    static constexpr int ACC_COLS = BN;                        // fp32 TMEM columns per accumulator
     static constexpr int ACC_STAGES = 512 / ACC_COLS >= 2 ? 2 : 1;
     static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
@@ -244,7 +245,6 @@ __global__ void __launch_bounds__(384, 1)
                 tc::mbar_wait(tc::smem_u32(&bars[2 * S + AS + acc]), acc_phase ^ 1);
                 tc::fence_after();
                 const uint32_t d1 = tmem_base + acc * Cfg::ACC_COLS;
-                const uint32_t d2 = d1 + Cfg::BN;
                 for (int kb = 0; kb < pr.k_blocks; ++kb) {
                     tc::mbar_wait(tc::smem_u32(&bars[stage]), phase);
                     tc::fence_after();
@@ -259,9 +259,9 @@ __global__ void __launch_bounds__(384, 1)
                         tc::mma_f16(d1, tc::smem_desc(a0 + koff), tc::smem_desc(b0 + koff), Cfg::IDESC,
                                     acc_flag);
                         if (SPLIT) {
-                            tc::mma_f16(d2, tc::smem_desc(a0 + koff), tc::smem_desc(bl + koff),
-                                        Cfg::IDESC, acc_flag);
-                            tc::mma_f16(d2, tc::smem_desc(al + koff), tc::smem_desc(b0 + koff),
+                            tc::mma_f16(d1, tc::smem_desc(a0 + koff), tc::smem_desc(bl + koff),
+                                        Cfg::IDESC, 1u);
+                            tc::mma_f16(d1, tc::smem_desc(al + koff), tc::smem_desc(b0 + koff),
                                         Cfg::IDESC, 1u);
                         }
                     }
@@ -306,12 +306,8 @@ __global__ void __launch_bounds__(384, 1)
             for (int c = 0; c < HU / 8; ++c) {
                 const int uc = half * HU + c * 8;  // unit offset within the tile
                 float g[4][8];
-                float g2[4][8];
 #pragma unroll
-                for (int gt = 0; gt < 4; ++gt) {
-                    tc::tmem_ld8(tbase + gt * UNITS + uc, g[gt]);
-                    if (SPLIT) tc::tmem_ld8(tbase + Cfg::BN + gt * UNITS + uc, g2[gt]);
-                }
+                for (int gt = 0; gt < 4; ++gt) tc::tmem_ld8(tbase + gt * UNITS + uc, g[gt]);
                 tc::tmem_wait_ld();
                 if (valid) {
                     const int u0 = nt * UNITS + uc;
@@ -336,13 +332,8 @@ __global__ void __launch_bounds__(384, 1)
                     float hv[8], cv[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        float gi = g[0][j], gf = g[1][j], go = g[2][j], gc = g[3][j];
-                        if (SPLIT) {
-                            gi = fmaf(g2[0][j], 1.0f / 2048.0f, gi);
-                            gf = fmaf(g2[1][j], 1.0f / 2048.0f, gf);
-                            go = fmaf(g2[2][j], 1.0f / 2048.0f, go);
-                            gc = fmaf(g2[3][j], 1.0f / 2048.0f, gc);
-                        }
+                        const float sc = SPLIT ? kSplitUnscale : 1.0f;
+                        float gi = g[0][j] * sc, gf = g[1][j] * sc, go = g[2][j] * sc, gc = g[3][j] * sc;
                         gi += gb[0][j];
                         gf += gb[1][j];
                         go += gb[2][j];
