@@ -140,6 +140,7 @@ struct BeamArgs {
     int* out_status;
     int cands_per_warp;        // smem capacity per warp (entries)
     const int* host_rej;       // [B*H_cur][V] first rejecting host predicate (or -1); may be null
+    int split_mode;            // selects the kernel instantiation only
 };
 
 // fp16 hi/lo split of an fp32 value, pre-scaled by 2^8 (exact) so that the

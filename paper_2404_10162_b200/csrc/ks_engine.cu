@@ -882,6 +882,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         b.out_fail_step = o_fstep;
         b.cands_per_warp = cpw;
         b.host_rej = host_rej;
+        b.split_mode = aa.split_mode;
         int warps = 8;
         while (warps > 1 && beam_smem_bytes(Hd, V, warps, cpw) > (size_t)E.beam_smem_max) --warps;
         const size_t smem = beam_smem_bytes(Hd, V, warps, cpw);

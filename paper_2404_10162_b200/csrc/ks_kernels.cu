@@ -18,6 +18,7 @@
 //   greedy_decode         src/decoding.cpp:107-124 (strict '>' argmax)
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "ks_common.cuh"
 
@@ -149,9 +150,9 @@ __global__ void __launch_bounds__(256) lstm_step_simt(LstmArgs a0, LstmArgs a1) 
 // FIRST (position 0, one row per config): also computes and stores u.
 // ---------------------------------------------------------------------------
 template <int SPLIT>
-__device__ __forceinline__ void store4(const AttnArgs& p, long long idx, float4 v) {
+__device__ __forceinline__ void store4p(float* A, __half* A_hi, __half* A_lo, long long idx, float4 v) {
     if (SPLIT == 0) {
-        *reinterpret_cast<float4*>(p.A + idx) = v;
+        *reinterpret_cast<float4*>(A + idx) = v;
     } else if (SPLIT == 1) {
         __half hi[4], lo[4];
         split_f16(v.x, hi[0], lo[0]);
@@ -163,16 +164,20 @@ __device__ __forceinline__ void store4(const AttnArgs& p, long long idx, float4 
         h.y = (uint32_t)__half_as_ushort(hi[2]) | ((uint32_t)__half_as_ushort(hi[3]) << 16);
         l.x = (uint32_t)__half_as_ushort(lo[0]) | ((uint32_t)__half_as_ushort(lo[1]) << 16);
         l.y = (uint32_t)__half_as_ushort(lo[2]) | ((uint32_t)__half_as_ushort(lo[3]) << 16);
-        *reinterpret_cast<uint2*>(p.A_hi + idx) = h;
-        *reinterpret_cast<uint2*>(p.A_lo + idx) = l;
+        *reinterpret_cast<uint2*>(A_hi + idx) = h;
+        *reinterpret_cast<uint2*>(A_lo + idx) = l;
     } else {
         __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
         __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
         uint2 h;
         h.x = *reinterpret_cast<uint32_t*>(&a);
         h.y = *reinterpret_cast<uint32_t*>(&b);
-        *reinterpret_cast<uint2*>(p.A_hi + idx) = h;
+        *reinterpret_cast<uint2*>(A_hi + idx) = h;
     }
+}
+template <int SPLIT>
+__device__ __forceinline__ void store4(const AttnArgs& p, long long idx, float4 v) {
+    store4p<SPLIT>(p.A, p.A_hi, p.A_lo, idx, v);
 }
 
 template <int ND, int SPLIT, bool FIRST>
@@ -263,13 +268,97 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
     }
 }
 
+// Config-per-warp variant for positions > 0: the H rows of a config share
+// a_t, so each a_t chunk is loaded once and reused for all rows (G at a time).
+template <int ND, int SPLIT>
+__global__ void __launch_bounds__(256) attention_cfg_t(AttnArgs p) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int H = p.H_rows;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if ((long long)b * H >= p.M) return;
+    const int Kd = p.NA2 + p.NS;
+    const float* act = p.act + (long long)b * kTin * p.NA2;
+    constexpr int G = 4;
+    for (int i0 = 0; i0 < H; i0 += G) {
+        const int ng = H - i0 < G ? H - i0 : G;
+        float al[G][kTin];
+#pragma unroll
+        for (int ii = 0; ii < G; ++ii) {
+            if (ii >= ng) break;
+            const int r = b * H + i0 + ii;
+            const int par = p.parent ? p.parent[r] : r;
+            const float* sh = (p.h_prev != nullptr && par >= 0) ? p.h_prev + (long long)par * p.ldh : nullptr;
+            float sd[ND > 0 ? ND : 1];
+#pragma unroll
+            for (int d = 0; d < ND; ++d) sd[d] = 0.0f;
+            for (int c = lane; c < p.NS / 4; c += 32) {
+                const float4 v = sh ? *reinterpret_cast<const float4*>(sh + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], p.Ws[(4 * c + e) * ND + d], sd[d]);
+                store4<SPLIT>(p, (long long)r * Kd + p.NA2 + 4 * c, v);
+            }
+            if (ND == 0) continue;
+#pragma unroll
+            for (int d = 0; d < ND; ++d) sd[d] = warp_sum_f(sd[d]);
+            float mx = -FLT_MAX;
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) {
+                float v = p.bo;
+#pragma unroll
+                for (int d = 0; d < ND; ++d)
+                    v = fmaf(tanhf(sd[d] + p.uatt[((long long)b * kTin + t) * ND + d]), p.wo[d], v);
+                al[ii][t] = v;
+                mx = fmaxf(mx, v);
+            }
+            float sum = 0.0f;
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) {
+                al[ii][t] = expf(al[ii][t] - mx);
+                sum += al[ii][t];
+            }
+            const float inv = 1.0f / sum;
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) al[ii][t] *= inv;
+        }
+        if (ND == 0) continue;
+        for (int c = lane; c < p.NA2 / 4; c += 32) {
+            float4 at[kTin];
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) at[t] = *reinterpret_cast<const float4*>(act + t * p.NA2 + 4 * c);
+#pragma unroll
+            for (int ii = 0; ii < G; ++ii) {
+                if (ii >= ng) break;
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < kTin; ++t) {
+                    acc.x = fmaf(al[ii][t], at[t].x, acc.x);
+                    acc.y = fmaf(al[ii][t], at[t].y, acc.y);
+                    acc.z = fmaf(al[ii][t], at[t].z, acc.z);
+                    acc.w = fmaf(al[ii][t], at[t].w, acc.w);
+                }
+                store4<SPLIT>(p, (long long)(b * H + i0 + ii) * Kd + 4 * c, acc);
+            }
+        }
+    }
+}
+
 template <int ND, int SPLIT>
 void launch_attention_nd(const AttnArgs& p, bool first, cudaStream_t s) {
-    const unsigned grid = (unsigned)((p.M + 7) / 8);
-    if (first)
-        attention_pack_t<ND, SPLIT, true><<<grid, 256, 0, s>>>(p);
-    else
-        attention_pack_t<ND, SPLIT, false><<<grid, 256, 0, s>>>(p);
+    static const bool per_cfg = [] {
+        const char* e = std::getenv("KS_ATTN_PER_ROW");
+        return !(e && std::atoi(e) != 0);
+    }();
+    if (first) {
+        attention_pack_t<ND, SPLIT, true><<<(unsigned)((p.M + 7) / 8), 256, 0, s>>>(p);
+    } else if (per_cfg && p.H_rows > 1) {
+        const int C = p.M / p.H_rows;
+        attention_cfg_t<ND, SPLIT><<<(unsigned)((C + 7) / 8), 256, 0, s>>>(p);
+    } else {
+        attention_pack_t<ND, SPLIT, false><<<(unsigned)((p.M + 7) / 8), 256, 0, s>>>(p);
+    }
 }
 
 template <int SPLIT>
@@ -320,8 +409,11 @@ __device__ bool pred_accepts(const BeamArgs& a, const PosMeta& m, const DevPred&
                              unsigned long long key, int pos, const long long* desc_b) {
     switch (q.kind) {
         case 1: {  // MASK
+            // Every earlier token of a live hypothesis already passed this (per-token)
+            // predicate at its own position, so only the new token needs checking --
+            // unless the predicate is full-sequence-only and runs just once, at the end.
             const unsigned char* allowed = a.pred_bytes + q.allowed_off;
-            for (int i = 0; i <= pos; ++i)
+            for (int i = q.full ? 0 : pos; i <= pos; ++i)
                 if (!allowed[m.value_offset[i] + key_token(key, m, i)]) return false;
             return true;
         }
@@ -347,10 +439,10 @@ __device__ bool pred_accepts(const BeamArgs& a, const PosMeta& m, const DevPred&
             }
             return prod <= (__int128)q.limit;
         }
-        case 4: {  // DIVIDES
+        case 4: {  // DIVIDES (per-token like MASK: earlier tokens already passed)
             for (int t = 0; t < q.n_terms; ++t) {
                 const int pp = a.term_pos[q.terms_off + t];
-                if (pp < 0 || pp > pos) continue;
+                if (pp < 0 || pp > pos || (!q.full && pp != pos)) continue;
                 const long long v = a.values[m.value_offset[pp] + key_token(key, m, pp)];
                 if (v <= 0 || desc_b == nullptr) return false;
                 if (desc_b[a.term_field[q.terms_off + t]] % v != 0) return false;
@@ -407,7 +499,7 @@ __device__ __forceinline__ int src_lane(int v) {
     return lane;
 }
 
-template <int VP>
+template <int VP, int SPLIT>
 __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int WS = VP == 4 ? 12 : VP + 4;  // padded W row: conflict-free 128-bit loads
@@ -624,25 +716,32 @@ size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp) {
     return (((size_t)NS * WS * 4 + 15) & ~(size_t)15) + (size_t)warps * cands_per_warp * 28;
 }
 
-bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
+template <int SPLIT>
+bool launch_beam_split(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
     const int V = m.vsize[a.pos];
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(beam_step_t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(beam_step_t<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(beam_step_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(beam_step_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<4, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<8, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<16, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<32, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
     if (V <= 4)
-        beam_step_t<4><<<grid, warps * 32, smem, s>>>(a, m);
+        beam_step_t<4, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
     else if (V <= 8)
-        beam_step_t<8><<<grid, warps * 32, smem, s>>>(a, m);
+        beam_step_t<8, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
     else if (V <= 16)
-        beam_step_t<16><<<grid, warps * 32, smem, s>>>(a, m);
+        beam_step_t<16, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
     else
-        beam_step_t<32><<<grid, warps * 32, smem, s>>>(a, m);
+        beam_step_t<32, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
     return cudaGetLastError() == cudaSuccess;
+}
+
+bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
+    if (a.split_mode == 0) return launch_beam_split<0>(a, m, warps, smem, grid, s);
+    if (a.split_mode == 1) return launch_beam_split<1>(a, m, warps, smem, grid, s);
+    return launch_beam_split<2>(a, m, warps, smem, grid, s);
 }
 
 }  // namespace ksb
