@@ -141,6 +141,9 @@ struct BeamArgs {
     int cands_per_warp;        // smem capacity per warp (entries)
     const int* host_rej;       // [B*H_cur][V] first rejecting host predicate (or -1); may be null
     int split_mode;            // selects the kernel instantiation only
+    int n_values;              // staged-table sizes (shared memory)
+    int n_terms;
+    int n_bytes;
 };
 
 // fp16 hi/lo split of an fp32 value, pre-scaled by 2^8 (exact) so that the

@@ -30,7 +30,7 @@ __global__ void lstm_step_simt(LstmArgs a0, LstmArgs a1);
 bool launch_attention(const AttnArgs& p, bool first, cudaStream_t s);
 __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long long* key,
                           int* status, int* fail_pred, int* fail_step);
-size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp);
+size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tables);
 bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s);
 // tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
@@ -492,6 +492,8 @@ namespace {
 
 struct PredDev {
     int n = 0;
+    int n_terms = 0;
+    int n_bytes = 0;
     bool needs_desc = false;
     bool has_host = false;
     ks_host_pred_fn hook = nullptr;
@@ -550,6 +552,8 @@ ks_status upload_preds(ks_engine& E, const ks_pred* preds, int n, PredDev& pd) {
         dp.push_back(d);
     }
     pd.n = n;
+    pd.n_terms = (int)tpos.size();
+    pd.n_bytes = (int)bytes.size();
     ks_status st;
     if ((st = upload(E.preds, dp.data(), dp.size() * sizeof(DevPred)))) return st;
     if ((st = upload(E.pbytes, bytes.data(), bytes.size()))) return st;
@@ -883,9 +887,14 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         b.cands_per_warp = cpw;
         b.host_rej = host_rej;
         b.split_mode = aa.split_mode;
+        b.n_values = (int)E.out_values.size();
+        b.n_terms = pd.n_terms;
+        b.n_bytes = pd.n_bytes;
+        const size_t tables = (size_t)b.n_values * 8 + (size_t)b.n_terms * 16 + (size_t)pd.n * sizeof(DevPred) +
+                              (size_t)b.n_bytes + 16;
         int warps = 8;
-        while (warps > 1 && beam_smem_bytes(Hd, V, warps, cpw) > (size_t)E.beam_smem_max) --warps;
-        const size_t smem = beam_smem_bytes(Hd, V, warps, cpw);
+        while (warps > 1 && beam_smem_bytes(Hd, V, warps, cpw, tables) > (size_t)E.beam_smem_max) --warps;
+        const size_t smem = beam_smem_bytes(Hd, V, warps, cpw, tables);
         if (smem > (size_t)E.beam_smem_max)
             return set_error(KS_ERR_UNSUPPORTED, "beam width x vocabulary too large for the beam kernel");
         // persistent: the head weights are staged into shared memory once per CTA

@@ -36,6 +36,11 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
 __device__ __forceinline__ double warp_max_d(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -271,7 +276,7 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
 // Config-per-warp variant for positions > 0: the H rows of a config share
 // a_t, so each a_t chunk is loaded once and reused for all rows (G at a time).
 template <int ND, int SPLIT>
-__global__ void __launch_bounds__(256) attention_cfg_t(AttnArgs p) {
+__global__ void __launch_bounds__(256, 3) attention_cfg_t(AttnArgs p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = p.H_rows;
     const int b = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -291,6 +296,7 @@ __global__ void __launch_bounds__(256) attention_cfg_t(AttnArgs p) {
             float sd[ND > 0 ? ND : 1];
 #pragma unroll
             for (int d = 0; d < ND; ++d) sd[d] = 0.0f;
+#pragma unroll 4
             for (int c = lane; c < p.NS / 4; c += 32) {
                 const float4 v = sh ? *reinterpret_cast<const float4*>(sh + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -324,6 +330,7 @@ __global__ void __launch_bounds__(256) attention_cfg_t(AttnArgs p) {
             for (int t = 0; t < kTin; ++t) al[ii][t] *= inv;
         }
         if (ND == 0) continue;
+#pragma unroll 2
         for (int c = lane; c < p.NA2 / 4; c += 32) {
             float4 at[kTin];
 #pragma unroll
@@ -345,15 +352,98 @@ __global__ void __launch_bounds__(256) attention_cfg_t(AttnArgs p) {
     }
 }
 
+// CTA-per-config variant (positions > 0): 4 warps; warp w scores rows w, w+4,
+// ... (s . W_s, energies, softmax -> alpha in shared memory), then every
+// thread owns a float4 column of a_t, loads its 7 steps once and writes the
+// context of all H rows of the config.
+template <int ND, int SPLIT>
+__global__ void __launch_bounds__(128) attention_cta_t(AttnArgs p) {
+    constexpr int kMaxRows = 64;
+    __shared__ float alpha[kMaxRows][kTin];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int H = p.H_rows;
+    const int b = blockIdx.x;
+    const int Kd = p.NA2 + p.NS;
+    for (int i = warp; i < H; i += 4) {
+        const int r = b * H + i;
+        const int par = p.parent ? p.parent[r] : r;
+        const float* sh = (p.h_prev != nullptr && par >= 0) ? p.h_prev + (long long)par * p.ldh : nullptr;
+        float sd[ND > 0 ? ND : 1];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) sd[d] = 0.0f;
+#pragma unroll 4
+        for (int c = lane; c < p.NS / 4; c += 32) {
+            const float4 v = sh ? *reinterpret_cast<const float4*>(sh + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+#pragma unroll
+                for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], p.Ws[(4 * c + e) * ND + d], sd[d]);
+            store4<SPLIT>(p, (long long)r * Kd + p.NA2 + 4 * c, v);
+        }
+        if (ND == 0) continue;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) sd[d] = warp_sum_f(sd[d]);
+        float e[kTin];
+        float mx = -FLT_MAX;
+#pragma unroll
+        for (int t = 0; t < kTin; ++t) {
+            float v = p.bo;
+#pragma unroll
+            for (int d = 0; d < ND; ++d)
+                v = fmaf(tanhf(sd[d] + p.uatt[((long long)b * kTin + t) * ND + d]), p.wo[d], v);
+            e[t] = v;
+            mx = fmaxf(mx, v);
+        }
+        float sum = 0.0f;
+#pragma unroll
+        for (int t = 0; t < kTin; ++t) {
+            e[t] = expf(e[t] - mx);
+            sum += e[t];
+        }
+        const float inv = 1.0f / sum;
+        if (lane < kTin) {
+            float my = e[0];
+#pragma unroll
+            for (int t = 1; t < kTin; ++t)
+                if (lane == t) my = e[t];
+            alpha[i][lane] = my * inv;
+        }
+    }
+    if (ND == 0) return;
+    __syncthreads();
+    const float* act = p.act + (long long)b * kTin * p.NA2;
+    for (int c = threadIdx.x; c < p.NA2 / 4; c += blockDim.x) {
+        float4 at[kTin];
+#pragma unroll
+        for (int t = 0; t < kTin; ++t) at[t] = *reinterpret_cast<const float4*>(act + t * p.NA2 + 4 * c);
+        for (int i = 0; i < H; ++i) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) {
+                const float al = alpha[i][t];
+                acc.x = fmaf(al, at[t].x, acc.x);
+                acc.y = fmaf(al, at[t].y, acc.y);
+                acc.z = fmaf(al, at[t].z, acc.z);
+                acc.w = fmaf(al, at[t].w, acc.w);
+            }
+            store4<SPLIT>(p, (long long)(b * H + i) * Kd + 4 * c, acc);
+        }
+    }
+}
+
 template <int ND, int SPLIT>
 void launch_attention_nd(const AttnArgs& p, bool first, cudaStream_t s) {
-    static const bool per_cfg = [] {
-        const char* e = std::getenv("KS_ATTN_PER_ROW");
-        return !(e && std::atoi(e) != 0);
+    // KS_ATTN_MODE: 0 = CTA per config (default), 1 = warp per row, 2 = warp per config
+    static const int mode = [] {
+        const char* e = std::getenv("KS_ATTN_MODE");
+        return e ? std::atoi(e) : 0;
     }();
     if (first) {
         attention_pack_t<ND, SPLIT, true><<<(unsigned)((p.M + 7) / 8), 256, 0, s>>>(p);
-    } else if (per_cfg && p.H_rows > 1) {
+    } else if (mode == 0 && p.H_rows > 1 && p.H_rows <= 64) {
+        attention_cta_t<ND, SPLIT><<<(unsigned)(p.M / p.H_rows), 128, 0, s>>>(p);
+    } else if (mode == 2 && p.H_rows > 1) {
         const int C = p.M / p.H_rows;
         attention_cfg_t<ND, SPLIT><<<(unsigned)((C + 7) / 8), 256, 0, s>>>(p);
     } else {
@@ -405,7 +495,43 @@ __device__ __forceinline__ int key_token(unsigned long long key, const PosMeta& 
     return (int)((key >> m.shift[i]) & ((1ull << m.bits[i]) - 1ull));
 }
 
-__device__ bool pred_accepts(const BeamArgs& a, const PosMeta& m, const DevPred& q,
+// Predicate programs and the output-value table, staged in shared memory once
+// per CTA (they are read for every candidate).
+struct PredTables {
+    const DevPred* preds;
+    const unsigned char* pred_bytes;
+    const int* term_pos;
+    const double* term_w;
+    const int* term_field;
+    const long long* values;
+};
+
+__device__ __forceinline__ size_t pred_tables_bytes(const BeamArgs& a) {
+    size_t n = (size_t)a.n_values * 8 + (size_t)a.n_terms * 8;
+    n += (size_t)a.n_preds * sizeof(DevPred);
+    n += (size_t)a.n_terms * 8 + (size_t)a.n_bytes;
+    return (n + 15) & ~(size_t)15;
+}
+
+__device__ PredTables stage_pred_tables(const BeamArgs& a, unsigned char* base) {
+    long long* values = reinterpret_cast<long long*>(base);
+    double* tw = reinterpret_cast<double*>(values + a.n_values);
+    DevPred* preds = reinterpret_cast<DevPred*>(tw + a.n_terms);
+    int* tpos = reinterpret_cast<int*>(preds + a.n_preds);
+    int* tfield = tpos + a.n_terms;
+    unsigned char* bytes = reinterpret_cast<unsigned char*>(tfield + a.n_terms);
+    for (int i = threadIdx.x; i < a.n_values; i += blockDim.x) values[i] = a.values[i];
+    for (int i = threadIdx.x; i < a.n_terms; i += blockDim.x) {
+        tw[i] = a.term_w[i];
+        tpos[i] = a.term_pos[i];
+        tfield[i] = a.term_field[i];
+    }
+    for (int i = threadIdx.x; i < a.n_preds; i += blockDim.x) preds[i] = a.preds[i];
+    for (int i = threadIdx.x; i < a.n_bytes; i += blockDim.x) bytes[i] = a.pred_bytes[i];
+    return PredTables{preds, bytes, tpos, tw, tfield, values};
+}
+
+__device__ bool pred_accepts(const PredTables& a, const PosMeta& m, const DevPred& q,
                              unsigned long long key, int pos, const long long* desc_b) {
     switch (q.kind) {
         case 1: {  // MASK
@@ -509,10 +635,12 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
         const int row = i / VP, v = i - row * VP;
         Wsh[row * WS + v] = v < V ? a.Wh[row * V + v] : 0.0f;
     }
+    const size_t wbytes = ((size_t)a.NS * WS * 4 + 15) & ~(size_t)15;
+    const PredTables tabs = stage_pred_tables(a, smem + wbytes);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    unsigned char* cbase = smem + ((size_t)(a.NS * WS * 4 + 15) & ~(size_t)15) + (size_t)warp * a.cands_per_warp * 28;
+    unsigned char* cbase = smem + wbytes + pred_tables_bytes(a) + (size_t)warp * a.cands_per_warp * 28;
     double* c_score = reinterpret_cast<double*>(cbase);
     double* c_lp = c_score + a.cands_per_warp;
     unsigned long long* c_key = reinterpret_cast<unsigned long long*>(c_lp + a.cands_per_warp);
@@ -559,6 +687,7 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
             }
             const float* h0 = a.h + r0 * a.NS;
             const float* h1 = h0 + a.NS;
+#pragma unroll 4
             for (int i = lane; i < a.NS; i += 32) {
                 const float x0 = live0 ? h0[i] : 0.0f;
                 const float x1 = live1 ? h1[i] : 0.0f;
@@ -590,13 +719,17 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                 }
                 last_live = j;
                 const long long r = r0 + jj;
-                // softmax in fp64, then log(max(p, 1e-300)) (nn.cpp:215-226, decoding.cpp:57-58)
-                const double l = lane < V ? (double)(lg[jj] + bias) : -INFINITY;
-                const double mx = warp_max_d(l);
-                const double ex = lane < V ? exp(l - mx) : 0.0;
-                const double sum = warp_sum_d(ex);
-                const double pr = ex / sum;
-                const double clp = a.lp_cur[r] + log(fmax(pr, 1e-300));
+                // log-softmax (nn.cpp:215-226) as (l - max) - log(sum exp), i.e. log(p)
+                // without underflow, floored at log(1e-300) like decoding.cpp:57-58; the
+                // hypothesis score accumulates in fp64
+                const float l = lane < V ? lg[jj] + bias : -INFINITY;
+                const float mx = warp_max_f(l);
+                const float ex = lane < V ? expf(l - mx) : 0.0f;
+                const float sum = warp_sum_f(ex);
+                const float lpt = fmaxf((l - mx) - logf(sum), -690.77552789821368f);
+                const double clp = a.lp_cur[r] + (double)lpt;
+                // greedy_decode's argmax of p == argmax of the logit (ties -> lowest index)
+                const double pr = (double)l;
                 const unsigned long long key = a.key_cur[r] | ((unsigned long long)lane << m.shift[a.pos]);
                 int rej = -1;
                 if (lane < V) {
@@ -606,10 +739,10 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                     const int qend = hrej >= 0 ? hrej : a.n_preds;
                     rej = hrej;
                     for (int q = 0; q < qend; ++q) {
-                        const DevPred pq = a.preds[q];
+                        const DevPred& pq = tabs.preds[q];
                         if (pq.kind == 5) continue;  // KS_PRED_HOST: decided by the hook
                         if (pq.full && !a.final_step) continue;
-                        if (!pred_accepts(a, m, pq, key, a.pos, desc_b)) {
+                        if (!pred_accepts(tabs, m, pq, key, a.pos, desc_b)) {
                             rej = q;
                             break;
                         }
@@ -648,10 +781,15 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
             continue;
         }
         const int ksel = n_alive < a.k ? n_alive : a.k;
-        for (int i = 0; i < ksel; ++i) {
-            double bs = -INFINITY;
-            unsigned long long bk = ~0ull;
-            int bc = -1;
+        // k rounds of warp argmax; each lane caches the best of its own candidates
+        // and only the lane that owned the winner rescans.
+        double bs = -INFINITY;
+        unsigned long long bk = ~0ull;
+        int bc = -1;
+        auto rescan = [&]() {
+            bs = -INFINITY;
+            bk = ~0ull;
+            bc = -1;
             for (int c = lane; c < nc; c += 32) {
                 if (c_meta[c] < 0) continue;
                 if (bc < 0 || better(c_score[c], c_key[c], bs, bk)) {
@@ -660,18 +798,24 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                     bc = c;
                 }
             }
+        };
+        rescan();
+        for (int i = 0; i < ksel; ++i) {
+            double ws = bs;
+            unsigned long long wk = bk;
+            int wc = bc;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                const double os = __shfl_xor_sync(0xffffffffu, bs, o);
-                const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-                if (oc >= 0 && (bc < 0 || better(os, ok, bs, bk))) {
-                    bs = os;
-                    bk = ok;
-                    bc = oc;
+                const double os = __shfl_xor_sync(0xffffffffu, ws, o);
+                const unsigned long long ok = __shfl_xor_sync(0xffffffffu, wk, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, wc, o);
+                if (oc >= 0 && (wc < 0 || better(os, ok, ws, wk))) {
+                    ws = os;
+                    wk = ok;
+                    wc = oc;
                 }
             }
-            if (lane == 0) {
+            if (wc == bc) {  // this lane owns the winner (candidate indices are unique)
                 const int meta = c_meta[bc];
                 const int j = meta >> 8, v = meta & 255;
                 const double clp = c_lp[bc];
@@ -688,9 +832,10 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                     a.slot_next[sl] = m.fb_offset[a.pos] + v;
                 }
                 c_meta[bc] = -1;
+                rescan();
             }
-            __syncwarp();
         }
+        __syncwarp();
         if (a.final_step) {
             for (int i = ksel + lane; i < a.k; i += 32) {
                 const long long o = (long long)b * a.k + i;
@@ -710,10 +855,11 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
     }
 }
 
-size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp) {
+size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tables) {
     const int VP = V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
     const int WS = VP == 4 ? 12 : VP + 4;
-    return (((size_t)NS * WS * 4 + 15) & ~(size_t)15) + (size_t)warps * cands_per_warp * 28;
+    return (((size_t)NS * WS * 4 + 15) & ~(size_t)15) + ((tables + 15) & ~(size_t)15) +
+           (size_t)warps * cands_per_warp * 28;
 }
 
 template <int SPLIT>
