@@ -39,9 +39,22 @@ sys.path.insert(0, ROOT)
 
 METRIC = "problem-configs/sec, constrained beam decode (beam=5)"
 UNIT = "configs/s"
-KERNEL = "ConvAsm1x1U"
-BEAM = 5
-CONFIGS_PER_GPU = 65536
+# BASELINE.json configs (cfg2 is the headline; the others are reported workloads)
+WORKLOADS = {
+    "cfg2": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=5, configs=65536, greedy=False,
+                 label="BASELINE config 2: constrained beam search beam=5"),
+    "cfg3": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=5, configs=131072, greedy=False,
+                 label="BASELINE config 3 per-GPU shard (1M configs / 8 GPUs): constrained beam search beam=5"),
+    "cfg5": dict(kernel="ConvAsmBwdWrW1x1", n_a=1024, n_s=1024, beam=16, configs=16384, greedy=False,
+                 label="BASELINE config 5 shape: n_a=n_s=1024 (1 layer; the reference has no layer count), "
+                       "beam=16, ConvAsmBwdWrW1x1"),
+    "cfg1": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=1, configs=1000, greedy=True,
+                 label="BASELINE config 1: greedy decode of 1k configs"),
+}
+W = WORKLOADS["cfg2"]
+KERNEL = W["kernel"]
+BEAM = W["beam"]
+CONFIGS_PER_GPU = W["configs"]
 BUDGET = 60.0
 
 
@@ -52,7 +65,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="f16x3", choices=["f16x3", "fp32", "bf16"])
-    ap.add_argument("--configs", type=int, default=CONFIGS_PER_GPU)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--configs", type=int, default=None, help="configs per GPU (default: the workload's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -67,10 +81,10 @@ def dist_env():
 def model_path():
     from paper_2404_10162_b200.synth import write_checkpoint
 
-    path = os.path.join(tempfile.gettempdir(), "ks_bench_attn_default.ckpt")
+    path = os.path.join(tempfile.gettempdir(), f"ks_bench_attn_{KERNEL}_{W['n_a']}_{W['n_s']}.ckpt")
     if not os.path.exists(path):
         tmp = path + f".{os.getpid()}"
-        write_checkpoint(tmp, KERNEL, "attn", 256, 512, 2, seed=1)
+        write_checkpoint(tmp, KERNEL, "attn", W["n_a"], W["n_s"], 2, seed=1)
         os.replace(tmp, path)
     return path
 
@@ -150,6 +164,18 @@ def reference_rate(path, tok, threads, seconds_target=15.0, max_configs=None):
     from oracle.oracle import RefModel
 
     r = RefModel(path)
+    if W["greedy"]:
+        n = min(len(tok), max(threads, 64))
+        t0 = time.perf_counter()
+        r.greedy(tok[:n], threads)
+        dt = time.perf_counter() - t0
+        n = int(min(len(tok), max(n, n / dt * seconds_target)))
+        if max_configs:
+            n = min(n, max_configs)
+        t0 = time.perf_counter()
+        r.greedy(tok[:n], threads)
+        dt = time.perf_counter() - t0
+        return n / dt, n, dt
     names = None
     line = "membership\nbudget bud %g " % BUDGET
     # param names from the checkpoint header
@@ -198,10 +224,10 @@ def run_reference_arm(args):
            "warmup": args.warmup, "ms_per_step": 1000.0 * tot_t / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"constrained beam search beam={BEAM}, {KERNEL} synthetic configs, "
-                                  "attn n_a=256 n_s=512 n_d=2 (bounded sample per step)",
+           "config": {"workload": f"{W['label']}, {KERNEL} synthetic configs, "
+                                  f"attn n_a={W['n_a']} n_s={W['n_s']} n_d=2 (bounded sample per step)",
                       "configs_per_step": int(tot_n / args.steps), "beam": BEAM,
-                      "predicates": f"membership + resource_budget(sum values <= {BUDGET:g})"},
+                      "predicates": "none (greedy)" if W["greedy"] else f"membership + resource_budget(sum values <= {BUDGET:g})"},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                             "sample": f"{int(tot_n / args.steps)} configs per step, "
                                       f"constrained_beam_search via parallel_stripes({threads})"},
@@ -232,7 +258,7 @@ def run_b200(args):
         head = f.read(8192).split(b"\n\n")[0].decode().split("\n")
     names = [l.split(": ", 1)[1].split(" = ")[0] for l in head if l.startswith("param.")]
     values = [[int(x) for x in l.split(" = ")[1].split(",")] for l in head if l.startswith("param.")]
-    preds = predicates(names, values)
+    preds = [] if W["greedy"] else predicates(names, values)
     T = eng.T
     stream = torch.cuda.current_stream()
     d_tok = torch.from_numpy(tok).cuda()
@@ -274,14 +300,21 @@ def run_b200(args):
         dist.barrier()
     value = B * world * args.steps / (ms / 1000.0)
 
-    # roofline of the dominant kernel (gate GEMM), timed on the engine stream
+    # roofline of the dominant kernel: the full-beam decoder gate GEMM launch
+    # (4.194 MFLOP per hypothesis-step x B*beam hypothesis-steps),
+    # CUDA events on the engine stream, averaged over those launches of one step
     eng.profile_reset(True)
     step()
     torch.cuda.synchronize()
     gemm_ms, gemm_n, useful = eng.profile()
+    each_ms, each_fl = eng.profile_launches()
     eng.profile_reset(False)
     bf16_peak, hbm_peak, peak_kind = peaks()
-    achieved = useful / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
+    top = each_fl >= each_fl.max() * 0.999
+    launch_ms = float(each_ms[top].mean())
+    launch_flops = float(each_fl[top].mean())
+    achieved = launch_flops / (launch_ms / 1000.0) / 1e12
+    step_achieved = useful / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
@@ -290,12 +323,18 @@ def run_b200(args):
         pass
 
     # end to end through the host C-ABI (pinned staging, copies in the timed region)
+    def host_call():
+        if W["greedy"]:
+            eng.greedy(tok)  # ks_greedy_batch: greedy_decode semantics (strict argmax of p)
+        else:
+            eng.beam(tok, BEAM, None, preds)
+
     for _ in range(max(1, args.warmup // 2)):
-        eng.beam(tok, BEAM, None, preds)
+        host_call()
     e2e_t = []
     for _ in range(max(2, args.steps // 2)):
         t0 = time.perf_counter()
-        eng.beam(tok, BEAM, None, preds)
+        host_call()
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = sum(e2e_t)
     if world > 1:
@@ -329,23 +368,26 @@ def run_b200(args):
             "dtype": {"f16x3": "f16x3 (fp16 hi/lo split, 3 MMAs, fp32 accumulate; fp32-grade)",
                       "fp32": "fp32", "bf16": "bf16 (fp32 accumulate)"}[args.precision],
             "data": "synthetic",
-            "config": {"workload": f"BASELINE config 2: constrained beam search beam={BEAM}, "
-                                   f"{B} synthetic {KERNEL} problem configs per GPU",
-                       "model": "attn n_a=256 n_s=512 n_d=2 (random init, reference checkpoint format)",
+            "config": {"workload": f"{W['label']}, {B} synthetic {KERNEL} problem configs per GPU",
+                       "model": f"attn n_a={W['n_a']} n_s={W['n_s']} n_d=2 (random init, reference checkpoint format)",
                        "configs_per_gpu": B, "beam": BEAM,
-                       "predicates": f"membership + resource_budget(sum values <= {BUDGET:g})",
+                       "predicates": "none (greedy)" if W["greedy"] else f"membership + resource_budget(sum values <= {BUDGET:g})",
                        "l2": "flushed (512 MiB write) before every timed step",
                        "parallelism": f"dp{world} (configs sharded by rank, no collective)"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "ks_beam_search_batch (host buffers)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
                          "frac": achieved / bf16_peak, "traffic": traffic,
-                         "kernel": "lstm_gemm_tc (gate GEMM + fused cell)" if args.precision != "fp32"
-                         else "lstm_step_simt",
+                         "kernel": ("lstm_gemm_tc (gate GEMM + fused LSTM cell), full-beam decoder launch"
+                                    if args.precision != "fp32" else "lstm_step_simt"),
                          "peak_kind": f"{peak_kind} bf16 dense (burst)",
-                         "useful_flops_per_step": useful, "gemm_launches_per_step": gemm_n,
-                         "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / (ms / args.steps),
-                         "mma_issued_tflops": achieved * mma_factor},
+                         "useful_flops_per_launch": launch_flops, "launch_ms": launch_ms,
+                         "launches_averaged": int(top.sum()),
+                         "mma_issued_tflops": achieved * mma_factor,
+                         "mma_issued_frac": achieved * mma_factor / bf16_peak,
+                         "all_gemm_launches": {"per_step": gemm_n, "ms_per_step": gemm_ms,
+                                               "useful_tflops": step_achieved,
+                                               "share_of_step": gemm_ms / (ms / args.steps)}},
             "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
@@ -356,7 +398,12 @@ def run_b200(args):
 
 
 def main():
+    global W, KERNEL, BEAM, CONFIGS_PER_GPU
     args = parse()
+    W = WORKLOADS[args.workload]
+    KERNEL, BEAM, CONFIGS_PER_GPU = W["kernel"], W["beam"], W["configs"]
+    if args.configs is None:
+        args.configs = CONFIGS_PER_GPU
     if args.impl == "reference":
         run_reference_arm(args)
     else:

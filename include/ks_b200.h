@@ -214,6 +214,9 @@ ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok, const int6
  * reset, and their count. */
 void ks_engine_profile_reset(ks_engine* eng, int32_t enable);
 double ks_engine_profile_gemm_ms(const ks_engine* eng, int64_t* launches, double* useful_flops);
+/* Per-launch view of the same profile: fills up to cap (ms, useful FLOPs)
+ * pairs in launch order and returns the number of launches recorded. */
+int64_t ks_engine_profile_launches(const ks_engine* eng, int64_t cap, double* ms, double* useful_flops);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,15 @@ struct kso_model {
     const double* att_o_b;
     const double* head_w[KSO_MAX_T];
     const double* head_b[KSO_MAX_T];
+    /* hybrid / hybrid-2 (models.cpp:296-371) */
+    int n_conv;
+    int conv_f[8], conv_k[8], conv_s[8];
+    const double* conv_w[8];
+    const double* conv_b[8];
+    const double* h2f_w[4];
+    const double* h2f_b[4];
+    const double* h2b_w[4];
+    const double* h2b_b[4];
 };
 
 /* ------------------------------------------------------------------------- */
@@ -195,6 +204,20 @@ kso_model* kso_load(const char* path) {
             m->n_d = atoi(val);
         } else if (!strcmp(key, "decoder_cell_size")) {
             m->cell = atoi(val);
+        } else if (!strcmp(key, "conv_layers")) {
+            const char* q = val;
+            m->n_conv = 0;
+            while (*q && m->n_conv < 8) {
+                int f, k, st;
+                if (sscanf(q, "%d,%d,%d", &f, &k, &st) != 3) break;
+                m->conv_f[m->n_conv] = f;
+                m->conv_k[m->n_conv] = k;
+                m->conv_s[m->n_conv] = st;
+                m->n_conv++;
+                const char* semi = strchr(q, ';');
+                if (!semi) break;
+                q = semi + 1;
+            }
         } else if (!strncmp(key, "input_vocab.", 12)) {
             for (int fi = 0; fi < KSO_T_IN; ++fi)
                 if (!strcmp(key + 12, fields[fi])) {
@@ -317,8 +340,21 @@ kso_model* kso_load(const char* path) {
     } else if (m->variant == 0) {
         bad |= resolve_lstm(m, "encoder", m->enc_f_w, m->enc_f_b);
         bad |= resolve_lstm(m, "decoder", m->dec_w, m->dec_b);
+    } else if (m->variant == 3 || m->variant == 4) {
+        bad |= resolve_lstm(m, "bilstm1.fwd", m->enc_f_w, m->enc_f_b);
+        bad |= resolve_lstm(m, "bilstm1.bwd", m->enc_b_w, m->enc_b_b);
+        bad |= resolve_lstm(m, "bilstm2.fwd", m->h2f_w, m->h2f_b);
+        bad |= resolve_lstm(m, "bilstm2.bwd", m->h2b_w, m->h2b_b);
+        for (int i = 0; i < m->n_conv && !bad; ++i) {
+            char name[64];
+            const kso_tensor_t* t;
+            snprintf(name, sizeof name, "conv.%d.filters", i);
+            if ((t = find_tensor(m, name))) m->conv_w[i] = t->data; else bad = 1;
+            snprintf(name, sizeof name, "conv.%d.bias", i);
+            if ((t = find_tensor(m, name))) m->conv_b[i] = t->data; else bad = 1;
+        }
     } else {
-        set_err("oracle covers enc-dec, attn and attn-2 only");
+        set_err("unknown model variant");
         kso_free(m);
         return NULL;
     }
@@ -441,6 +477,7 @@ static void softmax(double* v, int n) {
 /* ------------------------------------------------------------------------- */
 
 typedef struct {
+    double* dists; /* hybrid variants: every position's distribution (sum V_p) */
     double* act;   /* attn: 7 x 2 n_a */
     double* h0;    /* enc-dec thought vector */
     double* c0;
@@ -448,7 +485,9 @@ typedef struct {
     double* x;     /* decoder input buffer */
 } kso_enc;
 
-static int dec_size(const kso_model* m) { return m->variant == 0 ? m->e_size : m->n_s; }
+static int dec_size(const kso_model* m) {
+    return m->variant == 0 ? m->e_size : (m->variant >= 3 ? m->cell : m->n_s);
+}
 
 static size_t scratch_len(const kso_model* m) {
     int H = dec_size(m);
@@ -464,9 +503,132 @@ static int check_input(const kso_model* m, const int32_t* tok7) {
     return 0;
 }
 
+/* hybrid_encode (models.cpp:296-309) + conv1d_forward (nn.cpp:171-213): conv
+ * stack over the (d_in x 7) one-hot matrix, flattened row-major (f, o). */
+static double* hybrid_encoded(const kso_model* m, const int32_t* tok7, int* flat) {
+    int ch = m->d_in, len = KSO_T_IN;
+    double* x = (double*)calloc((size_t)ch * len, sizeof(double));
+    for (int t = 0; t < KSO_T_IN; ++t) x[(size_t)(m->in_offset[t] + tok7[t]) * len + t] = 1.0;
+    for (int i = 0; i < m->n_conv; ++i) {
+        const int f = m->conv_f[i], k = m->conv_k[i], st = m->conv_s[i];
+        const int o = (len - k) / st + 1;
+        double* y = (double*)calloc((size_t)f * o, sizeof(double));
+        for (int ff = 0; ff < f; ++ff)
+            for (int j = 0; j < o; ++j) {
+                double acc = m->conv_b[i][ff];
+                const int start = j * st;
+                for (int c = 0; c < ch; ++c) {
+                    const double* row = x + (size_t)c * len;
+                    for (int u = 0; u < k; ++u) acc += m->conv_w[i][((size_t)ff * ch + c) * k + u] * row[start + u];
+                }
+                y[(size_t)ff * o + j] = acc;
+            }
+        free(x);
+        x = y;
+        ch = f;
+        len = o;
+    }
+    *flat = ch * len;
+    return x;
+}
+
+/* hybrid2_decode (models.cpp:359-371) / hybrid encode branch (409-421):
+ * distributions of every position, independent of the decoded prefix. */
+static void hybrid_dists(const kso_model* m, const int32_t* tok7, kso_enc* e) {
+    int F;
+    double* enc = hybrid_encoded(m, tok7, &F);
+    const int H = m->cell, T = m->t_out;
+    const int nx2 = m->variant == 4 ? F : 2 * H;
+    double* sc = (double*)calloc((size_t)(F + 2 * H) * 6 + 64, sizeof(double));
+    double* f1 = (double*)calloc((size_t)T * H, sizeof(double));
+    double* b1 = (double*)calloc((size_t)T * H, sizeof(double));
+    double* f2 = (double*)calloc((size_t)T * H, sizeof(double));
+    double* b2 = (double*)calloc((size_t)T * H, sizeof(double));
+    double* h = (double*)calloc((size_t)H, sizeof(double));
+    double* c = (double*)calloc((size_t)H, sizeof(double));
+    double* h2 = (double*)calloc((size_t)H, sizeof(double));
+    double* c2 = (double*)calloc((size_t)H, sizeof(double));
+    double* fh = (double*)calloc((size_t)H, sizeof(double));
+    double* fc = (double*)calloc((size_t)H, sizeof(double));
+    double* x2 = (double*)calloc((size_t)2 * H + 1, sizeof(double));
+    /* bi-LSTM 1 over T copies of the encoding, zero initial state */
+    for (int t = 0; t < T; ++t) {
+        lstm_step(enc, F, h, c, H, m->enc_f_w, m->enc_f_b, h2, c2, sc);
+        memcpy(h, h2, sizeof(double) * (size_t)H);
+        memcpy(c, c2, sizeof(double) * (size_t)H);
+        memcpy(f1 + (size_t)t * H, h, sizeof(double) * (size_t)H);
+    }
+    memcpy(fh, h, sizeof(double) * (size_t)H);
+    memcpy(fc, c, sizeof(double) * (size_t)H);
+    memset(h, 0, sizeof(double) * (size_t)H);
+    memset(c, 0, sizeof(double) * (size_t)H);
+    for (int t = T - 1; t >= 0; --t) {
+        lstm_step(enc, F, h, c, H, m->enc_b_w, m->enc_b_b, h2, c2, sc);
+        memcpy(h, h2, sizeof(double) * (size_t)H);
+        memcpy(c, c2, sizeof(double) * (size_t)H);
+        memcpy(b1 + (size_t)t * H, h, sizeof(double) * (size_t)H);
+    }
+    /* bi-LSTM 2: hybrid-2 reads the encoding again and is seeded with
+     * bi-LSTM 1's final states (bilstm_seeded, models.cpp:314-344); hybrid
+     * reads bi-LSTM 1's activations from a zero state */
+    double *bh = h, *bc = c;  /* backward final state of bi-LSTM 1 */
+    double* sh = (double*)calloc((size_t)H, sizeof(double));
+    double* scc = (double*)calloc((size_t)H, sizeof(double));
+    if (m->variant == 4) {
+        memcpy(sh, fh, sizeof(double) * (size_t)H);
+        memcpy(scc, fc, sizeof(double) * (size_t)H);
+    }
+    for (int t = 0; t < T; ++t) {
+        const double* xin = enc;
+        if (m->variant == 3) {
+            memcpy(x2, f1 + (size_t)t * H, sizeof(double) * (size_t)H);
+            memcpy(x2 + H, b1 + (size_t)t * H, sizeof(double) * (size_t)H);
+            xin = x2;
+        }
+        lstm_step(xin, nx2, sh, scc, H, m->h2f_w, m->h2f_b, h2, c2, sc);
+        memcpy(sh, h2, sizeof(double) * (size_t)H);
+        memcpy(scc, c2, sizeof(double) * (size_t)H);
+        memcpy(f2 + (size_t)t * H, sh, sizeof(double) * (size_t)H);
+    }
+    if (m->variant == 4) {
+        memcpy(sh, bh, sizeof(double) * (size_t)H);
+        memcpy(scc, bc, sizeof(double) * (size_t)H);
+    } else {
+        memset(sh, 0, sizeof(double) * (size_t)H);
+        memset(scc, 0, sizeof(double) * (size_t)H);
+    }
+    for (int t = T - 1; t >= 0; --t) {
+        const double* xin = enc;
+        if (m->variant == 3) {
+            memcpy(x2, f1 + (size_t)t * H, sizeof(double) * (size_t)H);
+            memcpy(x2 + H, b1 + (size_t)t * H, sizeof(double) * (size_t)H);
+            xin = x2;
+        }
+        lstm_step(xin, nx2, sh, scc, H, m->h2b_w, m->h2b_b, h2, c2, sc);
+        memcpy(sh, h2, sizeof(double) * (size_t)H);
+        memcpy(scc, c2, sizeof(double) * (size_t)H);
+        memcpy(b2 + (size_t)t * H, sh, sizeof(double) * (size_t)H);
+    }
+    /* head_distributions (models.cpp:346-355) */
+    int off = 0;
+    for (int t = 0; t < T; ++t) {
+        memcpy(x2, f2 + (size_t)t * H, sizeof(double) * (size_t)H);
+        memcpy(x2 + H, b2 + (size_t)t * H, sizeof(double) * (size_t)H);
+        dense(x2, 2 * H, m->head_w[t], m->head_b[t], m->vsize[t], e->dists + off);
+        softmax(e->dists + off, m->vsize[t]);
+        off += m->vsize[t];
+    }
+    free(enc); free(sc); free(f1); free(b1); free(f2); free(b2); free(h); free(c); free(h2); free(c2);
+    free(fh); free(fc); free(x2); free(sh); free(scc);
+}
+
 /* encode (models.cpp:387-428): attn branch -> bilstm_forward (nn.cpp:130-165);
  * enc-dec branch -> forward LSTM, final state is the thought vector. */
 static void encode(const kso_model* m, const int32_t* tok7, kso_enc* e) {
+    if (m->variant >= 3) {
+        hybrid_dists(m, tok7, e);
+        return;
+    }
     double* onehot = e->scratch;                 /* d_in */
     double* sc = e->scratch + m->d_in + 8;       /* lstm scratch */
     if (m->variant == 0) {
@@ -516,6 +678,9 @@ static void encode(const kso_model* m, const int32_t* tok7, kso_enc* e) {
 }
 
 static void enc_alloc(const kso_model* m, kso_enc* e) {
+    int nd = 0;
+    for (int p = 0; p < m->t_out; ++p) nd += m->vsize[p];
+    e->dists = (double*)calloc((size_t)nd + 1, sizeof(double));
     e->act = (double*)calloc((size_t)KSO_T_IN * 2 * (size_t)(m->n_a + 1), sizeof(double));
     int H = dec_size(m);
     e->h0 = (double*)calloc((size_t)(m->e_size + 1), sizeof(double));
@@ -525,6 +690,7 @@ static void enc_alloc(const kso_model* m, kso_enc* e) {
 }
 
 static void enc_free(kso_enc* e) {
+    free(e->dists);
     free(e->act);
     free(e->h0);
     free(e->c0);
@@ -540,6 +706,14 @@ static void step(const kso_model* m, const kso_enc* e, const double* h, const do
     double* sc = e->scratch;
     double* x = e->x;
     int nx = 0;
+    if (m->variant >= 3) {  /* hybrid: static distributions (models.cpp:484-488) */
+        int off = 0;
+        for (int q = 0; q < pos; ++q) off += m->vsize[q];
+        memcpy(dist, e->dists + off, sizeof(double) * (size_t)m->vsize[pos]);
+        memcpy(h_out, h, sizeof(double) * (size_t)H);
+        memcpy(c_out, c, sizeof(double) * (size_t)H);
+        return;
+    }
     if (m->variant == 1 || m->variant == 2) {
         /* attention_weights (models.cpp:265-281) */
         const int A = 2 * m->n_a;

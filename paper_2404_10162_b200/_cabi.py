@@ -78,7 +78,8 @@ EXPORTS = [
     "ks_engine_destroy", "ks_engine_num_positions", "ks_engine_vocab_size",
     "ks_engine_precision", "ks_engine_last_launch_count", "ks_engine_set_chunk",
     "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
-    "ks_engine_profile_reset", "ks_engine_profile_gemm_ms",
+    "ks_engine_profile_reset", "ks_engine_profile_gemm_ms", "ks_engine_profile_launches",
+    "ks_beam_search_batch_hooked",
 ]
 
 
@@ -124,6 +125,8 @@ def lib():
     L.ks_engine_profile_reset.argtypes = [vp, i32]
     L.ks_engine_profile_gemm_ms.argtypes = [vp, P(i64), P(dbl)]
     L.ks_engine_profile_gemm_ms.restype = dbl
+    L.ks_engine_profile_launches.argtypes = [vp, i64, P(dbl), P(dbl)]
+    L.ks_engine_profile_launches.restype = i64
     _lib = L
     return L
 
@@ -224,6 +227,13 @@ class Engine:
 
     def profile_reset(self, enable=True):
         lib().ks_engine_profile_reset(self._h, int(enable))
+
+    def profile_launches(self):
+        n = lib().ks_engine_profile_launches(self._h, 0, None, None)
+        ms = np.zeros(n)
+        fl = np.zeros(n)
+        lib().ks_engine_profile_launches(self._h, n, _p(ms, C.c_double), _p(fl, C.c_double))
+        return ms, fl
 
     def profile(self):
         n = C.c_int64(0)

@@ -153,6 +153,7 @@ struct ks_engine {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
     std::vector<double> prof_flops;
     double prof_ms = 0.0, prof_useful = 0.0;
+    std::vector<std::pair<double, double>> prof_each;  // per GEMM launch: (ms, useful FLOPs)
     int64_t prof_n = 0;
     int tc_units = 64;
     int num_sms = 148;
@@ -931,6 +932,7 @@ ks_status collect_profile(ks_engine& E) {
         E.prof_ms += ms;
         E.prof_useful += E.prof_flops[i];
         E.prof_n++;
+        E.prof_each.emplace_back(ms, E.prof_flops[i]);
         cudaEventDestroy(E.prof_ev[i].first);
         cudaEventDestroy(E.prof_ev[i].second);
     }
@@ -1090,6 +1092,17 @@ extern "C" void ks_engine_profile_reset(ks_engine* eng, int32_t enable) {
     eng->prof_ms = 0.0;
     eng->prof_useful = 0.0;
     eng->prof_n = 0;
+    eng->prof_each.clear();
+}
+
+extern "C" int64_t ks_engine_profile_launches(const ks_engine* eng, int64_t cap, double* ms, double* useful) {
+    if (!eng) return 0;
+    const int64_t n = (int64_t)eng->prof_each.size();
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+        if (ms) ms[i] = eng->prof_each[(size_t)i].first;
+        if (useful) useful[i] = eng->prof_each[(size_t)i].second;
+    }
+    return n;
 }
 
 extern "C" double ks_engine_profile_gemm_ms(const ks_engine* eng, int64_t* launches, double* useful) {
