@@ -45,6 +45,9 @@ TINY_MODELS = [  # (file stem, variant, spec key, seed)
     ("tiny_attn_s434", "attn", "s434", 23),
     ("tiny_attn_s232", "attn", "s232", 5),
     ("tiny_attn_s22", "attn", "s22", 29),
+    ("tiny_hybrid2_s3423", "hybrid-2", "s3423", 11),
+    ("tiny_hybrid_s3423", "hybrid", "s3423", 12),
+    ("tiny_hybrid2_s434", "hybrid-2", "s434", 23),
 ]
 
 BUDGET_LINE = "budget tiny_budget {b} p0=0.5,p1=1.0,p2=1.5"
@@ -123,6 +126,23 @@ def main():
     r = rm.beam(tok, 5, desc, preds_text=line)
     for key in ("tokens", "log_prob", "count", "status", "fail_step"):
         golden[f"small/constrained/{key}"] = r[key]
+    # small trained hybrid-2 (the reference's default variant) on the same task
+    cfg = ks.ModelConfig(variant="hybrid-2", conv_layers=[(16, 3, 1), (8, 3, 1)], decoder_cell_size=32,
+                         dropout=0.0, recurrent_dropout=0.0)
+    params, log = ks.train(cfg, spec, train.samples[:2000], test.samples[:200], epochs=6,
+                           batch_size=32, seed=1, threads=8, learning_rate=3e-3)
+    hyb = os.path.join(HERE, "hybrid2_small_trained.ckpt")
+    ks.save_checkpoint(params, hyb)
+    print("small hybrid-2 test acc", log[-1]["test_avg_acc"])
+    rm = RefModel(hyb)
+    golden["hyb/greedy"] = rm.greedy(tok)
+    for k in (1, 5):
+        r = rm.beam(tok, k)
+        golden[f"hyb/k{k}/tokens"] = r["tokens"]
+        golden[f"hyb/k{k}/log_prob"] = r["log_prob"]
+    r = rm.beam(tok, 5, desc, preds_text=line)
+    for key in ("tokens", "log_prob", "count", "status", "fail_step"):
+        golden[f"hyb/constrained/{key}"] = r[key]
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **golden)
     print("wrote", len(golden), "arrays")
 

@@ -97,3 +97,19 @@ def test_oracle_matches_live_reference_default_size():
     a, b = o.beam(tok, 5, threads=8), r.beam(tok, 5, threads=8)
     np.testing.assert_array_equal(a["tokens"], b["tokens"])
     np.testing.assert_array_equal(a["log_prob"], b["log_prob"])
+
+
+def test_oracle_matches_reference_golden_trained_hybrid2(golden):
+    """The reference's default variant (hybrid-2): conv stack + seeded bi-LSTMs
+    (models.cpp:296-371), beam over static distributions."""
+    o = OracleModel(golden_path("hybrid2_small_trained.ckpt"))
+    tok, desc = golden["small/tok"], golden["small/desc"]
+    assert (o.greedy(tok) == golden["hyb/greedy"]).all()
+    for k in (1, 5):
+        r = o.beam(tok, k)
+        np.testing.assert_array_equal(r["tokens"], golden[f"hyb/k{k}/tokens"])
+        np.testing.assert_array_equal(r["log_prob"], golden[f"hyb/k{k}/log_prob"])
+    r = o.beam(tok, 5, desc, preds=[o.membership(), o.budget({n: 1.0 for n in o.names}, 28)])
+    np.testing.assert_array_equal(r["status"], golden["hyb/constrained/status"])
+    np.testing.assert_array_equal(r["tokens"], golden["hyb/constrained/tokens"])
+    np.testing.assert_array_equal(r["log_prob"], golden["hyb/constrained/log_prob"])
