@@ -196,8 +196,15 @@ enum class ModelVariant { enc_dec, attn, attn2, hybrid, hybrid2 };
 std::string variant_label(ModelVariant v);
 ModelVariant variant_from_label(const std::string& s);
 
+struct ConvLayerSpec {
+    int filters = 64;
+    int kernel_size = 3;
+    int stride = 1;
+};
+
 struct ModelConfig {
     ModelVariant variant = ModelVariant::hybrid2;
+    std::vector<ConvLayerSpec> conv_layers = {{64, 3, 1}, {32, 3, 1}};
     int encoder_state_size = 256;
     int pre_attention_size = 256;
     int post_attention_size = 512;

@@ -91,6 +91,10 @@ typedef struct {
     const char* const* tensor_names; /* reference names: "post.w_input", "head.3.bias", ... */
     const int32_t* tensor_numel;
     const float* const* tensor_data; /* fp32 (checkpoints are fp32, data.cpp:447-460) */
+    /* hybrid variants (models.hpp:22-41): conv stack and bi-LSTM cell size */
+    int32_t decoder_cell_size;
+    int32_t num_conv_layers;
+    const int32_t* conv_layers;      /* num_conv_layers x (filters, kernel_size, stride) */
 } ks_model_desc;
 
 /* Arithmetic of the gate GEMMs (the 99.6% of FLOPs):

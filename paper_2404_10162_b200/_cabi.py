@@ -66,6 +66,9 @@ class KsModelDesc(C.Structure):
         ("tensor_names", C.POINTER(C.c_char_p)),
         ("tensor_numel", C.POINTER(C.c_int32)),
         ("tensor_data", C.POINTER(C.POINTER(C.c_float))),
+        ("decoder_cell_size", C.c_int32),
+        ("num_conv_layers", C.c_int32),
+        ("conv_layers", C.POINTER(C.c_int32)),
     ]
 
 

@@ -411,6 +411,16 @@ ModelParams load_checkpoint(const std::string& path) {
     geti("post_attention_size", mp.config.post_attention_size);
     geti("attention_dense_nodes", mp.config.attention_dense_nodes);
     geti("decoder_cell_size", mp.config.decoder_cell_size);
+    if (!hdr("conv_layers").empty()) {
+        mp.config.conv_layers.clear();
+        std::stringstream ss(hdr("conv_layers"));
+        std::string layer;
+        while (std::getline(ss, layer, ';')) {
+            const auto v = ints(layer);
+            if (v.size() != 3) throw CheckpointError(CheckpointError::Kind::malformed, "bad conv layer spec: " + layer);
+            mp.config.conv_layers.push_back({(int)v[0], (int)v[1], (int)v[2]});
+        }
+    }
     if (!hdr("dropout").empty()) mp.config.dropout = std::stod(hdr("dropout"));
     if (!hdr("recurrent_dropout").empty()) mp.config.recurrent_dropout = std::stod(hdr("recurrent_dropout"));
     std::vector<FieldVocab> in, out;
@@ -469,8 +479,17 @@ SequencePredictor::SequencePredictor(const ModelParams& params, int device, Gemm
         numel.push_back(static_cast<int32_t>(t.values.size()));
         data.push_back(t.values.data());
     }
+    std::vector<int32_t> conv;
+    for (const auto& l : params.config.conv_layers) {
+        conv.push_back(l.filters);
+        conv.push_back(l.kernel_size);
+        conv.push_back(l.stride);
+    }
     ks_model_desc d{};
     d.variant = var;
+    d.decoder_cell_size = params.config.decoder_cell_size;
+    d.num_conv_layers = static_cast<int32_t>(params.config.conv_layers.size());
+    d.conv_layers = conv.data();
     d.encoder_state_size = params.config.encoder_state_size;
     d.pre_attention_size = params.config.pre_attention_size;
     d.post_attention_size = params.config.post_attention_size;

@@ -7,6 +7,7 @@
 // CheckpointError::Kind (errors.hpp:66-74): version, truncated, shape,
 // malformed, io.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -181,6 +182,22 @@ ks_status desc_from_checkpoint(const ks_checkpoint* ck, DescStore& store, ks_mod
     d.post_attention_size = geti("post_attention_size", 512);
     d.attention_dense_nodes = geti("attention_dense_nodes", 2);
     d.num_positions = geti("output_params", 0);
+    d.decoder_cell_size = geti("decoder_cell_size", 256);
+    store.conv.clear();
+    if (const char* cl = hdr("conv_layers")) {
+        std::stringstream ss(cl);
+        std::string layer;
+        while (std::getline(ss, layer, ';')) {
+            int f = 0, k = 0, st = 0;
+            if (std::sscanf(layer.c_str(), "%d,%d,%d", &f, &k, &st) == 3) {
+                store.conv.push_back(f);
+                store.conv.push_back(k);
+                store.conv.push_back(st);
+            }
+        }
+    }
+    d.num_conv_layers = (int32_t)(store.conv.size() / 3);
+    d.conv_layers = store.conv.data();
     auto parse_list = [](const std::string& s, std::vector<int64_t>& out) {
         std::stringstream ss(s);
         std::string piece;

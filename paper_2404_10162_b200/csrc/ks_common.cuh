@@ -70,6 +70,8 @@ struct LstmArgs {
     const int* parent;     // row -> c_prev row; null -> identity; <0 -> zero state
     float* h_out;
     long long ldh;
+    float* h_out2;         // optional second fp32 copy of h (hybrid: next operand + feature)
+    long long ldh2;
     float* c_out;
     long long ldc;
     __half* hA_hi;         // optional split copy of h_out for the next GEMM
@@ -141,9 +143,28 @@ struct BeamArgs {
     int cands_per_warp;        // smem capacity per warp (entries)
     const int* host_rej;       // [B*H_cur][V] first rejecting host predicate (or -1); may be null
     int split_mode;            // selects the kernel instantiation only
+    int h_per_config;          // hybrid: one feature row per config (static distributions)
     int n_values;              // staged-table sizes (shared memory)
     int n_terms;
     int n_bytes;
+};
+
+// Hybrid variants' convolutional encoder arguments (hybrid_conv).
+struct ConvArgs {
+    int C;
+    int n_conv;
+    int f[8], k[8], s[8];
+    const float* W[8];
+    const float* b[8];
+    int d_in;
+    int in_offset[kTin];
+    const int* tok;
+    int F, FP, CP, K;
+    int split_mode;
+    __half* Ahi[4];  // [dir*2 + pingpong]
+    __half* Alo[4];
+    float* Af[4];
+    int scratch_floats;  // per warp
 };
 
 // fp16 hi/lo split of an fp32 value, pre-scaled by 2^8 (exact) so that the

@@ -32,6 +32,7 @@ __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long 
                           int* status, int* fail_pred, int* fail_step);
 size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tables);
 bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s);
+bool launch_hybrid_conv(const ConvArgs& p, cudaStream_t s);
 // tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
                     const __half* W_lo0, const __half* W_hi1, const __half* W_lo1,
@@ -156,6 +157,13 @@ struct ks_engine {
     std::vector<std::pair<double, double>> prof_each;  // per GEMM launch: (ms, useful FLOPs)
     int64_t prof_n = 0;
     int tc_units = 64;
+    // hybrid-2 (models.cpp:296-371, 409-425)
+    int cell = 0, CP = 0, F = 0, FP = 0;
+    std::vector<int> conv_f, conv_k, conv_s;
+    std::vector<std::unique_ptr<DevMem>> convW, convB;
+    int conv_scratch = 0;
+    DevLstm hb1[2], hb2[2];
+    DevMem hybA, hybAf, hybC, hybH, feat;
     int num_sms = 148;
 };
 
@@ -266,9 +274,9 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
     if (!d || !out) return set_error(KS_ERR_PARAMETER, "null argument");
     if (precision < 0 || precision > 2) return set_error(KS_ERR_PARAMETER, "unknown precision mode");
     if (d->variant != KS_VARIANT_ATTN && d->variant != KS_VARIANT_ATTN2 &&
-        d->variant != KS_VARIANT_ENC_DEC)
+        d->variant != KS_VARIANT_ENC_DEC && d->variant != KS_VARIANT_HYBRID2)
         return set_error(KS_ERR_UNSUPPORTED,
-                         "the B200 engine implements the enc-dec, attn and attn-2 variants");
+                         "the B200 engine implements the enc-dec, attn, attn-2 and hybrid-2 variants");
     if (d->num_positions < 1 || d->num_positions > kMaxT)
         return set_error(KS_ERR_UNSUPPORTED, "number of output positions must be in [1, 16]");
     if (d->attention_dense_nodes < 1 || d->attention_dense_nodes > kMaxNd)
@@ -330,7 +338,9 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         ht.m[d->tensor_names[i]] = {d->tensor_data[i], d->tensor_numel[i]};
     std::string err;
     ks_status st;
-    if (E.variant == KS_VARIANT_ENC_DEC) {
+    if (E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID) {
+        // packed below
+    } else if (E.variant == KS_VARIANT_ENC_DEC) {
         std::vector<int> dense, slots;
         for (int k = 0; k < E.NE; ++k) dense.push_back(k < E.e ? E.d_in + k : -1);
         for (int s = 0; s < E.d_in; ++s) slots.push_back(s);
@@ -383,15 +393,64 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         if ((st = upload(E.attWo, wo, (size_t)E.n_d * 4))) return st;
         E.attBo = bo[0];
     }
-    const int Hd = E.variant == KS_VARIANT_ENC_DEC ? E.e : E.n_s;
-    const int HdP = E.variant == KS_VARIANT_ENC_DEC ? E.NE : E.NS;
+    if (E.variant == KS_VARIANT_HYBRID2) {
+        // conv stack over the (d_in x 7) one-hot matrix, then two seeded bi-LSTMs
+        if (d->num_conv_layers < 1 || d->num_conv_layers > 8 || !d->conv_layers)
+            return set_error(KS_ERR_UNSUPPORTED, "hybrid-2 needs 1..8 conv layers");
+        int ch = E.d_in, len = 7, scratch = 0;
+        for (int i = 0; i < d->num_conv_layers; ++i) {
+            const int f = d->conv_layers[3 * i], kk = d->conv_layers[3 * i + 1], sd = d->conv_layers[3 * i + 2];
+            if (f < 1 || kk < 1 || sd < 1 || len < kk)
+                return set_error(KS_ERR_SHAPE, "conv stack input length shorter than kernel size");
+            const int o = (len - kk) / sd + 1;
+            const float* W = ht.get("conv." + std::to_string(i) + ".filters", f * ch * kk, err);
+            const float* B = ht.get("conv." + std::to_string(i) + ".bias", f, err);
+            if (!W || !B) return set_error(KS_ERR_STATE, err);
+            E.conv_f.push_back(f);
+            E.conv_k.push_back(kk);
+            E.conv_s.push_back(sd);
+            E.convW.emplace_back(new DevMem());
+            E.convB.emplace_back(new DevMem());
+            if ((st = upload(*E.convW.back(), W, (size_t)f * ch * kk * 4))) return st;
+            if ((st = upload(*E.convB.back(), B, (size_t)f * 4))) return st;
+            scratch = std::max(scratch, f * o);
+            ch = f;
+            len = o;
+        }
+        E.F = ch * len;
+        E.FP = round_up(E.F, 64);
+        E.cell = d->decoder_cell_size;
+        E.CP = round_up(E.cell, 64);
+        E.conv_scratch = (scratch + 3) / 4 * 4;
+        std::vector<int> dense, slots{-1};
+        for (int kx = 0; kx < E.FP; ++kx) dense.push_back(kx < E.F ? kx : -1);
+        for (int kh = 0; kh < E.CP; ++kh) dense.push_back(kh < E.cell ? E.F + kh : -1);
+        static const char* names[4] = {"bilstm1.fwd", "bilstm1.bwd", "bilstm2.fwd", "bilstm2.bwd"};
+        DevLstm* dst[4] = {&E.hb1[0], &E.hb1[1], &E.hb2[0], &E.hb2[1]};
+        for (int q = 0; q < 4; ++q)
+            if ((st = pack_lstm(ht, names[q], E.F + E.cell, E.cell, E.CP, dense, slots, *dst[q], E.precision,
+                                E.tc_units)))
+                return st;
+    } else if (E.variant == KS_VARIANT_HYBRID) {
+        return set_error(KS_ERR_UNSUPPORTED, "hybrid (non-seeded) is not implemented on the B200 engine");
+    }
+    const bool hyb = E.variant == KS_VARIANT_HYBRID2;
+    const int Hd = hyb ? 2 * E.cell : (E.variant == KS_VARIANT_ENC_DEC ? E.e : E.n_s);
+    const int HdP = hyb ? 2 * E.CP : (E.variant == KS_VARIANT_ENC_DEC ? E.NE : E.NS);
     for (int p = 0; p < E.T; ++p) {
         const int V = E.vsize[p];
         const float* W = ht.get("head." + std::to_string(p) + ".weights", Hd * V, err);
         const float* b = ht.get("head." + std::to_string(p) + ".bias", V, err);
         if (!W || !b) return set_error(KS_ERR_STATE, err);
         std::vector<float> Wp((size_t)HdP * V, 0.0f);
-        std::memcpy(Wp.data(), W, sizeof(float) * (size_t)Hd * V);
+        if (hyb) {  // feature = [fwd h (cell) | bwd h (cell)] laid out [fwd | pad | bwd | pad]
+            for (int r = 0; r < Hd; ++r) {
+                const int dr = r < E.cell ? r : E.CP + (r - E.cell);
+                std::memcpy(Wp.data() + (size_t)dr * V, W + (size_t)r * V, sizeof(float) * (size_t)V);
+            }
+        } else {
+            std::memcpy(Wp.data(), W, sizeof(float) * (size_t)Hd * V);
+        }
         E.headW.emplace_back(new DevMem());
         E.headB.emplace_back(new DevMem());
         if ((st = upload(*E.headW.back(), Wp.data(), Wp.size() * 4))) return st;
@@ -575,18 +634,29 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
 #define ENS(buf, n) if ((e = (buf).ensure((size_t)(n))) != cudaSuccess) goto fail
     ENS(E.tok, C * 7 * 4);
     ENS(E.desc, C * 7 * 8);
-    ENS(E.act, C * 7 * (enc_dec ? E.NE : NA2) * 4);
-    ENS(E.uatt, C * 7 * E.n_d * 4 + 16);
-    ENS(E.encc, 2 * 2 * C * He * 4);
-    ENS(E.encA, 2 * 2 * 2 * C * He * 2);   // [dir][pingpong][hi/lo][C][He] fp16
-    if (E.precision == KS_PREC_FP32) {
-        ENS(E.Abuf, R * Kd * 4);
+    if (E.variant == KS_VARIANT_HYBRID2) {
+        const int64_t K = E.FP + E.CP;
+        if (E.precision == KS_PREC_FP32)
+            ENS(E.hybAf, 4 * C * K * 4);            // [dir*2 + pingpong][C][K] fp32
+        else
+            ENS(E.hybA, 2 * 4 * C * K * 2);         // [hi/lo][dir*2 + pingpong][C][K] fp16
+        ENS(E.hybC, 4 * C * E.CP * 4);              // [dir][pingpong][C][CP]
+        ENS(E.hybH, 2 * C * E.CP * 4);              // bi-LSTM 1 h scratch [dir][C][CP]
+        ENS(E.feat, (int64_t)E.T * C * 2 * E.CP * 4);  // [T][C][fwd | bwd]
     } else {
-        ENS(E.Ahi, R * Kd * 2);
-        ENS(E.Alo, R * Kd * 2);
+        ENS(E.act, C * 7 * (enc_dec ? E.NE : NA2) * 4);
+        ENS(E.uatt, C * 7 * E.n_d * 4 + 16);
+        ENS(E.encc, 2 * 2 * C * He * 4);
+        ENS(E.encA, 2 * 2 * 2 * C * He * 2);   // [dir][pingpong][hi/lo][C][He] fp16
+        if (E.precision == KS_PREC_FP32) {
+            ENS(E.Abuf, R * Kd * 4);
+        } else {
+            ENS(E.Ahi, R * Kd * 2);
+            ENS(E.Alo, R * Kd * 2);
+        }
+        ENS(E.hbuf, 2 * R * Hd * 4);
+        ENS(E.cbuf, 2 * R * Hd * 4);
     }
-    ENS(E.hbuf, 2 * R * Hd * 4);
-    ENS(E.cbuf, 2 * R * Hd * 4);
     for (int i = 0; i < 2; ++i) {
         ENS(E.live[i], R);
         ENS(E.lp[i], R * 8);
@@ -636,6 +706,98 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
     return KS_OK;
 }
 
+// hybrid-2 encoder: conv stack, bi-LSTM 1 over T_out copies of the encoding
+// (final states only), bi-LSTM 2 seeded with them; writes the per-position
+// features [fwd h_t | bwd h_t] (models.cpp:296-371, 422-425).
+ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
+    cudaStream_t s = E.stream;
+    const int T = E.T, CP = E.CP, FP = E.FP;
+    const int64_t K = FP + CP;
+    const bool split = E.precision != KS_PREC_FP32;
+    __half* hybA = E.hybA.as<__half>();
+    auto Ahi = [&](int dir, int pp) { return hybA + ((size_t)(dir * 2 + pp)) * C * K; };
+    auto Alo = [&](int dir, int pp) { return hybA + ((size_t)(4 + dir * 2 + pp)) * C * K; };
+    auto Af = [&](int dir, int pp) { return E.hybAf.as<float>() + ((size_t)(dir * 2 + pp)) * C * K; };
+    auto Cb = [&](int dir, int pp) { return E.hybC.as<float>() + ((size_t)(dir * 2 + pp)) * C * CP; };
+    ConvArgs ca{};
+    ca.C = (int)C;
+    ca.n_conv = (int)E.conv_f.size();
+    for (int i = 0; i < ca.n_conv; ++i) {
+        ca.f[i] = E.conv_f[(size_t)i];
+        ca.k[i] = E.conv_k[(size_t)i];
+        ca.s[i] = E.conv_s[(size_t)i];
+        ca.W[i] = E.convW[(size_t)i]->as<float>();
+        ca.b[i] = E.convB[(size_t)i]->as<float>();
+    }
+    ca.d_in = E.d_in;
+    for (int f = 0; f < 7; ++f) ca.in_offset[f] = E.in_offset[(size_t)f];
+    ca.tok = d_tok;
+    ca.F = E.F;
+    ca.FP = FP;
+    ca.CP = CP;
+    ca.K = (int)K;
+    ca.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
+    for (int q = 0; q < 4; ++q) {
+        ca.Ahi[q] = split ? Ahi(q / 2, q % 2) : nullptr;
+        ca.Alo[q] = split ? Alo(q / 2, q % 2) : nullptr;
+        ca.Af[q] = split ? nullptr : Af(q / 2, q % 2);
+    }
+    ca.scratch_floats = E.conv_scratch;
+    if (!launch_hybrid_conv(ca, s)) return set_error(KS_ERR_UNSUPPORTED, "conv stack too large for the conv kernel");
+    E.launches++;
+    ks_status st;
+    for (int step = 0; step < 2 * T; ++step) {
+        const bool second = step >= T;
+        const int cur = step & 1, nxt = cur ^ 1;
+        LstmArgs a[2];
+        for (int dir = 0; dir < 2; ++dir) {
+            LstmArgs& p = a[dir];
+            std::memset(&p, 0, sizeof p);
+            p.M = (int)C;
+            p.H = CP;
+            p.K = (int)K;
+            p.A = split ? nullptr : Af(dir, cur);
+            p.lda = K;
+            p.A_hi = split ? Ahi(dir, cur) : nullptr;
+            p.A_lo = split ? Alo(dir, cur) : nullptr;
+            DevLstm& L = second ? E.hb2[dir] : E.hb1[dir];
+            p.W = L.W.as<float>();
+            p.G = L.G.as<float>();
+            p.slot_ptr = nullptr;
+            p.slot_base = 0;
+            p.c_prev = step == 0 ? nullptr : Cb(dir, nxt);
+            p.ldc_prev = CP;
+            p.c_out = Cb(dir, cur);
+            p.ldc = CP;
+            // the new h feeds the next step's operand (h part of the other buffer)
+            if (split) {
+                p.hA_hi = Ahi(dir, nxt) + FP;
+                p.hA_lo = Alo(dir, nxt) + FP;
+                p.ldha = K;
+                p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
+            }
+            float* next_f32 = split ? nullptr : Af(dir, nxt) + FP;
+            if (!second) {
+                p.h_out = split ? E.hybH.as<float>() + (size_t)dir * C * CP : next_f32;
+                p.ldh = split ? CP : K;
+            } else {
+                const int t = dir == 0 ? step - T : T - 1 - (step - T);
+                p.h_out = E.feat.as<float>() + (size_t)t * C * 2 * CP + (size_t)dir * CP;
+                p.ldh = 2 * CP;
+                p.h_out2 = next_f32;
+                p.ldh2 = K;
+            }
+        }
+        if (step == 0 && !split) {
+            // FP32 mode: the step-0 operand's h part is zero (written by the conv kernel)
+        }
+        const double fl = 2.0 * 2.0 * (double)C * (E.F + E.cell) * 4.0 * E.cell;
+        if ((st = launch_lstm(E, a[0], &a[1], second ? E.hb2[0] : E.hb1[0], second ? &E.hb2[1] : &E.hb1[1], fl)))
+            return st;
+    }
+    return KS_OK;
+}
+
 // Decodes one chunk of C configs already resident on the device.
 ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greedy, const int* d_tok,
                     const long long* d_desc, const PredDev& pd, int* o_tok, double* o_lp,
@@ -656,9 +818,11 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     auto encc_at = [&](int dir, int pp) { return encc + ((size_t)dir * 2 + pp) * C * He; };
     auto encA_at = [&](int dir, int pp, int lo) { return encA + (((size_t)dir * 2 + pp) * 2 + lo) * C * He; };
 
+    const bool hybrid = E.variant == KS_VARIANT_HYBRID2;
+    if (hybrid && (st = encode_hybrid(E, C, d_tok))) return st;
     // ---- encoder (bi-LSTM over the 7 one-hot input steps, zero initial state)
     const int dirs = enc_dec ? 1 : 2;
-    for (int sidx = 0; sidx < 7; ++sidx) {
+    for (int sidx = 0; sidx < (hybrid ? 0 : 7); ++sidx) {
         LstmArgs a[2];
         for (int dir = 0; dir < dirs; ++dir) {
             const int t = dir == 0 ? sidx : 6 - sidx;
@@ -779,9 +943,11 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         aa.A_lo = E.Alo.as<__half>();
         aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
         if (enc_dec) aa.nd = 0;
-        if (!launch_attention(aa, pos == 0 && !enc_dec, s))
-            return set_error(KS_ERR_UNSUPPORTED, "attention_dense_nodes outside 1..8");
-        E.launches++;
+        if (!hybrid) {
+            if (!launch_attention(aa, pos == 0 && !enc_dec, s))
+                return set_error(KS_ERR_UNSUPPORTED, "attention_dense_nodes outside 1..8");
+            E.launches++;
+        }
 
         LstmArgs p{};
         p.M = M;
@@ -814,7 +980,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         if (enc_dec && pos == 0) p.ldc_prev = He;
         const double useful = 2.0 * (double)M * (double)(2 * E.n_a * (enc_dec ? 0 : 1) + (enc_dec ? E.e : E.n_s)) *
                               4.0 * (enc_dec ? E.e : E.n_s);
-        if ((st = launch_lstm(E, p, nullptr, E.dec, nullptr, useful))) return st;
+        if (!hybrid && (st = launch_lstm(E, p, nullptr, E.dec, nullptr, useful))) return st;
         const int* host_rej = nullptr;
         if (pd.has_host) {
             KS_CUDA(cudaEventSynchronize(keys_ready));
@@ -856,8 +1022,9 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         b.k = k;
         b.greedy = greedy ? 1 : 0;
         b.final_step = fin ? 1 : 0;
-        b.NS = Hd;
-        b.h = hb + (size_t)cur * R * Hd;
+        b.NS = hybrid ? 2 * E.CP : Hd;
+        b.h = hybrid ? E.feat.as<float>() + (size_t)pos * C * 2 * E.CP : hb + (size_t)cur * R * Hd;
+        b.h_per_config = hybrid ? 1 : 0;
         b.Wh = E.headW[(size_t)pos]->as<float>();
         b.bh = E.headB[(size_t)pos]->as<float>();
         b.live_cur = E.live[cur].as<unsigned char>();
@@ -894,8 +1061,8 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         const size_t tables = (size_t)b.n_values * 8 + (size_t)b.n_terms * 16 + (size_t)pd.n * sizeof(DevPred) +
                               (size_t)b.n_bytes + 16;
         int warps = 8;
-        while (warps > 1 && beam_smem_bytes(Hd, V, warps, cpw, tables) > (size_t)E.beam_smem_max) --warps;
-        const size_t smem = beam_smem_bytes(Hd, V, warps, cpw, tables);
+        while (warps > 1 && beam_smem_bytes(b.NS, V, warps, cpw, tables) > (size_t)E.beam_smem_max) --warps;
+        const size_t smem = beam_smem_bytes(b.NS, V, warps, cpw, tables);
         if (smem > (size_t)E.beam_smem_max)
             return set_error(KS_ERR_UNSUPPORTED, "beam width x vocabulary too large for the beam kernel");
         // persistent: the head weights are staged into shared memory once per CTA

@@ -346,6 +346,11 @@ __global__ void __launch_bounds__(384, 1)
                     float4* cd = reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u0);
                     hd[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
                     hd[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                    if (p.h_out2 != nullptr) {
+                        float4* h2 = reinterpret_cast<float4*>(p.h_out2 + (long long)row * p.ldh2 + u0);
+                        h2[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                        h2[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                    }
                     cd[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
                     cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
                     if (p.hA_hi != nullptr && p.ha_bf16) {

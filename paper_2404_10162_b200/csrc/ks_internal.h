@@ -21,6 +21,7 @@ struct DescStore {
     std::vector<const char*> name_ptrs;
     std::vector<int32_t> numel;
     std::vector<const float*> data;
+    std::vector<int32_t> conv;
 };
 
 ks_status desc_from_checkpoint(const ks_checkpoint* ck, DescStore& store, ks_model_desc& d);

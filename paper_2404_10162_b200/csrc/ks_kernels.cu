@@ -68,6 +68,7 @@ __device__ __forceinline__ void lstm_cell_store(const LstmArgs& p, int row, int 
     const float h = og * tanhf(c);
     p.c_out[(long long)row * p.ldc + u] = c;
     p.h_out[(long long)row * p.ldh + u] = h;
+    if (p.h_out2 != nullptr) p.h_out2[(long long)row * p.ldh2 + u] = h;
     if (p.hA_hi != nullptr) store_split_h(p, (long long)row * p.ldha + u, h);
 }
 
@@ -685,8 +686,9 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                 p0[v] = 0.0f;
                 p1[v] = 0.0f;
             }
-            const float* h0 = a.h + r0 * a.NS;
-            const float* h1 = h0 + a.NS;
+            // hybrid variants: every hypothesis of config b reads the same feature row
+            const float* h0 = a.h + (a.h_per_config ? (long long)b : r0) * a.NS;
+            const float* h1 = a.h_per_config ? h0 : h0 + a.NS;
 #pragma unroll 4
             for (int i = lane; i < a.NS; i += 32) {
                 const float x0 = live0 ? h0[i] : 0.0f;
@@ -888,6 +890,86 @@ bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, in
     if (a.split_mode == 0) return launch_beam_split<0>(a, m, warps, smem, grid, s);
     if (a.split_mode == 1) return launch_beam_split<1>(a, m, warps, smem, grid, s);
     return launch_beam_split<2>(a, m, warps, smem, grid, s);
+}
+
+}  // namespace ksb
+
+namespace ksb {
+
+// ---------------------------------------------------------------------------
+// hybrid_conv: the hybrid variants' convolutional encoder (hybrid_encode,
+// models.cpp:296-309; conv1d_forward, nn.cpp:171-213), one warp per config.
+// Layer 0 reads the one-hot (d_in x 7) input matrix as gathers of the hot
+// channel per time step; later layers are dense.  The flattened (f, o)
+// encoding is written as the x part of the bi-LSTM operands (split or fp32)
+// of both directions and both ping-pong buffers; the h part of buffer 0 is
+// zeroed (zero initial state).
+// ---------------------------------------------------------------------------
+
+
+__global__ void __launch_bounds__(128) hybrid_conv(ConvArgs p) {
+    extern __shared__ float cs[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (b >= p.C) return;
+    float* buf0 = cs + (size_t)warp * 2 * p.scratch_floats;
+    float* buf1 = buf0 + p.scratch_floats;
+    int hot[kTin];
+#pragma unroll
+    for (int t = 0; t < kTin; ++t) hot[t] = p.in_offset[t] + p.tok[(long long)b * kTin + t];
+    int ch = p.d_in, len = kTin;
+    float* in = nullptr;
+    float* out = buf0;
+    for (int i = 0; i < p.n_conv; ++i) {
+        const int f = p.f[i], k = p.k[i], st = p.s[i];
+        const int o = (len - k) / st + 1;
+        for (int idx = lane; idx < f * o; idx += 32) {
+            const int ff = idx / o, j = idx - ff * o;
+            float acc = p.b[i][ff];
+            if (i == 0) {
+                for (int u = 0; u < k; ++u) acc += p.W[0][((long long)ff * ch + hot[j * st + u]) * k + u];
+            } else {
+                for (int c = 0; c < ch; ++c)
+                    for (int u = 0; u < k; ++u)
+                        acc = fmaf(p.W[i][((long long)ff * ch + c) * k + u], in[c * len + j * st + u], acc);
+            }
+            out[idx] = acc;
+        }
+        __syncwarp();
+        in = out;
+        out = (out == buf0) ? buf1 : buf0;
+        ch = f;
+        len = o;
+    }
+    // x part of every operand buffer; zero h part of the step-0 buffers
+    for (int q = 0; q < 4; ++q) {
+        const long long base = (long long)b * p.K;
+        for (int c = lane; c < p.FP + ((q & 1) == 0 ? p.CP : 0); c += 32) {
+            const float v = c < p.F ? in[c] : 0.0f;
+            if (p.split_mode == 0) {
+                p.Af[q][base + c] = v;
+            } else if (p.split_mode == 1) {
+                __half hi, lo;
+                split_f16(v, hi, lo);
+                p.Ahi[q][base + c] = hi;
+                p.Alo[q][base + c] = lo;
+            } else {
+                reinterpret_cast<__nv_bfloat16*>(p.Ahi[q])[base + c] = __float2bfloat16_rn(v);
+            }
+        }
+    }
+}
+
+bool launch_hybrid_conv(const ConvArgs& p, cudaStream_t s) {
+    const size_t smem = (size_t)4 * 2 * p.scratch_floats * sizeof(float);
+    if (smem > 200 * 1024) return false;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(hybrid_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    hybrid_conv<<<(unsigned)((p.C + 3) / 4), 128, smem, s>>>(p);
+    return cudaGetLastError() == cudaSuccess;
 }
 
 }  // namespace ksb

@@ -52,8 +52,12 @@ def random_desc(o, tok):
     return np.array([[o.input_values[f][t] for f, t in enumerate(row)] for row in tok], np.int64)
 
 
+# the non-seeded `hybrid` variant is oracle-only; every other variant runs on the GPU
+GPU_TINY = [m[0] for m in TINY_MODELS if m[1] != "hybrid"]
+
+
 @pytest.mark.parametrize("precision", PRECISIONS)
-@pytest.mark.parametrize("stem", [m[0] for m in TINY_MODELS])
+@pytest.mark.parametrize("stem", GPU_TINY)
 def test_tiny_models_all_k(stem, precision):
     path = golden_path(stem + ".ckpt")
     o, e = OracleModel(path), engine(path, precision)
@@ -83,6 +87,33 @@ def test_small_trained_constrained(precision):
         n, ties, bad = compare_beams(g, a)
         assert n > 0.9 * len(tok)
         assert not bad, f"{preds}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_small_trained_hybrid2(precision):
+    """The reference's default variant: conv encoder + seeded bi-LSTMs on the
+    GPU, beam over static distributions."""
+    path = golden_path("hybrid2_small_trained.ckpt")
+    o, e = OracleModel(path), engine(path, precision)
+    tok = random_tokens(o, 2048, 12)
+    desc = random_desc(o, tok)
+    for preds in ([], [("membership", None), ("budget", ({n: 1.0 for n in o.names}, 28.0))]):
+        po = oracle_preds(o, preds)
+        a = o.beam(tok, 5, desc, po, threads=8)
+        g = e.beam(tok, 5, desc, po)
+        n, ties, bad = compare_beams(g, a)
+        assert n > 0.9 * len(tok)
+        assert not bad, f"{preds}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+    g1 = e.greedy(tok)
+    a1 = o.beam(tok, 1)
+    keep = a1["min_gap"] >= 1e-4
+    assert (g1[keep] == o.greedy(tok)[keep]).all()
+
+
+def test_hybrid_variant_is_rejected_cleanly():
+    from paper_2404_10162_b200._cabi import KsError
+    with pytest.raises(KsError, match="hybrid"):
+        engine(golden_path("tiny_hybrid_s3423.ckpt"), "f16x3")
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
