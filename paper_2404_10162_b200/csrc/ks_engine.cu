@@ -631,15 +631,16 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
     const int Kd = NA2 + Hd;
     const int He = enc_dec ? E.NE : E.NA;
     cudaError_t e = cudaSuccess;
-#define ENS(buf, n) if ((e = (buf).ensure((size_t)(n))) != cudaSuccess) goto fail
+#define ENS(buf, n) do { if ((e = (buf).ensure((size_t)(n))) != cudaSuccess) goto fail; } while (0)
     ENS(E.tok, C * 7 * 4);
     ENS(E.desc, C * 7 * 8);
     if (E.variant == KS_VARIANT_HYBRID2) {
         const int64_t K = E.FP + E.CP;
-        if (E.precision == KS_PREC_FP32)
+        if (E.precision == KS_PREC_FP32) {
             ENS(E.hybAf, 4 * C * K * 4);            // [dir*2 + pingpong][C][K] fp32
-        else
+        } else {
             ENS(E.hybA, 2 * 4 * C * K * 2);         // [hi/lo][dir*2 + pingpong][C][K] fp16
+        }
         ENS(E.hybC, 4 * C * E.CP * 4);              // [dir][pingpong][C][CP]
         ENS(E.hybH, 2 * C * E.CP * 4);              // bi-LSTM 1 h scratch [dir][C][CP]
         ENS(E.feat, (int64_t)E.T * C * 2 * E.CP * 4);  // [T][C][fwd | bwd]
