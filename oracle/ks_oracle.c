@@ -1097,3 +1097,84 @@ int kso_beam_batch(const kso_model* m, const int32_t* tok, const int64_t* desc, 
     free(th);
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Rng (proj/include/kernelseer/rng.hpp:13-71).  std::mt19937_64 is fully     */
+/* specified by the C++ standard ([rand.eng.mers] with the mt19937_64          */
+/* parameters), so this restatement reproduces the reference's streams.       */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    uint64_t mt[312];
+    int idx;
+} kso_mt64;
+
+static void mt64_seed(kso_mt64* g, uint64_t seed) {
+    g->mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+        g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+    g->idx = 312;
+}
+
+static uint64_t mt64_next(kso_mt64* g) {
+    if (g->idx >= 312) {
+        for (int i = 0; i < 312; ++i) {
+            const uint64_t x = (g->mt[i] & 0xFFFFFFFF80000000ULL) | (g->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+            uint64_t xa = x >> 1;
+            if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+            g->mt[i] = g->mt[(i + 156) % 312] ^ xa;
+        }
+        g->idx = 0;
+    }
+    uint64_t y = g->mt[g->idx++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+}
+
+static uint64_t rng_mix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+static void rng_derive(kso_mt64* g, uint64_t seed, uint64_t stream) {
+    mt64_seed(g, rng_mix(rng_mix(seed) + 0x9e3779b97f4a7c15ULL * (stream + 1)));
+}
+
+static double rng_uniform(kso_mt64* g) { return (double)(mt64_next(g) >> 11) * 0x1.0p-53; }
+
+void kso_uniforms(uint64_t seed, uint64_t stream, int64_t n, double* out) {
+    kso_mt64 g;
+    rng_derive(&g, seed, stream);
+    for (int64_t i = 0; i < n; ++i) out[i] = rng_uniform(&g);
+}
+
+void kso_dropout_masks(uint64_t seed, uint64_t stream, int n_in, double rate_in, int n_rec,
+                       double rate_rec, double* out) {
+    kso_mt64 g;
+    rng_derive(&g, seed, stream);
+    const double ki = 1.0 / (1.0 - rate_in), kr = 1.0 / (1.0 - rate_rec);
+    for (int i = 0; i < n_in; ++i) out[i] = rng_uniform(&g) < rate_in ? 0.0 : ki;
+    for (int i = 0; i < n_rec; ++i) out[n_in + i] = rng_uniform(&g) < rate_rec ? 0.0 : kr;
+}
+
+void kso_shuffle(uint64_t seed, uint64_t epoch, int64_t n, int64_t* order) {
+    kso_mt64 g;
+    rng_derive(&g, seed, 0x3ff000ULL + epoch);
+    for (int64_t i = 0; i < n; ++i) order[i] = i;
+    for (int64_t i = n; i > 1; --i) {
+        const uint64_t m = (uint64_t)i;
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % m;
+        uint64_t v;
+        do {
+            v = mt64_next(&g);
+        } while (v >= limit);
+        const int64_t j = (int64_t)(v % m);
+        const int64_t t = order[i - 1];
+        order[i - 1] = order[j];
+        order[j] = t;
+    }
+}

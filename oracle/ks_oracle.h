@@ -96,6 +96,19 @@ int kso_beam_batch(const kso_model* m, const int32_t* tok, const int64_t* desc, 
                    double* out_lp, int32_t* out_count, int32_t* out_status,
                    int32_t* out_fail_pred, int32_t* out_fail_step, double* out_min_gap);
 
+/* ---- Rng (proj/include/kernelseer/rng.hpp:13-71): mt19937_64 + derive ---- */
+/* Dropout masks of one sample as LstmMasks::make draws them
+ * (proj/src/models.cpp:559-573, nn::dropout_mask nn.cpp:237-248) from the stream
+ * Rng::derive(seed, stream): n_in input-mask entries (rate_in) then n_rec
+ * recurrent-mask entries (rate_rec); out: n_in + n_rec values (0 or 1/(1-rate)). */
+void kso_dropout_masks(uint64_t seed, uint64_t stream, int n_in, double rate_in, int n_rec,
+                       double rate_rec, double* out);
+/* train_model's per-epoch Fisher-Yates shuffle (proj/src/models.cpp:895-900):
+ * order[0..n) from Rng::derive(seed, 0x3ff000 + epoch). */
+void kso_shuffle(uint64_t seed, uint64_t epoch, int64_t n, int64_t* order);
+/* Uniform draws of Rng::derive(seed, stream).uniform() (test hook). */
+void kso_uniforms(uint64_t seed, uint64_t stream, int64_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,8 @@
 // proj/include/kernelseer/parallel.hpp:14-27) and calls beam_search /
 // constrained_beam_search per sample (proj/src/decoding.cpp:126-135).
 #include <atomic>
+#include <optional>
+#include <stdexcept>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -19,9 +21,13 @@
 #include "kernelseer/data.hpp"
 #include "kernelseer/decoding.hpp"
 #include "kernelseer/eval.hpp"
+#include "kernelseer/models.hpp"
+#include "kernelseer/nn.hpp"
 #include "kernelseer/parallel.hpp"
+#include "kernelseer/rng.hpp"
 
 using namespace kernelseer;
+using kernelseer::nn::Tensor;
 
 namespace {
 thread_local std::string g_err;
@@ -280,6 +286,147 @@ int ksref_synthetic(const char* kernel, int count, uint64_t seed, const char* di
         g_err = e.what();
         return -1;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Teacher-forced training (BASELINE config 4), reference side.
+// ---------------------------------------------------------------------------
+
+// Flat gradient / parameter layout: the tensors in ModelParams::tensors order
+// (std::map = alphabetical = checkpoint payload order, proj/src/data.cpp:497-509).
+int64_t ksref_num_params(void* h) {
+    int64_t n = 0;
+    for (const auto& [name, t] : static_cast<ModelParams*>(h)->tensors) n += t.size();
+    return n;
+}
+
+int ksref_get_params(void* h, double* out) {
+    int64_t o = 0;
+    for (const auto& [name, t] : static_cast<ModelParams*>(h)->tensors)
+        for (int i = 0; i < t.size(); ++i) out[o++] = t[i];
+    return 0;
+}
+
+// Sum over samples of model_loss_gradients (proj/src/models.cpp:788-797).
+// dropout_epoch < 0: no dropout (rng = nullptr).  Otherwise each sample b gets
+// the stream train_model gives it: Rng::derive(seed, epoch << 32 | idx[b])
+// (proj/src/models.cpp:915-918).  grads: flat, ksref_num_params doubles.
+int ksref_loss_grads(void* h, const int32_t* tok, const int32_t* tgt, int64_t B, int threads,
+                     int64_t dropout_epoch, uint64_t seed, const int64_t* idx, double* loss_sum,
+                     double* grads) {
+    try {
+        const ModelParams& mp = *static_cast<ModelParams*>(h);
+        const int T = mp.num_output_positions();
+        threads = std::max(1, threads);
+        std::vector<std::map<std::string, Tensor>> part(static_cast<size_t>(threads));
+        std::vector<double> ploss(static_cast<size_t>(threads), 0.0);
+        std::vector<std::string> errs(static_cast<size_t>(threads));
+        parallel_stripes(static_cast<int>(B), threads, [&](int w, int stride) {
+            try {
+                for (int64_t b = w; b < B; b += stride) {
+                    TokenSequence in, out;
+                    in.ids.assign(tok + 7 * b, tok + 7 * b + 7);
+                    out.ids.assign(tgt + T * b, tgt + T * b + T);
+                    std::optional<Rng> rng;
+                    if (dropout_epoch >= 0)
+                        rng.emplace(Rng::derive(seed, (static_cast<uint64_t>(dropout_epoch) << 32) |
+                                                          static_cast<uint64_t>(idx ? idx[b] : b)));
+                    auto [loss, g] = model_loss_gradients(mp, in, out, rng ? &*rng : nullptr);
+                    ploss[w] += loss;
+                    auto& acc = part[static_cast<size_t>(w)];
+                    for (auto& [name, t] : g) {
+                        auto it = acc.find(name);
+                        if (it == acc.end()) acc.emplace(name, t);
+                        else for (int i = 0; i < t.size(); ++i) it->second[i] += t[i];
+                    }
+                }
+            } catch (const std::exception& e) {
+                errs[static_cast<size_t>(w)] = e.what();
+            }
+        });
+        for (const auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
+        double ls = 0.0;
+        for (double l : ploss) ls += l;
+        if (loss_sum) *loss_sum = ls;
+        int64_t o = 0;
+        for (const auto& [name, t] : mp.tensors) {
+            for (int i = 0; i < t.size(); ++i) {
+                double v = 0.0;
+                for (const auto& pm : part) {
+                    auto it = pm.find(name);
+                    if (it != pm.end()) v += it->second[i];
+                }
+                grads[o++] = v;
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// One optimiser step of train_model's batch loop (proj/src/models.cpp:905-947):
+// summed per-sample grads (dropout streams as train_model), / batch,
+// clip_global_norm, adam_step.  The Adam state lives in the handle's trainer.
+struct RefTrainer {
+    nn::AdamState adam;
+};
+
+void* ksref_trainer_new(double lr) {
+    auto* t = new RefTrainer();
+    t->adam.config.learning_rate = lr;
+    return t;
+}
+void ksref_trainer_free(void* t) { delete static_cast<RefTrainer*>(t); }
+
+int ksref_train_step(void* h, void* trainer, const int32_t* tok, const int32_t* tgt, int64_t B,
+                     int threads, int64_t epoch, uint64_t seed, const int64_t* idx, double clip,
+                     double* loss_sum) {
+    try {
+        ModelParams& mp = *static_cast<ModelParams*>(h);
+        const int64_t n = ksref_num_params(h);
+        std::vector<double> g(static_cast<size_t>(n));
+        const bool drop = mp.config.dropout != 0.0 || mp.config.recurrent_dropout != 0.0;
+        if (ksref_loss_grads(h, tok, tgt, B, threads, drop ? epoch : -1, seed, idx, loss_sum, g.data()))
+            return -1;
+        std::map<std::string, Tensor> grads;
+        int64_t o = 0;
+        for (const auto& [name, t] : mp.tensors) {
+            Tensor gt(t.shape());
+            for (int i = 0; i < gt.size(); ++i) gt[i] = g[static_cast<size_t>(o++)] / static_cast<double>(B);
+            grads.emplace(name, std::move(gt));
+        }
+        nn::clip_global_norm(grads, clip);
+        nn::adam_step(mp.tensors, grads, static_cast<RefTrainer*>(trainer)->adam);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int ksref_save(void* h, const char* path) {
+    try {
+        save_checkpoint(*static_cast<ModelParams*>(h), path);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// Rng streams as the reference draws them (proj/include/kernelseer/rng.hpp).
+void ksref_uniforms(uint64_t seed, uint64_t stream, int64_t n, double* out) {
+    Rng r = Rng::derive(seed, stream);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.uniform();
+}
+
+void ksref_shuffle(uint64_t seed, uint64_t epoch, int64_t n, int64_t* order) {
+    for (int64_t i = 0; i < n; ++i) order[i] = i;
+    Rng r = Rng::derive(seed, 0x3ff000ULL + epoch);
+    for (int64_t i = n; i > 1; --i) std::swap(order[i - 1], order[r.uniform_int(static_cast<uint64_t>(i))]);
 }
 
 }  // extern "C"
