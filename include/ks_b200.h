@@ -19,6 +19,9 @@
  *                              membership_predicate /   src/constraints.cpp:198-242
  *                              resource_budget_predicate
  *   ks_status                  exception taxonomy       include/kernelseer/errors.hpp:10-87
+ *   ks_trainer_*               train_model batch body,  src/models.cpp:788-797, 827-856, 905-947,
+ *                              model_loss_gradients,    src/nn.cpp:262-297
+ *                              evaluate_set, adam_step
  *   the batch entry points     parallel_stripes fan-out include/kernelseer/parallel.hpp:14-27 as used
  *                              in topk_metrics          src/eval.cpp:105-137
  */
@@ -221,6 +224,60 @@ double ks_engine_profile_gemm_ms(const ks_engine* eng, int64_t* launches, double
 /* Per-launch view of the same profile: fills up to cap (ms, useful FLOPs)
  * pairs in launch order and returns the number of launches recorded. */
 int64_t ks_engine_profile_launches(const ks_engine* eng, int64_t cap, double* ms, double* useful_flops);
+
+
+/* ------------------------------------------------------------------------- */
+/* Teacher-forced training (BASELINE config 4).  Replaces the batch body of   */
+/* train_model (src/models.cpp:905-947: per-sample build_loss_graph +         */
+/* Tape::backward, summed gradients, / batch, clip_global_norm, adam_step),   */
+/* model_loss_gradients (src/models.cpp:788-797) summed over a batch, and     */
+/* evaluate_set (src/models.cpp:827-856) for the enc-dec / attn / attn-2      */
+/* variants.  fp32 parameters, moments and GEMMs; gradients are exchanged in  */
+/* the "train layout" (ks_trainer_to_reference_layout converts).              */
+/* ------------------------------------------------------------------------- */
+typedef struct ks_trainer ks_trainer;
+
+/* dropout / recurrent_dropout: ModelConfig::dropout / recurrent_dropout. */
+ks_status ks_trainer_create(const ks_model_desc* model, double dropout, double recurrent_dropout,
+                            int32_t device, ks_trainer** out);
+/* dropout rates from the checkpoint header (data.cpp:478-479). */
+ks_status ks_trainer_create_from_checkpoint(const char* path, int32_t device, ks_trainer** out);
+void ks_trainer_destroy(ks_trainer* tr);
+/* Length of the flat parameter / gradient buffers (= total reference parameter count). */
+int64_t ks_trainer_num_params(const ks_trainer* tr);
+int64_t ks_trainer_last_launch_count(const ks_trainer* tr);
+
+/* Forward + backward over B samples already on the device (d_tok B x 7 input
+ * token ids, d_tgt B x T target token ids, d_idx B sample ids or NULL = 0..B-1).
+ * dropout_epoch >= 0 with nonzero rates applies train_model's variational
+ * dropout, each sample's masks drawn from Rng::derive(seed, epoch << 32 | idx)
+ * (models.cpp:915-918); < 0 disables dropout (model_loss_gradients with a
+ * null rng).  d_grads (num_params floats, train layout) receives the SUM over
+ * the batch of the per-sample gradients (accumulate != 0 adds to it);
+ * d_grads == NULL runs the forward only (evaluate_set).  d_loss_sum (1 double)
+ * and d_matches (1 int64: per-position argmax hits) are device pointers, may
+ * be NULL.  Asynchronous on `stream`. */
+ks_status ks_trainer_loss_grads(ks_trainer* tr, const int32_t* d_tok, const int32_t* d_tgt,
+                                const int64_t* d_idx, int64_t B, int64_t dropout_epoch,
+                                uint64_t seed, float* d_grads, int32_t accumulate,
+                                double* d_loss_sum, int64_t* d_matches, void* stream);
+/* Optimiser step on summed gradients of `batch` samples (all ranks' sum after
+ * an all-reduce): grads / batch, clip_global_norm(clip), adam_step(lr) with
+ * AdamConfig defaults (nn.hpp:96-101).  Asynchronous on `stream`. */
+ks_status ks_trainer_apply(ks_trainer* tr, const float* d_grads, int64_t batch, double lr, double clip,
+                           void* stream);
+/* Host-buffer single-GPU step (the reference-facing call): copies, loss_grads,
+ * apply, and the loss sum / matches back to the host. */
+ks_status ks_trainer_step(ks_trainer* tr, const int32_t* tok, const int32_t* tgt, const int64_t* idx,
+                          int64_t B, int64_t epoch, uint64_t seed, double lr, double clip,
+                          double* out_loss_sum, int64_t* out_matches);
+/* Parameters in reference flat order (the model's tensors concatenated in
+ * ks_model_desc / checkpoint order), to and from the host. */
+ks_status ks_trainer_export(const ks_trainer* tr, float* host_ref_flat);
+ks_status ks_trainer_import(ks_trainer* tr, const float* host_ref_flat);
+/* Permutes a train-layout buffer (e.g. gradients) into reference flat order. */
+ks_status ks_trainer_to_reference_layout(const ks_trainer* tr, const float* host_train_flat,
+                                         float* host_ref_flat);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,10 @@ EXPORTS = [
     "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
     "ks_engine_profile_reset", "ks_engine_profile_gemm_ms", "ks_engine_profile_launches",
     "ks_beam_search_batch_hooked",
+    "ks_trainer_create", "ks_trainer_create_from_checkpoint", "ks_trainer_destroy",
+    "ks_trainer_num_params", "ks_trainer_last_launch_count", "ks_trainer_loss_grads",
+    "ks_trainer_apply", "ks_trainer_step", "ks_trainer_export", "ks_trainer_import",
+    "ks_trainer_to_reference_layout",
 ]
 
 
@@ -130,6 +134,20 @@ def lib():
     L.ks_engine_profile_gemm_ms.restype = dbl
     L.ks_engine_profile_launches.argtypes = [vp, i64, P(dbl), P(dbl)]
     L.ks_engine_profile_launches.restype = i64
+    L.ks_trainer_create.argtypes = [P(KsModelDesc), dbl, dbl, i32, P(vp)]
+    L.ks_trainer_create_from_checkpoint.argtypes = [C.c_char_p, i32, P(vp)]
+    L.ks_trainer_destroy.argtypes = [vp]
+    L.ks_trainer_num_params.argtypes = [vp]
+    L.ks_trainer_num_params.restype = i64
+    L.ks_trainer_last_launch_count.argtypes = [vp]
+    L.ks_trainer_last_launch_count.restype = i64
+    L.ks_trainer_loss_grads.argtypes = [vp, vp, vp, vp, i64, i64, C.c_uint64, vp, i32, vp, vp, vp]
+    L.ks_trainer_apply.argtypes = [vp, vp, i64, dbl, dbl, vp]
+    L.ks_trainer_step.argtypes = [vp, P(i32), P(i32), P(i64), i64, i64, C.c_uint64, dbl, dbl,
+                                  P(dbl), P(i64)]
+    L.ks_trainer_export.argtypes = [vp, P(C.c_float)]
+    L.ks_trainer_import.argtypes = [vp, P(C.c_float)]
+    L.ks_trainer_to_reference_layout.argtypes = [vp, P(C.c_float), P(C.c_float)]
     _lib = L
     return L
 
@@ -243,3 +261,60 @@ class Engine:
         useful = C.c_double(0.0)
         ms = lib().ks_engine_profile_gemm_ms(self._h, C.byref(n), C.byref(useful))
         return ms, n.value, useful.value
+
+
+class Trainer:
+    """Teacher-forced training on one GPU (BASELINE config 4): the C-ABI
+    ks_trainer_* (train_model's batch body, proj/src/models.cpp:905-947).
+    Device-buffer calls take raw device pointers (ints) and a cudaStream_t."""
+
+    def __init__(self, checkpoint: str, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        check(L.ks_trainer_create_from_checkpoint(checkpoint.encode(), device, C.byref(h)))
+        self._h = h
+        self.num_params = L.ks_trainer_num_params(h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ks_trainer_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def launches(self) -> int:
+        return lib().ks_trainer_last_launch_count(self._h)
+
+    def loss_grads_device(self, d_tok, d_tgt, d_idx, B, dropout_epoch, seed, d_grads, accumulate,
+                          d_loss, d_match, stream=0):
+        check(lib().ks_trainer_loss_grads(self._h, d_tok, d_tgt, d_idx, B, dropout_epoch, seed, d_grads,
+                                          int(accumulate), d_loss, d_match, stream))
+
+    def apply_device(self, d_grads, batch, lr, clip=5.0, stream=0):
+        check(lib().ks_trainer_apply(self._h, d_grads, batch, lr, clip, stream))
+
+    def step(self, tok, tgt, idx=None, epoch=-1, seed=0, lr=1e-3, clip=5.0):
+        """Host-buffer step: returns (loss_sum, matches)."""
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        tgt = np.ascontiguousarray(tgt, np.int32).reshape(len(tok), -1)
+        ix = None if idx is None else np.ascontiguousarray(idx, np.int64)
+        loss = C.c_double()
+        m = C.c_int64()
+        check(lib().ks_trainer_step(self._h, _p(tok, C.c_int32), _p(tgt, C.c_int32), _p(ix, C.c_int64),
+                                    len(tok), epoch, seed, lr, clip, C.byref(loss), C.byref(m)))
+        return loss.value, m.value
+
+    def export(self) -> np.ndarray:
+        out = np.empty(self.num_params, np.float32)
+        check(lib().ks_trainer_export(self._h, _p(out, C.c_float)))
+        return out
+
+    def import_(self, flat_ref):
+        v = np.ascontiguousarray(flat_ref, np.float32)
+        check(lib().ks_trainer_import(self._h, _p(v, C.c_float)))
+
+    def to_reference_layout(self, train_flat) -> np.ndarray:
+        v = np.ascontiguousarray(train_flat, np.float32)
+        out = np.empty(self.num_params, np.float32)
+        check(lib().ks_trainer_to_reference_layout(self._h, _p(v, C.c_float), _p(out, C.c_float)))
+        return out
