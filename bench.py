@@ -50,7 +50,13 @@ WORKLOADS = {
                        "beam=16, ConvAsmBwdWrW1x1"),
     "cfg1": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=1, configs=1000, greedy=True,
                  label="BASELINE config 1: greedy decode of 1k configs"),
+    "cfg4": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=0, configs=4096, greedy=False, train=True,
+                 label="BASELINE config 4: teacher-forced training step, global batch 4096, "
+                       "data-parallel with NCCL all-reduce"),
 }
+TRAIN_METRIC = "training samples/sec, teacher-forced step (batch 4096)"
+TRAIN_UNIT = "samples/s"
+TRAIN_LR = 1e-3
 W = WORKLOADS["cfg2"]
 KERNEL = W["kernel"]
 BEAM = W["beam"]
@@ -81,12 +87,33 @@ def dist_env():
 def model_path():
     from paper_2404_10162_b200.synth import write_checkpoint
 
-    path = os.path.join(tempfile.gettempdir(), f"ks_bench_attn_{KERNEL}_{W['n_a']}_{W['n_s']}.ckpt")
+    drop = 0.2 if W.get("train") else 0.0  # ModelConfig defaults (models.hpp:28-41) for training
+    path = os.path.join(tempfile.gettempdir(), f"ks_bench_attn_{KERNEL}_{W['n_a']}_{W['n_s']}_d{drop:g}.ckpt")
     if not os.path.exists(path):
         tmp = path + f".{os.getpid()}"
-        write_checkpoint(tmp, KERNEL, "attn", W["n_a"], W["n_s"], 2, seed=1)
+        write_checkpoint(tmp, KERNEL, "attn", W["n_a"], W["n_s"], 2, seed=1, dropout=drop, recurrent_dropout=drop)
         os.replace(tmp, path)
     return path
+
+
+def train_data(path, B, seed=4):
+    """Synthetic teacher-forcing batch: encoded descriptors + uniformly drawn target tokens."""
+    from oracle.train_oracle import Checkpoint  # header parsing only
+    from paper_2404_10162_b200.synth import descriptors
+
+    ck = Checkpoint(path)
+    desc = descriptors(B, KERNEL, seed=seed)
+    tok = np.stack([np.searchsorted(np.asarray(ck.inputs[f]), desc[:, f]) for f in range(7)], 1).astype(np.int32)
+    rng = np.random.default_rng(seed)
+    tgt = np.stack([rng.integers(0, v, B) for v in ck.vsizes], 1).astype(np.int32)
+    return tok, tgt, ck
+
+
+def train_flops_per_sample(ck):
+    """~3x the forward gate-GEMM FLOPs (forward, dX, dW)."""
+    dec = ck.T * 2.0 * (2 * ck.n_a + ck.n_s) * 4 * ck.n_s
+    enc = 2 * 7 * 2.0 * ck.n_a * 4 * ck.n_a
+    return 3.0 * (dec + enc)
 
 
 def predicates(param_names, values):
@@ -397,6 +424,175 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def reference_train_rate(path, tok, tgt, threads, n):
+    """The reference's own train_model batch body (oracle/_ref via ref_shim
+    ksref_train_step: per-sample tapes over parallel_stripes, / batch, clip,
+    Adam) on n samples; returns samples/s."""
+    import ctypes as C
+
+    from tests.golden.make_train_fixtures import ref_lib
+
+    L = ref_lib()
+    h = L.ksref_load(path.encode())
+    trn = L.ksref_trainer_new(TRAIN_LR)
+    loss = C.c_double()
+    P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+    idx = np.arange(n, dtype=np.int64)
+    t0 = time.perf_counter()
+    rc = L.ksref_train_step(h, trn, P(np.ascontiguousarray(tok[:n]), C.c_int32),
+                            P(np.ascontiguousarray(tgt[:n]), C.c_int32), n, threads, 1, 1, P(idx, C.c_int64),
+                            5.0, C.byref(loss))
+    dt = time.perf_counter() - t0
+    L.ksref_trainer_free(trn)
+    L.ksref_free(h)
+    if rc:
+        raise RuntimeError("reference train step failed")
+    return n / dt, dt
+
+
+def run_train_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    path = model_path()
+    tok, tgt, ck = train_data(path, 4096)
+    threads = os.cpu_count() or 1
+    rate0, _ = reference_train_rate(path, tok, tgt, threads, max(threads, 16))
+    n = int(min(4096, max(threads, rate0 * 6.0)))
+    times = []
+    for i in range(args.warmup + args.steps):
+        r, dt = reference_train_rate(path, tok, tgt, threads, n)
+        if i >= args.warmup:
+            times.append(dt)
+    value = n * len(times) / sum(times)
+    out = {"metric": TRAIN_METRIC, "value": value, "unit": TRAIN_UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1000.0 * sum(times) / len(times), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": W["label"] + " (bounded sample per step)", "samples_per_step": n,
+                      "model": "attn n_a=256 n_s=512 n_d=2, dropout 0.2 / recurrent 0.2 (ModelConfig defaults)"},
+           "cpu_baseline": {"value": value, "unit": TRAIN_UNIT, "cores": threads, "kind": "reference",
+                            "sample": f"{n} samples per step: train_model batch body (per-sample tapes over "
+                                      f"parallel_stripes({threads}), clip, Adam)"},
+           "e2e": {"value": value, "unit": TRAIN_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_train(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_10162_b200.train import DataParallelTrainer, shard_batch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    path = model_path()
+    GB = args.configs  # global batch
+    tok, tgt, ck = train_data(path, GB)
+    lo, hi = shard_batch(GB, rank, world)
+    dp = DataParallelTrainer(path, local, world)
+    stream = torch.cuda.current_stream()
+    d_tok = torch.from_numpy(tok[lo:hi]).cuda()
+    d_tgt = torch.from_numpy(tgt[lo:hi]).cuda()
+    d_idx = torch.arange(lo, hi, dtype=torch.int64, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    epoch = [0]
+
+    def step():
+        epoch[0] += 1
+        dp.step(d_tok, d_tgt, d_idx, GB, epoch[0], 1, TRAIN_LR, 5.0, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            step()
+            s1.record(stream)
+            evs.append((s0, s1))
+        torch.cuda.synchronize()
+    launches = dp.tr.launches()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = GB * args.steps / (ms / 1000.0)
+    loss, match = dp.stats()
+
+    # end to end: host (pinned) batch -> H2D, step, loss/matches D2H, every step
+    h_tok = torch.from_numpy(tok[lo:hi]).pin_memory()
+    h_tgt = torch.from_numpy(tgt[lo:hi]).pin_memory()
+    e2e_t = []
+    for i in range(max(2, args.steps // 2) + 1):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a = h_tok.cuda(non_blocking=True)
+        b = h_tgt.cuda(non_blocking=True)
+        epoch[0] += 1
+        dp.step(a, b, d_idx, GB, epoch[0], 1, TRAIN_LR, 5.0, stream)
+        dp.stats()
+        if i:
+            e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = GB * len(e2e_t) / e2e_s
+    fl = train_flops_per_sample(ck)
+    achieved = fl * value / 1e12
+    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import ref_available
+
+            if ref_available():
+                threads = os.cpu_count() or 1
+                r0, _ = reference_train_rate(path, tok, tgt, threads, max(threads, 16))
+                n = int(min(GB, max(threads, r0 * 15.0)))
+                rate, dt = reference_train_rate(path, tok, tgt, threads, n)
+                cpu = {"value": rate, "unit": TRAIN_UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"{n} samples in {dt:.1f} s (train_model batch body, parallel_stripes({threads}))"}
+        except Exception as ex:
+            cpu = {"value": None, "unit": TRAIN_UNIT, "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+    if rank == 0:
+        out = {"metric": TRAIN_METRIC, "value": value, "unit": TRAIN_UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+               "config": {"workload": W["label"], "global_batch": GB, "per_gpu_batch": hi - lo,
+                          "model": "attn n_a=256 n_s=512 n_d=2 (random init), dropout 0.2 / recurrent 0.2 "
+                                   "(ModelConfig defaults), ConvAsm1x1U T_out=8",
+                          "optimizer": f"Adam lr {TRAIN_LR:g}, clip 5.0",
+                          "l2": "flushed (512 MiB write) before every timed step",
+                          "parallelism": f"dp{world} (batch sharded, NCCL all-reduce of gradients)"},
+               "last_loss_per_sample": loss / GB, "last_position_accuracy": match / (GB * ck.T),
+               "e2e": {"value": e2e, "unit": TRAIN_UNIT, "h2d_bytes_per_step": int((hi - lo) * (7 + ck.T) * 4),
+                       "d2h_bytes_per_step": 16, "api": "DataParallelTrainer.step (ks_trainer_loss_grads + "
+                                                        "all-reduce + ks_trainer_apply) from pinned host buffers"},
+               "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                            "frac": achieved / fp32_peak, "traffic": None,
+                            "kernel": "whole step: fp32 cuBLAS SGEMMs (gates fwd, dX, dW) + fused cell/attention/head kernels",
+                            "peak_kind": "nominal fp32 CUDA-core FMA peak (148 SMs x 128 lanes x 2 x 1.965 GHz)",
+                            "flops_per_sample": fl},
+               "cpu_baseline": cpu, "gpu_launches": launches * args.steps, "clocks": clk.summary()}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     global W, KERNEL, BEAM, CONFIGS_PER_GPU
     args = parse()
@@ -404,7 +600,9 @@ def main():
     KERNEL, BEAM, CONFIGS_PER_GPU = W["kernel"], W["beam"], W["configs"]
     if args.configs is None:
         args.configs = CONFIGS_PER_GPU
-    if args.impl == "reference":
+    if W.get("train"):
+        (run_train_reference_arm if args.impl == "reference" else run_train)(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_b200(args)

@@ -31,7 +31,7 @@ def _dense(rng, prefix, n_in, n_out, t):
 
 
 def write_checkpoint(path, kernel="ConvAsm1x1U", variant="attn", n_a=256, n_s=512, n_d=2,
-                     e_size=256, seed=1, input_values=None):
+                     e_size=256, seed=1, input_values=None, dropout=0.0, recurrent_dropout=0.0):
     spec = BUILTIN_SPECS[kernel]
     grids = input_values or input_grids(kernel)
     d_in = sum(len(g) for g in grids)
@@ -56,7 +56,7 @@ def write_checkpoint(path, kernel="ConvAsm1x1U", variant="attn", n_a=256, n_s=51
     lines = ["format: kernelseer-checkpoint/1", f"variant: {variant}", f"kernel: {kernel}",
              "precision: fp32", f"encoder_state_size: {e_size}", f"pre_attention_size: {n_a}",
              f"post_attention_size: {n_s}", f"attention_dense_nodes: {n_d}",
-             "decoder_cell_size: 256", "dropout: 0", "recurrent_dropout: 0",
+             "decoder_cell_size: 256", f"dropout: {dropout:g}", f"recurrent_dropout: {recurrent_dropout:g}",
              "conv_layers: 64,3,1;32,3,1"]
     for f, g in zip(FIELDS, grids):
         lines.append(f"input_vocab.{f}: " + ",".join(str(v) for v in g))
