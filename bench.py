@@ -458,7 +458,7 @@ def run_train_reference_arm(args):
     tok, tgt, ck = train_data(path, 4096)
     threads = os.cpu_count() or 1
     rate0, _ = reference_train_rate(path, tok, tgt, threads, max(threads, 16))
-    n = int(min(4096, max(threads, rate0 * 6.0)))
+    n = int(min(4096, max(256, rate0 * 6.0)))
     times = []
     for i in range(args.warmup + args.steps):
         r, dt = reference_train_rate(path, tok, tgt, threads, n)

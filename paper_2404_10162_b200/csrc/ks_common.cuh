@@ -78,6 +78,32 @@ struct LstmArgs {
     __half* hA_lo;
     long long ldha;
     int ha_bf16;           // split copy as bf16 (BF16 mode) instead of fp16 hi/lo
+    long long ldw;         // tensor-core W row stride in elements (0: K)
+    int wcol;              // tensor-core W column offset (a K sub-range of the packed weight)
+    long long ldah;        // tensor-core A-plane row stride in elements (0: K)
+    // raw mode (the context projection P = a_t . W_ctx): no bias, no cell; the
+    // pre-activations are stored TRANSPOSED and split for the alpha-block MMA:
+    // pt_hi/lo[n][row], n = the tile's N index (gate-interleaved, = W row order)
+    int raw;
+    __half* pt_hi;
+    __half* pt_lo;
+    long long ldt;
+    // alpha-block mode (projected context): the first kb_alpha K-blocks of the B
+    // operand are P^T columns starting at 7 * b0(tile), b0 = first config of the
+    // 128-row tile (rows_per_cfg rows per config); the A operand's first
+    // 64*kb_alpha columns hold each row's alpha_t at 7 * (config - b0) + t
+    int kb_alpha;
+    int rows_per_cfg;
+    const __half* PT_hi;   // P^T planes [4H][ldpt]
+    const __half* PT_lo;
+    long long ldpt;
+    long long pt_rows;     // K extent of P^T (C * 7); reads beyond are zero-filled
+    // fused head (tensor-core epilogue): partial logits of the output head over
+    // the tile's units, hpart[row][slot][hvp] with slot = 2 * n_tile + half; the
+    // beam kernel sums the 2 * H / UNITS slots (models.cpp:490-491)
+    const float* hw;       // [H][hvp] zero-padded head weights (null: no fused head)
+    int hvp;               // padded vocabulary (4, 8 or 16)
+    float* hpart;
 };
 
 struct AttnArgs {
@@ -97,11 +123,20 @@ struct AttnArgs {
     float* uatt_out;       // [C][7][nd] written at position 0
     const float* wo;       // [nd]
     float bo;
-    float* A;              // FP32 operand out [M][NA2+NS]
+    float* A;              // FP32 operand out [M][a_ld]
     __half* A_hi;          // split operand out
     __half* A_lo;
     int split_mode;        // 0 fp32, 1 fp16 hi/lo (F16X3), 2 bf16 hi only (BF16)
+    // alpha-block mode (kalpha > 0): instead of ctx, write the block-diagonal
+    // alpha operand (kalpha columns, alpha_t at 7 * (config - b0(tile)) + t) and
+    // h_prev after it; operand row stride kalpha + NS.  Classic: [ctx ; h_prev].
+    int kalpha;
 };
+
+// Scales of the alpha-block MMA (F16X3): alpha in [0, 1] carries 2^12, P carries
+// 2^4, so alpha.P accumulates at the same 2^16 as the 2^8-scaled h.W terms.
+constexpr float kAlphaScale = 4096.0f;
+constexpr float kPScale = 16.0f;
 
 struct BeamArgs {
     int B;
@@ -113,6 +148,8 @@ struct BeamArgs {
     int final_step;
     int NS;
     const float* h;        // [B*H_cur][NS]
+    const float* hpart;    // [B*H_cur][hslots][VP] fused-head partial logits, or null (GEMV on h)
+    int hslots;
     const float* Wh;       // head weights [NS][V] (padded rows zero)
     const float* bh;       // [V]
     const unsigned char* live_cur;
@@ -179,6 +216,13 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
     const float xs = x * kSplitScale;
     hi = __float2half_rn(xs);
     lo = __float2half_rn(xs - __half2float(hi));   // residual exact in fp32
+}
+
+// Same split at an explicit power-of-two scale (alpha-block operands).
+__device__ __forceinline__ void split_f16s(float x, float scale, __half& hi, __half& lo) {
+    const float xs = x * scale;
+    hi = __float2half_rn(xs);
+    lo = __float2half_rn(xs - __half2float(hi));
 }
 
 __device__ __forceinline__ void store_split_h(const LstmArgs& p, long long idx, float h) {

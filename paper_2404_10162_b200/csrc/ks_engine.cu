@@ -33,6 +33,7 @@ __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long 
 size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tables);
 bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s);
 bool launch_hybrid_conv(const ConvArgs& p, cudaStream_t s);
+bool launch_split_rows(const float* src, long long n, __half* hi, __half* lo, int mode, cudaStream_t s);
 // tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
                     const __half* W_lo0, const __half* W_hi1, const __half* W_lo1,
@@ -137,6 +138,8 @@ struct ks_engine {
     DevMem attWs, attWa, attBh, attWo;
     float attBo = 0.0f;
     std::vector<std::unique_ptr<DevMem>> headW, headB;
+    std::vector<std::unique_ptr<DevMem>> headWp;  // [Hd][VP] zero-padded copies for the fused head
+    DevMem hpart;                                 // fused-head partial logits [R][2 Hd / units][VP]
     DevMem values;
     // workspace
     int64_t chunk = 65536;
@@ -165,7 +168,23 @@ struct ks_engine {
     DevLstm hb1[2], hb2[2];
     DevMem hybA, hybAf, hybC, hybH, feat;
     int num_sms = 148;
+    // projected context (attn / attn-2, tensor-core modes): ctx . W_ctx =
+    // sum_t alpha_t (a_t . W_ctx).  P = a_t . W_ctx is computed once per config
+    // (stored transposed, split: Pt [2][4NS][ldt]); from position 1 on the
+    // decoder GEMM contracts [alpha block | h_prev] against [P^T | W_h]
+    bool ctxproj = false;
+    bool ctxproj_force = false;   // KS_CTXPROJ=force: alpha blocks even where wider than ctx (tests)
+    DevMem Pt, actA;
+    bool proj_at(int pos, int H) const {
+        return ctxproj && pos > 0 && (ctxproj_force || alpha_cols_of(H) < 2 * NA);
+    }
+    static int alpha_cols_of(int H) { return (7 * (127 / H + 2) + 7 + 63) / 64 * 64; }
 };
+
+// Columns of the alpha block for rows_per_cfg rows per config: a 128-row tile
+// spans at most 127 / H + 2 configs, 7 columns each, plus up to 7 columns of
+// 8-alignment of the first (tile_k, ks_gemm_tc.cu), rounded to 64.
+static int alpha_cols(int H) { return ks_engine::alpha_cols_of(H); }
 
 namespace {
 
@@ -455,12 +474,24 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.headB.emplace_back(new DevMem());
         if ((st = upload(*E.headW.back(), Wp.data(), Wp.size() * 4))) return st;
         if ((st = upload(*E.headB.back(), b, (size_t)V * 4))) return st;
+        const int VP = V <= 4 ? 4 : V <= 8 ? 8 : 16;
+        std::vector<float> Wq((size_t)HdP * VP, 0.0f);
+        for (int r = 0; r < HdP; ++r)
+            for (int v = 0; v < V && V <= 16; ++v) Wq[(size_t)r * VP + v] = Wp[(size_t)r * V + v];
+        E.headWp.emplace_back(new DevMem());
+        if ((st = upload(*E.headWp.back(), Wq.data(), Wq.size() * 4))) return st;
     }
     std::vector<long long> vals(E.out_values.begin(), E.out_values.end());
     if ((st = upload(E.values, vals.data(), vals.size() * 8))) return st;
     if (cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking) != cudaSuccess)
         return set_error(KS_ERR_CUDA, "stream creation failed");
     E.beam_smem_max = 227 * 1024;
+    {
+        const char* cp = std::getenv("KS_CTXPROJ");
+        E.ctxproj = (E.variant == KS_VARIANT_ATTN || E.variant == KS_VARIANT_ATTN2) &&
+                    E.precision != KS_PREC_FP32 && !(cp && cp[0] == '0');
+        E.ctxproj_force = cp && std::string(cp) == "force";
+    }
     cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device);
     *out = eng.release();
     return KS_OK;
@@ -652,11 +683,18 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
         if (E.precision == KS_PREC_FP32) {
             ENS(E.Abuf, R * Kd * 4);
         } else {
-            ENS(E.Ahi, R * Kd * 2);
-            ENS(E.Alo, R * Kd * 2);
+            const int64_t lda = E.ctxproj ? std::max<int64_t>(Kd, alpha_cols(1) + Hd) : Kd;
+            ENS(E.Ahi, R * lda * 2);
+            ENS(E.Alo, R * lda * 2);
         }
         ENS(E.hbuf, 2 * R * Hd * 4);
         ENS(E.cbuf, 2 * R * Hd * 4);
+        if (E.precision != KS_PREC_FP32 && std::getenv("KS_FUSED_HEAD")) ENS(E.hpart, R * (2 * Hd / E.tc_units) * 16 * 4);
+        if (E.ctxproj) {
+            const int64_t ldt = (C * 7 + 7) / 8 * 8;
+            ENS(E.Pt, 2 * 4 * (int64_t)Hd * ldt * 2);   // [hi/lo][4NS][ldt] fp16
+            ENS(E.actA, 2 * C * 7 * (int64_t)NA2 * 2);
+        }
     }
     for (int i = 0; i < 2; ++i) {
         ENS(E.live[i], R);
@@ -868,6 +906,35 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         if ((st = launch_lstm(E, a[0], dirs == 2 ? &a[1] : nullptr, E.enc[0], dirs == 2 ? &E.enc[1] : nullptr, fl)))
             return st;
     }
+    bool any_proj = false;
+    for (int pos = 0, h = 1; pos < E.T; h = (int)std::min<int64_t>(k, (int64_t)h * E.vsize[(size_t)pos]), ++pos)
+        any_proj = any_proj || E.proj_at(pos, h);
+    if (any_proj) {
+        // context projection P[c][t] = a_t . W_ctx (the ctx rows of the post-LSTM weight),
+        // one GEMM over the C*7 encoder activations; raw pre-activations, no bias / cell
+        LstmArgs q{};
+        q.M = (int)(C * 7);
+        q.H = Hd;
+        q.K = NA2;
+        q.A = act;
+        q.lda = NA2;
+        __half* ahi = E.actA.as<__half>();
+        __half* alo = ahi + (size_t)C * 7 * NA2;
+        if (!launch_split_rows(act, (long long)C * 7 * NA2, ahi, alo, E.precision == KS_PREC_F16X3 ? 1 : 2, s))
+            return set_error(KS_ERR_CUDA, "split_rows launch failed");
+        E.launches++;
+        q.A_hi = ahi;
+        q.A_lo = alo;
+        q.W = E.dec.W.as<float>();
+        q.G = E.dec.G.as<float>();
+        q.ldw = Kd;                  // tensor-core layout [4H][Kd]: columns 0..NA2 are the ctx rows
+        q.wcol = 0;
+        q.raw = 1;
+        q.ldt = (C * 7 + 7) / 8 * 8;
+        q.pt_hi = E.Pt.as<__half>();
+        q.pt_lo = q.pt_hi + (size_t)4 * Hd * q.ldt;
+        if ((st = launch_lstm(E, q, nullptr, E.dec, nullptr, 0.0))) return st;
+    }
     beam_init<<<(unsigned)((C + 255) / 256), 256, 0, s>>>((int)C, E.live[0].as<unsigned char>(),
                                                           E.lp[0].as<double>(),
                                                           E.key[0].as<unsigned long long>(),
@@ -943,6 +1010,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         aa.A_hi = E.Ahi.as<__half>();
         aa.A_lo = E.Alo.as<__half>();
         aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
+        aa.kalpha = E.proj_at(pos, H) ? alpha_cols(H) : 0;
         if (enc_dec) aa.nd = 0;
         if (!hybrid) {
             if (!launch_attention(aa, pos == 0 && !enc_dec, s))
@@ -979,6 +1047,39 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         p.c_out = cb + (size_t)cur * R * Hd;
         p.ldc = Hd;
         if (enc_dec && pos == 0) p.ldc_prev = He;
+        if (E.ctxproj && pos == 0) {
+            // h = 0 at position 0: contract the ctx columns only
+            p.K = NA2;
+            p.ldah = Kd;
+            p.ldw = Kd;
+            p.wcol = 0;
+        } else if (E.proj_at(pos, H)) {
+            // [alpha block | h_prev] . [P^T | W_h]  (ctx . W_ctx = sum_t alpha_t P_t)
+            const int kal = alpha_cols(H);
+            p.K = kal + Hd;
+            p.ldah = 0;
+            p.ldw = Kd;
+            p.wcol = NA2;
+            p.kb_alpha = kal / 64;
+            p.rows_per_cfg = H;
+            p.PT_hi = E.Pt.as<__half>();
+            p.ldpt = (C * 7 + 7) / 8 * 8;
+            p.PT_lo = p.PT_hi + (size_t)4 * Hd * p.ldpt;
+            p.pt_rows = C * 7;
+        }
+        const int Vp = E.vsize[(size_t)pos];
+        // fused head (partial logits in the gate-GEMM epilogue): halves the beam kernel but
+        // measured net slower (the L2-bound GEMM loses more), so opt-in via KS_FUSED_HEAD=1
+        static const bool fh_env = [] {
+            const char* e = std::getenv("KS_FUSED_HEAD");
+            return e && e[0] == '1';
+        }();
+        const bool fused_head = fh_env && E.precision != KS_PREC_FP32 && Vp <= 16 && !hybrid && p.K > 0;
+        if (fused_head) {
+            p.hw = E.headWp[(size_t)pos]->as<float>();
+            p.hvp = Vp <= 4 ? 4 : Vp <= 8 ? 8 : 16;
+            p.hpart = E.hpart.as<float>();
+        }
         const double useful = 2.0 * (double)M * (double)(2 * E.n_a * (enc_dec ? 0 : 1) + (enc_dec ? E.e : E.n_s)) *
                               4.0 * (enc_dec ? E.e : E.n_s);
         if (!hybrid && (st = launch_lstm(E, p, nullptr, E.dec, nullptr, useful))) return st;
@@ -1026,6 +1127,8 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         b.NS = hybrid ? 2 * E.CP : Hd;
         b.h = hybrid ? E.feat.as<float>() + (size_t)pos * C * 2 * E.CP : hb + (size_t)cur * R * Hd;
         b.h_per_config = hybrid ? 1 : 0;
+        b.hpart = fused_head ? E.hpart.as<float>() : nullptr;
+        b.hslots = 2 * Hd / E.tc_units;
         b.Wh = E.headW[(size_t)pos]->as<float>();
         b.bh = E.headB[(size_t)pos]->as<float>();
         b.live_cur = E.live[cur].as<unsigned char>();

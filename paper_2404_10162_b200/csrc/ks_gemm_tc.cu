@@ -118,6 +118,28 @@ struct TcProblem {
     int tile_begin;  // first global tile index of this problem
 };
 
+// alpha-block mode: K-blocks of one tile.  The B operand's P^T columns start at
+// x0 = 7 * b0 rounded down to 8 (TMA tile loads need 16-byte aligned inner
+// coordinates) and end after the tile's last config; the A operand keeps
+// kb_alpha (max) alpha blocks, of which the tile contracts the first kba_t.
+struct TileK {
+    int kba_t;  // alpha K-blocks this tile contracts
+    int x0;     // first P^T column
+    int nkb;    // total K-blocks of the tile
+};
+__device__ __forceinline__ TileK tile_k(const LstmArgs& p, int k_blocks, int mt) {
+    TileK r{0, 0, k_blocks};
+    if (p.kb_alpha > 0) {
+        const int b0 = (mt * 128) / p.rows_per_cfg;
+        const int b1 = (mt * 128 + 127) / p.rows_per_cfg;
+        r.x0 = (7 * b0) & ~7;
+        r.kba_t = (7 * (b1 + 1) - r.x0 + 63) / 64;
+        if (r.kba_t > p.kb_alpha) r.kba_t = p.kb_alpha;
+        r.nkb = k_blocks - p.kb_alpha + r.kba_t;
+    }
+    return r;
+}
+
 struct TcParams {
     TcProblem prob[2];
     int n_prob;
@@ -211,19 +233,27 @@ __global__ void __launch_bounds__(384, 1)
                 const CUtensorMap* mal = pi ? &mAl1 : &mAl0;
                 const CUtensorMap* mb = pi ? &mB1 : &mB0;
                 const CUtensorMap* mbl = pi ? &mBl1 : &mBl0;
-                for (int kb = 0; kb < pr.k_blocks; ++kb) {
+                // alpha-block mode: B K-blocks [0, kba_t) come from P^T (held in the
+                // second problem's map slots) from column x0 on (see tile_k)
+                const TileK tk = tile_k(pr.p, pr.k_blocks, mt);
+                for (int kb = 0; kb < tk.nkb; ++kb) {
                     tc::mbar_wait(tc::smem_u32(&bars[S + stage]), phase ^ 1);
                     const uint32_t full = tc::smem_u32(&bars[stage]);
                     tc::mbar_expect_tx(full, Cfg::STAGE_BYTES);
                     unsigned char* st = smem + stage * Cfg::STAGE_BYTES;
-                    const int kx = kb * TC_BK;
+                    const bool from_pt = kb < tk.kba_t;
+                    // A: alpha blocks [0, kba_t), then the h columns after all kb_alpha blocks
+                    const int kx = (from_pt ? kb : kb - tk.kba_t + pr.p.kb_alpha) * TC_BK;
+                    const CUtensorMap* bmap = from_pt ? &mB1 : mb;
+                    const CUtensorMap* blmap = from_pt ? &mBl1 : mbl;
+                    const int bx = from_pt ? tk.x0 + kb * TC_BK : (kb - tk.kba_t) * TC_BK;
                     tc::tma_load_2d(tc::smem_u32(st), ma, full, kx, mt * TC_BM);
-                    tc::tma_load_2d(tc::smem_u32(st + Cfg::A_BYTES), mb, full, kx, nt * Cfg::BN);
+                    tc::tma_load_2d(tc::smem_u32(st + Cfg::A_BYTES), bmap, full, bx, nt * Cfg::BN);
                     if (SPLIT) {
                         tc::tma_load_2d(tc::smem_u32(st + Cfg::A_BYTES + Cfg::B_BYTES), mal, full, kx,
                                         mt * TC_BM);
-                        tc::tma_load_2d(tc::smem_u32(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES), mbl, full,
-                                        kx, nt * Cfg::BN);
+                        tc::tma_load_2d(tc::smem_u32(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES), blmap, full,
+                                        bx, nt * Cfg::BN);
                     }
                     if (++stage == S) {
                         stage = 0;
@@ -242,10 +272,12 @@ __global__ void __launch_bounds__(384, 1)
             for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
                 const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
                 const TcProblem& pr = P.prob[pi];
+                const int mt_i = (t - pr.tile_begin) / pr.n_tiles;
+                const int nkb = tile_k(pr.p, pr.k_blocks, mt_i).nkb;
                 tc::mbar_wait(tc::smem_u32(&bars[2 * S + AS + acc]), acc_phase ^ 1);
                 tc::fence_after();
                 const uint32_t d1 = tmem_base + acc * Cfg::ACC_COLS;
-                for (int kb = 0; kb < pr.k_blocks; ++kb) {
+                for (int kb = 0; kb < nkb; ++kb) {
                     tc::mbar_wait(tc::smem_u32(&bars[stage]), phase);
                     tc::fence_after();
                     const uint32_t a0 = tc::smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -295,10 +327,14 @@ __global__ void __launch_bounds__(384, 1)
             const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
             const int row = mt * TC_BM + q * 32 + lane;
             const bool valid = row < p.M;
+            const bool raw = p.raw != 0;
             // per-row gathers issued before waiting on the accumulator
-            const int slot = valid ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0) : 0;
-            const int crow = valid ? (p.parent ? p.parent[row] : row) : -1;
+            const int slot = (valid && !raw) ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0) : 0;
+            const int crow = (valid && !raw) ? (p.parent ? p.parent[row] : row) : -1;
             const float* G = p.G + (long long)slot * 4 * p.H;
+            float hl[16];  // fused head: partial logits over this thread's units
+#pragma unroll
+            for (int v = 0; v < 16; ++v) hl[v] = 0.0f;
             tc::mbar_wait(tc::smem_u32(&bars[2 * S + acc]), acc_phase);
             tc::fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
@@ -309,7 +345,27 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt) tc::tmem_ld8(tbase + gt * UNITS + uc, g[gt]);
                 tc::tmem_wait_ld();
-                if (valid) {
+                if (valid && raw) {
+                    // context projection P = a_t . W_ctx (no bias, no cell), stored
+                    // transposed in the B-operand order of the alpha-block MMA
+                    const float sc = SPLIT ? kSplitUnscale : 1.0f;
+#pragma unroll
+                    for (int gt = 0; gt < 4; ++gt) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const long long n = (long long)nt * Cfg::BN + gt * UNITS + uc + j;
+                            const float v = g[gt][j] * sc;
+                            if (SPLIT) {
+                                __half hi, lo;
+                                split_f16s(v, kPScale, hi, lo);
+                                p.pt_hi[n * p.ldt + row] = hi;
+                                p.pt_lo[n * p.ldt + row] = lo;
+                            } else {
+                                reinterpret_cast<__nv_bfloat16*>(p.pt_hi)[n * p.ldt + row] = __float2bfloat16_rn(v);
+                            }
+                        }
+                    }
+                } else if (valid) {
                     const int u0 = nt * UNITS + uc;
                     float gb[4][8];
 #pragma unroll
@@ -342,6 +398,21 @@ __global__ void __launch_bounds__(384, 1)
                         cv[j] = cn;
                         hv[j] = sigm_fast(go) * tanh_fast(cn);
                     }
+                    if (p.hw != nullptr) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4* w4 = reinterpret_cast<const float4*>(p.hw + (long long)(u0 + j) * p.hvp);
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4) {
+                                if (4 * q4 >= p.hvp) break;
+                                const float4 w = w4[q4];
+                                hl[4 * q4 + 0] = fmaf(hv[j], w.x, hl[4 * q4 + 0]);
+                                hl[4 * q4 + 1] = fmaf(hv[j], w.y, hl[4 * q4 + 1]);
+                                hl[4 * q4 + 2] = fmaf(hv[j], w.z, hl[4 * q4 + 2]);
+                                hl[4 * q4 + 3] = fmaf(hv[j], w.w, hl[4 * q4 + 3]);
+                            }
+                        }
+                    }
                     float4* hd = reinterpret_cast<float4*>(p.h_out + (long long)row * p.ldh + u0);
                     float4* cd = reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u0);
                     hd[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
@@ -369,6 +440,12 @@ __global__ void __launch_bounds__(384, 1)
                             *reinterpret_cast<const uint4*>(hl);
                     }
                 }
+            }
+            if (p.hw != nullptr && valid) {
+                float4* o = reinterpret_cast<float4*>(p.hpart + ((long long)row * 2 * pr.n_tiles + 2 * nt + half) * p.hvp);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+                    if (4 * q4 < p.hvp) o[q4] = make_float4(hl[4 * q4], hl[4 * q4 + 1], hl[4 * q4 + 2], hl[4 * q4 + 3]);
             }
             tc::fence_before();
             __syncwarp();
@@ -459,15 +536,29 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         pr.k_blocks = a.K / TC_BK;
         pr.tile_begin = tiles;
         tiles += pr.m_tiles * pr.n_tiles;
-        // A planes: [M][K] with row stride K (decoder operand / encoder split h)
-        const long long lda = a.K;
+        // A planes: [M][K] with row stride ldah (default K)
+        const long long lda = a.ldah ? a.ldah : a.K;
         if (!make_map(&maps[4 * i + 0], a.A_hi, a.M, a.K, lda, TC_BM)) return false;
         if (!make_map(&maps[4 * i + 1], SPLIT ? a.A_lo : a.A_hi, a.M, a.K, lda, TC_BM)) return false;
-        if (!make_map(&maps[4 * i + 2], wh[i], 4LL * a.H, a.K, a.K, Cfg::BN)) return false;
-        if (!make_map(&maps[4 * i + 3], SPLIT ? wl[i] : wh[i], 4LL * a.H, a.K, a.K, Cfg::BN)) return false;
+        // W planes: the K range after the alpha blocks, at column offset wcol
+        const long long ldw = a.ldw ? a.ldw : a.K;
+        const long long kw = a.K - (long long)a.kb_alpha * TC_BK;
+        const __half* w0 = wh[i] + a.wcol;
+        const __half* w1 = (SPLIT ? wl[i] : wh[i]) + a.wcol;
+        if (!make_map(&maps[4 * i + 2], w0, 4LL * a.H, kw, ldw, Cfg::BN)) return false;
+        if (!make_map(&maps[4 * i + 3], w1, 4LL * a.H, kw, ldw, Cfg::BN)) return false;
     }
-    if (P.n_prob == 1)
+    if (P.n_prob == 1) {
         for (int j = 4; j < 8; ++j) maps[j] = maps[j - 4];
+        if (a0.kb_alpha > 0) {  // P^T planes in the second problem's B slots
+            if (a0.kb_alpha * TC_BK > a0.K) return false;
+            if (!make_map(&maps[6], a0.PT_hi, 4LL * a0.H, a0.pt_rows, a0.ldpt, Cfg::BN)) return false;
+            if (!make_map(&maps[7], SPLIT ? a0.PT_lo : a0.PT_hi, 4LL * a0.H, a0.pt_rows, a0.ldpt, Cfg::BN))
+                return false;
+        }
+    } else if (a0.kb_alpha > 0 || (a1 && a1->kb_alpha > 0)) {
+        return false;
+    }
     P.total_tiles = tiles;
     const int grid = tiles < sm_count() ? tiles : sm_count();
     lstm_gemm_tc<UNITS, SPLIT><<<grid, 384, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3], maps[4],

@@ -16,6 +16,7 @@
 //   beam_search_impl      src/decoding.cpp:27-103 (children, 1e-300 floor, predicate
 //                         order, BeamExhaustedError, sort by (lp desc, prefix asc))
 //   greedy_decode         src/decoding.cpp:107-124 (strict '>' argmax)
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -186,6 +187,41 @@ __device__ __forceinline__ void store4(const AttnArgs& p, long long idx, float4 
     store4p<SPLIT>(p.A, p.A_hi, p.A_lo, idx, v);
 }
 
+// Alpha-block operand of the projected-context GEMM (row r of config b): the
+// first kalpha columns hold alpha_t at 7 * (b - b0) + t, b0 = first config of
+// r's 128-row tile, zeros elsewhere (written by the lanes of one warp).
+template <int SPLIT>
+__device__ __forceinline__ void write_alpha_block(const AttnArgs& p, int r, int b, const float (&al)[kTin],
+                                                  int lane) {
+    // column of alpha_0 = 7 * b - x0, x0 = 7 * b0 rounded down to 8 (see tile_k, ks_gemm_tc.cu)
+    const int b0 = ((r >> 7) << 7) / p.H_rows;
+    const int c0 = kTin * b - ((kTin * b0) & ~7);
+    const long long base = (long long)r * (p.kalpha + p.NS);
+    for (int c = lane; c < p.kalpha / 8; c += 32) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int idx = 8 * c + j - c0;
+            float x = 0.0f;
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) x = idx == t ? al[t] : x;
+            v[j] = x;
+        }
+        if (SPLIT == 1) {
+            __align__(16) __half hi[8], lo[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) split_f16s(v[j], kAlphaScale, hi[j], lo[j]);
+            *reinterpret_cast<uint4*>(p.A_hi + base + 8 * c) = *reinterpret_cast<const uint4*>(hi);
+            *reinterpret_cast<uint4*>(p.A_lo + base + 8 * c) = *reinterpret_cast<const uint4*>(lo);
+        } else {
+            __align__(16) __nv_bfloat16 hb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hb[j] = __float2bfloat16_rn(v[j]);
+            *reinterpret_cast<uint4*>(p.A_hi + base + 8 * c) = *reinterpret_cast<const uint4*>(hb);
+        }
+    }
+}
+
 template <int ND, int SPLIT, bool FIRST>
 __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -194,7 +230,8 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
     const int b = r / p.H_rows;
     const int par = p.parent ? p.parent[r] : r;
     const float* s = (p.h_prev != nullptr && par >= 0) ? p.h_prev + (long long)par * p.ldh : nullptr;
-    const int Kd = p.NA2 + p.NS;
+    const int Kd = p.kalpha ? p.kalpha + p.NS : p.NA2 + p.NS;
+    const int hc = p.kalpha ? p.kalpha : p.NA2;  // column of h_prev in the operand
     const long long base = (long long)r * Kd;
     float sd[ND > 0 ? ND : 1];
 #pragma unroll
@@ -208,7 +245,7 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
 #pragma unroll
                 for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], p.Ws[(4 * c + e) * ND + d], sd[d]);
         }
-        store4<SPLIT>(p, base + p.NA2 + 4 * c, v);
+        store4<SPLIT>(p, base + hc + 4 * c, v);
     }
     if (ND == 0) return;  // enc-dec: the operand is h_prev only
 #pragma unroll
@@ -260,6 +297,10 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
     const float inv = 1.0f / sum;
 #pragma unroll
     for (int t = 0; t < kTin; ++t) e[t] *= inv;
+    if (SPLIT != 0 && p.kalpha) {  // projected context: alpha . P^T on the tensor cores
+        write_alpha_block<SPLIT>(p, r, b, e, lane);
+        return;
+    }
     for (int c = lane; c < p.NA2 / 4; c += 32) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -282,7 +323,8 @@ __global__ void __launch_bounds__(256, 3) attention_cfg_t(AttnArgs p) {
     const int H = p.H_rows;
     const int b = blockIdx.x * (blockDim.x >> 5) + warp;
     if ((long long)b * H >= p.M) return;
-    const int Kd = p.NA2 + p.NS;
+    const int Kd = p.kalpha ? p.kalpha + p.NS : p.NA2 + p.NS;
+    const int hc = p.kalpha ? p.kalpha : p.NA2;
     const float* act = p.act + (long long)b * kTin * p.NA2;
     constexpr int G = 4;
     for (int i0 = 0; i0 < H; i0 += G) {
@@ -305,7 +347,7 @@ __global__ void __launch_bounds__(256, 3) attention_cfg_t(AttnArgs p) {
                 for (int e = 0; e < 4; ++e)
 #pragma unroll
                     for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], p.Ws[(4 * c + e) * ND + d], sd[d]);
-                store4<SPLIT>(p, (long long)r * Kd + p.NA2 + 4 * c, v);
+                store4<SPLIT>(p, (long long)r * Kd + hc + 4 * c, v);
             }
             if (ND == 0) continue;
 #pragma unroll
@@ -329,8 +371,14 @@ __global__ void __launch_bounds__(256, 3) attention_cfg_t(AttnArgs p) {
             const float inv = 1.0f / sum;
 #pragma unroll
             for (int t = 0; t < kTin; ++t) al[ii][t] *= inv;
+            if (SPLIT != 0 && p.kalpha) {
+                float a7[kTin];
+#pragma unroll
+                for (int t = 0; t < kTin; ++t) a7[t] = al[ii][t];
+                write_alpha_block<SPLIT>(p, r, b, a7, lane);
+            }
         }
-        if (ND == 0) continue;
+        if (ND == 0 || p.kalpha) continue;
 #pragma unroll 2
         for (int c = lane; c < p.NA2 / 4; c += 32) {
             float4 at[kTin];
@@ -364,7 +412,8 @@ __global__ void __launch_bounds__(128) attention_cta_t(AttnArgs p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int H = p.H_rows;
     const int b = blockIdx.x;
-    const int Kd = p.NA2 + p.NS;
+    const int Kd = p.kalpha ? p.kalpha + p.NS : p.NA2 + p.NS;
+    const int hc = p.kalpha ? p.kalpha : p.NA2;
     for (int i = warp; i < H; i += 4) {
         const int r = b * H + i;
         const int par = p.parent ? p.parent[r] : r;
@@ -380,7 +429,7 @@ __global__ void __launch_bounds__(128) attention_cta_t(AttnArgs p) {
             for (int e = 0; e < 4; ++e)
 #pragma unroll
                 for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], p.Ws[(4 * c + e) * ND + d], sd[d]);
-            store4<SPLIT>(p, (long long)r * Kd + p.NA2 + 4 * c, v);
+            store4<SPLIT>(p, (long long)r * Kd + hc + 4 * c, v);
         }
         if (ND == 0) continue;
 #pragma unroll
@@ -403,6 +452,12 @@ __global__ void __launch_bounds__(128) attention_cta_t(AttnArgs p) {
             sum += e[t];
         }
         const float inv = 1.0f / sum;
+        if (SPLIT != 0 && p.kalpha) {
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) e[t] *= inv;
+            write_alpha_block<SPLIT>(p, r, b, e, lane);
+            continue;
+        }
         if (lane < kTin) {
             float my = e[0];
 #pragma unroll
@@ -411,7 +466,7 @@ __global__ void __launch_bounds__(128) attention_cta_t(AttnArgs p) {
             alpha[i][lane] = my * inv;
         }
     }
-    if (ND == 0) return;
+    if (ND == 0 || p.kalpha) return;
     __syncthreads();
     const float* act = p.act + (long long)b * kTin * p.NA2;
     for (int c = threadIdx.x; c < p.NA2 / 4; c += blockDim.x) {
@@ -472,6 +527,26 @@ bool launch_attention(const AttnArgs& p, bool first, cudaStream_t s) {
     if (p.split_mode == 0) return launch_attention_split<0>(p, first, s);
     if (p.split_mode == 1) return launch_attention_split<1>(p, first, s);
     return launch_attention_split<2>(p, first, s);
+}
+
+// ---------------------------------------------------------------------------
+// split_rows: fp32 -> the tensor-core operand planes (fp16 hi/lo or bf16),
+// for the encoder activations a_t feeding the context projection P.
+// ---------------------------------------------------------------------------
+template <int SPLIT>
+__global__ void split_rows_t(const float* src, long long n4, __half* hi, __half* lo) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
+        store4p<SPLIT>(nullptr, hi, lo, 4 * i, reinterpret_cast<const float4*>(src)[i]);
+}
+
+bool launch_split_rows(const float* src, long long n, __half* hi, __half* lo, int mode, cudaStream_t s) {
+    const long long n4 = n / 4;
+    const unsigned grid = (unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16);
+    if (mode == 1)
+        split_rows_t<1><<<grid, 256, 0, s>>>(src, n4, hi, lo);
+    else
+        split_rows_t<2><<<grid, 256, 0, s>>>(src, n4, hi, lo);
+    return cudaGetLastError() == cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------
@@ -680,36 +755,53 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                 continue;
             }
             // head logits for rows j0, j0+1: logits[v] = b[v] + sum_i h[i] W[i][v]  (models.cpp:490-491)
-            float p0[VP], p1[VP];
+            float lg[2] = {0.0f, 0.0f};
+            if (a.hpart != nullptr) {
+                // fused head: the gate GEMM's epilogue left per-tile partial logits;
+                // lane v sums its token's slots in a fixed order
+                if (lane < VP) {
 #pragma unroll
-            for (int v = 0; v < VP; ++v) {
-                p0[v] = 0.0f;
-                p1[v] = 0.0f;
-            }
-            // hybrid variants: every hypothesis of config b reads the same feature row
-            const float* h0 = a.h + (a.h_per_config ? (long long)b : r0) * a.NS;
-            const float* h1 = a.h_per_config ? h0 : h0 + a.NS;
-#pragma unroll 4
-            for (int i = lane; i < a.NS; i += 32) {
-                const float x0 = live0 ? h0[i] : 0.0f;
-                const float x1 = live1 ? h1[i] : 0.0f;
-                const float4* w4 = reinterpret_cast<const float4*>(Wsh + i * WS);
-#pragma unroll
-                for (int q = 0; q < VP / 4; ++q) {
-                    const float4 w = w4[q];
-                    p0[4 * q + 0] = fmaf(x0, w.x, p0[4 * q + 0]);
-                    p0[4 * q + 1] = fmaf(x0, w.y, p0[4 * q + 1]);
-                    p0[4 * q + 2] = fmaf(x0, w.z, p0[4 * q + 2]);
-                    p0[4 * q + 3] = fmaf(x0, w.w, p0[4 * q + 3]);
-                    p1[4 * q + 0] = fmaf(x1, w.x, p1[4 * q + 0]);
-                    p1[4 * q + 1] = fmaf(x1, w.y, p1[4 * q + 1]);
-                    p1[4 * q + 2] = fmaf(x1, w.z, p1[4 * q + 2]);
-                    p1[4 * q + 3] = fmaf(x1, w.w, p1[4 * q + 3]);
+                    for (int jj = 0; jj < 2; ++jj) {
+                        if (!(jj == 0 ? live0 : live1)) continue;
+                        const float* hp = a.hpart + (r0 + jj) * (long long)a.hslots * VP + lane;
+                        float acc = 0.0f;
+                        for (int q = 0; q < a.hslots; ++q) acc += hp[q * VP];
+                        lg[jj] = acc;
+                    }
                 }
+            } else {
+                float p0[VP], p1[VP];
+#pragma unroll
+                for (int v = 0; v < VP; ++v) {
+                    p0[v] = 0.0f;
+                    p1[v] = 0.0f;
+                }
+                // hybrid variants: every hypothesis of config b reads the same feature row
+                const float* h0 = a.h + (a.h_per_config ? (long long)b : r0) * a.NS;
+                const float* h1 = a.h_per_config ? h0 : h0 + a.NS;
+#pragma unroll 4
+                for (int i = lane; i < a.NS; i += 32) {
+                    const float x0 = live0 ? h0[i] : 0.0f;
+                    const float x1 = live1 ? h1[i] : 0.0f;
+                    const float4* w4 = reinterpret_cast<const float4*>(Wsh + i * WS);
+#pragma unroll
+                    for (int q = 0; q < VP / 4; ++q) {
+                        const float4 w = w4[q];
+                        p0[4 * q + 0] = fmaf(x0, w.x, p0[4 * q + 0]);
+                        p0[4 * q + 1] = fmaf(x0, w.y, p0[4 * q + 1]);
+                        p0[4 * q + 2] = fmaf(x0, w.z, p0[4 * q + 2]);
+                        p0[4 * q + 3] = fmaf(x0, w.w, p0[4 * q + 3]);
+                        p1[4 * q + 0] = fmaf(x1, w.x, p1[4 * q + 0]);
+                        p1[4 * q + 1] = fmaf(x1, w.y, p1[4 * q + 1]);
+                        p1[4 * q + 2] = fmaf(x1, w.z, p1[4 * q + 2]);
+                        p1[4 * q + 3] = fmaf(x1, w.w, p1[4 * q + 3]);
+                    }
+                }
+                const float s0 = reduce_scatter<VP>(p0, lane);
+                const float s1 = reduce_scatter<VP>(p1, lane);
+                lg[0] = __shfl_sync(0xffffffffu, s0, my_src);
+                lg[1] = __shfl_sync(0xffffffffu, s1, my_src);
             }
-            const float s0 = reduce_scatter<VP>(p0, lane);
-            const float s1 = reduce_scatter<VP>(p1, lane);
-            const float lg[2] = {__shfl_sync(0xffffffffu, s0, my_src), __shfl_sync(0xffffffffu, s1, my_src)};
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
                 const int j = j0 + jj;

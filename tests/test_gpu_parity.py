@@ -173,3 +173,20 @@ def test_default_size_trained_parity(precision):
     n, ties, bad = compare_beams(g, a)
     assert n >= 0.9 * len(tok)
     assert not bad, f"{len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
+@pytest.mark.parametrize("mode", ["force", "0"])
+@pytest.mark.parametrize("stem", ["attn_small_trained", "tiny_attn_s3423", "tiny_attn2_s3423", "tiny_attn_s434"])
+def test_projected_context_modes(stem, mode, monkeypatch):
+    """KS_CTXPROJ: "force" runs every position > 0 through the alpha-block GEMM
+    ([alpha | h] . [P^T | W_h], ctx . W_ctx = sum_t alpha_t (a_t . W_ctx)) even
+    where the auto rule would keep the classic [ctx ; h] operand; "0" disables
+    it.  Both must meet the parity bar against the oracle."""
+    monkeypatch.setenv("KS_CTXPROJ", mode)
+    path = golden_path(stem + ".ckpt")
+    o, e = OracleModel(path), engine(path, "f16x3")
+    tok = random_tokens(o, 512, 21)
+    for k in (2, 5, 16):
+        a, g = o.beam(tok, k, threads=8), e.beam(tok, k)
+        n, ties, bad = compare_beams(g, a)
+        assert not bad, f"k={k}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
