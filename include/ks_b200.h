@@ -224,6 +224,11 @@ double ks_engine_profile_gemm_ms(const ks_engine* eng, int64_t* launches, double
 /* Per-launch view of the same profile: fills up to cap (ms, useful FLOPs)
  * pairs in launch order and returns the number of launches recorded. */
 int64_t ks_engine_profile_launches(const ks_engine* eng, int64_t cap, double* ms, double* useful_flops);
+/* Same, plus the FLOPs each launch issues to the tensor pipe (F16X3: three MMA
+ * passes; the projected-context GEMMs contract fewer columns than the
+ * reference's formula counts as useful). */
+int64_t ks_engine_profile_launches_ex(const ks_engine* eng, int64_t cap, double* ms, double* useful_flops,
+                                      double* mma_issued_flops);
 
 
 /* ------------------------------------------------------------------------- */

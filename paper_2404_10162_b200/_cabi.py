@@ -82,6 +82,7 @@ EXPORTS = [
     "ks_engine_precision", "ks_engine_last_launch_count", "ks_engine_set_chunk",
     "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
     "ks_engine_profile_reset", "ks_engine_profile_gemm_ms", "ks_engine_profile_launches",
+    "ks_engine_profile_launches_ex",
     "ks_beam_search_batch_hooked",
     "ks_trainer_create", "ks_trainer_create_from_checkpoint", "ks_trainer_destroy",
     "ks_trainer_num_params", "ks_trainer_last_launch_count", "ks_trainer_loss_grads",
@@ -134,6 +135,8 @@ def lib():
     L.ks_engine_profile_gemm_ms.restype = dbl
     L.ks_engine_profile_launches.argtypes = [vp, i64, P(dbl), P(dbl)]
     L.ks_engine_profile_launches.restype = i64
+    L.ks_engine_profile_launches_ex.argtypes = [vp, i64, P(dbl), P(dbl), P(dbl)]
+    L.ks_engine_profile_launches_ex.restype = i64
     L.ks_trainer_create.argtypes = [P(KsModelDesc), dbl, dbl, i32, P(vp)]
     L.ks_trainer_create_from_checkpoint.argtypes = [C.c_char_p, i32, P(vp)]
     L.ks_trainer_destroy.argtypes = [vp]
@@ -250,11 +253,13 @@ class Engine:
         lib().ks_engine_profile_reset(self._h, int(enable))
 
     def profile_launches(self):
+        """Per gate-GEMM launch of the last profiled call: (ms, useful FLOPs by the
+        reference formula, FLOPs issued to the tensor pipe)."""
         n = lib().ks_engine_profile_launches(self._h, 0, None, None)
-        ms = np.zeros(n)
-        fl = np.zeros(n)
-        lib().ks_engine_profile_launches(self._h, n, _p(ms, C.c_double), _p(fl, C.c_double))
-        return ms, fl
+        ms, fl, ex = np.zeros(n), np.zeros(n), np.zeros(n)
+        lib().ks_engine_profile_launches_ex(self._h, n, _p(ms, C.c_double), _p(fl, C.c_double),
+                                            _p(ex, C.c_double))
+        return ms, fl, ex
 
     def profile(self):
         n = C.c_int64(0)

@@ -155,9 +155,10 @@ struct ks_engine {
     // profiling of the gate GEMM launches
     bool prof = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
-    std::vector<double> prof_flops;
+    std::vector<double> prof_flops, prof_exec;
     double prof_ms = 0.0, prof_useful = 0.0;
     std::vector<std::pair<double, double>> prof_each;  // per GEMM launch: (ms, useful FLOPs)
+    std::vector<double> prof_each_exec;                // per GEMM launch: MMA FLOPs issued
     int64_t prof_n = 0;
     int tc_units = 64;
     // hybrid-2 (models.cpp:296-371, 409-425)
@@ -739,6 +740,25 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
         cudaEventRecord(ev1, E.stream);
         E.prof_ev.emplace_back(ev0, ev1);
         E.prof_flops.push_back(useful_flops);
+        // FLOPs the tensor pipe issues: 2 M K 4H per MMA pass (3 passes in F16X3); in
+        // alpha-block mode K varies per 128-row tile (tile_k, ks_gemm_tc.cu)
+        auto exec_of = [&](const LstmArgs& a) {
+            if (a.K <= 0) return 0.0;
+            const double passes = E.precision == KS_PREC_F16X3 ? 3.0 : 1.0;
+            double rowk = (double)a.M * a.K;
+            if (a.kb_alpha > 0) {
+                rowk = 0.0;
+                for (int mt = 0; mt * 128 < a.M; ++mt) {
+                    const int b0 = mt * 128 / a.rows_per_cfg, b1 = (mt * 128 + 127) / a.rows_per_cfg;
+                    const int x0 = (7 * b0) & ~7;
+                    const int kba = std::min(a.kb_alpha, (7 * (b1 + 1) - x0 + 63) / 64);
+                    const int rows = std::min(128, a.M - mt * 128);
+                    rowk += (double)rows * (a.K - 64.0 * (a.kb_alpha - kba));
+                }
+            }
+            return 2.0 * rowk * 4.0 * a.H * passes;
+        };
+        E.prof_exec.push_back(exec_of(a0) + (a1 ? exec_of(*a1) : 0.0));
     }
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("lstm launch: ") + cudaGetErrorString(err));
@@ -1204,11 +1224,13 @@ ks_status collect_profile(ks_engine& E) {
         E.prof_useful += E.prof_flops[i];
         E.prof_n++;
         E.prof_each.emplace_back(ms, E.prof_flops[i]);
+        E.prof_each_exec.push_back(E.prof_exec[i]);
         cudaEventDestroy(E.prof_ev[i].first);
         cudaEventDestroy(E.prof_ev[i].second);
     }
     E.prof_ev.clear();
     E.prof_flops.clear();
+    E.prof_exec.clear();
     return KS_OK;
 }
 
@@ -1364,6 +1386,7 @@ extern "C" void ks_engine_profile_reset(ks_engine* eng, int32_t enable) {
     eng->prof_useful = 0.0;
     eng->prof_n = 0;
     eng->prof_each.clear();
+    eng->prof_each_exec.clear();
 }
 
 extern "C" int64_t ks_engine_profile_launches(const ks_engine* eng, int64_t cap, double* ms, double* useful) {
@@ -1373,6 +1396,14 @@ extern "C" int64_t ks_engine_profile_launches(const ks_engine* eng, int64_t cap,
         if (ms) ms[i] = eng->prof_each[(size_t)i].first;
         if (useful) useful[i] = eng->prof_each[(size_t)i].second;
     }
+    return n;
+}
+
+extern "C" int64_t ks_engine_profile_launches_ex(const ks_engine* eng, int64_t cap, double* ms, double* useful,
+                                                 double* mma_issued) {
+    if (!eng) return 0;
+    const int64_t n = ks_engine_profile_launches(eng, cap, ms, useful);
+    for (int64_t i = 0; i < n && i < cap && mma_issued; ++i) mma_issued[i] = eng->prof_each_exec[(size_t)i];
     return n;
 }
 
