@@ -98,12 +98,6 @@ struct LstmArgs {
     const __half* PT_lo;
     long long ldpt;
     long long pt_rows;     // K extent of P^T (C * 7); reads beyond are zero-filled
-    // fused head (tensor-core epilogue): partial logits of the output head over
-    // the tile's units, hpart[row][slot][hvp] with slot = 2 * n_tile + half; the
-    // beam kernel sums the 2 * H / UNITS slots (models.cpp:490-491)
-    const float* hw;       // [H][hvp] zero-padded head weights (null: no fused head)
-    int hvp;               // padded vocabulary (4, 8 or 16)
-    float* hpart;
 };
 
 struct AttnArgs {
@@ -148,8 +142,6 @@ struct BeamArgs {
     int final_step;
     int NS;
     const float* h;        // [B*H_cur][NS]
-    const float* hpart;    // [B*H_cur][hslots][VP] fused-head partial logits, or null (GEMV on h)
-    int hslots;
     const float* Wh;       // head weights [NS][V] (padded rows zero)
     const float* bh;       // [V]
     const unsigned char* live_cur;

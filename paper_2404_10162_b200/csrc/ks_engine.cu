@@ -138,8 +138,6 @@ struct ks_engine {
     DevMem attWs, attWa, attBh, attWo;
     float attBo = 0.0f;
     std::vector<std::unique_ptr<DevMem>> headW, headB;
-    std::vector<std::unique_ptr<DevMem>> headWp;  // [Hd][VP] zero-padded copies for the fused head
-    DevMem hpart;                                 // fused-head partial logits [R][2 Hd / units][VP]
     DevMem values;
     // workspace
     int64_t chunk = 65536;
@@ -475,12 +473,6 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.headB.emplace_back(new DevMem());
         if ((st = upload(*E.headW.back(), Wp.data(), Wp.size() * 4))) return st;
         if ((st = upload(*E.headB.back(), b, (size_t)V * 4))) return st;
-        const int VP = V <= 4 ? 4 : V <= 8 ? 8 : 16;
-        std::vector<float> Wq((size_t)HdP * VP, 0.0f);
-        for (int r = 0; r < HdP; ++r)
-            for (int v = 0; v < V && V <= 16; ++v) Wq[(size_t)r * VP + v] = Wp[(size_t)r * V + v];
-        E.headWp.emplace_back(new DevMem());
-        if ((st = upload(*E.headWp.back(), Wq.data(), Wq.size() * 4))) return st;
     }
     std::vector<long long> vals(E.out_values.begin(), E.out_values.end());
     if ((st = upload(E.values, vals.data(), vals.size() * 8))) return st;
@@ -690,7 +682,6 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
         }
         ENS(E.hbuf, 2 * R * Hd * 4);
         ENS(E.cbuf, 2 * R * Hd * 4);
-        if (E.precision != KS_PREC_FP32 && std::getenv("KS_FUSED_HEAD")) ENS(E.hpart, R * (2 * Hd / E.tc_units) * 16 * 4);
         if (E.ctxproj) {
             const int64_t ldt = (C * 7 + 7) / 8 * 8;
             ENS(E.Pt, 2 * 4 * (int64_t)Hd * ldt * 2);   // [hi/lo][4NS][ldt] fp16
@@ -1087,19 +1078,6 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.PT_lo = p.PT_hi + (size_t)4 * Hd * p.ldpt;
             p.pt_rows = C * 7;
         }
-        const int Vp = E.vsize[(size_t)pos];
-        // fused head (partial logits in the gate-GEMM epilogue): halves the beam kernel but
-        // measured net slower (the L2-bound GEMM loses more), so opt-in via KS_FUSED_HEAD=1
-        static const bool fh_env = [] {
-            const char* e = std::getenv("KS_FUSED_HEAD");
-            return e && e[0] == '1';
-        }();
-        const bool fused_head = fh_env && E.precision != KS_PREC_FP32 && Vp <= 16 && !hybrid && p.K > 0;
-        if (fused_head) {
-            p.hw = E.headWp[(size_t)pos]->as<float>();
-            p.hvp = Vp <= 4 ? 4 : Vp <= 8 ? 8 : 16;
-            p.hpart = E.hpart.as<float>();
-        }
         const double useful = 2.0 * (double)M * (double)(2 * E.n_a * (enc_dec ? 0 : 1) + (enc_dec ? E.e : E.n_s)) *
                               4.0 * (enc_dec ? E.e : E.n_s);
         if (!hybrid && (st = launch_lstm(E, p, nullptr, E.dec, nullptr, useful))) return st;
@@ -1147,8 +1125,6 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         b.NS = hybrid ? 2 * E.CP : Hd;
         b.h = hybrid ? E.feat.as<float>() + (size_t)pos * C * 2 * E.CP : hb + (size_t)cur * R * Hd;
         b.h_per_config = hybrid ? 1 : 0;
-        b.hpart = fused_head ? E.hpart.as<float>() : nullptr;
-        b.hslots = 2 * Hd / E.tc_units;
         b.Wh = E.headW[(size_t)pos]->as<float>();
         b.bh = E.headB[(size_t)pos]->as<float>();
         b.live_cur = E.live[cur].as<unsigned char>();

@@ -332,19 +332,57 @@ __global__ void __launch_bounds__(384, 1)
             const int slot = (valid && !raw) ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0) : 0;
             const int crow = (valid && !raw) ? (p.parent ? p.parent[row] : row) : -1;
             const float* G = p.G + (long long)slot * 4 * p.H;
-            float hl[16];  // fused head: partial logits over this thread's units
+            const bool cell = valid && !raw;
+            const bool have_c = cell && p.c_prev != nullptr && crow >= 0;
+            // G[slot] and c_prev of the next chunk are loaded while the current one
+            // computes (chunk 0's before waiting on the accumulator): the epilogue is
+            // latency bound, and at small K (the encoder) it paces the whole GEMM
+            float gbn[4][8], cpn[8];
+            auto load_bc = [&](int c, float (&gbx)[4][8], float (&cpx)[8]) {
+                const int u0 = nt * UNITS + half * HU + c * 8;
 #pragma unroll
-            for (int v = 0; v < 16; ++v) hl[v] = 0.0f;
+                for (int gt = 0; gt < 4; ++gt) {
+                    float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+                    if (cell) {
+                        b0 = *reinterpret_cast<const float4*>(G + gt * p.H + u0);
+                        b1 = *reinterpret_cast<const float4*>(G + gt * p.H + u0 + 4);
+                    }
+                    gbx[gt][0] = b0.x; gbx[gt][1] = b0.y; gbx[gt][2] = b0.z; gbx[gt][3] = b0.w;
+                    gbx[gt][4] = b1.x; gbx[gt][5] = b1.y; gbx[gt][6] = b1.z; gbx[gt][7] = b1.w;
+                }
+                float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+                if (have_c) {
+                    c0 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0);
+                    c1 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0 + 4);
+                }
+                cpx[0] = c0.x; cpx[1] = c0.y; cpx[2] = c0.z; cpx[3] = c0.w;
+                cpx[4] = c1.x; cpx[5] = c1.y; cpx[6] = c1.z; cpx[7] = c1.w;
+            };
+            load_bc(0, gbn, cpn);
             tc::mbar_wait(tc::smem_u32(&bars[2 * S + acc]), acc_phase);
             tc::fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
+            constexpr int NCH = HU / 8;
 #pragma unroll 1
-            for (int c = 0; c < HU / 8; ++c) {
+            for (int c = 0; c < NCH; ++c) {
                 const int uc = half * HU + c * 8;  // unit offset within the tile
                 float g[4][8];
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt) tc::tmem_ld8(tbase + gt * UNITS + uc, g[gt]);
                 tc::tmem_wait_ld();
+                if (c == NCH - 1) {  // this warp's TMEM reads are done: release the accumulator
+                    tc::fence_before();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&bars[2 * S + AS + acc]));
+                }
+                float gb[4][8], cp[8];
+#pragma unroll
+                for (int gt = 0; gt < 4; ++gt)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) gb[gt][j] = gbn[gt][j];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cp[j] = cpn[j];
+                if (c + 1 < NCH) load_bc(c + 1, gbn, cpn);
                 if (valid && raw) {
                     // context projection P = a_t . W_ctx (no bias, no cell), stored
                     // transposed in the B-operand order of the alpha-block MMA
@@ -367,24 +405,6 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 } else if (valid) {
                     const int u0 = nt * UNITS + uc;
-                    float gb[4][8];
-#pragma unroll
-                    for (int gt = 0; gt < 4; ++gt) {
-                        const float4 b0 = *reinterpret_cast<const float4*>(G + gt * p.H + u0);
-                        const float4 b1 = *reinterpret_cast<const float4*>(G + gt * p.H + u0 + 4);
-                        gb[gt][0] = b0.x; gb[gt][1] = b0.y; gb[gt][2] = b0.z; gb[gt][3] = b0.w;
-                        gb[gt][4] = b1.x; gb[gt][5] = b1.y; gb[gt][6] = b1.z; gb[gt][7] = b1.w;
-                    }
-                    float cp[8];
-                    if (p.c_prev != nullptr && crow >= 0) {
-                        const float4 c0 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0);
-                        const float4 c1 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0 + 4);
-                        cp[0] = c0.x; cp[1] = c0.y; cp[2] = c0.z; cp[3] = c0.w;
-                        cp[4] = c1.x; cp[5] = c1.y; cp[6] = c1.z; cp[7] = c1.w;
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) cp[j] = 0.0f;
-                    }
                     float hv[8], cv[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -397,21 +417,6 @@ __global__ void __launch_bounds__(384, 1)
                         const float cn = sigm_fast(gf) * cp[j] + sigm_fast(gi) * tanh_fast(gc);
                         cv[j] = cn;
                         hv[j] = sigm_fast(go) * tanh_fast(cn);
-                    }
-                    if (p.hw != nullptr) {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4* w4 = reinterpret_cast<const float4*>(p.hw + (long long)(u0 + j) * p.hvp);
-#pragma unroll
-                            for (int q4 = 0; q4 < 4; ++q4) {
-                                if (4 * q4 >= p.hvp) break;
-                                const float4 w = w4[q4];
-                                hl[4 * q4 + 0] = fmaf(hv[j], w.x, hl[4 * q4 + 0]);
-                                hl[4 * q4 + 1] = fmaf(hv[j], w.y, hl[4 * q4 + 1]);
-                                hl[4 * q4 + 2] = fmaf(hv[j], w.z, hl[4 * q4 + 2]);
-                                hl[4 * q4 + 3] = fmaf(hv[j], w.w, hl[4 * q4 + 3]);
-                            }
-                        }
                     }
                     float4* hd = reinterpret_cast<float4*>(p.h_out + (long long)row * p.ldh + u0);
                     float4* cd = reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u0);
@@ -441,15 +446,6 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             }
-            if (p.hw != nullptr && valid) {
-                float4* o = reinterpret_cast<float4*>(p.hpart + ((long long)row * 2 * pr.n_tiles + 2 * nt + half) * p.hvp);
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4)
-                    if (4 * q4 < p.hvp) o[q4] = make_float4(hl[4 * q4], hl[4 * q4 + 1], hl[4 * q4 + 2], hl[4 * q4 + 3]);
-            }
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&bars[2 * S + AS + acc]));
             if (++acc == AS) {
                 acc = 0;
                 acc_phase ^= 1;

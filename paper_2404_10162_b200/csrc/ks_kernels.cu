@@ -756,20 +756,7 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
             }
             // head logits for rows j0, j0+1: logits[v] = b[v] + sum_i h[i] W[i][v]  (models.cpp:490-491)
             float lg[2] = {0.0f, 0.0f};
-            if (a.hpart != nullptr) {
-                // fused head: the gate GEMM's epilogue left per-tile partial logits;
-                // lane v sums its token's slots in a fixed order
-                if (lane < VP) {
-#pragma unroll
-                    for (int jj = 0; jj < 2; ++jj) {
-                        if (!(jj == 0 ? live0 : live1)) continue;
-                        const float* hp = a.hpart + (r0 + jj) * (long long)a.hslots * VP + lane;
-                        float acc = 0.0f;
-                        for (int q = 0; q < a.hslots; ++q) acc += hp[q * VP];
-                        lg[jj] = acc;
-                    }
-                }
-            } else {
+            {
                 float p0[VP], p1[VP];
 #pragma unroll
                 for (int v = 0; v < VP; ++v) {
