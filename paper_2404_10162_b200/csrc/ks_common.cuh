@@ -125,6 +125,7 @@ struct AttnArgs {
     // alpha operand (kalpha columns, alpha_t at 7 * (config - b0(tile)) + t) and
     // h_prev after it; operand row stride kalpha + NS.  Classic: [ctx ; h_prev].
     int kalpha;
+    int alpha_sparse;      // alpha-block layout unchanged since the last position: write the 7 values only
 };
 
 // Scales of the alpha-block MMA (F16X3): alpha in [0, 1] carries 2^12, P carries

@@ -977,6 +977,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             return set_error(KS_ERR_CUDA, "host-hook buffers");
         cudaEventCreateWithFlags(&keys_ready, cudaEventDisableTiming);
     }
+    int alpha_fill_H = -1;  // rows-per-config of the alpha-block layout currently in A_hi/lo
     for (int pos = 0; pos < E.T; ++pos) {
         const int cur = pos & 1, nxt = cur ^ 1;
         const int M = (int)(C * H);
@@ -1022,6 +1023,9 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         aa.A_lo = E.Alo.as<__half>();
         aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
         aa.kalpha = E.proj_at(pos, H) ? alpha_cols(H) : 0;
+        // same rows and layout as the previous alpha-block position: its zeros are still in place
+        aa.alpha_sparse = (aa.kalpha && alpha_fill_H == H) ? 1 : 0;
+        alpha_fill_H = aa.kalpha ? H : -1;
         if (enc_dec) aa.nd = 0;
         if (!hybrid) {
             if (!launch_attention(aa, pos == 0 && !enc_dec, s))

@@ -197,6 +197,22 @@ __device__ __forceinline__ void write_alpha_block(const AttnArgs& p, int r, int 
     const int b0 = ((r >> 7) << 7) / p.H_rows;
     const int c0 = kTin * b - ((kTin * b0) & ~7);
     const long long base = (long long)r * (p.kalpha + p.NS);
+    if (p.alpha_sparse) {  // the previous position left this layout's zeros in place
+        if (lane < kTin) {
+            float x = al[0];
+#pragma unroll
+            for (int t = 1; t < kTin; ++t) x = lane == t ? al[t] : x;
+            if (SPLIT == 1) {
+                __half hi, lo;
+                split_f16s(x, kAlphaScale, hi, lo);
+                p.A_hi[base + c0 + lane] = hi;
+                p.A_lo[base + c0 + lane] = lo;
+            } else {
+                reinterpret_cast<__nv_bfloat16*>(p.A_hi)[base + c0 + lane] = __float2bfloat16_rn(x);
+            }
+        }
+        return;
+    }
     for (int c = lane; c < p.kalpha / 8; c += 32) {
         float v[8];
 #pragma unroll
@@ -766,7 +782,7 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                 // hybrid variants: every hypothesis of config b reads the same feature row
                 const float* h0 = a.h + (a.h_per_config ? (long long)b : r0) * a.NS;
                 const float* h1 = a.h_per_config ? h0 : h0 + a.NS;
-#pragma unroll 4
+#pragma unroll(VP <= 8 ? 16 : 4)
                 for (int i = lane; i < a.NS; i += 32) {
                     const float x0 = live0 ? h0[i] : 0.0f;
                     const float x1 = live1 ? h1[i] : 0.0f;
