@@ -131,6 +131,10 @@ struct AttnArgs {
 // Scales of the alpha-block MMA (F16X3): alpha in [0, 1] carries 2^12, P carries
 // 2^4, so alpha.P accumulates at the same 2^16 as the 2^8-scaled h.W terms.
 constexpr float kAlphaScale = 4096.0f;
+// K-block of the tensor-core GEMM (fp16 elements per smem row): 64 -> 128-byte
+// swizzle, 2 pipeline stages in F16X3 (32 -> 64-byte swizzle, 4 stages, is
+// supported and parity-clean but measured 13% slower per launch).
+constexpr int kTcBK = 64;
 constexpr float kPScale = 16.0f;
 
 struct BeamArgs {

@@ -177,12 +177,12 @@ struct ks_engine {
     bool proj_at(int pos, int H) const {
         return ctxproj && pos > 0 && (ctxproj_force || alpha_cols_of(H) < 2 * NA);
     }
-    static int alpha_cols_of(int H) { return (7 * (127 / H + 2) + 7 + 63) / 64 * 64; }
+    static int alpha_cols_of(int H) { return (7 * (127 / H + 2) + 7 + kTcBK - 1) / kTcBK * kTcBK; }
 };
 
 // Columns of the alpha block for rows_per_cfg rows per config: a 128-row tile
 // spans at most 127 / H + 2 configs, 7 columns each, plus up to 7 columns of
-// 8-alignment of the first (tile_k, ks_gemm_tc.cu), rounded to 64.
+// 8-alignment of the first (tile_k, ks_gemm_tc.cu), rounded to the K-block.
 static int alpha_cols(int H) { return ks_engine::alpha_cols_of(H); }
 
 namespace {
@@ -742,9 +742,9 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
                 for (int mt = 0; mt * 128 < a.M; ++mt) {
                     const int b0 = mt * 128 / a.rows_per_cfg, b1 = (mt * 128 + 127) / a.rows_per_cfg;
                     const int x0 = (7 * b0) & ~7;
-                    const int kba = std::min(a.kb_alpha, (7 * (b1 + 1) - x0 + 63) / 64);
+                    const int kba = std::min(a.kb_alpha, (7 * (b1 + 1) - x0 + kTcBK - 1) / kTcBK);
                     const int rows = std::min(128, a.M - mt * 128);
-                    rowk += (double)rows * (a.K - 64.0 * (a.kb_alpha - kba));
+                    rowk += (double)rows * (a.K - (double)kTcBK * (a.kb_alpha - kba));
                 }
             }
             return 2.0 * rowk * 4.0 * a.H * passes;
@@ -1075,7 +1075,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.ldah = 0;
             p.ldw = Kd;
             p.wcol = NA2;
-            p.kb_alpha = kal / 64;
+            p.kb_alpha = kal / kTcBK;
             p.rows_per_cfg = H;
             p.PT_hi = E.Pt.as<__half>();
             p.ldpt = (C * 7 + 7) / 8 * 8;

@@ -69,11 +69,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
-// K-major, 128B-swizzled operand tile: rows of 64 fp16 (128 B), 8-row atoms of
-// 1024 B (SBO), LBO unused (1), descriptor version 1, layout SWIZZLE_128B (2).
+// K-major, swizzled operand tile: rows of kTcBK fp16, 8-row atoms (SBO), LBO
+// unused (1), descriptor version 1; kTcBK = 64: 128-byte rows, SWIZZLE_128B (2);
+// kTcBK = 32: rows of 32 fp16 (64 B), 8-row atoms of 512 B, layout SWIZZLE_64B (4).
+constexpr uint32_t kSwizzleAtom = 8 * kTcBK * 2;
+constexpr uint64_t kLayoutType = kTcBK == 64 ? 2 : 4;
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
-    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(kSwizzleAtom >> 4) << 32) |
+           ((uint64_t)1 << 46) | (kLayoutType << 61);
 }
 __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                         uint32_t idesc, uint32_t accum) {
@@ -133,7 +136,7 @@ __device__ __forceinline__ TileK tile_k(const LstmArgs& p, int k_blocks, int mt)
         const int b0 = (mt * 128) / p.rows_per_cfg;
         const int b1 = (mt * 128 + 127) / p.rows_per_cfg;
         r.x0 = (7 * b0) & ~7;
-        r.kba_t = (7 * (b1 + 1) - r.x0 + 63) / 64;
+        r.kba_t = (7 * (b1 + 1) - r.x0 + kTcBK - 1) / kTcBK;
         if (r.kba_t > p.kb_alpha) r.kba_t = p.kb_alpha;
         r.nkb = k_blocks - p.kb_alpha + r.kba_t;
     }
@@ -147,7 +150,7 @@ struct TcParams {
 };
 
 constexpr int TC_BM = 128;
-constexpr int TC_BK = 64;
+constexpr int TC_BK = kTcBK;
 
 template <int UNITS, bool SPLIT>
 struct TcCfg {
@@ -490,7 +493,8 @@ bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, 
     cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, TC_BK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

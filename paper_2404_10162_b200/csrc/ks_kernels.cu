@@ -513,7 +513,7 @@ void launch_attention_nd(const AttnArgs& p, bool first, cudaStream_t s) {
     }();
     if (first) {
         attention_pack_t<ND, SPLIT, true><<<(unsigned)((p.M + 7) / 8), 256, 0, s>>>(p);
-    } else if (mode == 0 && p.H_rows > 1 && p.H_rows <= 64) {
+    } else if (mode == 0 && p.H_rows > 1 && p.H_rows <= 64 && p.kalpha == 0) {
         attention_cta_t<ND, SPLIT><<<(unsigned)(p.M / p.H_rows), 128, 0, s>>>(p);
     } else if (mode == 2 && p.H_rows > 1) {
         const int C = p.M / p.H_rows;
