@@ -61,7 +61,7 @@ def build_engine(verbose: bool = False, force: bool = False) -> str:
             print(log)
     objs = [os.path.join(BUILD, s + ".o") for s in CU_SOURCES + CPP_SOURCES]
     if force or jobs or not os.path.exists(out):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-L/usr/local/cuda/lib64", "-lcublas",
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-L/usr/local/cuda/lib64", "-lcublas", "-lcublasLt",
               "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
     return out
 

@@ -34,6 +34,7 @@
 // recurrent rows; column g*H + j, gates input, forget, output, cand)  followed
 // by  Ws [S + 1][4H]  (one-hot slot rows, then the bias).  Adam and the clip
 // are elementwise / order-free, so they run on the flat buffer directly.
+#include <cublasLt.h>
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
@@ -280,26 +281,31 @@ struct AttnFwd {
     float* hid;          // [M][7][nd]
 };
 
+template <int ND>
 __global__ void k_attn_fwd(AttnFwd a) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= a.M) return;
     const long long r = warp;
     const float* s = a.s + r * a.ns;
-    float sw[kMaxNd];
-    for (int d = 0; d < a.nd; ++d) sw[d] = 0.0f;
+    float sw[ND];
+    #pragma unroll
+    for (int d = 0; d < ND; ++d) sw[d] = 0.0f;
     for (int j = lane; j < a.ns; j += 32) {
         const float sv = s[j];
-        for (int d = 0; d < a.nd; ++d) sw[d] += sv * a.Ws[(long long)j * a.nd + d];
+        #pragma unroll
+        for (int d = 0; d < ND; ++d) sw[d] += sv * a.Ws[(long long)j * ND + d];
     }
-    for (int d = 0; d < a.nd; ++d)
+    #pragma unroll
+    for (int d = 0; d < ND; ++d)
         for (int o = 16; o; o >>= 1) sw[d] += __shfl_xor_sync(0xffffffffu, sw[d], o);
     float e[kTin];
     float mx = -INFINITY;
     for (int t = 0; t < kTin; ++t) {
         float et = a.bo[0];
-        for (int d = 0; d < a.nd; ++d) {
-            const float hv = tanhf(sw[d] + a.U[(r * kTin + t) * a.nd + d] + a.bh[d]);
-            if (lane == 0) a.hid[(r * kTin + t) * a.nd + d] = hv;
+        #pragma unroll
+        for (int d = 0; d < ND; ++d) {
+            const float hv = tanhf(sw[d] + a.U[(r * kTin + t) * ND + d] + a.bh[d]);
+            if (lane == 0) a.hid[(r * kTin + t) * ND + d] = hv;
             et += hv * a.wo[d];
         }
         e[t] = et;
@@ -346,6 +352,7 @@ struct AttnBwd {
     float* rowacc;       // [M][nd + 1] (+=): sum_t hid*de, sum_t de
 };
 
+template <int ND>
 __global__ void k_attn_bwd(AttnBwd a) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= a.M) return;
@@ -367,39 +374,45 @@ __global__ void k_attn_bwd(AttnBwd a) {
         al[t] = a.alpha[r * kTin + t];
         dot += al[t] * dal[t];
     }
-    float dps[kMaxNd];
-    for (int d = 0; d < a.nd; ++d) dps[d] = 0.0f;
-    float dpre[kTin][kMaxNd];
+    float dps[ND];
+    #pragma unroll
+    for (int d = 0; d < ND; ++d) dps[d] = 0.0f;
+    float dpre[kTin][ND];
     float dbo = 0.0f;
     for (int t = 0; t < kTin; ++t) {
         de[t] = al[t] * (dal[t] - dot);
         dbo += de[t];
-        for (int d = 0; d < a.nd; ++d) {
-            const float hv = a.hid[(r * kTin + t) * a.nd + d];
+        #pragma unroll
+        for (int d = 0; d < ND; ++d) {
+            const float hv = a.hid[(r * kTin + t) * ND + d];
             dpre[t][d] = de[t] * a.wo[d] * (1.0f - hv * hv);
             dps[d] += dpre[t][d];
         }
     }
     if (lane == 0) {
-        float* ra = a.rowacc + r * (a.nd + 1);
-        for (int d = 0; d < a.nd; ++d) {
+        float* ra = a.rowacc + r * (ND + 1);
+        #pragma unroll
+        for (int d = 0; d < ND; ++d) {
             float s = 0.0f;
-            for (int t = 0; t < kTin; ++t) s += a.hid[(r * kTin + t) * a.nd + d] * de[t];
+            for (int t = 0; t < kTin; ++t) s += a.hid[(r * kTin + t) * ND + d] * de[t];
             ra[d] += s;
-            a.DPs[r * a.nd + d] = dps[d];
+            a.DPs[r * ND + d] = dps[d];
         }
-        ra[a.nd] += dbo;
+        ra[ND] += dbo;
         for (int t = 0; t < kTin; ++t)
-            for (int d = 0; d < a.nd; ++d) a.DPa[(r * kTin + t) * a.nd + d] += dpre[t][d];
+            #pragma unroll
+            for (int d = 0; d < ND; ++d) a.DPa[(r * kTin + t) * ND + d] += dpre[t][d];
     }
     float* dAr = a.dA + r * kTin * a.na2;
     for (int j = lane; j < a.na2; j += 32) {
         const float dc = mi ? dX[j] * mi[j] : dX[j];
-        float wa[kMaxNd];
-        for (int d = 0; d < a.nd; ++d) wa[d] = a.Wa[(long long)j * a.nd + d];
+        float wa[ND];
+        #pragma unroll
+        for (int d = 0; d < ND; ++d) wa[d] = a.Wa[(long long)j * ND + d];
         for (int t = 0; t < kTin; ++t) {
             float v = al[t] * dc;
-            for (int d = 0; d < a.nd; ++d) v += dpre[t][d] * wa[d];
+            #pragma unroll
+            for (int d = 0; d < ND; ++d) v += dpre[t][d] * wa[d];
             dAr[t * a.na2 + j] += v;
         }
     }
@@ -407,10 +420,30 @@ __global__ void k_attn_bwd(AttnBwd a) {
     for (int j = lane; j < a.ns; j += 32) {
         float v = dX[a.na2 + j];
         if (mr) v *= mr[j];
-        for (int d = 0; d < a.nd; ++d) v += dps[d] * a.Ws[(long long)j * a.nd + d];
+        #pragma unroll
+        for (int d = 0; d < ND; ++d) v += dps[d] * a.Ws[(long long)j * ND + d];
         a.dH[r * a.ns + j] = v;
     }
 }
+
+// n_d (attention_dense_nodes) as a compile-time constant keeps the per-row
+// energy terms in registers.
+#define KST_ND_DISPATCH(kernel, Args)                                                      \
+    inline bool launch_##kernel(int nd, const Args& a, unsigned grid, cudaStream_t s) {    \
+        switch (nd) {                                                                      \
+            case 1: kernel<1><<<grid, 256, 0, s>>>(a); return true;                        \
+            case 2: kernel<2><<<grid, 256, 0, s>>>(a); return true;                        \
+            case 3: kernel<3><<<grid, 256, 0, s>>>(a); return true;                        \
+            case 4: kernel<4><<<grid, 256, 0, s>>>(a); return true;                        \
+            case 5: kernel<5><<<grid, 256, 0, s>>>(a); return true;                        \
+            case 6: kernel<6><<<grid, 256, 0, s>>>(a); return true;                        \
+            case 7: kernel<7><<<grid, 256, 0, s>>>(a); return true;                        \
+            case 8: kernel<8><<<grid, 256, 0, s>>>(a); return true;                        \
+            default: return false;                                                         \
+        }                                                                                  \
+    }
+KST_ND_DISPATCH(k_attn_fwd, AttnFwd)
+KST_ND_DISPATCH(k_attn_bwd, AttnBwd)
 
 // Head + cross entropy (dense_forward, cross_entropy_logits, sum_scaled 1/T;
 // models.cpp:764-777), one warp per row: per-row loss (double), argmax match,
@@ -496,6 +529,61 @@ __global__ void k_colsum_final(const double* part, int N, int chunks, float* out
     double t = 0.0;
     for (int c = 0; c < chunks; ++c) t += part[(long long)c * N + n];
     out[n] = accumulate ? out[n] + (float)t : (float)t;
+}
+
+// 3xTF32 operand split: x = big + small with both parts tf32-exact (round to
+// nearest, 10-bit mantissa); big.big + big.small + small.big recovers an
+// fp32-grade product on the TF32 tensor cores (the dropped small.small term is
+// ~2^-22 relative).  Packs a (rows x cols, ld) matrix densely.
+__device__ __forceinline__ float tf32_rna(float x) {
+    unsigned u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    return __uint_as_float(u);
+}
+__global__ void k_split_tf32(const float* src, long long rows, int cols, long long ld, float* big, float* small,
+                             bool vec) {
+    const int cw = vec ? cols / 4 : cols;
+    for (long long r = blockIdx.y; r < rows; r += gridDim.y) {
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cw; c += gridDim.x * blockDim.x) {
+            if (vec) {
+                const float4 x = reinterpret_cast<const float4*>(src + r * ld)[c];
+                float4 b, sm;
+                b.x = tf32_rna(x.x); b.y = tf32_rna(x.y); b.z = tf32_rna(x.z); b.w = tf32_rna(x.w);
+                sm.x = tf32_rna(x.x - b.x); sm.y = tf32_rna(x.y - b.y); sm.z = tf32_rna(x.z - b.z); sm.w = tf32_rna(x.w - b.w);
+                reinterpret_cast<float4*>(big + r * cols)[c] = b;
+                reinterpret_cast<float4*>(small + r * cols)[c] = sm;
+            } else {
+                const float x = src[r * ld + c];
+                const float b = tf32_rna(x);
+                big[r * cols + c] = b;
+                small[r * cols + c] = tf32_rna(x - b);
+            }
+        }
+    }
+}
+
+// Same split, transposed: dst[c][r] (dense, ld = rows) from src[r][c] (ld), through
+// 32 x 32 shared-memory tiles so both sides stay coalesced.  Used for the
+// transposed A operand of the weight-gradient GEMMs (X^T . dZ): cuBLAS picks
+// legacy sm80 TF32 kernels for that layout, the NN form runs on sm100 kernels.
+__global__ void k_split_tf32_t(const float* src, long long rows, long long cols, long long ld, float* big,
+                               float* small) {
+    __shared__ float tile[32][33];
+    const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const long long r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * ld + c] : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const long long c = c0 + i, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) {
+            const float x = tile[threadIdx.x][i];
+            const float b = tf32_rna(x);
+            big[c * rows + r] = b;
+            small[c * rows + r] = tf32_rna(x - b);
+        }
+    }
 }
 
 // Loss / match totals (double, fixed order).
@@ -642,6 +730,13 @@ struct ks_trainer {
     DBuf Hx[2], Ce[2], Ze[2], dZe[2], A, U;
     DBuf Xd, Hs, Cd, Zd, dZd, alpha, hid, dlog, DHh, lossr, match;
     DBuf dXd, dH, dC, dA, DPs, DPa, rowacc, dHe, dCe, part, norm, grads_tmp;
+    bool tf32x3 = true;            // GEMM arithmetic: 3xTF32 tensor cores (default) or fp32 SIMT SGEMM
+    DBuf sp[4];                    // split scratch: A big/small, B big/small
+    DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
+    cublasLtHandle_t lt = nullptr;
+    std::map<const float*, std::pair<DBuf*, long long>> wsplit;  // per-call weight splits
+    std::vector<std::unique_ptr<DBuf[]>> wsplit_store;  // pool, reused call after call
+    size_t wsplit_used = 0;
     int n_in = 0;  // decoder input-mask width
     int vmax = 1;  // largest vocabulary (stride of the per-position dlogits blocks)
     long long launches = 0;
@@ -662,16 +757,134 @@ namespace {
             return set_error(KS_ERR_CUDA, std::string("cuBLAS ") + #call + " status " + std::to_string((int)s_)); \
     } while (0)
 
-// Row-major C[M x N] = alpha op(A) op(B) + beta C, on cuBLAS (column-major).
-ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
-                  long long lda, const float* B, long long ldb, float beta, float* C, long long ldc) {
-    if (M == 0 || N == 0) return KS_OK;
+ks_status gemm_one(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
+                   long long lda, const float* B, long long ldb, float beta, float* C, long long ldc,
+                   cublasComputeType_t ct) {
     const float one = 1.0f;
-    if (K == 0) return beta == 1.0f ? KS_OK : set_error(KS_ERR_SHAPE, "empty GEMM reduction");
-    KT_BLAS(cublasSgemm(t.blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N, (int)M,
-                        (int)K, &one, B, (int)ldb, A, (int)lda, &beta, C, (int)ldc));
+    KT_BLAS(cublasGemmEx(t.blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N, (int)M,
+                         (int)K, &one, B, CUDA_R_32F, (int)ldb, A, CUDA_R_32F, (int)lda, &beta, C, CUDA_R_32F,
+                         (int)ldc, ct, CUBLAS_GEMM_DEFAULT));
     ++t.launches;
     return KS_OK;
+}
+
+// TF32 pass through cuBLASLt: for the long weight-gradient reductions the plain
+// cublasGemmEx heuristic picks legacy sm80 TF32 kernels, cuBLASLt's picks the
+// sm100 ones (7.5 vs 9.8 ms per training step).  (Restricting the heuristic to
+// CUBLASLT_REDUCTION_SCHEME_NONE returned algorithms that produced wrong sums.)
+// Row-major C[M x N] = op(A) op(B) + beta C with A, B dense (A M x K, B as stored).
+ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long N, long long K, const float* A,
+                  long long lda, const float* B, long long ldb, float beta, float* C, long long ldc) {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+    cublasLtMatmulPreference_t pref = nullptr;
+    cublasStatus_t e = CUBLAS_STATUS_SUCCESS;
+    // column-major view: C^T (N x M) = op(B)^T (N x K) . A^T (K x M)
+    const cublasOperation_t tbo = tb ? CUBLAS_OP_T : CUBLAS_OP_N, tao = CUBLAS_OP_N;
+    const float one = 1.0f;
+    cublasLtMatmulHeuristicResult_t heur{};
+    int nres = 0;
+    const size_t wsz = t.blas_ws.bytes;
+    if ((e = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F))) goto done;
+    if ((e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tbo, sizeof tbo))) goto done;
+    if ((e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tao, sizeof tao))) goto done;
+    if ((e = cublasLtMatrixLayoutCreate(&la, CUDA_R_32F, tb ? K : N, tb ? N : K, ldb))) goto done;
+    if ((e = cublasLtMatrixLayoutCreate(&lb, CUDA_R_32F, K, M, lda))) goto done;
+    if ((e = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, N, M, ldc))) goto done;
+    if ((e = cublasLtMatmulPreferenceCreate(&pref))) goto done;
+    if ((e = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz)))
+        goto done;
+    if ((e = cublasLtMatmulAlgoGetHeuristic(t.lt, op, la, lb, lc, lc, pref, 1, &heur, &nres))) goto done;
+    if (nres < 1 || heur.state != CUBLAS_STATUS_SUCCESS) {
+        e = CUBLAS_STATUS_NOT_SUPPORTED;
+        goto done;
+    }
+    e = cublasLtMatmul(t.lt, op, &one, B, la, A, lb, &beta, C, lc, C, lc, &heur.algo, t.blas_ws.p, wsz, s);
+    ++t.launches;
+done:
+    if (pref) cublasLtMatmulPreferenceDestroy(pref);
+    if (lc) cublasLtMatrixLayoutDestroy(lc);
+    if (lb) cublasLtMatrixLayoutDestroy(lb);
+    if (la) cublasLtMatrixLayoutDestroy(la);
+    if (op) cublasLtMatmulDescDestroy(op);
+    if (e != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cuBLASLt TF32 GEMM status " + std::to_string((int)e));
+    return KS_OK;
+}
+
+// Splits a stored (rows x cols, ld) operand into dense big/small planes.
+ks_status split_into(ks_trainer& t, cudaStream_t s, const float* src, long long rows, long long cols, long long ld,
+                     DBuf& big, DBuf& small) {
+    const size_t bytes = (size_t)rows * cols * 4;
+    KT_CUDA(big.ensure(bytes));
+    KT_CUDA(small.ensure(bytes));
+    const bool vec = cols % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const long long cw = vec ? cols / 4 : cols;
+    dim3 grid((unsigned)std::min<long long>((cw + 255) / 256, 64), (unsigned)std::min<long long>(rows, 65535));
+    k_split_tf32<<<grid, 256, 0, s>>>(src, rows, (int)cols, ld, big.as<float>(), small.as<float>(), vec);
+    ++t.launches;
+    return KS_OK;
+}
+
+// Row-major C[M x N] = op(A) op(B) + beta C, on cuBLAS (column-major).  3xTF32
+// mode: both operands split (weights once per call, cached by pointer) and
+// C = beta C + small(A).big(B) + big(A).small(B) + big(A).big(B) on TF32 tensor
+// cores with fp32 accumulation; fp32 mode: one SGEMM (PEDANTIC, no TF32).
+ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
+                  long long lda, const float* B, long long ldb, float beta, float* C, long long ldc,
+                  bool b_is_weight = false) {
+    if (M == 0 || N == 0) return KS_OK;
+    if (K == 0) return beta == 1.0f ? KS_OK : set_error(KS_ERR_SHAPE, "empty GEMM reduction");
+    // narrow outputs (heads, attention, slot rows) stay fp32 SGEMMs
+    if (!t.tf32x3 || M < 128 || N < 128)
+        return gemm_one(t, ta, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_PEDANTIC);
+
+    cudaStream_t s;
+    KT_BLAS(cublasGetStream(t.blas, &s));
+    ks_status st;
+    const long long br = tb ? N : K, bc = tb ? K : N;
+    // A is packed row-major M x K (a transposed A is transposed while splitting)
+    if (ta) {
+        KT_CUDA(t.sp[0].ensure((size_t)M * K * 4));
+        KT_CUDA(t.sp[1].ensure((size_t)M * K * 4));
+        dim3 grid((unsigned)((M + 31) / 32), (unsigned)((K + 31) / 32));
+        if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
+        k_split_tf32_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, t.sp[0].as<float>(), t.sp[1].as<float>());
+        ++t.launches;
+    } else if ((st = split_into(t, s, A, M, K, lda, t.sp[0], t.sp[1]))) {
+        return st;
+    }
+    const long long ac = K;
+    const float *Bb, *Bs;
+    if (b_is_weight) {
+        auto it = t.wsplit.find(B);
+        if (it == t.wsplit.end()) {
+            if (t.wsplit_used == t.wsplit_store.size()) t.wsplit_store.emplace_back(new DBuf[2]);
+            DBuf* pair = t.wsplit_store[t.wsplit_used++].get();
+            if ((st = split_into(t, s, B, br, bc, ldb, pair[0], pair[1]))) return st;
+            it = t.wsplit.emplace(B, std::make_pair(pair, bc)).first;
+        }
+        Bb = it->second.first[0].as<float>();
+        Bs = it->second.first[1].as<float>();
+    } else {
+        if ((st = split_into(t, s, B, br, bc, ldb, t.sp[2], t.sp[3]))) return st;
+        Bb = t.sp[2].as<float>();
+        Bs = t.sp[3].as<float>();
+    }
+    const float* Ab = t.sp[0].as<float>();
+    const float* As = t.sp[1].as<float>();
+    static const bool use_lt = [] {
+        const char* e = std::getenv("KS_TRAIN_LT");
+        return !(e && e[0] == '0');
+    }();
+    if (use_lt) {
+        if ((st = gemm_lt(t, s, tb, M, N, K, As, ac, Bb, bc, beta, C, ldc))) return st;
+        if ((st = gemm_lt(t, s, tb, M, N, K, Ab, ac, Bs, bc, 1.0f, C, ldc))) return st;
+        return gemm_lt(t, s, tb, M, N, K, Ab, ac, Bb, bc, 1.0f, C, ldc);
+    }
+    const cublasComputeType_t ct = CUBLAS_COMPUTE_32F_FAST_TF32;
+    if ((st = gemm_one(t, false, tb, M, N, K, As, ac, Bb, bc, beta, C, ldc, ct))) return st;
+    if ((st = gemm_one(t, false, tb, M, N, K, Ab, ac, Bs, bc, 1.0f, C, ldc, ct))) return st;
+    return gemm_one(t, false, tb, M, N, K, Ab, ac, Bb, bc, 1.0f, C, ldc, ct);
 }
 
 ks_status colsum(ks_trainer& t, cudaStream_t s, const float* in, long long R, int N, long long ld, float* out,
@@ -755,6 +968,8 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
     ks_status st;
     if ((st = ensure_ws(t, M))) return st;
     KT_BLAS(cublasSetStream(t.blas, s));
+    t.wsplit.clear();  // weights may have changed since the last call (Adam, import)
+    t.wsplit_used = 0;
     const int T = t.T;
     const long long m = M;
     const bool attn = t.variant != KS_VARIANT_ENC_DEC;
@@ -806,7 +1021,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             const int tt = dir == 0 ? st_ : kTin - 1 - st_;
             float* Z = t.Ze[dir].as<float>() + (long long)st_ * m * 4 * H;
             if (st_ > 0 && (st = gemm_rm(t, false, false, m, 4LL * H, H, Hx + (long long)st_ * m * H, H,
-                                         P + L.wd(), 4LL * H, 0.0f, Z, 4LL * H)))
+                                         P + L.wd(), 4LL * H, 0.0f, Z, 4LL * H, true)))
                 return st;
             CellFwd c{};
             c.M = M;
@@ -872,11 +1087,12 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             af.ldx = Kd;
             af.alpha = t.alpha.as<float>() + (long long)p * m * 7;
             af.hid = t.hid.as<float>() + (long long)p * m * 7 * t.n_d;
-            k_attn_fwd<<<blocks(m * 32, 256), 256, 0, s>>>(af);
+            if (!launch_k_attn_fwd(t.n_d, af, blocks(m * 32, 256), s))
+                return set_error(KS_ERR_UNSUPPORTED, "attention_dense_nodes outside 1..8");
             ++t.launches;
         }
         float* Z = t.Zd.as<float>() + (long long)p * m * 4 * Hd;
-        if ((st = gemm_rm(t, false, false, m, 4LL * Hd, Kd, X, Kd, P + D.wd(), 4LL * Hd, 0.0f, Z, 4LL * Hd)))
+        if ((st = gemm_rm(t, false, false, m, 4LL * Hd, Kd, X, Kd, P + D.wd(), 4LL * Hd, 0.0f, Z, 4LL * Hd, true)))
             return st;
         CellFwd c{};
         c.M = M;
@@ -958,7 +1174,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         ++t.launches;
         // dX = dZ . Wd^T  -> [dctx | dh_rec]
         float* dX = t.dXd.as<float>();
-        if ((st = gemm_rm(t, false, true, m, Kd, 4LL * Hd, dZ, 4LL * Hd, P + D.wd(), 4LL * Hd, 0.0f, dX, Kd)))
+        if ((st = gemm_rm(t, false, true, m, Kd, 4LL * Hd, dZ, 4LL * Hd, P + D.wd(), 4LL * Hd, 0.0f, dX, Kd, true)))
             return st;
         if (attn) {
             AttnBwd ab{};
@@ -982,7 +1198,8 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             ab.DPs = t.DPs.as<float>() + (long long)p * m * t.n_d;
             ab.DPa = t.DPa.as<float>();
             ab.rowacc = t.rowacc.as<float>();
-            k_attn_bwd<<<blocks(m * 32, 256), 256, 0, s>>>(ab);
+            if (!launch_k_attn_bwd(t.n_d, ab, blocks(m * 32, 256), s))
+                return set_error(KS_ERR_UNSUPPORTED, "attention_dense_nodes outside 1..8");
             ++t.launches;
         } else {
             // enc-dec: dH = dX (the recurrent rows) * mr, via the next cell_bwd's mask2
@@ -1054,7 +1271,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             cb.dZ = dZ;
             k_cell_bwd<<<blocks(m * H, 256), 256, 0, s>>>(cb);
             ++t.launches;
-            if (st_ > 0 && (st = gemm_rm(t, false, true, m, H, 4LL * H, dZ, 4LL * H, P + L.wd(), 4LL * H, 0.0f, dHe, H)))
+            if (st_ > 0 && (st = gemm_rm(t, false, true, m, H, 4LL * H, dZ, 4LL * H, P + L.wd(), 4LL * H, 0.0f, dHe, H, true)))
                 return st;
         }
         float* Hx = t.Hx[dir].as<float>();
@@ -1274,7 +1491,12 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
         cudaMemset(t.adam_v.p, 0, (size_t)cursor * 4) != cudaSuccess)
         return set_error(KS_ERR_CUDA, "trainer upload failed");
     if (cublasCreate(&t.blas) != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cublasCreate failed");
-    cublasSetMathMode(t.blas, CUBLAS_PEDANTIC_MATH);  // true fp32 GEMMs (no TF32)
+    {
+        const char* g = std::getenv("KS_TRAIN_GEMM");
+        t.tf32x3 = !(g && std::string(g) == "fp32");
+    }
+    if (t.blas_ws.ensure((size_t)64 << 20) != cudaSuccess) return set_error(KS_ERR_CUDA, "cuBLAS workspace");
+    if (cublasLtCreate(&t.lt) != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cublasLtCreate failed");
     *out = tr.release();
     return KS_OK;
 }
@@ -1297,6 +1519,7 @@ extern "C" void ks_trainer_destroy(ks_trainer* t) {
     if (!t) return;
     cudaSetDevice(t->device);
     if (t->blas) cublasDestroy(t->blas);
+    if (t->lt) cublasLtDestroy(t->lt);
     delete t;
 }
 
