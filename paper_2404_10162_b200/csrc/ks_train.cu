@@ -784,6 +784,7 @@ ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long
     const float one = 1.0f;
     cublasLtMatmulHeuristicResult_t heur{};
     int nres = 0;
+    bool fallback = false;
     const size_t wsz = t.blas_ws.bytes;
     if ((e = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F))) goto done;
     if ((e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tbo, sizeof tbo))) goto done;
@@ -796,7 +797,7 @@ ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long
         goto done;
     if ((e = cublasLtMatmulAlgoGetHeuristic(t.lt, op, la, lb, lc, lc, pref, 1, &heur, &nres))) goto done;
     if (nres < 1 || heur.state != CUBLAS_STATUS_SUCCESS) {
-        e = CUBLAS_STATUS_NOT_SUPPORTED;
+        fallback = true;  // no cuBLASLt algorithm for this shape: cublasGemmEx below
         goto done;
     }
     e = cublasLtMatmul(t.lt, op, &one, B, la, A, lb, &beta, C, lc, C, lc, &heur.algo, t.blas_ws.p, wsz, s);
@@ -808,6 +809,8 @@ done:
     if (la) cublasLtMatrixLayoutDestroy(la);
     if (op) cublasLtMatmulDescDestroy(op);
     if (e != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cuBLASLt TF32 GEMM status " + std::to_string((int)e));
+    if (fallback)
+        return gemm_one(t, false, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_FAST_TF32);
     return KS_OK;
 }
 
