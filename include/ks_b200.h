@@ -248,8 +248,12 @@ ks_status ks_trainer_create(const ks_model_desc* model, double dropout, double r
 /* dropout rates from the checkpoint header (data.cpp:478-479). */
 ks_status ks_trainer_create_from_checkpoint(const char* path, int32_t device, ks_trainer** out);
 void ks_trainer_destroy(ks_trainer* tr);
-/* Length of the flat parameter / gradient buffers (= total reference parameter count). */
+/* Length of the flat train-layout parameter / gradient buffers (segments padded
+ * to 64 floats, so it is at least the reference parameter count). */
 int64_t ks_trainer_num_params(const ks_trainer* tr);
+/* The reference parameter count: length of the ks_trainer_export / import /
+ * to_reference_layout host arrays. */
+int64_t ks_trainer_num_ref_params(const ks_trainer* tr);
 int64_t ks_trainer_last_launch_count(const ks_trainer* tr);
 
 /* Forward + backward over B samples already on the device (d_tok B x 7 input

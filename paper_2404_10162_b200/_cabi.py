@@ -85,7 +85,7 @@ EXPORTS = [
     "ks_engine_profile_launches_ex",
     "ks_beam_search_batch_hooked",
     "ks_trainer_create", "ks_trainer_create_from_checkpoint", "ks_trainer_destroy",
-    "ks_trainer_num_params", "ks_trainer_last_launch_count", "ks_trainer_loss_grads",
+    "ks_trainer_num_params", "ks_trainer_num_ref_params", "ks_trainer_last_launch_count", "ks_trainer_loss_grads",
     "ks_trainer_apply", "ks_trainer_step", "ks_trainer_export", "ks_trainer_import",
     "ks_trainer_to_reference_layout",
 ]
@@ -142,6 +142,8 @@ def lib():
     L.ks_trainer_destroy.argtypes = [vp]
     L.ks_trainer_num_params.argtypes = [vp]
     L.ks_trainer_num_params.restype = i64
+    L.ks_trainer_num_ref_params.argtypes = [vp]
+    L.ks_trainer_num_ref_params.restype = i64
     L.ks_trainer_last_launch_count.argtypes = [vp]
     L.ks_trainer_last_launch_count.restype = i64
     L.ks_trainer_loss_grads.argtypes = [vp, vp, vp, vp, i64, i64, C.c_uint64, vp, i32, vp, vp, vp]
@@ -278,7 +280,8 @@ class Trainer:
         h = C.c_void_p()
         check(L.ks_trainer_create_from_checkpoint(checkpoint.encode(), device, C.byref(h)))
         self._h = h
-        self.num_params = L.ks_trainer_num_params(h)
+        self.num_params = L.ks_trainer_num_params(h)          # train-layout buffers (grads)
+        self.num_ref_params = L.ks_trainer_num_ref_params(h)  # reference order (export/import)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -310,7 +313,7 @@ class Trainer:
         return loss.value, m.value
 
     def export(self) -> np.ndarray:
-        out = np.empty(self.num_params, np.float32)
+        out = np.empty(self.num_ref_params, np.float32)
         check(lib().ks_trainer_export(self._h, _p(out, C.c_float)))
         return out
 
@@ -320,6 +323,6 @@ class Trainer:
 
     def to_reference_layout(self, train_flat) -> np.ndarray:
         v = np.ascontiguousarray(train_flat, np.float32)
-        out = np.empty(self.num_params, np.float32)
+        out = np.empty(self.num_ref_params, np.float32)
         check(lib().ks_trainer_to_reference_layout(self._h, _p(v, C.c_float), _p(out, C.c_float)))
         return out

@@ -720,7 +720,8 @@ struct ks_trainer {
     std::map<std::string, size_t> seg_of;
     long long off_attn_h = -1, off_attn_hb = -1, off_attn_o = -1, off_attn_ob = -1;
     std::vector<long long> off_head_w, off_head_b;
-    long long nparams = 0;
+    long long nparams = 0;        // train-layout length (segments padded to 64 floats)
+    long long nref = 0;           // reference parameter count (export / import order)
     DBuf params, adam_m, adam_v;
     long long adam_step = 0;
     cublasHandle_t blas = nullptr;
@@ -795,13 +796,31 @@ ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long
     if ((e = cublasLtMatmulPreferenceCreate(&pref))) goto done;
     if ((e = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz)))
         goto done;
-    if ((e = cublasLtMatmulAlgoGetHeuristic(t.lt, op, la, lb, lc, lc, pref, 1, &heur, &nres))) goto done;
-    if (nres < 1 || heur.state != CUBLAS_STATUS_SUCCESS) {
+    {
+        // the output may start anywhere in the flat gradient buffer: tell the heuristic
+        auto align = [](const void* ptr) {
+            uint32_t a = 256;
+            while (a > 4 && (reinterpret_cast<uintptr_t>(ptr) % a) != 0) a >>= 1;
+            return a;
+        };
+        const uint32_t aa = align(B), ab = align(A), ac = align(C);
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_A_BYTES, &aa, sizeof aa);
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_B_BYTES, &ab, sizeof ab);
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_C_BYTES, &ac, sizeof ac);
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &ac, sizeof ac);
+    }
+    if (cublasLtMatmulAlgoGetHeuristic(t.lt, op, la, lb, lc, lc, pref, 1, &heur, &nres) != CUBLAS_STATUS_SUCCESS ||
+        nres < 1 || heur.state != CUBLAS_STATUS_SUCCESS) {
         fallback = true;  // no cuBLASLt algorithm for this shape: cublasGemmEx below
         goto done;
     }
     e = cublasLtMatmul(t.lt, op, &one, B, la, A, lb, &beta, C, lc, C, lc, &heur.algo, t.blas_ws.p, wsz, s);
-    ++t.launches;
+    if (e == CUBLAS_STATUS_NOT_SUPPORTED) {
+        e = CUBLAS_STATUS_SUCCESS;
+        fallback = true;
+    } else {
+        ++t.launches;
+    }
 done:
     if (pref) cublasLtMatmulPreferenceDestroy(pref);
     if (lc) cublasLtMatrixLayoutDestroy(lc);
@@ -1406,6 +1425,9 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
         t.n_in = t.d_fb;
     }
     // layout, in the desc's tensor order (checkpoint order)
+    // every segment starts 256-byte aligned: GEMM outputs land at segment starts and
+    // the tensor-core kernels need aligned C (misaligned ones fall back to slow paths)
+    auto pad_seg = [](long long x) { return (x + 63) / 64 * 64; };
     long long cursor = 0;
     std::vector<bool> placed(t.lstms.size(), false);
     std::vector<int> seen(t.lstms.size(), 0);
@@ -1427,7 +1449,7 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
                                                    " elements, expected " + std::to_string(want));
             if (!placed[(size_t)li]) {
                 L.off = cursor;
-                cursor += L.size();
+                cursor = pad_seg(cursor + L.size());
                 placed[(size_t)li] = true;
             }
             sg.lstm = li;
@@ -1436,7 +1458,7 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
             ++seen[(size_t)li];
         } else {
             sg.off = cursor;
-            cursor += sg.numel;
+            cursor = pad_seg(cursor + sg.numel);
             auto expect = [&](long long n) -> ks_status {
                 return sg.numel == n ? KS_OK
                                      : set_error(KS_ERR_SHAPE, "tensor " + sg.name + " has " + std::to_string(sg.numel) +
@@ -1474,6 +1496,8 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
         if (t.off_head_w[(size_t)p] < 0 || t.off_head_b[(size_t)p] < 0)
             return set_error(KS_ERR_STATE, "model tensor 'head." + std::to_string(p) + "' is missing");
     t.nparams = cursor;
+    t.nref = 0;
+    for (const RefSeg& sg : t.segs) t.nref += sg.numel;
     std::vector<float> host((size_t)cursor, 0.0f);
     std::vector<const float*> src((size_t)d->num_tensors);
     for (int i = 0; i < d->num_tensors; ++i) src[(size_t)i] = d->tensor_data[i];
@@ -1527,6 +1551,7 @@ extern "C" void ks_trainer_destroy(ks_trainer* t) {
 }
 
 extern "C" int64_t ks_trainer_num_params(const ks_trainer* t) { return t ? t->nparams : 0; }
+extern "C" int64_t ks_trainer_num_ref_params(const ks_trainer* t) { return t ? t->nref : 0; }
 extern "C" int64_t ks_trainer_last_launch_count(const ks_trainer* t) { return t ? t->launches : 0; }
 
 extern "C" ks_status ks_trainer_loss_grads(ks_trainer* t, const int32_t* d_tok, const int32_t* d_tgt,

@@ -166,6 +166,6 @@ def test_export_import_roundtrip_is_identity():
     ck = TO.Checkpoint(path)
     tr = Trainer(path)
     np.testing.assert_array_equal(tr.export(), ck.flat().astype(np.float32))
-    v = np.random.default_rng(0).standard_normal(tr.num_params).astype(np.float32)
+    v = np.random.default_rng(0).standard_normal(tr.num_ref_params).astype(np.float32)
     tr.import_(v)
     np.testing.assert_array_equal(tr.export(), v)
