@@ -310,4 +310,55 @@ std::vector<EvalReport> topk_metrics(const SequencePredictor& predictor, const s
                                      std::span<const ConstraintPredicate> predicates = {},
                                      int threads = 1);
 
+// ------------------------------------------------------------------ training
+// (models.hpp:139-169, data.hpp, rng.hpp).  The teacher-forced training loop
+// of the reference, with each batch's forward / backward / Adam step on the
+// GPU (ks_trainer_*, enc-dec / attn / attn-2).  Initialisation, the epoch
+// shuffle and the per-sample dropout streams use the reference's Rng, so a
+// run reproduces the reference's trajectory up to fp32 vs fp64 arithmetic.
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed);
+    static Rng derive(std::uint64_t seed, std::uint64_t stream);
+    std::uint64_t next_u64();
+    double uniform();
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    std::uint64_t uniform_int(std::uint64_t n);
+
+private:
+    std::uint64_t mt_[312];
+    int idx_ = 312;
+};
+
+struct TrainOptions {
+    int epochs = 30;
+    int batch_size = 32;
+    std::uint64_t seed = 1;
+    int threads = 1;          // accepted for source compatibility; batches run on the GPU
+    double learning_rate = 1e-3;
+    double clip_norm = 5.0;
+};
+
+struct EpochStats {
+    int epoch = 0;
+    double train_loss = 0.0;
+    double train_accuracy = 0.0;  // per-position argmax accuracy, percent
+    double test_loss = 0.0;
+    double test_accuracy = 0.0;
+};
+
+struct TrainResult {
+    ModelParams params;
+    std::vector<EpochStats> log;
+};
+
+Vocabulary build_vocab(const KernelSpec& spec, const std::vector<Sample>& dataset);
+ModelParams init_model(const ModelConfig& config, const KernelSpec& spec, const Vocabulary& vocab,
+                       Precision precision, std::uint64_t seed);
+TrainResult train_model(const ModelConfig& config, const KernelSpec& spec, const Vocabulary& vocab,
+                        Precision precision, const std::vector<Sample>& train_set,
+                        const std::vector<Sample>& test_set, const TrainOptions& options,
+                        const std::function<void(const EpochStats&)>& on_epoch = {}, int device = 0);
+void save_checkpoint(const ModelParams& params, const std::string& path);
+
 }  // namespace kernelseer

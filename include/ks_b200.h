@@ -280,6 +280,10 @@ ks_status ks_trainer_apply(ks_trainer* tr, const float* d_grads, int64_t batch, 
 ks_status ks_trainer_step(ks_trainer* tr, const int32_t* tok, const int32_t* tgt, const int64_t* idx,
                           int64_t B, int64_t epoch, uint64_t seed, double lr, double clip,
                           double* out_loss_sum, int64_t* out_matches);
+/* Host-buffer forward only (evaluate_set, models.cpp:827-856): teacher-forced
+ * loss sum and per-position argmax matches of B samples, dropout off. */
+ks_status ks_trainer_evaluate(ks_trainer* tr, const int32_t* tok, const int32_t* tgt, int64_t B,
+                              double* out_loss_sum, int64_t* out_matches);
 /* Parameters in reference flat order (the model's tensors concatenated in
  * ks_model_desc / checkpoint order), to and from the host. */
 ks_status ks_trainer_export(const ks_trainer* tr, float* host_ref_flat);

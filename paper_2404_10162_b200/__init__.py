@@ -20,12 +20,14 @@ from ._kernelseer_b200 import (  # noqa: F401
     ConstraintPredicate,
     KernelSpec,
     KernelseerError,
+    ModelConfig,
     ModelParams,
     Sample,
     builtin_spec,
     builtin_specs,
     divisibility_predicate,
     greedy_predict,
+    init_model,
     load_checkpoint,
     membership_predicate,
     predict,
@@ -33,7 +35,9 @@ from ._kernelseer_b200 import (  # noqa: F401
     predicate,
     product_limit_predicate,
     resource_budget_predicate,
+    save_checkpoint,
     search_space_size,
     topk_metrics,
+    train,
     validate,
 )

@@ -86,7 +86,7 @@ EXPORTS = [
     "ks_beam_search_batch_hooked",
     "ks_trainer_create", "ks_trainer_create_from_checkpoint", "ks_trainer_destroy",
     "ks_trainer_num_params", "ks_trainer_num_ref_params", "ks_trainer_last_launch_count", "ks_trainer_loss_grads",
-    "ks_trainer_apply", "ks_trainer_step", "ks_trainer_export", "ks_trainer_import",
+    "ks_trainer_apply", "ks_trainer_step", "ks_trainer_evaluate", "ks_trainer_export", "ks_trainer_import",
     "ks_trainer_to_reference_layout",
 ]
 
@@ -150,6 +150,7 @@ def lib():
     L.ks_trainer_apply.argtypes = [vp, vp, i64, dbl, dbl, vp]
     L.ks_trainer_step.argtypes = [vp, P(i32), P(i32), P(i64), i64, i64, C.c_uint64, dbl, dbl,
                                   P(dbl), P(i64)]
+    L.ks_trainer_evaluate.argtypes = [vp, P(i32), P(i32), i64, P(dbl), P(i64)]
     L.ks_trainer_export.argtypes = [vp, P(C.c_float)]
     L.ks_trainer_import.argtypes = [vp, P(C.c_float)]
     L.ks_trainer_to_reference_layout.argtypes = [vp, P(C.c_float), P(C.c_float)]

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <sstream>
 
 #include "ks_b200.h"
@@ -831,6 +832,386 @@ std::vector<EvalReport> topk_metrics(const SequencePredictor& predictor, const s
         reports.push_back(std::move(r));
     }
     return reports;
+}
+
+// ------------------------------------------------------------------ training
+// Rng: mt19937_64 ([rand.eng.mers], parameters of std::mt19937_64) with the
+// reference's SplitMix-style derive and 53-bit uniforms (rng.hpp:13-71).
+Rng::Rng(std::uint64_t seed) {
+    mt_[0] = seed;
+    for (int i = 1; i < 312; ++i) mt_[i] = 6364136223846793005ULL * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + (std::uint64_t)i;
+    idx_ = 312;
+}
+
+Rng Rng::derive(std::uint64_t seed, std::uint64_t stream) {
+    auto mix = [](std::uint64_t z) {
+        z += 0x9e3779b97f4a7c15ULL;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    };
+    return Rng(mix(mix(seed) + 0x9e3779b97f4a7c15ULL * (stream + 1)));
+}
+
+std::uint64_t Rng::next_u64() {
+    if (idx_ >= 312) {
+        for (int i = 0; i < 312; ++i) {
+            const std::uint64_t x = (mt_[i] & 0xFFFFFFFF80000000ULL) | (mt_[(i + 1) % 312] & 0x7FFFFFFFULL);
+            std::uint64_t xa = x >> 1;
+            if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+            mt_[i] = mt_[(i + 156) % 312] ^ xa;
+        }
+        idx_ = 0;
+    }
+    std::uint64_t y = mt_[idx_++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+}
+
+double Rng::uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+
+std::uint64_t Rng::uniform_int(std::uint64_t n) {
+    const std::uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+    std::uint64_t v;
+    do {
+        v = next_u64();
+    } while (v >= limit);
+    return v % n;
+}
+
+// build_vocab (encoding.cpp:52-86): input values seen per field, ascending;
+// outputs are the spec's legal sets.
+Vocabulary build_vocab(const KernelSpec& spec, const std::vector<Sample>& dataset) {
+    if (dataset.empty()) throw ParameterError("build_vocab: dataset is empty");
+    std::array<std::vector<std::int64_t>, kNumInputFields> seen;
+    for (const Sample& smp : dataset) {
+        for (int f = 0; f < kNumInputFields; ++f) seen[(size_t)f].push_back(descriptor_field(smp.descriptor, f));
+        for (const auto& p : spec.params) {
+            auto it = smp.params.find(p.name);
+            if (it == smp.params.end()) throw ValidationError("sample missing parameter " + p.name, p.name);
+            if (std::find(p.values.begin(), p.values.end(), it->second) == p.values.end())
+                throw ValidationError("value " + std::to_string(it->second) + " of parameter " + p.name +
+                                          " is outside the legal set for kernel " + spec.name,
+                                      p.name);
+        }
+    }
+    std::vector<FieldVocab> in, out;
+    for (int f = 0; f < kNumInputFields; ++f) {
+        auto& v = seen[(size_t)f];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        in.push_back({kInputFieldNames[(size_t)f], v});
+    }
+    for (const auto& p : spec.params) out.push_back({p.name, p.values});
+    return Vocabulary(std::move(in), std::move(out));
+}
+
+namespace {
+
+int feedback_width(const Vocabulary& v) {
+    int w = 1;  // GO slot
+    for (const auto& f : v.output_params()) w += f.size();
+    return w;
+}
+int input_width(const Vocabulary& v) {
+    int w = 0;
+    for (const auto& f : v.input_fields()) w += f.size();
+    return w;
+}
+
+// nn::lstm_init (nn.cpp:309-318): w_* (in + H) x H ~ U(-1/sqrt(H), 1/sqrt(H)) drawn
+// in the order input, forget, output, cand; forget bias 1.
+void put_lstm_init(ModelParams& mp, const std::string& prefix, int in, int H, Rng& rng) {
+    const double lim = 1.0 / std::sqrt(static_cast<double>(H));
+    static const char* gates[4] = {"input", "forget", "output", "cand"};
+    for (const char* g : gates) {
+        HostTensor w;
+        w.shape = {in + H, H};
+        w.values.resize((size_t)(in + H) * H);
+        for (auto& x : w.values) x = static_cast<float>(rng.uniform(-lim, lim));
+        mp.tensors[prefix + ".w_" + g] = std::move(w);
+    }
+    for (const char* g : gates) {
+        HostTensor b;
+        b.shape = {H};
+        b.values.assign((size_t)H, std::string(g) == "forget" ? 1.0f : 0.0f);
+        mp.tensors[prefix + ".b_" + g] = std::move(b);
+    }
+}
+
+// nn::xavier_uniform / dense_init (nn.cpp:299-329)
+void put_dense_init(ModelParams& mp, const std::string& prefix, int in, int out, Rng& rng) {
+    const double lim = std::sqrt(6.0 / (in + out));
+    HostTensor w;
+    w.shape = {in, out};
+    w.values.resize((size_t)in * out);
+    for (auto& x : w.values) x = static_cast<float>(rng.uniform(-lim, lim));
+    mp.tensors[prefix + ".weights"] = std::move(w);
+    HostTensor b;
+    b.shape = {out};
+    b.values.assign((size_t)out, 0.0f);
+    mp.tensors[prefix + ".bias"] = std::move(b);
+}
+
+}  // namespace
+
+// init_model (models.cpp:178-259): same tensor names, shapes and draw order from
+// Rng::derive(seed, 0x171); values rounded to fp32 as a checkpoint stores them.
+ModelParams init_model(const ModelConfig& config, const KernelSpec& spec, const Vocabulary& vocab,
+                       Precision precision, std::uint64_t seed) {
+    spec.check();
+    if (vocab.num_output_positions() != spec.num_params())
+        throw ParameterError("vocabulary has " + std::to_string(vocab.num_output_positions()) +
+                             " output positions, kernel " + spec.name + " has " + std::to_string(spec.num_params()));
+    ModelParams mp;
+    mp.config = config;
+    mp.kernel = spec.name;
+    mp.precision = precision;
+    mp.vocab = vocab;
+    Rng rng = Rng::derive(seed, 0x171);
+    const int d_in = input_width(vocab), d_fb = feedback_width(vocab), T = vocab.num_output_positions();
+    int head_in = 0;
+    switch (config.variant) {
+        case ModelVariant::enc_dec:
+            put_lstm_init(mp, "encoder", d_in, config.encoder_state_size, rng);
+            put_lstm_init(mp, "decoder", d_fb, config.encoder_state_size, rng);
+            head_in = config.encoder_state_size;
+            break;
+        case ModelVariant::attn:
+        case ModelVariant::attn2: {
+            put_lstm_init(mp, "pre.fwd", d_in, config.pre_attention_size, rng);
+            put_lstm_init(mp, "pre.bwd", d_in, config.pre_attention_size, rng);
+            const int act = 2 * config.pre_attention_size;
+            put_lstm_init(mp, "post", config.variant == ModelVariant::attn ? act + d_fb : act, config.post_attention_size,
+                          rng);
+            put_dense_init(mp, "attn.hidden", config.post_attention_size + act, config.attention_dense_nodes, rng);
+            put_dense_init(mp, "attn.out", config.attention_dense_nodes, 1, rng);
+            head_in = config.post_attention_size;
+            break;
+        }
+        case ModelVariant::hybrid:
+        case ModelVariant::hybrid2: {
+            if (config.conv_layers.empty()) throw ParameterError("hybrid variants need at least one conv layer");
+            int ch = d_in, len = kNumInputFields;
+            for (std::size_t i = 0; i < config.conv_layers.size(); ++i) {
+                const ConvLayerSpec& l = config.conv_layers[i];
+                if (len < l.kernel_size) throw ShapeError("conv stack input length shorter than kernel size");
+                const int fan_in = ch * l.kernel_size, fan_out = l.filters * l.kernel_size;
+                const double lim = std::sqrt(6.0 / (fan_in + fan_out));
+                HostTensor f;
+                f.shape = {l.filters, ch, l.kernel_size};
+                f.values.resize((size_t)l.filters * ch * l.kernel_size);
+                for (auto& x : f.values) x = static_cast<float>(rng.uniform(-lim, lim));
+                mp.tensors["conv." + std::to_string(i) + ".filters"] = std::move(f);
+                HostTensor b;
+                b.shape = {l.filters};
+                b.values.assign((size_t)l.filters, 0.0f);
+                mp.tensors["conv." + std::to_string(i) + ".bias"] = std::move(b);
+                len = (len - l.kernel_size) / l.stride + 1;
+                ch = l.filters;
+            }
+            const int flat = ch * len, cell = config.decoder_cell_size;
+            put_lstm_init(mp, "bilstm1.fwd", flat, cell, rng);
+            put_lstm_init(mp, "bilstm1.bwd", flat, cell, rng);
+            const int b2 = config.variant == ModelVariant::hybrid ? 2 * cell : flat;
+            put_lstm_init(mp, "bilstm2.fwd", b2, cell, rng);
+            put_lstm_init(mp, "bilstm2.bwd", b2, cell, rng);
+            head_in = 2 * cell;
+            break;
+        }
+    }
+    for (int i = 0; i < T; ++i) put_dense_init(mp, "head." + std::to_string(i), head_in, vocab.output_param(i).size(), rng);
+    return mp;
+}
+
+// save_checkpoint (data.cpp:464-509): kernelseer-checkpoint/1.
+void save_checkpoint(const ModelParams& params, const std::string& path) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw CheckpointError(CheckpointError::Kind::io, "cannot write " + path);
+    const ModelConfig& c = params.config;
+    out << "format: kernelseer-checkpoint/1\n";
+    out << "variant: " << variant_label(c.variant) << "\n";
+    out << "kernel: " << params.kernel << "\n";
+    out << "precision: " << precision_label(params.precision) << "\n";
+    out << "encoder_state_size: " << c.encoder_state_size << "\n";
+    out << "pre_attention_size: " << c.pre_attention_size << "\n";
+    out << "post_attention_size: " << c.post_attention_size << "\n";
+    out << "attention_dense_nodes: " << c.attention_dense_nodes << "\n";
+    out << "decoder_cell_size: " << c.decoder_cell_size << "\n";
+    out << "dropout: " << c.dropout << "\n";
+    out << "recurrent_dropout: " << c.recurrent_dropout << "\n";
+    out << "conv_layers: ";
+    for (std::size_t i = 0; i < c.conv_layers.size(); ++i)
+        out << (i ? ";" : "") << c.conv_layers[i].filters << "," << c.conv_layers[i].kernel_size << ","
+            << c.conv_layers[i].stride;
+    out << "\n";
+    for (int f = 0; f < kNumInputFields; ++f)
+        out << "input_vocab." << params.vocab.input_field(f).name << ": " << join(params.vocab.input_field(f).values)
+            << "\n";
+    out << "output_params: " << params.vocab.num_output_positions() << "\n";
+    for (int i = 0; i < params.vocab.num_output_positions(); ++i)
+        out << "param." << i << ": " << params.vocab.output_param(i).name << " = "
+            << join(params.vocab.output_param(i).values) << "\n";
+    for (const auto& [name, t] : params.tensors) {
+        out << "tensor: " << name << " ";
+        for (std::size_t i = 0; i < t.shape.size(); ++i) out << (i ? "x" : "") << t.shape[i];
+        out << "\n";
+    }
+    out << "\n";
+    for (const auto& [name, t] : params.tensors) {
+        for (float v : t.values) {
+            std::uint32_t u;
+            std::memcpy(&u, &v, 4);
+            const unsigned char b[4] = {(unsigned char)(u & 0xFF), (unsigned char)((u >> 8) & 0xFF),
+                                        (unsigned char)((u >> 16) & 0xFF), (unsigned char)(u >> 24)};
+            out.write(reinterpret_cast<const char*>(b), 4);
+        }
+    }
+    if (!out) throw CheckpointError(CheckpointError::Kind::io, "write failed: " + path);
+}
+
+namespace {
+
+// The flattened ModelParams a ks_model_desc points into.
+struct DescHolder {
+    std::vector<int32_t> in_sizes, vsizes, conv;
+    std::vector<int64_t> in_vals, out_vals;
+    std::vector<const char*> names;
+    std::vector<int32_t> numel;
+    std::vector<const float*> data;
+    ks_model_desc d{};
+    explicit DescHolder(const ModelParams& params) {
+        for (const auto& f : params.vocab.input_fields()) {
+            in_sizes.push_back(f.size());
+            in_vals.insert(in_vals.end(), f.values.begin(), f.values.end());
+        }
+        for (const auto& f : params.vocab.output_params()) {
+            vsizes.push_back(f.size());
+            out_vals.insert(out_vals.end(), f.values.begin(), f.values.end());
+        }
+        for (const auto& [n, t] : params.tensors) {
+            names.push_back(n.c_str());
+            numel.push_back(static_cast<int32_t>(t.values.size()));
+            data.push_back(t.values.data());
+        }
+        for (const auto& l : params.config.conv_layers) {
+            conv.push_back(l.filters);
+            conv.push_back(l.kernel_size);
+            conv.push_back(l.stride);
+        }
+        d.variant = static_cast<int32_t>(params.config.variant);
+        d.decoder_cell_size = params.config.decoder_cell_size;
+        d.num_conv_layers = static_cast<int32_t>(params.config.conv_layers.size());
+        d.conv_layers = conv.data();
+        d.encoder_state_size = params.config.encoder_state_size;
+        d.pre_attention_size = params.config.pre_attention_size;
+        d.post_attention_size = params.config.post_attention_size;
+        d.attention_dense_nodes = params.config.attention_dense_nodes;
+        d.num_positions = params.num_output_positions();
+        d.input_sizes = in_sizes.data();
+        d.input_values = in_vals.data();
+        d.vocab_sizes = vsizes.data();
+        d.output_values = out_vals.data();
+        d.num_tensors = static_cast<int32_t>(names.size());
+        d.tensor_names = names.data();
+        d.tensor_numel = numel.data();
+        d.tensor_data = data.data();
+    }
+};
+
+}  // namespace
+
+// train_model (models.cpp:862-969): init_model, per epoch a Fisher-Yates shuffle
+// from Rng::derive(seed, 0x3ff000 + epoch), batches of batch_size in that order
+// (each sample's dropout stream Rng::derive(seed, epoch << 32 | index) drawn on the
+// device), gradient sum / batch, clip, Adam; then the test set teacher-forced
+// (dropout off).  One GPU; data-parallel training is paper_2404_10162_b200.train.
+TrainResult train_model(const ModelConfig& config, const KernelSpec& spec, const Vocabulary& vocab,
+                        Precision precision, const std::vector<Sample>& train_set,
+                        const std::vector<Sample>& test_set, const TrainOptions& options,
+                        const std::function<void(const EpochStats&)>& on_epoch, int device) {
+    if (train_set.empty()) throw ParameterError("train_model: empty training set");
+    if (options.epochs < 1 || options.batch_size < 1)
+        throw ParameterError("train_model: epochs and batch size must be >= 1");
+    if (config.dropout < 0.0 || config.dropout >= 1.0 || config.recurrent_dropout < 0.0 ||
+        config.recurrent_dropout >= 1.0)
+        throw ParameterError("dropout rates must be in [0,1)");
+    const int T = vocab.num_output_positions();
+    auto encode_all = [&](const std::vector<Sample>& set, std::vector<int32_t>& tok, std::vector<int32_t>& tgt) {
+        for (const Sample& smp : set) {
+            const TokenSequence in = encode_problem(smp.descriptor, vocab);
+            const TokenSequence out = encode_params(smp.params, spec, vocab);
+            tok.insert(tok.end(), in.ids.begin(), in.ids.end());
+            tgt.insert(tgt.end(), out.ids.begin(), out.ids.end());
+        }
+    };
+    std::vector<int32_t> tr_tok, tr_tgt, te_tok, te_tgt;
+    encode_all(train_set, tr_tok, tr_tgt);
+    encode_all(test_set, te_tok, te_tgt);
+
+    TrainResult result;
+    result.params = init_model(config, spec, vocab, precision, options.seed);
+    ks_trainer* tr = nullptr;
+    {
+        DescHolder h(result.params);
+        check(ks_trainer_create(&h.d, config.dropout, config.recurrent_dropout, device, &tr));
+    }
+    std::unique_ptr<ks_trainer, void (*)(ks_trainer*)> guard(tr, ks_trainer_destroy);
+    const int n = static_cast<int>(train_set.size());
+    std::vector<int32_t> btok, btgt;
+    std::vector<int64_t> bidx;
+    for (int epoch = 1; epoch <= options.epochs; ++epoch) {
+        std::vector<int> order((size_t)n);
+        for (int i = 0; i < n; ++i) order[(size_t)i] = i;
+        Rng shuffle = Rng::derive(options.seed, 0x3ff000ULL + static_cast<std::uint64_t>(epoch));
+        for (std::size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[shuffle.uniform_int(i)]);
+        double epoch_loss = 0.0;
+        long long matches = 0;
+        for (int start = 0; start < n; start += options.batch_size) {
+            const int B = std::min(n, start + options.batch_size) - start;
+            btok.resize((size_t)B * kNumInputFields);
+            btgt.resize((size_t)B * T);
+            bidx.resize((size_t)B);
+            for (int b = 0; b < B; ++b) {
+                const int idx = order[(size_t)(start + b)];
+                std::memcpy(&btok[(size_t)b * kNumInputFields], &tr_tok[(size_t)idx * kNumInputFields],
+                            sizeof(int32_t) * kNumInputFields);
+                std::memcpy(&btgt[(size_t)b * T], &tr_tgt[(size_t)idx * T], sizeof(int32_t) * (size_t)T);
+                bidx[(size_t)b] = idx;
+            }
+            double loss = 0.0;
+            int64_t m = 0;
+            check(ks_trainer_step(tr, btok.data(), btgt.data(), bidx.data(), B, epoch, options.seed,
+                                  options.learning_rate, options.clip_norm, &loss, &m));
+            epoch_loss += loss;
+            matches += m;
+        }
+        EpochStats st;
+        st.epoch = epoch;
+        st.train_loss = epoch_loss / n;
+        st.train_accuracy = 100.0 * static_cast<double>(matches) / (static_cast<double>(n) * T);
+        if (!test_set.empty()) {
+            double loss = 0.0;
+            int64_t m = 0;
+            check(ks_trainer_evaluate(tr, te_tok.data(), te_tgt.data(), (int64_t)test_set.size(), &loss, &m));
+            st.test_loss = loss / static_cast<double>(test_set.size());
+            st.test_accuracy = 100.0 * static_cast<double>(m) / (static_cast<double>(test_set.size()) * T);
+        }
+        result.log.push_back(st);
+        if (on_epoch) on_epoch(st);
+    }
+    // trained parameters back into the reference tensors (checkpoint order)
+    std::vector<float> flat((size_t)ks_trainer_num_ref_params(tr));
+    check(ks_trainer_export(tr, flat.data()));
+    std::size_t o = 0;
+    for (auto& [name, t] : result.params.tensors) {
+        std::copy(flat.begin() + (long)o, flat.begin() + (long)(o + t.values.size()), t.values.begin());
+        o += t.values.size();
+    }
+    return result;
 }
 
 }  // namespace kernelseer

@@ -14,6 +14,7 @@
 #include <pybind11/stl.h>
 
 #include <mutex>
+#include <tuple>
 
 #include "kernelseer_b200.hpp"
 
@@ -279,4 +280,86 @@ PYBIND11_MODULE(_kernelseer_b200, m) {
           },
           py::arg("params"), py::arg("test"), py::arg("k_values"),
           py::arg("predicates") = std::vector<ConstraintPredicate>{}, py::arg("threads") = 1);
+    // ------------------------------------------------------------ training
+    // (bindings/module.cpp:183-256): same class / kwargs / defaults; the batches
+    // run on the GPU (enc-dec / attn / attn-2).
+    py::class_<ModelConfig>(m, "ModelConfig")
+        .def(py::init([](const std::string& variant, int encoder_state_size, int pre_attention_size,
+                         int post_attention_size, int attention_dense_nodes,
+                         const std::vector<std::tuple<int, int, int>>& conv_layers, int decoder_cell_size,
+                         double dropout, double recurrent_dropout) {
+                 ModelConfig c;
+                 c.variant = variant_from_label(variant);
+                 c.encoder_state_size = encoder_state_size;
+                 c.pre_attention_size = pre_attention_size;
+                 c.post_attention_size = post_attention_size;
+                 c.attention_dense_nodes = attention_dense_nodes;
+                 c.conv_layers.clear();
+                 for (const auto& [f, k, st] : conv_layers) c.conv_layers.push_back({f, k, st});
+                 c.decoder_cell_size = decoder_cell_size;
+                 c.dropout = dropout;
+                 c.recurrent_dropout = recurrent_dropout;
+                 if (encoder_state_size < 1 || pre_attention_size < 1 || post_attention_size < 1 ||
+                     attention_dense_nodes < 1 || decoder_cell_size < 1)
+                     throw ParameterError("model sizes must be >= 1");
+                 if (dropout < 0.0 || dropout >= 1.0 || recurrent_dropout < 0.0 || recurrent_dropout >= 1.0)
+                     throw ParameterError("dropout rates must be in [0,1)");
+                 return c;
+             }),
+             py::arg("variant") = "hybrid-2", py::arg("encoder_state_size") = 256, py::arg("pre_attention_size") = 256,
+             py::arg("post_attention_size") = 512, py::arg("attention_dense_nodes") = 2,
+             py::arg("conv_layers") = std::vector<std::tuple<int, int, int>>{{64, 3, 1}, {32, 3, 1}},
+             py::arg("decoder_cell_size") = 256, py::arg("dropout") = 0.2, py::arg("recurrent_dropout") = 0.2)
+        .def_property_readonly("variant", [](const ModelConfig& c) { return variant_label(c.variant); });
+
+    m.def("train",
+          [](const ModelConfig& config, const KernelSpec& spec, const std::vector<Sample>& train_set,
+             const std::vector<Sample>& test_set, int epochs, int batch_size, std::uint64_t seed, int threads,
+             double learning_rate, int device) {
+              std::vector<Sample> all = train_set;
+              all.insert(all.end(), test_set.begin(), test_set.end());
+              const Vocabulary vocab = build_vocab(spec, all);
+              const Precision precision = train_set.empty() ? Precision::full : train_set[0].precision;
+              TrainOptions o;
+              o.epochs = epochs;
+              o.batch_size = batch_size;
+              o.seed = seed;
+              o.threads = threads;
+              o.learning_rate = learning_rate;
+              TrainResult r;
+              {
+                  py::gil_scoped_release release;
+                  r = train_model(config, spec, vocab, precision, train_set, test_set, o, {}, device);
+              }
+              py::list log;
+              for (const EpochStats& e : r.log) {
+                  py::dict row;
+                  row["epoch"] = e.epoch;
+                  row["train_loss"] = e.train_loss;
+                  row["train_avg_acc"] = e.train_accuracy;
+                  row["test_loss"] = e.test_loss;
+                  row["test_avg_acc"] = e.test_accuracy;
+                  log.append(row);
+              }
+              auto pm = std::make_shared<PyModel>();
+              pm->params = std::make_shared<ModelParams>(std::move(r.params));
+              pm->device = device;
+              return py::make_tuple(pm, log);
+          },
+          py::arg("config"), py::arg("spec"), py::arg("train_set"), py::arg("test_set"), py::arg("epochs") = 30,
+          py::arg("batch_size") = 32, py::arg("seed") = 1, py::arg("threads") = 1, py::arg("learning_rate") = 1e-3,
+          py::arg("device") = 0);
+
+    m.def("init_model",
+          [](const ModelConfig& config, const KernelSpec& spec, const std::vector<Sample>& samples, std::uint64_t seed) {
+              auto pm = std::make_shared<PyModel>();
+              pm->params = std::make_shared<ModelParams>(
+                  init_model(config, spec, build_vocab(spec, samples),
+                             samples.empty() ? Precision::full : samples[0].precision, seed));
+              return pm;
+          },
+          py::arg("config"), py::arg("spec"), py::arg("samples"), py::arg("seed") = 1,
+          "init_model (models.cpp:178-259) over build_vocab(spec, samples)");
+    m.def("save_checkpoint", [](const std::shared_ptr<PyModel>& p, const std::string& path) { save_checkpoint(*p->params, path); },
+          py::arg("params"), py::arg("path"));
 }

@@ -1625,6 +1625,30 @@ extern "C" ks_status ks_trainer_step(ks_trainer* t, const int32_t* tok, const in
     return KS_OK;
 }
 
+extern "C" ks_status ks_trainer_evaluate(ks_trainer* t, const int32_t* tok, const int32_t* tgt, int64_t B,
+                                         double* out_loss_sum, int64_t* out_matches) {
+    if (!t || !tok || !tgt) return set_error(KS_ERR_PARAMETER, "null argument");
+    if (B < 1) return set_error(KS_ERR_PARAMETER, "batch must be >= 1");
+    cudaSetDevice(t->device);
+    ks_status st;
+    if ((st = ensure_ws(*t, (int)B))) return st;
+    DBuf res;
+    KT_CUDA(res.ensure(16));
+    cudaStream_t s = nullptr;
+    KT_CUDA(cudaMemcpyAsync(t->tok.p, tok, (size_t)B * 7 * 4, cudaMemcpyHostToDevice, s));
+    KT_CUDA(cudaMemcpyAsync(t->tgt.p, tgt, (size_t)B * t->T * 4, cudaMemcpyHostToDevice, s));
+    t->launches = 0;
+    if ((st = run_batch(*t, (int)B, t->tok.as<int>(), t->tgt.as<int>(), nullptr, -1, 0, nullptr, false,
+                        res.as<double>(), reinterpret_cast<long long*>(res.as<char>() + 8), s)))
+        return st;
+    double hres[2];
+    KT_CUDA(cudaMemcpyAsync(hres, res.p, 16, cudaMemcpyDeviceToHost, s));
+    KT_CUDA(cudaStreamSynchronize(s));
+    if (out_loss_sum) *out_loss_sum = hres[0];
+    if (out_matches) std::memcpy(out_matches, &hres[1], 8);
+    return KS_OK;
+}
+
 extern "C" ks_status ks_trainer_export(const ks_trainer* t, float* host_ref_flat) {
     if (!t || !host_ref_flat) return set_error(KS_ERR_PARAMETER, "null argument");
     cudaSetDevice(t->device);
