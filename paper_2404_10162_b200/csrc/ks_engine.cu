@@ -1170,8 +1170,8 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         if (smem > (size_t)E.beam_smem_max)
             return set_error(KS_ERR_UNSUPPORTED, "beam width x vocabulary too large for the beam kernel");
         // persistent: the head weights are staged into shared memory once per CTA
-        const int per_sm = std::max(1, std::min(8, (int)((228 * 1024) / (smem + 1024))));
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((C + warps - 1) / warps, (int64_t)E.num_sms * per_sm));
+        // upper bound (one warp per config); launch_beam trims it to one resident wave
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((C + warps - 1) / warps, (int64_t)E.num_sms * 16));
         if (!launch_beam(b, E.meta, warps, smem, grid, s))
             return set_error(KS_ERR_CUDA, "beam kernel launch failed");
         E.launches++;

@@ -970,14 +970,17 @@ bool launch_beam_split(const BeamArgs& a, const PosMeta& m, int warps, size_t sm
         cudaFuncSetAttribute(beam_step_t<32, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    if (V <= 4)
-        beam_step_t<4, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
-    else if (V <= 8)
-        beam_step_t<8, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
-    else if (V <= 16)
-        beam_step_t<16, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
-    else
-        beam_step_t<32, SPLIT><<<grid, warps * 32, smem, s>>>(a, m);
+    auto kern = V <= 4 ? beam_step_t<4, SPLIT> : V <= 8 ? beam_step_t<8, SPLIT>
+              : V <= 16 ? beam_step_t<16, SPLIT> : beam_step_t<32, SPLIT>;
+    // persistent grid: exactly the CTAs that fit at once (registers and shared memory
+    // both limit residency; a partial second wave would leave most SMs idle)
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int g = std::min(grid, sms * per_sm);
+    kern<<<g, warps * 32, smem, s>>>(a, m);
     return cudaGetLastError() == cudaSuccess;
 }
 
