@@ -252,14 +252,22 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
     float sd[ND > 0 ? ND : 1];
 #pragma unroll
     for (int d = 0; d < ND; ++d) sd[d] = 0.0f;
+#pragma unroll 4
     for (int c = lane; c < p.NS / 4; c += 32) {
         const float4 v = s ? *reinterpret_cast<const float4*>(s + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
         if (ND > 0 && s) {
+            // the 4 W_s rows of this chunk are 4*ND contiguous floats: vector loads
             const float vv[4] = {v.x, v.y, v.z, v.w};
+            float w[4 * (ND > 0 ? ND : 1)];
+#pragma unroll
+            for (int q = 0; q < ND; ++q) {
+                const float4 w4 = reinterpret_cast<const float4*>(p.Ws + 4 * c * ND)[q];
+                w[4 * q] = w4.x; w[4 * q + 1] = w4.y; w[4 * q + 2] = w4.z; w[4 * q + 3] = w4.w;
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e)
 #pragma unroll
-                for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], p.Ws[(4 * c + e) * ND + d], sd[d]);
+                for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], w[e * ND + d], sd[d]);
         }
         store4<SPLIT>(p, base + hc + 4 * c, v);
     }
