@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ks_b200.h"
@@ -1214,19 +1215,51 @@ ks_status collect_profile(ks_engine& E) {
     return KS_OK;
 }
 
+// Host-side copies of the reference-facing call (pageable <-> pinned staging):
+// large ones are split over a few threads (one memcpy thread reaches ~10 GB/s).
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kPart = (size_t)2 << 20;
+    const int parts = (int)std::min<size_t>(8, bytes / kPart);
+    if (parts < 2) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t step = (bytes / parts + 63) / 64 * 64;
+    std::vector<std::thread> th;
+    for (int i = 1; i < parts; ++i) {
+        const size_t o = (size_t)i * step;
+        if (o >= bytes) break;
+        th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, std::min(step, bytes - o)); });
+    }
+    std::memcpy(dst, src, std::min(step, bytes));
+    for (auto& t : th) t.join();
+}
+
 ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, int64_t B, int32_t k,
                       bool greedy, const ks_pred* preds, int32_t n_preds, int32_t* out_tok,
                       double* out_lp, int32_t* out_count, int32_t* out_status, int32_t* out_fpred,
                       int32_t* out_fstep, ks_host_pred_fn hook = nullptr, void* user = nullptr) {
     ks_engine& E = *eng;
     const int T = E.T;
-    for (int64_t b = 0; b < B; ++b)
-        for (int f = 0; f < 7; ++f) {
-            const int t = tok[b * 7 + f];
-            if (t < 0 || t >= E.in_sizes[(size_t)f])
-                return set_error(KS_ERR_INDEX, "input token " + std::to_string(t) + " out of range for field " +
-                                                   std::to_string(f) + " (row " + std::to_string(b) + ")");
+    {
+        uint32_t lim[7];
+        for (int f = 0; f < 7; ++f) lim[f] = (uint32_t)E.in_sizes[(size_t)f];
+        bool bad = false;
+        for (int64_t b = 0; b < B && !bad; ++b) {
+            const int32_t* r = tok + b * 7;
+            bad = ((uint32_t)r[0] >= lim[0]) | ((uint32_t)r[1] >= lim[1]) | ((uint32_t)r[2] >= lim[2]) |
+                  ((uint32_t)r[3] >= lim[3]) | ((uint32_t)r[4] >= lim[4]) | ((uint32_t)r[5] >= lim[5]) |
+                  ((uint32_t)r[6] >= lim[6]);
         }
+        if (bad)
+            for (int64_t b = 0; b < B; ++b)
+                for (int f = 0; f < 7; ++f) {
+                    const int t = tok[b * 7 + f];
+                    if (t < 0 || t >= E.in_sizes[(size_t)f])
+                        return set_error(KS_ERR_INDEX, "input token " + std::to_string(t) + " out of range for field " +
+                                                           std::to_string(f) + " (row " + std::to_string(b) + ")");
+                }
+    }
     PredDev pd;
     ks_status st;
     if ((st = upload_preds(E, preds, n_preds, pd))) return st;
@@ -1248,7 +1281,7 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
         const int64_t n = std::min<int64_t>(C, B - c0);
         int32_t* htok = E.h_in.as<int32_t>();
         int64_t* hdesc = reinterpret_cast<int64_t*>(E.h_in.as<char>() + (size_t)C * 7 * 4);
-        std::memcpy(htok, tok + c0 * 7, (size_t)n * 7 * 4);
+        par_memcpy(htok, tok + c0 * 7, (size_t)n * 7 * 4);
         KS_CUDA(cudaMemcpyAsync(E.tok.p, htok, (size_t)n * 7 * 4, cudaMemcpyHostToDevice, E.stream));
         const long long* ddesc = nullptr;
         if (desc && pd.needs_desc) {
@@ -1272,9 +1305,9 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
             KS_CUDA(cudaMemcpyAsync(h_misc + 3 * C, E.ofstep.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
         }
         KS_CUDA(cudaStreamSynchronize(E.stream));
-        std::memcpy(out_tok + c0 * k * T, h_tok, (size_t)n * k * T * 4);
+        par_memcpy(out_tok + c0 * k * T, h_tok, (size_t)n * k * T * 4);
         if (!greedy) {
-            if (out_lp) std::memcpy(out_lp + c0 * k, h_lp, (size_t)n * k * 8);
+            if (out_lp) par_memcpy(out_lp + c0 * k, h_lp, (size_t)n * k * 8);
             if (out_count) std::memcpy(out_count + c0, h_misc, (size_t)n * 4);
             if (out_status) std::memcpy(out_status + c0, h_misc + C, (size_t)n * 4);
             if (out_fpred) std::memcpy(out_fpred + c0, h_misc + 2 * C, (size_t)n * 4);

@@ -282,13 +282,20 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
             float acc[ND > 0 ? ND : 1];
 #pragma unroll
             for (int d = 0; d < ND; ++d) acc[d] = 0.0f;
+#pragma unroll 4
             for (int c = lane; c < p.NA2 / 4; c += 32) {
                 const float4 a4 = *reinterpret_cast<const float4*>(act + t * p.NA2 + 4 * c);
                 const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+                float w[4 * (ND > 0 ? ND : 1)];
+#pragma unroll
+                for (int q = 0; q < ND; ++q) {
+                    const float4 w4 = reinterpret_cast<const float4*>(p.Wa + 4 * c * ND)[q];
+                    w[4 * q] = w4.x; w[4 * q + 1] = w4.y; w[4 * q + 2] = w4.z; w[4 * q + 3] = w4.w;
+                }
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) acc[d] = fmaf(av[e], p.Wa[(4 * c + e) * ND + d], acc[d]);
+                    for (int d = 0; d < ND; ++d) acc[d] = fmaf(av[e], w[e * ND + d], acc[d]);
             }
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
