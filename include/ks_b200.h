@@ -24,6 +24,7 @@
  *                              evaluate_set, adam_step
  *   the batch entry points     parallel_stripes fan-out include/kernelseer/parallel.hpp:14-27 as used
  *                              in topk_metrics          src/eval.cpp:105-137
+ *   ks_topk_metrics_batch      topk_metrics scoring     src/eval.cpp:100-146
  */
 #ifndef KS_B200_H
 #define KS_B200_H
@@ -203,6 +204,19 @@ ks_status ks_beam_search_batch_hooked(ks_engine* eng, const int32_t* tok, const 
                                       int32_t* out_tok, double* out_lp, int32_t* out_count,
                                       int32_t* out_status, int32_t* out_fail_pred,
                                       int32_t* out_fail_step);
+
+/* topk_metrics' inner loop on the device (src/eval.cpp:100-146): a beam
+ * search of width k over B configs (predicates / hook as
+ * ks_beam_search_batch_hooked; hook may be NULL), then per config the
+ * best-matching beam against truth (B x T token ids; most matching positions,
+ * ties to the higher-ranked beam) and the any-of-k perfect flag, reduced on the
+ * device.  out_pos_matches (T): per-position hits of the best-matching beams;
+ * out_perfect: configs with a perfect beam.  Exhausted configs score nothing
+ * (eval.cpp:114-116). */
+ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                                const int32_t* truth, int64_t B, int32_t beam_width,
+                                const ks_pred* preds, int32_t n_preds, ks_host_pred_fn hook,
+                                void* user, int64_t* out_pos_matches, int64_t* out_perfect);
 
 /* greedy_decode: out_tok B x T. */
 ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok);

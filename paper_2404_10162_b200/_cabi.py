@@ -83,7 +83,7 @@ EXPORTS = [
     "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
     "ks_engine_profile_reset", "ks_engine_profile_gemm_ms", "ks_engine_profile_launches",
     "ks_engine_profile_launches_ex",
-    "ks_beam_search_batch_hooked",
+    "ks_beam_search_batch_hooked", "ks_topk_metrics_batch",
     "ks_trainer_create", "ks_trainer_create_from_checkpoint", "ks_trainer_destroy",
     "ks_trainer_num_params", "ks_trainer_num_ref_params", "ks_trainer_last_launch_count", "ks_trainer_loss_grads",
     "ks_trainer_apply", "ks_trainer_step", "ks_trainer_evaluate", "ks_trainer_export", "ks_trainer_import",

@@ -795,38 +795,43 @@ std::vector<EvalReport> topk_metrics(const SequencePredictor& predictor, const s
     const ModelParams& params = predictor.params();
     const KernelSpec spec = spec_of(params);
     const int arity = predictor.num_positions();
-    std::vector<TokenSequence> inputs, truths;
+    const std::size_t B = test.size();
+    std::vector<int32_t> tok(B * 7), truth(B * (size_t)arity);
+    std::vector<int64_t> desc(B * 7);
     std::vector<ProblemDescriptor> descs;
-    for (const Sample& s : test) {
-        inputs.push_back(encode_problem(s.descriptor, params.vocab));
-        truths.push_back(encode_params(s.params, spec, params.vocab));
-        descs.push_back(s.descriptor);
+    descs.reserve(B);
+    for (std::size_t i = 0; i < B; ++i) {
+        const TokenSequence in = encode_problem(test[i].descriptor, params.vocab);
+        const TokenSequence tr = encode_params(test[i].params, spec, params.vocab);
+        std::copy(in.ids.begin(), in.ids.end(), tok.begin() + (long)(i * 7));
+        std::copy(tr.ids.begin(), tr.ids.end(), truth.begin() + (long)(i * (size_t)arity));
+        for (int f = 0; f < 7; ++f) desc[i * 7 + (size_t)f] = descriptor_field(test[i].descriptor, f);
+        descs.push_back(test[i].descriptor);
     }
+    ResolvedPreds rp = resolve(params, predicates);
     std::vector<EvalReport> reports;
     for (int k : k_values) {
-        const BatchResult br = beam_search_batch(predictor, inputs, descs, k, predicates);
-        std::vector<TokenSequence> best(test.size());
-        int hits = 0;
-        for (std::size_t i = 0; i < test.size(); ++i) {
-            int best_m = -1;
-            TokenSequence bs;
-            bs.role = TokenSequence::Role::output;
-            bs.ids.assign(static_cast<std::size_t>(arity), -1);
-            bool perfect = false;
-            for (const ScoredSequence& beam : br.beams[i]) {
-                int m = 0;
-                for (int p = 0; p < arity; ++p) m += beam.tokens.ids[static_cast<std::size_t>(p)] == truths[i].ids[static_cast<std::size_t>(p)];
-                if (m == arity) perfect = true;
-                if (m > best_m) {
-                    best_m = m;
-                    bs = beam.tokens;
-                }
-            }
-            hits += perfect ? 1 : 0;
-            best[i] = std::move(bs);
+        // one device pass per k (a width-k search does not contain the width-j beams);
+        // the best-matching beam / any-of-k scoring stays on the device
+        std::vector<int64_t> hits((size_t)arity);
+        int64_t perfect = 0;
+        HookCtx ctx{&params, predicates, &rp.host, descs, {}};
+        const ks_status s = ks_topk_metrics_batch(
+            predictor.engine(), tok.data(), desc.data(), truth.data(), static_cast<int64_t>(B), k,
+            rp.preds.empty() ? nullptr : rp.preds.data(), static_cast<int32_t>(rp.preds.size()),
+            rp.host.empty() ? nullptr : host_hook, &ctx, hits.data(), &perfect);
+        if (!ctx.error.empty()) throw Error("predicate raised: " + ctx.error);
+        check(s);
+        EvalReport r;
+        r.sample_count = static_cast<int>(B);
+        r.per_param_accuracy.resize((size_t)arity);
+        double sum = 0.0;
+        for (int p = 0; p < arity; ++p) {
+            r.per_param_accuracy[(size_t)p] = static_cast<double>(hits[(size_t)p]) / static_cast<double>(B) * 100.0;
+            sum += r.per_param_accuracy[(size_t)p];
         }
-        EvalReport r = compute_metrics(best, truths);
-        r.perfect_prediction = 100.0 * hits / static_cast<double>(test.size());
+        r.average_accuracy = sum / arity;
+        r.perfect_prediction = 100.0 * static_cast<double>(perfect) / static_cast<double>(B);
         r.beam_width = k;
         r.constrained = !predicates.empty();
         reports.push_back(std::move(r));

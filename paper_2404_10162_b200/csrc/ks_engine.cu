@@ -34,6 +34,8 @@ __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long 
 size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tables);
 bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s);
 bool launch_hybrid_conv(const ConvArgs& p, cudaStream_t s);
+bool launch_topk_eval(const int* out_tok, const int* count, const int* truth, int B, int k, int T,
+                      unsigned long long* pos_matches, unsigned long long* perfect, cudaStream_t s);
 bool launch_split_rows(const float* src, long long n, __half* hi, __half* lo, int mode, cudaStream_t s);
 // tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
@@ -147,6 +149,7 @@ struct ks_engine {
     DevMem otok, olp, ocount, ostatus, ofpred, ofstep;
     DevMem preds, pbytes, tpos, tw, tfield;
     DevMem hrej;                  // host-hook rejections [C*k][Vmax]
+    DevMem truth, evalc;          // topk_metrics: truths [C][T], counters [T + 1]
     HostMem h_in, h_out, hk_keys, hk_live, hk_rej;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
@@ -1343,6 +1346,72 @@ extern "C" ks_status ks_beam_search_batch_hooked(ks_engine* eng, const int32_t* 
     if (!tok || !out_tok) return set_error(KS_ERR_PARAMETER, "null token buffer");
     return decode_host(eng, tok, desc, B, k, false, preds, n_preds, out_tok, out_lp, out_count, out_status,
                        out_fpred, out_fstep, hook, user);
+}
+
+extern "C" ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                                           const int32_t* truth, int64_t B, int32_t k, const ks_pred* preds,
+                                           int32_t n_preds, ks_host_pred_fn hook, void* user,
+                                           int64_t* out_pos_matches, int64_t* out_perfect) {
+    ks_status st = check_common(eng, B, k, preds, n_preds);
+    if (st) return st;
+    if (!tok || !truth || !out_pos_matches || !out_perfect) return set_error(KS_ERR_PARAMETER, "null buffer");
+    ks_engine& E = *eng;
+    const int T = E.T;
+    for (int p = 0; p < T; ++p) out_pos_matches[p] = 0;
+    *out_perfect = 0;
+    if (B == 0) return KS_OK;
+    for (int64_t b = 0; b < B; ++b)
+        for (int p = 0; p < T; ++p) {
+            const int v = truth[b * T + p];
+            if (v < 0 || v >= E.vsize[(size_t)p])
+                return set_error(KS_ERR_INDEX, "truth token " + std::to_string(v) + " out of range at position " +
+                                                   std::to_string(p) + " (row " + std::to_string(b) + ")");
+        }
+    for (int64_t b = 0; b < B; ++b)
+        for (int f = 0; f < 7; ++f) {
+            const int t = tok[b * 7 + f];
+            if (t < 0 || t >= E.in_sizes[(size_t)f])
+                return set_error(KS_ERR_INDEX, "input token " + std::to_string(t) + " out of range for field " +
+                                                   std::to_string(f) + " (row " + std::to_string(b) + ")");
+        }
+    PredDev pd;
+    if ((st = upload_preds(E, preds, n_preds, pd))) return st;
+    if (pd.needs_desc && !desc) return set_error(KS_ERR_PARAMETER, "divisibility predicates need descriptors");
+    pd.hook = hook;
+    pd.user = user;
+    E.launches = 0;
+    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
+    if (E.otok.ensure((size_t)C * k * T * 4) || E.olp.ensure((size_t)C * k * 8) || E.ocount.ensure((size_t)C * 4) ||
+        E.ostatus.ensure((size_t)C * 4) || E.ofpred.ensure((size_t)C * 4) || E.ofstep.ensure((size_t)C * 4) ||
+        E.truth.ensure((size_t)C * T * 4) || E.evalc.ensure((size_t)(T + 1) * 8))
+        return set_error(KS_ERR_CUDA, "output allocation failed");
+    if ((st = ensure_workspace(E, C, k))) return st;
+    KS_CUDA(cudaMemsetAsync(E.evalc.p, 0, (size_t)(T + 1) * 8, E.stream));
+    for (int64_t c0 = 0; c0 < B; c0 += C) {
+        const int64_t n = std::min<int64_t>(C, B - c0);
+        KS_CUDA(cudaMemcpyAsync(E.tok.p, tok + c0 * 7, (size_t)n * 7 * 4, cudaMemcpyHostToDevice, E.stream));
+        KS_CUDA(cudaMemcpyAsync(E.truth.p, truth + c0 * T, (size_t)n * T * 4, cudaMemcpyHostToDevice, E.stream));
+        const long long* ddesc = nullptr;
+        if (desc && pd.needs_desc) {
+            KS_CUDA(cudaMemcpyAsync(E.desc.p, desc + c0 * 7, (size_t)n * 7 * 8, cudaMemcpyHostToDevice, E.stream));
+            ddesc = E.desc.as<long long>();
+        }
+        if ((st = run_chunk(E, n, c0, k, false, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
+                            E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>())))
+            return st;
+        unsigned long long* cnt = E.evalc.as<unsigned long long>();
+        if (!launch_topk_eval(E.otok.as<int>(), E.ocount.as<int>(), E.truth.as<int>(), (int)n, k, T, cnt, cnt + T,
+                              E.stream))
+            return set_error(KS_ERR_CUDA, "topk_eval launch failed");
+        E.launches++;
+    }
+    std::vector<unsigned long long> h((size_t)T + 1);
+    KS_CUDA(cudaMemcpyAsync(h.data(), E.evalc.p, (size_t)(T + 1) * 8, cudaMemcpyDeviceToHost, E.stream));
+    KS_CUDA(cudaStreamSynchronize(E.stream));
+    for (int p = 0; p < T; ++p) out_pos_matches[p] = (int64_t)h[(size_t)p];
+    *out_perfect = (int64_t)h[(size_t)T];
+    if (E.prof) collect_profile(E);
+    return KS_OK;
 }
 
 extern "C" ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok) {

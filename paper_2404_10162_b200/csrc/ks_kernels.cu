@@ -581,6 +581,56 @@ bool launch_split_rows(const float* src, long long n, __half* hi, __half* lo, in
 }
 
 // ---------------------------------------------------------------------------
+// topk_eval: topk_metrics' per-sample scoring on the device (eval.cpp:117-134,
+// 142-146): the best-matching beam (most matching positions, ties to the
+// higher-ranked beam) adds its per-position hits; a sample counts as perfect
+// if any of its beams matches every position.  One thread per config; the
+// integer sums go through shared memory and one atomic per block and counter.
+// ---------------------------------------------------------------------------
+__global__ void topk_eval(const int* out_tok, const int* count, const int* truth, int B, int k, int T,
+                          unsigned long long* pos_matches, unsigned long long* perfect) {
+    __shared__ unsigned int s_pos[kMaxT];
+    __shared__ unsigned int s_perf;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) s_pos[i] = 0;
+    if (threadIdx.x == 0) s_perf = 0;
+    __syncthreads();
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) {
+        const int* tr = truth + (long long)b * T;
+        const int n = count[b];
+        int best = -1, best_m = -1;
+        bool perf = false;
+        for (int j = 0; j < n; ++j) {
+            const int* bt = out_tok + ((long long)b * k + j) * T;
+            int m = 0;
+            for (int p = 0; p < T; ++p) m += bt[p] == tr[p];
+            perf = perf || m == T;
+            if (m > best_m) {
+                best_m = m;
+                best = j;
+            }
+        }
+        if (best >= 0) {
+            const int* bt = out_tok + ((long long)b * k + best) * T;
+            for (int p = 0; p < T; ++p)
+                if (bt[p] == tr[p]) atomicAdd(&s_pos[p], 1u);
+        }
+        if (perf) atomicAdd(&s_perf, 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < T; i += blockDim.x)
+        if (s_pos[i]) atomicAdd(&pos_matches[i], (unsigned long long)s_pos[i]);
+    if (threadIdx.x == 0 && s_perf) atomicAdd(perfect, (unsigned long long)s_perf);
+}
+
+bool launch_topk_eval(const int* out_tok, const int* count, const int* truth, int B, int k, int T,
+                      unsigned long long* pos_matches, unsigned long long* perfect, cudaStream_t s) {
+    if (T > kMaxT) return false;
+    topk_eval<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(out_tok, count, truth, B, k, T, pos_matches, perfect);
+    return cudaGetLastError() == cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
 // beam_init: position 0 has one live hypothesis per config (decoding.cpp:41-43).
 // ---------------------------------------------------------------------------
 __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long long* key,

@@ -45,6 +45,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "ks_b200.h"
@@ -691,6 +692,23 @@ struct TLstm {
     long long size() const { return (long long)(Kd() + S + 1) * 4 * H; }
 };
 
+// cuBLASLt plan of one GEMM shape (descriptors + chosen algorithm)
+struct LtKey {
+    bool tb;
+    long long M, N, K, lda, ldb, ldc;
+    uint32_t aa, ab, ac;
+    bool operator<(const LtKey& o) const {
+        return std::tie(tb, M, N, K, lda, ldb, ldc, aa, ab, ac) <
+               std::tie(o.tb, o.M, o.N, o.K, o.lda, o.ldb, o.ldc, o.aa, o.ab, o.ac);
+    }
+};
+struct LtPlan {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+    bool usable = false;
+};
+
 struct RefSeg {
     std::string name;
     long long numel;
@@ -735,6 +753,7 @@ struct ks_trainer {
     DBuf sp[4];                    // split scratch: A big/small, B big/small
     DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
     cublasLtHandle_t lt = nullptr;
+    std::map<LtKey, LtPlan> lt_plans;
     std::map<const float*, std::pair<DBuf*, long long>> wsplit;  // per-call weight splits
     std::vector<std::unique_ptr<DBuf[]>> wsplit_store;  // pool, reused call after call
     size_t wsplit_used = 0;
@@ -776,61 +795,61 @@ ks_status gemm_one(ks_trainer& t, bool ta, bool tb, long long M, long long N, lo
 // Row-major C[M x N] = op(A) op(B) + beta C with A, B dense (A M x K, B as stored).
 ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long N, long long K, const float* A,
                   long long lda, const float* B, long long ldb, float beta, float* C, long long ldc) {
-    cublasLtMatmulDesc_t op = nullptr;
-    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-    cublasLtMatmulPreference_t pref = nullptr;
-    cublasStatus_t e = CUBLAS_STATUS_SUCCESS;
-    // column-major view: C^T (N x M) = op(B)^T (N x K) . A^T (K x M)
-    const cublasOperation_t tbo = tb ? CUBLAS_OP_T : CUBLAS_OP_N, tao = CUBLAS_OP_N;
-    const float one = 1.0f;
-    cublasLtMatmulHeuristicResult_t heur{};
-    int nres = 0;
-    bool fallback = false;
-    const size_t wsz = t.blas_ws.bytes;
-    if ((e = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F))) goto done;
-    if ((e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tbo, sizeof tbo))) goto done;
-    if ((e = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tao, sizeof tao))) goto done;
-    if ((e = cublasLtMatrixLayoutCreate(&la, CUDA_R_32F, tb ? K : N, tb ? N : K, ldb))) goto done;
-    if ((e = cublasLtMatrixLayoutCreate(&lb, CUDA_R_32F, K, M, lda))) goto done;
-    if ((e = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, N, M, ldc))) goto done;
-    if ((e = cublasLtMatmulPreferenceCreate(&pref))) goto done;
-    if ((e = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz)))
-        goto done;
-    {
-        // the output may start anywhere in the flat gradient buffer: tell the heuristic
-        auto align = [](const void* ptr) {
-            uint32_t a = 256;
-            while (a > 4 && (reinterpret_cast<uintptr_t>(ptr) % a) != 0) a >>= 1;
-            return a;
-        };
-        const uint32_t aa = align(B), ab = align(A), ac = align(C);
-        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_A_BYTES, &aa, sizeof aa);
-        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_B_BYTES, &ab, sizeof ab);
-        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_C_BYTES, &ac, sizeof ac);
-        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &ac, sizeof ac);
+    auto align = [](const void* ptr) {
+        uint32_t a = 256;
+        while (a > 4 && (reinterpret_cast<uintptr_t>(ptr) % a) != 0) a >>= 1;
+        return a;
+    };
+    const uint32_t aa = align(B), ab = align(A), ac = align(C);
+    const LtKey key{tb, M, N, K, lda, ldb, ldc, aa, ab, ac};
+    auto it = t.lt_plans.find(key);
+    if (it == t.lt_plans.end()) {
+        // one plan per shape: descriptors + the heuristic's algorithm, built once
+        // (the heuristic query costs tens of microseconds of host time per call)
+        LtPlan pl;
+        cublasLtMatmulPreference_t pref = nullptr;
+        // column-major view: C^T (N x M) = op(B)^T (N x K) . A^T (K x M)
+        const cublasOperation_t tbo = tb ? CUBLAS_OP_T : CUBLAS_OP_N, tao = CUBLAS_OP_N;
+        const size_t wsz = t.blas_ws.bytes;
+        cublasLtMatmulHeuristicResult_t heur{};
+        int nres = 0;
+        bool ok = cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS &&
+                  cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &tbo, sizeof tbo) == CUBLAS_STATUS_SUCCESS &&
+                  cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tao, sizeof tao) == CUBLAS_STATUS_SUCCESS &&
+                  cublasLtMatrixLayoutCreate(&pl.la, CUDA_R_32F, tb ? K : N, tb ? N : K, ldb) == CUBLAS_STATUS_SUCCESS &&
+                  cublasLtMatrixLayoutCreate(&pl.lb, CUDA_R_32F, K, M, lda) == CUBLAS_STATUS_SUCCESS &&
+                  cublasLtMatrixLayoutCreate(&pl.lc, CUDA_R_32F, N, M, ldc) == CUBLAS_STATUS_SUCCESS &&
+                  cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS &&
+                  cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz) ==
+                      CUBLAS_STATUS_SUCCESS;
+        if (ok) {
+            // the output may start anywhere in the flat gradient buffer: tell the heuristic
+            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_A_BYTES, &aa, sizeof aa);
+            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_B_BYTES, &ab, sizeof ab);
+            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_C_BYTES, &ac, sizeof ac);
+            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &ac, sizeof ac);
+            ok = cublasLtMatmulAlgoGetHeuristic(t.lt, pl.op, pl.la, pl.lb, pl.lc, pl.lc, pref, 1, &heur, &nres) ==
+                     CUBLAS_STATUS_SUCCESS &&
+                 nres >= 1 && heur.state == CUBLAS_STATUS_SUCCESS;
+        }
+        if (pref) cublasLtMatmulPreferenceDestroy(pref);
+        pl.usable = ok;  // no cuBLASLt algorithm for this shape: cublasGemmEx below
+        if (ok) pl.algo = heur.algo;
+        it = t.lt_plans.emplace(key, pl).first;
     }
-    if (cublasLtMatmulAlgoGetHeuristic(t.lt, op, la, lb, lc, lc, pref, 1, &heur, &nres) != CUBLAS_STATUS_SUCCESS ||
-        nres < 1 || heur.state != CUBLAS_STATUS_SUCCESS) {
-        fallback = true;  // no cuBLASLt algorithm for this shape: cublasGemmEx below
-        goto done;
+    const LtPlan& pl = it->second;
+    if (pl.usable) {
+        const float one = 1.0f;
+        const cublasStatus_t e = cublasLtMatmul(t.lt, pl.op, &one, B, pl.la, A, pl.lb, &beta, C, pl.lc, C, pl.lc,
+                                                &pl.algo, t.blas_ws.p, t.blas_ws.bytes, s);
+        if (e == CUBLAS_STATUS_SUCCESS) {
+            ++t.launches;
+            return KS_OK;
+        }
+        if (e != CUBLAS_STATUS_NOT_SUPPORTED)
+            return set_error(KS_ERR_CUDA, "cuBLASLt TF32 GEMM status " + std::to_string((int)e));
     }
-    e = cublasLtMatmul(t.lt, op, &one, B, la, A, lb, &beta, C, lc, C, lc, &heur.algo, t.blas_ws.p, wsz, s);
-    if (e == CUBLAS_STATUS_NOT_SUPPORTED) {
-        e = CUBLAS_STATUS_SUCCESS;
-        fallback = true;
-    } else {
-        ++t.launches;
-    }
-done:
-    if (pref) cublasLtMatmulPreferenceDestroy(pref);
-    if (lc) cublasLtMatrixLayoutDestroy(lc);
-    if (lb) cublasLtMatrixLayoutDestroy(lb);
-    if (la) cublasLtMatrixLayoutDestroy(la);
-    if (op) cublasLtMatmulDescDestroy(op);
-    if (e != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cuBLASLt TF32 GEMM status " + std::to_string((int)e));
-    if (fallback)
-        return gemm_one(t, false, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_FAST_TF32);
-    return KS_OK;
+    return gemm_one(t, false, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_FAST_TF32);
 }
 
 // Splits a stored (rows x cols, ld) operand into dense big/small planes.
@@ -1546,6 +1565,12 @@ extern "C" void ks_trainer_destroy(ks_trainer* t) {
     if (!t) return;
     cudaSetDevice(t->device);
     if (t->blas) cublasDestroy(t->blas);
+    for (auto& kv : t->lt_plans) {
+        if (kv.second.lc) cublasLtMatrixLayoutDestroy(kv.second.lc);
+        if (kv.second.lb) cublasLtMatrixLayoutDestroy(kv.second.lb);
+        if (kv.second.la) cublasLtMatrixLayoutDestroy(kv.second.la);
+        if (kv.second.op) cublasLtMatmulDescDestroy(kv.second.op);
+    }
     if (t->lt) cublasLtDestroy(t->lt);
     delete t;
 }

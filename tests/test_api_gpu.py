@@ -162,3 +162,45 @@ def test_engine_precision_switch(ks, oracle):
     ref = ks.predict(p, d, beam_width=5)
     p.set_engine(0, "fp32")
     assert [e["params"] for e in ks.predict(p, d, beam_width=5)] == [e["params"] for e in ref]
+
+
+def test_topk_metrics_device_scoring_with_hits_and_exhaustion(ks, params, oracle):
+    """Device-side best-match / any-of-k scoring (ks_topk_metrics_batch) with
+    truths that are hit (the oracle's own 2nd beam) and a tight budget that
+    exhausts some configs (scored as no hits, eval.cpp:114-116)."""
+    ds = descs(oracle, 120, 11)
+    tok = np.concatenate([tok_of(oracle, d) for d in ds])
+    budget = 26.0
+    pred_o = [oracle.membership(), oracle.budget({n: 1.0 for n in oracle.names}, budget)]
+    a = oracle.beam(tok, 3, None, pred_o, threads=4)
+    if (a["min_gap"] < 1e-4).any():
+        pytest.skip("tie-adjacent configs in this sample")
+    rng = np.random.default_rng(3)
+    samples, truths = [], []
+    for b, d in enumerate(ds):
+        if a["count"][b] >= 2 and b % 2 == 0:
+            truth = [int(x) for x in a["tokens"][b, 1]]
+        else:
+            truth = [int(rng.integers(len(v))) for v in oracle.values]
+        truths.append(truth)
+        samples.append(ks.Sample(d, {n: oracle.values[i][t] for i, (n, t) in enumerate(zip(oracle.names, truth))},
+                                 "ConvAsm1x1U"))
+    preds = [ks.membership_predicate(params.spec),
+             ks.resource_budget_predicate({n: 1.0 for n in oracle.names}, budget)]
+    rep = ks.topk_metrics(params, samples, [3], predicates=preds)[0]
+    T = oracle.T
+    per, perfect = np.zeros(T), 0
+    for b in range(len(ds)):
+        best, bm, hit = None, -1, False
+        for j in range(a["count"][b]):
+            m = sum(int(a["tokens"][b, j, p] == truths[b][p]) for p in range(T))
+            hit |= m == T
+            if m > bm:
+                bm, best = m, a["tokens"][b, j]
+        if best is not None:
+            per += np.array([best[p] == truths[b][p] for p in range(T)])
+        perfect += hit
+    assert perfect > 0
+    assert math.isclose(rep["average_accuracy"], float(np.mean(per / len(ds) * 100)), rel_tol=1e-9)
+    assert math.isclose(rep["perfect_prediction"], 100.0 * perfect / len(ds), rel_tol=1e-9)
+    assert rep["constrained"]
