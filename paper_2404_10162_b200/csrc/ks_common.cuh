@@ -201,6 +201,16 @@ struct ConvArgs {
     int scratch_floats;  // per warp
 };
 
+// hybrid (layered) bi-LSTM 2 operands from bi-LSTM 1's sequence
+struct HybPackArgs {
+    const float* H1;   // [T][C][2CP]
+    int C, T, CP;
+    int split_mode;
+    __half* Xhi[2];    // per direction [T][C][3CP]
+    __half* Xlo[2];
+    float* Xf[2];
+};
+
 // fp16 hi/lo split of an fp32 value, pre-scaled by 2^8 (exact) so that the
 // residual of values down to ~5e-4 stays in the normal fp16 range:
 //   x * 2^8 ~= hi + lo   (22 significant bits)

@@ -34,6 +34,7 @@ __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long 
 size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tables);
 bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s);
 bool launch_hybrid_conv(const ConvArgs& p, cudaStream_t s);
+bool launch_hybrid_pack(const HybPackArgs& p, cudaStream_t s);
 bool launch_topk_eval(const int* out_tok, const int* count, const int* truth, int B, int k, int T,
                       unsigned long long* pos_matches, unsigned long long* perfect, cudaStream_t s);
 bool launch_split_rows(const float* src, long long n, __half* hi, __half* lo, int mode, cudaStream_t s);
@@ -170,6 +171,8 @@ struct ks_engine {
     int conv_scratch = 0;
     DevLstm hb1[2], hb2[2];
     DevMem hybA, hybAf, hybC, hybH, feat;
+    bool layered = false;         // hybrid: bi-LSTM 2 runs over bi-LSTM 1's sequence (not seeded)
+    DevMem hybH1, hybX2;          // layered: H1 [T][C][2CP] fp32; bi-LSTM 2 operands per dir and step
     int num_sms = 148;
     // projected context (attn / attn-2, tensor-core modes): ctx . W_ctx =
     // sum_t alpha_t (a_t . W_ctx).  P = a_t . W_ctx is computed once per config
@@ -296,9 +299,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
     if (!d || !out) return set_error(KS_ERR_PARAMETER, "null argument");
     if (precision < 0 || precision > 2) return set_error(KS_ERR_PARAMETER, "unknown precision mode");
     if (d->variant != KS_VARIANT_ATTN && d->variant != KS_VARIANT_ATTN2 &&
-        d->variant != KS_VARIANT_ENC_DEC && d->variant != KS_VARIANT_HYBRID2)
-        return set_error(KS_ERR_UNSUPPORTED,
-                         "the B200 engine implements the enc-dec, attn, attn-2 and hybrid-2 variants");
+        d->variant != KS_VARIANT_ENC_DEC && d->variant != KS_VARIANT_HYBRID2 && d->variant != KS_VARIANT_HYBRID)
+        return set_error(KS_ERR_UNSUPPORTED, "unknown model variant");
     if (d->num_positions < 1 || d->num_positions > kMaxT)
         return set_error(KS_ERR_UNSUPPORTED, "number of output positions must be in [1, 16]");
     if (d->attention_dense_nodes < 1 || d->attention_dense_nodes > kMaxNd)
@@ -415,10 +417,12 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         if ((st = upload(E.attWo, wo, (size_t)E.n_d * 4))) return st;
         E.attBo = bo[0];
     }
-    if (E.variant == KS_VARIANT_HYBRID2) {
-        // conv stack over the (d_in x 7) one-hot matrix, then two seeded bi-LSTMs
+    if (E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID) {
+        // conv stack over the (d_in x 7) one-hot matrix, then two bi-LSTMs (hybrid-2:
+        // the second seeded with the first's final states; hybrid: over its sequence)
+        E.layered = E.variant == KS_VARIANT_HYBRID;
         if (d->num_conv_layers < 1 || d->num_conv_layers > 8 || !d->conv_layers)
-            return set_error(KS_ERR_UNSUPPORTED, "hybrid-2 needs 1..8 conv layers");
+            return set_error(KS_ERR_UNSUPPORTED, "hybrid variants need 1..8 conv layers");
         int ch = E.d_in, len = 7, scratch = 0;
         for (int i = 0; i < d->num_conv_layers; ++i) {
             const int f = d->conv_layers[3 * i], kk = d->conv_layers[3 * i + 1], sd = d->conv_layers[3 * i + 2];
@@ -449,14 +453,21 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         for (int kh = 0; kh < E.CP; ++kh) dense.push_back(kh < E.cell ? E.F + kh : -1);
         static const char* names[4] = {"bilstm1.fwd", "bilstm1.bwd", "bilstm2.fwd", "bilstm2.bwd"};
         DevLstm* dst[4] = {&E.hb1[0], &E.hb1[1], &E.hb2[0], &E.hb2[1]};
-        for (int q = 0; q < 4; ++q)
-            if ((st = pack_lstm(ht, names[q], E.F + E.cell, E.cell, E.CP, dense, slots, *dst[q], E.precision,
-                                E.tc_units)))
+        // layered bi-LSTM 2 input = [fwd h1_t | bwd h1_t] (2 cell rows), device K layout
+        // [fwd (CP) | bwd (CP) | h (CP)]
+        std::vector<int> dense2;
+        for (int k2 = 0; k2 < 3 * E.CP; ++k2) {
+            const int part = k2 / E.CP, i = k2 % E.CP;
+            dense2.push_back(i < E.cell ? part * E.cell + i : -1);
+        }
+        for (int q = 0; q < 4; ++q) {
+            const bool two = E.layered && q >= 2;
+            if ((st = pack_lstm(ht, names[q], two ? 3 * E.cell : E.F + E.cell, E.cell, E.CP, two ? dense2 : dense,
+                                slots, *dst[q], E.precision, E.tc_units)))
                 return st;
-    } else if (E.variant == KS_VARIANT_HYBRID) {
-        return set_error(KS_ERR_UNSUPPORTED, "hybrid (non-seeded) is not implemented on the B200 engine");
+        }
     }
-    const bool hyb = E.variant == KS_VARIANT_HYBRID2;
+    const bool hyb = E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID;
     const int Hd = hyb ? 2 * E.cell : (E.variant == KS_VARIANT_ENC_DEC ? E.e : E.n_s);
     const int HdP = hyb ? 2 * E.CP : (E.variant == KS_VARIANT_ENC_DEC ? E.NE : E.NS);
     for (int p = 0; p < E.T; ++p) {
@@ -662,8 +673,13 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
 #define ENS(buf, n) do { if ((e = (buf).ensure((size_t)(n))) != cudaSuccess) goto fail; } while (0)
     ENS(E.tok, C * 7 * 4);
     ENS(E.desc, C * 7 * 8);
-    if (E.variant == KS_VARIANT_HYBRID2) {
+    if (E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID) {
         const int64_t K = E.FP + E.CP;
+        if (E.layered) {
+            const int64_t K2 = 3LL * E.CP;
+            ENS(E.hybH1, (int64_t)E.T * C * 2 * E.CP * 4);
+            ENS(E.hybX2, E.precision == KS_PREC_FP32 ? 2LL * E.T * C * K2 * 4 : 2LL * 2 * E.T * C * K2 * 2);
+        }
         if (E.precision == KS_PREC_FP32) {
             ENS(E.hybAf, 4 * C * K * 4);            // [dir*2 + pingpong][C][K] fp32
         } else {
@@ -760,9 +776,11 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
     return KS_OK;
 }
 
-// hybrid-2 encoder: conv stack, bi-LSTM 1 over T_out copies of the encoding
-// (final states only), bi-LSTM 2 seeded with them; writes the per-position
-// features [fwd h_t | bwd h_t] (models.cpp:296-371, 422-425).
+// hybrid encoders: conv stack, bi-LSTM 1 over T_out copies of the encoding;
+// hybrid-2: bi-LSTM 2 over the same copies seeded with bi-LSTM 1's final
+// states (models.cpp:296-371, 422-425); hybrid: bi-LSTM 2 over bi-LSTM 1's
+// activation sequence from a zero state (models.cpp:409-418).  Writes the
+// per-position features [fwd h_t | bwd h_t].
 ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
     cudaStream_t s = E.stream;
     const int T = E.T, CP = E.CP, FP = E.FP;
@@ -800,9 +818,30 @@ ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
     if (!launch_hybrid_conv(ca, s)) return set_error(KS_ERR_UNSUPPORTED, "conv stack too large for the conv kernel");
     E.launches++;
     ks_status st;
+    // layered (hybrid): bi-LSTM 2 operands [fwd h1_t | bwd h1_t | h2] per direction and step
+    const int64_t K2 = 3LL * CP;
+    auto X2hi = [&](int dir, int t) { return E.hybX2.as<__half>() + ((size_t)(dir * T + t)) * C * K2; };
+    auto X2lo = [&](int dir, int t) { return E.hybX2.as<__half>() + ((size_t)((2 + dir) * T + t)) * C * K2; };
+    auto X2f = [&](int dir, int t) { return E.hybX2.as<float>() + ((size_t)(dir * T + t)) * C * K2; };
+    float* H1 = E.layered ? E.hybH1.as<float>() : nullptr;
     for (int step = 0; step < 2 * T; ++step) {
         const bool second = step >= T;
         const int cur = step & 1, nxt = cur ^ 1;
+        if (E.layered && step == T) {
+            HybPackArgs hp{};
+            hp.H1 = H1;
+            hp.C = (int)C;
+            hp.T = T;
+            hp.CP = CP;
+            hp.split_mode = ca.split_mode;
+            for (int dir = 0; dir < 2; ++dir) {
+                hp.Xhi[dir] = split ? X2hi(dir, 0) : nullptr;
+                hp.Xlo[dir] = split ? X2lo(dir, 0) : nullptr;
+                hp.Xf[dir] = split ? nullptr : X2f(dir, 0);
+            }
+            if (!launch_hybrid_pack(hp, s)) return set_error(KS_ERR_CUDA, "hybrid pack launch failed");
+            E.launches++;
+        }
         LstmArgs a[2];
         for (int dir = 0; dir < 2; ++dir) {
             LstmArgs& p = a[dir];
@@ -814,12 +853,20 @@ ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
             p.lda = K;
             p.A_hi = split ? Ahi(dir, cur) : nullptr;
             p.A_lo = split ? Alo(dir, cur) : nullptr;
+            const int t = second ? (dir == 0 ? step - T : T - 1 - (step - T)) : (dir == 0 ? step : T - 1 - step);
+            if (E.layered && second) {
+                p.K = (int)K2;
+                p.lda = K2;
+                p.A = split ? nullptr : X2f(dir, t);
+                p.A_hi = split ? X2hi(dir, t) : nullptr;
+                p.A_lo = split ? X2lo(dir, t) : nullptr;
+            }
             DevLstm& L = second ? E.hb2[dir] : E.hb1[dir];
             p.W = L.W.as<float>();
             p.G = L.G.as<float>();
             p.slot_ptr = nullptr;
             p.slot_base = 0;
-            p.c_prev = step == 0 ? nullptr : Cb(dir, nxt);
+            p.c_prev = (step == 0 || (E.layered && step == T)) ? nullptr : Cb(dir, nxt);
             p.ldc_prev = CP;
             p.c_out = Cb(dir, cur);
             p.ldc = CP;
@@ -831,21 +878,36 @@ ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
                 p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
             }
             float* next_f32 = split ? nullptr : Af(dir, nxt) + FP;
+            if (E.layered && second) {
+                // the next step of this direction reads h from its own operand buffer
+                const int tn = dir == 0 ? t + 1 : t - 1;
+                const bool more = tn >= 0 && tn < T;
+                p.hA_hi = (split && more) ? X2hi(dir, tn) + 2 * CP : nullptr;
+                p.hA_lo = (split && more) ? X2lo(dir, tn) + 2 * CP : nullptr;
+                p.ldha = K2;
+                next_f32 = (!split && more) ? X2f(dir, tn) + 2 * CP : nullptr;
+            }
             if (!second) {
-                p.h_out = split ? E.hybH.as<float>() + (size_t)dir * C * CP : next_f32;
-                p.ldh = split ? CP : K;
+                if (E.layered) {  // bi-LSTM 1's sequence feeds bi-LSTM 2
+                    p.h_out = H1 + (size_t)t * C * 2 * CP + (size_t)dir * CP;
+                    p.ldh = 2 * CP;
+                    p.h_out2 = next_f32;
+                    p.ldh2 = K;
+                } else {
+                    p.h_out = split ? E.hybH.as<float>() + (size_t)dir * C * CP : next_f32;
+                    p.ldh = split ? CP : K;
+                }
             } else {
-                const int t = dir == 0 ? step - T : T - 1 - (step - T);
                 p.h_out = E.feat.as<float>() + (size_t)t * C * 2 * CP + (size_t)dir * CP;
                 p.ldh = 2 * CP;
                 p.h_out2 = next_f32;
-                p.ldh2 = K;
+                p.ldh2 = E.layered ? K2 : K;
             }
         }
         if (step == 0 && !split) {
             // FP32 mode: the step-0 operand's h part is zero (written by the conv kernel)
         }
-        const double fl = 2.0 * 2.0 * (double)C * (E.F + E.cell) * 4.0 * E.cell;
+        const double fl = 2.0 * 2.0 * (double)C * ((E.layered && second) ? 3 * E.cell : E.F + E.cell) * 4.0 * E.cell;
         if ((st = launch_lstm(E, a[0], &a[1], second ? E.hb2[0] : E.hb1[0], second ? &E.hb2[1] : &E.hb1[1], fl)))
             return st;
     }
@@ -872,7 +934,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     auto encc_at = [&](int dir, int pp) { return encc + ((size_t)dir * 2 + pp) * C * He; };
     auto encA_at = [&](int dir, int pp, int lo) { return encA + (((size_t)dir * 2 + pp) * 2 + lo) * C * He; };
 
-    const bool hybrid = E.variant == KS_VARIANT_HYBRID2;
+    const bool hybrid = E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID;
     if (hybrid && (st = encode_hybrid(E, C, d_tok))) return st;
     // ---- encoder (bi-LSTM over the 7 one-hot input steps, zero initial state)
     const int dirs = enc_dec ? 1 : 2;

@@ -1123,6 +1123,40 @@ __global__ void __launch_bounds__(128) hybrid_conv(ConvArgs p) {
     }
 }
 
+// hybrid: bi-LSTM 2 operand of step t = [fwd h1_t | bwd h1_t | h2]; the h2
+// part of each direction's first step is the zero initial state, the others
+// are written by bi-LSTM 2's own epilogue.
+__global__ void hybrid_pack(HybPackArgs p) {
+    const long long K2 = 3LL * p.CP;
+    const long long n = (long long)p.T * p.C * K2;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / K2;
+        const int col = (int)(i - row * K2);
+        const int t = (int)(row / p.C);
+        const bool hpart = col >= 2 * p.CP;
+        const float v = hpart ? 0.0f : p.H1[row * 2 * p.CP + col];
+        for (int dir = 0; dir < 2; ++dir) {
+            if (hpart && t != (dir == 0 ? 0 : p.T - 1)) continue;
+            if (p.split_mode == 0) {
+                p.Xf[dir][i] = v;
+            } else if (p.split_mode == 1) {
+                __half hi, lo;
+                split_f16(v, hi, lo);
+                p.Xhi[dir][i] = hi;
+                p.Xlo[dir][i] = lo;
+            } else {
+                reinterpret_cast<__nv_bfloat16*>(p.Xhi[dir])[i] = __float2bfloat16_rn(v);
+            }
+        }
+    }
+}
+
+bool launch_hybrid_pack(const HybPackArgs& p, cudaStream_t s) {
+    const long long n = (long long)p.T * p.C * 3 * p.CP;
+    hybrid_pack<<<(unsigned)std::min<long long>((n + 255) / 256, 148LL * 64), 256, 0, s>>>(p);
+    return cudaGetLastError() == cudaSuccess;
+}
+
 bool launch_hybrid_conv(const ConvArgs& p, cudaStream_t s) {
     const size_t smem = (size_t)4 * 2 * p.scratch_floats * sizeof(float);
     if (smem > 200 * 1024) return false;

@@ -52,8 +52,8 @@ def random_desc(o, tok):
     return np.array([[o.input_values[f][t] for f, t in enumerate(row)] for row in tok], np.int64)
 
 
-# the non-seeded `hybrid` variant is oracle-only; every other variant runs on the GPU
-GPU_TINY = [m[0] for m in TINY_MODELS if m[1] != "hybrid"]
+# every reference variant (enc-dec, attn, attn-2, hybrid, hybrid-2) runs on the GPU
+GPU_TINY = [m[0] for m in TINY_MODELS]
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
@@ -110,10 +110,19 @@ def test_small_trained_hybrid2(precision):
     assert (g1[keep] == o.greedy(tok)[keep]).all()
 
 
-def test_hybrid_variant_is_rejected_cleanly():
-    from paper_2404_10162_b200._cabi import KsError
-    with pytest.raises(KsError, match="hybrid"):
-        engine(golden_path("tiny_hybrid_s3423.ckpt"), "f16x3")
+@pytest.mark.parametrize("precision", PRECISIONS + ["bf16"])
+def test_hybrid_layered_variant_runs(precision):
+    """hybrid: bi-LSTM 2 over bi-LSTM 1's activation sequence (models.cpp:409-418);
+    bf16 only has to run (reduced precision)."""
+    path = golden_path("tiny_hybrid_s3423.ckpt")
+    o, e = OracleModel(path), engine(path, precision)
+    tok = random_tokens(o, 256, 13)
+    a, g = o.beam(tok, 4), e.beam(tok, 4)
+    if precision == "bf16":
+        assert (g["count"] == a["count"]).all()
+        return
+    n, ties, bad = compare_beams(g, a)
+    assert not bad, f"{len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
