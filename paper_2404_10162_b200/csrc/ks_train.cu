@@ -63,59 +63,86 @@ constexpr int kMaxT = 16;
 // device kernels
 // ---------------------------------------------------------------------------
 
-// mt19937_64 ([rand.eng.mers]) + Rng::derive / uniform (rng.hpp:13-71).
-struct Mt64 {
-    unsigned long long mt[312];
-    int idx;
-};
+// Rng::derive's seed mixing (rng.hpp:19-21, 64-68).
 __device__ __forceinline__ unsigned long long rng_mix(unsigned long long z) {
     z += 0x9e3779b97f4a7c15ULL;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
     return z ^ (z >> 31);
 }
-__device__ void mt_seed(Mt64& g, unsigned long long s) {
-    g.mt[0] = s;
-    for (int i = 1; i < 312; ++i) g.mt[i] = 6364136223846793005ULL * (g.mt[i - 1] ^ (g.mt[i - 1] >> 62)) + i;
-    g.idx = 312;
+// One warp per sample: input mask (n_in) then recurrent mask (n_rec), as
+// LstmMasks::make -> nn::dropout_mask draw them (nn.cpp:237-248).  The
+// mt19937_64 state lives in shared memory; seeding is serial (lane 0), the
+// twist runs in three dependency-respecting parallel phases (i < 156 reads only
+// old words; 156 <= i < 311 reads old mt[i + 1] and the phase-1 results; i = 311
+// reads the new mt[0]), and the 312 tempered outputs of a block go one per lane.
+__device__ __forceinline__ unsigned long long mt_twist_one(const unsigned long long* mt, int i) {
+    const unsigned long long x = (mt[i] & 0xFFFFFFFF80000000ULL) | (mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+    unsigned long long xa = x >> 1;
+    if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+    return mt[(i + 156) % 312] ^ xa;
 }
-__device__ unsigned long long mt_next(Mt64& g) {
-    if (g.idx >= 312) {
-        for (int i = 0; i < 312; ++i) {
-            const unsigned long long x = (g.mt[i] & 0xFFFFFFFF80000000ULL) | (g.mt[(i + 1) % 312] & 0x7FFFFFFFULL);
-            unsigned long long xa = x >> 1;
-            if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
-            g.mt[i] = g.mt[(i + 156) % 312] ^ xa;
-        }
-        g.idx = 0;
-    }
-    unsigned long long y = g.mt[g.idx++];
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
     y ^= (y >> 29) & 0x5555555555555555ULL;
     y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
     y ^= (y << 37) & 0xFFF7EEE000000000ULL;
-    y ^= y >> 43;
-    return y;
+    return y ^ (y >> 43);
 }
 
-// One thread per sample: input mask (n_in) then recurrent mask (n_rec), as
-// LstmMasks::make -> nn::dropout_mask draw them (nn.cpp:237-248).
 __global__ void k_dropout_masks(int M, unsigned long long seed, long long epoch, const long long* idx,
                                 long long idx_base, int n_in, double rate_in, int n_rec, double rate_rec,
                                 float* mi, float* mr) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ unsigned long long st[8][312];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + w;
     if (b >= M) return;
-    Mt64 g;
-    const unsigned long long id = idx ? (unsigned long long)idx[b] : (unsigned long long)(idx_base + b);
-    const unsigned long long stream = ((unsigned long long)epoch << 32) | id;
-    mt_seed(g, rng_mix(rng_mix(seed) + 0x9e3779b97f4a7c15ULL * (stream + 1)));
-    const float ki = (float)(1.0 / (1.0 - rate_in)), kr = (float)(1.0 / (1.0 - rate_rec));
-    for (int i = 0; i < n_in; ++i) {
-        const double u = (double)(mt_next(g) >> 11) * 0x1.0p-53;
-        mi[(long long)b * n_in + i] = u < rate_in ? 0.0f : ki;
+    unsigned long long* mt = st[w];
+    if (lane == 0) {
+        const unsigned long long id = idx ? (unsigned long long)idx[b] : (unsigned long long)(idx_base + b);
+        const unsigned long long stream = ((unsigned long long)epoch << 32) | id;
+        mt[0] = rng_mix(rng_mix(seed) + 0x9e3779b97f4a7c15ULL * (stream + 1));
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
     }
-    for (int i = 0; i < n_rec; ++i) {
-        const double u = (double)(mt_next(g) >> 11) * 0x1.0p-53;
-        mr[(long long)b * n_rec + i] = u < rate_rec ? 0.0f : kr;
+    __syncwarp();
+    const float ki = (float)(1.0 / (1.0 - rate_in)), kr = (float)(1.0 / (1.0 - rate_rec));
+    const int n = n_in + n_rec;
+    for (int base = 0; base < n; base += 312) {
+        unsigned long long v[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = lane + 32 * q;
+            if (i < 156) v[q] = mt_twist_one(mt, i);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = lane + 32 * q;
+            if (i < 156) mt[i] = v[q];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = 156 + lane + 32 * q;
+            if (i < 311) v[q] = mt_twist_one(mt, i);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = 156 + lane + 32 * q;
+            if (i < 311) mt[i] = v[q];
+        }
+        __syncwarp();
+        if (lane == 0) mt[311] = mt_twist_one(mt, 311);
+        __syncwarp();
+        for (int e = lane; e < 312 && base + e < n; e += 32) {
+            const int g = base + e;
+            const double u = (double)(mt_temper(mt[e]) >> 11) * 0x1.0p-53;
+            if (g < n_in)
+                mi[(long long)b * n_in + g] = u < rate_in ? 0.0f : ki;
+            else
+                mr[(long long)b * n_rec + (g - n_in)] = u < rate_rec ? 0.0f : kr;
+        }
+        __syncwarp();
     }
 }
 
@@ -331,8 +358,9 @@ __global__ void k_attn_fwd(AttnFwd a) {
 
 // Attention backward, one warp per row.  Input dX = [dctx | dh_rec] (the dX
 // GEMM of the post LSTM); produces dH = dh_rec * mr + ds (ds through s.Ws),
-// accumulates dA, the per-row sums for attn.out, and the dpre terms reduced
-// later by GEMMs (DPs for Ws, DPa for Wa, bh).
+// keeps this position's (masked) dctx for k_attn_dA, accumulates the per-row
+// sums for attn.out and the dpre terms reduced later by GEMMs (DPs for Ws,
+// DPa for Wa and bh).
 struct AttnBwd {
     int M, na2, ns, nd;
     const float* dX;     // [M][ldx]
@@ -346,7 +374,7 @@ struct AttnBwd {
     const float* Ws;     // [ns][nd]
     const float* Wa;     // [na2][nd]
     const float* wo;     // [nd]
-    float* dA;           // [M][7][na2] (+=)
+    float* dctx_out;     // [M][na2] (=) this position's masked dctx
     float* dH;           // [M][ns] (=)
     float* DPs;          // [M][nd] (=) this position
     float* DPa;          // [M][7][nd] (+=)
@@ -404,19 +432,7 @@ __global__ void k_attn_bwd(AttnBwd a) {
             #pragma unroll
             for (int d = 0; d < ND; ++d) a.DPa[(r * kTin + t) * ND + d] += dpre[t][d];
     }
-    float* dAr = a.dA + r * kTin * a.na2;
-    for (int j = lane; j < a.na2; j += 32) {
-        const float dc = mi ? dX[j] * mi[j] : dX[j];
-        float wa[ND];
-        #pragma unroll
-        for (int d = 0; d < ND; ++d) wa[d] = a.Wa[(long long)j * ND + d];
-        for (int t = 0; t < kTin; ++t) {
-            float v = al[t] * dc;
-            #pragma unroll
-            for (int d = 0; d < ND; ++d) v += dpre[t][d] * wa[d];
-            dAr[t * a.na2 + j] += v;
-        }
-    }
+    for (int j = lane; j < a.na2; j += 32) a.dctx_out[r * a.na2 + j] = mi ? dX[j] * mi[j] : dX[j];
     const float* mr = a.mr ? a.mr + r * a.ns : nullptr;
     for (int j = lane; j < a.ns; j += 32) {
         float v = dX[a.na2 + j];
@@ -424,6 +440,50 @@ __global__ void k_attn_bwd(AttnBwd a) {
         #pragma unroll
         for (int d = 0; d < ND; ++d) v += dps[d] * a.Ws[(long long)j * ND + d];
         a.dH[r * a.ns + j] = v;
+    }
+}
+
+// dA[r][t] = sum_p alpha_p[r][t] dctx_p[r] + (sum_p dpre_p[r][t]) . Wa^T: the
+// encoder activations' gradient from every decoder position at once (one pass
+// instead of a read-modify-write of dA per position).  One warp per row.
+struct AttnDA {
+    int M, T, na2;
+    const float* alpha;  // [T][M][7]
+    const float* dctx;   // [T][M][na2]
+    const float* DPa;    // [M][7][nd]
+    const float* Wa;     // [na2][nd]
+    float* dA;           // [M][7][na2]
+};
+
+template <int ND>
+__global__ void k_attn_dA(AttnDA a) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= a.M) return;
+    const long long r = warp, M = a.M;
+    float dpa[kTin][ND];
+    for (int t = 0; t < kTin; ++t)
+#pragma unroll
+        for (int d = 0; d < ND; ++d) dpa[t][d] = a.DPa[(r * kTin + t) * ND + d];
+    for (int j = lane; j < a.na2; j += 32) {
+        float acc[kTin];
+        float wa[ND];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) wa[d] = a.Wa[(long long)j * ND + d];
+#pragma unroll
+        for (int t = 0; t < kTin; ++t) {
+            float v = 0.0f;
+#pragma unroll
+            for (int d = 0; d < ND; ++d) v += dpa[t][d] * wa[d];
+            acc[t] = v;
+        }
+        for (int p = 0; p < a.T; ++p) {
+            const float dc = a.dctx[((long long)p * M + r) * a.na2 + j];
+            const float* al = a.alpha + ((long long)p * M + r) * kTin;
+#pragma unroll
+            for (int t = 0; t < kTin; ++t) acc[t] += al[t] * dc;
+        }
+#pragma unroll
+        for (int t = 0; t < kTin; ++t) a.dA[(r * kTin + t) * a.na2 + j] = acc[t];
     }
 }
 
@@ -445,6 +505,7 @@ __global__ void k_attn_bwd(AttnBwd a) {
     }
 KST_ND_DISPATCH(k_attn_fwd, AttnFwd)
 KST_ND_DISPATCH(k_attn_bwd, AttnBwd)
+KST_ND_DISPATCH(k_attn_dA, AttnDA)
 
 // Head + cross entropy (dense_forward, cross_entropy_logits, sum_scaled 1/T;
 // models.cpp:764-777), one warp per row: per-row loss (double), argmax match,
@@ -467,41 +528,49 @@ __global__ void k_head(HeadArgs a) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* Wsm = sh;                          // ns * V
     float* hrow = sh + a.ns * a.V + w * (a.ns + 32);
+    float* dsm = hrow + a.ns;                 // this warp's dlogits (32)
     for (int i = threadIdx.x; i < a.ns * a.V; i += blockDim.x) Wsm[i] = a.W[i];
     __syncthreads();
-    const long long r = (long long)blockIdx.x * warps + w;
-    if (r >= a.M) return;
-    for (int j = lane; j < a.ns; j += 32) hrow[j] = a.h[r * a.ns + j];
-    __syncwarp();
-    float lg = 0.0f;  // lane v holds logit v
-    for (int v = 0; v < a.V; ++v) {
-        float part = 0.0f;
-        for (int j = lane; j < a.ns; j += 32) part += hrow[j] * Wsm[j * a.V + v];
-        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == v) lg = part + a.b[v];
-    }
-    const bool act = lane < a.V;
-    float mx = act ? lg : -INFINITY;
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    // argmax, lowest index on ties
-    int am = (act && lg == mx) ? lane : 64;
-    for (int o = 16; o; o >>= 1) am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
-    const float ex = act ? expf(lg - mx) : 0.0f;
-    float s = ex;
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const int t = a.tgt[r * a.T + a.p];
-    const float lt = __shfl_sync(0xffffffffu, lg, t);
-    if (lane == 0) {
-        a.loss[r] = -((double)lt - (double)mx - log((double)s)) / a.T;
-        a.match[r] = am == t ? 1 : 0;
-    }
-    const float d = act ? (ex / s - (lane == t ? 1.0f : 0.0f)) / (float)a.T : 0.0f;
-    if (act) a.dlog[r * a.V + lane] = d;
-    if (!a.dh) return;
-    for (int j = lane; j < a.ns; j += 32) {
-        float v = 0.0f;
-        for (int q = 0; q < a.V; ++q) v += __shfl_sync(0xffffffffu, d, q) * Wsm[j * a.V + q];
-        a.dh[r * a.ns + j] = v;
+    // persistent: the head weights are staged once per block, warps loop over rows
+    for (long long r = (long long)blockIdx.x * warps + w; r < a.M; r += (long long)gridDim.x * warps) {
+        for (int j = lane; j < a.ns; j += 32) hrow[j] = a.h[r * a.ns + j];
+        __syncwarp();
+        float lg = 0.0f;  // lane v holds logit v
+        for (int v = 0; v < a.V; ++v) {
+            float part = 0.0f;
+            for (int j = lane; j < a.ns; j += 32) part += hrow[j] * Wsm[j * a.V + v];
+            for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            if (lane == v) lg = part + a.b[v];
+        }
+        const bool act = lane < a.V;
+        float mx = act ? lg : -INFINITY;
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        // argmax, lowest index on ties
+        int am = (act && lg == mx) ? lane : 64;
+        for (int o = 16; o; o >>= 1) am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
+        const float ex = act ? expf(lg - mx) : 0.0f;
+        float s = ex;
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const int t = a.tgt[r * a.T + a.p];
+        const float lt = __shfl_sync(0xffffffffu, lg, t);
+        if (lane == 0) {
+            a.loss[r] = -((double)lt - (double)mx - log((double)s)) / a.T;
+            a.match[r] = am == t ? 1 : 0;
+        }
+        const float d = act ? (ex / s - (lane == t ? 1.0f : 0.0f)) / (float)a.T : 0.0f;
+        if (act) a.dlog[r * a.V + lane] = d;
+        if (a.dh) {
+            // dh = dlogits . W^T; the dlogits go through shared memory (the j loop's
+            // trip count differs per lane, so no shuffles inside it)
+            dsm[lane] = d;
+            __syncwarp();
+            for (int j = lane; j < a.ns; j += 32) {
+                float v = 0.0f;
+                for (int q = 0; q < a.V; ++q) v += dsm[q] * Wsm[j * a.V + q];
+                a.dh[r * a.ns + j] = v;
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -748,7 +817,7 @@ struct ks_trainer {
     DBuf tok, tgt, idx, mi, mr, enc_slot, dec_slot, dec_val, enc_sm[2], dec_sm;
     DBuf Hx[2], Ce[2], Ze[2], dZe[2], A, U;
     DBuf Xd, Hs, Cd, Zd, dZd, alpha, hid, dlog, DHh, lossr, match;
-    DBuf dXd, dH, dC, dA, DPs, DPa, rowacc, dHe, dCe, part, norm, grads_tmp;
+    DBuf dXd, dH, dC, dA, Dctx, DPs, DPa, rowacc, dHe, dCe, part, norm, grads_tmp;
     bool tf32x3 = true;            // GEMM arithmetic: 3xTF32 tensor cores (default) or fp32 SIMT SGEMM
     DBuf sp[4];                    // split scratch: A big/small, B big/small
     DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
@@ -990,6 +1059,7 @@ ks_status ensure_ws(ks_trainer& t, int M) {
         TE(t.alpha, T * m * 7 * 4);
         TE(t.hid, T * m * 7 * t.n_d * 4);
         TE(t.dA, m * 7 * na2 * 4);
+        TE(t.Dctx, T * m * na2 * 4);
         TE(t.DPs, T * m * t.n_d * 4);
         TE(t.DPa, m * 7 * t.n_d * 4);
         TE(t.rowacc, m * (t.n_d + 1) * 4);
@@ -1022,7 +1092,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
     float* mi = drop ? t.mi.as<float>() : nullptr;
     float* mr = drop ? t.mr.as<float>() : nullptr;
     if (drop) {
-        k_dropout_masks<<<blocks(m, 64), 64, 0, s>>>(M, seed, dropout_epoch, d_idx, 0, t.n_in, t.dropout, Hd,
+        k_dropout_masks<<<blocks(m, 8), 256, 0, s>>>(M, seed, dropout_epoch, d_idx, 0, t.n_in, t.dropout, Hd,
                                                      t.rdropout, mi, mr);
         ++t.launches;
     }
@@ -1176,7 +1246,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             KT_CUDA(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             head_attr = smem;
         }
-        k_head<<<blocks(m, hw), hw * 32, smem, s>>>(ha);
+        k_head<<<(unsigned)std::min<long long>(blocks(m, hw), 148LL * 4), hw * 32, smem, s>>>(ha);
         ++t.launches;
     }
     k_loss_total<<<1, 256, 0, s>>>(t.lossr.as<double>(), t.match.as<int>(), (long long)T * m, d_loss, d_match,
@@ -1192,7 +1262,6 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
     KT_CUDA(cudaMemsetAsync(dH, 0, m * Hd * 4, s));
     KT_CUDA(cudaMemsetAsync(dC, 0, m * Hd * 4, s));
     if (attn) {
-        KT_CUDA(cudaMemsetAsync(t.dA.p, 0, m * 7 * na2 * 4, s));
         KT_CUDA(cudaMemsetAsync(t.DPa.p, 0, m * 7 * t.n_d * 4, s));
         KT_CUDA(cudaMemsetAsync(t.rowacc.p, 0, m * (t.n_d + 1) * 4, s));
     }
@@ -1234,7 +1303,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             ab.Ws = Wh;
             ab.Wa = Wh + (long long)t.n_s * t.n_d;
             ab.wo = P + t.off_attn_o;
-            ab.dA = t.dA.as<float>();
+            ab.dctx_out = t.Dctx.as<float>() + (long long)p * m * na2;
             ab.dH = dH;
             ab.DPs = t.DPs.as<float>() + (long long)p * m * t.n_d;
             ab.DPa = t.DPa.as<float>();
@@ -1273,6 +1342,18 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         if ((st = colsum(t, s, t.DPa.as<float>(), 7 * m, t.n_d, t.n_d, G + t.off_attn_hb, true))) return st;
         if ((st = colsum(t, s, t.rowacc.as<float>(), m, t.n_d, t.n_d + 1, G + t.off_attn_o, true))) return st;
         if ((st = colsum(t, s, t.rowacc.as<float>() + t.n_d, m, 1, t.n_d + 1, G + t.off_attn_ob, true))) return st;
+        AttnDA da{};
+        da.M = M;
+        da.T = T;
+        da.na2 = na2;
+        da.alpha = t.alpha.as<float>();
+        da.dctx = t.Dctx.as<float>();
+        da.DPa = t.DPa.as<float>();
+        da.Wa = Wh + (long long)t.n_s * t.n_d;
+        da.dA = t.dA.as<float>();
+        if (!launch_k_attn_dA(t.n_d, da, blocks(m * 32, 256), s))
+            return set_error(KS_ERR_UNSUPPORTED, "attention_dense_nodes outside 1..8");
+        ++t.launches;
     }
     // ---------------------------------------------------------------- encoder backward
     for (int dir = 0; dir < dirs; ++dir) {
