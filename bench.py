@@ -356,11 +356,14 @@ def run_b200(args):
         pass
 
     # end to end through the host C-ABI (pinned staging, copies in the timed region)
+    host_out = [None]
+
     def host_call():
         if W["greedy"]:
             eng.greedy(tok)  # ks_greedy_batch: greedy_decode semantics (strict argmax of p)
         else:
-            eng.beam(tok, BEAM, None, preds)
+            # caller-owned result buffers, reused call after call as a serving loop would
+            host_out[0] = eng.beam(tok, BEAM, None, preds, out=host_out[0])
 
     for _ in range(max(1, args.warmup // 2)):
         host_call()
@@ -487,7 +490,7 @@ def run_train(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2404_10162_b200.train import DataParallelTrainer, shard_batch
+    from paper_2404_10162_b200.dptrain import DataParallelTrainer, shard_batch
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)

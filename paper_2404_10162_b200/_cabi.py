@@ -220,16 +220,22 @@ class Engine:
                                        _p(tok, C.c_int32), C.byref(bad)))
         return tok
 
-    def beam(self, tok, k, desc=None, preds=()):
+    def beam(self, tok, k, desc=None, preds=(), out=None):
+        """ks_beam_search_batch.  `out` (optional) is a dict of caller-owned result
+        arrays from a previous call with the same B and k, reused in place."""
         tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
         B = len(tok)
         d = None if desc is None else np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
-        out_tok = np.empty((B, k, self.T), np.int32)
-        out_lp = np.empty((B, k), np.float64)
-        cnt = np.empty(B, np.int32)
-        st = np.empty(B, np.int32)
-        fp = np.empty(B, np.int32)
-        fs = np.empty(B, np.int32)
+        if out is not None and out["tokens"].shape == (B, k, self.T):
+            out_tok, out_lp, cnt = out["tokens"], out["log_prob"], out["count"]
+            st, fp, fs = out["status"], out["fail_pred"], out["fail_step"]
+        else:
+            out_tok = np.empty((B, k, self.T), np.int32)
+            out_lp = np.empty((B, k), np.float64)
+            cnt = np.empty(B, np.int32)
+            st = np.empty(B, np.int32)
+            fp = np.empty(B, np.int32)
+            fs = np.empty(B, np.int32)
         arr, keep = pack_preds(list(preds))
         check(lib().ks_beam_search_batch(self._h, _p(tok, C.c_int32), _p(d, C.c_int64), B, k, arr,
                                          len(preds), _p(out_tok, C.c_int32), _p(out_lp, C.c_double),

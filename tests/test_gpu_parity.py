@@ -199,3 +199,18 @@ def test_projected_context_modes(stem, mode, monkeypatch):
         a, g = o.beam(tok, k, threads=8), e.beam(tok, k)
         n, ties, bad = compare_beams(g, a)
         assert not bad, f"k={k}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_paper_beam_width_100(precision):
+    """OPCS-BS at the paper's k = 100 (Table IV): wide candidate sets
+    (H_p * V_p up to 1600) go through the shared-memory candidate buffers."""
+    path = golden_path("attn_small_trained.ckpt")
+    o, e = OracleModel(path), engine(path, precision)
+    tok = random_tokens(o, 96, 31)
+    preds = oracle_preds(o, [("membership", None), ("budget", ({n: 1.0 for n in o.names}, 30.0))])
+    a = o.beam(tok, 100, None, preds, threads=8)
+    g = e.beam(tok, 100, None, preds)
+    n, ties, bad = compare_beams(g, a)
+    assert (g["count"] == a["count"]).all()
+    assert not bad, f"{len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"

@@ -10,7 +10,7 @@ import socket
 import numpy as np
 import torch.multiprocessing as mp
 
-from paper_2404_10162_b200.train import shard_batch
+from paper_2404_10162_b200.dptrain import shard_batch
 from tests.util import golden_path
 
 
@@ -34,7 +34,7 @@ def _worker(rank, world, port, B, out_dir):
     import torch.distributed as dist
 
     from oracle import train_oracle as TO
-    from paper_2404_10162_b200.train import allreduce_sum, shard_batch
+    from paper_2404_10162_b200.dptrain import allreduce_sum, shard_batch
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
