@@ -110,6 +110,10 @@ typedef struct {
  *                  reported as decoded-sequence agreement. */
 enum { KS_PREC_F16X3 = 0, KS_PREC_FP32 = 1, KS_PREC_BF16 = 2 };
 
+/* An engine owns its weights and one device workspace: calls on the same
+ * engine are serialized by an internal lock (safe from several threads, as the
+ * reference's read-only SequencePredictor is); create one engine per GPU /
+ * stream for concurrent decoding.  A ks_trainer is single-threaded. */
 typedef struct ks_engine ks_engine;
 
 ks_status ks_engine_create(const ks_model_desc* model, int32_t device, int32_t precision,

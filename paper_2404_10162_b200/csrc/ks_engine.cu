@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -171,6 +172,7 @@ struct ks_engine {
     int conv_scratch = 0;
     DevLstm hb1[2], hb2[2];
     DevMem hybA, hybAf, hybC, hybH, feat;
+    std::mutex mu;                // calls share the workspace: one decode at a time per engine
     bool layered = false;         // hybrid: bi-LSTM 2 runs over bi-LSTM 1's sequence (not seeded)
     DevMem hybH1, hybX2;          // layered: H1 [T][C][2CP] fp32; bi-LSTM 2 operands per dir and step
     int num_sms = 148;
@@ -536,6 +538,8 @@ extern "C" int32_t ks_engine_vocab_size(const ks_engine* eng, int32_t p) {
 extern "C" int32_t ks_engine_precision(const ks_engine* eng) { return eng ? eng->precision : -1; }
 extern "C" int64_t ks_engine_last_launch_count(const ks_engine* eng) { return eng ? eng->launches : 0; }
 extern "C" ks_status ks_engine_set_chunk(ks_engine* eng, int64_t c) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
     if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
     eng->chunk = c > 0 ? c : 65536;
     return KS_OK;
@@ -1389,6 +1393,8 @@ extern "C" ks_status ks_beam_search_batch(ks_engine* eng, const int32_t* tok, co
                                           int64_t B, int32_t k, const ks_pred* preds, int32_t n_preds,
                                           int32_t* out_tok, double* out_lp, int32_t* out_count,
                                           int32_t* out_status, int32_t* out_fpred, int32_t* out_fstep) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
     ks_status st = check_common(eng, B, k, preds, n_preds);
     if (st) return st;
     if (B == 0) return KS_OK;
@@ -1402,6 +1408,8 @@ extern "C" ks_status ks_beam_search_batch_hooked(ks_engine* eng, const int32_t* 
                                                  ks_host_pred_fn hook, void* user, int32_t* out_tok,
                                                  double* out_lp, int32_t* out_count, int32_t* out_status,
                                                  int32_t* out_fpred, int32_t* out_fstep) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
     ks_status st = check_common(eng, B, k, preds, n_preds);
     if (st) return st;
     if (B == 0) return KS_OK;
@@ -1414,6 +1422,8 @@ extern "C" ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, c
                                            const int32_t* truth, int64_t B, int32_t k, const ks_pred* preds,
                                            int32_t n_preds, ks_host_pred_fn hook, void* user,
                                            int64_t* out_pos_matches, int64_t* out_perfect) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
     ks_status st = check_common(eng, B, k, preds, n_preds);
     if (st) return st;
     if (!tok || !truth || !out_pos_matches || !out_perfect) return set_error(KS_ERR_PARAMETER, "null buffer");
@@ -1477,6 +1487,8 @@ extern "C" ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, c
 }
 
 extern "C" ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
     ks_status st = check_common(eng, B, 1, nullptr, 0);
     if (st) return st;
     if (B == 0) return KS_OK;
@@ -1490,6 +1502,8 @@ extern "C" ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok,
                                            int32_t* d_out_tok, double* d_out_lp, int32_t* d_out_count,
                                            int32_t* d_out_status, int32_t* d_out_fpred,
                                            int32_t* d_out_fstep, void* stream) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
     ks_status st = check_common(eng, B, k, preds, n_preds);
     if (st) return st;
     if (B == 0) return KS_OK;

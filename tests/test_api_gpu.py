@@ -204,3 +204,30 @@ def test_topk_metrics_device_scoring_with_hits_and_exhaustion(ks, params, oracle
     assert math.isclose(rep["average_accuracy"], float(np.mean(per / len(ds) * 100)), rel_tol=1e-9)
     assert math.isclose(rep["perfect_prediction"], 100.0 * perfect / len(ds), rel_tol=1e-9)
     assert rep["constrained"]
+
+
+def test_concurrent_calls_on_one_engine(ks, params, oracle):
+    """The reference's predictor is shared read-only across threads
+    (models.hpp:78-79); the GIL is released around device work, so calls on one
+    engine from several threads must serialize inside the engine."""
+    import threading
+
+    ds = descs(oracle, 64, 21)
+    ref = ks.predict_batch(params, ds, beam_width=4)
+    out = [None] * 6
+    errs = []
+
+    def work(i):
+        try:
+            out[i] = ks.predict_batch(params, ds, beam_width=4)
+        except Exception as ex:  # pragma: no cover - reported below
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(out))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for o in out:
+        assert [[e["params"] for e in r] for r in o] == [[e["params"] for e in r] for r in ref]
