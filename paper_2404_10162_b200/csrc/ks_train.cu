@@ -604,14 +604,20 @@ __global__ void k_colsum_final(const double* part, int N, int chunks, float* out
 // 3xTF32 operand split: x = big + small with both parts tf32-exact (round to
 // nearest, 10-bit mantissa); big.big + big.small + small.big recovers an
 // fp32-grade product on the TF32 tensor cores (the dropped small.small term is
-// ~2^-22 relative).  Packs a (rows x cols, ld) matrix densely.
+// ~2^-22 relative).
 __device__ __forceinline__ float tf32_rna(float x) {
     unsigned u;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
     return __uint_as_float(u);
 }
-__global__ void k_split_tf32(const float* src, long long rows, int cols, long long ld, float* big, float* small,
-                             bool vec) {
+// 3xTF32 as ONE GEMM over a tripled reduction: A' = [small(A) | big(A) | big(A)]
+// and B' = [big(B) ; small(B) ; big(B)] (stacked along K) give
+// A'.B' = small.big + big.small + big.big in a single cuBLASLt call (one C
+// read/write instead of three, 3x longer K per launch).  `stack` = 0: the three
+// parts side by side in each row (out rows x 3cols); 1: stacked (3rows x cols).
+// Part i is small(x) when bit i of small_mask is set, big(x) otherwise.
+__global__ void k_split_cat(const float* src, long long rows, int cols, long long ld, float* out, int stack,
+                            int small_mask, bool vec) {
     const int cw = vec ? cols / 4 : cols;
     for (long long r = blockIdx.y; r < rows; r += gridDim.y) {
         for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cw; c += gridDim.x * blockDim.x) {
@@ -620,24 +626,26 @@ __global__ void k_split_tf32(const float* src, long long rows, int cols, long lo
                 float4 b, sm;
                 b.x = tf32_rna(x.x); b.y = tf32_rna(x.y); b.z = tf32_rna(x.z); b.w = tf32_rna(x.w);
                 sm.x = tf32_rna(x.x - b.x); sm.y = tf32_rna(x.y - b.y); sm.z = tf32_rna(x.z - b.z); sm.w = tf32_rna(x.w - b.w);
-                reinterpret_cast<float4*>(big + r * cols)[c] = b;
-                reinterpret_cast<float4*>(small + r * cols)[c] = sm;
+#pragma unroll
+                for (int part = 0; part < 3; ++part) {
+                    float* dst = stack ? out + ((long long)part * rows + r) * cols : out + r * 3LL * cols + (long long)part * cols;
+                    reinterpret_cast<float4*>(dst)[c] = ((small_mask >> part) & 1) ? sm : b;
+                }
             } else {
                 const float x = src[r * ld + c];
-                const float b = tf32_rna(x);
-                big[r * cols + c] = b;
-                small[r * cols + c] = tf32_rna(x - b);
+                const float b = tf32_rna(x), sm = tf32_rna(x - b);
+#pragma unroll
+                for (int part = 0; part < 3; ++part) {
+                    float* dst = stack ? out + ((long long)part * rows + r) * cols : out + r * 3LL * cols + (long long)part * cols;
+                    dst[c] = ((small_mask >> part) & 1) ? sm : b;
+                }
             }
         }
     }
 }
 
-// Same split, transposed: dst[c][r] (dense, ld = rows) from src[r][c] (ld), through
-// 32 x 32 shared-memory tiles so both sides stay coalesced.  Used for the
-// transposed A operand of the weight-gradient GEMMs (X^T . dZ): cuBLAS picks
-// legacy sm80 TF32 kernels for that layout, the NN form runs on sm100 kernels.
-__global__ void k_split_tf32_t(const float* src, long long rows, long long cols, long long ld, float* big,
-                               float* small) {
+// Transposed variant for A^T: out (cols x 3rows), row c = [small | big | big] of column c.
+__global__ void k_split_cat_t(const float* src, long long rows, long long cols, long long ld, float* out) {
     __shared__ float tile[32][33];
     const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -650,8 +658,10 @@ __global__ void k_split_tf32_t(const float* src, long long rows, long long cols,
         if (c < cols && r < rows) {
             const float x = tile[threadIdx.x][i];
             const float b = tf32_rna(x);
-            big[c * rows + r] = b;
-            small[c * rows + r] = tf32_rna(x - b);
+            float* row = out + c * 3 * rows;
+            row[r] = tf32_rna(x - b);
+            row[rows + r] = b;
+            row[2 * rows + r] = b;
         }
     }
 }
@@ -823,7 +833,7 @@ struct ks_trainer {
     DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
     cublasLtHandle_t lt = nullptr;
     std::map<LtKey, LtPlan> lt_plans;
-    std::map<const float*, std::pair<DBuf*, long long>> wsplit;  // per-call weight splits
+    std::map<std::pair<const float*, bool>, std::pair<DBuf*, long long>> wsplit;  // per-call weight splits
     std::vector<std::unique_ptr<DBuf[]>> wsplit_store;  // pool, reused call after call
     size_t wsplit_used = 0;
     int n_in = 0;  // decoder input-mask width
@@ -921,24 +931,20 @@ ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long
     return gemm_one(t, false, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_FAST_TF32);
 }
 
-// Splits a stored (rows x cols, ld) operand into dense big/small planes.
-ks_status split_into(ks_trainer& t, cudaStream_t s, const float* src, long long rows, long long cols, long long ld,
-                     DBuf& big, DBuf& small) {
-    const size_t bytes = (size_t)rows * cols * 4;
-    KT_CUDA(big.ensure(bytes));
-    KT_CUDA(small.ensure(bytes));
-    const bool vec = cols % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+void launch_split_cat(ks_trainer& t, cudaStream_t s, const float* src, long long rows, long long cols, long long ld,
+                      float* out, int stack, int small_mask) {
+    const bool vec = cols % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     const long long cw = vec ? cols / 4 : cols;
     dim3 grid((unsigned)std::min<long long>((cw + 255) / 256, 64), (unsigned)std::min<long long>(rows, 65535));
-    k_split_tf32<<<grid, 256, 0, s>>>(src, rows, (int)cols, ld, big.as<float>(), small.as<float>(), vec);
+    k_split_cat<<<grid, 256, 0, s>>>(src, rows, (int)cols, ld, out, stack, small_mask, vec);
     ++t.launches;
-    return KS_OK;
 }
 
 // Row-major C[M x N] = op(A) op(B) + beta C, on cuBLAS (column-major).  3xTF32
-// mode: both operands split (weights once per call, cached by pointer) and
-// C = beta C + small(A).big(B) + big(A).small(B) + big(A).big(B) on TF32 tensor
-// cores with fp32 accumulation; fp32 mode: one SGEMM (PEDANTIC, no TF32).
+// mode: both operands split (weights once per call, cached by pointer and
+// layout) into the concatenated-K form of k_split_cat, one TF32 tensor-core
+// GEMM with fp32 accumulation; fp32 mode: one SGEMM (PEDANTIC, no TF32).
 ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
                   long long lda, const float* B, long long ldb, float beta, float* C, long long ldc,
                   bool b_is_weight = false) {
@@ -951,50 +957,50 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
     cudaStream_t s;
     KT_BLAS(cublasGetStream(t.blas, &s));
     ks_status st;
-    const long long br = tb ? N : K, bc = tb ? K : N;
-    // A is packed row-major M x K (a transposed A is transposed while splitting)
+    const long long K3 = 3 * K;
+    // A' = [small | big | big] (M x 3K; a transposed A is transposed while splitting)
+    KT_CUDA(t.sp[0].ensure((size_t)M * K3 * 4));
     if (ta) {
-        KT_CUDA(t.sp[0].ensure((size_t)M * K * 4));
-        KT_CUDA(t.sp[1].ensure((size_t)M * K * 4));
         dim3 grid((unsigned)((M + 31) / 32), (unsigned)((K + 31) / 32));
         if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
-        k_split_tf32_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, t.sp[0].as<float>(), t.sp[1].as<float>());
+        k_split_cat_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, t.sp[0].as<float>());
         ++t.launches;
-    } else if ((st = split_into(t, s, A, M, K, lda, t.sp[0], t.sp[1]))) {
-        return st;
+    } else {
+        launch_split_cat(t, s, A, M, K, lda, t.sp[0].as<float>(), 0, 0b001);
     }
-    const long long ac = K;
-    const float *Bb, *Bs;
+    // B' = [big ; small ; big] along K: stacked rows (K x N) or side by side (tb: N x K)
+    const float* Bc;
+    const long long br = tb ? N : K, bc = tb ? K : N;
+    const size_t bbytes = (size_t)br * bc * 3 * 4;
+    auto split_b = [&](DBuf& dst) -> ks_status {
+        KT_CUDA(dst.ensure(bbytes));
+        launch_split_cat(t, s, B, br, bc, ldb, dst.as<float>(), tb ? 0 : 1, 0b010);
+        return KS_OK;
+    };
     if (b_is_weight) {
-        auto it = t.wsplit.find(B);
+        // cached per (weight, layout): the forward uses W stacked along K, the dX GEMMs
+        // W^T side by side
+        const std::pair<const float*, bool> key(B, tb);
+        auto it = t.wsplit.find(key);
         if (it == t.wsplit.end()) {
             if (t.wsplit_used == t.wsplit_store.size()) t.wsplit_store.emplace_back(new DBuf[2]);
-            DBuf* pair = t.wsplit_store[t.wsplit_used++].get();
-            if ((st = split_into(t, s, B, br, bc, ldb, pair[0], pair[1]))) return st;
-            it = t.wsplit.emplace(B, std::make_pair(pair, bc)).first;
+            DBuf* buf = t.wsplit_store[t.wsplit_used++].get();
+            if ((st = split_b(buf[0]))) return st;
+            it = t.wsplit.emplace(key, std::make_pair(buf, bc)).first;
         }
-        Bb = it->second.first[0].as<float>();
-        Bs = it->second.first[1].as<float>();
+        Bc = it->second.first[0].as<float>();
     } else {
-        if ((st = split_into(t, s, B, br, bc, ldb, t.sp[2], t.sp[3]))) return st;
-        Bb = t.sp[2].as<float>();
-        Bs = t.sp[3].as<float>();
+        if ((st = split_b(t.sp[2]))) return st;
+        Bc = t.sp[2].as<float>();
     }
-    const float* Ab = t.sp[0].as<float>();
-    const float* As = t.sp[1].as<float>();
+    const long long ldb3 = tb ? K3 : N;
     static const bool use_lt = [] {
         const char* e = std::getenv("KS_TRAIN_LT");
         return !(e && e[0] == '0');
     }();
-    if (use_lt) {
-        if ((st = gemm_lt(t, s, tb, M, N, K, As, ac, Bb, bc, beta, C, ldc))) return st;
-        if ((st = gemm_lt(t, s, tb, M, N, K, Ab, ac, Bs, bc, 1.0f, C, ldc))) return st;
-        return gemm_lt(t, s, tb, M, N, K, Ab, ac, Bb, bc, 1.0f, C, ldc);
-    }
-    const cublasComputeType_t ct = CUBLAS_COMPUTE_32F_FAST_TF32;
-    if ((st = gemm_one(t, false, tb, M, N, K, As, ac, Bb, bc, beta, C, ldc, ct))) return st;
-    if ((st = gemm_one(t, false, tb, M, N, K, Ab, ac, Bs, bc, 1.0f, C, ldc, ct))) return st;
-    return gemm_one(t, false, tb, M, N, K, Ab, ac, Bb, bc, 1.0f, C, ldc, ct);
+    if (use_lt) return gemm_lt(t, s, tb, M, N, K3, t.sp[0].as<float>(), K3, Bc, ldb3, beta, C, ldc);
+    return gemm_one(t, false, tb, M, N, K3, t.sp[0].as<float>(), K3, Bc, ldb3, beta, C, ldc,
+                    CUBLAS_COMPUTE_32F_FAST_TF32);
 }
 
 ks_status colsum(ks_trainer& t, cudaStream_t s, const float* in, long long R, int N, long long ld, float* out,
