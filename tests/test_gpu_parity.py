@@ -214,3 +214,27 @@ def test_paper_beam_width_100(precision):
     n, ties, bad = compare_beams(g, a)
     assert (g["count"] == a["count"]).all()
     assert not bad, f"{len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
+@pytest.mark.parametrize("kernel", ["ConvAsm1x1U", "ConvOclDirectFwd1x1", "ConvAsmBwdWrW1x1", "ConvAsmBwdWrW3x3"])
+@pytest.mark.parametrize("variant", ["attn", "enc-dec"])
+def test_builtin_kernel_specs(kernel, variant, tmp_path):
+    """Every builtin Table-I spec (T_out 6..10, V up to 16, feedback widths up
+    to 59) through the engine vs the oracle.  Random weights with the heads
+    scaled x40 so distributions are peaked (untrained heads leave nearly every
+    config tie-adjacent)."""
+    from paper_2404_10162_b200.synth import write_checkpoint
+
+    raw = write_checkpoint(str(tmp_path / "raw.ckpt"), kernel, variant, n_a=32, n_s=64, e_size=48, seed=17)
+    path = ckpt_util.modified(raw, str(tmp_path / "m.ckpt"),
+                              lambda t: [t.__setitem__(n, t[n] * 40.0) for n in list(t) if n.startswith("head.")])
+    o, e = OracleModel(path), engine(path, "f16x3")
+    tok = random_tokens(o, 512, 5)
+    desc = random_desc(o, tok)
+    preds = oracle_preds(o, [("membership", None), ("budget", ({n: 1.0 for n in o.names}, float(sum(
+        sorted(v)[len(v) // 2] for v in o.values))))])
+    a = o.beam(tok, 5, desc, preds, threads=8)
+    g = e.beam(tok, 5, desc, preds)
+    n, ties, bad = compare_beams(g, a)
+    assert n >= 0.5 * len(tok), f"only {n} non-tie-adjacent configs"
+    assert not bad, f"{len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
