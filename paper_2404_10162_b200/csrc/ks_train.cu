@@ -828,6 +828,7 @@ struct ks_trainer {
     DBuf Hx[2], Ce[2], Ze[2], dZe[2], A, U;
     DBuf Xd, Hs, Cd, Zd, dZd, alpha, hid, dlog, DHh, lossr, match;
     DBuf dXd, dH, dC, dA, Dctx, DPs, DPa, rowacc, dHe, dCe, part, norm, grads_tmp;
+    DBuf res;                      // {loss sum, matches} of the last step / evaluate
     bool tf32x3 = true;            // GEMM arithmetic: 3xTF32 tensor cores (default) or fp32 SIMT SGEMM
     DBuf sp[4];                    // split scratch: A big/small, B big/small
     DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
@@ -1715,8 +1716,8 @@ extern "C" ks_status ks_trainer_step(ks_trainer* t, const int32_t* tok, const in
     if ((st = ensure_ws(*t, (int)B))) return st;
     if (!t->grads_tmp.p || t->grads_tmp.bytes < (size_t)t->nparams * 4)
         KT_CUDA(t->grads_tmp.ensure((size_t)t->nparams * 4));
-    DBuf res;
-    KT_CUDA(res.ensure(16));
+    KT_CUDA(t->res.ensure(16));
+    DBuf& res = t->res;
     cudaStream_t s = nullptr;
     KT_CUDA(cudaMemcpyAsync(t->tok.p, tok, (size_t)B * 7 * 4, cudaMemcpyHostToDevice, s));
     KT_CUDA(cudaMemcpyAsync(t->tgt.p, tgt, (size_t)B * t->T * 4, cudaMemcpyHostToDevice, s));
@@ -1744,8 +1745,8 @@ extern "C" ks_status ks_trainer_evaluate(ks_trainer* t, const int32_t* tok, cons
     cudaSetDevice(t->device);
     ks_status st;
     if ((st = ensure_ws(*t, (int)B))) return st;
-    DBuf res;
-    KT_CUDA(res.ensure(16));
+    KT_CUDA(t->res.ensure(16));
+    DBuf& res = t->res;
     cudaStream_t s = nullptr;
     KT_CUDA(cudaMemcpyAsync(t->tok.p, tok, (size_t)B * 7 * 4, cudaMemcpyHostToDevice, s));
     KT_CUDA(cudaMemcpyAsync(t->tgt.p, tgt, (size_t)B * t->T * 4, cudaMemcpyHostToDevice, s));
