@@ -738,6 +738,13 @@ __device__ bool pred_accepts(const PredTables& a, const PosMeta& m, const DevPre
 }
 
 
+// Order-preserving unsigned image of an fp64 score (-0.0 folded onto +0.0 so
+// that it compares equal, as in better()); 0 is never produced for a non-NaN.
+__device__ __forceinline__ unsigned long long order_key(double s) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(s + 0.0);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 // Candidate order: higher score first, exact ties to the smaller packed
 // prefix key (= lexicographically smaller prefix; Candidate::operator<,
 // decoding.cpp:21-24).
@@ -788,9 +795,15 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
     constexpr int WS = VP == 4 ? 12 : VP + 4;  // padded W row: conflict-free 128-bit loads
     const int V = m.vsize[a.pos];
     float* Wsh = reinterpret_cast<float*>(smem);
+    // NS % 4 == 0: hidden rows are read as float4 (lane owns elements 4q..4q+3), so
+    // W row i is stored at slot (i % 4) * NS/4 + i / 4 -- for a fixed component the
+    // lanes then read consecutive slots, conflict-free like the scalar layout.
+    const bool v4 = (a.NS & 3) == 0 && (reinterpret_cast<uintptr_t>(a.h) & 15) == 0;
+    const int NQ = a.NS >> 2;
     for (int i = threadIdx.x; i < a.NS * VP; i += blockDim.x) {
         const int row = i / VP, v = i - row * VP;
-        Wsh[row * WS + v] = v < V ? a.Wh[row * V + v] : 0.0f;
+        const int slot = v4 ? (row & 3) * NQ + (row >> 2) : row;
+        Wsh[slot * WS + v] = v < V ? a.Wh[row * V + v] : 0.0f;
     }
     const size_t wbytes = ((size_t)a.NS * WS * 4 + 15) & ~(size_t)15;
     const PredTables tabs = stage_pred_tables(a, smem + wbytes);
@@ -847,6 +860,35 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                 // hybrid variants: every hypothesis of config b reads the same feature row
                 const float* h0 = a.h + (a.h_per_config ? (long long)b : r0) * a.NS;
                 const float* h1 = a.h_per_config ? h0 : h0 + a.NS;
+                if (v4) {
+                    // 128-bit loads, both rows' loads in flight together
+                    const float4* h04 = reinterpret_cast<const float4*>(h0);
+                    const float4* h14 = reinterpret_cast<const float4*>(h1);
+                    const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll 4
+                    for (int q = lane; q < NQ; q += 32) {
+                        const float4 x0 = live0 ? __ldg(h04 + q) : z4;
+                        const float4 x1 = live1 ? __ldg(h14 + q) : z4;
+                        const float xs0[4] = {x0.x, x0.y, x0.z, x0.w};
+                        const float xs1[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float4* w4 = reinterpret_cast<const float4*>(Wsh + (e * NQ + q) * WS);
+#pragma unroll
+                            for (int qq = 0; qq < VP / 4; ++qq) {
+                                const float4 w = w4[qq];
+                                p0[4 * qq + 0] = fmaf(xs0[e], w.x, p0[4 * qq + 0]);
+                                p0[4 * qq + 1] = fmaf(xs0[e], w.y, p0[4 * qq + 1]);
+                                p0[4 * qq + 2] = fmaf(xs0[e], w.z, p0[4 * qq + 2]);
+                                p0[4 * qq + 3] = fmaf(xs0[e], w.w, p0[4 * qq + 3]);
+                                p1[4 * qq + 0] = fmaf(xs1[e], w.x, p1[4 * qq + 0]);
+                                p1[4 * qq + 1] = fmaf(xs1[e], w.y, p1[4 * qq + 1]);
+                                p1[4 * qq + 2] = fmaf(xs1[e], w.z, p1[4 * qq + 2]);
+                                p1[4 * qq + 3] = fmaf(xs1[e], w.w, p1[4 * qq + 3]);
+                            }
+                        }
+                    }
+                } else
 #pragma unroll(VP <= 8 ? 16 : 4)
                 for (int i = lane; i < a.NS; i += 32) {
                     const float x0 = live0 ? h0[i] : 0.0f;
@@ -880,7 +922,6 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                     continue;
                 }
                 last_live = j;
-                const long long r = r0 + jj;
                 // log-softmax (nn.cpp:215-226) as (l - max) - log(sum exp), i.e. log(p)
                 // without underflow, floored at log(1e-300) like decoding.cpp:57-58; the
                 // hypothesis score accumulates in fp64
@@ -888,35 +929,47 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                 const float mx = warp_max_f(l);
                 const float ex = lane < V ? expf(l - mx) : 0.0f;
                 const float sum = warp_sum_f(ex);
-                const float lpt = fmaxf((l - mx) - logf(sum), -690.77552789821368f);
-                const double clp = a.lp_cur[r] + (double)lpt;
-                // greedy_decode's argmax of p == argmax of the logit (ties -> lowest index)
-                const double pr = (double)l;
-                const unsigned long long key = a.key_cur[r] | ((unsigned long long)lane << m.shift[a.pos]);
-                int rej = -1;
                 if (lane < V) {
-                    // host-evaluated (opaque) predicates: registration index of the first
-                    // rejecting one; typed predicates registered before it still win
-                    const int hrej = a.host_rej ? a.host_rej[r * V + lane] : -1;
-                    const int qend = hrej >= 0 ? hrej : a.n_preds;
-                    rej = hrej;
-                    for (int q = 0; q < qend; ++q) {
-                        const DevPred& pq = tabs.preds[q];
-                        if (pq.kind == 5) continue;  // KS_PRED_HOST: decided by the hook
-                        if (pq.full && !a.final_step) continue;
-                        if (!pred_accepts(tabs, m, pq, key, a.pos, desc_b)) {
-                            rej = q;
-                            break;
-                        }
-                    }
+                    const float lpt = fmaxf((l - mx) - logf(sum), -690.77552789821368f);
+                    const double clp = a.lp_cur[r0 + jj] + (double)lpt;
                     const int c = j * V + lane;
-                    c_score[c] = a.greedy ? pr : clp;
+                    // greedy_decode's argmax of p == argmax of the logit (ties -> lowest index)
+                    c_score[c] = a.greedy ? (double)l : clp;
                     c_lp[c] = clp;
-                    c_key[c] = key;
-                    c_meta[c] = rej < 0 ? ((j << 8) | lane) : -2 - rej;
+                    c_meta[c] = 0;  // live, predicates pending
                 }
-                n_alive += __popc(__ballot_sync(0xffffffffu, lane < V && rej < 0));
             }
+        }
+        __syncwarp();
+        // Constraint predicates over all H_cur x V children at once, 32 per pass
+        // (lane-dense even when V < 32).
+        for (int c0 = 0; c0 < nc; c0 += 32) {
+            const int c = c0 + lane;
+            int rej = -1;
+            bool ok = false;
+            if (c < nc && c_meta[c] == 0) {
+                const int j = c / V, v = c - j * V;
+                const long long r = (long long)b * a.H_cur + j;
+                const unsigned long long key = a.key_cur[r] | ((unsigned long long)v << m.shift[a.pos]);
+                // host-evaluated (opaque) predicates: registration index of the first
+                // rejecting one; typed predicates registered before it still win
+                const int hrej = a.host_rej ? a.host_rej[r * V + v] : -1;
+                const int qend = hrej >= 0 ? hrej : a.n_preds;
+                rej = hrej;
+                for (int q = 0; q < qend; ++q) {
+                    const DevPred& pq = tabs.preds[q];
+                    if (pq.kind == 5) continue;  // KS_PRED_HOST: decided by the hook
+                    if (pq.full && !a.final_step) continue;
+                    if (!pred_accepts(tabs, m, pq, key, a.pos, desc_b)) {
+                        rej = q;
+                        break;
+                    }
+                }
+                c_key[c] = key;
+                c_meta[c] = rej < 0 ? ((j << 8) | v) : -2 - rej;
+                ok = rej < 0;
+            }
+            n_alive += __popc(__ballot_sync(0xffffffffu, ok));
         }
         __syncwarp();
         if (n_alive == 0) {
@@ -944,7 +997,10 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
         }
         const int ksel = n_alive < a.k ? n_alive : a.k;
         // k rounds of warp argmax; each lane caches the best of its own candidates
-        // and only the lane that owned the winner rescans.
+        // and only the lane that owned the winner rescans.  The argmax runs on the
+        // order-preserving 64-bit image of the fp64 score with two redux.sync maxima
+        // (high word, then low word among the lanes holding that high word); exact
+        // score ties fall back to the smallest prefix key the same way.
         double bs = -INFINITY;
         unsigned long long bk = ~0ull;
         int bc = -1;
@@ -963,21 +1019,20 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
         };
         rescan();
         for (int i = 0; i < ksel; ++i) {
-            double ws = bs;
-            unsigned long long wk = bk;
-            int wc = bc;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double os = __shfl_xor_sync(0xffffffffu, ws, o);
-                const unsigned long long ok = __shfl_xor_sync(0xffffffffu, wk, o);
-                const int oc = __shfl_xor_sync(0xffffffffu, wc, o);
-                if (oc >= 0 && (wc < 0 || better(os, ok, ws, wk))) {
-                    ws = os;
-                    wk = ok;
-                    wc = oc;
-                }
+            const unsigned long long u = bc < 0 ? 0ull : order_key(bs);
+            const unsigned uh = (unsigned)(u >> 32), ul = (unsigned)u;
+            const unsigned mh = __reduce_max_sync(0xffffffffu, uh);
+            const unsigned ml = __reduce_max_sync(0xffffffffu, uh == mh ? ul : 0u);
+            unsigned tie = __ballot_sync(0xffffffffu, bc >= 0 && uh == mh && ul == ml);
+            if (tie & (tie - 1)) {  // equal scores: smaller packed prefix key wins
+                const bool in = (tie >> lane) & 1u;
+                const unsigned kh = (unsigned)(bk >> 32), kl = (unsigned)bk;
+                const unsigned nh = __reduce_min_sync(0xffffffffu, in ? kh : 0xffffffffu);
+                const unsigned nl = __reduce_min_sync(0xffffffffu, in && kh == nh ? kl : 0xffffffffu);
+                tie = __ballot_sync(0xffffffffu, in && kh == nh && kl == nl);
             }
-            if (wc == bc) {  // this lane owns the winner (candidate indices are unique)
+            const int wl = __ffs(tie) - 1;
+            if (lane == wl) {  // this lane owns the winner (prefix keys are unique)
                 const int meta = c_meta[bc];
                 const int j = meta >> 8, v = meta & 255;
                 const double clp = c_lp[bc];
