@@ -239,10 +239,7 @@ __device__ __forceinline__ void write_alpha_block(const AttnArgs& p, int r, int 
 }
 
 template <int ND, int SPLIT, bool FIRST>
-__global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (r >= p.M) return;
+__device__ __forceinline__ void attention_row(const AttnArgs& p, int r, int lane) {
     const int b = r / p.H_rows;
     const int par = p.parent ? p.parent[r] : r;
     const float* s = (p.h_prev != nullptr && par >= 0) ? p.h_prev + (long long)par * p.ldh : nullptr;
@@ -309,25 +306,31 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
 #pragma unroll
             for (int d = 0; d < ND; ++d) u[t][d] = p.uatt[((long long)b * kTin + t) * ND + d];
     }
-    float e[kTin];
-    float mx = -FLT_MAX;
-#pragma unroll
-    for (int t = 0; t < kTin; ++t) {
+    // e_t on lane t: b_o + sum_d tanh(s.W_s[:,d] + u[t][d]) w_o[d]; softmax over
+    // lanes 0..7 (lane 7 carries exp = 0)
+    float ev = -FLT_MAX;
+    if (lane < kTin) {
         float v = p.bo;
 #pragma unroll
-        for (int d = 0; d < ND; ++d) v = fmaf(tanhf(sd[d] + u[t][d]), p.wo[d], v);
-        e[t] = v;
-        mx = fmaxf(mx, v);
-    }
-    float sum = 0.0f;
+        for (int d = 0; d < ND; ++d) {
+            float ut = u[0][d];
 #pragma unroll
-    for (int t = 0; t < kTin; ++t) {
-        e[t] = expf(e[t] - mx);
-        sum += e[t];
+            for (int t = 1; t < kTin; ++t) ut = lane == t ? u[t][d] : ut;
+            v = fmaf(tanhf(sd[d] + ut), p.wo[d], v);
+        }
+        ev = v;
     }
-    const float inv = 1.0f / sum;
+    float mx = ev;
 #pragma unroll
-    for (int t = 0; t < kTin; ++t) e[t] *= inv;
+    for (int o = 4; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float ex = lane < kTin ? expf(ev - mx) : 0.0f;
+    float sum = ex;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float al_lane = ex * (1.0f / sum);
+    float e[kTin];
+#pragma unroll
+    for (int t = 0; t < kTin; ++t) e[t] = __shfl_sync(0xffffffffu, al_lane, t);
     if (SPLIT != 0 && p.kalpha) {  // projected context: alpha . P^T on the tensor cores
         write_alpha_block<SPLIT>(p, r, b, e, lane);
         return;
@@ -344,6 +347,14 @@ __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
         }
         store4<SPLIT>(p, base + 4 * c, acc);
     }
+}
+
+template <int ND, int SPLIT, bool FIRST>
+__global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // persistent: one warp per row, grid-strided (the grid is sized to one resident wave)
+    for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < p.M; r += gridDim.x * (blockDim.x >> 5))
+        attention_row<ND, SPLIT, FIRST>(p, r, lane);
 }
 
 // Config-per-warp variant for positions > 0: the H rows of a config share
@@ -526,15 +537,24 @@ void launch_attention_nd(const AttnArgs& p, bool first, cudaStream_t s) {
         const char* e = std::getenv("KS_ATTN_MODE");
         return e ? std::atoi(e) : 0;
     }();
+    // warp-per-row kernel: persistent grid of one resident wave
+    auto wave = [](void (*kern)(AttnArgs), long long want) -> unsigned {
+        int per_sm = 0, sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        return (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)sms * per_sm));
+    };
     if (first) {
-        attention_pack_t<ND, SPLIT, true><<<(unsigned)((p.M + 7) / 8), 256, 0, s>>>(p);
+        attention_pack_t<ND, SPLIT, true><<<wave(attention_pack_t<ND, SPLIT, true>, (p.M + 7) / 8), 256, 0, s>>>(p);
     } else if (mode == 0 && p.H_rows > 1 && p.H_rows <= 64 && p.kalpha == 0) {
         attention_cta_t<ND, SPLIT><<<(unsigned)(p.M / p.H_rows), 128, 0, s>>>(p);
     } else if (mode == 2 && p.H_rows > 1) {
         const int C = p.M / p.H_rows;
         attention_cfg_t<ND, SPLIT><<<(unsigned)((C + 7) / 8), 256, 0, s>>>(p);
     } else {
-        attention_pack_t<ND, SPLIT, false><<<(unsigned)((p.M + 7) / 8), 256, 0, s>>>(p);
+        attention_pack_t<ND, SPLIT, false><<<wave(attention_pack_t<ND, SPLIT, false>, (p.M + 7) / 8), 256, 0, s>>>(p);
     }
 }
 
