@@ -29,6 +29,7 @@
 
 namespace ksb {
 __global__ void lstm_step_simt(LstmArgs a0, LstmArgs a1);
+bool launch_lstm_k0(const LstmArgs& a0, const LstmArgs* a1, int sms, cudaStream_t s);
 bool launch_attention(const AttnArgs& p, bool first, cudaStream_t s);
 __global__ void beam_init(int B, unsigned char* live, double* lp, unsigned long long* key,
                           int* status, int* fail_pred, int* fail_step);
@@ -744,6 +745,10 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
                               L1 ? L1->Whi.as<__half>() : nullptr, L1 ? L1->Wlo.as<__half>() : nullptr,
                               E.stream, &n, E.tc_units);
         if (!done) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
+    }
+    if (!done && a0.K == 0 && launch_lstm_k0(a0, a1, E.num_sms, E.stream)) {
+        done = true;
+        n = 1;
     }
     if (!done) {
         dim3 grid((unsigned)((a0.M + SB_M_HOST - 1) / SB_M_HOST), (unsigned)(a0.H / 32), a1 ? 2u : 1u);

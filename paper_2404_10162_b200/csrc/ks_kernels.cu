@@ -81,6 +81,72 @@ __device__ __forceinline__ int row_crow(const LstmArgs& p, int row) {
 }
 
 // ---------------------------------------------------------------------------
+// lstm_cell_k0: an LSTM step with no dense input (K = 0: the first encoder
+// step, zero state), i.e. gates = G[slot] -- pure elementwise, 4 units per
+// thread with 128-bit loads/stores; same cell arithmetic as lstm_cell_store.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lstm_cell_k0(LstmArgs a0, LstmArgs a1) {
+    const LstmArgs& p = blockIdx.y == 0 ? a0 : a1;
+    const int H4 = p.H >> 2;
+    const long long n = (long long)p.M * H4;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(i / H4), u = (int)(i - (long long)row * H4) * 4;
+        const float* G = p.G + (long long)row_slot(p, row) * 4 * p.H + u;
+        const float4 gi = *reinterpret_cast<const float4*>(G);
+        const float4 gf = *reinterpret_cast<const float4*>(G + p.H);
+        const float4 go = *reinterpret_cast<const float4*>(G + 2 * p.H);
+        const float4 gc = *reinterpret_cast<const float4*>(G + 3 * p.H);
+        const int crow = row_crow(p, row);
+        float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (p.c_prev != nullptr && crow >= 0) cp = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u);
+        const float I[4] = {gi.x, gi.y, gi.z, gi.w}, F[4] = {gf.x, gf.y, gf.z, gf.w};
+        const float O[4] = {go.x, go.y, go.z, go.w}, Cg[4] = {gc.x, gc.y, gc.z, gc.w};
+        const float Cp[4] = {cp.x, cp.y, cp.z, cp.w};
+        float c[4], h[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            c[j] = sigmoidf_(F[j]) * Cp[j] + sigmoidf_(I[j]) * tanhf(Cg[j]);
+            h[j] = sigmoidf_(O[j]) * tanhf(c[j]);
+        }
+        *reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u) = make_float4(c[0], c[1], c[2], c[3]);
+        *reinterpret_cast<float4*>(p.h_out + (long long)row * p.ldh + u) = make_float4(h[0], h[1], h[2], h[3]);
+        if (p.h_out2 != nullptr)
+            *reinterpret_cast<float4*>(p.h_out2 + (long long)row * p.ldh2 + u) = make_float4(h[0], h[1], h[2], h[3]);
+        if (p.hA_hi != nullptr) {
+            const long long idx = (long long)row * p.ldha + u;
+            if (p.ha_bf16) {
+                __align__(8) __nv_bfloat16 hb[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) hb[j] = __float2bfloat16_rn(h[j]);
+                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.hA_hi) + idx) = *reinterpret_cast<const uint2*>(hb);
+            } else {
+                __align__(8) __half hh[4], hl[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) split_f16(h[j], hh[j], hl[j]);
+                *reinterpret_cast<uint2*>(p.hA_hi + idx) = *reinterpret_cast<const uint2*>(hh);
+                *reinterpret_cast<uint2*>(p.hA_lo + idx) = *reinterpret_cast<const uint2*>(hl);
+            }
+        }
+    }
+}
+
+bool lstm_k0_ok(const LstmArgs& p) {
+    auto al = [](const void* q, int b) { return (reinterpret_cast<uintptr_t>(q) & (uintptr_t)(b - 1)) == 0; };
+    return p.K == 0 && p.H % 4 == 0 && al(p.G, 16) && p.ldc % 4 == 0 && p.ldh % 4 == 0 && al(p.c_out, 16) &&
+           al(p.h_out, 16) && (p.c_prev == nullptr || (p.ldc_prev % 4 == 0 && al(p.c_prev, 16))) &&
+           (p.h_out2 == nullptr || (p.ldh2 % 4 == 0 && al(p.h_out2, 16))) &&
+           (p.hA_hi == nullptr || (p.ldha % 4 == 0 && al(p.hA_hi, 8) && (p.ha_bf16 || al(p.hA_lo, 8))));
+}
+
+bool launch_lstm_k0(const LstmArgs& a0, const LstmArgs* a1, int sms, cudaStream_t s) {
+    if (!lstm_k0_ok(a0) || (a1 && (!lstm_k0_ok(*a1) || a1->M != a0.M || a1->H != a0.H))) return false;
+    const long long n = (long long)a0.M * (a0.H / 4);
+    const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)sms * 8));
+    lstm_cell_k0<<<dim3(gx, a1 ? 2u : 1u), 256, 0, s>>>(a0, a1 ? *a1 : a0);
+    return cudaGetLastError() == cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
 // lstm_step_simt: tile 64 rows x 32 hidden units (x4 gates), 256 threads,
 // K chunks of 32 through shared memory, 4x(2 units x 4 gates) per thread.
 // ---------------------------------------------------------------------------
