@@ -141,9 +141,11 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p["bf16_tflops"], p.get("hbm_gbs"), "measured"
+        # the gate GEMMs run inside a step of tens of ms, back to back under the power
+        # cap: the sustained figure is the one for them (burst kept in the line too)
+        return p.get("bf16_tflops_sustained", p["bf16_tflops"]), p.get("hbm_gbs"), "measured", p["bf16_tflops"]
     except Exception:
-        return 1590.0, 6650.0, "fallback"
+        return 1590.0, 6650.0, "fallback", 1590.0
 
 
 class ClockSampler:
@@ -348,7 +350,7 @@ def run_b200(args):
     gemm_ms, gemm_n, useful = eng.profile()
     each_ms, each_fl, each_ex = eng.profile_launches()
     eng.profile_reset(False)
-    bf16_peak, hbm_peak, peak_kind = peaks()
+    bf16_peak, hbm_peak, peak_kind, bf16_burst = peaks()
     launch_ms = float(each_ms.mean())
     launch_flops = float(each_fl.mean())
     achieved = float(each_fl.sum()) / (float(each_ms.sum()) / 1000.0) / 1e12
@@ -425,7 +427,7 @@ def run_b200(args):
                          "frac": achieved / bf16_peak, "traffic": traffic,
                          "kernel": ("lstm_gemm_tc (gate GEMMs + fused LSTM cell, incl. the context projection), "
                                     "all launches of one step" if args.precision != "fp32" else "lstm_step_simt"),
-                         "peak_kind": f"{peak_kind} bf16 dense (burst)",
+                         "peak_kind": f"{peak_kind} bf16 dense, sustained (MEASURED_PEAKS.json; burst {bf16_burst:g})",
                          "algorithmic": "reference formula (SURVEY 8(d)) FLOPs / summed launch time",
                          "useful_flops_per_launch": launch_flops, "launch_ms": launch_ms,
                          "launches_averaged": int(len(each_ms)),

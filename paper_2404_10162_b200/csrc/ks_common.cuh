@@ -94,6 +94,7 @@ struct LstmArgs {
     // 64*kb_alpha columns hold each row's alpha_t at 7 * (config - b0) + t
     int kb_alpha;
     int rows_per_cfg;
+    int alpha_tile;        // rows of the alpha-block layout tile: 128, or 256 for CTA-pair GEMMs
     const __half* PT_hi;   // P^T planes [4H][ldpt]
     const __half* PT_lo;
     long long ldpt;
@@ -125,6 +126,7 @@ struct AttnArgs {
     // alpha operand (kalpha columns, alpha_t at 7 * (config - b0(tile)) + t) and
     // h_prev after it; operand row stride kalpha + NS.  Classic: [ctx ; h_prev].
     int kalpha;
+    int alpha_tile;        // rows of the GEMM tile the alpha block is laid out for (128 / 256)
     int alpha_sparse;      // alpha-block layout unchanged since the last position: write the 7 values only
 };
 

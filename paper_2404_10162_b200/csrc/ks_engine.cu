@@ -43,7 +43,7 @@ bool launch_split_rows(const float* src, long long n, __half* hi, __half* lo, in
 // tensor-core gate GEMM (ks_gemm_tc.cu); returns false when the shape is not supported
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
                     const __half* W_lo0, const __half* W_hi1, const __half* W_lo1,
-                    cudaStream_t stream, int* launches, int units);
+                    cudaStream_t stream, int* launches, int units, bool pair);
 }  // namespace ksb
 
 using namespace ksb;
@@ -184,16 +184,21 @@ struct ks_engine {
     bool ctxproj = false;
     bool ctxproj_force = false;   // KS_CTXPROJ=force: alpha blocks even where wider than ctx (tests)
     DevMem Pt, actA;
+    // KS_TC_PAIR=1: gate GEMMs on CTA pairs (M = 256 tiles, tcgen05 cta_group::2)
+    bool pair = false;
+    int tile_rows() const { return pair ? 256 : 128; }
     bool proj_at(int pos, int H) const {
         return ctxproj && pos > 0 && (ctxproj_force || alpha_cols_of(H) < 2 * NA);
     }
-    static int alpha_cols_of(int H) { return (7 * (127 / H + 2) + 7 + kTcBK - 1) / kTcBK * kTcBK; }
+    int alpha_cols_of(int H) const {
+        return (7 * ((tile_rows() - 1) / H + 2) + 7 + kTcBK - 1) / kTcBK * kTcBK;
+    }
 };
 
-// Columns of the alpha block for rows_per_cfg rows per config: a 128-row tile
-// spans at most 127 / H + 2 configs, 7 columns each, plus up to 7 columns of
-// 8-alignment of the first (tile_k, ks_gemm_tc.cu), rounded to the K-block.
-static int alpha_cols(int H) { return ks_engine::alpha_cols_of(H); }
+// Columns of the alpha block for rows_per_cfg rows per config: a TR-row tile
+// (128, or 256 for CTA pairs) spans at most (TR - 1) / H + 2 configs, 7 columns
+// each, plus up to 7 columns of 8-alignment of the first (tile_k,
+// ks_gemm_tc.cu), rounded to the K-block.
 
 namespace {
 
@@ -502,6 +507,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.ctxproj = (E.variant == KS_VARIANT_ATTN || E.variant == KS_VARIANT_ATTN2) &&
                     E.precision != KS_PREC_FP32 && !(cp && cp[0] == '0');
         E.ctxproj_force = cp && std::string(cp) == "force";
+        const char* tp = std::getenv("KS_TC_PAIR");
+        E.pair = tp && tp[0] == '1' && E.tc_units == 64;
     }
     cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device);
     *out = eng.release();
@@ -701,7 +708,7 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
         if (E.precision == KS_PREC_FP32) {
             ENS(E.Abuf, R * Kd * 4);
         } else {
-            const int64_t lda = E.ctxproj ? std::max<int64_t>(Kd, alpha_cols(1) + Hd) : Kd;
+            const int64_t lda = E.ctxproj ? std::max<int64_t>(Kd, E.alpha_cols_of(1) + Hd) : Kd;
             ENS(E.Ahi, R * lda * 2);
             ENS(E.Alo, R * lda * 2);
         }
@@ -743,7 +750,7 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
     if (E.precision != KS_PREC_FP32 && a0.K > 0) {
         done = launch_lstm_tc(a0, a1, E.precision, L0.Whi.as<__half>(), L0.Wlo.as<__half>(),
                               L1 ? L1->Whi.as<__half>() : nullptr, L1 ? L1->Wlo.as<__half>() : nullptr,
-                              E.stream, &n, E.tc_units);
+                              E.stream, &n, E.tc_units, E.pair);
         if (!done) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
     }
     if (!done && a0.K == 0 && launch_lstm_k0(a0, a1, E.num_sms, E.stream)) {
@@ -768,11 +775,12 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
             double rowk = (double)a.M * a.K;
             if (a.kb_alpha > 0) {
                 rowk = 0.0;
-                for (int mt = 0; mt * 128 < a.M; ++mt) {
-                    const int b0 = mt * 128 / a.rows_per_cfg, b1 = (mt * 128 + 127) / a.rows_per_cfg;
+                const int TR = a.alpha_tile;
+                for (int mt = 0; mt * TR < a.M; ++mt) {
+                    const int b0 = mt * TR / a.rows_per_cfg, b1 = (mt * TR + TR - 1) / a.rows_per_cfg;
                     const int x0 = (7 * b0) & ~7;
                     const int kba = std::min(a.kb_alpha, (7 * (b1 + 1) - x0 + kTcBK - 1) / kTcBK);
-                    const int rows = std::min(128, a.M - mt * 128);
+                    const int rows = std::min(TR, a.M - mt * TR);
                     rowk += (double)rows * (a.K - (double)kTcBK * (a.kb_alpha - kba));
                 }
             }
@@ -1097,7 +1105,8 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         aa.A_hi = E.Ahi.as<__half>();
         aa.A_lo = E.Alo.as<__half>();
         aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
-        aa.kalpha = E.proj_at(pos, H) ? alpha_cols(H) : 0;
+        aa.kalpha = E.proj_at(pos, H) ? E.alpha_cols_of(H) : 0;
+        aa.alpha_tile = E.tile_rows();
         // same rows and layout as the previous alpha-block position: its zeros are still in place
         aa.alpha_sparse = (aa.kalpha && alpha_fill_H == H) ? 1 : 0;
         alpha_fill_H = aa.kalpha ? H : -1;
@@ -1145,13 +1154,14 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.wcol = 0;
         } else if (E.proj_at(pos, H)) {
             // [alpha block | h_prev] . [P^T | W_h]  (ctx . W_ctx = sum_t alpha_t P_t)
-            const int kal = alpha_cols(H);
+            const int kal = E.alpha_cols_of(H);
             p.K = kal + Hd;
             p.ldah = 0;
             p.ldw = Kd;
             p.wcol = NA2;
             p.kb_alpha = kal / kTcBK;
             p.rows_per_cfg = H;
+            p.alpha_tile = E.tile_rows();
             p.PT_hi = E.Pt.as<__half>();
             p.ldpt = (C * 7 + 7) / 8 * 8;
             p.PT_lo = p.PT_hi + (size_t)4 * Hd * p.ldpt;

@@ -66,6 +66,28 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
         : "memory");
 }
+// CTA-pair form: the completion goes to the LEADER CTA's barrier (the pair's
+// shared::cluster addresses differ in bit 24; clearing it names rank 0's copy).
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(bar), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -85,6 +107,21 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// pair commit: arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"((unsigned short)3)
+        : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile(
@@ -130,11 +167,13 @@ struct TileK {
     int x0;     // first P^T column
     int nkb;    // total K-blocks of the tile
 };
+// mt indexes alpha tiles of TR rows (128, or 256 = one CTA pair)
+template <int TR>
 __device__ __forceinline__ TileK tile_k(const LstmArgs& p, int k_blocks, int mt) {
     TileK r{0, 0, k_blocks};
     if (p.kb_alpha > 0) {
-        const int b0 = (mt * 128) / p.rows_per_cfg;
-        const int b1 = (mt * 128 + 127) / p.rows_per_cfg;
+        const int b0 = (mt * TR) / p.rows_per_cfg;
+        const int b1 = (mt * TR + TR - 1) / p.rows_per_cfg;
         r.x0 = (7 * b0) & ~7;
         r.kba_t = (7 * (b1 + 1) - r.x0 + kTcBK - 1) / kTcBK;
         if (r.kba_t > p.kb_alpha) r.kba_t = p.kb_alpha;
@@ -152,12 +191,16 @@ struct TcParams {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = kTcBK;
 
-template <int UNITS, bool SPLIT>
+// CG = 2: a CTA pair (cluster of 2 on one TPC) runs M = 256 MMAs with
+// tcgen05.mma.cta_group::2: each CTA holds its 128 A rows and HALF of the B tile
+// (BN/2 gate rows), so per-SM shared-memory operand traffic drops by a third;
+// only the leader CTA issues MMAs.
+template <int UNITS, bool SPLIT, int CG = 1>
 struct TcCfg {
     static constexpr int BN = 4 * UNITS;                       // gate columns per tile
     static constexpr int PLANES = SPLIT ? 2 : 1;
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;          // one plane
-    static constexpr int B_BYTES = BN * TC_BK * 2;
+    static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;      // this CTA's share of one plane
     static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
     static constexpr int ACC_COLS = BN;                        // fp32 TMEM columns per accumulator
     static constexpr int ACC_STAGES = 512 / ACC_COLS >= 2 ? 2 : 1;
@@ -166,7 +209,7 @@ struct TcCfg {
     // instruction descriptor: fp32 accumulate (bits 4-5 = 1), A/B fp16 (0) or bf16 (1) at
     // bits 7-9 / 10-12, both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
     static constexpr uint32_t IDESC = (1u << 4) | ((SPLIT ? 0u : 1u) << 7) | ((SPLIT ? 0u : 1u) << 10) |
-                                      ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+                                      ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((CG * TC_BM) >> 4) << 24);
 };
 
 // Cell nonlinearities with MUFU exp2 + fast reciprocal: absolute error ~1e-7,
@@ -174,15 +217,19 @@ struct TcCfg {
 __device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float tanh_fast(float x) { return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x)); }
 
-template <int UNITS, bool SPLIT>
+template <int UNITS, bool SPLIT, int CG>
 __global__ void __launch_bounds__(384, 1)
     lstm_gemm_tc(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap mA0,
                  const __grid_constant__ CUtensorMap mAl0, const __grid_constant__ CUtensorMap mB0,
                  const __grid_constant__ CUtensorMap mBl0, const __grid_constant__ CUtensorMap mA1,
                  const __grid_constant__ CUtensorMap mAl1, const __grid_constant__ CUtensorMap mB1,
                  const __grid_constant__ CUtensorMap mBl1) {
-    using Cfg = TcCfg<UNITS, SPLIT>;
+    using Cfg = TcCfg<UNITS, SPLIT, CG>;
     constexpr int S = Cfg::STAGES;
+    constexpr int TR = CG * TC_BM;  // rows per (pair) tile
+    const int rank = CG == 2 ? (int)tc::cluster_rank() : 0;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
     constexpr int AS = Cfg::ACC_STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -199,7 +246,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int a = 0; a < AS; ++a) {
             tc::mbar_init(tc::smem_u32(&bars[2 * S + a]), 1);
-            tc::mbar_init(tc::smem_u32(&bars[2 * S + AS + a]), 8);  // one arrive per epilogue warp
+            tc::mbar_init(tc::smem_u32(&bars[2 * S + AS + a]), 8 * CG);  // one arrive per epilogue warp (of the pair)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -212,13 +259,21 @@ __global__ void __launch_bounds__(384, 1)
         }
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         tc::smem_u32(tmem_slot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             tc::smem_u32(tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             tc::smem_u32(tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc::fence_before();
     __syncthreads();
+    if (CG == 2) tc::cluster_sync();  // the peer's barriers are initialised before any remote arrive
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -227,22 +282,25 @@ __global__ void __launch_bounds__(384, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+            for (int t = cid; t < P.total_tiles; t += ncl) {
                 const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
                 const TcProblem& pr = P.prob[pi];
                 const int lt = t - pr.tile_begin;
-                const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
+                const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;  // mt: (pair) tile
+                const int arow = (mt * CG + rank) * TC_BM;                    // this CTA's A rows
+                const int brow = nt * Cfg::BN + rank * (Cfg::BN / CG);       // this CTA's B rows
                 const CUtensorMap* ma = pi ? &mA1 : &mA0;
                 const CUtensorMap* mal = pi ? &mAl1 : &mAl0;
                 const CUtensorMap* mb = pi ? &mB1 : &mB0;
                 const CUtensorMap* mbl = pi ? &mBl1 : &mBl0;
                 // alpha-block mode: B K-blocks [0, kba_t) come from P^T (held in the
                 // second problem's map slots) from column x0 on (see tile_k)
-                const TileK tk = tile_k(pr.p, pr.k_blocks, mt);
+                const TileK tk = tile_k<TR>(pr.p, pr.k_blocks, mt);
                 for (int kb = 0; kb < tk.nkb; ++kb) {
                     tc::mbar_wait(tc::smem_u32(&bars[S + stage]), phase ^ 1);
                     const uint32_t full = tc::smem_u32(&bars[stage]);
-                    tc::mbar_expect_tx(full, Cfg::STAGE_BYTES);
+                    // pair: the leader's barrier counts both CTAs' bytes
+                    if (leader) tc::mbar_expect_tx(full, CG * Cfg::STAGE_BYTES);
                     unsigned char* st = smem + stage * Cfg::STAGE_BYTES;
                     const bool from_pt = kb < tk.kba_t;
                     // A: alpha blocks [0, kba_t), then the h columns after all kb_alpha blocks
@@ -250,13 +308,17 @@ __global__ void __launch_bounds__(384, 1)
                     const CUtensorMap* bmap = from_pt ? &mB1 : mb;
                     const CUtensorMap* blmap = from_pt ? &mBl1 : mbl;
                     const int bx = from_pt ? tk.x0 + kb * TC_BK : (kb - tk.kba_t) * TC_BK;
-                    tc::tma_load_2d(tc::smem_u32(st), ma, full, kx, mt * TC_BM);
-                    tc::tma_load_2d(tc::smem_u32(st + Cfg::A_BYTES), bmap, full, bx, nt * Cfg::BN);
+                    auto load = [&](uint32_t dst, const CUtensorMap* m, int x, int y) {
+                        if (CG == 2)
+                            tc::tma_load_2d_pair(dst, m, full, x, y);
+                        else
+                            tc::tma_load_2d(dst, m, full, x, y);
+                    };
+                    load(tc::smem_u32(st), ma, kx, arow);
+                    load(tc::smem_u32(st + Cfg::A_BYTES), bmap, bx, brow);
                     if (SPLIT) {
-                        tc::tma_load_2d(tc::smem_u32(st + Cfg::A_BYTES + Cfg::B_BYTES), mal, full, kx,
-                                        mt * TC_BM);
-                        tc::tma_load_2d(tc::smem_u32(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES), blmap, full,
-                                        bx, nt * Cfg::BN);
+                        load(tc::smem_u32(st + Cfg::A_BYTES + Cfg::B_BYTES), mal, kx, arow);
+                        load(tc::smem_u32(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES), blmap, bx, brow);
                     }
                     if (++stage == S) {
                         stage = 0;
@@ -267,16 +329,16 @@ __global__ void __launch_bounds__(384, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        if (lane == 0 && leader) {
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+            for (int t = cid; t < P.total_tiles; t += ncl) {
                 const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
                 const TcProblem& pr = P.prob[pi];
                 const int mt_i = (t - pr.tile_begin) / pr.n_tiles;
-                const int nkb = tile_k(pr.p, pr.k_blocks, mt_i).nkb;
+                const int nkb = tile_k<TR>(pr.p, pr.k_blocks, mt_i).nkb;
                 tc::mbar_wait(tc::smem_u32(&bars[2 * S + AS + acc]), acc_phase ^ 1);
                 tc::fence_after();
                 const uint32_t d1 = tmem_base + acc * Cfg::ACC_COLS;
@@ -291,22 +353,31 @@ __global__ void __launch_bounds__(384, 1)
                     for (int k = 0; k < TC_BK / 16; ++k) {
                         const uint32_t acc_flag = (kb > 0 || k > 0) ? 1u : 0u;
                         const uint32_t koff = k * 32;  // 16 fp16 = 32 bytes along the swizzled row
-                        tc::mma_f16(d1, tc::smem_desc(a0 + koff), tc::smem_desc(b0 + koff), Cfg::IDESC,
-                                    acc_flag);
+                        auto mma = [&](uint32_t a, uint32_t b, uint32_t f) {
+                            if (CG == 2)
+                                tc::mma_f16_pair(d1, tc::smem_desc(a), tc::smem_desc(b), Cfg::IDESC, f);
+                            else
+                                tc::mma_f16(d1, tc::smem_desc(a), tc::smem_desc(b), Cfg::IDESC, f);
+                        };
+                        mma(a0 + koff, b0 + koff, acc_flag);
                         if (SPLIT) {
-                            tc::mma_f16(d1, tc::smem_desc(a0 + koff), tc::smem_desc(bl + koff),
-                                        Cfg::IDESC, 1u);
-                            tc::mma_f16(d1, tc::smem_desc(al + koff), tc::smem_desc(b0 + koff),
-                                        Cfg::IDESC, 1u);
+                            mma(a0 + koff, bl + koff, 1u);
+                            mma(al + koff, b0 + koff, 1u);
                         }
                     }
-                    tc::mma_commit(tc::smem_u32(&bars[S + stage]));  // frees the smem stage
+                    if (CG == 2)  // frees the smem stage (in both CTAs)
+                        tc::mma_commit_pair(tc::smem_u32(&bars[S + stage]));
+                    else
+                        tc::mma_commit(tc::smem_u32(&bars[S + stage]));
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc::mma_commit(tc::smem_u32(&bars[2 * S + acc]));  // accumulator ready
+                if (CG == 2)  // accumulator ready (both CTAs' epilogues)
+                    tc::mma_commit_pair(tc::smem_u32(&bars[2 * S + acc]));
+                else
+                    tc::mma_commit(tc::smem_u32(&bars[2 * S + acc]));
                 if (++acc == AS) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -322,13 +393,13 @@ __global__ void __launch_bounds__(384, 1)
         constexpr int HU = UNITS / 2;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+        for (int t = cid; t < P.total_tiles; t += ncl) {
             const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
             const TcProblem& pr = P.prob[pi];
             const LstmArgs& p = pr.p;
             const int lt = t - pr.tile_begin;
             const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
-            const int row = mt * TC_BM + q * 32 + lane;
+            const int row = (mt * CG + rank) * TC_BM + q * 32 + lane;
             const bool valid = row < p.M;
             const bool raw = p.raw != 0;
             // per-row gathers issued before waiting on the accumulator
@@ -376,7 +447,12 @@ __global__ void __launch_bounds__(384, 1)
                 if (c == NCH - 1) {  // this warp's TMEM reads are done: release the accumulator
                     tc::fence_before();
                     __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&bars[2 * S + AS + acc]));
+                    if (lane == 0) {
+                        if (CG == 2 && !leader)
+                            tc::mbar_arrive_remote(tc::smem_u32(&bars[2 * S + AS + acc]), 0);
+                        else
+                            tc::mbar_arrive(tc::smem_u32(&bars[2 * S + AS + acc]));
+                    }
                 }
                 float gb[4][8], cp[8];
 #pragma unroll
@@ -456,9 +532,13 @@ __global__ void __launch_bounds__(384, 1)
         }
     }
     __syncthreads();
+    if (CG == 2) tc::cluster_sync();  // no CTA leaves while its peer may still signal it
     if (warp == 2) {
         tc::fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
 }
 
@@ -508,17 +588,21 @@ int sm_count() {
     return n;
 }
 
-template <int UNITS, bool SPLIT>
+template <int UNITS, bool SPLIT, int CG>
 bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, const __half* Wl0,
                  const __half* Wh1, const __half* Wl1, cudaStream_t stream) {
-    using Cfg = TcCfg<UNITS, SPLIT>;
+    using Cfg = TcCfg<UNITS, SPLIT, CG>;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::SMEM) != cudaSuccess)
+            return false;
+        if (CG == 2 && cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT, CG>,
+                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
             return false;
         attr = true;
     }
+    constexpr int BROWS = Cfg::BN / CG;  // B rows each CTA loads
     TcParams P{};
     CUtensorMap maps[8];
     const LstmArgs* args[2] = {&a0, a1};
@@ -531,7 +615,8 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         if (a.K % TC_BK != 0 || a.H % UNITS != 0) return false;
         TcProblem& pr = P.prob[i];
         pr.p = a;
-        pr.m_tiles = (a.M + TC_BM - 1) / TC_BM;
+        pr.m_tiles = ((a.M + TC_BM - 1) / TC_BM + CG - 1) / CG;  // (pair) tiles
+        if (a.kb_alpha > 0 && a.alpha_tile != CG * TC_BM) return false;  // operand laid out for another tile
         pr.n_tiles = a.H / UNITS;
         pr.k_blocks = a.K / TC_BK;
         pr.tile_begin = tiles;
@@ -545,25 +630,42 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         const long long kw = a.K - (long long)a.kb_alpha * TC_BK;
         const __half* w0 = wh[i] + a.wcol;
         const __half* w1 = (SPLIT ? wl[i] : wh[i]) + a.wcol;
-        if (!make_map(&maps[4 * i + 2], w0, 4LL * a.H, kw, ldw, Cfg::BN)) return false;
-        if (!make_map(&maps[4 * i + 3], w1, 4LL * a.H, kw, ldw, Cfg::BN)) return false;
+        if (!make_map(&maps[4 * i + 2], w0, 4LL * a.H, kw, ldw, BROWS)) return false;
+        if (!make_map(&maps[4 * i + 3], w1, 4LL * a.H, kw, ldw, BROWS)) return false;
     }
     if (P.n_prob == 1) {
         for (int j = 4; j < 8; ++j) maps[j] = maps[j - 4];
         if (a0.kb_alpha > 0) {  // P^T planes in the second problem's B slots
             if (a0.kb_alpha * TC_BK > a0.K) return false;
-            if (!make_map(&maps[6], a0.PT_hi, 4LL * a0.H, a0.pt_rows, a0.ldpt, Cfg::BN)) return false;
-            if (!make_map(&maps[7], SPLIT ? a0.PT_lo : a0.PT_hi, 4LL * a0.H, a0.pt_rows, a0.ldpt, Cfg::BN))
+            if (!make_map(&maps[6], a0.PT_hi, 4LL * a0.H, a0.pt_rows, a0.ldpt, BROWS)) return false;
+            if (!make_map(&maps[7], SPLIT ? a0.PT_lo : a0.PT_hi, 4LL * a0.H, a0.pt_rows, a0.ldpt, BROWS))
                 return false;
         }
     } else if (a0.kb_alpha > 0 || (a1 && a1->kb_alpha > 0)) {
         return false;
     }
     P.total_tiles = tiles;
-    const int grid = tiles < sm_count() ? tiles : sm_count();
-    lstm_gemm_tc<UNITS, SPLIT><<<grid, 384, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3], maps[4],
-                                                                 maps[5], maps[6], maps[7]);
-    return cudaGetLastError() == cudaSuccess;
+    const int units = sm_count() / CG;  // persistent: one CTA (pair) per SM (pair)
+    const int grid = CG * (tiles < units ? tiles : units);
+    if (CG == 1) {
+        lstm_gemm_tc<UNITS, SPLIT, CG><<<grid, 384, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3],
+                                                                          maps[4], maps[5], maps[6], maps[7]);
+        return cudaGetLastError() == cudaSuccess;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr_c[1];
+    attr_c[0].id = cudaLaunchAttributeClusterDimension;
+    attr_c[0].val.clusterDim.x = 2;
+    attr_c[0].val.clusterDim.y = 1;
+    attr_c[0].val.clusterDim.z = 1;
+    cfg.attrs = attr_c;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, lstm_gemm_tc<UNITS, SPLIT, CG>, P, maps[0], maps[1], maps[2], maps[3], maps[4],
+                              maps[5], maps[6], maps[7]) == cudaSuccess;
 }
 
 }  // namespace
@@ -572,14 +674,17 @@ int tc_units_default() { return 32; }
 
 bool launch_lstm_tc(const LstmArgs& a0, const LstmArgs* a1, int mode, const __half* W_hi0,
                     const __half* W_lo0, const __half* W_hi1, const __half* W_lo1, cudaStream_t stream,
-                    int* launches, int units) {
+                    int* launches, int units, bool pair) {
     bool ok;
-    if (mode == 0)
-        ok = units == 64 ? launch_impl<64, true>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream)
-                         : launch_impl<32, true>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream);
+    if (pair && units == 64)
+        ok = mode == 0 ? launch_impl<64, true, 2>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream)
+                       : launch_impl<64, false, 2>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream);
+    else if (mode == 0)
+        ok = units == 64 ? launch_impl<64, true, 1>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream)
+                         : launch_impl<32, true, 1>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream);
     else
-        ok = units == 64 ? launch_impl<64, false>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream)
-                         : launch_impl<32, false>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream);
+        ok = units == 64 ? launch_impl<64, false, 1>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream)
+                         : launch_impl<32, false, 1>(a0, a1, W_hi0, W_lo0, W_hi1, W_lo1, stream);
     if (ok && launches) *launches = 1;
     return ok;
 }

@@ -260,7 +260,7 @@ template <int SPLIT>
 __device__ __forceinline__ void write_alpha_block(const AttnArgs& p, int r, int b, const float (&al)[kTin],
                                                   int lane) {
     // column of alpha_0 = 7 * b - x0, x0 = 7 * b0 rounded down to 8 (see tile_k, ks_gemm_tc.cu)
-    const int b0 = ((r >> 7) << 7) / p.H_rows;
+    const int b0 = (r / p.alpha_tile * p.alpha_tile) / p.H_rows;
     const int c0 = kTin * b - ((kTin * b0) & ~7);
     const long long base = (long long)r * (p.kalpha + p.NS);
     if (p.alpha_sparse) {  // the previous position left this layout's zeros in place
