@@ -201,6 +201,22 @@ def test_projected_context_modes(stem, mode, monkeypatch):
         assert not bad, f"k={k}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
 
 
+@pytest.mark.parametrize("ctxproj", ["1", "force"])
+@pytest.mark.parametrize("stem", ["attn_small_trained", "tiny_attn_s3423", "tiny_attn2_s3423", "tiny_encdec_s3423"])
+def test_cta_pair_gemm(stem, ctxproj, monkeypatch):
+    """KS_TC_PAIR=1: every gate GEMM on CTA pairs (tcgen05.mma.cta_group::2,
+    M = 256 tiles, alpha blocks laid out for 256-row tiles) meets the same bar."""
+    monkeypatch.setenv("KS_TC_PAIR", "1")
+    monkeypatch.setenv("KS_CTXPROJ", ctxproj)
+    path = golden_path(stem + ".ckpt")
+    o, e = OracleModel(path), engine(path, "f16x3")
+    tok = random_tokens(o, 700, 23)
+    for k in (1, 5, 16):
+        a, g = o.beam(tok, k, threads=8), e.beam(tok, k)
+        n, ties, bad = compare_beams(g, a)
+        assert not bad, f"k={k}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
 @pytest.mark.parametrize("precision", PRECISIONS)
 def test_paper_beam_width_100(precision):
     """OPCS-BS at the paper's k = 100 (Table IV): wide candidate sets
