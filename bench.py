@@ -167,6 +167,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the sampler is live (first row in) before the timed region starts, so even a
+            # region shorter than the 100 ms period is bracketed by samples
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
         return self
@@ -177,6 +182,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            n, t0 = len(self.rows), time.perf_counter()
+            while len(self.rows) == n and time.perf_counter() - t0 < 0.3:  # one sample after the region
+                time.sleep(0.005)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)

@@ -15,6 +15,7 @@
 // H_0 = 1, H_{p+1} = min(k, H_p * V_p)), so the GEMM M dimension carries no
 // padding beyond the reference's own live counts in the unconstrained case.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
@@ -243,6 +244,16 @@ __device__ __forceinline__ void store_split_h(const LstmArgs& p, long long idx, 
         p.hA_hi[idx] = hi;
         p.hA_lo[idx] = lo;
     }
+}
+
+// Function attributes (cudaFuncSetAttribute) are per device: `mask` records the
+// devices a launcher has configured; returns true the first time for the current
+// device (setting an attribute twice from racing threads is harmless).
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    return (mask.fetch_or(bit) & bit) == 0;
 }
 
 }  // namespace ksb

@@ -579,12 +579,9 @@ bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, 
 }
 
 int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int n = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
 }
 
@@ -592,15 +589,11 @@ template <int UNITS, bool SPLIT, int CG>
 bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, const __half* Wl0,
                  const __half* Wh1, const __half* Wl1, cudaStream_t stream) {
     using Cfg = TcCfg<UNITS, SPLIT, CG>;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         if (cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::SMEM) != cudaSuccess)
             return false;
-        if (CG == 2 && cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT, CG>,
-                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
-            return false;
-        attr = true;
     }
     constexpr int BROWS = Cfg::BN / CG;  // B rows each CTA loads
     TcParams P{};

@@ -1168,13 +1168,12 @@ size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tabl
 template <int SPLIT>
 bool launch_beam_split(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
     const int V = m.vsize[a.pos];
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(beam_step_t<4, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(beam_step_t<8, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(beam_step_t<16, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(beam_step_t<32, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
     }
     auto kern = V <= 4 ? beam_step_t<4, SPLIT> : V <= 8 ? beam_step_t<8, SPLIT>
               : V <= 16 ? beam_step_t<16, SPLIT> : beam_step_t<32, SPLIT>;
@@ -1301,11 +1300,8 @@ bool launch_hybrid_pack(const HybPackArgs& p, cudaStream_t s) {
 bool launch_hybrid_conv(const ConvArgs& p, cudaStream_t s) {
     const size_t smem = (size_t)4 * 2 * p.scratch_floats * sizeof(float);
     if (smem > 200 * 1024) return false;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(hybrid_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) cudaFuncSetAttribute(hybrid_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     hybrid_conv<<<(unsigned)((p.C + 3) / 4), 128, smem, s>>>(p);
     return cudaGetLastError() == cudaSuccess;
 }

@@ -15,7 +15,7 @@ want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "lts__t_bytes.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-        "launch__grid_size", "launch__block_size"]
+        "launch__grid_size", "launch__block_size", "sm__cycles_elapsed.avg.per_second"]
 for r in rows[2:]:
     print("==", r[hdr.index("Kernel Name")][:70])
     for w in want:
