@@ -186,13 +186,28 @@ struct ks_engine {
     DevMem Pt, actA;
     // KS_TC_PAIR=1: gate GEMMs on CTA pairs (M = 256 tiles, tcgen05 cta_group::2)
     bool pair = false;
-    int tile_rows() const { return pair ? 256 : 128; }
     bool proj_at(int pos, int H) const {
         return ctxproj && pos > 0 && (ctxproj_force || alpha_cols_of(H) < 2 * NA);
     }
-    int alpha_cols_of(int H) const {
-        return (7 * ((tile_rows() - 1) / H + 2) + 7 + kTcBK - 1) / kTcBK * kTcBK;
+    // Alpha-block columns for TR-row tiles of H rows per config: TR % H == 0 ->
+    // every tile holds TR / H whole configs; otherwise up to (TR - 1) / H + 2
+    // (partial configs at both ends); 7 columns each, plus up to 7 columns of
+    // 8-alignment of the first (tile_k, ks_gemm_tc.cu), rounded to the K-block.
+    static int alpha_cols_for(int TR, int H) {
+        const int cfgs = TR % H == 0 ? TR / H : (TR - 1) / H + 2;
+        return (7 * cfgs + 7 + kTcBK - 1) / kTcBK * kTcBK;
     }
+    // Rows per alpha-block GEMM tile: a CTA pair's 256, else 128 or the largest
+    // multiple of H below it (config-aligned: e.g. 125 rows = 25 configs at beam 5
+    // need 3 alpha K-blocks instead of 4), whichever contracts fewer columns per row.
+    int alpha_tile_of(int H) const {
+        if (pair) return 256;
+        const int ra = H <= 128 ? 128 / H * H : 128;
+        const double plain = (NS + alpha_cols_for(128, H)) / 128.0;
+        const double aligned = (NS + alpha_cols_for(ra, H)) / (double)ra;
+        return aligned < plain ? ra : 128;
+    }
+    int alpha_cols_of(int H) const { return alpha_cols_for(alpha_tile_of(H), H); }
 };
 
 // Columns of the alpha block for rows_per_cfg rows per config: a TR-row tile
@@ -1106,7 +1121,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         aa.A_lo = E.Alo.as<__half>();
         aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
         aa.kalpha = E.proj_at(pos, H) ? E.alpha_cols_of(H) : 0;
-        aa.alpha_tile = E.tile_rows();
+        aa.alpha_tile = E.alpha_tile_of(H);
         // same rows and layout as the previous alpha-block position: its zeros are still in place
         aa.alpha_sparse = (aa.kalpha && alpha_fill_H == H) ? 1 : 0;
         alpha_fill_H = aa.kalpha ? H : -1;
@@ -1161,7 +1176,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.wcol = NA2;
             p.kb_alpha = kal / kTcBK;
             p.rows_per_cfg = H;
-            p.alpha_tile = E.tile_rows();
+            p.alpha_tile = E.alpha_tile_of(H);
             p.PT_hi = E.Pt.as<__half>();
             p.ldpt = (C * 7 + 7) / 8 * 8;
             p.PT_lo = p.PT_hi + (size_t)4 * Hd * p.ldpt;

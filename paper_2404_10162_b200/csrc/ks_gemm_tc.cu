@@ -167,9 +167,9 @@ struct TileK {
     int x0;     // first P^T column
     int nkb;    // total K-blocks of the tile
 };
-// mt indexes alpha tiles of TR rows (128, or 256 = one CTA pair)
-template <int TR>
-__device__ __forceinline__ TileK tile_k(const LstmArgs& p, int k_blocks, int mt) {
+// mt indexes alpha tiles of TR rows (<= 128 -- config-aligned tiles hold whole
+// configs -- or 256 = one CTA pair)
+__device__ __forceinline__ TileK tile_k(const LstmArgs& p, int k_blocks, int mt, int TR) {
     TileK r{0, 0, k_blocks};
     if (p.kb_alpha > 0) {
         const int b0 = (mt * TR) / p.rows_per_cfg;
@@ -226,7 +226,10 @@ __global__ void __launch_bounds__(384, 1)
                  const __grid_constant__ CUtensorMap mBl1) {
     using Cfg = TcCfg<UNITS, SPLIT, CG>;
     constexpr int S = Cfg::STAGES;
-    constexpr int TR = CG * TC_BM;  // rows per (pair) tile
+    // rows per tile of a problem: 128 (a CTA pair: 2 x 128); alpha-block launches on
+    // one CTA may use config-aligned tiles of alpha_tile <= 128 rows (whole configs
+    // per tile: fewer alpha columns)
+    auto tile_rows = [&](const LstmArgs& a) { return (CG == 1 && a.kb_alpha > 0) ? a.alpha_tile : CG * TC_BM; };
     const int rank = CG == 2 ? (int)tc::cluster_rank() : 0;
     const bool leader = rank == 0;
     const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
@@ -287,7 +290,8 @@ __global__ void __launch_bounds__(384, 1)
                 const TcProblem& pr = P.prob[pi];
                 const int lt = t - pr.tile_begin;
                 const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;  // mt: (pair) tile
-                const int arow = (mt * CG + rank) * TC_BM;                    // this CTA's A rows
+                const int TRp = tile_rows(pr.p);
+                const int arow = CG == 1 ? mt * TRp : (mt * CG + rank) * TC_BM;  // this CTA's A rows
                 const int brow = nt * Cfg::BN + rank * (Cfg::BN / CG);       // this CTA's B rows
                 const CUtensorMap* ma = pi ? &mA1 : &mA0;
                 const CUtensorMap* mal = pi ? &mAl1 : &mAl0;
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(384, 1)
                 const CUtensorMap* mbl = pi ? &mBl1 : &mBl0;
                 // alpha-block mode: B K-blocks [0, kba_t) come from P^T (held in the
                 // second problem's map slots) from column x0 on (see tile_k)
-                const TileK tk = tile_k<TR>(pr.p, pr.k_blocks, mt);
+                const TileK tk = tile_k(pr.p, pr.k_blocks, mt, TRp);
                 for (int kb = 0; kb < tk.nkb; ++kb) {
                     tc::mbar_wait(tc::smem_u32(&bars[S + stage]), phase ^ 1);
                     const uint32_t full = tc::smem_u32(&bars[stage]);
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
                 const TcProblem& pr = P.prob[pi];
                 const int mt_i = (t - pr.tile_begin) / pr.n_tiles;
-                const int nkb = tile_k<TR>(pr.p, pr.k_blocks, mt_i).nkb;
+                const int nkb = tile_k(pr.p, pr.k_blocks, mt_i, tile_rows(pr.p)).nkb;
                 tc::mbar_wait(tc::smem_u32(&bars[2 * S + AS + acc]), acc_phase ^ 1);
                 tc::fence_after();
                 const uint32_t d1 = tmem_base + acc * Cfg::ACC_COLS;
@@ -399,8 +403,9 @@ __global__ void __launch_bounds__(384, 1)
             const LstmArgs& p = pr.p;
             const int lt = t - pr.tile_begin;
             const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
-            const int row = (mt * CG + rank) * TC_BM + q * 32 + lane;
-            const bool valid = row < p.M;
+            const int TRp = tile_rows(p);
+            const int row = (CG == 1 ? mt * TRp : (mt * CG + rank) * TC_BM) + q * 32 + lane;
+            const bool valid = row < p.M && (CG == 2 || q * 32 + lane < TRp);
             const bool raw = p.raw != 0;
             // per-row gathers issued before waiting on the accumulator
             const int slot = (valid && !raw) ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0) : 0;
@@ -608,8 +613,10 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         if (a.K % TC_BK != 0 || a.H % UNITS != 0) return false;
         TcProblem& pr = P.prob[i];
         pr.p = a;
-        pr.m_tiles = ((a.M + TC_BM - 1) / TC_BM + CG - 1) / CG;  // (pair) tiles
-        if (a.kb_alpha > 0 && a.alpha_tile != CG * TC_BM) return false;  // operand laid out for another tile
+        if (a.kb_alpha > 0 && (CG == 2 ? a.alpha_tile != 2 * TC_BM : (a.alpha_tile < 1 || a.alpha_tile > TC_BM)))
+            return false;  // operand laid out for another tile
+        const int tr = (CG == 1 && a.kb_alpha > 0) ? a.alpha_tile : TC_BM;
+        pr.m_tiles = ((a.M + tr - 1) / tr + CG - 1) / CG;  // (pair) tiles
         pr.n_tiles = a.H / UNITS;
         pr.k_blocks = a.K / TC_BK;
         pr.tile_begin = tiles;
