@@ -195,13 +195,14 @@ class Engine:
         check(L.ks_engine_create_from_checkpoint(checkpoint.encode(), device, PREC[precision],
                                                  C.byref(h)))
         self._h = h
+        self._destroy = L.ks_engine_destroy  # bound now: module globals may be gone at shutdown
         self.T = L.ks_engine_num_positions(h)
         self.vsizes = [L.ks_engine_vocab_size(h, p) for p in range(self.T)]
         self.precision = precision
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().ks_engine_destroy(self._h)
+            self._destroy(self._h)
             self._h = None
 
     __del__ = close
@@ -287,12 +288,13 @@ class Trainer:
         h = C.c_void_p()
         check(L.ks_trainer_create_from_checkpoint(checkpoint.encode(), device, C.byref(h)))
         self._h = h
+        self._destroy = L.ks_trainer_destroy
         self.num_params = L.ks_trainer_num_params(h)          # train-layout buffers (grads)
         self.num_ref_params = L.ks_trainer_num_ref_params(h)  # reference order (export/import)
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().ks_trainer_destroy(self._h)
+            self._destroy(self._h)
             self._h = None
 
     __del__ = close
