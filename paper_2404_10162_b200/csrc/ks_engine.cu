@@ -124,6 +124,8 @@ struct DevLstm {
     DevMem W;       // FP32: [K][4H] (u*4+g)
     DevMem Whi;     // TC: [4H][K] gate-interleaved per 64-unit tile
     DevMem Wlo;
+    DevMem Whi32;   // the same planes interleaved per 32-unit tile (small batches)
+    DevMem Wlo32;
     DevMem G;       // [slots][4][H]
 };
 
@@ -186,6 +188,10 @@ struct ks_engine {
     DevMem Pt, actA;
     // KS_TC_PAIR=1: gate GEMMs on CTA pairs (M = 256 tiles, tcgen05 cta_group::2)
     bool pair = false;
+    // N-tile width of the current chunk's gate GEMMs: tc_units, or 32 when 64-unit
+    // tiles would leave SMs idle (small batches; needs the 32-unit weight planes)
+    int units_now = 64;
+    bool pair_now() const { return pair && units_now == 64; }
     bool proj_at(int pos, int H) const {
         return ctxproj && pos > 0 && (ctxproj_force || alpha_cols_of(H) < 2 * NA);
     }
@@ -201,7 +207,7 @@ struct ks_engine {
     // multiple of H below it (config-aligned: e.g. 125 rows = 25 configs at beam 5
     // need 3 alpha K-blocks instead of 4), whichever contracts fewer columns per row.
     int alpha_tile_of(int H) const {
-        if (pair) return 256;
+        if (pair_now()) return 256;
         const int ra = H <= 128 ? 128 / H * H : 128;
         const double plain = (NS + alpha_cols_for(128, H)) / 128.0;
         const double aligned = (NS + alpha_cols_for(ra, H)) / (double)ra;
@@ -300,6 +306,21 @@ ks_status pack_lstm(const HostTensors& ht, const std::string& prefix, int rows, 
         if ((e = out.Wlo.ensure(Wlo.size() * 2)) != cudaSuccess) goto fail;
         if ((e = cudaMemcpy(out.Whi.p, Whi.data(), Whi.size() * 2, cudaMemcpyHostToDevice))) goto fail;
         if ((e = cudaMemcpy(out.Wlo.p, Wlo.data(), Wlo.size() * 2, cudaMemcpyHostToDevice))) goto fail;
+        if (units == 64 && Hp % 32 == 0) {
+            // 32-unit interleave: a row permutation of the 64-unit planes
+            std::vector<__half> h32(Whi.size()), l32(Wlo.size());
+            for (int u = 0; u < Hp; ++u)
+                for (int g = 0; g < 4; ++g) {
+                    const size_t n64 = (size_t)(u / 64) * 256 + (size_t)g * 64 + (u % 64);
+                    const size_t n32 = (size_t)(u / 32) * 128 + (size_t)g * 32 + (u % 32);
+                    std::memcpy(&h32[n32 * K], &Whi[n64 * K], (size_t)K * 2);
+                    std::memcpy(&l32[n32 * K], &Wlo[n64 * K], (size_t)K * 2);
+                }
+            if ((e = out.Whi32.ensure(h32.size() * 2)) != cudaSuccess) goto fail;
+            if ((e = out.Wlo32.ensure(l32.size() * 2)) != cudaSuccess) goto fail;
+            if ((e = cudaMemcpy(out.Whi32.p, h32.data(), h32.size() * 2, cudaMemcpyHostToDevice))) goto fail;
+            if ((e = cudaMemcpy(out.Wlo32.p, l32.data(), l32.size() * 2, cudaMemcpyHostToDevice))) goto fail;
+        }
     }
     if ((e = out.G.ensure(G.size() * 4)) != cudaSuccess) goto fail;
     if ((e = cudaMemcpy(out.G.p, G.data(), G.size() * 4, cudaMemcpyHostToDevice))) goto fail;
@@ -763,9 +784,11 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
     int n = 0;
     bool done = false;
     if (E.precision != KS_PREC_FP32 && a0.K > 0) {
-        done = launch_lstm_tc(a0, a1, E.precision, L0.Whi.as<__half>(), L0.Wlo.as<__half>(),
-                              L1 ? L1->Whi.as<__half>() : nullptr, L1 ? L1->Wlo.as<__half>() : nullptr,
-                              E.stream, &n, E.tc_units, E.pair);
+        const bool u32 = E.units_now == 32 && E.tc_units == 64;  // 32-unit planes of 64-unit packings
+        auto whi = [&](DevLstm& L) { return (u32 ? L.Whi32 : L.Whi).as<__half>(); };
+        auto wlo = [&](DevLstm& L) { return (u32 ? L.Wlo32 : L.Wlo).as<__half>(); };
+        done = launch_lstm_tc(a0, a1, E.precision, whi(L0), wlo(L0), L1 ? whi(*L1) : nullptr,
+                              L1 ? wlo(*L1) : nullptr, E.stream, &n, E.units_now, E.pair_now());
         if (!done) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
     }
     if (!done && a0.K == 0 && launch_lstm_k0(a0, a1, E.num_sms, E.stream)) {
@@ -954,6 +977,15 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     if ((st = ensure_workspace(E, C, k))) return st;
     cudaStream_t s = E.stream;
     const bool enc_dec = E.variant == KS_VARIANT_ENC_DEC;
+    {
+        // small batches: 32-unit N tiles double the CTAs of every gate GEMM of the chunk
+        // (the weights, P^T and every launch of a chunk use one tile width)
+        const bool hyb = E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID;
+        const DevLstm& ref = hyb ? E.hb1[0] : E.dec;
+        const int64_t rows = C * (int64_t)std::max(1, k);
+        const int64_t tiles64 = (rows + 127) / 128 * std::max(1, ref.H / 64);
+        E.units_now = (E.tc_units == 64 && ref.Whi32.p != nullptr && tiles64 < E.num_sms) ? 32 : E.tc_units;
+    }
     const bool split = E.precision != KS_PREC_FP32;
     const int He = enc_dec ? E.NE : E.NA;
     const int NA2 = enc_dec ? 0 : 2 * E.NA;
