@@ -582,9 +582,16 @@ def run_train(args):
     fl = train_flops_per_sample(ck)
     achieved = fl * value / 1e12
     # the gate GEMMs run on the TF32 tensor cores as 3 passes of split operands
-    # (fp32-grade); no measured TF32 peak exists for this pool, so the nominal
-    # dense TF32 figure of B200_PROFILING.md is the denominator
-    tf32_peak = 1100.0
+    # (fp32-grade): the denominator is the TF32 rate measured on this pool the way
+    # MEASURED_PEAKS.json measures bf16 (tools/measure_tf32.py, sustained: the
+    # GEMMs run back to back inside the step), else the nominal B200_PROFILING.md figure
+    try:
+        with open(os.path.join(ROOT, "profiles", "measured_tf32.json")) as f:
+            tf32_peak = float(json.load(f)["tf32_tflops_sustained"])
+        tf32_kind = "measured dense TF32, sustained (profiles/measured_tf32.json, tools/measure_tf32.py)"
+    except Exception:
+        tf32_peak = 1100.0
+        tf32_kind = "nominal dense TF32 (B200_PROFILING.md; no measured TF32 peak)"
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -618,7 +625,7 @@ def run_train(args):
                             "frac": achieved / tf32_peak, "traffic": None,
                             "kernel": "whole training step: 3xTF32 gate GEMMs (cuBLASLt, split operands) + fused "
                                       "cell / attention / head / dropout kernels",
-                            "peak_kind": "nominal dense TF32 (B200_PROFILING.md; no measured TF32 peak)",
+                            "peak_kind": tf32_kind,
                             "flops_per_sample": fl, "mma_issued_tflops_upper": 3.0 * achieved},
                "cpu_baseline": cpu, "gpu_launches": launches * args.steps, "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
