@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <atomic>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -80,6 +81,10 @@ namespace {
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
 constexpr int SB_M_HOST = 64;
 
+// bumped on every device (re)allocation: captured decode graphs bake buffer
+// addresses into their kernel parameters and are re-captured when it moves
+std::atomic<unsigned long long> g_alloc_gen{0};
+
 struct DevMem {
     void* p = nullptr;
     size_t bytes = 0;
@@ -88,6 +93,7 @@ struct DevMem {
     }
     cudaError_t ensure(size_t n) {
         if (n <= bytes) return cudaSuccess;
+        g_alloc_gen.fetch_add(1);
         if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
@@ -176,6 +182,22 @@ struct ks_engine {
     DevLstm hb1[2], hb2[2];
     DevMem hybA, hybAf, hybC, hybH, feat;
     std::mutex mu;                // calls share the workspace: one decode at a time per engine
+    // predicate tables last uploaded (identical tables are not re-uploaded; a change
+    // waits for the engine stream so in-flight decodes never see a half-written table)
+    std::vector<unsigned char> pred_blob;
+    // CUDA graphs of whole single-chunk decodes, keyed by everything their kernel
+    // parameters bake in (KS_GRAPHS=0 disables)
+    bool use_graphs = true;
+    struct GraphEntry {
+        std::vector<long long> key;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+    };
+    std::vector<GraphEntry> graphs;
+    ~ks_engine() {
+        for (auto& g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+    }
     bool layered = false;         // hybrid: bi-LSTM 2 runs over bi-LSTM 1's sequence (not seeded)
     DevMem hybH1, hybX2;          // layered: H1 [T][C][2CP] fp32; bi-LSTM 2 operands per dir and step
     int num_sms = 148;
@@ -545,6 +567,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.ctxproj_force = cp && std::string(cp) == "force";
         const char* tp = std::getenv("KS_TC_PAIR");
         E.pair = tp && tp[0] == '1' && E.tc_units == 64;
+        const char* kg = std::getenv("KS_GRAPHS");
+        E.use_graphs = !(kg && kg[0] == '0');
     }
     cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device);
     *out = eng.release();
@@ -701,12 +725,30 @@ ks_status upload_preds(ks_engine& E, const ks_pred* preds, int n, PredDev& pd) {
     pd.n = n;
     pd.n_terms = (int)tpos.size();
     pd.n_bytes = (int)bytes.size();
+    std::vector<unsigned char> blob;
+    auto put = [&](const void* p, size_t nb) {
+        const size_t o = blob.size();
+        blob.resize(o + nb + 8);
+        std::memcpy(blob.data() + o, &nb, 8);
+        if (nb) std::memcpy(blob.data() + o + 8, p, nb);
+    };
+    put(dp.data(), dp.size() * sizeof(DevPred));
+    put(bytes.data(), bytes.size());
+    put(tpos.data(), tpos.size() * 4);
+    put(tw.data(), tw.size() * 8);
+    put(tfield.data(), tfield.size() * 4);
+    if (blob == E.pred_blob && E.preds.p) return KS_OK;  // tables already on the device
+    // the engine stream may still be reading the previous tables (device API calls
+    // return before their kernels finish)
+    KS_CUDA(cudaStreamSynchronize(E.stream));
+    E.pred_blob.clear();
     ks_status st;
     if ((st = upload(E.preds, dp.data(), dp.size() * sizeof(DevPred)))) return st;
     if ((st = upload(E.pbytes, bytes.data(), bytes.size()))) return st;
     if ((st = upload(E.tpos, tpos.data(), tpos.size() * 4))) return st;
     if ((st = upload(E.tw, tw.data(), tw.size() * 8))) return st;
     if ((st = upload(E.tfield, tfield.data(), tfield.size() * 4))) return st;
+    E.pred_blob = std::move(blob);
     return KS_OK;
 }
 
@@ -1318,6 +1360,52 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     return KS_OK;
 }
 
+// run_chunk through a cached CUDA graph: one launch replays the whole decode of a
+// chunk (tens of kernels), removing the per-kernel launch gaps that dominate
+// small batches.  Not used with host predicates (host round trips), profiling
+// (events) or when disabled.
+ks_status run_chunk_graph(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greedy, const int* d_tok,
+                          const long long* d_desc, const PredDev& pd, int* o_tok, double* o_lp, int* o_count,
+                          int* o_status, int* o_fpred, int* o_fstep) {
+    if (!E.use_graphs || E.prof || pd.has_host)
+        return run_chunk(E, C, cfg_base, k, greedy, d_tok, d_desc, pd, o_tok, o_lp, o_count, o_status, o_fpred,
+                         o_fstep);
+    ks_status st;
+    if ((st = ensure_workspace(E, C, k))) return st;  // allocations before the key is taken
+    auto P = [](const void* p) { return (long long)reinterpret_cast<uintptr_t>(p); };
+    const std::vector<long long> key = {C, cfg_base, k, greedy ? 1 : 0, P(d_tok), P(d_desc), pd.n, pd.n_terms,
+                                        pd.n_bytes, pd.needs_desc ? 1 : 0, P(o_tok), P(o_lp), P(o_count),
+                                        P(o_status), P(o_fpred), P(o_fstep),
+                                        (long long)g_alloc_gen.load()};
+    for (auto& g : E.graphs)
+        if (g.key == key) {
+            KS_CUDA(cudaGraphLaunch(g.exec, E.stream));
+            E.launches += g.launches;
+            return KS_OK;
+        }
+    const int64_t l0 = E.launches;
+    KS_CUDA(cudaStreamBeginCapture(E.stream, cudaStreamCaptureModeRelaxed));
+    st = run_chunk(E, C, cfg_base, k, greedy, d_tok, d_desc, pd, o_tok, o_lp, o_count, o_status, o_fpred, o_fstep);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(E.stream, &graph);
+    if (st) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ce != cudaSuccess || !graph) return set_error(KS_ERR_CUDA, std::string("decode graph capture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("decode graph instantiate: ") + cudaGetErrorString(ie));
+    if (E.graphs.size() >= 8) {
+        cudaGraphExecDestroy(E.graphs.front().exec);
+        E.graphs.erase(E.graphs.begin());
+    }
+    E.graphs.push_back({key, exec, E.launches - l0});
+    KS_CUDA(cudaGraphLaunch(exec, E.stream));
+    return KS_OK;
+}
+
 ks_status check_common(ks_engine* eng, int64_t B, int32_t k, const ks_pred* preds, int32_t n) {
     if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
     if (k < 1) return set_error(KS_ERR_PARAMETER, "beam width must be >= 1, got " + std::to_string(k));
@@ -1420,7 +1508,7 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
             KS_CUDA(cudaMemcpyAsync(E.desc.p, hdesc, (size_t)n * 7 * 8, cudaMemcpyHostToDevice, E.stream));
             ddesc = E.desc.as<long long>();
         }
-        if ((st = run_chunk(E, n, c0, k, greedy, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
+        if ((st = run_chunk_graph(E, n, c0, k, greedy, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
                             E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>())))
             return st;
         char* ho = E.h_out.as<char>();
@@ -1585,7 +1673,7 @@ extern "C" ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok,
     const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
     for (int64_t c0 = 0; c0 < B; c0 += C) {
         const int64_t n = std::min<int64_t>(C, B - c0);
-        st = run_chunk(E, n, c0, k, false, d_tok + c0 * 7, d_desc ? reinterpret_cast<const long long*>(d_desc) + c0 * 7 : nullptr,
+        st = run_chunk_graph(E, n, c0, k, false, d_tok + c0 * 7, d_desc ? reinterpret_cast<const long long*>(d_desc) + c0 * 7 : nullptr,
                        pd, d_out_tok + c0 * k * T, d_out_lp + c0 * k, d_out_count + c0,
                        d_out_status ? d_out_status + c0 : nullptr, d_out_fpred ? d_out_fpred + c0 : nullptr,
                        d_out_fstep ? d_out_fstep + c0 : nullptr);

@@ -254,3 +254,25 @@ def test_builtin_kernel_specs(kernel, variant, tmp_path):
     n, ties, bad = compare_beams(g, a)
     assert n >= 0.5 * len(tok), f"only {n} non-tie-adjacent configs"
     assert not bad, f"{len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
+def test_graph_replay_follows_new_inputs_and_predicates(monkeypatch):
+    """Decodes replay a cached CUDA graph per (batch shape, predicate layout,
+    buffers): consecutive calls with new tokens, new budget values (same table
+    layout) and a different beam width must each match the oracle, and match an
+    engine with graphs off (KS_GRAPHS=0) bit for bit."""
+    path = golden_path("attn_small_trained.ckpt")
+    o = OracleModel(path)
+    e = engine(path, "f16x3")
+    monkeypatch.setenv("KS_GRAPHS", "0")
+    e_plain = engine(path, "f16x3")
+    for call, (seed, budget, k) in enumerate([(41, 30.0, 5), (42, 26.0, 5), (43, 30.0, 5), (44, 28.0, 3)]):
+        tok = random_tokens(o, 300, seed)
+        preds = oracle_preds(o, [("membership", None), ("budget", ({n: 1.0 for n in o.names}, budget))])
+        g = e.beam(tok, k, None, preds)
+        p = e_plain.beam(tok, k, None, preds)
+        for key in g:
+            np.testing.assert_array_equal(g[key], p[key], err_msg=f"call {call}: {key}")
+        a = o.beam(tok, k, None, preds, threads=8)
+        n, ties, bad = compare_beams(g, a)
+        assert not bad, f"call {call}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
