@@ -876,7 +876,7 @@ __device__ __forceinline__ int src_lane(int v) {
 }
 
 template <int VP, int SPLIT>
-__global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
+__global__ void __launch_bounds__(256, VP == 32 ? 1 : VP == 16 ? 2 : 3) beam_step_t(BeamArgs a, PosMeta m) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int WS = VP == 4 ? 12 : VP + 4;  // padded W row: conflict-free 128-bit loads
     const int V = m.vsize[a.pos];
@@ -937,15 +937,28 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
             // head logits for rows j0, j0+1: logits[v] = b[v] + sum_i h[i] W[i][v]  (models.cpp:490-491)
             float lg[2] = {0.0f, 0.0f};
             {
-                float p0[VP], p1[VP];
+                // paired fp32 FMAs (FFMA2: two exact fp32 fma.rn per instruction)
+                float2 q0[VP / 2], q1[VP / 2];
 #pragma unroll
-                for (int v = 0; v < VP; ++v) {
-                    p0[v] = 0.0f;
-                    p1[v] = 0.0f;
+                for (int v = 0; v < VP / 2; ++v) {
+                    q0[v] = make_float2(0.0f, 0.0f);
+                    q1[v] = make_float2(0.0f, 0.0f);
                 }
                 // hybrid variants: every hypothesis of config b reads the same feature row
                 const float* h0 = a.h + (a.h_per_config ? (long long)b : r0) * a.NS;
                 const float* h1 = a.h_per_config ? h0 : h0 + a.NS;
+                auto fma_row = [&](float x0, float x1, const float4* w4) {
+                    const float2 X0 = make_float2(x0, x0), X1 = make_float2(x1, x1);
+#pragma unroll
+                    for (int qq = 0; qq < VP / 4; ++qq) {
+                        const float4 w = w4[qq];
+                        const float2 wa = make_float2(w.x, w.y), wb = make_float2(w.z, w.w);
+                        q0[2 * qq] = __ffma2_rn(X0, wa, q0[2 * qq]);
+                        q0[2 * qq + 1] = __ffma2_rn(X0, wb, q0[2 * qq + 1]);
+                        q1[2 * qq] = __ffma2_rn(X1, wa, q1[2 * qq]);
+                        q1[2 * qq + 1] = __ffma2_rn(X1, wb, q1[2 * qq + 1]);
+                    }
+                };
                 if (v4) {
                     // 128-bit loads, both rows' loads in flight together
                     const float4* h04 = reinterpret_cast<const float4*>(h0);
@@ -955,43 +968,24 @@ __global__ void __launch_bounds__(256) beam_step_t(BeamArgs a, PosMeta m) {
                     for (int q = lane; q < NQ; q += 32) {
                         const float4 x0 = live0 ? __ldg(h04 + q) : z4;
                         const float4 x1 = live1 ? __ldg(h14 + q) : z4;
-                        const float xs0[4] = {x0.x, x0.y, x0.z, x0.w};
-                        const float xs1[4] = {x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float4* w4 = reinterpret_cast<const float4*>(Wsh + (e * NQ + q) * WS);
-#pragma unroll
-                            for (int qq = 0; qq < VP / 4; ++qq) {
-                                const float4 w = w4[qq];
-                                p0[4 * qq + 0] = fmaf(xs0[e], w.x, p0[4 * qq + 0]);
-                                p0[4 * qq + 1] = fmaf(xs0[e], w.y, p0[4 * qq + 1]);
-                                p0[4 * qq + 2] = fmaf(xs0[e], w.z, p0[4 * qq + 2]);
-                                p0[4 * qq + 3] = fmaf(xs0[e], w.w, p0[4 * qq + 3]);
-                                p1[4 * qq + 0] = fmaf(xs1[e], w.x, p1[4 * qq + 0]);
-                                p1[4 * qq + 1] = fmaf(xs1[e], w.y, p1[4 * qq + 1]);
-                                p1[4 * qq + 2] = fmaf(xs1[e], w.z, p1[4 * qq + 2]);
-                                p1[4 * qq + 3] = fmaf(xs1[e], w.w, p1[4 * qq + 3]);
-                            }
-                        }
+                        fma_row(x0.x, x1.x, reinterpret_cast<const float4*>(Wsh + (0 * NQ + q) * WS));
+                        fma_row(x0.y, x1.y, reinterpret_cast<const float4*>(Wsh + (1 * NQ + q) * WS));
+                        fma_row(x0.z, x1.z, reinterpret_cast<const float4*>(Wsh + (2 * NQ + q) * WS));
+                        fma_row(x0.w, x1.w, reinterpret_cast<const float4*>(Wsh + (3 * NQ + q) * WS));
                     }
-                } else
+                } else {
 #pragma unroll(VP <= 8 ? 16 : 4)
-                for (int i = lane; i < a.NS; i += 32) {
-                    const float x0 = live0 ? h0[i] : 0.0f;
-                    const float x1 = live1 ? h1[i] : 0.0f;
-                    const float4* w4 = reinterpret_cast<const float4*>(Wsh + i * WS);
+                    for (int i = lane; i < a.NS; i += 32)
+                        fma_row(live0 ? h0[i] : 0.0f, live1 ? h1[i] : 0.0f,
+                                reinterpret_cast<const float4*>(Wsh + i * WS));
+                }
+                float p0[VP], p1[VP];
 #pragma unroll
-                    for (int q = 0; q < VP / 4; ++q) {
-                        const float4 w = w4[q];
-                        p0[4 * q + 0] = fmaf(x0, w.x, p0[4 * q + 0]);
-                        p0[4 * q + 1] = fmaf(x0, w.y, p0[4 * q + 1]);
-                        p0[4 * q + 2] = fmaf(x0, w.z, p0[4 * q + 2]);
-                        p0[4 * q + 3] = fmaf(x0, w.w, p0[4 * q + 3]);
-                        p1[4 * q + 0] = fmaf(x1, w.x, p1[4 * q + 0]);
-                        p1[4 * q + 1] = fmaf(x1, w.y, p1[4 * q + 1]);
-                        p1[4 * q + 2] = fmaf(x1, w.z, p1[4 * q + 2]);
-                        p1[4 * q + 3] = fmaf(x1, w.w, p1[4 * q + 3]);
-                    }
+                for (int v = 0; v < VP / 2; ++v) {
+                    p0[2 * v] = q0[v].x;
+                    p0[2 * v + 1] = q0[v].y;
+                    p1[2 * v] = q1[v].x;
+                    p1[2 * v + 1] = q1[v].y;
                 }
                 const float s0 = reduce_scatter<VP>(p0, lane);
                 const float s1 = reduce_scatter<VP>(p1, lane);
