@@ -228,6 +228,15 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
     lo = __float2half_rn(xs - __half2float(hi));   // residual exact in fp32
 }
 
+// split_f16 on two values at once: one paired fp32 multiply, packed f32->f16x2
+// conversions and a paired subtract; bit-identical to two split_f16 calls.
+__device__ __forceinline__ void split_f16x2(float x, float y, __half2& hi, __half2& lo) {
+    const float2 s = __fmul2_rn(make_float2(x, y), make_float2(kSplitScale, kSplitScale));
+    hi = __float22half2_rn(s);
+    const float2 h = __half22float2(hi);
+    lo = __float22half2_rn(__fadd2_rn(s, make_float2(-h.x, -h.y)));
+}
+
 // Same split at an explicit power-of-two scale (alpha-block operands).
 __device__ __forceinline__ void split_f16s(float x, float scale, __half& hi, __half& lo) {
     const float xs = x * scale;

@@ -227,16 +227,14 @@ __device__ __forceinline__ void store4p(float* A, __half* A_hi, __half* A_lo, lo
     if (SPLIT == 0) {
         *reinterpret_cast<float4*>(A + idx) = v;
     } else if (SPLIT == 1) {
-        __half hi[4], lo[4];
-        split_f16(v.x, hi[0], lo[0]);
-        split_f16(v.y, hi[1], lo[1]);
-        split_f16(v.z, hi[2], lo[2]);
-        split_f16(v.w, hi[3], lo[3]);
+        __half2 h01, l01, h23, l23;
+        split_f16x2(v.x, v.y, h01, l01);
+        split_f16x2(v.z, v.w, h23, l23);
         uint2 h, l;
-        h.x = (uint32_t)__half_as_ushort(hi[0]) | ((uint32_t)__half_as_ushort(hi[1]) << 16);
-        h.y = (uint32_t)__half_as_ushort(hi[2]) | ((uint32_t)__half_as_ushort(hi[3]) << 16);
-        l.x = (uint32_t)__half_as_ushort(lo[0]) | ((uint32_t)__half_as_ushort(lo[1]) << 16);
-        l.y = (uint32_t)__half_as_ushort(lo[2]) | ((uint32_t)__half_as_ushort(lo[3]) << 16);
+        h.x = *reinterpret_cast<uint32_t*>(&h01);
+        h.y = *reinterpret_cast<uint32_t*>(&h23);
+        l.x = *reinterpret_cast<uint32_t*>(&l01);
+        l.y = *reinterpret_cast<uint32_t*>(&l23);
         *reinterpret_cast<uint2*>(A_hi + idx) = h;
         *reinterpret_cast<uint2*>(A_lo + idx) = l;
     } else {
@@ -327,10 +325,19 @@ __device__ __forceinline__ void attention_row(const AttnArgs& p, int r, int lane
                 const float4 w4 = reinterpret_cast<const float4*>(p.Ws + 4 * c * ND)[q];
                 w[4 * q] = w4.x; w[4 * q + 1] = w4.y; w[4 * q + 2] = w4.z; w[4 * q + 3] = w4.w;
             }
+            if (ND == 2) {  // paired FMAs: (sd0, sd1) += v_e (w_e0, w_e1)
+                float2 acc2 = make_float2(sd[0], sd[ND - 1]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
+                for (int e = 0; e < 4; ++e)
+                    acc2 = __ffma2_rn(make_float2(vv[e], vv[e]), make_float2(w[e * ND], w[e * ND + ND - 1]), acc2);
+                sd[0] = acc2.x;
+                sd[ND - 1] = acc2.y;
+            } else {
 #pragma unroll
-                for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], w[e * ND + d], sd[d]);
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) sd[d] = fmaf(vv[e], w[e * ND + d], sd[d]);
+            }
         }
         store4<SPLIT>(p, base + hc + 4 * c, v);
     }
