@@ -490,17 +490,24 @@ __global__ void __launch_bounds__(384, 1)
                 } else if (valid) {
                     const int u0 = nt * UNITS + uc;
                     float hv[8], cv[8];
+                    const float sc = SPLIT ? kSplitUnscale : 1.0f;  // a power of two: the scaling is exact
+                    const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float sc = SPLIT ? kSplitUnscale : 1.0f;
-                        float gi = g[0][j] * sc, gf = g[1][j] * sc, go = g[2][j] * sc, gc = g[3][j] * sc;
-                        gi += gb[0][j];
-                        gf += gb[1][j];
-                        go += gb[2][j];
-                        gc += gb[3][j];
-                        const float cn = sigm_fast(gf) * cp[j] + sigm_fast(gi) * tanh_fast(gc);
-                        cv[j] = cn;
-                        hv[j] = sigm_fast(go) * tanh_fast(cn);
+                    for (int j = 0; j < 8; j += 2) {
+                        // gate pre-activations of units j, j+1 on paired FMAs (FFMA2)
+                        float2 z[4];
+#pragma unroll
+                        for (int gt = 0; gt < 4; ++gt)
+                            z[gt] = __ffma2_rn(make_float2(g[gt][j], g[gt][j + 1]), sc2,
+                                               make_float2(gb[gt][j], gb[gt][j + 1]));
+                        const float zi[2] = {z[0].x, z[0].y}, zf[2] = {z[1].x, z[1].y};
+                        const float zo[2] = {z[2].x, z[2].y}, zc[2] = {z[3].x, z[3].y};
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const float cn = sigm_fast(zf[e]) * cp[j + e] + sigm_fast(zi[e]) * tanh_fast(zc[e]);
+                            cv[j + e] = cn;
+                            hv[j + e] = sigm_fast(zo[e]) * tanh_fast(cn);
+                        }
                     }
                     float4* hd = reinterpret_cast<float4*>(p.h_out + (long long)row * p.ldh + u0);
                     float4* cd = reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u0);
@@ -520,9 +527,9 @@ __global__ void __launch_bounds__(384, 1)
                         *reinterpret_cast<uint4*>(p.hA_hi + (long long)row * p.ldha + u0) =
                             *reinterpret_cast<const uint4*>(hb);
                     } else if (p.hA_hi != nullptr) {
-                        __align__(16) __half hh[8], hl[8];
+                        __align__(16) __half2 hh[4], hl[4];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) split_f16(hv[j], hh[j], hl[j]);
+                        for (int j = 0; j < 4; ++j) split_f16x2(hv[2 * j], hv[2 * j + 1], hh[j], hl[j]);
                         *reinterpret_cast<uint4*>(p.hA_hi + (long long)row * p.ldha + u0) =
                             *reinterpret_cast<const uint4*>(hh);
                         *reinterpret_cast<uint4*>(p.hA_lo + (long long)row * p.ldha + u0) =
