@@ -19,4 +19,4 @@ python tools/launch_summary.py gpurun_out/m/launches.csv > gpurun_out/m/launches
 # warm-up step = 15 gate GEMMs: skip them and the 6 encoder launches of the timed step
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lstm_gemm_tc" -s 21 -c 4 -o gpurun_out/m/prof_gemm python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/m/prof_gemm.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"beam_step_t|attention_pack_t" -s 20 -c 4 -o gpurun_out/m/prof_beam_attn python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/m/prof_beam_attn.log 2>&1
-tail -1 gpurun_out/m/prof_gemm.log gpurun_out/m/prof_beam_attn.log
+tail -n 1 gpurun_out/m/prof_gemm.log; tail -n 1 gpurun_out/m/prof_beam_attn.log
