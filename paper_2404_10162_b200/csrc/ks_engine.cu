@@ -1384,19 +1384,27 @@ ks_status run_chunk_graph(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool
             return KS_OK;
         }
     const int64_t l0 = E.launches;
-    KS_CUDA(cudaStreamBeginCapture(E.stream, cudaStreamCaptureModeRelaxed));
+    // a capture that fails (an operation the driver refuses inside a capture) turns
+    // graphs off for this engine and the chunk runs as plain launches
+    auto plain = [&]() {
+        (void)cudaGetLastError();
+        E.use_graphs = false;
+        E.launches = l0;
+        return run_chunk(E, C, cfg_base, k, greedy, d_tok, d_desc, pd, o_tok, o_lp, o_count, o_status, o_fpred,
+                         o_fstep);
+    };
+    if (cudaStreamBeginCapture(E.stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) return plain();
     st = run_chunk(E, C, cfg_base, k, greedy, d_tok, d_desc, pd, o_tok, o_lp, o_count, o_status, o_fpred, o_fstep);
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(E.stream, &graph);
-    if (st) {
+    if (st || ce != cudaSuccess || !graph) {
         if (graph) cudaGraphDestroy(graph);
-        return st;
+        return plain();
     }
-    if (ce != cudaSuccess || !graph) return set_error(KS_ERR_CUDA, std::string("decode graph capture: ") + cudaGetErrorString(ce));
     cudaGraphExec_t exec = nullptr;
     const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
-    if (ie != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("decode graph instantiate: ") + cudaGetErrorString(ie));
+    if (ie != cudaSuccess) return plain();
     if (E.graphs.size() >= 8) {
         cudaGraphExecDestroy(E.graphs.front().exec);
         E.graphs.erase(E.graphs.begin());
