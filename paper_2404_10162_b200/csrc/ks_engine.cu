@@ -1366,8 +1366,9 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
 // (events) or when disabled.
 ks_status run_chunk_graph(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greedy, const int* d_tok,
                           const long long* d_desc, const PredDev& pd, int* o_tok, double* o_lp, int* o_count,
-                          int* o_status, int* o_fpred, int* o_fstep) {
-    if (!E.use_graphs || E.prof || pd.has_host)
+                          int* o_status, int* o_fpred, int* o_fstep, bool single_chunk) {
+    // multi-chunk decodes would cycle through one graph per chunk offset: plain launches
+    if (!single_chunk || !E.use_graphs || E.prof || pd.has_host)
         return run_chunk(E, C, cfg_base, k, greedy, d_tok, d_desc, pd, o_tok, o_lp, o_count, o_status, o_fpred,
                          o_fstep);
     ks_status st;
@@ -1517,7 +1518,8 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
             ddesc = E.desc.as<long long>();
         }
         if ((st = run_chunk_graph(E, n, c0, k, greedy, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
-                            E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>())))
+                                  E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>(),
+                                  B <= C)))
             return st;
         char* ho = E.h_out.as<char>();
         int32_t* h_tok = reinterpret_cast<int32_t*>(ho);
@@ -1684,7 +1686,7 @@ extern "C" ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok,
         st = run_chunk_graph(E, n, c0, k, false, d_tok + c0 * 7, d_desc ? reinterpret_cast<const long long*>(d_desc) + c0 * 7 : nullptr,
                        pd, d_out_tok + c0 * k * T, d_out_lp + c0 * k, d_out_count + c0,
                        d_out_status ? d_out_status + c0 : nullptr, d_out_fpred ? d_out_fpred + c0 : nullptr,
-                       d_out_fstep ? d_out_fstep + c0 : nullptr);
+                       d_out_fstep ? d_out_fstep + c0 : nullptr, B <= C);
         if (st) break;
     }
     cudaEventRecord(ev, E.stream);
