@@ -179,7 +179,6 @@ struct BeamArgs {
     int* out_status;
     int cands_per_warp;        // smem capacity per warp (entries)
     const int* host_rej;       // [B*H_cur][V] first rejecting host predicate (or -1); may be null
-    int split_mode;            // selects the kernel instantiation only
     int h_per_config;          // hybrid: one feature row per config (static distributions)
     int n_values;              // staged-table sizes (shared memory)
     int n_terms;

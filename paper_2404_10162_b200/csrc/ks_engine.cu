@@ -1332,7 +1332,6 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         b.out_fail_step = o_fstep;
         b.cands_per_warp = cpw;
         b.host_rej = host_rej;
-        b.split_mode = aa.split_mode;
         b.n_values = (int)E.out_values.size();
         b.n_terms = pd.n_terms;
         b.n_bytes = pd.n_bytes;

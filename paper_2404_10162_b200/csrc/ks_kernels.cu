@@ -882,7 +882,7 @@ __device__ __forceinline__ int src_lane(int v) {
     return lane;
 }
 
-template <int VP, int SPLIT>
+template <int VP>
 __global__ void __launch_bounds__(256, VP == 32 ? 1 : VP == 16 ? 2 : 3) beam_step_t(BeamArgs a, PosMeta m) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int WS = VP == 4 ? 12 : VP + 4;  // padded W row: conflict-free 128-bit loads
@@ -1166,18 +1166,16 @@ size_t beam_smem_bytes(int NS, int V, int warps, int cands_per_warp, size_t tabl
            (size_t)warps * cands_per_warp * 28;
 }
 
-template <int SPLIT>
-bool launch_beam_split(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
+bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
     const int V = m.vsize[a.pos];
     static std::atomic<unsigned long long> attr{0};
     if (first_on_device(attr)) {
-        cudaFuncSetAttribute(beam_step_t<4, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(beam_step_t<8, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(beam_step_t<16, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(beam_step_t<32, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(beam_step_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     }
-    auto kern = V <= 4 ? beam_step_t<4, SPLIT> : V <= 8 ? beam_step_t<8, SPLIT>
-              : V <= 16 ? beam_step_t<16, SPLIT> : beam_step_t<32, SPLIT>;
+    auto kern = V <= 4 ? beam_step_t<4> : V <= 8 ? beam_step_t<8> : V <= 16 ? beam_step_t<16> : beam_step_t<32>;
     // persistent grid: exactly the CTAs that fit at once (registers and shared memory
     // both limit residency; a partial second wave would leave most SMs idle)
     int per_sm = 0, dev = 0, sms = 148;
@@ -1188,12 +1186,6 @@ bool launch_beam_split(const BeamArgs& a, const PosMeta& m, int warps, size_t sm
     const int g = std::min(grid, sms * per_sm);
     kern<<<g, warps * 32, smem, s>>>(a, m);
     return cudaGetLastError() == cudaSuccess;
-}
-
-bool launch_beam(const BeamArgs& a, const PosMeta& m, int warps, size_t smem, int grid, cudaStream_t s) {
-    if (a.split_mode == 0) return launch_beam_split<0>(a, m, warps, smem, grid, s);
-    if (a.split_mode == 1) return launch_beam_split<1>(a, m, warps, smem, grid, s);
-    return launch_beam_split<2>(a, m, warps, smem, grid, s);
 }
 
 }  // namespace ksb
