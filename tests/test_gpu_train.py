@@ -169,3 +169,12 @@ def test_export_import_roundtrip_is_identity():
     v = np.random.default_rng(0).standard_normal(tr.num_ref_params).astype(np.float32)
     tr.import_(v)
     np.testing.assert_array_equal(tr.export(), v)
+
+
+def test_f16x3_training_gemms_meet_the_gradient_bar(monkeypatch):
+    """KS_TRAIN_GEMM=f16x3: every training GEMM as fp16 hi/lo at a per-operand
+    power-of-two scale (device max-reduction) -- same gradient bar as 3xTF32."""
+    monkeypatch.setenv("KS_TRAIN_GEMM", "f16x3")
+    test_small_trained_gradients_vs_oracle(0.2)
+    if os.path.exists(BIG_CKPT):
+        test_default_size_gradients_vs_oracle()
