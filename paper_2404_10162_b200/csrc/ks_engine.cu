@@ -595,7 +595,10 @@ extern "C" void ks_engine_destroy(ks_engine* eng) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
     }
-    if (eng->stream) cudaStreamDestroy(eng->stream);
+    if (eng->stream) {
+        cudaStreamSynchronize(eng->stream);  // device-API decodes may still be running
+        cudaStreamDestroy(eng->stream);
+    }
     delete eng;
 }
 
