@@ -262,11 +262,34 @@ struct CellBwd {
     const float* mask2;     // [M][H] or null, applied to dh2
     float* dc;              // [M][H] in: dc from the next step (zeroed at the end), out: dc_prev
     float* dZ;              // [M][4H]
+    int* amax0;             // F16X3 trainer GEMMs: max |dZ| of this launch / of every step, or null
+    int* amax1;
 };
 
-__global__ void k_cell_bwd(CellBwd a) {
-    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= (long long)a.M * a.H) return;
+__device__ __forceinline__ void cell_bwd_elem(const CellBwd& a, long long tid, float& mx);
+__global__ void __launch_bounds__(256) k_cell_bwd(CellBwd a) {
+    float mx = 0.0f;
+    for (long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x; tid < (long long)a.M * a.H;
+         tid += (long long)gridDim.x * blockDim.x)
+        cell_bwd_elem(a, tid, mx);
+    if (a.amax0 == nullptr && a.amax1 == nullptr) return;
+    // the max |dZ| the F16X3 split of the dX / dW GEMMs needs, one atomic per block
+    __shared__ float wm[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        mx = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (threadIdx.x == 0 && mx > 0.0f) {
+            if (a.amax0) atomicMax(a.amax0, __float_as_int(mx));
+            if (a.amax1) atomicMax(a.amax1, __float_as_int(mx));
+        }
+    }
+}
+__device__ __forceinline__ void cell_bwd_elem(const CellBwd& a, long long tid, float& mx) {
     const int r = (int)(tid / a.H), j = (int)(tid % a.H);
     const int H = a.H;
     const float* A = a.act + (long long)r * 4 * H;
@@ -282,11 +305,14 @@ __global__ void k_cell_bwd(CellBwd a) {
     const float dc = a.dc[(long long)r * H + j] + dh * o * (1.0f - tc * tc);
     const float dout = dh * tc;
     float* dZ = a.dZ + (long long)r * 4 * H;
-    dZ[j] = dc * g * i * (1.0f - i);
-    dZ[H + j] = dc * cp * f * (1.0f - f);
-    dZ[2 * H + j] = dout * o * (1.0f - o);
-    dZ[3 * H + j] = dc * i * (1.0f - g * g);
+    const float z0 = dc * g * i * (1.0f - i), z1 = dc * cp * f * (1.0f - f);
+    const float z2 = dout * o * (1.0f - o), z3 = dc * i * (1.0f - g * g);
+    dZ[j] = z0;
+    dZ[H + j] = z1;
+    dZ[2 * H + j] = z2;
+    dZ[3 * H + j] = z3;
     a.dc[(long long)r * H + j] = dc * f;
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(z0), fabsf(z1)), fmaxf(fabsf(z2), fabsf(z3))));
 }
 
 // Attention forward, one warp per row (the tape form of attention_weights +
@@ -940,6 +966,7 @@ struct ks_trainer {
     bool f16x3 = true;             // ... as F16X3 with per-operand scales (default) or 3xTF32
     DBuf scal;                     // F16X3: per-step max|x| slots and GEMM alphas; [2] = {0, 1} betas
     int scal_used = 0;
+    int act_bound_bits = 0;        // host copy of the activation bound written to its slot
     std::map<std::pair<const float*, bool>, int> wslot;  // cached weight split -> its max|x| slot
     DBuf sp[4];                    // split scratch: A big/small, B big/small
     DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
@@ -1113,9 +1140,12 @@ void launch_split_cat(ks_trainer& t, cudaStream_t s, const float* src, long long
 // mode: both operands split (weights once per call, cached by pointer and
 // layout) into the concatenated-K form of k_split_cat, one TF32 tensor-core
 // GEMM with fp32 accumulation; fp32 mode: one SGEMM (PEDANTIC, no TF32).
+// a_amax / b_amax (F16X3 only): device slots already holding max |A| / |B| (a
+// bound: activations are tanh outputs times dropout scales; dZ maxima come fused
+// from k_cell_bwd), so no max-reduction pass over that operand is needed.
 ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
                   long long lda, const float* B, long long ldb, float beta, float* C, long long ldc,
-                  bool b_is_weight = false) {
+                  bool b_is_weight = false, const int* a_amax = nullptr, const int* b_amax = nullptr) {
     if (M == 0 || N == 0) return KS_OK;
     if (K == 0) return beta == 1.0f ? KS_OK : set_error(KS_ERR_SHAPE, "empty GEMM reduction");
     // narrow outputs (heads, attention, slot rows) stay fp32 SGEMMs
@@ -1136,35 +1166,39 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
         };
         if (t.scal_used + 3 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
         int* slots = t.scal.as<int>();
-        const int sa = t.scal_used++, salpha = t.scal_used++;
+        const int salpha = t.scal_used++;
+        int sa = -1;
+        if (!a_amax) sa = t.scal_used++;
+        const int* amaxA = a_amax ? a_amax : slots + sa;
         // A' = [lo | hi | hi] (M x 3K, row stride lda3)
         const long long lda3 = r8(K3);
         KT_CUDA(t.sp[0].ensure((size_t)M * lda3 * 2));
         __half* a16 = t.sp[0].as<__half>();
-        absmax(A, ta ? K : M, ta ? M : K, lda, slots + sa);
+        if (!a_amax) absmax(A, ta ? K : M, ta ? M : K, lda, slots + sa);
         if (ta) {
             dim3 grid((unsigned)((M + 31) / 32), (unsigned)((K + 31) / 32));
             if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
-            k_split16_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, a16, lda3, slots + sa);
+            k_split16_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, a16, lda3, amaxA);
         } else {
             dim3 grid((unsigned)std::min<long long>((K + 255) / 256, 64), (unsigned)std::min<long long>(M, 65535));
-            k_split16<<<grid, 256, 0, s>>>(A, M, (int)K, lda, a16, lda3, 0, 0b001, slots + sa);
+            k_split16<<<grid, 256, 0, s>>>(A, M, (int)K, lda, a16, lda3, 0, 0b001, amaxA);
         }
         ++t.launches;
         // B' = [hi ; hi ; lo] along K: stacked (3K x N, row stride ldb3) or side by side (tb: N x 3K)
         const long long br = tb ? N : K, bc = tb ? K : N;
         const long long ldb3 = tb ? r8(K3) : r8(N);
         const size_t bbytes = (size_t)(tb ? N : K3) * ldb3 * 2;
-        auto split_b = [&](DBuf& dst, int slot) -> ks_status {
+        auto split_b = [&](DBuf& dst, const int* amax, int slot) -> ks_status {
             KT_CUDA(dst.ensure(bbytes));
-            absmax(B, br, bc, ldb, slots + slot);
+            if (!amax) absmax(B, br, bc, ldb, slots + slot);
             dim3 grid((unsigned)std::min<long long>((bc + 255) / 256, 64), (unsigned)std::min<long long>(br, 65535));
-            k_split16<<<grid, 256, 0, s>>>(B, br, (int)bc, ldb, dst.as<__half>(), ldb3, tb ? 0 : 1, 0b100, slots + slot);
+            k_split16<<<grid, 256, 0, s>>>(B, br, (int)bc, ldb, dst.as<__half>(), ldb3, tb ? 0 : 1, 0b100,
+                                           amax ? amax : slots + slot);
             ++t.launches;
             return KS_OK;
         };
         const __half* b16;
-        int sb;
+        const int* amaxB;
         if (b_is_weight) {
             const std::pair<const float*, bool> key(B, tb);
             auto it = t.wsplit.find(key);
@@ -1173,20 +1207,24 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
                 DBuf* buf = t.wsplit_store[t.wsplit_used++].get();
                 if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
                 const int slot = t.scal_used++;
-                if ((st = split_b(buf[0], slot))) return st;
+                if ((st = split_b(buf[0], nullptr, slot))) return st;
                 it = t.wsplit.emplace(key, std::make_pair(buf, bc)).first;
                 t.wslot[key] = slot;
             }
             b16 = it->second.first[0].as<__half>();
-            sb = t.wslot[key];
+            amaxB = slots + t.wslot[key];
         } else {
-            if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
-            sb = t.scal_used++;
-            if ((st = split_b(t.sp[2], sb))) return st;
+            int sb = -1;
+            if (!b_amax) {
+                if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
+                sb = t.scal_used++;
+            }
+            if ((st = split_b(t.sp[2], b_amax, sb))) return st;
             b16 = t.sp[2].as<__half>();
+            amaxB = b_amax ? b_amax : slots + sb;
         }
         float* alpha = reinterpret_cast<float*>(slots + salpha);
-        k_f16_alpha<<<1, 1, 0, s>>>(slots + sa, slots + sb, alpha);
+        k_f16_alpha<<<1, 1, 0, s>>>(amaxA, amaxB, alpha);
         ++t.launches;
         const float* betap = reinterpret_cast<const float*>(slots + kScalSlots) + (beta == 0.0f ? 0 : 1);
         if (beta != 0.0f && beta != 1.0f) return set_error(KS_ERR_PARAMETER, "F16X3 GEMM beta must be 0 or 1");
@@ -1322,9 +1360,20 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
     t.wsplit.clear();  // weights may have changed since the last call (Adam, import)
     t.wslot.clear();
     t.wsplit_used = 0;
-    if (t.f16x3) {  // fresh max|x| slots for this step's GEMMs
+    // F16X3: fresh max|x| slots for this step's GEMMs; slot 0 bounds every activation
+    // operand (LSTM outputs are tanh-bounded, times at most the dropout scale)
+    int* act_amax = nullptr;
+    auto new_slot = [&]() -> int* {
+        if (!t.f16x3 || t.scal_used >= kScalSlots) return nullptr;  // null: the GEMM reduces itself
+        return t.scal.as<int>() + t.scal_used++;
+    };
+    if (t.f16x3) {
         KT_CUDA(cudaMemsetAsync(t.scal.p, 0, (size_t)kScalSlots * 4, s));
         t.scal_used = 0;
+        const float bound = (float)(1.0 / (1.0 - std::max(t.dropout, t.rdropout))) * 1.001f;
+        std::memcpy(&t.act_bound_bits, &bound, 4);
+        act_amax = new_slot();
+        KT_CUDA(cudaMemcpyAsync(act_amax, &t.act_bound_bits, 4, cudaMemcpyHostToDevice, s));
     }
     const int T = t.T;
     const long long m = M;
@@ -1377,7 +1426,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             const int tt = dir == 0 ? st_ : kTin - 1 - st_;
             float* Z = t.Ze[dir].as<float>() + (long long)st_ * m * 4 * H;
             if (st_ > 0 && (st = gemm_rm(t, false, false, m, 4LL * H, H, Hx + (long long)st_ * m * H, H,
-                                         P + L.wd(), 4LL * H, 0.0f, Z, 4LL * H, true)))
+                                         P + L.wd(), 4LL * H, 0.0f, Z, 4LL * H, true, act_amax)))
                 return st;
             CellFwd c{};
             c.M = M;
@@ -1448,7 +1497,8 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             ++t.launches;
         }
         float* Z = t.Zd.as<float>() + (long long)p * m * 4 * Hd;
-        if ((st = gemm_rm(t, false, false, m, 4LL * Hd, Kd, X, Kd, P + D.wd(), 4LL * Hd, 0.0f, Z, 4LL * Hd, true)))
+        if ((st = gemm_rm(t, false, false, m, 4LL * Hd, Kd, X, Kd, P + D.wd(), 4LL * Hd, 0.0f, Z, 4LL * Hd, true,
+                          act_amax)))
             return st;
         CellFwd c{};
         c.M = M;
@@ -1510,8 +1560,10 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         KT_CUDA(cudaMemsetAsync(t.DPa.p, 0, m * 7 * t.n_d * 4, s));
         KT_CUDA(cudaMemsetAsync(t.rowacc.p, 0, m * (t.n_d + 1) * 4, s));
     }
+    int* dzd_amax = new_slot();  // max |dZ| over every position (the dW GEMM)
     for (int p = T - 1; p >= 0; --p) {
         float* dZ = t.dZd.as<float>() + (long long)p * m * 4 * Hd;
+        int* dz_amax = new_slot();
         CellBwd cb{};
         cb.M = M;
         cb.H = Hd;
@@ -1525,11 +1577,14 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         cb.mask2 = attn ? nullptr : mr;  // enc-dec: dH is the raw dX of the next step's h rows
         cb.dc = dC;
         cb.dZ = dZ;
-        k_cell_bwd<<<blocks(m * Hd, 256), 256, 0, s>>>(cb);
+        cb.amax0 = dz_amax;
+        cb.amax1 = dzd_amax;
+        k_cell_bwd<<<std::min(blocks(m * Hd, 256), 148u * 8u), 256, 0, s>>>(cb);
         ++t.launches;
         // dX = dZ . Wd^T  -> [dctx | dh_rec]
         float* dX = t.dXd.as<float>();
-        if ((st = gemm_rm(t, false, true, m, Kd, 4LL * Hd, dZ, 4LL * Hd, P + D.wd(), 4LL * Hd, 0.0f, dX, Kd, true)))
+        if ((st = gemm_rm(t, false, true, m, Kd, 4LL * Hd, dZ, 4LL * Hd, P + D.wd(), 4LL * Hd, 0.0f, dX, Kd, true,
+                          dz_amax)))
             return st;
         if (attn) {
             AttnBwd ab{};
@@ -1563,7 +1618,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
     }
     // decoder weight gradients: one GEMM over all (position, row) pairs
     if ((st = gemm_rm(t, true, false, Kd, 4LL * Hd, (long long)T * m, Xd, Kd, t.dZd.as<float>(), 4LL * Hd, 1.0f,
-                      G + D.wd(), 4LL * Hd)))
+                      G + D.wd(), 4LL * Hd, false, act_amax, dzd_amax)))
         return st;
     if ((st = gemm_rm(t, true, false, D.S + 1, 4LL * Hd, (long long)T * m, t.dec_sm.as<float>(), D.S + 1,
                       t.dZd.as<float>(), 4LL * Hd, 1.0f, G + D.ws(), 4LL * Hd)))
@@ -1613,9 +1668,11 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             // enc-dec: the decoder's step-0 gradients flow into the encoder's final state
             KT_CUDA(cudaMemcpyAsync(dCe, dC, m * H * 4, cudaMemcpyDeviceToDevice, s));
         }
+        int* dze_amax = new_slot();  // max |dZ| over the 7 steps (the dW GEMM)
         for (int st_ = kTin - 1; st_ >= 0; --st_) {
             const int tt = dir == 0 ? st_ : kTin - 1 - st_;
             float* dZ = t.dZe[dir].as<float>() + (long long)st_ * m * 4 * H;
+            int* dz_amax = new_slot();
             CellBwd cb{};
             cb.M = M;
             cb.H = H;
@@ -1636,14 +1693,17 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             }
             cb.dc = dCe;
             cb.dZ = dZ;
-            k_cell_bwd<<<blocks(m * H, 256), 256, 0, s>>>(cb);
+            cb.amax0 = dz_amax;
+            cb.amax1 = dze_amax;
+            k_cell_bwd<<<std::min(blocks(m * H, 256), 148u * 8u), 256, 0, s>>>(cb);
             ++t.launches;
-            if (st_ > 0 && (st = gemm_rm(t, false, true, m, H, 4LL * H, dZ, 4LL * H, P + L.wd(), 4LL * H, 0.0f, dHe, H, true)))
+            if (st_ > 0 && (st = gemm_rm(t, false, true, m, H, 4LL * H, dZ, 4LL * H, P + L.wd(), 4LL * H, 0.0f, dHe, H, true,
+                                         dz_amax)))
                 return st;
         }
         float* Hx = t.Hx[dir].as<float>();
         if ((st = gemm_rm(t, true, false, H, 4LL * H, 7 * m, Hx, H, t.dZe[dir].as<float>(), 4LL * H, 1.0f,
-                          G + L.wd(), 4LL * H)))
+                          G + L.wd(), 4LL * H, false, act_amax, dze_amax)))
             return st;
         if ((st = gemm_rm(t, true, false, t.d_in + 1, 4LL * H, 7 * m, t.enc_sm[dir].as<float>(), t.d_in + 1,
                           t.dZe[dir].as<float>(), 4LL * H, 1.0f, G + L.ws(), 4LL * H)))
@@ -1866,10 +1926,9 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
     {
         const char* g = std::getenv("KS_TRAIN_GEMM");
         t.tf32x3 = !(g && std::string(g) == "fp32");
-        // F16X3 (KS_TRAIN_GEMM=f16x3): 2.4x faster GEMMs, but the per-operand max|x|
-        // reductions and fp16 split passes cost more than they save at this model size
-        // (6.14 vs 5.96 ms per cfg4 step), so 3xTF32 stays the default
-        t.f16x3 = g && std::string(g) == "f16x3";
+        // F16X3 by default (fp16 GEMMs run 2.4x the TF32 rate); KS_TRAIN_GEMM=tf32x3 keeps
+        // the 3xTF32 split, =fp32 the SIMT SGEMM
+        t.f16x3 = !(g && (std::string(g) == "fp32" || std::string(g) == "tf32x3"));
         const float betas[2] = {0.0f, 1.0f};
         if (t.scal.ensure((size_t)(kScalSlots + 2) * 4) != cudaSuccess ||
             cudaMemcpy(t.scal.as<char>() + (size_t)kScalSlots * 4, betas, 8, cudaMemcpyHostToDevice) != cudaSuccess)

@@ -171,10 +171,10 @@ def test_export_import_roundtrip_is_identity():
     np.testing.assert_array_equal(tr.export(), v)
 
 
-def test_f16x3_training_gemms_meet_the_gradient_bar(monkeypatch):
-    """KS_TRAIN_GEMM=f16x3: every training GEMM as fp16 hi/lo at a per-operand
-    power-of-two scale (device max-reduction) -- same gradient bar as 3xTF32."""
-    monkeypatch.setenv("KS_TRAIN_GEMM", "f16x3")
+def test_tf32x3_training_gemms_meet_the_gradient_bar(monkeypatch):
+    """KS_TRAIN_GEMM=tf32x3: the 3xTF32 split (the alternative to the default
+    per-operand-scaled F16X3) meets the same gradient bar."""
+    monkeypatch.setenv("KS_TRAIN_GEMM", "tf32x3")
     test_small_trained_gradients_vs_oracle(0.2)
     if os.path.exists(BIG_CKPT):
         test_default_size_gradients_vs_oracle()
