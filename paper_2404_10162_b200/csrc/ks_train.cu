@@ -734,9 +734,12 @@ __device__ __forceinline__ void split_f16x2s(float x, float y, float sc, __half2
 // The F16X3 analogue of k_split_cat: part i of each row (stack 0: side by side,
 // row stride ldo) or block (stack 1: stacked along K, row stride ldo) is lo(x)
 // when bit i of lo_mask is set, hi(x) otherwise.
+// alpha (optional): the GEMM's unscale 2^-(e + e_other), written by one thread
 __global__ void k_split16(const float* src, long long rows, int cols, long long ld, __half* out, long long ldo,
-                          int stack, int lo_mask, const int* amax) {
+                          int stack, int lo_mask, const int* amax, const int* amax_other, float* alpha) {
     const float sc = exp2f((float)f16_scale_exp(*amax));
+    if (alpha && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        *alpha = exp2f(-(float)(f16_scale_exp(*amax) + f16_scale_exp(*amax_other)));
     // 4 columns per thread (16-byte loads, 8-byte stores) when the layout allows it
     const bool vec = (cols & 3) == 0 && (ld & 3) == 0 && (ldo & 3) == 0 &&
                      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
@@ -773,9 +776,11 @@ __global__ void k_split16(const float* src, long long rows, int cols, long long 
 }
 // Transposed: out (cols x 3 rows, row stride ldo), row c = [lo | hi | hi] of column c.
 __global__ void k_split16_t(const float* src, long long rows, long long cols, long long ld, __half* out, long long ldo,
-                            const int* amax) {
+                            const int* amax, const int* amax_other, float* alpha) {
     __shared__ float tile[32][33];
     const float sc = exp2f((float)f16_scale_exp(*amax));
+    if (alpha && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+        *alpha = exp2f(-(float)(f16_scale_exp(*amax) + f16_scale_exp(*amax_other)));
     const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const long long r = r0 + i, c = c0 + threadIdx.x;
@@ -793,9 +798,6 @@ __global__ void k_split16_t(const float* src, long long rows, long long cols, lo
             row[2 * rows + r] = hi;
         }
     }
-}
-__global__ void k_f16_alpha(const int* amax_a, const int* amax_b, float* alpha) {
-    *alpha = exp2f(-(float)(f16_scale_exp(*amax_a) + f16_scale_exp(*amax_b)));
 }
 
 // Loss / match totals (double, fixed order).
@@ -1170,20 +1172,6 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
         int sa = -1;
         if (!a_amax) sa = t.scal_used++;
         const int* amaxA = a_amax ? a_amax : slots + sa;
-        // A' = [lo | hi | hi] (M x 3K, row stride lda3)
-        const long long lda3 = r8(K3);
-        KT_CUDA(t.sp[0].ensure((size_t)M * lda3 * 2));
-        __half* a16 = t.sp[0].as<__half>();
-        if (!a_amax) absmax(A, ta ? K : M, ta ? M : K, lda, slots + sa);
-        if (ta) {
-            dim3 grid((unsigned)((M + 31) / 32), (unsigned)((K + 31) / 32));
-            if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
-            k_split16_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, a16, lda3, amaxA);
-        } else {
-            dim3 grid((unsigned)std::min<long long>((K + 255) / 256, 64), (unsigned)std::min<long long>(M, 65535));
-            k_split16<<<grid, 256, 0, s>>>(A, M, (int)K, lda, a16, lda3, 0, 0b001, amaxA);
-        }
-        ++t.launches;
         // B' = [hi ; hi ; lo] along K: stacked (3K x N, row stride ldb3) or side by side (tb: N x 3K)
         const long long br = tb ? N : K, bc = tb ? K : N;
         const long long ldb3 = tb ? r8(K3) : r8(N);
@@ -1193,7 +1181,7 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
             if (!amax) absmax(B, br, bc, ldb, slots + slot);
             dim3 grid((unsigned)std::min<long long>((bc + 255) / 256, 64), (unsigned)std::min<long long>(br, 65535));
             k_split16<<<grid, 256, 0, s>>>(B, br, (int)bc, ldb, dst.as<__half>(), ldb3, tb ? 0 : 1, 0b100,
-                                           amax ? amax : slots + slot);
+                                           amax ? amax : slots + slot, nullptr, nullptr);
             ++t.launches;
             return KS_OK;
         };
@@ -1223,8 +1211,20 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
             b16 = t.sp[2].as<__half>();
             amaxB = b_amax ? b_amax : slots + sb;
         }
+        // A' = [lo | hi | hi] (M x 3K, row stride lda3); its split also writes the GEMM's alpha
         float* alpha = reinterpret_cast<float*>(slots + salpha);
-        k_f16_alpha<<<1, 1, 0, s>>>(amaxA, amaxB, alpha);
+        const long long lda3 = r8(K3);
+        KT_CUDA(t.sp[0].ensure((size_t)M * lda3 * 2));
+        __half* a16 = t.sp[0].as<__half>();
+        if (!a_amax) absmax(A, ta ? K : M, ta ? M : K, lda, slots + sa);
+        if (ta) {
+            dim3 grid((unsigned)((M + 31) / 32), (unsigned)((K + 31) / 32));
+            if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
+            k_split16_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, a16, lda3, amaxA, amaxB, alpha);
+        } else {
+            dim3 grid((unsigned)std::min<long long>((K + 255) / 256, 64), (unsigned)std::min<long long>(M, 65535));
+            k_split16<<<grid, 256, 0, s>>>(A, M, (int)K, lda, a16, lda3, 0, 0b001, amaxA, amaxB, alpha);
+        }
         ++t.launches;
         const float* betap = reinterpret_cast<const float*>(slots + kScalSlots) + (beta == 0.0f ? 0 : 1);
         if (beta != 0.0f && beta != 1.0f) return set_error(KS_ERR_PARAMETER, "F16X3 GEMM beta must be 0 or 1");
