@@ -744,8 +744,12 @@ __global__ void k_split16(const float* src, long long rows, int cols, long long 
     const bool vec = (cols & 3) == 0 && (ld & 3) == 0 && (ldo & 3) == 0 &&
                      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
     const int cw = vec ? cols >> 2 : cols;
-    for (long long r = blockIdx.y; r < rows; r += gridDim.y) {
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cw; c += gridDim.x * blockDim.x) {
+    // flat grid-stride over (row, column group): narrow rows do not idle most threads
+    const long long n = rows * (long long)cw;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / cw;
+        const int c = (int)(i - r * cw);
+        {
             if (vec) {
                 const float4 x = reinterpret_cast<const float4*>(src + r * ld)[c];
                 __half2 h01, l01, h23, l23;
@@ -1075,6 +1079,10 @@ ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long
 // F16X3 pass through cuBLASLt: fp16 operands, fp32 accumulation and output,
 // alpha (the 2^-(eA+eB) unscale) and beta read from device memory.
 constexpr int kScalSlots = 4096;
+inline unsigned split16_grid(long long rows, long long cols) {
+    const long long items = rows * ((cols + 3) / 4);
+    return (unsigned)std::max<long long>(1, std::min<long long>((items + 255) / 256, 148LL * 16));
+}
 ks_status gemm_lt16(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long N, long long K, const __half* A,
                     long long lda, const __half* B, long long ldb, const float* alpha, const float* beta, float* C,
                     long long ldc) {
@@ -1179,8 +1187,7 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
         auto split_b = [&](DBuf& dst, const int* amax, int slot) -> ks_status {
             KT_CUDA(dst.ensure(bbytes));
             if (!amax) absmax(B, br, bc, ldb, slots + slot);
-            dim3 grid((unsigned)std::min<long long>((bc + 255) / 256, 64), (unsigned)std::min<long long>(br, 65535));
-            k_split16<<<grid, 256, 0, s>>>(B, br, (int)bc, ldb, dst.as<__half>(), ldb3, tb ? 0 : 1, 0b100,
+            k_split16<<<split16_grid(br, bc), 256, 0, s>>>(B, br, (int)bc, ldb, dst.as<__half>(), ldb3, tb ? 0 : 1, 0b100,
                                            amax ? amax : slots + slot, nullptr, nullptr);
             ++t.launches;
             return KS_OK;
@@ -1222,8 +1229,7 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
             if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
             k_split16_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, a16, lda3, amaxA, amaxB, alpha);
         } else {
-            dim3 grid((unsigned)std::min<long long>((K + 255) / 256, 64), (unsigned)std::min<long long>(M, 65535));
-            k_split16<<<grid, 256, 0, s>>>(A, M, (int)K, lda, a16, lda3, 0, 0b001, amaxA, amaxB, alpha);
+            k_split16<<<split16_grid(M, K), 256, 0, s>>>(A, M, (int)K, lda, a16, lda3, 0, 0b001, amaxA, amaxB, alpha);
         }
         ++t.launches;
         const float* betap = reinterpret_cast<const float*>(slots + kScalSlots) + (beta == 0.0f ? 0 : 1);
