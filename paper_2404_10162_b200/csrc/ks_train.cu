@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -83,6 +84,11 @@ __device__ __forceinline__ unsigned long long mt_twist_one(const unsigned long l
     if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
     return mt[(i + 156) % 312] ^ xa;
 }
+__global__ void k_set_u64x2(unsigned long long* d, unsigned long long a, unsigned long long b) {
+    d[0] = a;
+    d[1] = b;
+}
+__global__ void k_set_int(int* d, int v) { *d = v; }
 __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
     y ^= (y >> 29) & 0x5555555555555555ULL;
     y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
@@ -90,10 +96,13 @@ __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
     return y ^ (y >> 43);
 }
 
-__global__ void k_dropout_masks(int M, unsigned long long seed, long long epoch, const long long* idx,
+// se = {seed, epoch} in device memory (written per step outside the captured graph)
+__global__ void k_dropout_masks(int M, const unsigned long long* se, const long long* idx,
                                 long long idx_base, int n_in, double rate_in, int n_rec, double rate_rec,
                                 float* mi, float* mr) {
     __shared__ unsigned long long st[8][312];
+    const unsigned long long seed = se[0];
+    const long long epoch = (long long)se[1];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * (blockDim.x >> 5) + w;
     if (b >= M) return;
@@ -879,6 +888,9 @@ namespace {
 
 using namespace kst;
 
+// bumped on every (re)allocation: captured training-step graphs bake buffer addresses
+std::atomic<unsigned long long> g_train_alloc_gen{0};
+
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -887,6 +899,7 @@ struct DBuf {
     }
     cudaError_t ensure(size_t n) {
         if (n <= bytes) return cudaSuccess;
+        g_train_alloc_gen.fetch_add(1);
         if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
@@ -972,7 +985,19 @@ struct ks_trainer {
     bool f16x3 = true;             // ... as F16X3 with per-operand scales (default) or 3xTF32
     DBuf scal;                     // F16X3: per-step max|x| slots and GEMM alphas; [2] = {0, 1} betas
     int scal_used = 0;
-    int act_bound_bits = 0;        // host copy of the activation bound written to its slot
+    int act_bound_bits = 0;        // the activation bound's float bits, written to its slot
+    DBuf se;                       // {seed, epoch} of the current step (dropout masks)
+    // CUDA graphs of whole ks_trainer_loss_grads batches on the trainer's own stream
+    // (the caller's stream may be the legacy default stream, which cannot be captured)
+    bool use_graphs = true;
+    cudaStream_t gs = nullptr;
+    cudaEvent_t gev = nullptr;
+    struct GraphEntry {
+        std::vector<long long> key;
+        cudaGraphExec_t exec = nullptr;
+        long long launches = 0;
+    };
+    std::vector<GraphEntry> graphs;
     std::map<std::pair<const float*, bool>, int> wslot;  // cached weight split -> its max|x| slot
     DBuf sp[4];                    // split scratch: A big/small, B big/small
     DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
@@ -1379,7 +1404,8 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         const float bound = (float)(1.0 / (1.0 - std::max(t.dropout, t.rdropout))) * 1.001f;
         std::memcpy(&t.act_bound_bits, &bound, 4);
         act_amax = new_slot();
-        KT_CUDA(cudaMemcpyAsync(act_amax, &t.act_bound_bits, 4, cudaMemcpyHostToDevice, s));
+        k_set_int<<<1, 1, 0, s>>>(act_amax, t.act_bound_bits);
+        ++t.launches;
     }
     const int T = t.T;
     const long long m = M;
@@ -1392,7 +1418,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
     float* mi = drop ? t.mi.as<float>() : nullptr;
     float* mr = drop ? t.mr.as<float>() : nullptr;
     if (drop) {
-        k_dropout_masks<<<blocks(m, 8), 256, 0, s>>>(M, seed, dropout_epoch, d_idx, 0, t.n_in, t.dropout, Hd,
+        k_dropout_masks<<<blocks(m, 8), 256, 0, s>>>(M, t.se.as<unsigned long long>(), d_idx, 0, t.n_in, t.dropout, Hd,
                                                      t.rdropout, mi, mr);
         ++t.launches;
     }
@@ -1942,6 +1968,18 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
     }
     if (t.blas_ws.ensure((size_t)64 << 20) != cudaSuccess) return set_error(KS_ERR_CUDA, "cuBLAS workspace");
     if (cublasLtCreate(&t.lt) != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cublasLtCreate failed");
+    // cuBLAS on a fixed workspace (no allocations inside captured graphs)
+    if (cublasSetWorkspace(t.blas, t.blas_ws.p, t.blas_ws.bytes) != CUBLAS_STATUS_SUCCESS)
+        return set_error(KS_ERR_CUDA, "cublasSetWorkspace failed");
+    if (t.se.ensure(16) != cudaSuccess || cudaMemset(t.se.p, 0, 16) != cudaSuccess)
+        return set_error(KS_ERR_CUDA, "trainer step scalars");
+    {
+        const char* kg = std::getenv("KS_GRAPHS");
+        t.use_graphs = !(kg && kg[0] == '0');
+        if (cudaStreamCreateWithFlags(&t.gs, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&t.gev, cudaEventDisableTiming) != cudaSuccess)
+            return set_error(KS_ERR_CUDA, "trainer stream");
+    }
     *out = tr.release();
     return KS_OK;
 }
@@ -1963,6 +2001,11 @@ extern "C" ks_status ks_trainer_create_from_checkpoint(const char* path, int32_t
 extern "C" void ks_trainer_destroy(ks_trainer* t) {
     if (!t) return;
     cudaSetDevice(t->device);
+    if (t->gs) cudaStreamSynchronize(t->gs);
+    for (auto& g : t->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (t->gev) cudaEventDestroy(t->gev);
+    if (t->gs) cudaStreamDestroy(t->gs);
     if (t->blas) cublasDestroy(t->blas);
     for (auto& kv : t->lt_plans) {
         if (kv.second.lc) cublasLtMatrixLayoutDestroy(kv.second.lc);
@@ -1988,9 +2031,83 @@ extern "C" ks_status ks_trainer_loss_grads(ks_trainer* t, const int32_t* d_tok, 
     if (!d_tok || !d_tgt) return set_error(KS_ERR_PARAMETER, "null token buffer");
     cudaSetDevice(t->device);
     t->launches = 0;
-    return run_batch(*t, (int)B, d_tok, d_tgt, reinterpret_cast<const long long*>(d_idx), dropout_epoch, seed,
-                     d_grads, accumulate != 0, d_loss_sum, reinterpret_cast<long long*>(d_matches),
-                     reinterpret_cast<cudaStream_t>(stream));
+    cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+    const long long* idx = reinterpret_cast<const long long*>(d_idx);
+    long long* match = reinterpret_cast<long long*>(d_matches);
+    ks_status st;
+    if ((st = ensure_ws(*t, (int)B))) return st;
+    if (!t->use_graphs) {
+        k_set_u64x2<<<1, 1, 0, user>>>(t->se.as<unsigned long long>(), seed, (unsigned long long)dropout_epoch);
+        t->launches = 1;
+        return run_batch(*t, (int)B, d_tok, d_tgt, idx, dropout_epoch, seed, d_grads, accumulate != 0, d_loss_sum,
+                         match, user);
+    }
+    // the whole batch (~250 launches) replays as one CUDA graph on the trainer stream;
+    // seed / epoch are device values written just before it
+    KT_CUDA(cudaEventRecord(t->gev, user));
+    KT_CUDA(cudaStreamWaitEvent(t->gs, t->gev, 0));
+    k_set_u64x2<<<1, 1, 0, t->gs>>>(t->se.as<unsigned long long>(), seed, (unsigned long long)dropout_epoch);
+    auto P = [](const void* q) { return (long long)reinterpret_cast<uintptr_t>(q); };
+    auto key_now = [&]() {
+        return std::vector<long long>{B, P(d_tok), P(d_tgt), P(idx), P(d_grads), accumulate ? 1 : 0, P(d_loss_sum),
+                                      P(match), dropout_epoch >= 0 ? 1 : 0,
+                                      (long long)g_train_alloc_gen.load()};
+    };
+    const std::vector<long long> key = key_now();
+    ks_trainer::GraphEntry* hit = nullptr;
+    for (auto& g : t->graphs)
+        if (g.key == key) hit = &g;
+    if (hit && hit->exec) {
+        KT_CUDA(cudaGraphLaunch(hit->exec, t->gs));
+        t->launches = 1 + hit->launches;
+    } else if (!hit) {
+        // first batch of this shape: plain launches, so every workspace reaches its size
+        // (a buffer grown inside a capture would free memory already captured)
+        t->launches = 1;
+        st = run_batch(*t, (int)B, d_tok, d_tgt, idx, dropout_epoch, seed, d_grads, accumulate != 0, d_loss_sum,
+                       match, t->gs);
+        if (t->graphs.size() >= 8) {
+            if (t->graphs.front().exec) cudaGraphExecDestroy(t->graphs.front().exec);
+            t->graphs.erase(t->graphs.begin());
+        }
+        t->graphs.push_back({key_now(), nullptr, 0});
+    } else {
+        t->launches = 0;
+        const bool began = cudaStreamBeginCapture(t->gs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        st = run_batch(*t, (int)B, d_tok, d_tgt, idx, dropout_epoch, seed, d_grads, accumulate != 0, d_loss_sum,
+                       match, t->gs);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = began ? cudaStreamEndCapture(t->gs, &graph) : cudaErrorUnknown;
+        cudaGraphExec_t exec = nullptr;
+        const bool ok = began && !st && ce == cudaSuccess && graph &&
+                        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        if (!ok) {  // capture refused: this trainer runs plain launches from now on
+            (void)cudaGetLastError();
+            t->use_graphs = false;
+            t->launches = 1;
+            st = run_batch(*t, (int)B, d_tok, d_tgt, idx, dropout_epoch, seed, d_grads, accumulate != 0, d_loss_sum,
+                           match, t->gs);
+        } else {
+            if (key_now() != key) {  // something was (re)allocated during the capture: do not keep it
+                cudaGraphExecDestroy(exec);
+                hit->key = key_now();
+                t->use_graphs = false;
+                (void)cudaGetLastError();
+                t->launches = 1;
+                st = run_batch(*t, (int)B, d_tok, d_tgt, idx, dropout_epoch, seed, d_grads, accumulate != 0,
+                               d_loss_sum, match, t->gs);
+            } else {
+                hit->exec = exec;
+                hit->launches = t->launches;
+                KT_CUDA(cudaGraphLaunch(exec, t->gs));
+                t->launches += 1;
+            }
+        }
+    }
+    KT_CUDA(cudaEventRecord(t->gev, t->gs));
+    KT_CUDA(cudaStreamWaitEvent(user, t->gev, 0));
+    return st;
 }
 
 extern "C" ks_status ks_trainer_apply(ks_trainer* t, const float* d_grads, int64_t batch, double lr, double clip,
@@ -2033,7 +2150,8 @@ extern "C" ks_status ks_trainer_step(ks_trainer* t, const int32_t* tok, const in
     KT_CUDA(cudaMemcpyAsync(t->tok.p, tok, (size_t)B * 7 * 4, cudaMemcpyHostToDevice, s));
     KT_CUDA(cudaMemcpyAsync(t->tgt.p, tgt, (size_t)B * t->T * 4, cudaMemcpyHostToDevice, s));
     if (idx) KT_CUDA(cudaMemcpyAsync(t->idx.p, idx, (size_t)B * 8, cudaMemcpyHostToDevice, s));
-    t->launches = 0;
+    k_set_u64x2<<<1, 1, 0, s>>>(t->se.as<unsigned long long>(), seed, (unsigned long long)epoch);
+    t->launches = 1;
     if ((st = run_batch(*t, (int)B, t->tok.as<int>(), t->tgt.as<int>(), idx ? t->idx.as<long long>() : nullptr,
                         epoch, seed, t->grads_tmp.as<float>(), false, res.as<double>(),
                         reinterpret_cast<long long*>(res.as<char>() + 8), s)))

@@ -178,3 +178,35 @@ def test_tf32x3_training_gemms_meet_the_gradient_bar(monkeypatch):
     test_small_trained_gradients_vs_oracle(0.2)
     if os.path.exists(BIG_CKPT):
         test_default_size_gradients_vs_oracle()
+
+
+@pytest.mark.parametrize("stem", ["attn_small_trained", "tiny_encdec_s3423"])
+def test_graph_replayed_batches_equal_plain_launches(stem, monkeypatch):
+    """ks_trainer_loss_grads replays one CUDA graph per batch shape and buffer set
+    (first call plain, second captured, later replayed); seed and epoch are device
+    values written before the replay.  Every call must equal a trainer with graphs
+    off (KS_GRAPHS=0) bit for bit, across epochs (different dropout masks)."""
+    import torch
+    from paper_2404_10162_b200._cabi import Trainer
+    with tempfile.TemporaryDirectory() as tmp:
+        path = with_dropout(golden_path(stem + ".ckpt"), os.path.join(tmp, "drop.ckpt"), (0.2, 0.2))
+        ck = TO.Checkpoint(path)
+        tr = Trainer(path)
+        monkeypatch.setenv("KS_GRAPHS", "0")
+        tr0 = Trainer(path)
+    B = 384
+    tok, tgt = _batch(ck, B, 21)
+    t_tok, t_tgt = _dev(tok, np.int32), _dev(tgt, np.int32)
+    t_idx = _dev(np.arange(B) * 3, np.int64)
+    outs = []
+    for _ in range(2):
+        outs.append((torch.zeros(tr.num_params, dtype=torch.float32, device="cuda"),
+                     torch.zeros(1, dtype=torch.float64, device="cuda"),
+                     torch.zeros(1, dtype=torch.int64, device="cuda")))
+    for epoch in (1, 2, 3, 4, 5):
+        for trainer, (g, loss, match) in ((tr, outs[0]), (tr0, outs[1])):
+            trainer.loss_grads_device(t_tok.data_ptr(), t_tgt.data_ptr(), t_idx.data_ptr(), B, epoch, 7,
+                                      g.data_ptr(), 0, loss.data_ptr(), match.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0][0], outs[1][0]), f"epoch {epoch}: gradients differ"
+        assert float(outs[0][1].item()) == float(outs[1][1].item()) and int(outs[0][2].item()) == int(outs[1][2].item())
