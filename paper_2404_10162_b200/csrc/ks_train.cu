@@ -2047,6 +2047,14 @@ extern "C" ks_status ks_trainer_loss_grads(ks_trainer* t, const int32_t* d_tok, 
     KT_CUDA(cudaEventRecord(t->gev, user));
     KT_CUDA(cudaStreamWaitEvent(t->gs, t->gev, 0));
     k_set_u64x2<<<1, 1, 0, t->gs>>>(t->se.as<unsigned long long>(), seed, (unsigned long long)dropout_epoch);
+    // inputs staged into the trainer's own buffers: the graph key does not follow the
+    // caller's (possibly per-step) input allocations
+    KT_CUDA(cudaMemcpyAsync(t->tok.p, d_tok, (size_t)B * 7 * 4, cudaMemcpyDeviceToDevice, t->gs));
+    KT_CUDA(cudaMemcpyAsync(t->tgt.p, d_tgt, (size_t)B * t->T * 4, cudaMemcpyDeviceToDevice, t->gs));
+    if (idx) KT_CUDA(cudaMemcpyAsync(t->idx.p, idx, (size_t)B * 8, cudaMemcpyDeviceToDevice, t->gs));
+    d_tok = t->tok.as<int32_t>();
+    d_tgt = t->tgt.as<int32_t>();
+    if (idx) idx = t->idx.as<long long>();
     auto P = [](const void* q) { return (long long)reinterpret_cast<uintptr_t>(q); };
     auto key_now = [&]() {
         return std::vector<long long>{B, P(d_tok), P(d_tgt), P(idx), P(d_grads), accumulate ? 1 : 0, P(d_loss_sum),
