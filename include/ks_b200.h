@@ -225,6 +225,13 @@ ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, const int64_
 /* greedy_decode: out_tok B x T. */
 ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok);
 
+/* Page-lock (cudaHostRegister) / release a caller buffer.  Result buffers of the
+ * host-buffer calls above that are page-locked receive the device-to-host copy
+ * directly (no staging copy); callers reusing result buffers call by call
+ * register them once.  No reference counterpart (a B200-side addition). */
+ks_status ks_host_register(void* p, int64_t bytes);
+ks_status ks_host_unregister(void* p);
+
 /* Device-resident variant: every pointer is device memory; runs on `stream`
  * (a cudaStream_t, NULL = legacy default) and returns without synchronising. */
 ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok, const int64_t* d_desc,

@@ -9,6 +9,7 @@ fallback.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 
 import numpy as np
@@ -81,6 +82,7 @@ EXPORTS = [
     "ks_engine_destroy", "ks_engine_num_positions", "ks_engine_vocab_size",
     "ks_engine_precision", "ks_engine_last_launch_count", "ks_engine_set_chunk",
     "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
+    "ks_host_register", "ks_host_unregister",
     "ks_engine_profile_reset", "ks_engine_profile_gemm_ms", "ks_engine_profile_launches",
     "ks_engine_profile_launches_ex",
     "ks_beam_search_batch_hooked", "ks_topk_metrics_batch",
@@ -89,6 +91,25 @@ EXPORTS = [
     "ks_trainer_apply", "ks_trainer_step", "ks_trainer_evaluate", "ks_trainer_export", "ks_trainer_import",
     "ks_trainer_to_reference_layout",
 ]
+
+
+def pin_results(out):
+    """Page-lock the result arrays of a beam() call for their lifetime, so later
+    calls reusing them (`out=`) receive the device-to-host copy directly.
+    Registration costs tens of ms for a 65k-config result set: worth it only for a
+    long-running loop over the same buffers."""
+    for a in out.values():
+        if isinstance(a, np.ndarray):
+            _pin(a)
+    return out
+
+
+def _pin(a):
+    """Page-lock a numpy array for the array's lifetime (ks_host_register)."""
+    L = lib()
+    ptr = a.ctypes.data
+    if L.ks_host_register(C.c_void_p(ptr), a.nbytes) == 0:
+        weakref.finalize(a, L.ks_host_unregister, C.c_void_p(ptr))
 
 
 def _p(a, ct):
@@ -109,6 +130,8 @@ def lib():
     L.ks_last_error.restype = C.c_char_p
     L.ks_last_error_field.restype = C.c_char_p
     L.ks_checkpoint_load.argtypes = [C.c_char_p, P(vp)]
+    L.ks_host_register.argtypes = [vp, C.c_int64]
+    L.ks_host_unregister.argtypes = [vp]
     L.ks_checkpoint_error_kind.restype = i32
     L.ks_checkpoint_free.argtypes = [vp]
     L.ks_checkpoint_header.argtypes = [vp, C.c_char_p]
@@ -230,6 +253,7 @@ class Engine:
         if out is not None and out["tokens"].shape == (B, k, self.T):
             out_tok, out_lp, cnt = out["tokens"], out["log_prob"], out["count"]
             st, fp, fs = out["status"], out["fail_pred"], out["fail_step"]
+
         else:
             out_tok = np.empty((B, k, self.T), np.int32)
             out_lp = np.empty((B, k), np.float64)

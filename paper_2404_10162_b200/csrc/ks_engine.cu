@@ -1507,6 +1507,16 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
         E.ofpred.ensure((size_t)C * 4) || E.ofstep.ensure((size_t)C * 4))
         return set_error(KS_ERR_CUDA, "output allocation failed");
     if ((st = ensure_workspace(E, C, k))) return st;
+    // page-locked result buffers take the device-to-host copy directly
+    auto pinned = [](const void* p) {
+        if (!p) return true;
+        cudaPointerAttributes a{};
+        const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+        (void)cudaGetLastError();
+        return ok;
+    };
+    const bool direct = pinned(out_tok) && (greedy || (pinned(out_lp) && pinned(out_count) && pinned(out_status) &&
+                                                         pinned(out_fpred) && pinned(out_fstep)));
     for (int64_t c0 = 0; c0 < B; c0 += C) {
         const int64_t n = std::min<int64_t>(C, B - c0);
         int32_t* htok = E.h_in.as<int32_t>();
@@ -1523,6 +1533,18 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
                                   E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>(),
                                   B <= C)))
             return st;
+        if (direct) {
+            KS_CUDA(cudaMemcpyAsync(out_tok + c0 * k * T, E.otok.p, (size_t)n * k * T * 4, cudaMemcpyDeviceToHost, E.stream));
+            if (!greedy) {
+                if (out_lp) KS_CUDA(cudaMemcpyAsync(out_lp + c0 * k, E.olp.p, (size_t)n * k * 8, cudaMemcpyDeviceToHost, E.stream));
+                if (out_count) KS_CUDA(cudaMemcpyAsync(out_count + c0, E.ocount.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+                if (out_status) KS_CUDA(cudaMemcpyAsync(out_status + c0, E.ostatus.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+                if (out_fpred) KS_CUDA(cudaMemcpyAsync(out_fpred + c0, E.ofpred.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+                if (out_fstep) KS_CUDA(cudaMemcpyAsync(out_fstep + c0, E.ofstep.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
+            }
+            KS_CUDA(cudaStreamSynchronize(E.stream));
+            continue;
+        }
         char* ho = E.h_out.as<char>();
         int32_t* h_tok = reinterpret_cast<int32_t*>(ho);
         double* h_lp = reinterpret_cast<double*>(ho + (size_t)C * k * T * 4);
@@ -1645,6 +1667,27 @@ extern "C" ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, c
     for (int p = 0; p < T; ++p) out_pos_matches[p] = (int64_t)h[(size_t)p];
     *out_perfect = (int64_t)h[(size_t)T];
     if (E.prof) collect_profile(E);
+    return KS_OK;
+}
+
+extern "C" ks_status ks_host_register(void* p, int64_t bytes) {
+    if (!p || bytes <= 0) return set_error(KS_ERR_PARAMETER, "null or empty host buffer");
+    const cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        (void)cudaGetLastError();
+        return KS_OK;
+    }
+    if (e != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+    return KS_OK;
+}
+
+extern "C" ks_status ks_host_unregister(void* p) {
+    if (!p) return set_error(KS_ERR_PARAMETER, "null host buffer");
+    const cudaError_t e = cudaHostUnregister(p);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return set_error(KS_ERR_CUDA, std::string("cudaHostUnregister: ") + cudaGetErrorString(e));
+    }
     return KS_OK;
 }
 

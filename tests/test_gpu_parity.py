@@ -276,3 +276,19 @@ def test_graph_replay_follows_new_inputs_and_predicates(monkeypatch):
         a = o.beam(tok, k, None, preds, threads=8)
         n, ties, bad = compare_beams(g, a)
         assert not bad, f"call {call}: {len(bad)} mismatching of {n} (ties {ties}); first {bad[:5]}"
+
+
+def test_page_locked_result_buffers():
+    """Result arrays page-locked with pin_results (ks_host_register) receive the
+    device-to-host copy directly; the results equal the staged path's."""
+    from paper_2404_10162_b200._cabi import pin_results
+    path = golden_path("attn_small_trained.ckpt")
+    o, e = OracleModel(path), engine(path, "f16x3")
+    tok = random_tokens(o, 700, 51)
+    preds = oracle_preds(o, [("membership", None), ("budget", ({n: 1.0 for n in o.names}, 28.0))])
+    ref = e.beam(tok, 5, None, preds)
+    out = pin_results(e.beam(tok, 5, None, preds))
+    for _ in range(2):
+        out = e.beam(tok, 5, None, preds, out=out)
+        for key in ref:
+            np.testing.assert_array_equal(out[key], ref[key], err_msg=key)
