@@ -1180,11 +1180,14 @@ void launch_split_cat(ks_trainer& t, cudaStream_t s, const float* src, long long
 // from k_cell_bwd), so no max-reduction pass over that operand is needed.
 ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
                   long long lda, const float* B, long long ldb, float beta, float* C, long long ldc,
-                  bool b_is_weight = false, const int* a_amax = nullptr, const int* b_amax = nullptr) {
+                  bool b_is_weight = false, const int* a_amax = nullptr, const int* b_amax = nullptr,
+                  bool b_cache = false) {
     if (M == 0 || N == 0) return KS_OK;
     if (K == 0) return beta == 1.0f ? KS_OK : set_error(KS_ERR_SHAPE, "empty GEMM reduction");
-    // narrow outputs (heads, attention, slot rows) stay fp32 SGEMMs
-    if (!t.tf32x3 || M < 128 || N < 128)
+    // narrow outputs (heads, attention, and slot rows unless their B split is shared
+    // with the dense weight gradient, F16X3) stay fp32 SGEMMs
+    const bool narrow = (t.f16x3 && b_cache) ? (std::max(M, N) < 128 || std::min(M, N) < 16) : (M < 128 || N < 128);
+    if (!t.tf32x3 || narrow)
         return gemm_one(t, ta, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_PEDANTIC);
 
     cudaStream_t s;
@@ -1219,15 +1222,22 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
         };
         const __half* b16;
         const int* amaxB;
-        if (b_is_weight) {
+        if (b_is_weight || b_cache) {
+            // weights, and operands two GEMMs of this step share (b_cache: the dZ of every
+            // step, B of both the dense and the slot-row weight gradients), split once
             const std::pair<const float*, bool> key(B, tb);
             auto it = t.wsplit.find(key);
             if (it == t.wsplit.end()) {
                 if (t.wsplit_used == t.wsplit_store.size()) t.wsplit_store.emplace_back(new DBuf[2]);
                 DBuf* buf = t.wsplit_store[t.wsplit_used++].get();
-                if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
-                const int slot = t.scal_used++;
-                if ((st = split_b(buf[0], nullptr, slot))) return st;
+                int slot;
+                if (b_amax) {
+                    slot = (int)(b_amax - slots);
+                } else {
+                    if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
+                    slot = t.scal_used++;
+                }
+                if ((st = split_b(buf[0], b_amax, slot))) return st;
                 it = t.wsplit.emplace(key, std::make_pair(buf, bc)).first;
                 t.wslot[key] = slot;
             }
@@ -1650,10 +1660,11 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
     }
     // decoder weight gradients: one GEMM over all (position, row) pairs
     if ((st = gemm_rm(t, true, false, Kd, 4LL * Hd, (long long)T * m, Xd, Kd, t.dZd.as<float>(), 4LL * Hd, 1.0f,
-                      G + D.wd(), 4LL * Hd, false, act_amax, dzd_amax)))
+                      G + D.wd(), 4LL * Hd, false, act_amax, dzd_amax, dzd_amax != nullptr)))
         return st;
     if ((st = gemm_rm(t, true, false, D.S + 1, 4LL * Hd, (long long)T * m, t.dec_sm.as<float>(), D.S + 1,
-                      t.dZd.as<float>(), 4LL * Hd, 1.0f, G + D.ws(), 4LL * Hd)))
+                      t.dZd.as<float>(), 4LL * Hd, 1.0f, G + D.ws(), 4LL * Hd, false, act_amax, dzd_amax,
+                      dzd_amax != nullptr)))
         return st;
     for (int p = 0; p < T; ++p) {
         const int V = t.vsize[(size_t)p];
@@ -1735,10 +1746,11 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         }
         float* Hx = t.Hx[dir].as<float>();
         if ((st = gemm_rm(t, true, false, H, 4LL * H, 7 * m, Hx, H, t.dZe[dir].as<float>(), 4LL * H, 1.0f,
-                          G + L.wd(), 4LL * H, false, act_amax, dze_amax)))
+                          G + L.wd(), 4LL * H, false, act_amax, dze_amax, dze_amax != nullptr)))
             return st;
         if ((st = gemm_rm(t, true, false, t.d_in + 1, 4LL * H, 7 * m, t.enc_sm[dir].as<float>(), t.d_in + 1,
-                          t.dZe[dir].as<float>(), 4LL * H, 1.0f, G + L.ws(), 4LL * H)))
+                          t.dZe[dir].as<float>(), 4LL * H, 1.0f, G + L.ws(), 4LL * H, false, act_amax, dze_amax,
+                          dze_amax != nullptr)))
             return st;
     }
     const cudaError_t err = cudaGetLastError();
