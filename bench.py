@@ -244,6 +244,25 @@ def reference_rate(path, tok, threads, seconds_target=15.0, max_configs=None):
     return n / dt, n, dt
 
 
+def engine_libs_mapped():
+    """Our engine libraries mapped into this process (/proc/self/maps)."""
+    try:
+        with open("/proc/self/maps") as f:
+            maps = f.read()
+    except OSError:
+        return []
+    names = ("libks_b200", "libkernelseer_b200", "_kernelseer_b200")
+    return sorted({l.split()[-1] for l in maps.splitlines() if any(n in l for n in names)})
+
+
+def assert_no_engine_mapped():
+    """The reference arm times the unmodified reference only: none of our
+    libraries may be mapped next to it."""
+    libs = engine_libs_mapped()
+    if libs:
+        raise RuntimeError(f"reference arm has engine libraries mapped: {libs}")
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -254,6 +273,7 @@ def run_reference_arm(args):
     path = model_path()
     desc = descriptors(args.configs * max(1, args.gpus), KERNEL)
     tok, bad = RefModel(path).encode(desc)
+    assert_no_engine_mapped()
     threads = os.cpu_count() or 1
     # one step = a bounded sample sized so the whole W+K run ends within minutes
     rate, n, dt = reference_rate(path, tok, threads, seconds_target=6.0)
@@ -486,6 +506,8 @@ def run_train_reference_arm(args):
     path = model_path()
     tok, tgt, ck = train_data(path, 4096)
     threads = os.cpu_count() or 1
+    reference_train_rate(path, tok, tgt, threads, 1)  # loads oracle/_ref
+    assert_no_engine_mapped()
     rate0, _ = reference_train_rate(path, tok, tgt, threads, max(threads, 16))
     n = int(min(4096, max(256, rate0 * 6.0)))
     times = []

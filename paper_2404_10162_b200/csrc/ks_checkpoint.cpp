@@ -8,6 +8,7 @@
 // malformed, io.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -37,6 +38,17 @@ ks_status fail(int kind, const std::string& msg) {
 }  // namespace
 
 extern "C" int32_t ks_checkpoint_error_kind(void) { return g_ck_kind; }
+
+// The header keys the reference reader accepts (data.cpp:524-613); anything else
+// is CheckpointError(malformed) there, and here.
+static bool known_key(const std::string& k) {
+    static const char* plain[] = {"variant", "kernel", "precision", "encoder_state_size",
+                                  "pre_attention_size", "post_attention_size", "attention_dense_nodes",
+                                  "decoder_cell_size", "dropout", "recurrent_dropout", "output_params"};
+    for (const char* p : plain)
+        if (k == p) return true;
+    return k.rfind("input_vocab.", 0) == 0 || k.rfind("param.", 0) == 0;
+}
 
 extern "C" ks_status ks_checkpoint_load(const char* path, ks_checkpoint** out) {
     enum { VERSION = 0, TRUNCATED = 1, SHAPE = 2, MALFORMED = 3, IO = 4 };
@@ -91,7 +103,41 @@ extern "C" ks_status ks_checkpoint_load(const char* path, ks_checkpoint** out) {
                 delete ck;
                 return fail(SHAPE, "tensor " + t.name + " has no shape");
             }
+            // every reference tensor is rank 1 or 2 (models.cpp:178-259); dims are
+            // positive (a zero / negative dim would wrap the payload byte count)
+            if (t.dims.size() > 3) {
+                delete ck;
+                return fail(SHAPE, "tensor " + t.name + " has rank " + std::to_string(t.dims.size()));
+            }
+            for (int32_t dd : t.dims)
+                if (dd <= 0) {
+                    delete ck;
+                    return fail(SHAPE, "tensor " + t.name + " has a non-positive dimension");
+                }
             ck->tensors.push_back(std::move(t));
+        } else if (key == "conv_layers") {
+            // each layer is exactly three integers (data.cpp:566-578)
+            std::stringstream ss(val);
+            std::string layer;
+            while (std::getline(ss, layer, ';')) {
+                int n = 0;
+                std::stringstream ls(layer);
+                std::string tokn;
+                bool bad = false;
+                while (std::getline(ls, tokn, ',')) {
+                    char* end = nullptr;
+                    std::strtol(tokn.c_str(), &end, 10);
+                    bad = bad || tokn.empty() || *end != '\0';
+                    ++n;
+                }
+                if (bad || n != 3) {
+                    delete ck;
+                    return fail(MALFORMED, "bad conv layer spec: " + layer);
+                }
+            }
+        } else if (!known_key(key)) {
+            delete ck;
+            return fail(MALFORMED, "unknown header key '" + key + "'");
         }
         ck->header.emplace_back(std::move(key), std::move(val));
     }

@@ -888,8 +888,17 @@ namespace {
 
 using namespace kst;
 
-// bumped on every (re)allocation: captured training-step graphs bake buffer addresses
-std::atomic<unsigned long long> g_train_alloc_gen{0};
+// Allocation generation of the trainer whose API call is running on this thread
+// (bumped on every (re)allocation of its buffers): captured training-step graphs
+// bake buffer addresses, so a trainer's graph key includes ITS generation only --
+// another trainer allocating (another GPU's thread, a second trainer in the same
+// process) neither invalidates its graphs nor trips its post-capture check.
+thread_local unsigned long long* tl_alloc_gen = nullptr;
+struct GenScope {
+    unsigned long long* prev;
+    explicit GenScope(unsigned long long* g) : prev(tl_alloc_gen) { tl_alloc_gen = g; }
+    ~GenScope() { tl_alloc_gen = prev; }
+};
 
 struct DBuf {
     void* p = nullptr;
@@ -899,7 +908,7 @@ struct DBuf {
     }
     cudaError_t ensure(size_t n) {
         if (n <= bytes) return cudaSuccess;
-        g_train_alloc_gen.fetch_add(1);
+        if (tl_alloc_gen) ++*tl_alloc_gen;
         if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
@@ -990,6 +999,8 @@ struct ks_trainer {
     // CUDA graphs of whole ks_trainer_loss_grads batches on the trainer's own stream
     // (the caller's stream may be the legacy default stream, which cannot be captured)
     bool use_graphs = true;
+    unsigned long long alloc_gen = 0;  // this trainer's buffer generation (GenScope)
+    size_t head_attr = 0;              // k_head's dynamic-smem attribute set so far (on this trainer's device)
     cudaStream_t gs = nullptr;
     cudaEvent_t gev = nullptr;
     struct GraphEntry {
@@ -1153,7 +1164,21 @@ ks_status gemm_lt16(ks_trainer& t, cudaStream_t s, bool tb, long long M, long lo
         it = t.lt_plans.emplace(key, pl).first;
     }
     const LtPlan& pl = it->second;
-    if (!pl.usable) return set_error(KS_ERR_UNSUPPORTED, "no cuBLASLt fp16 algorithm for a training GEMM shape");
+    if (!pl.usable) {
+        // no cuBLASLt algorithm for this shape (odd M such as S + 1 or d_in + 1):
+        // the same tripled-K fp16 product through cublasGemmEx (fp32 compute),
+        // alpha / beta read from device memory like the cuBLASLt path
+        KT_BLAS(cublasSetStream(t.blas, s));
+        KT_BLAS(cublasSetPointerMode(t.blas, CUBLAS_POINTER_MODE_DEVICE));
+        const cublasStatus_t ge =
+            cublasGemmEx(t.blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_OP_N, (int)N, (int)M, (int)K, alpha, B,
+                         CUDA_R_16F, (int)ldb, A, CUDA_R_16F, (int)lda, beta, C, CUDA_R_32F, (int)ldc,
+                         CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+        cublasSetPointerMode(t.blas, CUBLAS_POINTER_MODE_HOST);
+        if (ge != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cublasGemmEx F16X3 fallback status " + std::to_string((int)ge));
+        ++t.launches;
+        return KS_OK;
+    }
     const cublasStatus_t e = cublasLtMatmul(t.lt, pl.op, alpha, B, pl.la, A, pl.lb, beta, C, pl.lc, C, pl.lc, &pl.algo,
                                             t.blas_ws.p, t.blas_ws.bytes, s);
     if (e != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cuBLASLt F16X3 GEMM status " + std::to_string((int)e));
@@ -1578,10 +1603,10 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         const int hw = 8;
         const size_t smem = ((size_t)Hd * ha.V + (size_t)hw * (Hd + 32)) * 4;
         if (smem > 200 * 1024) return set_error(KS_ERR_UNSUPPORTED, "head too large for the head kernel");
-        static size_t head_attr = 0;
-        if (smem > 48 * 1024 && smem > head_attr) {
+        // function attributes are per device: each trainer sets it on its own device
+        if (smem > 48 * 1024 && smem > t.head_attr) {
             KT_CUDA(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            head_attr = smem;
+            t.head_attr = smem;
         }
         k_head<<<(unsigned)std::min<long long>(blocks(m, hw), 148LL * 4), hw * 32, smem, s>>>(ha);
         ++t.launches;
@@ -2037,6 +2062,7 @@ extern "C" ks_status ks_trainer_loss_grads(ks_trainer* t, const int32_t* d_tok, 
                                            const int64_t* d_idx, int64_t B, int64_t dropout_epoch, uint64_t seed,
                                            float* d_grads, int32_t accumulate, double* d_loss_sum,
                                            int64_t* d_matches, void* stream) {
+    GenScope gen_scope_(t ? &t->alloc_gen : nullptr);
     if (!t) return set_error(KS_ERR_PARAMETER, "null trainer");
     if (B < 0 || B > (1LL << 24)) return set_error(KS_ERR_PARAMETER, "batch size out of range");
     if (B == 0) return KS_OK;
@@ -2071,7 +2097,7 @@ extern "C" ks_status ks_trainer_loss_grads(ks_trainer* t, const int32_t* d_tok, 
     auto key_now = [&]() {
         return std::vector<long long>{B, P(d_tok), P(d_tgt), P(idx), P(d_grads), accumulate ? 1 : 0, P(d_loss_sum),
                                       P(match), dropout_epoch >= 0 ? 1 : 0,
-                                      (long long)g_train_alloc_gen.load()};
+                                      (long long)t->alloc_gen};
     };
     const std::vector<long long> key = key_now();
     ks_trainer::GraphEntry* hit = nullptr;
@@ -2110,9 +2136,10 @@ extern "C" ks_status ks_trainer_loss_grads(ks_trainer* t, const int32_t* d_tok, 
                            match, t->gs);
         } else {
             if (key_now() != key) {  // something was (re)allocated during the capture: do not keep it
+                // drop this entry (re-captured on a later call under the new key);
+                // graphs stay on
                 cudaGraphExecDestroy(exec);
                 hit->key = key_now();
-                t->use_graphs = false;
                 (void)cudaGetLastError();
                 t->launches = 1;
                 st = run_batch(*t, (int)B, d_tok, d_tgt, idx, dropout_epoch, seed, d_grads, accumulate != 0,
@@ -2132,6 +2159,7 @@ extern "C" ks_status ks_trainer_loss_grads(ks_trainer* t, const int32_t* d_tok, 
 
 extern "C" ks_status ks_trainer_apply(ks_trainer* t, const float* d_grads, int64_t batch, double lr, double clip,
                                       void* stream) {
+    GenScope gen_scope_(t ? &t->alloc_gen : nullptr);
     if (!t || !d_grads) return set_error(KS_ERR_PARAMETER, "null argument");
     if (batch < 1) return set_error(KS_ERR_PARAMETER, "batch must be >= 1");
     cudaSetDevice(t->device);
@@ -2157,6 +2185,7 @@ extern "C" ks_status ks_trainer_apply(ks_trainer* t, const float* d_grads, int64
 extern "C" ks_status ks_trainer_step(ks_trainer* t, const int32_t* tok, const int32_t* tgt, const int64_t* idx,
                                      int64_t B, int64_t epoch, uint64_t seed, double lr, double clip,
                                      double* out_loss_sum, int64_t* out_matches) {
+    GenScope gen_scope_(t ? &t->alloc_gen : nullptr);
     if (!t || !tok || !tgt) return set_error(KS_ERR_PARAMETER, "null argument");
     if (B < 1) return set_error(KS_ERR_PARAMETER, "batch must be >= 1");
     cudaSetDevice(t->device);
@@ -2189,6 +2218,7 @@ extern "C" ks_status ks_trainer_step(ks_trainer* t, const int32_t* tok, const in
 
 extern "C" ks_status ks_trainer_evaluate(ks_trainer* t, const int32_t* tok, const int32_t* tgt, int64_t B,
                                          double* out_loss_sum, int64_t* out_matches) {
+    GenScope gen_scope_(t ? &t->alloc_gen : nullptr);
     if (!t || !tok || !tgt) return set_error(KS_ERR_PARAMETER, "null argument");
     if (B < 1) return set_error(KS_ERR_PARAMETER, "batch must be >= 1");
     cudaSetDevice(t->device);
@@ -2221,6 +2251,7 @@ extern "C" ks_status ks_trainer_export(const ks_trainer* t, float* host_ref_flat
 }
 
 extern "C" ks_status ks_trainer_import(ks_trainer* t, const float* host_ref_flat) {
+    GenScope gen_scope_(t ? &t->alloc_gen : nullptr);
     if (!t || !host_ref_flat) return set_error(KS_ERR_PARAMETER, "null argument");
     cudaSetDevice(t->device);
     std::vector<float> host((size_t)t->nparams, 0.0f);
