@@ -36,6 +36,7 @@
 #include <vector>
 
 struct ks_engine;
+struct ks_engine_group;
 
 namespace kernelseer {
 
@@ -73,6 +74,37 @@ private:
     std::string predicate_;
     int step_;
 };
+
+// ---------------------------------------------------------------- tensors
+namespace nn {
+// The host fp64 tensor of the reference (tensor.hpp:13-55), reduced to what
+// callers of the decode API touch: distributions returned by
+// SequencePredictor::step / model_forward.
+class Tensor {
+public:
+    Tensor() = default;
+    explicit Tensor(std::vector<int> shape);
+    Tensor(std::vector<int> shape, std::vector<double> data);
+    static Tensor vec(std::vector<double> data);
+    const std::vector<int>& shape() const { return shape_; }
+    int rank() const { return static_cast<int>(shape_.size()); }
+    int dim(int i) const { return shape_[static_cast<std::size_t>(i)]; }
+    int size() const { return static_cast<int>(data_.size()); }
+    bool empty() const { return data_.empty(); }
+    double* data() { return data_.data(); }
+    const double* data() const { return data_.data(); }
+    std::vector<double>& values() { return data_; }
+    const std::vector<double>& values() const { return data_; }
+    double& operator[](int i) { return data_[static_cast<std::size_t>(i)]; }
+    double operator[](int i) const { return data_[static_cast<std::size_t>(i)]; }
+    double& at(int i, int j) { return data_[static_cast<std::size_t>(i) * shape_[1] + j]; }
+    double at(int i, int j) const { return data_[static_cast<std::size_t>(i) * shape_[1] + j]; }
+
+private:
+    std::vector<int> shape_;
+    std::vector<double> data_;
+};
+}  // namespace nn
 
 // ---------------------------------------------------------------- problems
 enum class Precision { full, half };
@@ -231,24 +263,84 @@ struct ModelParams {
 KernelSpec spec_of(const ModelParams& params);
 ModelParams load_checkpoint(const std::string& path);
 
+// Benchmark / parity workloads (B200 addition, ks_synthetic_descriptors):
+// configs start..start+count-1, config i drawn from Rng::derive(seed, i)
+// uniformly with replacement over the model's input vocabulary.
+std::vector<ProblemDescriptor> synthetic_descriptors(const ModelParams& params, std::int64_t count,
+                                                     std::uint64_t seed = 2404, std::int64_t start = 0);
+
 // GEMM arithmetic of the engine (see ks_b200.h).
 enum class GemmPrecision { f16x3 = 0, fp32 = 1, bf16 = 2 };
 
-// Stepping facade of the reference, here a handle on a device engine built
-// from the params (weights packed and uploaded once, shared by copies).
+// Per-input work shared by all hypotheses (models.hpp:65-70).  The encoder
+// state lives on the device, so the host record keeps the input tokens; the
+// reference's activations / h / c / dists members are kept for source
+// compatibility and stay empty.
+struct EncodedInput {
+    TokenSequence input;
+    std::vector<nn::Tensor> activations;
+    nn::Tensor h, c;
+    std::vector<nn::Tensor> dists;
+};
+
+// Per-hypothesis decoder state (models.hpp:72-76): the position and the tokens
+// fed back so far (fed[q] = token emitted at position q); h / c are not
+// materialised on the host.
+struct DecoderState {
+    nn::Tensor h, c;
+    int position = 0;
+    std::vector<int> fed;
+};
+
+// Stepping facade of the reference (models.hpp:78-98), here a handle on a
+// device engine built from the params (weights packed and uploaded once,
+// shared by copies).  Beam search does not go through step(): it runs whole
+// batches on the device (beam_search_batch).  step() stays functional for API
+// compatibility as a batch-of-1 device call (ks_forward_batch) that replays
+// the decoder over the fed-back prefix: O(position) device work per call.
 class SequencePredictor {
 public:
-    explicit SequencePredictor(const ModelParams& params, int device = 0,
+    // device = kAllDevices: one engine per visible GPU, batches sharded across
+    // them (the B200 counterpart of parallel_stripes over all host threads);
+    // device >= 0: that GPU only.
+    static constexpr int kAllDevices = -1;
+    explicit SequencePredictor(const ModelParams& params, int device = kAllDevices,
                                GemmPrecision precision = GemmPrecision::f16x3);
+    SequencePredictor(const ModelParams& params, std::vector<int> devices,
+                      GemmPrecision precision = GemmPrecision::f16x3);
     int num_positions() const;
     int vocab_size(int position) const;
     const ModelParams& params() const { return *params_; }
-    ks_engine* engine() const;
+    ks_engine* engine() const;           // the first device's engine
+    ks_engine_group* group() const;      // every device's engine
+    int num_devices() const;
+
+    EncodedInput encode(const TokenSequence& input) const;
+    DecoderState initial_state(const EncodedInput& enc) const;
+    // Distribution for state.position; prev_token is the token emitted at the
+    // previous position (ignored at position 0, which consumes GO).  Advances
+    // the state; StateError past the last position, IndexError for a
+    // prev_token outside the previous position's vocabulary.
+    nn::Tensor step(const EncodedInput& enc, DecoderState& state, int prev_token) const;
 
 private:
+    void create(const std::vector<int>& devices, GemmPrecision precision);
     const ModelParams* params_;
-    std::shared_ptr<ks_engine> engine_;
+    std::shared_ptr<ks_engine_group> group_;
 };
+
+// model_forward (models.hpp:100-103, models.cpp:495-514): per-position output
+// distributions in infer mode; with teacher tokens the decoder consumes them
+// as feedback, otherwise its own argmax.
+std::vector<nn::Tensor> model_forward(const ModelParams& params, const TokenSequence& input,
+                                      const std::vector<int>* teacher = nullptr);
+// Same on an existing predictor's engine, and batched: one device pass over
+// all inputs (teachers empty or one per input).  scores (optional) receives
+// each input's sequence score sum_p log(max(p_p[token_p], 1e-300)).
+std::vector<std::vector<nn::Tensor>> model_forward_batch(const SequencePredictor& predictor,
+                                                         std::span<const TokenSequence> inputs,
+                                                         std::span<const std::vector<int>> teachers = {},
+                                                         std::vector<double>* scores = nullptr);
 
 struct ScoredSequence {
     TokenSequence tokens;

@@ -15,6 +15,8 @@
  *   ks_beam_search_batch       beam_search /            src/decoding.cpp:27-103, 126-135
  *                              constrained_beam_search  include/kernelseer/decoding.hpp:28-36
  *   ks_greedy_batch            greedy_decode            src/decoding.cpp:107-124, include/kernelseer/decoding.hpp:23-24
+ *   ks_forward_batch           model_forward /          src/models.cpp:495-514, 387-493,
+ *                              SequencePredictor::step  include/kernelseer/models.hpp:80-103
  *   ks_pred (typed programs)   ConstraintPredicate +    include/kernelseer/constraints.hpp:45-63,
  *                              membership_predicate /   src/constraints.cpp:198-242
  *                              resource_budget_predicate
@@ -25,6 +27,8 @@
  *   the batch entry points     parallel_stripes fan-out include/kernelseer/parallel.hpp:14-27 as used
  *                              in topk_metrics          src/eval.cpp:105-137
  *   ks_topk_metrics_batch      topk_metrics scoring     src/eval.cpp:100-146
+ *   ks_engine_group_*, ks_group_*  parallel_stripes     include/kernelseer/parallel.hpp:14-27,
+ *                              (multi-GPU sharding)     src/eval.cpp:105-137
  */
 #ifndef KS_B200_H
 #define KS_B200_H
@@ -137,6 +141,19 @@ ks_status ks_engine_set_chunk(ks_engine* eng, int64_t configs_per_chunk);
 ks_status ks_encode_problems(const ks_engine* eng, const int64_t* desc, int64_t B,
                              int32_t allow_nearest, int32_t* tok, int64_t* bad_row);
 
+/* Synthetic problem descriptors (benchmark / parity workloads):
+ * config start+i (i < count) draws each of the 7 input fields uniformly with
+ * replacement from the vocabulary (input_sizes[7], input_values concatenated per
+ * field), one Rng::uniform_int per field in order n,c,h,w,k,y,x, from its own
+ * stream Rng::derive(seed, start + i) (rng.hpp:19-43).  out_desc: count x 7.
+ * The reference's generate_synthetic (data.cpp:348-395) draws unique grid
+ * points and cannot produce 64k / 1M configs; no other reference counterpart. */
+ks_status ks_synthetic_descriptors(const int32_t* input_sizes, const int64_t* input_values,
+                                   uint64_t seed, int64_t start, int64_t count, int64_t* out_desc);
+/* The same over an engine's model input vocabulary. */
+ks_status ks_engine_synthetic_descriptors(const ks_engine* eng, uint64_t seed, int64_t start,
+                                          int64_t count, int64_t* out_desc);
+
 /* ------------------------------------------------------------------------- */
 /* Typed predicate programs.  ConstraintPredicate::fn is an opaque callable in  */
 /* the reference (constraints.hpp:49); the engine evaluates these typed forms */
@@ -225,6 +242,18 @@ ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, const int64_
 /* greedy_decode: out_tok B x T. */
 ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok);
 
+/* model_forward (models.cpp:495-514) for B inputs at once: the decoder runs
+ * greedily over all T positions, feeding back teacher[b][p] (B x T token ids)
+ * when teacher != NULL, else its own argmax (lowest index on ties).
+ *   out_dist  B x sum_p V_p: each position's softmax distribution (nn.cpp:215-226)
+ *   out_tok   B x T (optional): the tokens fed back (teacher or argmax)
+ *   out_score B (optional): sum_p log(max(dist_p[tok_p], 1e-300)), the
+ *             teacher-forced sequence score of decoding_test.cpp:38-46
+ * Also the device half of SequencePredictor::encode / initial_state / step
+ * (models.hpp:80-98) in the C++ and Python layers. */
+ks_status ks_forward_batch(ks_engine* eng, const int32_t* tok, const int32_t* teacher, int64_t B,
+                           double* out_dist, int32_t* out_tok, double* out_score);
+
 /* Page-lock (cudaHostRegister) / release a caller buffer.  Result buffers of the
  * host-buffer calls above that are page-locked receive the device-to-host copy
  * directly (no staging copy); callers reusing result buffers call by call
@@ -240,6 +269,43 @@ ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok, const int6
                                 int32_t* d_out_count, int32_t* d_out_status,
                                 int32_t* d_out_fail_pred, int32_t* d_out_fail_step,
                                 void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Engine groups: one engine per GPU, a batch sharded across them.  Replaces   */
+/* parallel_stripes (parallel.hpp:14-27) as used by topk_metrics              */
+/* (eval.cpp:105-137): configs are independent, so each device decodes a      */
+/* contiguous balanced shard [g*B/G, (g+1)*B/G) on its own host thread and    */
+/* writes its slice of the caller's outputs -- no collective, config order    */
+/* preserved.  Outputs and errors are those of the single-engine calls; a     */
+/* host predicate hook sees the caller's config indices and may be called     */
+/* from several threads at once (one per device).                             */
+/* ------------------------------------------------------------------------- */
+typedef struct ks_engine_group ks_engine_group;
+
+/* Number of visible CUDA devices. */
+int32_t ks_device_count(void);
+/* devices == NULL / n_devices <= 0: every visible device.  The same device may
+ * appear more than once (several engines sharing a GPU). */
+ks_status ks_engine_group_create_from_checkpoint(const char* path, const int32_t* devices, int32_t n_devices,
+                                                 int32_t precision, ks_engine_group** out);
+ks_status ks_engine_group_create(const ks_model_desc* model, const int32_t* devices, int32_t n_devices,
+                                 int32_t precision, ks_engine_group** out);
+void ks_engine_group_destroy(ks_engine_group* g);
+int32_t ks_engine_group_size(const ks_engine_group* g);
+ks_engine* ks_engine_group_engine(const ks_engine_group* g, int32_t i);
+ks_status ks_group_beam_search_batch(ks_engine_group* g, const int32_t* tok, const int64_t* desc, int64_t B,
+                                     int32_t beam_width, const ks_pred* preds, int32_t n_preds,
+                                     ks_host_pred_fn hook, void* user, int32_t* out_tok, double* out_lp,
+                                     int32_t* out_count, int32_t* out_status, int32_t* out_fail_pred,
+                                     int32_t* out_fail_step);
+ks_status ks_group_greedy_batch(ks_engine_group* g, const int32_t* tok, int64_t B, int32_t* out_tok);
+ks_status ks_group_forward_batch(ks_engine_group* g, const int32_t* tok, const int32_t* teacher, int64_t B,
+                                 double* out_dist, int32_t* out_tok, double* out_score);
+/* Counters summed over the shards. */
+ks_status ks_group_topk_metrics_batch(ks_engine_group* g, const int32_t* tok, const int64_t* desc,
+                                      const int32_t* truth, int64_t B, int32_t beam_width, const ks_pred* preds,
+                                      int32_t n_preds, ks_host_pred_fn hook, void* user,
+                                      int64_t* out_pos_matches, int64_t* out_perfect);
 
 /* Kernel-level timing hook for bench.py: accumulated device milliseconds of
  * the gate-GEMM launches (CUDA events on the launching stream) since the last

@@ -267,6 +267,10 @@ def rlib():
         L.ksref_init_save_spec.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_uint64, C.c_char_p]
         L.ksref_synthetic.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_char_p,
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        L.ksref_encode_ex.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.c_int,
+                                      C.POINTER(C.c_int32), C.c_char_p]
+        L.ksref_descriptors.argtypes = [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_int64)]
         _rlib = L
     return _rlib
 
@@ -316,6 +320,17 @@ class RefModel:
         bad = rlib().ksref_encode(self._h, _p(desc, C.c_int64), len(desc), _p(tok, C.c_int32))
         return tok, bad
 
+    def encode_ex(self, desc, allow_nearest=False):
+        """encode_problem per descriptor with the snap option: (tok B x 7 with -1 rows
+        on ValidationError, field name of each error or "")."""
+        desc = np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
+        tok = np.zeros(desc.shape, np.int32)
+        buf = C.create_string_buffer(16 * len(desc))
+        rlib().ksref_encode_ex(self._h, _p(desc, C.c_int64), len(desc), int(allow_nearest),
+                               _p(tok, C.c_int32), buf)
+        raw = buf.raw
+        return tok, [raw[16 * b:16 * b + 16].split(b"\0", 1)[0].decode() for b in range(len(desc))]
+
     def beam(self, tok, k, desc=None, preds_text="", threads=1):
         tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
         B = len(tok)
@@ -337,6 +352,14 @@ class RefModel:
         fail_names = [raw[64 * b:64 * b + 64].split(b"\0", 1)[0].decode() for b in range(B)]
         return {"tokens": out_tok, "log_prob": out_lp, "count": cnt, "status": st,
                 "fail_step": fs, "fail_name": fail_names}
+
+    def descriptors(self, count, seed=2404, start=0):
+        """Workload configs start..start+count-1 drawn with the reference's Rng
+        (ref_shim ksref_descriptors): the checker of ks_synthetic_descriptors."""
+        out = np.zeros((count, 7), np.int64)
+        if rlib().ksref_descriptors(self._h, seed, start, count, _p(out, C.c_int64)):
+            raise RuntimeError(rlib().ksref_last_error().decode())
+        return out
 
     def greedy(self, tok, threads=1):
         tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)

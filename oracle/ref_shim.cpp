@@ -11,6 +11,7 @@
 #include <optional>
 #include <stdexcept>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <sstream>
@@ -105,6 +106,25 @@ int ksref_encode(void* h, const int64_t* desc, int64_t B, int32_t* tok) {
             for (int f = 0; f < 7; ++f) tok[7 * b + f] = t.ids[f];
         } catch (const std::exception&) {
             for (int f = 0; f < 7; ++f) tok[7 * b + f] = -1;
+            ++bad;
+        }
+    }
+    return bad;
+}
+
+// encode_problem with the allow_nearest snap (encoding.cpp:87-113) for each of B
+// descriptors: tok B x 7 (-1 row on error), err_field B x 16 chars ("" when ok).
+int ksref_encode_ex(void* h, const int64_t* desc, int64_t B, int allow_nearest, int32_t* tok, char* err_field) {
+    const ModelParams& mp = *static_cast<ModelParams*>(h);
+    int bad = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        err_field[16 * b] = 0;
+        try {
+            TokenSequence t = encode_problem(desc_of(desc + 7 * b), mp.vocab, allow_nearest != 0);
+            for (int f = 0; f < 7; ++f) tok[7 * b + f] = t.ids[f];
+        } catch (const ValidationError& e) {
+            for (int f = 0; f < 7; ++f) tok[7 * b + f] = -1;
+            std::snprintf(err_field + 16 * b, 16, "%s", e.field().c_str());
             ++bad;
         }
     }
@@ -279,6 +299,27 @@ int ksref_synthetic(const char* kernel, int count, uint64_t seed, const char* di
                         if (vals[j] == val) id = static_cast<int>(j);
                     out_params[i * spec.num_params() + p] = id;
                 }
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// Benchmark / parity workloads drawn with the reference's own Rng (rng.hpp:19-43):
+// config start+i draws each input field uniformly with replacement from the model's
+// input vocabulary, fields in order n,c,h,w,k,y,x, from Rng::derive(seed, start+i).
+// The checker for ks_synthetic_descriptors.
+int ksref_descriptors(void* h, uint64_t seed, int64_t start, int64_t count, int64_t* out) {
+    try {
+        const ModelParams& mp = *static_cast<ModelParams*>(h);
+        for (int64_t i = 0; i < count; ++i) {
+            Rng r = Rng::derive(seed, static_cast<std::uint64_t>(start + i));
+            for (int f = 0; f < kNumInputFields; ++f) {
+                const auto& vals = mp.vocab.input_field(f).values;
+                out[7 * i + f] = vals[static_cast<std::size_t>(r.uniform_int(vals.size()))];
             }
         }
         return 0;

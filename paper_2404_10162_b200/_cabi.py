@@ -89,7 +89,10 @@ EXPORTS = [
     "ks_trainer_create", "ks_trainer_create_from_checkpoint", "ks_trainer_destroy",
     "ks_trainer_num_params", "ks_trainer_num_ref_params", "ks_trainer_last_launch_count", "ks_trainer_loss_grads",
     "ks_trainer_apply", "ks_trainer_step", "ks_trainer_evaluate", "ks_trainer_export", "ks_trainer_import",
-    "ks_trainer_to_reference_layout",
+    "ks_trainer_to_reference_layout", "ks_synthetic_descriptors", "ks_engine_synthetic_descriptors", "ks_forward_batch",
+    "ks_device_count", "ks_engine_group_create", "ks_engine_group_create_from_checkpoint", "ks_engine_group_destroy",
+    "ks_engine_group_size", "ks_engine_group_engine", "ks_group_beam_search_batch", "ks_group_greedy_batch",
+    "ks_group_forward_batch", "ks_group_topk_metrics_batch",
 ]
 
 
@@ -177,8 +180,30 @@ def lib():
     L.ks_trainer_export.argtypes = [vp, P(C.c_float)]
     L.ks_trainer_import.argtypes = [vp, P(C.c_float)]
     L.ks_trainer_to_reference_layout.argtypes = [vp, P(C.c_float), P(C.c_float)]
+    L.ks_engine_group_create_from_checkpoint.argtypes = [C.c_char_p, P(i32), i32, i32, P(vp)]
+    L.ks_engine_group_destroy.argtypes = [vp]
+    L.ks_engine_group_size.argtypes = [vp]
+    L.ks_engine_group_engine.argtypes = [vp, i32]
+    L.ks_engine_group_engine.restype = vp
+    L.ks_group_beam_search_batch.argtypes = [vp, P(i32), P(i64), i64, i32, P(KsPred), i32, vp, vp, P(i32),
+                                             P(dbl), P(i32), P(i32), P(i32), P(i32)]
+    L.ks_group_greedy_batch.argtypes = [vp, P(i32), i64, P(i32)]
+    L.ks_forward_batch.argtypes = [vp, P(i32), P(i32), i64, P(dbl), P(i32), P(dbl)]
+    L.ks_synthetic_descriptors.argtypes = [P(i32), P(i64), C.c_uint64, i64, i64, P(i64)]
+    L.ks_engine_synthetic_descriptors.argtypes = [vp, C.c_uint64, i64, i64, P(i64)]
     _lib = L
     return L
+
+
+def synthetic_descriptors(input_values, count, seed=2404, start=0):
+    """ks_synthetic_descriptors over a vocabulary given as 7 lists of field
+    values: configs start..start+count-1, each from Rng::derive(seed, i)."""
+    sizes = np.array([len(v) for v in input_values], np.int32)
+    vals = np.concatenate([np.asarray(v, np.int64) for v in input_values])
+    out = np.empty((count, 7), np.int64)
+    check(lib().ks_synthetic_descriptors(_p(sizes, C.c_int32), _p(vals, C.c_int64), seed, start, count,
+                                         _p(out, C.c_int64)))
+    return out
 
 
 def check(code: int):
@@ -236,6 +261,12 @@ class Engine:
     def launches(self) -> int:
         return lib().ks_engine_last_launch_count(self._h)
 
+    def synthetic(self, count, seed=2404, start=0):
+        """Synthetic descriptors over the model's input vocabulary (ks_engine_synthetic_descriptors)."""
+        out = np.empty((count, 7), np.int64)
+        check(lib().ks_engine_synthetic_descriptors(self._h, seed, start, count, _p(out, C.c_int64)))
+        return out
+
     def encode(self, desc, allow_nearest=False):
         desc = np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
         tok = np.zeros(desc.shape, np.int32)
@@ -275,6 +306,21 @@ class Engine:
         check(lib().ks_greedy_batch(self._h, _p(tok, C.c_int32), len(tok), _p(out, C.c_int32)))
         return out
 
+    def forward(self, tok, teacher=None):
+        """ks_forward_batch: per-position distributions (list of B x V_p arrays), the
+        fed-back tokens (B x T) and the sequence scores (B)."""
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        B = len(tok)
+        t = None if teacher is None else np.ascontiguousarray(teacher, np.int32).reshape(B, self.T)
+        sv = sum(self.vsizes)
+        dist = np.empty((B, sv), np.float64)
+        fed = np.empty((B, self.T), np.int32)
+        score = np.empty(B, np.float64)
+        check(lib().ks_forward_batch(self._h, _p(tok, C.c_int32), _p(t, C.c_int32), B, _p(dist, C.c_double),
+                                     _p(fed, C.c_int32), _p(score, C.c_double)))
+        offs = np.cumsum([0] + self.vsizes)
+        return [dist[:, offs[p]:offs[p + 1]] for p in range(self.T)], fed, score
+
     def beam_device(self, d_tok, d_desc, B, k, preds, d_out, stream=0):
         """All buffers are device pointers (ints); d_out = dict of pointers."""
         arr, keep = pack_preds(list(preds))
@@ -300,6 +346,45 @@ class Engine:
         useful = C.c_double(0.0)
         ms = lib().ks_engine_profile_gemm_ms(self._h, C.byref(n), C.byref(useful))
         return ms, n.value, useful.value
+
+
+class EngineGroup:
+    """One engine per listed device (None: every visible GPU); batches are
+    sharded contiguously across them (ks_group_*), results in config order."""
+
+    def __init__(self, checkpoint: str, devices=None, precision: str = "f16x3"):
+        L = lib()
+        h = C.c_void_p()
+        devs = None if devices is None else np.ascontiguousarray(devices, np.int32)
+        check(L.ks_engine_group_create_from_checkpoint(checkpoint.encode(), _p(devs, C.c_int32),
+                                                       0 if devs is None else len(devs), PREC[precision],
+                                                       C.byref(h)))
+        self._h = h
+        self._destroy = L.ks_engine_group_destroy
+        self.size = L.ks_engine_group_size(h)
+        self.T = L.ks_engine_num_positions(L.ks_engine_group_engine(h, 0))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def beam(self, tok, k, desc=None, preds=()):
+        tok = np.ascontiguousarray(tok, np.int32).reshape(-1, 7)
+        B = len(tok)
+        d = None if desc is None else np.ascontiguousarray(desc, np.int64).reshape(-1, 7)
+        out_tok = np.empty((B, k, self.T), np.int32)
+        out_lp = np.empty((B, k), np.float64)
+        cnt, st, fp, fs = (np.empty(B, np.int32) for _ in range(4))
+        arr, keep = pack_preds(list(preds))
+        check(lib().ks_group_beam_search_batch(self._h, _p(tok, C.c_int32), _p(d, C.c_int64), B, k, arr, len(preds),
+                                               None, None, _p(out_tok, C.c_int32), _p(out_lp, C.c_double),
+                                               _p(cnt, C.c_int32), _p(st, C.c_int32), _p(fp, C.c_int32),
+                                               _p(fs, C.c_int32)))
+        return {"tokens": out_tok, "log_prob": out_lp, "count": cnt, "status": st, "fail_pred": fp,
+                "fail_step": fs}
 
 
 class Trainer:

@@ -18,7 +18,7 @@ BUILD = os.path.join(PKG, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["ks_kernels.cu", "ks_engine.cu", "ks_gemm_tc.cu", "ks_train.cu"]
-CPP_SOURCES = ["ks_checkpoint.cpp"]
+CPP_SOURCES = ["ks_checkpoint.cpp", "ks_synth.cpp", "ks_group.cpp"]
 
 
 def _run(cmd):
@@ -52,7 +52,7 @@ def build_engine(verbose: bool = False, force: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")
         if force or _newer([src] + headers, obj):
-            jobs.append(["g++", "-std=c++17", "-O2", "-fPIC", f"-I{ROOT}/include",
+            jobs.append(["g++", "-std=c++17", "-O2", "-fPIC", "-pthread", f"-I{ROOT}/include",
                          "-I/usr/local/cuda/include", "-c", src, "-o", obj])
     with cf.ThreadPoolExecutor(max_workers=max(1, len(jobs))) as ex:
         logs = list(ex.map(_run, jobs))

@@ -461,6 +461,17 @@ ModelParams load_checkpoint(const std::string& path) {
 // ------------------------------------------------------------------ predictor
 SequencePredictor::SequencePredictor(const ModelParams& params, int device, GemmPrecision precision)
     : params_(&params) {
+    create(device == kAllDevices ? std::vector<int>{} : std::vector<int>{device}, precision);
+}
+
+SequencePredictor::SequencePredictor(const ModelParams& params, std::vector<int> devices, GemmPrecision precision)
+    : params_(&params) {
+    if (devices.empty()) throw ParameterError("empty device list");
+    create(devices, precision);
+}
+
+void SequencePredictor::create(const std::vector<int>& devices, GemmPrecision precision) {
+    const ModelParams& params = *params_;
     const int var = static_cast<int>(params.config.variant);
     std::vector<int32_t> in_sizes, vsizes;
     std::vector<int64_t> in_vals, out_vals;
@@ -504,14 +515,141 @@ SequencePredictor::SequencePredictor(const ModelParams& params, int device, Gemm
     d.tensor_names = names.data();
     d.tensor_numel = numel.data();
     d.tensor_data = data.data();
-    ks_engine* e = nullptr;
-    check(ks_engine_create(&d, device, static_cast<int32_t>(precision), &e));
-    engine_ = std::shared_ptr<ks_engine>(e, ks_engine_destroy);
+    ks_engine_group* g = nullptr;
+    check(ks_engine_group_create(&d, devices.empty() ? nullptr : devices.data(), static_cast<int32_t>(devices.size()),
+                                 static_cast<int32_t>(precision), &g));
+    group_ = std::shared_ptr<ks_engine_group>(g, ks_engine_group_destroy);
 }
 
 int SequencePredictor::num_positions() const { return params_->num_output_positions(); }
 int SequencePredictor::vocab_size(int position) const { return params_->vocab.output_param(position).size(); }
-ks_engine* SequencePredictor::engine() const { return engine_.get(); }
+ks_engine* SequencePredictor::engine() const { return ks_engine_group_engine(group_.get(), 0); }
+ks_engine_group* SequencePredictor::group() const { return group_.get(); }
+int SequencePredictor::num_devices() const { return ks_engine_group_size(group_.get()); }
+
+// ------------------------------------------------------------------ nn::Tensor
+namespace nn {
+Tensor::Tensor(std::vector<int> shape) : shape_(std::move(shape)) {
+    std::size_t n = 1;
+    for (int d : shape_) {
+        if (d < 0) throw ShapeError("negative tensor dimension");
+        n *= static_cast<std::size_t>(d);
+    }
+    data_.assign(n, 0.0);
+}
+Tensor::Tensor(std::vector<int> shape, std::vector<double> data) : shape_(std::move(shape)), data_(std::move(data)) {
+    std::size_t n = 1;
+    for (int d : shape_) n *= static_cast<std::size_t>(d);
+    if (n != data_.size()) throw ShapeError("tensor data size does not match its shape");
+}
+Tensor Tensor::vec(std::vector<double> data) {
+    const int n = static_cast<int>(data.size());
+    return Tensor({n}, std::move(data));
+}
+}  // namespace nn
+
+// ------------------------------------------------------------------ stepping facade
+std::vector<std::vector<nn::Tensor>> model_forward_batch(const SequencePredictor& predictor,
+                                                         std::span<const TokenSequence> inputs,
+                                                         std::span<const std::vector<int>> teachers,
+                                                         std::vector<double>* scores) {
+    const int T = predictor.num_positions();
+    const std::size_t B = inputs.size();
+    if (!teachers.empty() && teachers.size() != B)
+        throw ParameterError("model_forward_batch: " + std::to_string(teachers.size()) + " teachers for " +
+                             std::to_string(B) + " inputs");
+    std::vector<int32_t> tok(B * 7), tch(teachers.empty() ? 0 : B * T);
+    for (std::size_t b = 0; b < B; ++b) {
+        if (inputs[b].length() != kNumInputFields)
+            throw ParameterError("model input must have 7 tokens, got " + std::to_string(inputs[b].length()));
+        for (int f = 0; f < 7; ++f) tok[b * 7 + f] = inputs[b].ids[static_cast<std::size_t>(f)];
+        if (!teachers.empty()) {
+            if (static_cast<int>(teachers[b].size()) != T)  // models.cpp:499-503
+                throw ParameterError("teacher sequence length " + std::to_string(teachers[b].size()) + " vs " +
+                                     std::to_string(T) + " output positions");
+            for (int p = 0; p < T; ++p) tch[b * T + p] = teachers[b][static_cast<std::size_t>(p)];
+        }
+    }
+    std::vector<int> off(T + 1, 0);
+    for (int p = 0; p < T; ++p) off[p + 1] = off[p] + predictor.vocab_size(p);
+    std::vector<double> dist(B * off[T]), sc(B);
+    if (B)
+        check(ks_group_forward_batch(predictor.group(), tok.data(), tch.empty() ? nullptr : tch.data(),
+                               static_cast<int64_t>(B), dist.data(), nullptr, sc.data()));
+    std::vector<std::vector<nn::Tensor>> out(B);
+    for (std::size_t b = 0; b < B; ++b)
+        for (int p = 0; p < T; ++p)
+            out[b].push_back(nn::Tensor::vec(std::vector<double>(dist.begin() + b * off[T] + off[p],
+                                                                 dist.begin() + b * off[T] + off[p + 1])));
+    if (scores) *scores = std::move(sc);
+    return out;
+}
+
+std::vector<nn::Tensor> model_forward(const ModelParams& params, const TokenSequence& input,
+                                      const std::vector<int>* teacher) {
+    const SequencePredictor predictor(params);
+    std::vector<std::vector<int>> t;
+    if (teacher) t.push_back(*teacher);
+    return model_forward_batch(predictor, std::span<const TokenSequence>(&input, 1),
+                               std::span<const std::vector<int>>(t))[0];
+}
+
+EncodedInput SequencePredictor::encode(const TokenSequence& input) const {
+    if (input.length() != kNumInputFields)  // models.cpp:112-116
+        throw ParameterError("model input must have 7 tokens, got " + std::to_string(input.length()));
+    for (int f = 0; f < kNumInputFields; ++f) {
+        const int t = input.ids[static_cast<std::size_t>(f)];
+        if (t < 0 || t >= params_->vocab.input_field(f).size())  // input_onehot, encoding.cpp:182-190
+            throw IndexError("input_onehot: token " + std::to_string(t) + " out of range for field " +
+                             params_->vocab.input_field(f).name);
+    }
+    EncodedInput enc;
+    enc.input = input;
+    return enc;
+}
+
+DecoderState SequencePredictor::initial_state(const EncodedInput&) const { return DecoderState{}; }
+
+nn::Tensor SequencePredictor::step(const EncodedInput& enc, DecoderState& state, int prev_token) const {
+    const int T = num_positions();
+    const int pos = state.position;
+    if (pos < 0 || pos >= T) throw StateError("decoder stepped past the last output position");  // models.cpp:452-454
+    if (static_cast<int>(state.fed.size()) != std::max(0, pos - 1))
+        throw StateError("decoder state does not match its position");
+    const ModelVariant var = params_->config.variant;
+    const bool feedback = var == ModelVariant::attn || var == ModelVariant::enc_dec;
+    if (pos > 0) {
+        if (feedback && (prev_token < 0 || prev_token >= vocab_size(pos - 1)))  // encoding.cpp:192-199
+            throw IndexError("feedback_onehot: token " + std::to_string(prev_token) + " out of range for position " +
+                             std::to_string(pos - 1));
+        state.fed.push_back(feedback ? prev_token : 0);
+    }
+    std::vector<int> teacher(static_cast<std::size_t>(T), 0);
+    std::copy(state.fed.begin(), state.fed.end(), teacher.begin());
+    const std::vector<int> one[1] = {teacher};
+    auto d = model_forward_batch(*this, std::span<const TokenSequence>(&enc.input, 1),
+                                 std::span<const std::vector<int>>(one, 1));
+    state.position = pos + 1;
+    return std::move(d[0][static_cast<std::size_t>(pos)]);
+}
+
+std::vector<ProblemDescriptor> synthetic_descriptors(const ModelParams& params, std::int64_t count,
+                                                     std::uint64_t seed, std::int64_t start) {
+    if (count < 0 || start < 0) throw ParameterError("synthetic_descriptors: negative count / start");
+    std::vector<int32_t> sizes;
+    std::vector<int64_t> vals;
+    for (const auto& f : params.vocab.input_fields()) {
+        sizes.push_back(f.size());
+        vals.insert(vals.end(), f.values.begin(), f.values.end());
+    }
+    if (sizes.size() != kNumInputFields) throw StateError("model has no input vocabulary");
+    std::vector<int64_t> raw(static_cast<std::size_t>(count) * 7);
+    check(ks_synthetic_descriptors(sizes.data(), vals.data(), seed, start, count, raw.data()));
+    std::vector<ProblemDescriptor> out(static_cast<std::size_t>(count));
+    for (std::int64_t i = 0; i < count; ++i)
+        for (int f = 0; f < 7; ++f) set_descriptor_field(out[static_cast<std::size_t>(i)], f, raw[i * 7 + f]);
+    return out;
+}
 
 // ------------------------------------------------------------------ decode
 namespace {
@@ -597,12 +735,16 @@ ResolvedPreds resolve(const ModelParams& mp, std::span<const ConstraintPredicate
     return r;
 }
 
+// The hook runs on one host thread per device of the predictor's group; the
+// predicates themselves are called concurrently, as the reference calls them
+// from its parallel_stripes workers.
 struct HookCtx {
     const ModelParams* mp;
     std::span<const ConstraintPredicate> preds;
     const std::vector<int>* host;
     std::span<const ProblemDescriptor> descs;
     std::string error;
+    std::mutex mu;  // guards error
 };
 
 // Evaluates the opaque predicates exactly as beam_search_impl does
@@ -635,7 +777,8 @@ int32_t host_hook(void* user, int32_t position, int32_t final_step, int64_t n_ro
             }
         }
     } catch (const std::exception& e) {
-        ctx->error = e.what();
+        std::lock_guard<std::mutex> g(ctx->mu);
+        if (ctx->error.empty()) ctx->error = e.what();
         return 1;
     }
     return 0;
@@ -670,8 +813,8 @@ BatchResult beam_search_batch(const SequencePredictor& predictor, std::span<cons
     std::vector<int32_t> otok(B * k * T), cnt(B), st(B), fp(B), fs(B);
     std::vector<double> olp(B * k);
     HookCtx ctx{&mp, predicates, &rp.host, descriptors, {}};
-    ks_status s = ks_beam_search_batch_hooked(
-        predictor.engine(), tok.data(), desc.empty() ? nullptr : desc.data(), static_cast<int64_t>(B),
+    ks_status s = ks_group_beam_search_batch(
+        predictor.group(), tok.data(), desc.empty() ? nullptr : desc.data(), static_cast<int64_t>(B),
         beam_width, rp.preds.empty() ? nullptr : rp.preds.data(), static_cast<int32_t>(rp.preds.size()),
         rp.host.empty() ? nullptr : host_hook, &ctx, otok.data(), olp.data(), cnt.data(), st.data(), fp.data(),
         fs.data());
@@ -709,7 +852,7 @@ std::vector<TokenSequence> greedy_decode_batch(const SequencePredictor& predicto
             throw ParameterError("model input must have 7 tokens, got " + std::to_string(inputs[b].length()));
         for (int f = 0; f < 7; ++f) tok[b * 7 + f] = inputs[b].ids[static_cast<std::size_t>(f)];
     }
-    check(ks_greedy_batch(predictor.engine(), tok.data(), static_cast<int64_t>(B), out.data()));
+    check(ks_group_greedy_batch(predictor.group(), tok.data(), static_cast<int64_t>(B), out.data()));
     std::vector<TokenSequence> res(B);
     for (std::size_t b = 0; b < B; ++b) {
         res[b].role = TokenSequence::Role::output;
@@ -816,8 +959,8 @@ std::vector<EvalReport> topk_metrics(const SequencePredictor& predictor, const s
         std::vector<int64_t> hits((size_t)arity);
         int64_t perfect = 0;
         HookCtx ctx{&params, predicates, &rp.host, descs, {}};
-        const ks_status s = ks_topk_metrics_batch(
-            predictor.engine(), tok.data(), desc.data(), truth.data(), static_cast<int64_t>(B), k,
+        const ks_status s = ks_group_topk_metrics_batch(
+            predictor.group(), tok.data(), desc.data(), truth.data(), static_cast<int64_t>(B), k,
             rp.preds.empty() ? nullptr : rp.preds.data(), static_cast<int32_t>(rp.preds.size()),
             rp.host.empty() ? nullptr : host_hook, &ctx, hits.data(), &perfect);
         if (!ctx.error.empty()) throw Error("predicate raised: " + ctx.error);

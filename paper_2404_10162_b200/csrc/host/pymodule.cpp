@@ -14,9 +14,11 @@
 #include <pybind11/stl.h>
 
 #include <mutex>
+#include <optional>
 #include <tuple>
 
 #include "kernelseer_b200.hpp"
+#include "ks_b200.h"
 
 namespace py = pybind11;
 using namespace kernelseer;
@@ -26,12 +28,15 @@ namespace {
 struct PyModel {
     std::shared_ptr<ModelParams> params;
     std::shared_ptr<SequencePredictor> predictor;
-    int device = 0;
+    int device = SequencePredictor::kAllDevices;  // every visible GPU (set_engine narrows it)
+    std::vector<int> devices;                     // explicit device list (set_engine([...]))
     GemmPrecision precision = GemmPrecision::f16x3;
     std::mutex mu;
     const SequencePredictor& pred() {
         std::lock_guard<std::mutex> g(mu);
-        if (!predictor) predictor = std::make_shared<SequencePredictor>(*params, device, precision);
+        if (!predictor)
+            predictor = devices.empty() ? std::make_shared<SequencePredictor>(*params, device, precision)
+                                        : std::make_shared<SequencePredictor>(*params, devices, precision);
         return *predictor;
     }
 };
@@ -140,14 +145,22 @@ PYBIND11_MODULE(_kernelseer_b200, m) {
         .def_property_readonly("variant", [](PyModel& p) { return variant_label(p.params->config.variant); })
         .def_property_readonly("spec", [](PyModel& p) { return spec_of(*p.params); })
         .def("set_engine",
-             [](PyModel& p, int device, const std::string& precision) {
+             [](PyModel& p, const py::object& device, const std::string& precision) {
                  std::lock_guard<std::mutex> g(p.mu);
-                 p.device = device;
+                 p.devices.clear();
+                 if (py::isinstance<py::int_>(device)) {
+                     p.device = py::cast<int>(device);
+                 } else {  // a list of devices (the same GPU may repeat)
+                     p.devices = py::cast<std::vector<int>>(device);
+                     if (p.devices.empty()) throw ParameterError("empty device list");
+                 }
                  p.precision = precision_of(precision);
                  p.predictor.reset();
              },
-             py::arg("device") = 0, py::arg("precision") = "f16x3",
-             "Select the GPU and the gate-GEMM arithmetic (f16x3 | fp32 | bf16) of the cached engine")
+             py::arg("device") = -1, py::arg("precision") = "f16x3",
+             "Select the GPU (-1: every visible GPU, batches sharded across them; or a list of devices) and the gate-GEMM "
+             "arithmetic (f16x3 | fp32 | bf16) of the cached engines")
+        .def_property_readonly("num_devices", [](PyModel& p) { return p.pred().num_devices(); })
         .def("__repr__", [](PyModel& p) {
             return "<ModelParams " + variant_label(p.params->config.variant) + " for " + p.params->kernel + ">";
         });
@@ -255,6 +268,90 @@ PYBIND11_MODULE(_kernelseer_b200, m) {
           py::arg("params"), py::arg("descriptors"), py::arg("beam_width") = 1,
           py::arg("predicates") = std::vector<ConstraintPredicate>{}, py::arg("snap") = false,
           "Batched predict: one entry per descriptor (a beam list, or an exhaustion record)");
+
+    // ------------------------------------------------------------ stepping facade
+    // (models.hpp:65-103; the reference's pybind module does not bind these --
+    // B200 additions for the teacher-forced scorer and the stepping API)
+    m.def("encode_problem",
+          [](std::shared_ptr<PyModel> pm, const py::dict& descriptor, bool snap) {
+              return encode_problem(descriptor_from_dict(descriptor), pm->params->vocab, snap).ids;
+          },
+          py::arg("params"), py::arg("descriptor"), py::arg("snap") = false,
+          "encode_problem (encoding.cpp:87-113): 7 input token ids; ValidationError naming the field");
+    m.def("model_forward",
+          [](std::shared_ptr<PyModel> pm, const std::vector<std::vector<int>>& inputs,
+             const std::optional<std::vector<std::vector<int>>>& teachers) {
+              std::vector<TokenSequence> ins;
+              for (const auto& t : inputs) {
+                  TokenSequence s;
+                  s.ids = t;
+                  ins.push_back(std::move(s));
+              }
+              const SequencePredictor& pred = pm->pred();
+              std::vector<double> scores;
+              std::vector<std::vector<nn::Tensor>> d;
+              std::vector<std::vector<int>> tch = teachers ? *teachers : std::vector<std::vector<int>>{};
+              {
+                  py::gil_scoped_release nogil;
+                  d = model_forward_batch(pred, ins, tch, &scores);
+              }
+              py::list dists;
+              for (const auto& row : d) {
+                  py::list r;
+                  for (const auto& t : row) r.append(t.values());
+                  dists.append(r);
+              }
+              return py::make_tuple(dists, scores);
+          },
+          py::arg("params"), py::arg("inputs"), py::arg("teachers") = py::none(),
+          "model_forward (models.cpp:495-514) over many input token sequences in one device pass: "
+          "(per input, per position distributions; per input sequence score sum log max(p, 1e-300))");
+
+    py::class_<EncodedInput>(m, "EncodedInput")
+        .def_property_readonly("input", [](const EncodedInput& e) { return e.input.ids; });
+    py::class_<DecoderState>(m, "DecoderState")
+        .def_readonly("position", &DecoderState::position)
+        .def_readonly("fed", &DecoderState::fed);
+    struct PyPredictor {
+        std::shared_ptr<PyModel> pm;
+    };
+    py::class_<PyPredictor>(m, "SequencePredictor")
+        .def(py::init([](std::shared_ptr<PyModel> pm) { return PyPredictor{pm}; }), py::arg("params"))
+        .def("num_positions", [](PyPredictor& p) { return p.pm->pred().num_positions(); })
+        .def("vocab_size", [](PyPredictor& p, int pos) { return p.pm->pred().vocab_size(pos); }, py::arg("position"))
+        .def("encode",
+             [](PyPredictor& p, const std::vector<int>& ids) {
+                 TokenSequence s;
+                 s.ids = ids;
+                 return p.pm->pred().encode(s);
+             },
+             py::arg("input"))
+        .def("initial_state", [](PyPredictor& p, const EncodedInput& e) { return p.pm->pred().initial_state(e); },
+             py::arg("enc"))
+        .def("step",
+             [](PyPredictor& p, const EncodedInput& e, DecoderState& st, int prev) {
+                 const SequencePredictor& pred = p.pm->pred();
+                 nn::Tensor t;
+                 {
+                     py::gil_scoped_release nogil;
+                     t = pred.step(e, st, prev);
+                 }
+                 return t.values();
+             },
+             py::arg("enc"), py::arg("state"), py::arg("prev_token"));
+
+    m.def("device_count", [] { return ks_device_count(); }, "visible CUDA devices");
+    m.def("synthetic_descriptors",
+          [](std::shared_ptr<PyModel> pm, std::int64_t count, std::uint64_t seed, std::int64_t start) {
+              const auto ds = synthetic_descriptors(*pm->params, count, seed, start);
+              py::array_t<std::int64_t> out({(py::ssize_t)count, (py::ssize_t)7});
+              auto w = out.mutable_unchecked<2>();
+              for (std::int64_t i = 0; i < count; ++i)
+                  for (int f = 0; f < 7; ++f) w(i, f) = descriptor_field(ds[(std::size_t)i], f);
+              return out;
+          },
+          py::arg("params"), py::arg("count"), py::arg("seed") = 2404, py::arg("start") = 0,
+          "Workload configs start..start+count-1 (count x 7: n,c,h,w,k,y,x), config i from Rng::derive(seed, i)");
 
     m.def("topk_metrics",
           [](std::shared_ptr<PyModel> pm, const std::vector<Sample>& test, const std::vector<int>& k_values,

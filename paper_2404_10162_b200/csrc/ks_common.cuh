@@ -183,6 +183,13 @@ struct BeamArgs {
     int n_values;              // staged-table sizes (shared memory)
     int n_terms;
     int n_bytes;
+    // model_forward (models.cpp:495-514), greedy mode only: the fed-back token is
+    // teacher[b][pos] instead of the argmax when teacher != null, and the position's
+    // softmax distribution goes to out_dist[b][dist_off + v] (row stride dist_ld)
+    const int* teacher;        // [B][T] or null
+    double* out_dist;          // [B][dist_ld] or null
+    int dist_ld;
+    int dist_off;
 };
 
 // Hybrid variants' convolutional encoder arguments (hybrid_conv).

@@ -198,6 +198,11 @@ struct ks_engine {
         for (auto& g : graphs)
             if (g.exec) cudaGraphExecDestroy(g.exec);
     }
+    // model_forward (ks_forward_batch): set for the duration of that call only
+    const int* fw_teacher = nullptr;  // device [C][T] teacher tokens of the chunk, or null (argmax)
+    double* fw_dist = nullptr;        // device [C][sum V] distributions of the chunk
+    int fw_ld = 0;
+    DevMem fwt, fwd;
     bool layered = false;         // hybrid: bi-LSTM 2 runs over bi-LSTM 1's sequence (not seeded)
     DevMem hybH1, hybX2;          // layered: H1 [T][C][2CP] fp32; bi-LSTM 2 operands per dir and step
     int num_sms = 148;
@@ -614,6 +619,12 @@ extern "C" ks_status ks_engine_set_chunk(ks_engine* eng, int64_t c) {
     if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
     eng->chunk = c > 0 ? c : 65536;
     return KS_OK;
+}
+
+extern "C" ks_status ks_engine_synthetic_descriptors(const ks_engine* eng, uint64_t seed, int64_t start,
+                                                     int64_t count, int64_t* out_desc) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    return ks_synthetic_descriptors(eng->in_sizes.data(), eng->in_values.data(), seed, start, count, out_desc);
 }
 
 extern "C" ks_status ks_encode_problems(const ks_engine* eng, const int64_t* desc, int64_t B,
@@ -1338,6 +1349,14 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         b.n_values = (int)E.out_values.size();
         b.n_terms = pd.n_terms;
         b.n_bytes = pd.n_bytes;
+        if (E.fw_dist) {  // model_forward (ks_forward_batch): greedy, one row per config
+            b.teacher = E.fw_teacher;
+            b.out_dist = E.fw_dist;
+            b.dist_ld = E.fw_ld;
+            int off = 0;
+            for (int q = 0; q < pos; ++q) off += E.vsize[(size_t)q];
+            b.dist_off = off;
+        }
         const size_t tables = (size_t)b.n_values * 8 + (size_t)b.n_terms * 16 + (size_t)pd.n * sizeof(DevPred) +
                               (size_t)b.n_bytes + 16;
         int warps = 8;
@@ -1700,6 +1719,72 @@ extern "C" ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t
     if (!tok || !out_tok) return set_error(KS_ERR_PARAMETER, "null token buffer");
     return decode_host(eng, tok, nullptr, B, 1, true, nullptr, 0, out_tok, nullptr, nullptr, nullptr, nullptr,
                        nullptr);
+}
+
+extern "C" ks_status ks_forward_batch(ks_engine* eng, const int32_t* tok, const int32_t* teacher, int64_t B,
+                                      double* out_dist, int32_t* out_tok, double* out_score) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    if (B < 0 || B > (1LL << 31)) return set_error(KS_ERR_PARAMETER, "batch size out of range");
+    if (B == 0) return KS_OK;
+    if (!tok || !out_dist) return set_error(KS_ERR_PARAMETER, "null buffer");
+    ks_engine& E = *eng;
+    cudaSetDevice(E.device);
+    const int T = E.T;
+    int SV = 0;
+    for (int q = 0; q < T; ++q) SV += E.vsize[(size_t)q];
+    for (int64_t b = 0; b < B; ++b)
+        for (int f = 0; f < 7; ++f) {
+            const int t = tok[b * 7 + f];
+            if (t < 0 || t >= E.in_sizes[(size_t)f])
+                return set_error(KS_ERR_INDEX, "input token " + std::to_string(t) + " out of range for field " +
+                                                   std::to_string(f) + " (row " + std::to_string(b) + ")");
+        }
+    if (teacher)
+        for (int64_t b = 0; b < B; ++b)
+            for (int q = 0; q < T; ++q) {
+                const int t = teacher[b * T + q];
+                if (t < 0 || t >= E.vsize[(size_t)q])
+                    return set_error(KS_ERR_INDEX, "teacher token " + std::to_string(t) + " out of range at position " +
+                                                       std::to_string(q) + " (row " + std::to_string(b) + ")");
+            }
+    PredDev pd;
+    ks_status st;
+    if ((st = upload_preds(E, nullptr, 0, pd))) return st;
+    E.launches = 0;
+    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
+    if (E.otok.ensure((size_t)C * T * 4) || E.olp.ensure((size_t)C * 8) || E.ocount.ensure((size_t)C * 4) ||
+        E.fwd.ensure((size_t)C * SV * 8) || (teacher && E.fwt.ensure((size_t)C * T * 4)) ||
+        E.tok.ensure((size_t)C * 7 * 4))
+        return set_error(KS_ERR_CUDA, "forward buffers");
+    if ((st = ensure_workspace(E, C, 1))) return st;
+    struct Reset {  // the forward hooks never outlive this call
+        ks_engine& e;
+        ~Reset() {
+            e.fw_teacher = nullptr;
+            e.fw_dist = nullptr;
+        }
+    } reset{E};
+    E.fw_teacher = teacher ? E.fwt.as<int>() : nullptr;
+    E.fw_dist = E.fwd.as<double>();
+    E.fw_ld = SV;
+    std::vector<int32_t> tk;
+    for (int64_t c0 = 0; c0 < B; c0 += C) {
+        const int64_t n = std::min<int64_t>(C, B - c0);
+        KS_CUDA(cudaMemcpyAsync(E.tok.p, tok + c0 * 7, (size_t)n * 7 * 4, cudaMemcpyHostToDevice, E.stream));
+        if (teacher)
+            KS_CUDA(cudaMemcpyAsync(E.fwt.p, teacher + c0 * T, (size_t)n * T * 4, cudaMemcpyHostToDevice, E.stream));
+        if ((st = run_chunk(E, n, c0, 1, true, E.tok.as<int>(), nullptr, pd, E.otok.as<int>(), E.olp.as<double>(),
+                            E.ocount.as<int>(), nullptr, nullptr, nullptr)))
+            return st;
+        KS_CUDA(cudaMemcpyAsync(out_dist + c0 * SV, E.fwd.p, (size_t)n * SV * 8, cudaMemcpyDeviceToHost, E.stream));
+        if (out_tok)
+            KS_CUDA(cudaMemcpyAsync(out_tok + c0 * T, E.otok.p, (size_t)n * T * 4, cudaMemcpyDeviceToHost, E.stream));
+        if (out_score)
+            KS_CUDA(cudaMemcpyAsync(out_score + c0, E.olp.p, (size_t)n * 8, cudaMemcpyDeviceToHost, E.stream));
+        KS_CUDA(cudaStreamSynchronize(E.stream));
+    }
+    return KS_OK;
 }
 
 extern "C" ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok, const int64_t* d_desc,

@@ -1020,8 +1020,13 @@ __global__ void __launch_bounds__(256, VP == 32 ? 1 : VP == 16 ? 2 : 3) beam_ste
                     const float lpt = fmaxf((l - mx) - logf(sum), -690.77552789821368f);
                     const double clp = a.lp_cur[r0 + jj] + (double)lpt;
                     const int c = j * V + lane;
-                    // greedy_decode's argmax of p == argmax of the logit (ties -> lowest index)
-                    c_score[c] = a.greedy ? (double)l : clp;
+                    // model_forward: the softmax (nn.cpp:215-226) of this position
+                    if (a.out_dist) a.out_dist[(long long)b * a.dist_ld + a.dist_off + lane] = (double)(ex / sum);
+                    // greedy_decode's argmax of p == argmax of the logit (ties -> lowest index);
+                    // teacher forcing feeds back the teacher's token instead
+                    c_score[c] = a.greedy ? (a.teacher ? (lane == a.teacher[(long long)b * T + a.pos] ? 1.0 : 0.0)
+                                                       : (double)l)
+                                          : clp;
                     c_lp[c] = clp;
                     c_meta[c] = 0;  // live, predicates pending
                 }

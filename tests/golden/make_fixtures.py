@@ -3,7 +3,7 @@
 Run in the build container (needs /root/reference and `make -C oracle ref`):
 
     python tests/golden/make_fixtures.py            # small committed fixtures
-    python tests/golden/make_fixtures.py --big      # + the git-ignored default-size
+    python tests/golden/make_fixtures.py --big      # + the default-size (tracked)
                                                     #   trained checkpoint (~2 min, 8 cores)
 
 Checkpoints are written by the reference's own init_model/train +
@@ -147,11 +147,10 @@ def main():
     print("wrote", len(golden), "arrays")
 
     if args.big:
-        os.makedirs(os.path.join(HERE, "_big"), exist_ok=True)
         cfg = ks.ModelConfig(variant="attn", dropout=0.0, recurrent_dropout=0.0)
         params, log = ks.train(cfg, spec, train.samples[:2000], test.samples[:200], epochs=4,
                                batch_size=32, seed=1, threads=8, learning_rate=2e-3)
-        ks.save_checkpoint(params, os.path.join(HERE, "_big", "attn_default_trained.ckpt"))
+        ks.save_checkpoint(params, os.path.join(HERE, "attn_default_trained.ckpt"))
         print("default model test acc", log[-1]["test_avg_acc"])
 
 

@@ -170,7 +170,6 @@ def test_chunking_is_transparent(precision):
         np.testing.assert_array_equal(full[key], part[key])
 
 
-@pytest.mark.skipif(not os.path.exists(BIG_CKPT), reason="default-size trained checkpoint absent")
 @pytest.mark.parametrize("precision", PRECISIONS)
 def test_default_size_trained_parity(precision):
     o, e = OracleModel(BIG_CKPT), engine(BIG_CKPT, precision)

@@ -126,7 +126,6 @@ def test_small_trained_gradients_vs_oracle(drop):
     assert l2 == loss and m2 == match
 
 
-@pytest.mark.skipif(not os.path.exists(BIG_CKPT), reason="default-size trained checkpoint absent")
 def test_default_size_gradients_vs_oracle():
     """n_a=256, n_s=512 (2.87M parameters), dropout 0.2/0.2 as the reference default."""
     from paper_2404_10162_b200._cabi import Trainer

@@ -88,7 +88,7 @@ def test_oracle_matches_live_reference_random():
     np.testing.assert_array_equal(a["log_prob"], b["log_prob"])
 
 
-@pytest.mark.skipif(not (ref_available() and os.path.exists(BIG_CKPT)),
+@pytest.mark.skipif(not ref_available(),
                     reason="reference build or default-size checkpoint absent")
 def test_oracle_matches_live_reference_default_size():
     o, r = OracleModel(BIG_CKPT), RefModel(BIG_CKPT)

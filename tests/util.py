@@ -4,7 +4,7 @@ import os
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-BIG_CKPT = os.path.join(ROOT, "tests", "golden", "_big", "attn_default_trained.ckpt")
+BIG_CKPT = os.path.join(ROOT, "tests", "golden", "attn_default_trained.ckpt")
 
 # Tie rule: a config is tie-adjacent when two candidates whose
 # order decides top-k membership or final rank are within this relative gap
