@@ -39,29 +39,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "problem-configs/sec, constrained beam decode (beam=5)"
 UNIT = "configs/s"
-# BASELINE.json configs (cfg2 is the headline; the others are reported workloads)
-WORKLOADS = {
-    "cfg2": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=5, configs=65536, greedy=False,
-                 label="BASELINE config 2: constrained beam search beam=5"),
-    "cfg3": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=5, configs=131072, greedy=False,
-                 label="BASELINE config 3 per-GPU shard (1M configs / 8 GPUs): constrained beam search beam=5"),
-    "cfg5": dict(kernel="ConvAsmBwdWrW1x1", n_a=1024, n_s=1024, beam=16, configs=16384, greedy=False,
-                 label="BASELINE config 5 shape: n_a=n_s=1024 (1 layer; the reference has no layer count), "
-                       "beam=16, ConvAsmBwdWrW1x1"),
-    "cfg1": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=1, configs=1000, greedy=True,
-                 label="BASELINE config 1: greedy decode of 1k configs"),
-    "cfg4": dict(kernel="ConvAsm1x1U", n_a=256, n_s=512, beam=0, configs=4096, greedy=False, train=True,
-                 label="BASELINE config 4: teacher-forced training step, global batch 4096, "
-                       "data-parallel with NCCL all-reduce"),
-}
+from paper_2404_10162_b200 import workloads as WL  # noqa: E402  (pure Python: maps no engine library)
+
+# BASELINE.json configs: cfg2 is the headline (N=1); the others are reported workloads.
+# scaling: "weak" = `configs` per GPU; "strong" = `configs` in total, sharded over the GPUs.
+WORKLOADS = {k: dict(v, scaling="strong" if k == "cfg3" else "weak") for k, v in WL.WORKLOADS.items()}
+WORKLOADS["cfg4"] = dict(model="train", beam=0, configs=4096, greedy=False, train=True, scaling="strong",
+                         label="BASELINE config 4: teacher-forced training step, global batch 4096, "
+                               "data-parallel with NCCL all-reduce")
 TRAIN_METRIC = "training samples/sec, teacher-forced step (batch 4096)"
 TRAIN_UNIT = "samples/s"
 TRAIN_LR = 1e-3
 W = WORKLOADS["cfg2"]
-KERNEL = W["kernel"]
+WNAME = "cfg2"
 BEAM = W["beam"]
-CONFIGS_PER_GPU = W["configs"]
-BUDGET = 60.0
 
 
 def metric_name():
@@ -82,8 +73,10 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="f16x3", choices=["f16x3", "fp32", "bf16"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
-    ap.add_argument("--configs", type=int, default=None, help="configs per GPU (default: the workload's)")
+    ap.add_argument("--configs", type=int, default=None,
+                    help="configs per GPU (weak workloads) or in total (cfg3); default: the workload's")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the fixture parity / agreement block")
     return ap.parse_args()
 
 
@@ -94,47 +87,29 @@ def dist_env():
     return rank, world, local
 
 
-def model_path():
-    from paper_2404_10162_b200.synth import write_checkpoint
-
-    drop = 0.2 if W.get("train") else 0.0  # ModelConfig defaults (models.hpp:28-41) for training
-    path = os.path.join(tempfile.gettempdir(), f"ks_bench_attn_{KERNEL}_{W['n_a']}_{W['n_s']}_d{drop:g}.ckpt")
-    if not os.path.exists(path):
-        tmp = path + f".{os.getpid()}"
-        write_checkpoint(tmp, KERNEL, "attn", W["n_a"], W["n_s"], 2, seed=1, dropout=drop, recurrent_dropout=drop)
-        os.replace(tmp, path)
-    return path
-
-
-def train_data(path, B, seed=4):
-    """Synthetic teacher-forcing batch: encoded descriptors + uniformly drawn target tokens."""
-    from oracle.train_oracle import Checkpoint  # header parsing only
-    from paper_2404_10162_b200.synth import descriptors
-
-    ck = Checkpoint(path)
-    desc = descriptors(B, KERNEL, seed=seed)
-    tok = np.stack([np.searchsorted(np.asarray(ck.inputs[f]), desc[:, f]) for f in range(7)], 1).astype(np.int32)
-    rng = np.random.default_rng(seed)
-    tgt = np.stack([rng.integers(0, v, B) for v in ck.vsizes], 1).astype(np.int32)
-    return tok, tgt, ck
+def model_path(reference=False):
+    """The workload's checkpoint (paper_2404_10162_b200/workloads.py): the tracked
+    reference-trained default model, or the cfg5 init_model checkpoint (written
+    by our byte-identical init_model, or by the reference's in the reference arm)."""
+    if W["model"] == "default":
+        return WL.DEFAULT_CKPT
+    if W["model"] == "cfg5":
+        return WL.cfg5_checkpoint_reference() if reference else WL.cfg5_checkpoint_ours()
+    return WL.train_checkpoint(reference)
 
 
-def train_flops_per_sample(ck):
-    """SURVEY.md §8(d): ~3x the forward gate-GEMM FLOPs (forward, dX, dW)."""
-    dec = ck.T * 2.0 * (2 * ck.n_a + ck.n_s) * 4 * ck.n_s
-    enc = 2 * 7 * 2.0 * ck.n_a * 4 * ck.n_a
-    return 3.0 * (dec + enc)
+def shard(args, rank, world):
+    """Config range [lo, hi) of this rank: weak = `configs` per GPU (rank-major),
+    strong = balanced contiguous shards of `configs` in total."""
+    from paper_2404_10162_b200.parallel import shard_bounds, weak_shard
+
+    if W["scaling"] == "strong":
+        return shard_bounds(args.configs, rank, world)
+    return weak_shard(args.configs, rank)
 
 
-def predicates(param_names, values):
-    """membership_predicate(spec) + resource_budget_predicate({p: 1.0}, 60)."""
-    from paper_2404_10162_b200._cabi import PRED_BUDGET, PRED_MASK
-
-    allowed = np.ones(sum(len(v) for v in values), np.uint8)
-    names = sorted(param_names)
-    return [{"kind": PRED_MASK, "allowed": allowed},
-            {"kind": PRED_BUDGET, "term_pos": np.array([param_names.index(n) for n in names], np.int32),
-             "term_w": np.ones(len(names)), "budget": BUDGET}]
+def total_configs(args, world):
+    return args.configs if W["scaling"] == "strong" else args.configs * world
 
 
 def peaks():
@@ -206,44 +181,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def reference_rate(path, tok, threads, seconds_target=15.0, max_configs=None):
-    """Times the reference's own constrained_beam_search (oracle/_ref) on host cores."""
-    from oracle.oracle import RefModel
-
-    r = RefModel(path)
-    if W["greedy"]:
-        n = min(len(tok), max(threads, 64))
-        t0 = time.perf_counter()
-        r.greedy(tok[:n], threads)
-        dt = time.perf_counter() - t0
-        n = int(min(len(tok), max(n, n / dt * seconds_target)))
-        if max_configs:
-            n = min(n, max_configs)
-        t0 = time.perf_counter()
-        r.greedy(tok[:n], threads)
-        dt = time.perf_counter() - t0
-        return n / dt, n, dt
-    names = None
-    line = "membership\nbudget bud %g " % BUDGET
-    # param names from the checkpoint header
-    with open(path, "rb") as f:
-        head = f.read(8192).split(b"\n\n")[0].decode().split("\n")
-    names = [l.split(": ", 1)[1].split(" = ")[0] for l in head if l.startswith("param.")]
-    line += ",".join(f"{n}=1.0" for n in names)
-    n0 = max(threads, 8)
-    t0 = time.perf_counter()
-    r.beam(tok[:n0], BEAM, None, line, threads)
-    dt = time.perf_counter() - t0
-    rate0 = n0 / dt
-    n = int(min(len(tok), max(n0, rate0 * seconds_target)))
-    if max_configs:
-        n = min(n, max_configs)
-    t0 = time.perf_counter()
-    r.beam(tok[:n], BEAM, None, line, threads)
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt
-
-
 def engine_libs_mapped():
     """Our engine libraries mapped into this process (/proc/self/maps)."""
     try:
@@ -263,25 +200,48 @@ def assert_no_engine_mapped():
         raise RuntimeError(f"reference arm has engine libraries mapped: {libs}")
 
 
+def reference_rate(r, tok, desc, path, threads, seconds_target=15.0, max_configs=None):
+    """Times the reference's own (constrained) beam search / greedy decode
+    (oracle/_ref, parallel_stripes over `threads`) on a prefix of tok sized to
+    ~seconds_target; returns (configs/s, configs, seconds)."""
+    def run(n):
+        t0 = time.perf_counter()
+        if W["greedy"]:
+            r.greedy(tok[:n], threads)
+        else:
+            r.beam(tok[:n], BEAM, desc[:n], WL.reference_predicate_text(path), threads)
+        return time.perf_counter() - t0
+
+    n0 = min(len(tok), max(threads, 8 if not W["greedy"] else 64))
+    rate0 = n0 / run(n0)
+    n = int(min(len(tok), max(n0, rate0 * seconds_target)))
+    if max_configs:
+        n = min(n, max_configs)
+    dt = run(n)
+    return n / dt, n, dt
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_2404_10162_b200.synth import descriptors
     from oracle.oracle import RefModel
 
-    path = model_path()
-    desc = descriptors(args.configs * max(1, args.gpus), KERNEL)
-    tok, bad = RefModel(path).encode(desc)
+    path = model_path(reference=True)
+    r = RefModel(path)
     assert_no_engine_mapped()
     threads = os.cpu_count() or 1
+    # the same configs our arm decodes (Rng::derive(2404, i), the reference's own Rng)
+    n_pool = min(total_configs(args, args.gpus), 1 << 16)
+    desc = r.descriptors(n_pool, WL.SEED)
+    tok, bad = r.encode(desc)
     # one step = a bounded sample sized so the whole W+K run ends within minutes
-    rate, n, dt = reference_rate(path, tok, threads, seconds_target=6.0)
+    rate, n, dt = reference_rate(r, tok, desc, path, threads, seconds_target=6.0)
     step_n = max(threads, int(rate * 6.0))
     times = []
     for i in range(args.warmup + args.steps):
-        r_, n_, dt_ = reference_rate(path, tok[(i * step_n) % max(1, len(tok) - step_n):], threads,
-                                     seconds_target=6.0, max_configs=step_n)
+        o = (i * step_n) % max(1, len(tok) - step_n)
+        r_, n_, dt_ = reference_rate(r, tok[o:], desc[o:], path, threads, seconds_target=6.0, max_configs=step_n)
         if i >= args.warmup:
             times.append((n_, dt_))
     tot_n = sum(t[0] for t in times)
@@ -289,17 +249,68 @@ def run_reference_arm(args):
     value = tot_n / tot_t
     out = {"metric": metric_name(), "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1000.0 * tot_t / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": W["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"{W['label']}, {KERNEL} synthetic configs, "
-                                  f"attn n_a={W['n_a']} n_s={W['n_s']} n_d=2 (bounded sample per step)",
+           "config": {"workload": f"{W['label']} (bounded sample per step)", "model": model_label(path),
                       "configs_per_step": int(tot_n / args.steps), "beam": BEAM,
-                      "predicates": "none (greedy)" if W["greedy"] else f"membership + resource_budget(sum values <= {BUDGET:g})"},
+                      "predicates": predicate_label(path),
+                      "inputs": "configs 0.. of the workload, Rng::derive(2404, i) over the model vocabulary"},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                             "sample": f"{int(tot_n / args.steps)} configs per step, "
-                                      f"constrained_beam_search via parallel_stripes({threads})"},
+                                      f"{'greedy_decode' if W['greedy'] else 'constrained_beam_search'} "
+                                      f"via parallel_stripes({threads})"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def model_label(path):
+    h = WL.read_header(path)["header"]
+    what = {"default": "reference-trained default model (tests/golden/attn_default_trained.ckpt)",
+            "cfg5": f"reference init_model(seed 1), heads x{WL.HEAD_SCALE:g}",
+            "train": "reference init_model(seed 1), dropout 0.2 / recurrent 0.2"}[W["model"]]
+    return (f"{h['variant']} n_a={h['pre_attention_size']} n_s={h['post_attention_size']} "
+            f"n_d={h['attention_dense_nodes']}, {h['kernel']}: {what}")
+
+
+def predicate_label(path):
+    if W["greedy"]:
+        return "none (greedy)"
+    return f"membership + resource_budget(sum values <= {WL.BUDGETS[WL.read_header(path)['header']['kernel']]:g})"
+
+
+def fixture_check(eng, precision, path, local):
+    """Decodes the workload's reference-decoded parity fixture
+    (tests/golden/baseline_parity.npz) with the benched
+    engine: parity counts under the tie rule (F16X3 / FP32), or decoded-sequence
+    agreement with the reference and with F16X3 (BF16, reduced precision)."""
+    key = {"cfg1": "cfg1", "cfg2": "cfg2", "cfg3": "cfg2", "cfg5": "cfg5"}.get(WNAME)
+    fx_path = os.path.join(ROOT, "tests", "golden", "baseline_parity.npz")
+    if key is None or not os.path.exists(fx_path):
+        return None
+    fx = np.load(fx_path)
+    r = {k.split("/", 1)[1]: fx[k] for k in fx.files if k.startswith(key + "/")}
+    tie = r["min_gap"] < 1e-4
+
+    def decode(e):
+        if W["greedy"]:
+            return e.greedy(r["tok"])[:, None, :]
+        return e.beam(r["tok"], BEAM, r["desc"], WL.predicate_dicts(path))["tokens"]
+
+    ref_tok = r["tokens"] if r["tokens"].ndim == 3 else r["tokens"][:, None, :]
+    g = decode(eng)
+    same_full = (g == ref_tok).all(axis=(1, 2))
+    same_top1 = (g[:, 0] == ref_tok[:, 0]).all(axis=1)
+    out = {"fixture": f"tests/golden/baseline_parity.npz:{key} (reference-decoded)", "configs": int(len(tie)),
+           "tie_adjacent": int(tie.sum()), "mismatching_non_tie": int((~same_full & ~tie).sum())}
+    if precision == "bf16":
+        from paper_2404_10162_b200 import _cabi
+
+        f = decode(_cabi.Engine(path, local, "f16x3"))
+        out = {"fixture": out["fixture"], "configs": out["configs"],
+               "vs_reference": {"top1": float(same_top1.mean()), "full_list": float(same_full.mean())},
+               "vs_f16x3": {"top1": float((g[:, 0] == f[:, 0]).all(axis=1).mean()),
+                            "full_list": float((g == f).all(axis=(1, 2)).mean())}}
+    return out
 
 
 def run_b200(args):
@@ -307,7 +318,6 @@ def run_b200(args):
     import torch.distributed as dist
 
     from paper_2404_10162_b200 import _cabi
-    from paper_2404_10162_b200.synth import descriptors
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -315,17 +325,11 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     path = model_path()
     eng = _cabi.Engine(path, local, args.precision)
-    B = args.configs
-    from paper_2404_10162_b200.parallel import weak_shard
-
-    lo, hi = weak_shard(B, rank)
-    desc = descriptors(B * world, KERNEL)[lo:hi]
+    lo, hi = shard(args, rank, world)
+    B = hi - lo
+    desc = eng.synthetic(B, WL.SEED, lo)  # configs lo..hi-1 of the workload: Rng::derive(2404, i)
     tok = eng.encode(desc)
-    with open(path, "rb") as f:
-        head = f.read(8192).split(b"\n\n")[0].decode().split("\n")
-    names = [l.split(": ", 1)[1].split(" = ")[0] for l in head if l.startswith("param.")]
-    values = [[int(x) for x in l.split(" = ")[1].split(",")] for l in head if l.startswith("param.")]
-    preds = [] if W["greedy"] else predicates(names, values)
+    preds = [] if W["greedy"] else WL.predicate_dicts(path)
     T = eng.T
     stream = torch.cuda.current_stream()
     d_tok = torch.from_numpy(tok).cuda()
@@ -365,7 +369,7 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    value = B * world * args.steps / (ms / 1000.0)
+    value = total_configs(args, world) * args.steps / (ms / 1000.0)
 
     # roofline of the dominant kernel (lstm_gemm_tc, the gate GEMMs): every launch of one
     # step on the engine stream (CUDA events), algorithmic FLOPs by the reference formula
@@ -388,14 +392,10 @@ def run_b200(args):
                  "useful_tflops": float(each_fl[top].mean()) / (float(each_ms[top].mean()) / 1000.0) / 1e12,
                  "mma_issued_tflops": float(each_ex[top].mean()) / (float(each_ms[top].mean()) / 1000.0) / 1e12}
     step_achieved = useful / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
-            traffic = json.load(f).get(args.precision)
-    except Exception:
-        pass
+    traffic = traffic_of(args.precision, B)
 
-    # end to end through the host C-ABI (pinned staging, copies in the timed region)
+    # end to end through the host C-ABI (host buffers; H2D of tokens and D2H of beams and
+    # log-probs inside the timed region)
     host_out = [None]
 
     def host_call():
@@ -409,6 +409,8 @@ def run_b200(args):
         host_call()
     e2e_t = []
     for _ in range(max(2, args.steps // 2)):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         host_call()
         e2e_t.append(time.perf_counter() - t0)
@@ -417,42 +419,56 @@ def run_b200(args):
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = B * world * len(e2e_t) / e2e_s
+    e2e = total_configs(args, world) * len(e2e_t) / e2e_s
     h2d = B * 7 * 4
-    d2h = B * BEAM * T * 4 + B * BEAM * 8 + 4 * B * 4
+    d2h = B * BEAM * T * 4 if W["greedy"] else B * BEAM * T * 4 + B * BEAM * 8 + 4 * B * 4
 
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = fixture_check(eng, args.precision, path, local)
+        except Exception as ex:  # reported, never fatal for the GPU number
+            parity = {"error": str(ex)}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
-            from oracle.oracle import ref_available
+            from oracle.oracle import RefModel, ref_available
 
             if ref_available():
                 threads = os.cpu_count() or 1
-                rate, n, dt = reference_rate(path, tok, threads, seconds_target=15.0)
+                ref_path = model_path(reference=True)
+                rate, n, dt = reference_rate(RefModel(ref_path), tok, desc, ref_path, threads, seconds_target=15.0)
                 cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                       "sample": f"{n} configs of the same workload in {dt:.1f} s "
-                                 f"(reference constrained_beam_search, parallel_stripes({threads}))"}
-        except Exception as ex:  # reported, never fatal for the GPU number
+                       "sample": f"the first {n} configs of the same workload in {dt:.1f} s (reference "
+                                 f"{'greedy_decode' if W['greedy'] else 'constrained_beam_search'}, "
+                                 f"parallel_stripes({threads}))"}
+        except Exception as ex:
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
     if rank == 0:
         out = {
             "metric": metric_name(), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": W["scaling"], "vs_baseline": None,
             "dtype": {"f16x3": "f16x3 (fp16 hi/lo split, 3 MMAs, fp32 accumulate; fp32-grade)",
                       "fp32": "fp32", "bf16": "bf16 (fp32 accumulate)"}[args.precision],
             "data": "synthetic",
-            "config": {"workload": f"{W['label']}, {B} synthetic {KERNEL} problem configs per GPU",
-                       "model": f"attn n_a={W['n_a']} n_s={W['n_s']} n_d=2 (random init, reference checkpoint format)",
-                       "configs_per_gpu": B, "beam": BEAM,
-                       "predicates": "none (greedy)" if W["greedy"] else f"membership + resource_budget(sum values <= {BUDGET:g})",
+            "config": {"workload": f"{W['label']}: {total_configs(args, world)} synthetic configs"
+                                   f"{' per GPU' if W['scaling'] == 'weak' else ' in total'}",
+                       "model": model_label(path),
+                       "configs_per_gpu": B, "configs_total": total_configs(args, world), "beam": BEAM,
+                       "inputs": "config i = Rng::derive(2404, i) draw over the model vocabulary "
+                                 "(ks_synthetic_descriptors; rank r decodes its contiguous shard)",
+                       "predicates": predicate_label(path),
                        "l2": "flushed (512 MiB write) before every timed step",
                        "parallelism": f"dp{world} (configs sharded by rank, no collective)"},
+            "parity": parity,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "ks_beam_search_batch (host buffers)"},
+                    "api": "ks_greedy_batch (host buffers)" if W["greedy"]
+                    else "ks_beam_search_batch (host buffers)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
-                         "frac": achieved / bf16_peak, "traffic": traffic,
+                         "frac": achieved / bf16_peak, "traffic": traffic["bytes"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else "no ncu capture for this workload",
                          "kernel": ("lstm_gemm_tc (gate GEMMs + fused LSTM cell, incl. the context projection), "
                                     "all launches of one step" if args.precision != "fp32" else "lstm_step_simt"),
                          "peak_kind": f"{peak_kind} bf16 dense, sustained (MEASURED_PEAKS.json; burst {bf16_burst:g})",
@@ -471,6 +487,47 @@ def run_b200(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def traffic_of(precision, configs_per_gpu):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the full-beam
+    gate-GEMM launch from the ncu --set full capture of THIS workload and
+    precision (profiles/traffic.json, written by tools/measure_traffic.py), when
+    the captured batch matches."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)[WNAME][precision]
+    except Exception:
+        return None
+    if int(t.get("configs_per_gpu", -1)) != int(configs_per_gpu):
+        return None
+    return {"bytes": t["dram_bytes"], "source": t["source"]}
+
+
+def train_data(path, B, seed=4):
+    """Synthetic teacher-forcing batch: the workload's configs (Rng::derive(2404, i)
+    over the model vocabulary, encoded) + uniformly drawn target tokens (numpy,
+    seeded: both arms train on identical batches)."""
+    from oracle.train_oracle import Checkpoint  # header parsing only
+    from paper_2404_10162_b200 import _cabi
+
+    ck = Checkpoint(path)
+    h = WL.read_header(path)
+    desc = _cabi.synthetic_descriptors(h["inputs"], B, WL.SEED) if not W.get("ref_arm") else None
+    if desc is None:
+        from oracle.oracle import RefModel
+        desc = RefModel(path).descriptors(B, WL.SEED)
+    tok = np.stack([np.searchsorted(np.asarray(h["inputs"][f]), desc[:, f]) for f in range(7)], 1).astype(np.int32)
+    rng = np.random.default_rng(seed)
+    tgt = np.stack([rng.integers(0, v, B) for v in ck.vsizes], 1).astype(np.int32)
+    return tok, tgt, ck
+
+
+def train_flops_per_sample(ck):
+    """SURVEY.md §8(d): ~3x the forward gate-GEMM FLOPs (forward, dX, dW)."""
+    dec = ck.T * 2.0 * (2 * ck.n_a + ck.n_s) * 4 * ck.n_s
+    enc = 2 * 7 * 2.0 * ck.n_a * 4 * ck.n_a
+    return 3.0 * (dec + enc)
 
 
 def reference_train_rate(path, tok, tgt, threads, n):
@@ -503,7 +560,8 @@ def run_train_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    path = model_path()
+    W["ref_arm"] = True  # configs from the reference's own Rng, no engine library
+    path = model_path(reference=True)
     tok, tgt, ck = train_data(path, 4096)
     threads = os.cpu_count() or 1
     reference_train_rate(path, tok, tgt, threads, 1)  # loads oracle/_ref
@@ -662,12 +720,12 @@ def run_train(args):
 
 
 def main():
-    global W, KERNEL, BEAM, CONFIGS_PER_GPU
+    global W, WNAME, BEAM
     args = parse()
-    W = WORKLOADS[args.workload]
-    KERNEL, BEAM, CONFIGS_PER_GPU = W["kernel"], W["beam"], W["configs"]
+    W, WNAME = WORKLOADS[args.workload], args.workload
+    BEAM = W["beam"]
     if args.configs is None:
-        args.configs = CONFIGS_PER_GPU
+        args.configs = W["configs"]
     if W.get("train"):
         (run_train_reference_arm if args.impl == "reference" else run_train)(args)
     elif args.impl == "reference":

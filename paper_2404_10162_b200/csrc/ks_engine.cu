@@ -162,6 +162,15 @@ struct ks_engine {
     DevMem hrej;                  // host-hook rejections [C*k][Vmax]
     DevMem truth, evalc;          // topk_metrics: truths [C][T], counters [T + 1]
     HostMem h_in, h_out, hk_keys, hk_live, hk_rej;
+    // chunk pipeline (decode_chunks): two sets of chunk I/O buffers; chunk i decodes
+    // from / into set i & 1 on `stream` while the results of chunk i - 1 leave on
+    // `copy_stream` and are unpacked on the host
+    struct ChunkIO {
+        DevMem tok, desc, otok, olp, ocount, ostatus, ofpred, ofstep;
+        HostMem h_in, h_out;
+        cudaEvent_t dec_done = nullptr, copy_done = nullptr;
+    } io[2];
+    cudaStream_t copy_stream = nullptr;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     int beam_smem_max = 0;
@@ -197,6 +206,11 @@ struct ks_engine {
     ~ks_engine() {
         for (auto& g : graphs)
             if (g.exec) cudaGraphExecDestroy(g.exec);
+        for (auto& b : io) {
+            if (b.dec_done) cudaEventDestroy(b.dec_done);
+            if (b.copy_done) cudaEventDestroy(b.copy_done);
+        }
+        if (copy_stream) cudaStreamDestroy(copy_stream);
     }
     // model_forward (ks_forward_batch): set for the duration of that call only
     const int* fw_teacher = nullptr;  // device [C][T] teacher tokens of the chunk, or null (argmax)
@@ -562,8 +576,13 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
     }
     std::vector<long long> vals(E.out_values.begin(), E.out_values.end());
     if ((st = upload(E.values, vals.data(), vals.size() * 8))) return st;
-    if (cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&E.copy_stream, cudaStreamNonBlocking) != cudaSuccess)
         return set_error(KS_ERR_CUDA, "stream creation failed");
+    for (auto& b : E.io)
+        if (cudaEventCreateWithFlags(&b.dec_done, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&b.copy_done, cudaEventDisableTiming) != cudaSuccess)
+            return set_error(KS_ERR_CUDA, "event creation failed");
     E.beam_smem_max = 227 * 1024;
     {
         const char* cp = std::getenv("KS_CTXPROJ");
@@ -1388,14 +1407,17 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
 ks_status run_chunk_graph(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greedy, const int* d_tok,
                           const long long* d_desc, const PredDev& pd, int* o_tok, double* o_lp, int* o_count,
                           int* o_status, int* o_fpred, int* o_fstep, bool single_chunk) {
-    // multi-chunk decodes would cycle through one graph per chunk offset: plain launches
+    // multi-chunk decodes through caller buffers would cycle through one graph per chunk
+    // offset: plain launches (decode_chunks passes its two internal buffer sets instead)
     if (!single_chunk || !E.use_graphs || E.prof || pd.has_host)
         return run_chunk(E, C, cfg_base, k, greedy, d_tok, d_desc, pd, o_tok, o_lp, o_count, o_status, o_fpred,
                          o_fstep);
     ks_status st;
     if ((st = ensure_workspace(E, C, k))) return st;  // allocations before the key is taken
     auto P = [](const void* p) { return (long long)reinterpret_cast<uintptr_t>(p); };
-    const std::vector<long long> key = {C, cfg_base, k, greedy ? 1 : 0, P(d_tok), P(d_desc), pd.n, pd.n_terms,
+    // cfg_base only reaches the host-hook rows, and host predicates bypass graphs: a
+    // chunk at any offset replays the graph of its buffers
+    const std::vector<long long> key = {C, k, greedy ? 1 : 0, P(d_tok), P(d_desc), pd.n, pd.n_terms,
                                         pd.n_bytes, pd.needs_desc ? 1 : 0, P(o_tok), P(o_lp), P(o_count),
                                         P(o_status), P(o_fpred), P(o_fstep),
                                         (long long)g_alloc_gen.load()};
@@ -1484,6 +1506,149 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     for (auto& t : th) t.join();
 }
 
+// Where a decode call's inputs come from and its results go.
+struct ChunkOut {
+    int32_t* tok;
+    double* lp;
+    int32_t* count;
+    int32_t* status;
+    int32_t* fpred;
+    int32_t* fstep;
+};
+
+// The chunk pipeline behind every batch decode.  B configs run in chunks of C =
+// E.chunk; chunk i uses buffer set s = i & 1:
+//   stream:       [inputs -> io[s].tok]  wait(copy_done[s])  decode (CUDA graph)  record dec_done[s]
+//   copy_stream:  wait(dec_done[s])  results io[s] -> caller (D2H / D2D)  record copy_done[s]
+//   host:         stage chunk i's inputs; unpack chunk i-1's results (staged D2H)
+// so chunk i's decode overlaps chunk i-1's result transfer and host unpacking, and
+// every chunk replays one of (at most) three graphs: full chunk in set 0 / 1, the
+// tail chunk.  device_io: tok / desc / outputs are device pointers and `user` is the
+// caller's stream (ordered before and after the call by events); otherwise host
+// buffers, page-locked results receiving the D2H copy directly.
+ks_status decode_chunks(ks_engine& E, int64_t B, int k, bool greedy, const PredDev& pd, const int32_t* tok,
+                        const int64_t* desc, bool device_io, int32_t* out_tok, double* out_lp, int32_t* out_count,
+                        int32_t* out_status, int32_t* out_fpred, int32_t* out_fstep, cudaStream_t user) {
+    const int T = E.T;
+    E.launches = 0;
+    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
+    const bool want_desc = desc && pd.needs_desc;
+    for (auto& b : E.io) {
+        if (b.tok.ensure((size_t)C * 7 * 4) || (want_desc && b.desc.ensure((size_t)C * 7 * 8)) ||
+            b.otok.ensure((size_t)C * k * T * 4) || b.olp.ensure((size_t)C * k * 8) ||
+            b.ocount.ensure((size_t)C * 4) || b.ostatus.ensure((size_t)C * 4) || b.ofpred.ensure((size_t)C * 4) ||
+            b.ofstep.ensure((size_t)C * 4))
+            return set_error(KS_ERR_CUDA, "chunk buffer allocation failed");
+        if (!device_io && (b.h_in.ensure((size_t)C * 7 * 4 + (size_t)C * 7 * 8) ||
+                           b.h_out.ensure((size_t)C * k * T * 4 + (size_t)C * k * 8 + (size_t)C * 4 * 4)))
+            return set_error(KS_ERR_CUDA, "pinned staging allocation failed");
+    }
+    ks_status st;
+    if ((st = ensure_workspace(E, C, k))) return st;
+    cudaStream_t s = E.stream, cs = E.copy_stream;
+    if (device_io) {  // the caller's prior work (inputs) before ours
+        KS_CUDA(cudaEventRecord(E.io[1].dec_done, user));
+        KS_CUDA(cudaStreamWaitEvent(s, E.io[1].dec_done, 0));
+    }
+    // page-locked host results take the device-to-host copy directly
+    auto pinned = [](const void* p) {
+        if (!p) return true;
+        cudaPointerAttributes a{};
+        const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+        (void)cudaGetLastError();
+        return ok;
+    };
+    const bool direct = device_io || (pinned(out_tok) && (greedy || (pinned(out_lp) && pinned(out_count) &&
+                                                                    pinned(out_status) && pinned(out_fpred) &&
+                                                                    pinned(out_fstep))));
+    const cudaMemcpyKind out_kind = device_io ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    // host side of a staged chunk: pinned staging -> caller buffers
+    auto unpack = [&](int sb, int64_t c0, int64_t n) -> ks_status {
+        KS_CUDA(cudaEventSynchronize(E.io[sb].copy_done));
+        if (direct) return KS_OK;
+        const char* ho = E.io[sb].h_out.as<char>();
+        const int32_t* h_tok = reinterpret_cast<const int32_t*>(ho);
+        const double* h_lp = reinterpret_cast<const double*>(ho + (size_t)C * k * T * 4);
+        const int32_t* h_misc = reinterpret_cast<const int32_t*>(ho + (size_t)C * k * T * 4 + (size_t)C * k * 8);
+        par_memcpy(out_tok + c0 * k * T, h_tok, (size_t)n * k * T * 4);
+        if (!greedy) {
+            if (out_lp) par_memcpy(out_lp + c0 * k, h_lp, (size_t)n * k * 8);
+            if (out_count) std::memcpy(out_count + c0, h_misc, (size_t)n * 4);
+            if (out_status) std::memcpy(out_status + c0, h_misc + C, (size_t)n * 4);
+            if (out_fpred) std::memcpy(out_fpred + c0, h_misc + 2 * C, (size_t)n * 4);
+            if (out_fstep) std::memcpy(out_fstep + c0, h_misc + 3 * C, (size_t)n * 4);
+        }
+        return KS_OK;
+    };
+    int64_t prev_c0 = -1, prev_n = 0;
+    int prev_sb = 0;
+    for (int64_t c0 = 0, i = 0; c0 < B; c0 += C, ++i) {
+        const int64_t n = std::min<int64_t>(C, B - c0);
+        const int sb = (int)(i & 1);
+        auto& b = E.io[sb];
+        // inputs of this chunk (the staging of set sb was last read by chunk i - 2's
+        // upload, which completed before its results were unpacked)
+        const long long* ddesc = nullptr;
+        if (device_io) {
+            KS_CUDA(cudaMemcpyAsync(b.tok.p, tok + c0 * 7, (size_t)n * 7 * 4, cudaMemcpyDeviceToDevice, s));
+            if (want_desc)
+                KS_CUDA(cudaMemcpyAsync(b.desc.p, desc + c0 * 7, (size_t)n * 7 * 8, cudaMemcpyDeviceToDevice, s));
+        } else {
+            int32_t* htok = b.h_in.as<int32_t>();
+            par_memcpy(htok, tok + c0 * 7, (size_t)n * 7 * 4);
+            KS_CUDA(cudaMemcpyAsync(b.tok.p, htok, (size_t)n * 7 * 4, cudaMemcpyHostToDevice, s));
+            if (want_desc) {
+                int64_t* hdesc = reinterpret_cast<int64_t*>(b.h_in.as<char>() + (size_t)C * 7 * 4);
+                std::memcpy(hdesc, desc + c0 * 7, (size_t)n * 7 * 8);
+                KS_CUDA(cudaMemcpyAsync(b.desc.p, hdesc, (size_t)n * 7 * 8, cudaMemcpyHostToDevice, s));
+            }
+        }
+        if (want_desc) ddesc = b.desc.as<long long>();
+        // the decode overwrites set sb's results: chunk i - 2's copy-out must be done
+        KS_CUDA(cudaStreamWaitEvent(s, b.copy_done, 0));
+        if ((st = run_chunk_graph(E, n, c0, k, greedy, b.tok.as<int>(), ddesc, pd, b.otok.as<int>(),
+                                  b.olp.as<double>(), b.ocount.as<int>(), b.ostatus.as<int>(), b.ofpred.as<int>(),
+                                  b.ofstep.as<int>(), true)))
+            return st;
+        KS_CUDA(cudaEventRecord(b.dec_done, s));
+        KS_CUDA(cudaStreamWaitEvent(cs, b.dec_done, 0));
+        if (direct) {
+            KS_CUDA(cudaMemcpyAsync(out_tok + c0 * k * T, b.otok.p, (size_t)n * k * T * 4, out_kind, cs));
+            if (!greedy) {
+                if (out_lp) KS_CUDA(cudaMemcpyAsync(out_lp + c0 * k, b.olp.p, (size_t)n * k * 8, out_kind, cs));
+                if (out_count) KS_CUDA(cudaMemcpyAsync(out_count + c0, b.ocount.p, (size_t)n * 4, out_kind, cs));
+                if (out_status) KS_CUDA(cudaMemcpyAsync(out_status + c0, b.ostatus.p, (size_t)n * 4, out_kind, cs));
+                if (out_fpred) KS_CUDA(cudaMemcpyAsync(out_fpred + c0, b.ofpred.p, (size_t)n * 4, out_kind, cs));
+                if (out_fstep) KS_CUDA(cudaMemcpyAsync(out_fstep + c0, b.ofstep.p, (size_t)n * 4, out_kind, cs));
+            }
+        } else {
+            char* ho = b.h_out.as<char>();
+            int32_t* h_misc = reinterpret_cast<int32_t*>(ho + (size_t)C * k * T * 4 + (size_t)C * k * 8);
+            KS_CUDA(cudaMemcpyAsync(ho, b.otok.p, (size_t)n * k * T * 4, cudaMemcpyDeviceToHost, cs));
+            if (!greedy) {
+                KS_CUDA(cudaMemcpyAsync(ho + (size_t)C * k * T * 4, b.olp.p, (size_t)n * k * 8, cudaMemcpyDeviceToHost, cs));
+                KS_CUDA(cudaMemcpyAsync(h_misc, b.ocount.p, (size_t)n * 4, cudaMemcpyDeviceToHost, cs));
+                KS_CUDA(cudaMemcpyAsync(h_misc + C, b.ostatus.p, (size_t)n * 4, cudaMemcpyDeviceToHost, cs));
+                KS_CUDA(cudaMemcpyAsync(h_misc + 2 * C, b.ofpred.p, (size_t)n * 4, cudaMemcpyDeviceToHost, cs));
+                KS_CUDA(cudaMemcpyAsync(h_misc + 3 * C, b.ofstep.p, (size_t)n * 4, cudaMemcpyDeviceToHost, cs));
+            }
+        }
+        KS_CUDA(cudaEventRecord(b.copy_done, cs));
+        // the previous chunk's results, unpacked while this chunk decodes
+        if (!device_io && prev_c0 >= 0 && (st = unpack(prev_sb, prev_c0, prev_n))) return st;
+        prev_c0 = c0;
+        prev_n = n;
+        prev_sb = sb;
+    }
+    if (device_io) {  // the caller's stream continues after our last copy
+        if (prev_c0 >= 0) KS_CUDA(cudaStreamWaitEvent(user, E.io[prev_sb].copy_done, 0));
+    } else if (prev_c0 >= 0 && (st = unpack(prev_sb, prev_c0, prev_n))) {
+        return st;
+    }
+    if (E.prof) collect_profile(E);
+    return KS_OK;
+}
+
 ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, int64_t B, int32_t k,
                       bool greedy, const ks_pred* preds, int32_t n_preds, int32_t* out_tok,
                       double* out_lp, int32_t* out_count, int32_t* out_status, int32_t* out_fpred,
@@ -1515,79 +1680,8 @@ ks_status decode_host(ks_engine* eng, const int32_t* tok, const int64_t* desc, i
     if (pd.needs_desc && !desc) return set_error(KS_ERR_PARAMETER, "divisibility predicates need descriptors");
     pd.hook = hook;
     pd.user = user;
-    E.launches = 0;
-    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
-    const size_t in_bytes = (size_t)C * 7 * 4 + (size_t)C * 7 * 8;
-    const size_t out_bytes = (size_t)C * k * T * 4 + (size_t)C * k * 8 + (size_t)C * 4 * 4;
-    if (E.h_in.ensure(in_bytes) != cudaSuccess || E.h_out.ensure(out_bytes) != cudaSuccess)
-        return set_error(KS_ERR_CUDA, "pinned staging allocation failed");
-    if (E.otok.ensure((size_t)C * k * T * 4) || E.olp.ensure((size_t)C * k * 8) ||
-        E.ocount.ensure((size_t)C * 4) || E.ostatus.ensure((size_t)C * 4) ||
-        E.ofpred.ensure((size_t)C * 4) || E.ofstep.ensure((size_t)C * 4))
-        return set_error(KS_ERR_CUDA, "output allocation failed");
-    if ((st = ensure_workspace(E, C, k))) return st;
-    // page-locked result buffers take the device-to-host copy directly
-    auto pinned = [](const void* p) {
-        if (!p) return true;
-        cudaPointerAttributes a{};
-        const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
-        (void)cudaGetLastError();
-        return ok;
-    };
-    const bool direct = pinned(out_tok) && (greedy || (pinned(out_lp) && pinned(out_count) && pinned(out_status) &&
-                                                         pinned(out_fpred) && pinned(out_fstep)));
-    for (int64_t c0 = 0; c0 < B; c0 += C) {
-        const int64_t n = std::min<int64_t>(C, B - c0);
-        int32_t* htok = E.h_in.as<int32_t>();
-        int64_t* hdesc = reinterpret_cast<int64_t*>(E.h_in.as<char>() + (size_t)C * 7 * 4);
-        par_memcpy(htok, tok + c0 * 7, (size_t)n * 7 * 4);
-        KS_CUDA(cudaMemcpyAsync(E.tok.p, htok, (size_t)n * 7 * 4, cudaMemcpyHostToDevice, E.stream));
-        const long long* ddesc = nullptr;
-        if (desc && pd.needs_desc) {
-            std::memcpy(hdesc, desc + c0 * 7, (size_t)n * 7 * 8);
-            KS_CUDA(cudaMemcpyAsync(E.desc.p, hdesc, (size_t)n * 7 * 8, cudaMemcpyHostToDevice, E.stream));
-            ddesc = E.desc.as<long long>();
-        }
-        if ((st = run_chunk_graph(E, n, c0, k, greedy, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
-                                  E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>(),
-                                  B <= C)))
-            return st;
-        if (direct) {
-            KS_CUDA(cudaMemcpyAsync(out_tok + c0 * k * T, E.otok.p, (size_t)n * k * T * 4, cudaMemcpyDeviceToHost, E.stream));
-            if (!greedy) {
-                if (out_lp) KS_CUDA(cudaMemcpyAsync(out_lp + c0 * k, E.olp.p, (size_t)n * k * 8, cudaMemcpyDeviceToHost, E.stream));
-                if (out_count) KS_CUDA(cudaMemcpyAsync(out_count + c0, E.ocount.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-                if (out_status) KS_CUDA(cudaMemcpyAsync(out_status + c0, E.ostatus.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-                if (out_fpred) KS_CUDA(cudaMemcpyAsync(out_fpred + c0, E.ofpred.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-                if (out_fstep) KS_CUDA(cudaMemcpyAsync(out_fstep + c0, E.ofstep.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-            }
-            KS_CUDA(cudaStreamSynchronize(E.stream));
-            continue;
-        }
-        char* ho = E.h_out.as<char>();
-        int32_t* h_tok = reinterpret_cast<int32_t*>(ho);
-        double* h_lp = reinterpret_cast<double*>(ho + (size_t)C * k * T * 4);
-        int32_t* h_misc = reinterpret_cast<int32_t*>(ho + (size_t)C * k * T * 4 + (size_t)C * k * 8);
-        KS_CUDA(cudaMemcpyAsync(h_tok, E.otok.p, (size_t)n * k * T * 4, cudaMemcpyDeviceToHost, E.stream));
-        if (!greedy) {
-            KS_CUDA(cudaMemcpyAsync(h_lp, E.olp.p, (size_t)n * k * 8, cudaMemcpyDeviceToHost, E.stream));
-            KS_CUDA(cudaMemcpyAsync(h_misc, E.ocount.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-            KS_CUDA(cudaMemcpyAsync(h_misc + C, E.ostatus.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-            KS_CUDA(cudaMemcpyAsync(h_misc + 2 * C, E.ofpred.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-            KS_CUDA(cudaMemcpyAsync(h_misc + 3 * C, E.ofstep.p, (size_t)n * 4, cudaMemcpyDeviceToHost, E.stream));
-        }
-        KS_CUDA(cudaStreamSynchronize(E.stream));
-        par_memcpy(out_tok + c0 * k * T, h_tok, (size_t)n * k * T * 4);
-        if (!greedy) {
-            if (out_lp) par_memcpy(out_lp + c0 * k, h_lp, (size_t)n * k * 8);
-            if (out_count) std::memcpy(out_count + c0, h_misc, (size_t)n * 4);
-            if (out_status) std::memcpy(out_status + c0, h_misc + C, (size_t)n * 4);
-            if (out_fpred) std::memcpy(out_fpred + c0, h_misc + 2 * C, (size_t)n * 4);
-            if (out_fstep) std::memcpy(out_fstep + c0, h_misc + 3 * C, (size_t)n * 4);
-        }
-    }
-    if (E.prof) collect_profile(E);
-    return KS_OK;
+    return decode_chunks(E, B, k, greedy, pd, tok, desc, /*device_io=*/false, out_tok, out_lp, out_count,
+                         out_status, out_fpred, out_fstep, nullptr);
 }
 
 }  // namespace
@@ -1803,27 +1897,8 @@ extern "C" ks_status ks_beam_search_device(ks_engine* eng, const int32_t* d_tok,
     PredDev pd;
     if ((st = upload_preds(E, preds, n_preds, pd))) return st;
     if (pd.needs_desc && !d_desc) return set_error(KS_ERR_PARAMETER, "divisibility predicates need descriptors");
-    E.launches = 0;
-    cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
-    cudaEvent_t ev;
-    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaEventRecord(ev, user);
-    cudaStreamWaitEvent(E.stream, ev, 0);
-    const int T = E.T;
-    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
-    for (int64_t c0 = 0; c0 < B; c0 += C) {
-        const int64_t n = std::min<int64_t>(C, B - c0);
-        st = run_chunk_graph(E, n, c0, k, false, d_tok + c0 * 7, d_desc ? reinterpret_cast<const long long*>(d_desc) + c0 * 7 : nullptr,
-                       pd, d_out_tok + c0 * k * T, d_out_lp + c0 * k, d_out_count + c0,
-                       d_out_status ? d_out_status + c0 : nullptr, d_out_fpred ? d_out_fpred + c0 : nullptr,
-                       d_out_fstep ? d_out_fstep + c0 : nullptr, B <= C);
-        if (st) break;
-    }
-    cudaEventRecord(ev, E.stream);
-    cudaStreamWaitEvent(user, ev, 0);
-    cudaEventDestroy(ev);
-    if (!st && E.prof) collect_profile(E);
-    return st;
+    return decode_chunks(E, B, k, false, pd, d_tok, d_desc, /*device_io=*/true, d_out_tok, d_out_lp, d_out_count,
+                         d_out_status, d_out_fpred, d_out_fstep, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" void ks_engine_profile_reset(ks_engine* eng, int32_t enable) {

@@ -1,6 +1,6 @@
 """Parity fixtures for the BASELINE.json workloads, made BY THE REFERENCE.
 
-    python tests/golden/make_baseline_fixtures.py        (~15 min on 8 cores)
+    python tests/golden/make_baseline_fixtures.py [cfg1|cfg2|cfg5 ...]   (~10 min on 8 cores)
 
 Writes tests/golden/baseline_parity.npz:
 
@@ -72,20 +72,26 @@ def decode_both(path, idx, k, greedy=False):
 
 
 def main():
-    fx = {}
-    print("cfg1", flush=True)
-    for k, v in decode_both(W.DEFAULT_CKPT, np.arange(1000, dtype=np.int64), 1, greedy=True).items():
-        fx[f"cfg1/{k}"] = v
-    print("cfg5", flush=True)
-    p5 = W.cfg5_checkpoint_reference()
-    fx["cfg5/sha256"] = np.array(W.sha256(p5))
-    for k, v in decode_both(p5, np.arange(256, dtype=np.int64), 16).items():
-        fx[f"cfg5/{k}"] = v
-    print("cfg2", flush=True)
-    for k, v in decode_both(W.DEFAULT_CKPT, cfg2_indices(), 5).items():
-        fx[f"cfg2/{k}"] = v
-    np.savez_compressed(os.path.join(HERE, "baseline_parity.npz"), **fx)
-    print("cfg5 sha256", fx["cfg5/sha256"])
+    out = os.path.join(HERE, "baseline_parity.npz")
+    only = sys.argv[1:]  # e.g. `cfg5`: regenerate that workload, keep the others
+    fx = dict(np.load(out)) if only and os.path.exists(out) else {}
+    want = lambda c: not only or c in only  # noqa: E731
+    if want("cfg1"):
+        print("cfg1", flush=True)
+        for k, v in decode_both(W.DEFAULT_CKPT, np.arange(1000, dtype=np.int64), 1, greedy=True).items():
+            fx[f"cfg1/{k}"] = v
+    if want("cfg5"):
+        print("cfg5", flush=True)
+        p5 = W.cfg5_checkpoint_reference()
+        fx["cfg5/sha256"] = np.array(W.sha256(p5))
+        for k, v in decode_both(p5, np.arange(256, dtype=np.int64), 16).items():
+            fx[f"cfg5/{k}"] = v
+    if want("cfg2"):
+        print("cfg2", flush=True)
+        for k, v in decode_both(W.DEFAULT_CKPT, cfg2_indices(), 5).items():
+            fx[f"cfg2/{k}"] = v
+    np.savez_compressed(out, **fx)
+    print("cfg5 sha256", fx["cfg5/sha256"], "(workloads.CFG5_SHA256)")
 
 
 if __name__ == "__main__":
