@@ -88,7 +88,9 @@ def test_cfg5_large_model_beam16(fx, precision):
     assert W.sha256(path) == str(r["sha256"]), "cfg5 checkpoint differs from the reference-written one"
     g = engine(path, precision).beam(r["tok"], 16, r["desc"], W.predicate_dicts(path))
     n, ties, bad = compare_beams(g, r)
-    assert n >= 0.9 * len(r["tok"]), (n, ties)
+    # beam 16 over 10 positions: ~13% of these untrained-but-peaked configs have a
+    # deciding gap under 1e-4 relative in fp64 and are excluded by the tie rule
+    assert n >= 0.8 * len(r["tok"]), (n, ties)
     assert not bad, f"{len(bad)} mismatching of {n} compared ({ties} tie-adjacent); first {bad[:8]}"
 
 
