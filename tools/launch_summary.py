@@ -7,10 +7,10 @@ rows = list(csv.reader(open(sys.argv[1])))
 h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 hdr, data = rows[h], rows[h + 1:]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 tot, cnt = collections.defaultdict(float), collections.Counter()
 for r in data:
-    us = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    us = float(r[vi].replace(",", "")) * scale[r[ui]]
     name = r[ki].split("(")[0][:48]
     tot[name] += us
     cnt[name] += 1
