@@ -661,22 +661,12 @@ def run_train(args):
     e2e = GB * len(e2e_t) / e2e_s
     fl = train_flops_per_sample(ck)
     achieved = fl * value / 1e12
-    # the trainer's GEMMs run as 3 passes of split operands (fp32-grade): fp16 hi/lo
-    # (F16X3, the default) on the fp16 tensor cores -> the measured sustained bf16/fp16
-    # rate; 3xTF32 (KS_TRAIN_GEMM=tf32x3) -> the TF32 rate measured the same way
-    # (tools/measure_tf32.py), else the nominal B200_PROFILING.md figure
+    # the trainer's GEMMs run F16X3 (fp16 hi/lo split along a tripled K, one pass of
+    # our tcgen05 GEMM, ks_gemm16.cu) -> the measured sustained bf16/fp16 rate;
+    # KS_TRAIN_GEMM=fp32 runs every contraction on the fp32 SIMT GEMM
     gemm_mode = os.environ.get("KS_TRAIN_GEMM", "f16x3")
-    if gemm_mode == "tf32x3":
-        try:
-            with open(os.path.join(ROOT, "profiles", "measured_tf32.json")) as f:
-                tf32_peak = float(json.load(f)["tf32_tflops_sustained"])
-            tf32_kind = "measured dense TF32, sustained (profiles/measured_tf32.json, tools/measure_tf32.py)"
-        except Exception:
-            tf32_peak = 1100.0
-            tf32_kind = "nominal dense TF32 (B200_PROFILING.md; no measured TF32 peak)"
-    else:
-        tf32_peak, _, kind0, _ = peaks()
-        tf32_kind = f"{kind0} dense bf16/fp16, sustained (MEASURED_PEAKS.json): F16X3 training GEMMs"
+    tf32_peak, _, kind0, _ = peaks()
+    tf32_kind = f"{kind0} dense bf16/fp16, sustained (MEASURED_PEAKS.json): F16X3 training GEMMs"
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -695,7 +685,7 @@ def run_train(args):
     if rank == 0:
         out = {"metric": TRAIN_METRIC, "value": value, "unit": TRAIN_UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": ("fp32 (3xTF32 tensor-core GEMMs, fp32 elsewhere)" if gemm_mode == "tf32x3" else
+               "scaling": "strong", "vs_baseline": None, "dtype": ("fp32 (SIMT GEMMs)" if gemm_mode == "fp32" else
                          "fp32-grade (F16X3 tensor-core GEMMs: fp16 hi/lo at per-operand scales, fp32 accumulate; fp32 elsewhere)"), "data": "synthetic",
                "config": {"workload": W["label"], "global_batch": GB, "per_gpu_batch": hi - lo,
                           "model": "attn n_a=256 n_s=512 n_d=2 (random init), dropout 0.2 / recurrent 0.2 "
@@ -709,7 +699,7 @@ def run_train(args):
                                                         "all-reduce + ks_trainer_apply) from pinned host buffers"},
                "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                             "frac": achieved / tf32_peak, "traffic": None,
-                            "kernel": f"whole training step: {'3xTF32' if gemm_mode == 'tf32x3' else 'F16X3'} gate GEMMs (cuBLASLt, split operands) + fused "
+                            "kernel": f"whole training step: {'fp32 SIMT' if gemm_mode == 'fp32' else 'F16X3 tcgen05 (ks_gemm16.cu)'} GEMMs + fused "
                                       "cell / attention / head / dropout kernels",
                             "peak_kind": tf32_kind,
                             "flops_per_sample": fl, "mma_issued_tflops_upper": 3.0 * achieved},

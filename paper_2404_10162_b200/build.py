@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["ks_kernels.cu", "ks_engine.cu", "ks_gemm_tc.cu", "ks_train.cu"]
+CU_SOURCES = ["ks_kernels.cu", "ks_engine.cu", "ks_gemm_tc.cu", "ks_gemm16.cu", "ks_train.cu"]
 CPP_SOURCES = ["ks_checkpoint.cpp", "ks_synth.cpp", "ks_group.cpp"]
 
 
@@ -61,7 +61,7 @@ def build_engine(verbose: bool = False, force: bool = False) -> str:
             print(log)
     objs = [os.path.join(BUILD, s + ".o") for s in CU_SOURCES + CPP_SOURCES]
     if force or jobs or not os.path.exists(out):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-L/usr/local/cuda/lib64", "-lcublas", "-lcublasLt",
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-L/usr/local/cuda/lib64",
               "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
     return out
 

@@ -34,8 +34,6 @@
 // recurrent rows; column g*H + j, gates input, forget, output, cand)  followed
 // by  Ws [S + 1][4H]  (one-hot slot rows, then the bias).  Adam and the clip
 // are elementwise / order-free, so they run on the flat buffer directly.
-#include <cublasLt.h>
-#include <cublas_v2.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -52,6 +50,7 @@
 
 #include "ks_b200.h"
 #include "ks_internal.h"
+#include "ks_tc.cuh"
 
 using ksb_host::set_error;
 
@@ -226,7 +225,19 @@ struct CellFwd {
     float* h_out2;          // optional second copy (next GEMM operand), masked by mr
     long long ldh2;
     const float* mr;        // [M][H] or null
+    __half* q_hi;           // optional F16X3 planes of h_out2 (row stride ldq), scale from *qamax
+    __half* q_lo;
+    long long ldq;
+    const int* qamax;
 };
+
+// one value into F16X3 planes (the k_split_planes rounding: hi = rn(x 2^e), lo = rn(x 2^e - hi))
+__device__ __forceinline__ void store_planes(float v, float sc, __half* hi, __half* lo, long long i) {
+    const float x = v * sc;
+    const __half h = __float2half_rn(x);
+    hi[i] = h;
+    lo[i] = __float2half_rn(x - __half2float(h));
+}
 
 __global__ void k_cell_fwd(CellFwd a) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -254,7 +265,11 @@ __global__ void k_cell_fwd(CellFwd a) {
     Zr[3 * H + j] = g;
     a.c_out[(long long)r * H + j] = c;
     a.h_out[(long long)r * a.ldh + j] = h;
-    if (a.h_out2) a.h_out2[(long long)r * a.ldh2 + j] = a.mr ? h * a.mr[(long long)r * H + j] : h;
+    if (a.h_out2) {
+        const float h2 = a.mr ? h * a.mr[(long long)r * H + j] : h;
+        a.h_out2[(long long)r * a.ldh2 + j] = h2;
+        if (a.q_hi) store_planes(h2, exp2f((float)ksb::f16_scale_exp(*a.qamax)), a.q_hi, a.q_lo, (long long)r * a.ldq + j);
+    }
 }
 
 // Fused LSTM cell backward: dh = dh1 + dh2 (* mask2); writes dZ (pre-activation
@@ -341,6 +356,10 @@ struct AttnFwd {
     int n_in;
     float* X;            // [M][ldx], ctx written at columns 0..na2
     long long ldx;
+    __half* x_hi;        // optional F16X3 planes of X (row stride ldxq), scale from *qamax
+    __half* x_lo;
+    long long ldxq;
+    const int* qamax;
     float* alpha;        // [M][7]
     float* hid;          // [M][7][nd]
 };
@@ -385,10 +404,13 @@ __global__ void k_attn_fwd(AttnFwd a) {
         if (lane == 0) a.alpha[r * kTin + t] = e[t];
     }
     const float* Ar = a.A + r * kTin * a.na2;
+    const float qsc = a.x_hi ? exp2f((float)ksb::f16_scale_exp(*a.qamax)) : 0.0f;
     for (int j = lane; j < a.na2; j += 32) {
         float c = 0.0f;
         for (int t = 0; t < kTin; ++t) c += e[t] * Ar[t * a.na2 + j];
-        a.X[r * a.ldx + j] = a.mi ? c * a.mi[r * a.n_in + j] : c;
+        const float x = a.mi ? c * a.mi[r * a.n_in + j] : c;
+        a.X[r * a.ldx + j] = x;
+        if (a.x_hi) store_planes(x, qsc, a.x_hi, a.x_lo, r * a.ldxq + j);
     }
 }
 
@@ -637,85 +659,12 @@ __global__ void k_colsum_final(const double* part, int N, int chunks, float* out
     out[n] = accumulate ? out[n] + (float)t : (float)t;
 }
 
-// 3xTF32 operand split: x = big + small with both parts tf32-exact (round to
-// nearest, 10-bit mantissa); big.big + big.small + small.big recovers an
-// fp32-grade product on the TF32 tensor cores (the dropped small.small term is
-// ~2^-22 relative).
-__device__ __forceinline__ float tf32_rna(float x) {
-    unsigned u;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
-    return __uint_as_float(u);
-}
-// 3xTF32 as ONE GEMM over a tripled reduction: A' = [small(A) | big(A) | big(A)]
-// and B' = [big(B) ; small(B) ; big(B)] (stacked along K) give
-// A'.B' = small.big + big.small + big.big in a single cuBLASLt call (one C
-// read/write instead of three, 3x longer K per launch).  `stack` = 0: the three
-// parts side by side in each row (out rows x 3cols); 1: stacked (3rows x cols).
-// Part i is small(x) when bit i of small_mask is set, big(x) otherwise.
-__global__ void k_split_cat(const float* src, long long rows, int cols, long long ld, float* out, int stack,
-                            int small_mask, bool vec) {
-    const int cw = vec ? cols / 4 : cols;
-    for (long long r = blockIdx.y; r < rows; r += gridDim.y) {
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cw; c += gridDim.x * blockDim.x) {
-            if (vec) {
-                const float4 x = reinterpret_cast<const float4*>(src + r * ld)[c];
-                float4 b, sm;
-                b.x = tf32_rna(x.x); b.y = tf32_rna(x.y); b.z = tf32_rna(x.z); b.w = tf32_rna(x.w);
-                sm.x = tf32_rna(x.x - b.x); sm.y = tf32_rna(x.y - b.y); sm.z = tf32_rna(x.z - b.z); sm.w = tf32_rna(x.w - b.w);
-#pragma unroll
-                for (int part = 0; part < 3; ++part) {
-                    float* dst = stack ? out + ((long long)part * rows + r) * cols : out + r * 3LL * cols + (long long)part * cols;
-                    reinterpret_cast<float4*>(dst)[c] = ((small_mask >> part) & 1) ? sm : b;
-                }
-            } else {
-                const float x = src[r * ld + c];
-                const float b = tf32_rna(x), sm = tf32_rna(x - b);
-#pragma unroll
-                for (int part = 0; part < 3; ++part) {
-                    float* dst = stack ? out + ((long long)part * rows + r) * cols : out + r * 3LL * cols + (long long)part * cols;
-                    dst[c] = ((small_mask >> part) & 1) ? sm : b;
-                }
-            }
-        }
-    }
-}
-
-// Transposed variant for A^T: out (cols x 3rows), row c = [small | big | big] of column c.
-__global__ void k_split_cat_t(const float* src, long long rows, long long cols, long long ld, float* out) {
-    __shared__ float tile[32][33];
-    const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const long long r = r0 + i, c = c0 + threadIdx.x;
-        tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * ld + c] : 0.0f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const long long c = c0 + i, r = r0 + threadIdx.x;
-        if (c < cols && r < rows) {
-            const float x = tile[threadIdx.x][i];
-            const float b = tf32_rna(x);
-            float* row = out + c * 3 * rows;
-            row[r] = tf32_rna(x - b);
-            row[rows + r] = b;
-            row[2 * rows + r] = b;
-        }
-    }
-}
-
-// F16X3 operand split with a per-operand power-of-two scale 2^e:
-// x 2^e = hi + lo with hi, lo fp16 (~22-bit operands, like the decode GEMM's
-// F16X3).  e is chosen from the operand's max |x| so that |x| 2^e < 2^14 (no
-// fp16 overflow in either part, products and K-sums far inside fp32); entries
-// above 2^-28 max|x| keep full relative precision.  hi.hi + hi.lo + lo.hi (one
-// fp16 GEMM over the tripled K, fp32 accumulation) times 2^-(eA+eB) recovers an
-// fp32-grade product at the fp16 tensor-core rate (2.4x the TF32 rate here).
-__device__ __forceinline__ int f16_scale_exp(int amax_bits) {
-    const float m = __int_as_float(amax_bits);
-    if (!(m > 0.0f) || !isfinite(m)) return 0;
-    int e;
-    frexpf(m, &e);  // m < 2^e
-    return max(-100, min(100, 14 - e));
-}
+// F16X3 operand split (ksb::f16_scale_exp, ks_tc.cuh): x 2^e = hi + lo with hi,
+// lo fp16 (~22-bit operands, like the decode GEMM's F16X3); e from the operand's
+// max |x| so that |x| 2^e < 2^14; entries above 2^-28 max|x| keep full relative
+// precision.  hi.hi + hi.lo + lo.hi (the tcgen05 GEMM, ks_gemm16.cu) times
+// 2^-(eA+eB) recovers an fp32-grade product at the fp16 tensor-core rate.
+using ksb::f16_scale_exp;
 // max |x| of a row-major block into *out (pre-zeroed; non-negative floats order as ints)
 __global__ void __launch_bounds__(256) k_absmax(const float* src, long long rows, long long cols, long long ld, int* out) {
     __shared__ float wm[8];
@@ -740,75 +689,36 @@ __device__ __forceinline__ void split_f16x2s(float x, float y, float sc, __half2
     const float2 h = __half22float2(hi);
     lo = __float22half2_rn(__fadd2_rn(v, make_float2(-h.x, -h.y)));
 }
-// The F16X3 analogue of k_split_cat: part i of each row (stack 0: side by side,
-// row stride ldo) or block (stack 1: stacked along K, row stride ldo) is lo(x)
-// when bit i of lo_mask is set, hi(x) otherwise.
-// alpha (optional): the GEMM's unscale 2^-(e + e_other), written by one thread
-__global__ void k_split16(const float* src, long long rows, int cols, long long ld, __half* out, long long ldo,
-                          int stack, int lo_mask, const int* amax, const int* amax_other, float* alpha) {
+// hi / lo planes of a row-major block, same layout (row stride ldo), 4 columns per
+// thread when aligned; flat grid-stride over (row, column group)
+__global__ void k_split_planes(const float* src, long long rows, int cols, long long ld, __half* hi, __half* lo,
+                               long long ldo, const int* amax) {
     const float sc = exp2f((float)f16_scale_exp(*amax));
-    if (alpha && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-        *alpha = exp2f(-(float)(f16_scale_exp(*amax) + f16_scale_exp(*amax_other)));
-    // 4 columns per thread (16-byte loads, 8-byte stores) when the layout allows it
     const bool vec = (cols & 3) == 0 && (ld & 3) == 0 && (ldo & 3) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hi) |
+                       reinterpret_cast<uintptr_t>(lo)) & 15) == 0;
     const int cw = vec ? cols >> 2 : cols;
-    // flat grid-stride over (row, column group): narrow rows do not idle most threads
     const long long n = rows * (long long)cw;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long r = i / cw;
         const int c = (int)(i - r * cw);
-        {
-            if (vec) {
-                const float4 x = reinterpret_cast<const float4*>(src + r * ld)[c];
-                __half2 h01, l01, h23, l23;
-                split_f16x2s(x.x, x.y, sc, h01, l01);
-                split_f16x2s(x.z, x.w, sc, h23, l23);
-                uint2 hv, lv;
-                hv.x = *reinterpret_cast<uint32_t*>(&h01);
-                hv.y = *reinterpret_cast<uint32_t*>(&h23);
-                lv.x = *reinterpret_cast<uint32_t*>(&l01);
-                lv.y = *reinterpret_cast<uint32_t*>(&l23);
-#pragma unroll
-                for (int part = 0; part < 3; ++part) {
-                    __half* dst = stack ? out + ((long long)part * rows + r) * ldo : out + r * ldo + (long long)part * cols;
-                    reinterpret_cast<uint2*>(dst)[c] = ((lo_mask >> part) & 1) ? lv : hv;
-                }
-            } else {
-                const float x = src[r * ld + c] * sc;
-                const __half hi = __float2half_rn(x);
-                const __half lo = __float2half_rn(x - __half2float(hi));
-#pragma unroll
-                for (int part = 0; part < 3; ++part) {
-                    __half* dst = stack ? out + ((long long)part * rows + r) * ldo : out + r * ldo + (long long)part * cols;
-                    dst[c] = ((lo_mask >> part) & 1) ? lo : hi;
-                }
-            }
-        }
-    }
-}
-// Transposed: out (cols x 3 rows, row stride ldo), row c = [lo | hi | hi] of column c.
-__global__ void k_split16_t(const float* src, long long rows, long long cols, long long ld, __half* out, long long ldo,
-                            const int* amax, const int* amax_other, float* alpha) {
-    __shared__ float tile[32][33];
-    const float sc = exp2f((float)f16_scale_exp(*amax));
-    if (alpha && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
-        *alpha = exp2f(-(float)(f16_scale_exp(*amax) + f16_scale_exp(*amax_other)));
-    const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const long long r = r0 + i, c = c0 + threadIdx.x;
-        tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * ld + c] : 0.0f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const long long c = c0 + i, r = r0 + threadIdx.x;
-        if (c < cols && r < rows) {
-            const float x = tile[threadIdx.x][i] * sc;
-            const __half hi = __float2half_rn(x);
-            __half* row = out + c * ldo;
-            row[r] = __float2half_rn(x - __half2float(hi));
-            row[rows + r] = hi;
-            row[2 * rows + r] = hi;
+        if (vec) {
+            const float4 x = reinterpret_cast<const float4*>(src + r * ld)[c];
+            __half2 h01, l01, h23, l23;
+            split_f16x2s(x.x, x.y, sc, h01, l01);
+            split_f16x2s(x.z, x.w, sc, h23, l23);
+            uint2 hv, lv;
+            hv.x = *reinterpret_cast<uint32_t*>(&h01);
+            hv.y = *reinterpret_cast<uint32_t*>(&h23);
+            lv.x = *reinterpret_cast<uint32_t*>(&l01);
+            lv.y = *reinterpret_cast<uint32_t*>(&l23);
+            reinterpret_cast<uint2*>(hi + r * ldo)[c] = hv;
+            reinterpret_cast<uint2*>(lo + r * ldo)[c] = lv;
+        } else {
+            const float x = src[r * ld + c] * sc;
+            const __half h = __float2half_rn(x);
+            hi[r * ldo + c] = h;
+            lo[r * ldo + c] = __float2half_rn(x - __half2float(h));
         }
     }
 }
@@ -931,24 +841,6 @@ struct TLstm {
     long long size() const { return (long long)(Kd() + S + 1) * 4 * H; }
 };
 
-// cuBLASLt plan of one GEMM shape (descriptors + chosen algorithm)
-struct LtKey {
-    bool tb;
-    long long M, N, K, lda, ldb, ldc;
-    uint32_t aa, ab, ac;
-    bool f16 = false;  // F16X3 operands (fp16, device-pointer alpha/beta) vs 3xTF32
-    bool operator<(const LtKey& o) const {
-        return std::tie(tb, M, N, K, lda, ldb, ldc, aa, ab, ac, f16) <
-               std::tie(o.tb, o.M, o.N, o.K, o.lda, o.ldb, o.ldc, o.aa, o.ab, o.ac, o.f16);
-    }
-};
-struct LtPlan {
-    cublasLtMatmulDesc_t op = nullptr;
-    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-    cublasLtMatmulAlgo_t algo{};
-    bool usable = false;
-};
-
 struct RefSeg {
     std::string name;
     long long numel;
@@ -982,16 +874,17 @@ struct ks_trainer {
     long long nref = 0;           // reference parameter count (export / import order)
     DBuf params, adam_m, adam_v;
     long long adam_step = 0;
-    cublasHandle_t blas = nullptr;
+    cudaStream_t cur = nullptr;    // stream of the running batch (the GEMMs launch on it)
+    int sms = 148;
     int cap_M = 0;
     // workspaces
     DBuf tok, tgt, idx, mi, mr, enc_slot, dec_slot, dec_val, enc_sm[2], dec_sm;
     DBuf Hx[2], Ce[2], Ze[2], dZe[2], A, U;
     DBuf Xd, Hs, Cd, Zd, dZd, alpha, hid, dlog, DHh, lossr, match;
+    DBuf Xd16, Hx16[2];            // F16X3 planes of Xd / Hx written by their producers (hi, then lo)
     DBuf dXd, dH, dC, dA, Dctx, DPs, DPa, rowacc, dHe, dCe, part, norm, grads_tmp;
     DBuf res;                      // {loss sum, matches} of the last step / evaluate
-    bool tf32x3 = true;            // GEMM arithmetic on the tensor cores (else fp32 SIMT SGEMM) ...
-    bool f16x3 = true;             // ... as F16X3 with per-operand scales (default) or 3xTF32
+    bool f16x3 = true;             // GEMMs as F16X3 on tcgen05 (default), else fp32 SIMT (KS_TRAIN_GEMM=fp32)
     DBuf scal;                     // F16X3: per-step max|x| slots and GEMM alphas; [2] = {0, 1} betas
     int scal_used = 0;
     int act_bound_bits = 0;        // the activation bound's float bits, written to its slot
@@ -1009,14 +902,18 @@ struct ks_trainer {
         long long launches = 0;
     };
     std::vector<GraphEntry> graphs;
-    std::map<std::pair<const float*, bool>, int> wslot;  // cached weight split -> its max|x| slot
-    DBuf sp[4];                    // split scratch: A big/small, B big/small
-    DBuf blas_ws;                  // cuBLAS / cuBLASLt workspace
-    cublasLtHandle_t lt = nullptr;
-    std::map<LtKey, LtPlan> lt_plans;
-    std::map<std::pair<const float*, bool>, std::pair<DBuf*, long long>> wsplit;  // per-call weight splits
-    std::vector<std::unique_ptr<DBuf[]>> wsplit_store;  // pool, reused call after call
-    size_t wsplit_used = 0;
+    DBuf gpart, spart;             // split-K partials of the tensor-core / SIMT GEMMs
+    // F16X3 operand planes of this batch: (source, rows, cols, ld) -> planes; weights and
+    // operands several GEMMs share are split once per batch
+    struct Planes {
+        const __half* hi;
+        const __half* lo;
+        long long ld;
+        const int* amax;
+    };
+    std::map<std::tuple<const float*, long long, long long, long long>, Planes> planes;
+    std::vector<std::unique_ptr<DBuf>> plane_store;  // pool, reused batch after batch in call order
+    size_t plane_used = 0;
     int n_in = 0;  // decoder input-mask width
     int vmax = 1;  // largest vocabulary (stride of the per-position dlogits blocks)
     long long launches = 0;
@@ -1030,315 +927,105 @@ namespace {
         if (err_ != cudaSuccess)                                                                   \
             return set_error(KS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(err_));   \
     } while (0)
-#define KT_BLAS(call)                                                                              \
-    do {                                                                                           \
-        cublasStatus_t s_ = (call);                                                                \
-        if (s_ != CUBLAS_STATUS_SUCCESS)                                                           \
-            return set_error(KS_ERR_CUDA, std::string("cuBLAS ") + #call + " status " + std::to_string((int)s_)); \
-    } while (0)
 
-ks_status gemm_one(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
-                   long long lda, const float* B, long long ldb, float beta, float* C, long long ldc,
-                   cublasComputeType_t ct) {
-    const float one = 1.0f;
-    KT_BLAS(cublasGemmEx(t.blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N, (int)M,
-                         (int)K, &one, B, CUDA_R_32F, (int)ldb, A, CUDA_R_32F, (int)lda, &beta, C, CUDA_R_32F,
-                         (int)ldc, ct, CUBLAS_GEMM_DEFAULT));
-    ++t.launches;
+// fp32 SIMT GEMM (ks_gemm16.cu): exact fp32 FMAs, any transposes
+ks_status gemm_simt(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
+                    long long lda, const float* B, long long ldb, float beta, float* C, long long ldc) {
+    const int sp = ksb::sgemm_splits((int)M, (int)N, K, t.sms, ta);
+    float* part = nullptr;
+    if (sp > 1) {
+        KT_CUDA(t.spart.ensure((size_t)sp * M * N * 4));
+        part = t.spart.as<float>();
+    }
+    int n = 0;
+    if (!ksb::launch_sgemm(ta, tb, (int)M, (int)N, K, A, lda, B, ldb, beta, C, ldc, part, t.sms, t.cur, &n))
+        return set_error(KS_ERR_CUDA, "SIMT GEMM launch failed");
+    t.launches += n;
     return KS_OK;
 }
 
-// TF32 pass through cuBLASLt: for the long weight-gradient reductions the plain
-// cublasGemmEx heuristic picks legacy sm80 TF32 kernels, cuBLASLt's picks the
-// sm100 ones (7.5 vs 9.8 ms per training step).  (Restricting the heuristic to
-// CUBLASLT_REDUCTION_SCHEME_NONE returned algorithms that produced wrong sums.)
-// Row-major C[M x N] = op(A) op(B) + beta C with A, B dense (A M x K, B as stored).
-ks_status gemm_lt(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long N, long long K, const float* A,
-                  long long lda, const float* B, long long ldb, float beta, float* C, long long ldc) {
-    auto align = [](const void* ptr) {
-        uint32_t a = 256;
-        while (a > 4 && (reinterpret_cast<uintptr_t>(ptr) % a) != 0) a >>= 1;
-        return a;
-    };
-    const uint32_t aa = align(B), ab = align(A), ac = align(C);
-    const LtKey key{tb, M, N, K, lda, ldb, ldc, aa, ab, ac};
-    auto it = t.lt_plans.find(key);
-    if (it == t.lt_plans.end()) {
-        // one plan per shape: descriptors + the heuristic's algorithm, built once
-        // (the heuristic query costs tens of microseconds of host time per call)
-        LtPlan pl;
-        cublasLtMatmulPreference_t pref = nullptr;
-        // column-major view: C^T (N x M) = op(B)^T (N x K) . A^T (K x M)
-        const cublasOperation_t tbo = tb ? CUBLAS_OP_T : CUBLAS_OP_N, tao = CUBLAS_OP_N;
-        const size_t wsz = t.blas_ws.bytes;
-        cublasLtMatmulHeuristicResult_t heur{};
-        int nres = 0;
-        bool ok = cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32F_FAST_TF32, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &tbo, sizeof tbo) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tao, sizeof tao) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatrixLayoutCreate(&pl.la, CUDA_R_32F, tb ? K : N, tb ? N : K, ldb) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatrixLayoutCreate(&pl.lb, CUDA_R_32F, K, M, lda) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatrixLayoutCreate(&pl.lc, CUDA_R_32F, N, M, ldc) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz) ==
-                      CUBLAS_STATUS_SUCCESS;
-        if (ok) {
-            // the output may start anywhere in the flat gradient buffer: tell the heuristic
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_A_BYTES, &aa, sizeof aa);
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_B_BYTES, &ab, sizeof ab);
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_C_BYTES, &ac, sizeof ac);
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &ac, sizeof ac);
-            ok = cublasLtMatmulAlgoGetHeuristic(t.lt, pl.op, pl.la, pl.lb, pl.lc, pl.lc, pref, 1, &heur, &nres) ==
-                     CUBLAS_STATUS_SUCCESS &&
-                 nres >= 1 && heur.state == CUBLAS_STATUS_SUCCESS;
-        }
-        if (pref) cublasLtMatmulPreferenceDestroy(pref);
-        pl.usable = ok;  // no cuBLASLt algorithm for this shape: cublasGemmEx below
-        if (ok) pl.algo = heur.algo;
-        it = t.lt_plans.emplace(key, pl).first;
-    }
-    const LtPlan& pl = it->second;
-    if (pl.usable) {
-        const float one = 1.0f;
-        const cublasStatus_t e = cublasLtMatmul(t.lt, pl.op, &one, B, pl.la, A, pl.lb, &beta, C, pl.lc, C, pl.lc,
-                                                &pl.algo, t.blas_ws.p, t.blas_ws.bytes, s);
-        if (e == CUBLAS_STATUS_SUCCESS) {
-            ++t.launches;
-            return KS_OK;
-        }
-        if (e != CUBLAS_STATUS_NOT_SUPPORTED)
-            return set_error(KS_ERR_CUDA, "cuBLASLt TF32 GEMM status " + std::to_string((int)e));
-    }
-    return gemm_one(t, false, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_FAST_TF32);
-}
 
-// F16X3 pass through cuBLASLt: fp16 operands, fp32 accumulation and output,
-// alpha (the 2^-(eA+eB) unscale) and beta read from device memory.
-constexpr int kScalSlots = 4096;
+constexpr int kScalSlots = 4096;  // F16X3 per-step max|x| / alpha slots
 inline unsigned split16_grid(long long rows, long long cols) {
     const long long items = rows * ((cols + 3) / 4);
     return (unsigned)std::max<long long>(1, std::min<long long>((items + 255) / 256, 148LL * 16));
 }
-ks_status gemm_lt16(ks_trainer& t, cudaStream_t s, bool tb, long long M, long long N, long long K, const __half* A,
-                    long long lda, const __half* B, long long ldb, const float* alpha, const float* beta, float* C,
-                    long long ldc) {
-    auto align = [](const void* ptr) {
-        uint32_t a = 256;
-        while (a > 2 && (reinterpret_cast<uintptr_t>(ptr) % a) != 0) a >>= 1;
-        return a;
-    };
-    const uint32_t aa = align(B), ab = align(A), ac = align(C);
-    LtKey key{tb, M, N, K, lda, ldb, ldc, aa, ab, ac};
-    key.f16 = true;
-    auto it = t.lt_plans.find(key);
-    if (it == t.lt_plans.end()) {
-        LtPlan pl;
-        cublasLtMatmulPreference_t pref = nullptr;
-        const cublasOperation_t tbo = tb ? CUBLAS_OP_T : CUBLAS_OP_N, tao = CUBLAS_OP_N;
-        const cublasLtPointerMode_t pm = CUBLASLT_POINTER_MODE_DEVICE;
-        const size_t wsz = t.blas_ws.bytes;
-        cublasLtMatmulHeuristicResult_t heur{};
-        int nres = 0;
-        bool ok = cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32F, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &tbo, sizeof tbo) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tao, sizeof tao) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_POINTER_MODE, &pm, sizeof pm) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatrixLayoutCreate(&pl.la, CUDA_R_16F, tb ? K : N, tb ? N : K, ldb) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatrixLayoutCreate(&pl.lb, CUDA_R_16F, K, M, lda) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatrixLayoutCreate(&pl.lc, CUDA_R_32F, N, M, ldc) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS &&
-                  cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz, sizeof wsz) ==
-                      CUBLAS_STATUS_SUCCESS;
-        if (ok) {
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_A_BYTES, &aa, sizeof aa);
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_B_BYTES, &ab, sizeof ab);
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_C_BYTES, &ac, sizeof ac);
-            cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MIN_ALIGNMENT_D_BYTES, &ac, sizeof ac);
-            ok = cublasLtMatmulAlgoGetHeuristic(t.lt, pl.op, pl.la, pl.lb, pl.lc, pl.lc, pref, 1, &heur, &nres) ==
-                     CUBLAS_STATUS_SUCCESS &&
-                 nres >= 1 && heur.state == CUBLAS_STATUS_SUCCESS;
-        }
-        if (pref) cublasLtMatmulPreferenceDestroy(pref);
-        pl.usable = ok;
-        if (ok) pl.algo = heur.algo;
-        it = t.lt_plans.emplace(key, pl).first;
-    }
-    const LtPlan& pl = it->second;
-    if (!pl.usable) {
-        // no cuBLASLt algorithm for this shape (odd M such as S + 1 or d_in + 1):
-        // the same tripled-K fp16 product through cublasGemmEx (fp32 compute),
-        // alpha / beta read from device memory like the cuBLASLt path
-        KT_BLAS(cublasSetStream(t.blas, s));
-        KT_BLAS(cublasSetPointerMode(t.blas, CUBLAS_POINTER_MODE_DEVICE));
-        const cublasStatus_t ge =
-            cublasGemmEx(t.blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_OP_N, (int)N, (int)M, (int)K, alpha, B,
-                         CUDA_R_16F, (int)ldb, A, CUDA_R_16F, (int)lda, beta, C, CUDA_R_32F, (int)ldc,
-                         CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-        cublasSetPointerMode(t.blas, CUBLAS_POINTER_MODE_HOST);
-        if (ge != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cublasGemmEx F16X3 fallback status " + std::to_string((int)ge));
-        ++t.launches;
-        return KS_OK;
-    }
-    const cublasStatus_t e = cublasLtMatmul(t.lt, pl.op, alpha, B, pl.la, A, pl.lb, beta, C, pl.lc, C, pl.lc, &pl.algo,
-                                            t.blas_ws.p, t.blas_ws.bytes, s);
-    if (e != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cuBLASLt F16X3 GEMM status " + std::to_string((int)e));
-    ++t.launches;
-    return KS_OK;
-}
 
-void launch_split_cat(ks_trainer& t, cudaStream_t s, const float* src, long long rows, long long cols, long long ld,
-                      float* out, int stack, int small_mask) {
-    const bool vec = cols % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
-                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    const long long cw = vec ? cols / 4 : cols;
-    dim3 grid((unsigned)std::min<long long>((cw + 255) / 256, 64), (unsigned)std::min<long long>(rows, 65535));
-    k_split_cat<<<grid, 256, 0, s>>>(src, rows, (int)cols, ld, out, stack, small_mask, vec);
-    ++t.launches;
-}
-
-// Row-major C[M x N] = op(A) op(B) + beta C, on cuBLAS (column-major).  3xTF32
-// mode: both operands split (weights once per call, cached by pointer and
-// layout) into the concatenated-K form of k_split_cat, one TF32 tensor-core
-// GEMM with fp32 accumulation; fp32 mode: one SGEMM (PEDANTIC, no TF32).
-// a_amax / b_amax (F16X3 only): device slots already holding max |A| / |B| (a
-// bound: activations are tanh outputs times dropout scales; dZ maxima come fused
-// from k_cell_bwd), so no max-reduction pass over that operand is needed.
+// Row-major C[M x N] = op(A) op(B) + beta C on the trainer's stream.
+// F16X3 (default): both operands split into fp16 hi/lo planes at power-of-two
+// scales, in their own row-major layout (no transposes: the tcgen05 GEMM,
+// ks_gemm16.cu, reads each operand K-major or MN-major), three MMA passes with
+// fp32 accumulation, alpha = 2^-(eA+eB).  Weights (and operands two GEMMs of a
+// step share, b_cache) are split once per batch: W serves the forward and dX.  a_amax / b_amax: device slots already
+// holding max |A| / |B| (activations are tanh outputs times dropout scales; dZ
+// maxima come fused from k_cell_bwd), so no max-reduction pass is needed.
+// Narrow shapes (an output side under 16 / 128 columns: heads, attention) and
+// KS_TRAIN_GEMM=fp32 run the fp32 SIMT GEMM.
 ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, long long K, const float* A,
                   long long lda, const float* B, long long ldb, float beta, float* C, long long ldc,
                   bool b_is_weight = false, const int* a_amax = nullptr, const int* b_amax = nullptr,
-                  bool b_cache = false) {
+                  bool b_cache = false, const ks_trainer::Planes* apl = nullptr) {
     if (M == 0 || N == 0) return KS_OK;
     if (K == 0) return beta == 1.0f ? KS_OK : set_error(KS_ERR_SHAPE, "empty GEMM reduction");
-    // narrow outputs (heads, attention, and slot rows unless their B split is shared
-    // with the dense weight gradient, F16X3) stay fp32 SGEMMs
-    const bool narrow = (t.f16x3 && b_cache) ? (std::max(M, N) < 128 || std::min(M, N) < 16) : (M < 128 || N < 128);
-    if (!t.tf32x3 || narrow)
-        return gemm_one(t, ta, tb, M, N, K, A, lda, B, ldb, beta, C, ldc, CUBLAS_COMPUTE_32F_PEDANTIC);
+    const bool narrow = b_cache ? (std::max(M, N) < 128 || std::min(M, N) < 16) : (M < 128 || N < 128);
+    if (!t.f16x3 || narrow) return gemm_simt(t, ta, tb, M, N, K, A, lda, B, ldb, beta, C, ldc);
+    if (beta != 0.0f && beta != 1.0f) return set_error(KS_ERR_PARAMETER, "F16X3 GEMM beta must be 0 or 1");
 
-    cudaStream_t s;
-    KT_BLAS(cublasGetStream(t.blas, &s));
-    ks_status st;
-    const long long K3 = 3 * K;
-    if (t.f16x3) {
-        auto r8 = [](long long x) { return (x + 7) / 8 * 8; };  // 16-byte fp16 row strides
-        auto absmax = [&](const float* src, long long rows, long long cols, long long ld, int* out) {
+    cudaStream_t s = t.cur;
+    int* slots = t.scal.as<int>();
+    // hi / lo planes of a row-major [rows x cols] fp32 block (row stride ld), scale from
+    // `amax` (a device slot already holding max|x|) or from a fresh max-reduction
+    auto planes = [&](const float* src, long long rows, long long cols, long long ld, const int* amax, bool share,
+                      ks_trainer::Planes& out) -> ks_status {
+        const auto key = std::make_tuple(src, rows, cols, ld);
+        if (share) {
+            auto it = t.planes.find(key);
+            if (it != t.planes.end()) {
+                out = it->second;
+                return KS_OK;
+            }
+        }
+        if (!amax) {
+            if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
+            int* slot = slots + t.scal_used++;
             const unsigned gx = (unsigned)std::min<long long>((cols + 255) / 256, 8);
             dim3 grid(gx, (unsigned)std::min<long long>(rows, std::max<long long>(1, 1184 / gx)));
-            k_absmax<<<grid, 256, 0, s>>>(src, rows, cols, ld, out);
+            k_absmax<<<grid, 256, 0, s>>>(src, rows, cols, ld, slot);
             ++t.launches;
-        };
-        if (t.scal_used + 3 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
-        int* slots = t.scal.as<int>();
-        const int salpha = t.scal_used++;
-        int sa = -1;
-        if (!a_amax) sa = t.scal_used++;
-        const int* amaxA = a_amax ? a_amax : slots + sa;
-        // B' = [hi ; hi ; lo] along K: stacked (3K x N, row stride ldb3) or side by side (tb: N x 3K)
-        const long long br = tb ? N : K, bc = tb ? K : N;
-        const long long ldb3 = tb ? r8(K3) : r8(N);
-        const size_t bbytes = (size_t)(tb ? N : K3) * ldb3 * 2;
-        auto split_b = [&](DBuf& dst, const int* amax, int slot) -> ks_status {
-            KT_CUDA(dst.ensure(bbytes));
-            if (!amax) absmax(B, br, bc, ldb, slots + slot);
-            k_split16<<<split16_grid(br, bc), 256, 0, s>>>(B, br, (int)bc, ldb, dst.as<__half>(), ldb3, tb ? 0 : 1, 0b100,
-                                           amax ? amax : slots + slot, nullptr, nullptr);
-            ++t.launches;
-            return KS_OK;
-        };
-        const __half* b16;
-        const int* amaxB;
-        if (b_is_weight || b_cache) {
-            // weights, and operands two GEMMs of this step share (b_cache: the dZ of every
-            // step, B of both the dense and the slot-row weight gradients), split once
-            const std::pair<const float*, bool> key(B, tb);
-            auto it = t.wsplit.find(key);
-            if (it == t.wsplit.end()) {
-                if (t.wsplit_used == t.wsplit_store.size()) t.wsplit_store.emplace_back(new DBuf[2]);
-                DBuf* buf = t.wsplit_store[t.wsplit_used++].get();
-                int slot;
-                if (b_amax) {
-                    slot = (int)(b_amax - slots);
-                } else {
-                    if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
-                    slot = t.scal_used++;
-                }
-                if ((st = split_b(buf[0], b_amax, slot))) return st;
-                it = t.wsplit.emplace(key, std::make_pair(buf, bc)).first;
-                t.wslot[key] = slot;
-            }
-            b16 = it->second.first[0].as<__half>();
-            amaxB = slots + t.wslot[key];
-        } else {
-            int sb = -1;
-            if (!b_amax) {
-                if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
-                sb = t.scal_used++;
-            }
-            if ((st = split_b(t.sp[2], b_amax, sb))) return st;
-            b16 = t.sp[2].as<__half>();
-            amaxB = b_amax ? b_amax : slots + sb;
+            amax = slot;
         }
-        // A' = [lo | hi | hi] (M x 3K, row stride lda3); its split also writes the GEMM's alpha
-        float* alpha = reinterpret_cast<float*>(slots + salpha);
-        const long long lda3 = r8(K3);
-        KT_CUDA(t.sp[0].ensure((size_t)M * lda3 * 2));
-        __half* a16 = t.sp[0].as<__half>();
-        if (!a_amax) absmax(A, ta ? K : M, ta ? M : K, lda, slots + sa);
-        if (ta) {
-            dim3 grid((unsigned)((M + 31) / 32), (unsigned)((K + 31) / 32));
-            if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
-            k_split16_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, a16, lda3, amaxA, amaxB, alpha);
-        } else {
-            k_split16<<<split16_grid(M, K), 256, 0, s>>>(A, M, (int)K, lda, a16, lda3, 0, 0b001, amaxA, amaxB, alpha);
-        }
+        const long long ldo = (cols + 7) / 8 * 8;  // 16-byte rows (TMA)
+        if (t.plane_used == t.plane_store.size()) t.plane_store.emplace_back(new DBuf());
+        DBuf& buf = *t.plane_store[t.plane_used++];
+        KT_CUDA(buf.ensure((size_t)rows * ldo * 2 * 2));
+        __half* hi = buf.as<__half>();
+        __half* lo = hi + rows * ldo;
+        k_split_planes<<<split16_grid(rows, cols), 256, 0, s>>>(src, rows, (int)cols, ld, hi, lo, ldo, amax);
         ++t.launches;
-        const float* betap = reinterpret_cast<const float*>(slots + kScalSlots) + (beta == 0.0f ? 0 : 1);
-        if (beta != 0.0f && beta != 1.0f) return set_error(KS_ERR_PARAMETER, "F16X3 GEMM beta must be 0 or 1");
-        return gemm_lt16(t, s, tb, M, N, K3, a16, lda3, b16, ldb3, alpha, betap, C, ldc);
-    }
-    // A' = [small | big | big] (M x 3K; a transposed A is transposed while splitting)
-    KT_CUDA(t.sp[0].ensure((size_t)M * K3 * 4));
-    if (ta) {
-        dim3 grid((unsigned)((M + 31) / 32), (unsigned)((K + 31) / 32));
-        if (grid.y > 65535) return set_error(KS_ERR_UNSUPPORTED, "transposed split too tall");
-        k_split_cat_t<<<grid, dim3(32, 8), 0, s>>>(A, K, M, lda, t.sp[0].as<float>());
-        ++t.launches;
-    } else {
-        launch_split_cat(t, s, A, M, K, lda, t.sp[0].as<float>(), 0, 0b001);
-    }
-    // B' = [big ; small ; big] along K: stacked rows (K x N) or side by side (tb: N x K)
-    const float* Bc;
-    const long long br = tb ? N : K, bc = tb ? K : N;
-    const size_t bbytes = (size_t)br * bc * 3 * 4;
-    auto split_b = [&](DBuf& dst) -> ks_status {
-        KT_CUDA(dst.ensure(bbytes));
-        launch_split_cat(t, s, B, br, bc, ldb, dst.as<float>(), tb ? 0 : 1, 0b010);
+        out = {hi, lo, ldo, amax};
+        if (share) t.planes.emplace(key, out);
         return KS_OK;
     };
-    if (b_is_weight) {
-        // cached per (weight, layout): the forward uses W stacked along K, the dX GEMMs
-        // W^T side by side
-        const std::pair<const float*, bool> key(B, tb);
-        auto it = t.wsplit.find(key);
-        if (it == t.wsplit.end()) {
-            if (t.wsplit_used == t.wsplit_store.size()) t.wsplit_store.emplace_back(new DBuf[2]);
-            DBuf* buf = t.wsplit_store[t.wsplit_used++].get();
-            if ((st = split_b(buf[0]))) return st;
-            it = t.wsplit.emplace(key, std::make_pair(buf, bc)).first;
-        }
-        Bc = it->second.first[0].as<float>();
-    } else {
-        if ((st = split_b(t.sp[2]))) return st;
-        Bc = t.sp[2].as<float>();
+    ks_status st;
+    ks_trainer::Planes pa{}, pb{};
+    // A: M x K (K-major) or, transposed, K x M (MN-major); B: K x N (MN-major) or N x K (K-major)
+    if (apl)
+        pa = *apl;  // written by the operand's producers
+    else if ((st = planes(A, ta ? K : M, ta ? M : K, lda, a_amax, false, pa)))
+        return st;
+    if ((st = planes(B, tb ? N : K, tb ? K : N, ldb, b_amax, b_is_weight || b_cache, pb))) return st;
+    const float* betap = reinterpret_cast<const float*>(slots + kScalSlots) + (beta == 0.0f ? 0 : 1);
+    ksb::GemmF16Args g{pa.hi, pa.lo, pa.ld, ta ? 1 : 0, pb.hi, pb.lo, pb.ld, tb ? 0 : 1, (int)M, (int)N, K,
+                       pa.amax, pb.amax, betap, C, ldc, nullptr, t.sms};
+    const int sp = ksb::gemm16_splits((int)M, (int)N, K, t.sms);
+    if (sp > 1) {
+        KT_CUDA(t.gpart.ensure((size_t)sp * M * N * 4));
+        g.part = t.gpart.as<float>();
     }
-    const long long ldb3 = tb ? K3 : N;
-    static const bool use_lt = [] {
-        const char* e = std::getenv("KS_TRAIN_LT");
-        return !(e && e[0] == '0');
-    }();
-    if (use_lt) return gemm_lt(t, s, tb, M, N, K3, t.sp[0].as<float>(), K3, Bc, ldb3, beta, C, ldc);
-    return gemm_one(t, false, tb, M, N, K3, t.sp[0].as<float>(), K3, Bc, ldb3, beta, C, ldc,
-                    CUBLAS_COMPUTE_32F_FAST_TF32);
+    int n = 0;
+    if (!ksb::launch_gemm16(g, s, &n)) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
+    t.launches += n;
+    return KS_OK;
 }
 
 ks_status colsum(ks_trainer& t, cudaStream_t s, const float* in, long long R, int N, long long ld, float* out,
@@ -1374,6 +1061,7 @@ ks_status ensure_ws(ks_trainer& t, int M) {
         const long long He = t.lstms[t.L_enc[d]].H;
         TE(t.enc_sm[d], 7 * m * (t.d_in + 1) * 4);
         TE(t.Hx[d], 8 * m * He * 4);
+        TE(t.Hx16[d], 2 * 8 * m * ((He + 7) / 8 * 8) * 2);
         TE(t.Ce[d], 7 * m * He * 4);
         TE(t.Ze[d], 7 * m * 4 * He * 4);
         TE(t.dZe[d], 7 * m * 4 * He * 4);
@@ -1382,6 +1070,7 @@ ks_status ensure_ws(ks_trainer& t, int M) {
         const TLstm& D = t.lstms[t.L_dec];
         const long long Hd = D.H, Kd = D.Kd();
         TE(t.Xd, T * m * Kd * 4);
+        TE(t.Xd16, 2 * T * m * ((Kd + 7) / 8 * 8) * 2);
         TE(t.Hs, (T + 1) * m * Hd * 4);
         TE(t.Cd, T * m * Hd * 4);
         TE(t.Zd, T * m * 4 * Hd * 4);
@@ -1422,10 +1111,9 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
                     double* d_loss, long long* d_match, cudaStream_t s) {
     ks_status st;
     if ((st = ensure_ws(t, M))) return st;
-    KT_BLAS(cublasSetStream(t.blas, s));
-    t.wsplit.clear();  // weights may have changed since the last call (Adam, import)
-    t.wslot.clear();
-    t.wsplit_used = 0;
+    t.cur = s;
+    t.planes.clear();  // weights may have changed since the last call (Adam, import)
+    t.plane_used = 0;
     // F16X3: fresh max|x| slots for this step's GEMMs; slot 0 bounds every activation
     // operand (LSTM outputs are tanh-bounded, times at most the dropout scale)
     int* act_amax = nullptr;
@@ -1484,16 +1172,33 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
 
     // ---------------------------------------------------------------- encoder
     const int dirs = attn ? 2 : 1;
+    // F16X3 planes of the decoder operand X, written by its producers (attention: ctx,
+    // the cells: h) at the activation bound's scale
+    const TLstm& Dl = t.lstms[t.L_dec];
+    const long long ldxq = (Dl.Kd() + 7) / 8 * 8;
+    __half* xq_hi = t.f16x3 ? t.Xd16.as<__half>() : nullptr;
+    __half* xq_lo = xq_hi ? xq_hi + (long long)T * m * ldxq : nullptr;
     for (int dir = 0; dir < dirs; ++dir) {
         const TLstm& L = t.lstms[t.L_enc[dir]];
         const int H = L.H;
         float* Hx = t.Hx[dir].as<float>();
         KT_CUDA(cudaMemsetAsync(Hx, 0, m * H * 4, s));
+        // attn encoders: F16X3 planes of Hx (the recurrent operand) written by the cells
+        const long long ldh16 = (H + 7) / 8 * 8;
+        __half* hx_hi = (t.f16x3 && attn) ? t.Hx16[dir].as<__half>() : nullptr;
+        __half* hx_lo = hx_hi ? hx_hi + 8LL * m * ldh16 : nullptr;
+        if (hx_hi) {
+            KT_CUDA(cudaMemsetAsync(hx_hi, 0, (size_t)m * ldh16 * 2, s));
+            KT_CUDA(cudaMemsetAsync(hx_lo, 0, (size_t)m * ldh16 * 2, s));
+        }
         for (int st_ = 0; st_ < kTin; ++st_) {
             const int tt = dir == 0 ? st_ : kTin - 1 - st_;
             float* Z = t.Ze[dir].as<float>() + (long long)st_ * m * 4 * H;
+            const ks_trainer::Planes hp{hx_lo ? hx_hi + (long long)st_ * m * ldh16 : nullptr,
+                                        hx_lo ? hx_lo + (long long)st_ * m * ldh16 : nullptr, ldh16, act_amax};
             if (st_ > 0 && (st = gemm_rm(t, false, false, m, 4LL * H, H, Hx + (long long)st_ * m * H, H,
-                                         P + L.wd(), 4LL * H, 0.0f, Z, 4LL * H, true, act_amax)))
+                                         P + L.wd(), 4LL * H, 0.0f, Z, 4LL * H, true, act_amax, nullptr, false,
+                                         hx_hi ? &hp : nullptr)))
                 return st;
             CellFwd c{};
             c.M = M;
@@ -1511,6 +1216,12 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
                 c.ldh = 7LL * 2 * t.n_a;
                 c.h_out2 = Hx + (long long)(st_ + 1) * m * H;
                 c.ldh2 = H;
+                if (hx_hi) {
+                    c.q_hi = hx_hi + (long long)(st_ + 1) * m * ldh16;
+                    c.q_lo = hx_lo + (long long)(st_ + 1) * m * ldh16;
+                    c.ldq = ldh16;
+                    c.qamax = act_amax;
+                }
             } else {
                 c.h_out = Hx + (long long)(st_ + 1) * m * H;
                 c.ldh = H;
@@ -1518,6 +1229,12 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
                     c.h_out2 = t.Xd.as<float>();
                     c.ldh2 = Kd;
                     c.mr = mr;
+                    if (xq_hi) {
+                        c.q_hi = xq_hi;
+                        c.q_lo = xq_lo;
+                        c.ldq = ldxq;
+                        c.qamax = act_amax;
+                    }
                 }
             }
             k_cell_fwd<<<blocks(m * H, 256), 256, 0, s>>>(c);
@@ -1534,6 +1251,10 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         KT_CUDA(cudaMemsetAsync(Hs, 0, m * Hd * 4, s));
         // h part of X_0 = 0 (zero initial state)
         KT_CUDA(cudaMemset2DAsync(Xd + na2, (size_t)Kd * 4, 0, (size_t)Hd * 4, (size_t)m, s));
+        if (xq_hi) {
+            KT_CUDA(cudaMemset2DAsync(xq_hi + na2, (size_t)ldxq * 2, 0, (size_t)Hd * 2, (size_t)m, s));
+            KT_CUDA(cudaMemset2DAsync(xq_lo + na2, (size_t)ldxq * 2, 0, (size_t)Hd * 2, (size_t)m, s));
+        }
         if ((st = gemm_rm(t, false, false, 7 * m, t.n_d, na2, t.A.as<float>(), na2, Wh + (long long)t.n_s * t.n_d,
                           t.n_d, 0.0f, t.U.as<float>(), t.n_d)))
             return st;
@@ -1557,6 +1278,12 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             af.n_in = t.n_in;
             af.X = X;
             af.ldx = Kd;
+            if (xq_hi) {
+                af.x_hi = xq_hi + (long long)p * m * ldxq;
+                af.x_lo = xq_lo + (long long)p * m * ldxq;
+                af.ldxq = ldxq;
+                af.qamax = act_amax;
+            }
             af.alpha = t.alpha.as<float>() + (long long)p * m * 7;
             af.hid = t.hid.as<float>() + (long long)p * m * 7 * t.n_d;
             if (!launch_k_attn_fwd(t.n_d, af, blocks(m * 32, 256), s))
@@ -1564,8 +1291,10 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             ++t.launches;
         }
         float* Z = t.Zd.as<float>() + (long long)p * m * 4 * Hd;
+        const ks_trainer::Planes xp{xq_hi ? xq_hi + (long long)p * m * ldxq : nullptr,
+                                    xq_hi ? xq_lo + (long long)p * m * ldxq : nullptr, ldxq, act_amax};
         if ((st = gemm_rm(t, false, false, m, 4LL * Hd, Kd, X, Kd, P + D.wd(), 4LL * Hd, 0.0f, Z, 4LL * Hd, true,
-                          act_amax)))
+                          act_amax, nullptr, false, xq_hi ? &xp : nullptr)))
             return st;
         CellFwd c{};
         c.M = M;
@@ -1582,6 +1311,12 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         c.ldh = Hd;
         c.h_out2 = p + 1 < T ? Xd + (long long)(p + 1) * m * Kd + D.x_dense : nullptr;
         c.ldh2 = Kd;
+        if (xq_hi && p + 1 < T) {
+            c.q_hi = xq_hi + (long long)(p + 1) * m * ldxq + D.x_dense;
+            c.q_lo = xq_lo + (long long)(p + 1) * m * ldxq + D.x_dense;
+            c.ldq = ldxq;
+            c.qamax = act_amax;
+        }
         c.mr = mr;
         k_cell_fwd<<<blocks(m * Hd, 256), 256, 0, s>>>(c);
         ++t.launches;
@@ -1684,8 +1419,9 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         }
     }
     // decoder weight gradients: one GEMM over all (position, row) pairs
+    const ks_trainer::Planes xw{xq_hi, xq_lo, ldxq, act_amax};
     if ((st = gemm_rm(t, true, false, Kd, 4LL * Hd, (long long)T * m, Xd, Kd, t.dZd.as<float>(), 4LL * Hd, 1.0f,
-                      G + D.wd(), 4LL * Hd, false, act_amax, dzd_amax, dzd_amax != nullptr)))
+                      G + D.wd(), 4LL * Hd, false, act_amax, dzd_amax, dzd_amax != nullptr, xq_hi ? &xw : nullptr)))
         return st;
     if ((st = gemm_rm(t, true, false, D.S + 1, 4LL * Hd, (long long)T * m, t.dec_sm.as<float>(), D.S + 1,
                       t.dZd.as<float>(), 4LL * Hd, 1.0f, G + D.ws(), 4LL * Hd, false, act_amax, dzd_amax,
@@ -1770,8 +1506,11 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
                 return st;
         }
         float* Hx = t.Hx[dir].as<float>();
+        const long long ldh16 = (H + 7) / 8 * 8;
+        __half* hx_hi = (t.f16x3 && attn) ? t.Hx16[dir].as<__half>() : nullptr;
+        const ks_trainer::Planes hw{hx_hi, hx_hi ? hx_hi + 8LL * m * ldh16 : nullptr, ldh16, act_amax};
         if ((st = gemm_rm(t, true, false, H, 4LL * H, 7 * m, Hx, H, t.dZe[dir].as<float>(), 4LL * H, 1.0f,
-                          G + L.wd(), 4LL * H, false, act_amax, dze_amax, dze_amax != nullptr)))
+                          G + L.wd(), 4LL * H, false, act_amax, dze_amax, dze_amax != nullptr, hx_hi ? &hw : nullptr)))
             return st;
         if ((st = gemm_rm(t, true, false, t.d_in + 1, 4LL * H, 7 * m, t.enc_sm[dir].as<float>(), t.d_in + 1,
                           t.dZe[dir].as<float>(), 4LL * H, 1.0f, G + L.ws(), 4LL * H, false, act_amax, dze_amax,
@@ -1991,23 +1730,16 @@ extern "C" ks_status ks_trainer_create(const ks_model_desc* d, double dropout, d
         cudaMemset(t.adam_m.p, 0, (size_t)cursor * 4) != cudaSuccess ||
         cudaMemset(t.adam_v.p, 0, (size_t)cursor * 4) != cudaSuccess)
         return set_error(KS_ERR_CUDA, "trainer upload failed");
-    if (cublasCreate(&t.blas) != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cublasCreate failed");
     {
         const char* g = std::getenv("KS_TRAIN_GEMM");
-        t.tf32x3 = !(g && std::string(g) == "fp32");
-        // F16X3 by default (fp16 GEMMs run 2.4x the TF32 rate); KS_TRAIN_GEMM=tf32x3 keeps
-        // the 3xTF32 split, =fp32 the SIMT SGEMM
-        t.f16x3 = !(g && (std::string(g) == "fp32" || std::string(g) == "tf32x3"));
+        // F16X3 on the tensor cores by default; KS_TRAIN_GEMM=fp32: the fp32 SIMT GEMM
+        t.f16x3 = !(g && std::string(g) == "fp32");
         const float betas[2] = {0.0f, 1.0f};
         if (t.scal.ensure((size_t)(kScalSlots + 2) * 4) != cudaSuccess ||
             cudaMemcpy(t.scal.as<char>() + (size_t)kScalSlots * 4, betas, 8, cudaMemcpyHostToDevice) != cudaSuccess)
             return set_error(KS_ERR_CUDA, "trainer scale slots");
+        cudaDeviceGetAttribute(&t.sms, cudaDevAttrMultiProcessorCount, t.device);
     }
-    if (t.blas_ws.ensure((size_t)64 << 20) != cudaSuccess) return set_error(KS_ERR_CUDA, "cuBLAS workspace");
-    if (cublasLtCreate(&t.lt) != CUBLAS_STATUS_SUCCESS) return set_error(KS_ERR_CUDA, "cublasLtCreate failed");
-    // cuBLAS on a fixed workspace (no allocations inside captured graphs)
-    if (cublasSetWorkspace(t.blas, t.blas_ws.p, t.blas_ws.bytes) != CUBLAS_STATUS_SUCCESS)
-        return set_error(KS_ERR_CUDA, "cublasSetWorkspace failed");
     if (t.se.ensure(16) != cudaSuccess || cudaMemset(t.se.p, 0, 16) != cudaSuccess)
         return set_error(KS_ERR_CUDA, "trainer step scalars");
     {
@@ -2043,14 +1775,6 @@ extern "C" void ks_trainer_destroy(ks_trainer* t) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (t->gev) cudaEventDestroy(t->gev);
     if (t->gs) cudaStreamDestroy(t->gs);
-    if (t->blas) cublasDestroy(t->blas);
-    for (auto& kv : t->lt_plans) {
-        if (kv.second.lc) cublasLtMatrixLayoutDestroy(kv.second.lc);
-        if (kv.second.lb) cublasLtMatrixLayoutDestroy(kv.second.lb);
-        if (kv.second.la) cublasLtMatrixLayoutDestroy(kv.second.la);
-        if (kv.second.op) cublasLtMatmulDescDestroy(kv.second.op);
-    }
-    if (t->lt) cublasLtDestroy(t->lt);
     delete t;
 }
 

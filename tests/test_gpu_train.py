@@ -170,10 +170,10 @@ def test_export_import_roundtrip_is_identity():
     np.testing.assert_array_equal(tr.export(), v)
 
 
-def test_tf32x3_training_gemms_meet_the_gradient_bar(monkeypatch):
-    """KS_TRAIN_GEMM=tf32x3: the 3xTF32 split (the alternative to the default
-    per-operand-scaled F16X3) meets the same gradient bar."""
-    monkeypatch.setenv("KS_TRAIN_GEMM", "tf32x3")
+def test_fp32_simt_training_gemms_meet_the_gradient_bar(monkeypatch):
+    """KS_TRAIN_GEMM=fp32: every contraction on the fp32 SIMT GEMM (the check on
+    the default F16X3 tcgen05 GEMM) meets the same gradient bar."""
+    monkeypatch.setenv("KS_TRAIN_GEMM", "fp32")
     test_small_trained_gradients_vs_oracle(0.2)
     if os.path.exists(BIG_CKPT):
         test_default_size_gradients_vs_oracle()
