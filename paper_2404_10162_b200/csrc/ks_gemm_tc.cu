@@ -99,6 +99,119 @@ struct TcCfg {
 __device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float tanh_fast(float x) { return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x)); }
 
+// Cell-mode epilogue of one accumulator (rows row0 + [q*32, q*32+32) of the tile,
+// units [half*UNITS/2, +UNITS/2) of N tile nt).  bars[tfull + acc] / bars[tempty + acc]:
+// the accumulator's full / empty barriers.  Each 16-row group g of the warp's 32
+// rows is read with tcgen05.ld.16x256b: lane t holds rows t/4 and t/4 + 8 of the
+// group, units 2(t%4), 2(t%4)+1 of each 8-unit chunk, all four gates (one load per
+// gate block) -- the LSTM cell needs no exchange, and the 4 lanes of a quad write
+// one row's 8 units (a whole 32-byte segment) per store instruction.
+template <int UNITS, bool SPLIT, int CG>
+__device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars, uint32_t tmem_base, int acc,
+                                               uint32_t acc_phase, int row0, int TRp, int nt, int q, int half,
+                                               int lane, int tfull, int tempty, int acc_cols, bool leader) {
+    constexpr int HU = UNITS / 2;
+    constexpr int NCH = HU / 8;
+    const int tq = lane >> 2, tcol = 2 * (lane & 3);
+    int rows[4], slots[4], crows[4];
+    bool valid[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // i = 2 g + j: group g, row t/4 + 8 j
+        const int lr = q * 32 + 16 * (i >> 1) + tq + 8 * (i & 1);
+        rows[i] = row0 + lr;
+        valid[i] = rows[i] < p.M && (CG == 2 || lr < TRp);
+        slots[i] = valid[i] ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)rows[i] * p.slot_stride] : 0) : 0;
+        crows[i] = valid[i] ? (p.parent ? p.parent[rows[i]] : rows[i]) : -1;
+    }
+    const bool have_cprev = p.c_prev != nullptr;
+    // G[slot] (4 gates) and c_prev of the chunk's 2 units per row, prefetched a chunk ahead
+    float2 gn[4][4], cn[4];
+    auto load_bc = [&](int c, float2 (&gx)[4][4], float2 (&cx)[4]) {
+        const int u0 = nt * UNITS + half * HU + c * 8 + tcol;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float* G = p.G + (long long)slots[i] * 4 * p.H;
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt)
+                gx[i][gt] = valid[i] ? *reinterpret_cast<const float2*>(G + gt * p.H + u0) : make_float2(0.f, 0.f);
+            cx[i] = (valid[i] && have_cprev && crows[i] >= 0)
+                        ? *reinterpret_cast<const float2*>(p.c_prev + (long long)crows[i] * p.ldc_prev + u0)
+                        : make_float2(0.f, 0.f);
+        }
+    };
+    load_bc(0, gn, cn);
+    tc::mbar_wait(tc::smem_u32(&bars[tfull + acc]), acc_phase);
+    tc::fence_after();
+    const uint32_t tq_base = tmem_base + ((uint32_t)(q * 32) << 16) + acc * acc_cols;
+    constexpr float sc = SPLIT ? kSplitUnscale : 1.0f;  // a power of two: exact
+    const float2 sc2 = make_float2(sc, sc);
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+        const int uc = half * HU + c * 8;
+        float v[2][4][4];  // [group][gate][r0u0, r0u1, r1u0, r1u1]
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt)
+                tc::tmem_ld16x256(tq_base + ((uint32_t)(16 * g) << 16) + gt * UNITS + uc, v[g][gt]);
+        tc::tmem_wait_ld();
+        if (c == NCH - 1) {  // this warp's TMEM reads are done: release the accumulator
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2 && !leader)
+                    tc::mbar_arrive_remote(tc::smem_u32(&bars[tempty + acc]), 0);
+                else
+                    tc::mbar_arrive(tc::smem_u32(&bars[tempty + acc]));
+            }
+        }
+        float2 gb[4][4], cp[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            cp[i] = cn[i];
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt) gb[i][gt] = gn[i][gt];
+        }
+        if (c + 1 < NCH) load_bc(c + 1, gn, cn);
+        const int u0 = nt * UNITS + uc + tcol;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!valid[i]) continue;
+            const int g = i >> 1, j = i & 1;
+            float2 z[4];
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt)
+                z[gt] = __ffma2_rn(make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]), sc2, gb[i][gt]);
+            const float zi[2] = {z[0].x, z[0].y}, zf[2] = {z[1].x, z[1].y};
+            const float zo[2] = {z[2].x, z[2].y}, zc[2] = {z[3].x, z[3].y};
+            const float cpv[2] = {cp[i].x, cp[i].y};
+            float hv[2], cv[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float cnv = sigm_fast(zf[e]) * cpv[e] + sigm_fast(zi[e]) * tanh_fast(zc[e]);
+                cv[e] = cnv;
+                hv[e] = sigm_fast(zo[e]) * tanh_fast(cnv);
+            }
+            const long long r = rows[i];
+            // streaming (evict-first) stores: h and c are re-read once, by the next kernels,
+            // and would otherwise push the GEMM's reused operands (W, P^T) out of L2
+            __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[0], hv[1]));
+            if (p.h_out2 != nullptr)
+                __stcs(reinterpret_cast<float2*>(p.h_out2 + r * p.ldh2 + u0), make_float2(hv[0], hv[1]));
+            __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[0], cv[1]));
+            if (p.hA_hi != nullptr && p.ha_bf16) {
+                *reinterpret_cast<__nv_bfloat162*>(p.hA_hi + r * p.ldha + u0) =
+                    __floats2bfloat162_rn(hv[0], hv[1]);
+            } else if (p.hA_hi != nullptr) {
+                __half2 hh, hl;
+                split_f16x2(hv[0], hv[1], hh, hl);
+                *reinterpret_cast<__half2*>(p.hA_hi + r * p.ldha + u0) = hh;
+                *reinterpret_cast<__half2*>(p.hA_lo + r * p.ldha + u0) = hl;
+            }
+        }
+    }
+}
+
 template <int UNITS, bool SPLIT, int CG>
 __global__ void __launch_bounds__(384, 1)
     lstm_gemm_tc(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap mA0,
@@ -286,40 +399,24 @@ __global__ void __launch_bounds__(384, 1)
             const int lt = t - pr.tile_begin;
             const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
             const int TRp = tile_rows(p);
-            const int row = (CG == 1 ? mt * TRp : (mt * CG + rank) * TC_BM) + q * 32 + lane;
+            const int row0 = CG == 1 ? mt * TRp : (mt * CG + rank) * TC_BM;  // first row of this CTA's tile
+            if (!p.raw) {
+                // cell mode: 16x256b TMEM loads, so the 4 lanes of a quad hold 2 consecutive
+                // units each of the same row -- every h / c / split-h store instruction
+                // writes whole 32-byte row segments (half the L1 wavefronts of row-per-lane)
+                epilogue_cells<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half, lane,
+                                          2 * S, 2 * S + AS, Cfg::ACC_COLS, leader);
+                if (++acc == AS) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                continue;
+            }
+            const int row = row0 + q * 32 + lane;
             const bool valid = row < p.M && (CG == 2 || q * 32 + lane < TRp);
-            const bool raw = p.raw != 0;
-            // per-row gathers issued before waiting on the accumulator
-            const int slot = (valid && !raw) ? p.slot_base + (p.slot_ptr ? p.slot_ptr[(long long)row * p.slot_stride] : 0) : 0;
-            const int crow = (valid && !raw) ? (p.parent ? p.parent[row] : row) : -1;
-            const float* G = p.G + (long long)slot * 4 * p.H;
-            const bool cell = valid && !raw;
-            const bool have_c = cell && p.c_prev != nullptr && crow >= 0;
-            // G[slot] and c_prev of the next chunk are loaded while the current one
-            // computes (chunk 0's before waiting on the accumulator): the epilogue is
-            // latency bound, and at small K (the encoder) it paces the whole GEMM
-            float gbn[4][8], cpn[8];
-            auto load_bc = [&](int c, float (&gbx)[4][8], float (&cpx)[8]) {
-                const int u0 = nt * UNITS + half * HU + c * 8;
-#pragma unroll
-                for (int gt = 0; gt < 4; ++gt) {
-                    float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
-                    if (cell) {
-                        b0 = *reinterpret_cast<const float4*>(G + gt * p.H + u0);
-                        b1 = *reinterpret_cast<const float4*>(G + gt * p.H + u0 + 4);
-                    }
-                    gbx[gt][0] = b0.x; gbx[gt][1] = b0.y; gbx[gt][2] = b0.z; gbx[gt][3] = b0.w;
-                    gbx[gt][4] = b1.x; gbx[gt][5] = b1.y; gbx[gt][6] = b1.z; gbx[gt][7] = b1.w;
-                }
-                float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
-                if (have_c) {
-                    c0 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0);
-                    c1 = *reinterpret_cast<const float4*>(p.c_prev + (long long)crow * p.ldc_prev + u0 + 4);
-                }
-                cpx[0] = c0.x; cpx[1] = c0.y; cpx[2] = c0.z; cpx[3] = c0.w;
-                cpx[4] = c1.x; cpx[5] = c1.y; cpx[6] = c1.z; cpx[7] = c1.w;
-            };
-            load_bc(0, gbn, cpn);
+            // raw mode (the context projection P = a_t . W_ctx: no bias, no cell): the
+            // pre-activations are stored transposed and split, in the B-operand order of
+            // the alpha-block MMA; lane = row, so each 2-byte column store is coalesced
             tc::mbar_wait(tc::smem_u32(&bars[2 * S + acc]), acc_phase);
             tc::fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS;
@@ -341,81 +438,22 @@ __global__ void __launch_bounds__(384, 1)
                             tc::mbar_arrive(tc::smem_u32(&bars[2 * S + AS + acc]));
                     }
                 }
-                float gb[4][8], cp[8];
+                if (!valid) continue;
+                const float sc = SPLIT ? kSplitUnscale : 1.0f;
 #pragma unroll
-                for (int gt = 0; gt < 4; ++gt)
+                for (int gt = 0; gt < 4; ++gt) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) gb[gt][j] = gbn[gt][j];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) cp[j] = cpn[j];
-                if (c + 1 < NCH) load_bc(c + 1, gbn, cpn);
-                if (valid && raw) {
-                    // context projection P = a_t . W_ctx (no bias, no cell), stored
-                    // transposed in the B-operand order of the alpha-block MMA
-                    const float sc = SPLIT ? kSplitUnscale : 1.0f;
-#pragma unroll
-                    for (int gt = 0; gt < 4; ++gt) {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const long long n = (long long)nt * Cfg::BN + gt * UNITS + uc + j;
-                            const float v = g[gt][j] * sc;
-                            if (SPLIT) {
-                                __half hi, lo;
-                                split_f16s(v, kPScale, hi, lo);
-                                p.pt_hi[n * p.ldt + row] = hi;
-                                p.pt_lo[n * p.ldt + row] = lo;
-                            } else {
-                                reinterpret_cast<__nv_bfloat16*>(p.pt_hi)[n * p.ldt + row] = __float2bfloat16_rn(v);
-                            }
+                    for (int j = 0; j < 8; ++j) {
+                        const long long n = (long long)nt * Cfg::BN + gt * UNITS + uc + j;
+                        const float v = g[gt][j] * sc;
+                        if (SPLIT) {
+                            __half hi, lo;
+                            split_f16s(v, kPScale, hi, lo);
+                            p.pt_hi[n * p.ldt + row] = hi;
+                            p.pt_lo[n * p.ldt + row] = lo;
+                        } else {
+                            reinterpret_cast<__nv_bfloat16*>(p.pt_hi)[n * p.ldt + row] = __float2bfloat16_rn(v);
                         }
-                    }
-                } else if (valid) {
-                    const int u0 = nt * UNITS + uc;
-                    float hv[8], cv[8];
-                    const float sc = SPLIT ? kSplitUnscale : 1.0f;  // a power of two: the scaling is exact
-                    const float2 sc2 = make_float2(sc, sc);
-#pragma unroll
-                    for (int j = 0; j < 8; j += 2) {
-                        // gate pre-activations of units j, j+1 on paired FMAs (FFMA2)
-                        float2 z[4];
-#pragma unroll
-                        for (int gt = 0; gt < 4; ++gt)
-                            z[gt] = __ffma2_rn(make_float2(g[gt][j], g[gt][j + 1]), sc2,
-                                               make_float2(gb[gt][j], gb[gt][j + 1]));
-                        const float zi[2] = {z[0].x, z[0].y}, zf[2] = {z[1].x, z[1].y};
-                        const float zo[2] = {z[2].x, z[2].y}, zc[2] = {z[3].x, z[3].y};
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const float cn = sigm_fast(zf[e]) * cp[j + e] + sigm_fast(zi[e]) * tanh_fast(zc[e]);
-                            cv[j + e] = cn;
-                            hv[j + e] = sigm_fast(zo[e]) * tanh_fast(cn);
-                        }
-                    }
-                    float4* hd = reinterpret_cast<float4*>(p.h_out + (long long)row * p.ldh + u0);
-                    float4* cd = reinterpret_cast<float4*>(p.c_out + (long long)row * p.ldc + u0);
-                    hd[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
-                    hd[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
-                    if (p.h_out2 != nullptr) {
-                        float4* h2 = reinterpret_cast<float4*>(p.h_out2 + (long long)row * p.ldh2 + u0);
-                        h2[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
-                        h2[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
-                    }
-                    cd[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-                    cd[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
-                    if (p.hA_hi != nullptr && p.ha_bf16) {
-                        __align__(16) __nv_bfloat16 hb[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) hb[j] = __float2bfloat16_rn(hv[j]);
-                        *reinterpret_cast<uint4*>(p.hA_hi + (long long)row * p.ldha + u0) =
-                            *reinterpret_cast<const uint4*>(hb);
-                    } else if (p.hA_hi != nullptr) {
-                        __align__(16) __half2 hh[4], hl[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) split_f16x2(hv[2 * j], hv[2 * j + 1], hh[j], hl[j]);
-                        *reinterpret_cast<uint4*>(p.hA_hi + (long long)row * p.ldha + u0) =
-                            *reinterpret_cast<const uint4*>(hh);
-                        *reinterpret_cast<uint4*>(p.hA_lo + (long long)row * p.ldha + u0) =
-                            *reinterpret_cast<const uint4*>(hl);
                     }
                 }
             }
