@@ -95,6 +95,8 @@ struct LstmArgs {
     // 64*kb_alpha columns hold each row's alpha_t at 7 * (config - b0) + t
     int kb_alpha;
     int rows_per_cfg;
+    int fan;               // > 1: row r is the shared parent of child rows r*fan .. r*fan+fan-1 (the
+                           // epilogue adds each child's G[slot] and writes the children's h, c)
     int drop_pass;         // precision study only (KS_F16X2): 1 skips A_lo.W_hi, 2 skips A_hi.W_lo
     int alpha_tile;        // rows of the alpha-block layout tile: 128, or 256 for CTA-pair GEMMs
     const __half* PT_hi;   // P^T planes [4H][ldpt]

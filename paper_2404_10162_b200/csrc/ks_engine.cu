@@ -1206,15 +1206,22 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             c_prev = encc_at(0, 6 & 1);
             par = nullptr;                              // H_0 = 1: row r = config r
         }
+        // position 1: every hypothesis is a child of the single root (H_0 = 1), and
+        // siblings share [ctx | h_prev] and c_prev -- attention and the gate GEMM run
+        // once per config (classic ctx operand) and the GEMM epilogue fans each
+        // parent row's gates out to its H children (gates + G[slot(child)])
+        const bool fan = pos == 1 && H > 1 && !enc_dec && !hybrid && E.precision != KS_PREC_FP32 &&
+                         E.ctxproj && !E.pair_now();
+        const int Mg = fan ? (int)C : M;  // rows of this position's attention and gate GEMM
         AttnArgs aa{};
-        aa.M = M;
-        aa.H_rows = H;
+        aa.M = Mg;
+        aa.H_rows = fan ? 1 : H;
         aa.NS = Hd;
         aa.NA2 = NA2;
         aa.nd = E.n_d;
         aa.h_prev = h_prev;
         aa.ldh = Hd;
-        aa.parent = par;
+        aa.parent = fan ? nullptr : par;  // fan: row b of position 0 is config b's root
         aa.act = act;
         aa.uatt = E.uatt.as<float>();
         aa.Ws = enc_dec ? nullptr : E.attWs.as<float>();
@@ -1227,7 +1234,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         aa.A_hi = E.Ahi.as<__half>();
         aa.A_lo = E.Alo.as<__half>();
         aa.split_mode = E.precision == KS_PREC_FP32 ? 0 : (E.precision == KS_PREC_F16X3 ? 1 : 2);
-        aa.kalpha = E.proj_at(pos, H) ? E.alpha_cols_of(H) : 0;
+        aa.kalpha = (!fan && E.proj_at(pos, H)) ? E.alpha_cols_of(H) : 0;
         aa.alpha_tile = E.alpha_tile_of(H);
         // same rows and layout as the previous alpha-block position: its zeros are still in place
         aa.alpha_sparse = (aa.kalpha && alpha_fill_H == H) ? 1 : 0;
@@ -1240,7 +1247,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         }
 
         LstmArgs p{};
-        p.M = M;
+        p.M = Mg;
         p.H = Hd;
         p.K = Kd;
         p.A = E.Abuf.as<float>();
@@ -1262,7 +1269,8 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         }
         p.c_prev = c_prev;
         p.ldc_prev = Hd;
-        p.parent = par;
+        p.parent = fan ? nullptr : par;
+        p.fan = fan ? H : 0;
         p.h_out = hb + (size_t)cur * R * Hd;
         p.ldh = Hd;
         p.c_out = cb + (size_t)cur * R * Hd;
@@ -1274,7 +1282,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.ldah = Kd;
             p.ldw = Kd;
             p.wcol = 0;
-        } else if (E.proj_at(pos, H)) {
+        } else if (!fan && E.proj_at(pos, H)) {
             // [alpha block | h_prev] . [P^T | W_h]  (ctx . W_ctx = sum_t alpha_t P_t)
             const int kal = E.alpha_cols_of(H);
             p.K = kal + Hd;

@@ -96,8 +96,22 @@ struct TcCfg {
 
 // Cell nonlinearities with MUFU exp2 + fast reciprocal: absolute error ~1e-7,
 // far below the fp32-grade GEMM tolerance (the FP32 mode keeps libm expf/tanhf).
-__device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
-__device__ __forceinline__ float tanh_fast(float x) { return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * x)); }
+// The LSTM cell (nn.cpp:88-128) with 5 exp2 + 2 reciprocals on the MUFU pipe instead
+// of 5 + 5: with A = 1 + e^-f, B = 1 + e^-i, G = 1 + e^2g (sig(f) = 1/A, sig(i) = 1/B,
+// tanh(g) = (G - 2)/G),  c' = (c B G + A (G - 2)) / (A B G);  with O = 1 + e^-o and
+// Q = 1 + e^2c',  h' = (Q - 2) / (O Q).  Arguments are clamped so the products stay
+// finite (|sig, tanh| saturate to within 1.4e-11 of their limits there, far below
+// the fp32 resolution of the states).
+__device__ __forceinline__ void lstm_cell_fast(float zi, float zf, float zo, float zg, float cp, float& c,
+                                               float& h) {
+    const float A = 1.0f + __expf(-fminf(fmaxf(zf, -25.0f), 25.0f));
+    const float B = 1.0f + __expf(-fminf(fmaxf(zi, -25.0f), 25.0f));
+    const float G = 1.0f + __expf(2.0f * fminf(fmaxf(zg, -12.5f), 12.5f));
+    c = __fdividef(fmaf(cp * B, G, A * (G - 2.0f)), A * B * G);
+    const float O = 1.0f + __expf(-fminf(fmaxf(zo, -25.0f), 25.0f));
+    const float Q = 1.0f + __expf(2.0f * fminf(fmaxf(c, -12.5f), 12.5f));
+    h = __fdividef(Q - 2.0f, O * Q);
+}
 
 // Cell-mode epilogue of one accumulator (rows row0 + [q*32, q*32+32) of the tile,
 // units [half*UNITS/2, +UNITS/2) of N tile nt).  bars[tfull + acc] / bars[tempty + acc]:
@@ -188,9 +202,7 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
             float hv[2], cv[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const float cnv = sigm_fast(zf[e]) * cpv[e] + sigm_fast(zi[e]) * tanh_fast(zc[e]);
-                cv[e] = cnv;
-                hv[e] = sigm_fast(zo[e]) * tanh_fast(cnv);
+                lstm_cell_fast(zi[e], zf[e], zo[e], zc[e], cpv[e], cv[e], hv[e]);
             }
             const long long r = rows[i];
             // streaming (evict-first) stores: h and c are re-read once, by the next kernels,
@@ -207,6 +219,99 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
                 split_f16x2(hv[0], hv[1], hh, hl);
                 *reinterpret_cast<__half2*>(p.hA_hi + r * p.ldha + u0) = hh;
                 *reinterpret_cast<__half2*>(p.hA_lo + r * p.ldha + u0) = hl;
+            }
+        }
+    }
+}
+
+// Fan-out cell epilogue: the GEMM ran on PARENT rows (children of one parent share
+// [ctx | h_prev] and c_prev and differ only by the fed-back token's one-hot row,
+// i.e. by G[slot]); each parent row's pre-activations D serve its `fan` children:
+// gates(child) = D + G[slot(child)], c_prev = the parent's c.  Layout as
+// epilogue_cells (16x256b loads: a quad of lanes = one row, 8 units).
+template <int UNITS, bool SPLIT, int CG>
+__device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, uint32_t tmem_base, int acc,
+                                             uint32_t acc_phase, int row0, int TRp, int nt, int q, int half,
+                                             int lane, int tfull, int tempty, int acc_cols, bool leader) {
+    constexpr int HU = UNITS / 2;
+    constexpr int NCH = HU / 8;
+    const int tq = lane >> 2, tcol = 2 * (lane & 3);
+    const int fan = p.fan;
+    int rows[4];
+    bool valid[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int lr = q * 32 + 16 * (i >> 1) + tq + 8 * (i & 1);
+        rows[i] = row0 + lr;
+        valid[i] = rows[i] < p.M && (CG == 2 || lr < TRp);
+    }
+    const bool have_cprev = p.c_prev != nullptr;
+    float2 cn[4];
+    auto load_c = [&](int c, float2 (&cx)[4]) {
+        const int u0 = nt * UNITS + half * HU + c * 8 + tcol;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            cx[i] = (valid[i] && have_cprev)
+                        ? *reinterpret_cast<const float2*>(p.c_prev + (long long)rows[i] * p.ldc_prev + u0)
+                        : make_float2(0.f, 0.f);
+    };
+    load_c(0, cn);
+    tc::mbar_wait(tc::smem_u32(&bars[tfull + acc]), acc_phase);
+    tc::fence_after();
+    const uint32_t tq_base = tmem_base + ((uint32_t)(q * 32) << 16) + acc * acc_cols;
+    constexpr float sc = SPLIT ? kSplitUnscale : 1.0f;  // a power of two: exact
+    const float2 sc2 = make_float2(sc, sc);
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+        const int uc = half * HU + c * 8;
+        float v[2][4][4];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt)
+                tc::tmem_ld16x256(tq_base + ((uint32_t)(16 * g) << 16) + gt * UNITS + uc, v[g][gt]);
+        tc::tmem_wait_ld();
+        if (c == NCH - 1) {
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2 && !leader)
+                    tc::mbar_arrive_remote(tc::smem_u32(&bars[tempty + acc]), 0);
+                else
+                    tc::mbar_arrive(tc::smem_u32(&bars[tempty + acc]));
+            }
+        }
+        float2 cp[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp[i] = cn[i];
+        if (c + 1 < NCH) load_c(c + 1, cn);
+        const int u0 = nt * UNITS + uc + tcol;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!valid[i]) continue;
+            const int g = i >> 1, j = i & 1;
+            float2 d[4];
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt) d[gt] = make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]);
+            const float cpv[2] = {cp[i].x, cp[i].y};
+#pragma unroll 1
+            for (int f = 0; f < fan; ++f) {
+                const long long r = (long long)rows[i] * fan + f;
+                const int slot = p.slot_base + (p.slot_ptr ? p.slot_ptr[r * p.slot_stride] : 0);
+                const float* G = p.G + (long long)slot * 4 * p.H;
+                float2 z[4];
+#pragma unroll
+                for (int gt = 0; gt < 4; ++gt)
+                    z[gt] = __ffma2_rn(d[gt], sc2, *reinterpret_cast<const float2*>(G + gt * p.H + u0));
+                const float zi[2] = {z[0].x, z[0].y}, zf[2] = {z[1].x, z[1].y};
+                const float zo[2] = {z[2].x, z[2].y}, zc[2] = {z[3].x, z[3].y};
+                float hv[2], cv[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    lstm_cell_fast(zi[e], zf[e], zo[e], zc[e], cpv[e], cv[e], hv[e]);
+                }
+                __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[0], hv[1]));
+                __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[0], cv[1]));
             }
         }
     }
@@ -404,8 +509,12 @@ __global__ void __launch_bounds__(384, 1)
                 // cell mode: 16x256b TMEM loads, so the 4 lanes of a quad hold 2 consecutive
                 // units each of the same row -- every h / c / split-h store instruction
                 // writes whole 32-byte row segments (half the L1 wavefronts of row-per-lane)
-                epilogue_cells<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half, lane,
-                                          2 * S, 2 * S + AS, Cfg::ACC_COLS, leader);
+                if (p.fan > 1)
+                    epilogue_fan<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half, lane,
+                                                   2 * S, 2 * S + AS, Cfg::ACC_COLS, leader);
+                else
+                    epilogue_cells<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half,
+                                                     lane, 2 * S, 2 * S + AS, Cfg::ACC_COLS, leader);
                 if (++acc == AS) {
                     acc = 0;
                     acc_phase ^= 1;
