@@ -286,30 +286,30 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
         for (int i = 0; i < 4; ++i) cp[i] = cn[i];
         if (c + 1 < NCH) load_c(c + 1, cn);
         const int u0 = nt * UNITS + uc + tcol;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if (!valid[i]) continue;
-            const int g = i >> 1, j = i & 1;
-            float2 d[4];
-#pragma unroll
-            for (int gt = 0; gt < 4; ++gt) d[gt] = make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]);
-            const float cpv[2] = {cp[i].x, cp[i].y};
+        // child f of the thread's 4 rows at a time: their slot and G loads are independent
 #pragma unroll 1
-            for (int f = 0; f < fan; ++f) {
+        for (int f = 0; f < fan; ++f) {
+            float2 gz[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
                 const long long r = (long long)rows[i] * fan + f;
-                const int slot = p.slot_base + (p.slot_ptr ? p.slot_ptr[r * p.slot_stride] : 0);
+                const int slot = valid[i] ? p.slot_base + (p.slot_ptr ? p.slot_ptr[r * p.slot_stride] : 0) : 0;
                 const float* G = p.G + (long long)slot * 4 * p.H;
+#pragma unroll
+                for (int gt = 0; gt < 4; ++gt) gz[i][gt] = *reinterpret_cast<const float2*>(G + gt * p.H + u0);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (!valid[i]) continue;
+                const int g = i >> 1, j = i & 1;
                 float2 z[4];
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt)
-                    z[gt] = __ffma2_rn(d[gt], sc2, *reinterpret_cast<const float2*>(G + gt * p.H + u0));
-                const float zi[2] = {z[0].x, z[0].y}, zf[2] = {z[1].x, z[1].y};
-                const float zo[2] = {z[2].x, z[2].y}, zc[2] = {z[3].x, z[3].y};
+                    z[gt] = __ffma2_rn(make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]), sc2, gz[i][gt]);
                 float hv[2], cv[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    lstm_cell_fast(zi[e], zf[e], zo[e], zc[e], cpv[e], cv[e], hv[e]);
-                }
+                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[i].x, cv[0], hv[0]);
+                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[i].y, cv[1], hv[1]);
+                const long long r = (long long)rows[i] * fan + f;
                 __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[0], hv[1]));
                 __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[0], cv[1]));
             }
