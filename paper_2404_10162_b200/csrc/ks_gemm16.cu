@@ -511,6 +511,22 @@ __global__ void __launch_bounds__(256) sgemm_tile(const SgArgs a) {
     }
 }
 
+// many splits, few outputs: one warp per output, lanes over the splits (fixed-order shuffle tree)
+__global__ void sgemm_reduce_warp(const float* part, int splits, int M, int N, float* C, long long ldc, float beta) {
+    const long long n = (long long)M * N;
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    float s = 0.0f;
+    for (int k = lane; k < splits; k += 32) s += part[k * n + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        const long long r = i / N, c = i - r * N;
+        float* d = C + r * ldc + c;
+        *d = beta != 0.0f ? fmaf(beta, *d, s) : s;
+    }
+}
 __global__ void sgemm_reduce(const float* part, int splits, int M, int N, float* C, long long ldc, float beta) {
     const long long n = (long long)M * N;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -602,7 +618,7 @@ __global__ void __launch_bounds__(256) sgemm_narrow_cols(const SgArgs a) {
 long long narrow_kchunk(int M, long long K, int sms) {
     const long long rb = (M + 255) / 256;
     long long chunks = std::max(1LL, std::min((4LL * sms + rb - 1) / rb, (K + 63) / 64));
-    chunks = std::min(chunks, 256LL);
+    chunks = std::min(chunks, 128LL);
     long long ch = (K + chunks - 1) / chunks;
     return (ch + 63) / 64 * 64;
 }
@@ -671,7 +687,10 @@ bool launch_sgemm(bool ta, bool tb, int M, int N, long long K, const float* A, l
     if (splits > 1) {
         const long long tot = (long long)M * N;
         const int blocks = (int)std::min<long long>((tot + 255) / 256, 8LL * sms);
-        sgemm_reduce<<<blocks, 256, 0, stream>>>(part, splits, M, N, C, ldc, beta);
+        if (splits >= 16 && tot <= 65536)
+            sgemm_reduce_warp<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, stream>>>(part, splits, M, N, C, ldc, beta);
+        else
+            sgemm_reduce<<<blocks, 256, 0, stream>>>(part, splits, M, N, C, ldc, beta);
         if (cudaGetLastError() != cudaSuccess) return false;
         ++n;
     }

@@ -651,12 +651,15 @@ __global__ void k_colsum_partial(const float* in, long long R, int N, long long 
         part[(long long)c * N + n] = t;
     }
 }
+// one warp per column: lanes stride over the chunks, fixed-order shuffle tree
 __global__ void k_colsum_final(const double* part, int N, int chunks, float* out, int accumulate) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (n >= N) return;
     double t = 0.0;
-    for (int c = 0; c < chunks; ++c) t += part[(long long)c * N + n];
-    out[n] = accumulate ? out[n] + (float)t : (float)t;
+    for (int c = lane; c < chunks; c += 32) t += part[(long long)c * N + n];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) out[n] = accumulate ? out[n] + (float)t : (float)t;
 }
 
 // F16X3 operand split (ksb::f16_scale_exp, ks_tc.cuh): x 2^e = hi + lo with hi,
@@ -1034,7 +1037,7 @@ ks_status colsum(ks_trainer& t, cudaStream_t s, const float* in, long long R, in
     KT_CUDA(t.part.ensure((size_t)chunks * N * 8));
     dim3 g((N + 31) / 32, chunks), b(32, 8);
     k_colsum_partial<<<g, b, 0, s>>>(in, R, N, ld, chunks, t.part.as<double>());
-    k_colsum_final<<<(N + 127) / 128, 128, 0, s>>>(t.part.as<double>(), N, chunks, out, accumulate ? 1 : 0);
+    k_colsum_final<<<(N + 7) / 8, 256, 0, s>>>(t.part.as<double>(), N, chunks, out, accumulate ? 1 : 0);
     t.launches += 2;
     return KS_OK;
 }
