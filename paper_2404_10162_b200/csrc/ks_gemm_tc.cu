@@ -188,35 +188,35 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
         }
         if (c + 1 < NCH) load_bc(c + 1, gn, cn);
         const int u0 = nt * UNITS + uc + tcol;
+        // the 8 cells of the chunk (4 rows x 2 units) computed unconditionally and
+        // interleaved (independent dependency chains), stores predicated per row
+        float hv[4][2], cv[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            if (!valid[i]) continue;
             const int g = i >> 1, j = i & 1;
             float2 z[4];
 #pragma unroll
             for (int gt = 0; gt < 4; ++gt)
                 z[gt] = __ffma2_rn(make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]), sc2, gb[i][gt]);
-            const float zi[2] = {z[0].x, z[0].y}, zf[2] = {z[1].x, z[1].y};
-            const float zo[2] = {z[2].x, z[2].y}, zc[2] = {z[3].x, z[3].y};
-            const float cpv[2] = {cp[i].x, cp[i].y};
-            float hv[2], cv[2];
+            lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[i].x, cv[i][0], hv[i][0]);
+            lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[i].y, cv[i][1], hv[i][1]);
+        }
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                lstm_cell_fast(zi[e], zf[e], zo[e], zc[e], cpv[e], cv[e], hv[e]);
-            }
+        for (int i = 0; i < 4; ++i) {
+            if (!valid[i]) continue;
             const long long r = rows[i];
             // streaming (evict-first) stores: h and c are re-read once, by the next kernels,
             // and would otherwise push the GEMM's reused operands (W, P^T) out of L2
-            __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[0], hv[1]));
+            __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[i][0], hv[i][1]));
             if (p.h_out2 != nullptr)
-                __stcs(reinterpret_cast<float2*>(p.h_out2 + r * p.ldh2 + u0), make_float2(hv[0], hv[1]));
-            __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[0], cv[1]));
+                __stcs(reinterpret_cast<float2*>(p.h_out2 + r * p.ldh2 + u0), make_float2(hv[i][0], hv[i][1]));
+            __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[i][0], cv[i][1]));
             if (p.hA_hi != nullptr && p.ha_bf16) {
                 *reinterpret_cast<__nv_bfloat162*>(p.hA_hi + r * p.ldha + u0) =
-                    __floats2bfloat162_rn(hv[0], hv[1]);
+                    __floats2bfloat162_rn(hv[i][0], hv[i][1]);
             } else if (p.hA_hi != nullptr) {
                 __half2 hh, hl;
-                split_f16x2(hv[0], hv[1], hh, hl);
+                split_f16x2(hv[i][0], hv[i][1], hh, hl);
                 *reinterpret_cast<__half2*>(p.hA_hi + r * p.ldha + u0) = hh;
                 *reinterpret_cast<__half2*>(p.hA_lo + r * p.ldha + u0) = hl;
             }
@@ -298,20 +298,23 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt) gz[i][gt] = *reinterpret_cast<const float2*>(G + gt * p.H + u0);
             }
+            float hv[4][2], cv[4][2];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                if (!valid[i]) continue;
                 const int g = i >> 1, j = i & 1;
                 float2 z[4];
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt)
                     z[gt] = __ffma2_rn(make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]), sc2, gz[i][gt]);
-                float hv[2], cv[2];
-                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[i].x, cv[0], hv[0]);
-                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[i].y, cv[1], hv[1]);
+                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[i].x, cv[i][0], hv[i][0]);
+                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[i].y, cv[i][1], hv[i][1]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (!valid[i]) continue;
                 const long long r = (long long)rows[i] * fan + f;
-                __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[0], hv[1]));
-                __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[0], cv[1]));
+                __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[i][0], hv[i][1]));
+                __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[i][0], cv[i][1]));
             }
         }
     }
