@@ -407,6 +407,11 @@ def run_b200(args):
 
     for _ in range(max(1, args.warmup // 2)):
         host_call()
+    if host_out[0] is not None:
+        # a serving loop page-locks its long-lived result buffers once (ks_host_register,
+        # outside the timed region): the device-to-host copy then lands in them directly
+        _cabi.pin_results(host_out[0])
+        host_call()
     e2e_t = []
     for _ in range(max(2, args.steps // 2)):
         if world > 1:

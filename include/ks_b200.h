@@ -383,6 +383,16 @@ ks_status ks_trainer_import(ks_trainer* tr, const float* host_ref_flat);
 ks_status ks_trainer_to_reference_layout(const ks_trainer* tr, const float* host_train_flat,
                                          float* host_ref_flat);
 
+/* The training contractions' GEMM as a library call (csrc/ks_gemm16.cu), on
+ * caller DEVICE buffers and stream: C[M x N] = op(A) op(B) + beta C, row-major
+ * fp32; op(A) = A^T when ta (A stored K x M), op(B) = B^T when tb (B stored
+ * N x K); beta 0 or 1.  F16X3 on tcgen05: both operands split into fp16 hi/lo
+ * planes at power-of-two scales, hi.hi + hi.lo + lo.hi with fp32 accumulation
+ * (fp32-grade; the reference's fp64 GEMMs are autodiff.cpp:326-544's matmuls).
+ * Replaces the reference's training-time `matmul` (tensor.hpp / autodiff.cpp). */
+ks_status ks_gemm_f16x3(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                        const float* B, int64_t ldb, float beta, float* C, int64_t ldc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

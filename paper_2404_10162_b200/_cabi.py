@@ -82,7 +82,7 @@ EXPORTS = [
     "ks_engine_destroy", "ks_engine_num_positions", "ks_engine_vocab_size",
     "ks_engine_precision", "ks_engine_last_launch_count", "ks_engine_set_chunk",
     "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
-    "ks_host_register", "ks_host_unregister",
+    "ks_host_register", "ks_host_unregister", "ks_gemm_f16x3",
     "ks_engine_profile_reset", "ks_engine_profile_gemm_ms", "ks_engine_profile_launches",
     "ks_engine_profile_launches_ex",
     "ks_beam_search_batch_hooked", "ks_topk_metrics_batch",
@@ -135,6 +135,7 @@ def lib():
     L.ks_checkpoint_load.argtypes = [C.c_char_p, P(vp)]
     L.ks_host_register.argtypes = [vp, C.c_int64]
     L.ks_host_unregister.argtypes = [vp]
+    L.ks_gemm_f16x3.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, C.c_float, vp, i64, vp]
     L.ks_checkpoint_error_kind.restype = i32
     L.ks_checkpoint_free.argtypes = [vp]
     L.ks_checkpoint_header.argtypes = [vp, C.c_char_p]
@@ -193,6 +194,25 @@ def lib():
     L.ks_engine_synthetic_descriptors.argtypes = [vp, C.c_uint64, i64, i64, P(i64)]
     _lib = L
     return L
+
+
+def gemm_f16x3(A, B, C=None, ta=False, tb=False, beta=0.0, stream=None):
+    """ks_gemm_f16x3 on CUDA fp32 torch tensors (row-major, unit column stride):
+    C = op(A) op(B) + beta C with op = transpose when ta / tb; returns C."""
+    import torch
+    M, K = (A.shape[1], A.shape[0]) if ta else (A.shape[0], A.shape[1])
+    N = B.shape[0] if tb else B.shape[1]
+    if (B.shape[1] if tb else B.shape[0]) != K:
+        raise ValueError("inner dimensions differ")
+    if C is None:
+        C = torch.zeros((M, N), dtype=torch.float32, device=A.device)
+    for t in (A, B, C):
+        if t.dtype != torch.float32 or not t.is_cuda or t.stride(1) != 1:
+            raise ValueError("CUDA fp32 tensors with unit column stride expected")
+    s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+    check(lib().ks_gemm_f16x3(int(ta), int(tb), M, N, K, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                              float(beta), C.data_ptr(), C.stride(0), s))
+    return C
 
 
 def synthetic_descriptors(input_values, count, seed=2404, start=0):

@@ -424,6 +424,89 @@ bool launch_gemm16(const GemmF16Args& g, cudaStream_t stream, int* launches) {
 }
 
 // ---------------------------------------------------------------------------
+// F16X3 operand planes
+// ---------------------------------------------------------------------------
+namespace {
+
+// F16X3 operand split (ksb::f16_scale_exp, ks_tc.cuh): x 2^e = hi + lo with hi,
+// lo fp16 (~22-bit operands, like the decode GEMM's F16X3); e from the operand's
+// max |x| so that |x| 2^e < 2^14; entries above 2^-28 max|x| keep full relative
+// precision.  hi.hi + hi.lo + lo.hi (the tcgen05 GEMM, ks_gemm16.cu) times
+// 2^-(eA+eB) recovers an fp32-grade product at the fp16 tensor-core rate.
+// max |x| of a row-major block into *out (pre-zeroed; non-negative floats order as ints)
+__global__ void __launch_bounds__(256) k_absmax(const float* src, long long rows, long long cols, long long ld, int* out) {
+    __shared__ float wm[8];
+    float m = 0.0f;
+    for (long long r = blockIdx.y; r < rows; r += gridDim.y)
+        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (long long)gridDim.x * blockDim.x)
+            m = fmaxf(m, fabsf(src[r * ld + c]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one atomic per block
+        m = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0 && m > 0.0f) atomicMax(out, __float_as_int(m));
+    }
+}
+__device__ __forceinline__ void split_f16x2s(float x, float y, float sc, __half2& hi, __half2& lo) {
+    const float2 v = __fmul2_rn(make_float2(x, y), make_float2(sc, sc));
+    hi = __float22half2_rn(v);
+    const float2 h = __half22float2(hi);
+    lo = __float22half2_rn(__fadd2_rn(v, make_float2(-h.x, -h.y)));
+}
+// hi / lo planes of a row-major block, same layout (row stride ldo), 4 columns per
+// thread when aligned; flat grid-stride over (row, column group)
+__global__ void k_split_planes(const float* src, long long rows, int cols, long long ld, __half* hi, __half* lo,
+                               long long ldo, const int* amax) {
+    const float sc = exp2f((float)f16_scale_exp(*amax));
+    const bool vec = (cols & 3) == 0 && (ld & 3) == 0 && (ldo & 3) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hi) |
+                       reinterpret_cast<uintptr_t>(lo)) & 15) == 0;
+    const int cw = vec ? cols >> 2 : cols;
+    const long long n = rows * (long long)cw;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / cw;
+        const int c = (int)(i - r * cw);
+        if (vec) {
+            const float4 x = reinterpret_cast<const float4*>(src + r * ld)[c];
+            __half2 h01, l01, h23, l23;
+            split_f16x2s(x.x, x.y, sc, h01, l01);
+            split_f16x2s(x.z, x.w, sc, h23, l23);
+            uint2 hv, lv;
+            hv.x = *reinterpret_cast<uint32_t*>(&h01);
+            hv.y = *reinterpret_cast<uint32_t*>(&h23);
+            lv.x = *reinterpret_cast<uint32_t*>(&l01);
+            lv.y = *reinterpret_cast<uint32_t*>(&l23);
+            reinterpret_cast<uint2*>(hi + r * ldo)[c] = hv;
+            reinterpret_cast<uint2*>(lo + r * ldo)[c] = lv;
+        } else {
+            const float x = src[r * ld + c] * sc;
+            const __half h = __float2half_rn(x);
+            hi[r * ldo + c] = h;
+            lo[r * ldo + c] = __float2half_rn(x - __half2float(h));
+        }
+    }
+}
+
+}  // namespace
+
+void launch_absmax(const float* src, long long rows, long long cols, long long ld, int* out, cudaStream_t s) {
+    const unsigned gx = (unsigned)std::min<long long>((cols + 255) / 256, 8);
+    dim3 grid(gx, (unsigned)std::min<long long>(rows, std::max<long long>(1, 1184 / gx)));
+    k_absmax<<<grid, 256, 0, s>>>(src, rows, cols, ld, out);
+}
+
+void launch_split_planes(const float* src, long long rows, long long cols, long long ld, __half* hi, __half* lo,
+                         long long ldo, const int* amax, cudaStream_t s) {
+    const long long items = rows * ((cols + 3) / 4);
+    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((items + 255) / 256, 148LL * 16));
+    k_split_planes<<<grid, 256, 0, s>>>(src, rows, (int)cols, ld, hi, lo, ldo, amax);
+}
+
+// ---------------------------------------------------------------------------
 // fp32 SIMT GEMM (exact fp32 FMA, any transposes): the narrow training
 // contractions (heads, attention: an output side below 16 columns, where a
 // 128 x 128+ tensor-core tile would be mostly padding) and KS_TRAIN_GEMM=fp32.
@@ -699,3 +782,53 @@ bool launch_sgemm(bool ta, bool tb, int M, int N, long long K, const float* A, l
 }
 
 }  // namespace ksb
+
+// ---------------------------------------------------------------------------
+// C-ABI: the training GEMM as a library call on caller device buffers
+// ---------------------------------------------------------------------------
+#include "ks_b200.h"
+#include "ks_internal.h"
+
+extern "C" ks_status ks_gemm_f16x3(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, const float* A,
+                                   int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
+                                   void* stream) {
+    using ksb_host::set_error;
+    if (M <= 0 || N <= 0 || K <= 0) return set_error(KS_ERR_SHAPE, "ks_gemm_f16x3: empty GEMM");
+    if (beta != 0.0f && beta != 1.0f) return set_error(KS_ERR_PARAMETER, "ks_gemm_f16x3: beta must be 0 or 1");
+    if (M > (1LL << 30) || N > (1LL << 30)) return set_error(KS_ERR_SHAPE, "ks_gemm_f16x3: M, N too large");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // planes in the operands' own layouts: A is M x K (or K x M when ta), B is K x N (or N x K when tb)
+    const long long ar = ta ? K : M, ac = ta ? M : K, br = tb ? N : K, bc = tb ? K : N;
+    const long long lda16 = (ac + 7) / 8 * 8, ldb16 = (bc + 7) / 8 * 8;
+    const int splits = ksb::gemm16_splits((int)M, (int)N, K, sms);
+    const size_t abytes = (size_t)ar * lda16 * 4, bbytes = (size_t)br * ldb16 * 4;  // hi + lo planes
+    const size_t pbytes = splits > 1 ? (size_t)splits * M * N * 4 : 0;
+    char* ws = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), 256 + abytes + bbytes + pbytes, s);
+    if (e != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("ks_gemm_f16x3: ") + cudaGetErrorString(e));
+    int* amax = reinterpret_cast<int*>(ws);       // [0] A, [1] B
+    float* betad = reinterpret_cast<float*>(ws + 16);
+    __half* a_hi = reinterpret_cast<__half*>(ws + 256);
+    __half* a_lo = a_hi + (size_t)ar * lda16;
+    __half* b_hi = reinterpret_cast<__half*>(ws + 256 + abytes);
+    __half* b_lo = b_hi + (size_t)br * ldb16;
+    float* part = pbytes ? reinterpret_cast<float*>(ws + 256 + abytes + bbytes) : nullptr;
+    const float bsc[1] = {beta};
+    cudaMemsetAsync(amax, 0, 8, s);
+    cudaMemcpyAsync(betad, bsc, 4, cudaMemcpyHostToDevice, s);
+    ksb::launch_absmax(A, ar, ac, lda, amax, s);
+    ksb::launch_absmax(B, br, bc, ldb, amax + 1, s);
+    ksb::launch_split_planes(A, ar, ac, lda, a_hi, a_lo, lda16, amax, s);
+    ksb::launch_split_planes(B, br, bc, ldb, b_hi, b_lo, ldb16, amax + 1, s);
+    ksb::GemmF16Args g{a_hi, a_lo, lda16, ta ? 1 : 0, b_hi, b_lo, ldb16, tb ? 0 : 1, (int)M, (int)N, K,
+                       amax, amax + 1, betad, C, ldc, part, sms};
+    const bool ok = ksb::launch_gemm16(g, s, nullptr);
+    e = cudaFreeAsync(ws, s);
+    if (!ok) return set_error(KS_ERR_CUDA, "ks_gemm_f16x3: tensor-core GEMM launch failed");
+    if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
+        return set_error(KS_ERR_CUDA, std::string("ks_gemm_f16x3: ") + cudaGetErrorString(e));
+    return KS_OK;
+}

@@ -184,6 +184,11 @@ struct GemmF16Args {
     int sms;
 };
 int gemm16_splits(int M, int N, long long K, int sms);
+// F16X3 operand planes of a row-major fp32 block: max |x| into *out (pre-zeroed; float
+// bits), then hi / lo planes (row stride ldo) at the scale 2^f16_scale_exp(*amax)
+void launch_absmax(const float* src, long long rows, long long cols, long long ld, int* out, cudaStream_t s);
+void launch_split_planes(const float* src, long long rows, long long cols, long long ld, __half* hi, __half* lo,
+                         long long ldo, const int* amax, cudaStream_t s);
 bool launch_gemm16(const GemmF16Args& g, cudaStream_t stream, int* launches);
 // fp32 SIMT GEMM, C[M x N] = op(A) op(B) + beta C row-major; part: split-K
 // workspace of sgemm_splits(M, N, K, sms) * M * N floats (when > 1)

@@ -662,69 +662,8 @@ __global__ void k_colsum_final(const double* part, int N, int chunks, float* out
     if (lane == 0) out[n] = accumulate ? out[n] + (float)t : (float)t;
 }
 
-// F16X3 operand split (ksb::f16_scale_exp, ks_tc.cuh): x 2^e = hi + lo with hi,
-// lo fp16 (~22-bit operands, like the decode GEMM's F16X3); e from the operand's
-// max |x| so that |x| 2^e < 2^14; entries above 2^-28 max|x| keep full relative
-// precision.  hi.hi + hi.lo + lo.hi (the tcgen05 GEMM, ks_gemm16.cu) times
-// 2^-(eA+eB) recovers an fp32-grade product at the fp16 tensor-core rate.
+// F16X3 operand splits: ksb::launch_absmax / ksb::launch_split_planes (ks_gemm16.cu)
 using ksb::f16_scale_exp;
-// max |x| of a row-major block into *out (pre-zeroed; non-negative floats order as ints)
-__global__ void __launch_bounds__(256) k_absmax(const float* src, long long rows, long long cols, long long ld, int* out) {
-    __shared__ float wm[8];
-    float m = 0.0f;
-    for (long long r = blockIdx.y; r < rows; r += gridDim.y)
-        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (long long)gridDim.x * blockDim.x)
-            m = fmaxf(m, fabsf(src[r * ld + c]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x < 32) {  // one atomic per block
-        m = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (threadIdx.x == 0 && m > 0.0f) atomicMax(out, __float_as_int(m));
-    }
-}
-__device__ __forceinline__ void split_f16x2s(float x, float y, float sc, __half2& hi, __half2& lo) {
-    const float2 v = __fmul2_rn(make_float2(x, y), make_float2(sc, sc));
-    hi = __float22half2_rn(v);
-    const float2 h = __half22float2(hi);
-    lo = __float22half2_rn(__fadd2_rn(v, make_float2(-h.x, -h.y)));
-}
-// hi / lo planes of a row-major block, same layout (row stride ldo), 4 columns per
-// thread when aligned; flat grid-stride over (row, column group)
-__global__ void k_split_planes(const float* src, long long rows, int cols, long long ld, __half* hi, __half* lo,
-                               long long ldo, const int* amax) {
-    const float sc = exp2f((float)f16_scale_exp(*amax));
-    const bool vec = (cols & 3) == 0 && (ld & 3) == 0 && (ldo & 3) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(hi) |
-                       reinterpret_cast<uintptr_t>(lo)) & 15) == 0;
-    const int cw = vec ? cols >> 2 : cols;
-    const long long n = rows * (long long)cw;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i / cw;
-        const int c = (int)(i - r * cw);
-        if (vec) {
-            const float4 x = reinterpret_cast<const float4*>(src + r * ld)[c];
-            __half2 h01, l01, h23, l23;
-            split_f16x2s(x.x, x.y, sc, h01, l01);
-            split_f16x2s(x.z, x.w, sc, h23, l23);
-            uint2 hv, lv;
-            hv.x = *reinterpret_cast<uint32_t*>(&h01);
-            hv.y = *reinterpret_cast<uint32_t*>(&h23);
-            lv.x = *reinterpret_cast<uint32_t*>(&l01);
-            lv.y = *reinterpret_cast<uint32_t*>(&l23);
-            reinterpret_cast<uint2*>(hi + r * ldo)[c] = hv;
-            reinterpret_cast<uint2*>(lo + r * ldo)[c] = lv;
-        } else {
-            const float x = src[r * ld + c] * sc;
-            const __half h = __float2half_rn(x);
-            hi[r * ldo + c] = h;
-            lo[r * ldo + c] = __float2half_rn(x - __half2float(h));
-        }
-    }
-}
 
 // Loss / match totals (double, fixed order).
 __global__ void k_loss_total(const double* loss, const int* match, long long n, double* out_loss,
@@ -991,9 +930,7 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
         if (!amax) {
             if (t.scal_used + 1 > kScalSlots) return set_error(KS_ERR_UNSUPPORTED, "too many GEMMs in one training step");
             int* slot = slots + t.scal_used++;
-            const unsigned gx = (unsigned)std::min<long long>((cols + 255) / 256, 8);
-            dim3 grid(gx, (unsigned)std::min<long long>(rows, std::max<long long>(1, 1184 / gx)));
-            k_absmax<<<grid, 256, 0, s>>>(src, rows, cols, ld, slot);
+            ksb::launch_absmax(src, rows, cols, ld, slot, s);
             ++t.launches;
             amax = slot;
         }
@@ -1003,7 +940,7 @@ ks_status gemm_rm(ks_trainer& t, bool ta, bool tb, long long M, long long N, lon
         KT_CUDA(buf.ensure((size_t)rows * ldo * 2 * 2));
         __half* hi = buf.as<__half>();
         __half* lo = hi + rows * ldo;
-        k_split_planes<<<split16_grid(rows, cols), 256, 0, s>>>(src, rows, (int)cols, ld, hi, lo, ldo, amax);
+        ksb::launch_split_planes(src, rows, cols, ld, hi, lo, ldo, amax, s);
         ++t.launches;
         out = {hi, lo, ldo, amax};
         if (share) t.planes.emplace(key, out);
