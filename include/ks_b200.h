@@ -238,6 +238,15 @@ ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, const int64_
                                 const int32_t* truth, int64_t B, int32_t beam_width,
                                 const ks_pred* preds, int32_t n_preds, ks_host_pred_fn hook,
                                 void* user, int64_t* out_pos_matches, int64_t* out_perfect);
+/* topk_metrics over several beam widths (eval.cpp:74-152 runs one search per
+ * k): each chunk is encoded ONCE (bi-LSTM / conv encoder and the context
+ * projection) and decoded at every width, widest first; results identical to
+ * n_k ks_topk_metrics_batch calls.  out_pos_matches: n_k x T, out_perfect: n_k,
+ * both in k_values order. */
+ks_status ks_topk_metrics_multi(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                                const int32_t* truth, int64_t B, const int32_t* k_values, int32_t n_k,
+                                const ks_pred* preds, int32_t n_preds, ks_host_pred_fn hook,
+                                void* user, int64_t* out_pos_matches, int64_t* out_perfect);
 
 /* greedy_decode: out_tok B x T. */
 ks_status ks_greedy_batch(ks_engine* eng, const int32_t* tok, int64_t B, int32_t* out_tok);
@@ -302,6 +311,10 @@ ks_status ks_group_greedy_batch(ks_engine_group* g, const int32_t* tok, int64_t 
 ks_status ks_group_forward_batch(ks_engine_group* g, const int32_t* tok, const int32_t* teacher, int64_t B,
                                  double* out_dist, int32_t* out_tok, double* out_score);
 /* Counters summed over the shards. */
+ks_status ks_group_topk_metrics_multi(ks_engine_group* g, const int32_t* tok, const int64_t* desc,
+                                      const int32_t* truth, int64_t B, const int32_t* k_values, int32_t n_k,
+                                      const ks_pred* preds, int32_t n_preds, ks_host_pred_fn hook, void* user,
+                                      int64_t* out_pos_matches, int64_t* out_perfect);
 ks_status ks_group_topk_metrics_batch(ks_engine_group* g, const int32_t* tok, const int64_t* desc,
                                       const int32_t* truth, int64_t B, int32_t beam_width, const ks_pred* preds,
                                       int32_t n_preds, ks_host_pred_fn hook, void* user,

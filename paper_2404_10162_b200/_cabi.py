@@ -82,7 +82,7 @@ EXPORTS = [
     "ks_engine_destroy", "ks_engine_num_positions", "ks_engine_vocab_size",
     "ks_engine_precision", "ks_engine_last_launch_count", "ks_engine_set_chunk",
     "ks_encode_problems", "ks_beam_search_batch", "ks_greedy_batch", "ks_beam_search_device",
-    "ks_host_register", "ks_host_unregister", "ks_gemm_f16x3",
+    "ks_host_register", "ks_host_unregister",
     "ks_engine_profile_reset", "ks_engine_profile_gemm_ms", "ks_engine_profile_launches",
     "ks_engine_profile_launches_ex",
     "ks_beam_search_batch_hooked", "ks_topk_metrics_batch",
@@ -92,7 +92,8 @@ EXPORTS = [
     "ks_trainer_to_reference_layout", "ks_synthetic_descriptors", "ks_engine_synthetic_descriptors", "ks_forward_batch",
     "ks_device_count", "ks_engine_group_create", "ks_engine_group_create_from_checkpoint", "ks_engine_group_destroy",
     "ks_engine_group_size", "ks_engine_group_engine", "ks_group_beam_search_batch", "ks_group_greedy_batch",
-    "ks_group_forward_batch", "ks_group_topk_metrics_batch",
+    "ks_group_forward_batch", "ks_group_topk_metrics_batch", "ks_topk_metrics_multi",
+    "ks_group_topk_metrics_multi", "ks_gemm_f16x3",
 ]
 
 

@@ -952,30 +952,34 @@ std::vector<EvalReport> topk_metrics(const SequencePredictor& predictor, const s
         descs.push_back(test[i].descriptor);
     }
     ResolvedPreds rp = resolve(params, predicates);
+    // one device call for every k (a width-k search does not contain the width-j beams,
+    // so each k is still its own search, as eval.cpp:74-152 runs them): each chunk is
+    // encoded once and decoded at every width; the best-matching beam / any-of-k
+    // scoring stays on the device
+    const int nk = static_cast<int>(k_values.size());
+    std::vector<int32_t> ks(k_values.begin(), k_values.end());
+    std::vector<int64_t> hits((size_t)nk * (size_t)arity), perfect((size_t)nk);
+    HookCtx ctx{&params, predicates, &rp.host, descs, {}};
+    const ks_status s = ks_group_topk_metrics_multi(
+        predictor.group(), tok.data(), desc.data(), truth.data(), static_cast<int64_t>(B), ks.data(), nk,
+        rp.preds.empty() ? nullptr : rp.preds.data(), static_cast<int32_t>(rp.preds.size()),
+        rp.host.empty() ? nullptr : host_hook, &ctx, hits.data(), perfect.data());
+    if (!ctx.error.empty()) throw Error("predicate raised: " + ctx.error);
+    check(s);
     std::vector<EvalReport> reports;
-    for (int k : k_values) {
-        // one device pass per k (a width-k search does not contain the width-j beams);
-        // the best-matching beam / any-of-k scoring stays on the device
-        std::vector<int64_t> hits((size_t)arity);
-        int64_t perfect = 0;
-        HookCtx ctx{&params, predicates, &rp.host, descs, {}};
-        const ks_status s = ks_group_topk_metrics_batch(
-            predictor.group(), tok.data(), desc.data(), truth.data(), static_cast<int64_t>(B), k,
-            rp.preds.empty() ? nullptr : rp.preds.data(), static_cast<int32_t>(rp.preds.size()),
-            rp.host.empty() ? nullptr : host_hook, &ctx, hits.data(), &perfect);
-        if (!ctx.error.empty()) throw Error("predicate raised: " + ctx.error);
-        check(s);
+    for (int i = 0; i < nk; ++i) {
         EvalReport r;
         r.sample_count = static_cast<int>(B);
         r.per_param_accuracy.resize((size_t)arity);
         double sum = 0.0;
         for (int p = 0; p < arity; ++p) {
-            r.per_param_accuracy[(size_t)p] = static_cast<double>(hits[(size_t)p]) / static_cast<double>(B) * 100.0;
+            r.per_param_accuracy[(size_t)p] =
+                static_cast<double>(hits[(size_t)i * arity + p]) / static_cast<double>(B) * 100.0;
             sum += r.per_param_accuracy[(size_t)p];
         }
         r.average_accuracy = sum / arity;
-        r.perfect_prediction = 100.0 * static_cast<double>(perfect) / static_cast<double>(B);
-        r.beam_width = k;
+        r.perfect_prediction = 100.0 * static_cast<double>(perfect[(size_t)i]) / static_cast<double>(B);
+        r.beam_width = k_values[(size_t)i];
         r.constrained = !predicates.empty();
         reports.push_back(std::move(r));
     }

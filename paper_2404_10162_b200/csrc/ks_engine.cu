@@ -197,6 +197,7 @@ struct ks_engine {
     // CUDA graphs of whole single-chunk decodes, keyed by everything their kernel
     // parameters bake in (KS_GRAPHS=0 disables)
     bool use_graphs = true;
+    bool pt_valid = false;  // the workspace's P^T belongs to the last encoded chunk
     struct GraphEntry {
         std::vector<long long> key;
         cudaGraphExec_t exec = nullptr;
@@ -1045,14 +1046,18 @@ ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
 }
 
 // Decodes one chunk of C configs already resident on the device.
+// reuse_encoder: the chunk's encoder outputs (a_t, encoder state, P^T, hybrid
+// features) from the previous run_chunk on the SAME tokens are still in the
+// workspace -- decode again at another beam width without re-encoding
+// (topk_metrics over several k, eval.cpp:74-152)
 ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greedy, const int* d_tok,
                     const long long* d_desc, const PredDev& pd, int* o_tok, double* o_lp,
-                    int* o_count, int* o_status, int* o_fpred, int* o_fstep) {
+                    int* o_count, int* o_status, int* o_fpred, int* o_fstep, bool reuse_encoder = false) {
     ks_status st;
     if ((st = ensure_workspace(E, C, k))) return st;
     cudaStream_t s = E.stream;
     const bool enc_dec = E.variant == KS_VARIANT_ENC_DEC;
-    {
+    if (!reuse_encoder) {
         // small batches: 32-unit N tiles double the CTAs of every gate GEMM of the chunk
         // (the weights, P^T and every launch of a chunk use one tile width)
         const bool hyb = E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID;
@@ -1074,10 +1079,10 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     auto encA_at = [&](int dir, int pp, int lo) { return encA + (((size_t)dir * 2 + pp) * 2 + lo) * C * He; };
 
     const bool hybrid = E.variant == KS_VARIANT_HYBRID2 || E.variant == KS_VARIANT_HYBRID;
-    if (hybrid && (st = encode_hybrid(E, C, d_tok))) return st;
+    if (!reuse_encoder && hybrid && (st = encode_hybrid(E, C, d_tok))) return st;
     // ---- encoder (bi-LSTM over the 7 one-hot input steps, zero initial state)
     const int dirs = enc_dec ? 1 : 2;
-    for (int sidx = 0; sidx < (hybrid ? 0 : 7); ++sidx) {
+    for (int sidx = 0; sidx < ((hybrid || reuse_encoder) ? 0 : 7); ++sidx) {
         LstmArgs a[2];
         for (int dir = 0; dir < dirs; ++dir) {
             const int t = dir == 0 ? sidx : 6 - sidx;
@@ -1125,7 +1130,9 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     bool any_proj = false;
     for (int pos = 0, h = 1; pos < E.T; h = (int)std::min<int64_t>(k, (int64_t)h * E.vsize[(size_t)pos]), ++pos)
         any_proj = any_proj || E.proj_at(pos, h);
-    if (any_proj) {
+    if (any_proj && reuse_encoder && !E.pt_valid)
+        return set_error(KS_ERR_STATE, "encoder reuse without a context projection in the workspace");
+    if (any_proj && !reuse_encoder) {
         // context projection P[c][t] = a_t . W_ctx (the ctx rows of the post-LSTM weight),
         // one GEMM over the C*7 encoder activations; raw pre-activations, no bias / cell
         LstmArgs q{};
@@ -1151,6 +1158,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         q.pt_lo = q.pt_hi + (size_t)4 * Hd * q.ldt;
         if ((st = launch_lstm(E, q, nullptr, E.dec, nullptr, 0.0))) return st;
     }
+    if (!reuse_encoder) E.pt_valid = any_proj;
     beam_init<<<(unsigned)((C + 255) / 256), 256, 0, s>>>((int)C, E.live[0].as<unsigned char>(),
                                                           E.lp[0].as<double>(),
                                                           E.key[0].as<unsigned long long>(),
@@ -1787,6 +1795,94 @@ extern "C" ks_status ks_topk_metrics_batch(ks_engine* eng, const int32_t* tok, c
     KS_CUDA(cudaStreamSynchronize(E.stream));
     for (int p = 0; p < T; ++p) out_pos_matches[p] = (int64_t)h[(size_t)p];
     *out_perfect = (int64_t)h[(size_t)T];
+    if (E.prof) collect_profile(E);
+    return KS_OK;
+}
+
+extern "C" ks_status ks_topk_metrics_multi(ks_engine* eng, const int32_t* tok, const int64_t* desc,
+                                           const int32_t* truth, int64_t B, const int32_t* k_values, int32_t n_k,
+                                           const ks_pred* preds, int32_t n_preds, ks_host_pred_fn hook, void* user,
+                                           int64_t* out_pos_matches, int64_t* out_perfect) {
+    if (!eng) return set_error(KS_ERR_PARAMETER, "null engine");
+    if (!k_values || n_k < 1) return set_error(KS_ERR_PARAMETER, "no beam widths");
+    int kmax = 0;
+    for (int i = 0; i < n_k; ++i) {
+        if (k_values[i] < 1) return set_error(KS_ERR_PARAMETER, "beam width must be >= 1");
+        kmax = std::max(kmax, (int)k_values[i]);
+    }
+    std::lock_guard<std::mutex> lock(eng->mu);
+    ks_status st = check_common(eng, B, kmax, preds, n_preds);
+    if (st) return st;
+    if (!tok || !truth || !out_pos_matches || !out_perfect) return set_error(KS_ERR_PARAMETER, "null buffer");
+    ks_engine& E = *eng;
+    const int T = E.T;
+    for (int64_t i = 0; i < (int64_t)n_k * T; ++i) out_pos_matches[i] = 0;
+    for (int i = 0; i < n_k; ++i) out_perfect[i] = 0;
+    if (B == 0) return KS_OK;
+    for (int64_t b = 0; b < B; ++b)
+        for (int p = 0; p < T; ++p) {
+            const int v = truth[b * T + p];
+            if (v < 0 || v >= E.vsize[(size_t)p])
+                return set_error(KS_ERR_INDEX, "truth token " + std::to_string(v) + " out of range at position " +
+                                                   std::to_string(p) + " (row " + std::to_string(b) + ")");
+        }
+    for (int64_t b = 0; b < B; ++b)
+        for (int f = 0; f < 7; ++f) {
+            const int t = tok[b * 7 + f];
+            if (t < 0 || t >= E.in_sizes[(size_t)f])
+                return set_error(KS_ERR_INDEX, "input token " + std::to_string(t) + " out of range for field " +
+                                                   std::to_string(f) + " (row " + std::to_string(b) + ")");
+        }
+    PredDev pd;
+    if ((st = upload_preds(E, preds, n_preds, pd))) return st;
+    if (pd.needs_desc && !desc) return set_error(KS_ERR_PARAMETER, "divisibility predicates need descriptors");
+    pd.hook = hook;
+    pd.user = user;
+    E.launches = 0;
+    // widest first: its encoding fixes the chunk's GEMM tile width and computes the
+    // context projection every narrower width may use
+    std::vector<int> order((size_t)n_k);
+    for (int i = 0; i < n_k; ++i) order[(size_t)i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return k_values[a] > k_values[b]; });
+    const int64_t C = std::max<int64_t>(1, std::min<int64_t>(B, E.chunk));
+    if (E.otok.ensure((size_t)C * kmax * T * 4) || E.olp.ensure((size_t)C * kmax * 8) ||
+        E.ocount.ensure((size_t)C * 4) || E.ostatus.ensure((size_t)C * 4) || E.ofpred.ensure((size_t)C * 4) ||
+        E.ofstep.ensure((size_t)C * 4) || E.truth.ensure((size_t)C * T * 4) ||
+        E.evalc.ensure((size_t)n_k * (T + 1) * 8))
+        return set_error(KS_ERR_CUDA, "output allocation failed");
+    if ((st = ensure_workspace(E, C, kmax))) return st;  // no reallocation between the widths
+    KS_CUDA(cudaMemsetAsync(E.evalc.p, 0, (size_t)n_k * (T + 1) * 8, E.stream));
+    unsigned long long* cnt = E.evalc.as<unsigned long long>();
+    for (int64_t c0 = 0; c0 < B; c0 += C) {
+        const int64_t n = std::min<int64_t>(C, B - c0);
+        KS_CUDA(cudaMemcpyAsync(E.tok.p, tok + c0 * 7, (size_t)n * 7 * 4, cudaMemcpyHostToDevice, E.stream));
+        KS_CUDA(cudaMemcpyAsync(E.truth.p, truth + c0 * T, (size_t)n * T * 4, cudaMemcpyHostToDevice, E.stream));
+        const long long* ddesc = nullptr;
+        if (desc && pd.needs_desc) {
+            KS_CUDA(cudaMemcpyAsync(E.desc.p, desc + c0 * 7, (size_t)n * 7 * 8, cudaMemcpyHostToDevice, E.stream));
+            ddesc = E.desc.as<long long>();
+        }
+        for (size_t oi = 0; oi < order.size(); ++oi) {
+            const int i = order[oi];
+            const int k = k_values[i];
+            if ((st = run_chunk(E, n, c0, k, false, E.tok.as<int>(), ddesc, pd, E.otok.as<int>(), E.olp.as<double>(),
+                                E.ocount.as<int>(), E.ostatus.as<int>(), E.ofpred.as<int>(), E.ofstep.as<int>(),
+                                oi > 0)))
+                return st;
+            unsigned long long* ci = cnt + (size_t)i * (T + 1);
+            if (!launch_topk_eval(E.otok.as<int>(), E.ocount.as<int>(), E.truth.as<int>(), (int)n, k, T, ci, ci + T,
+                                  E.stream))
+                return set_error(KS_ERR_CUDA, "topk_eval launch failed");
+            E.launches++;
+        }
+    }
+    std::vector<unsigned long long> h((size_t)n_k * (T + 1));
+    KS_CUDA(cudaMemcpyAsync(h.data(), E.evalc.p, h.size() * 8, cudaMemcpyDeviceToHost, E.stream));
+    KS_CUDA(cudaStreamSynchronize(E.stream));
+    for (int i = 0; i < n_k; ++i) {
+        for (int p = 0; p < T; ++p) out_pos_matches[(size_t)i * T + p] = (int64_t)h[(size_t)i * (T + 1) + p];
+        out_perfect[i] = (int64_t)h[(size_t)i * (T + 1) + T];
+    }
     if (E.prof) collect_profile(E);
     return KS_OK;
 }

@@ -235,3 +235,36 @@ extern "C" ks_status ks_group_topk_metrics_batch(ks_engine_group* G, const int32
     for (size_t g = 0; g < n; ++g) *out_perfect += perf[g];
     return KS_OK;
 }
+
+extern "C" ks_status ks_group_topk_metrics_multi(ks_engine_group* G, const int32_t* tok, const int64_t* desc,
+                                                 const int32_t* truth, int64_t B, const int32_t* k_values,
+                                                 int32_t n_k, const ks_pred* preds, int32_t n_preds,
+                                                 ks_host_pred_fn hook, void* user, int64_t* out_pos_matches,
+                                                 int64_t* out_perfect) {
+    if (!G) return set_error(KS_ERR_PARAMETER, "null engine group");
+    if (B < 0) return set_error(KS_ERR_PARAMETER, "batch size out of range");
+    if (!out_pos_matches || !out_perfect || !k_values || n_k < 1) return set_error(KS_ERR_PARAMETER, "null buffer");
+    const int64_t T = G->T;
+    const size_t n = G->engines.size();
+    std::vector<std::vector<int64_t>> pos(n, std::vector<int64_t>(static_cast<size_t>(n_k * T), 0));
+    std::vector<std::vector<int64_t>> perf(n, std::vector<int64_t>(static_cast<size_t>(n_k), 0));
+    std::vector<HookShift> hs(n);
+    const ks_status st = for_shards(*G, B, [&](int g, int64_t lo, int64_t hi) {
+        HookShift& h = hs[static_cast<size_t>(g)];
+        h = HookShift{hook, user, lo, {}};
+        return ks_topk_metrics_multi(G->engines[static_cast<size_t>(g)], tok + lo * 7, desc ? desc + lo * 7 : nullptr,
+                                     truth + lo * T, hi - lo, k_values, n_k, preds, n_preds,
+                                     hook ? shifted_hook : nullptr, hook ? &h : nullptr,
+                                     pos[static_cast<size_t>(g)].data(), perf[static_cast<size_t>(g)].data());
+    });
+    if (st) return st;
+    for (int64_t i = 0; i < (int64_t)n_k * T; ++i) {
+        out_pos_matches[i] = 0;
+        for (size_t g = 0; g < n; ++g) out_pos_matches[i] += pos[g][static_cast<size_t>(i)];
+    }
+    for (int i = 0; i < n_k; ++i) {
+        out_perfect[i] = 0;
+        for (size_t g = 0; g < n; ++g) out_perfect[i] += perf[g][static_cast<size_t>(i)];
+    }
+    return KS_OK;
+}

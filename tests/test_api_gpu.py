@@ -231,3 +231,26 @@ def test_concurrent_calls_on_one_engine(ks, params, oracle):
     assert not errs
     for o in out:
         assert [[e["params"] for e in r] for r in o] == [[e["params"] for e in r] for r in ref]
+
+
+@pytest.mark.parametrize("stem", ["attn_small_trained", "hybrid2_small_trained", "tiny_encdec_s3423"])
+def test_topk_metrics_several_widths_equal_separate_calls(ks, stem):
+    """topk_metrics over several k encodes each chunk once and decodes it at
+    every width, widest first (ks_topk_metrics_multi); the reports must equal
+    one call per k, in the caller's k order -- for the attn (context
+    projection reused), hybrid-2 (conv features reused) and enc-dec variants."""
+    path = golden_path(stem + ".ckpt")
+    p = ks.load_checkpoint(path)
+    o = OracleModel(path)
+    rng = np.random.default_rng(17)
+    samples = []
+    for _ in range(300):
+        d = {f: int(o.input_values[i][rng.integers(len(o.input_values[i]))]) for i, f in enumerate(FIELDS)}
+        truth = {n: o.values[i][int(rng.integers(len(o.values[i])))] for i, n in enumerate(o.names)}
+        samples.append(ks.Sample(d, truth, p.spec.name))
+    widths = [1, 5, 3, 8]
+    together = ks.topk_metrics(p, samples, widths)
+    apart = [ks.topk_metrics(p, samples, [k])[0] for k in widths]
+    assert [r["beam_width"] for r in together] == widths
+    for a, b in zip(together, apart):
+        assert a == b
