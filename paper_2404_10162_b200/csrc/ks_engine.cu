@@ -1104,8 +1104,21 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
                 p.h_out = act + (size_t)t * NA2 + dir * E.NA;
                 p.ldh = act_ld;
             }
-            p.A_hi = encA_at(dir, (sidx + 1) & 1, 0);
-            p.A_lo = encA_at(dir, (sidx + 1) & 1, 1);
+            // attn / attn-2 with the context projection: the encoder's split h goes
+            // straight into the a_t operand planes of the projection GEMM (actA rows
+            // b*7 + t, columns dir*NA..), and the next step reads its A operand there
+            // (row stride 7*NA2) -- no separate split pass over a_t
+            const bool to_actA = !enc_dec && split && E.ctxproj;
+            __half* aAhi = to_actA ? E.actA.as<__half>() : nullptr;
+            __half* aAlo = to_actA ? aAhi + (size_t)C * 7 * NA2 : nullptr;
+            if (to_actA) {
+                p.A_hi = aAhi + (size_t)tprev * NA2 + dir * E.NA;
+                p.A_lo = aAlo + (size_t)tprev * NA2 + dir * E.NA;
+                p.ldah = act_ld;
+            } else {
+                p.A_hi = encA_at(dir, (sidx + 1) & 1, 0);
+                p.A_lo = encA_at(dir, (sidx + 1) & 1, 1);
+            }
             p.W = E.enc[dir].W.as<float>();
             p.G = E.enc[dir].G.as<float>();
             p.slot_ptr = d_tok + t;
@@ -1116,7 +1129,12 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.parent = nullptr;
             p.c_out = encc_at(dir, sidx & 1);
             p.ldc = He;
-            if (split) {
+            if (split && to_actA) {
+                p.hA_hi = aAhi + (size_t)t * NA2 + dir * E.NA;
+                p.hA_lo = aAlo + (size_t)t * NA2 + dir * E.NA;
+                p.ldha = act_ld;
+                p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
+            } else if (split) {
                 p.hA_hi = encA_at(dir, sidx & 1, 0);
                 p.hA_lo = encA_at(dir, sidx & 1, 1);
                 p.ldha = He;
@@ -1141,11 +1159,8 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         q.K = NA2;
         q.A = act;
         q.lda = NA2;
-        __half* ahi = E.actA.as<__half>();
+        __half* ahi = E.actA.as<__half>();  // written by the encoder steps (to_actA above)
         __half* alo = ahi + (size_t)C * 7 * NA2;
-        if (!launch_split_rows(act, (long long)C * 7 * NA2, ahi, alo, E.precision == KS_PREC_F16X3 ? 1 : 2, s))
-            return set_error(KS_ERR_CUDA, "split_rows launch failed");
-        E.launches++;
         q.A_hi = ahi;
         q.A_lo = alo;
         q.W = E.dec.W.as<float>();
