@@ -664,6 +664,8 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
             }();
             pr.p.drop_pass = drop;
         }
+        // the fan-out epilogue writes only h and c of the children
+        if (a.fan > 1 && (a.h_out2 != nullptr || a.hA_hi != nullptr || a.raw)) return false;
         if (a.kb_alpha > 0 && (CG == 2 ? a.alpha_tile != 2 * TC_BM : (a.alpha_tile < 1 || a.alpha_tile > TC_BM)))
             return false;  // operand laid out for another tile
         const int tr = (CG == 1 && a.kb_alpha > 0) ? a.alpha_tile : TC_BM;

@@ -888,10 +888,6 @@ ks_status gemm_simt(ks_trainer& t, bool ta, bool tb, long long M, long long N, l
 
 
 constexpr int kScalSlots = 4096;  // F16X3 per-step max|x| / alpha slots
-inline unsigned split16_grid(long long rows, long long cols) {
-    const long long items = rows * ((cols + 3) / 4);
-    return (unsigned)std::max<long long>(1, std::min<long long>((items + 255) / 256, 148LL * 16));
-}
 
 // Row-major C[M x N] = op(A) op(B) + beta C on the trainer's stream.
 // F16X3 (default): both operands split into fp16 hi/lo planes at power-of-two
