@@ -594,6 +594,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.pair = tp && tp[0] == '1' && E.tc_units == 64;
         const char* kg = std::getenv("KS_GRAPHS");
         E.use_graphs = !(kg && kg[0] == '0');
+        const char* kc = std::getenv("KS_CHUNK");
+        if (kc && std::atoll(kc) > 0) E.chunk = std::atoll(kc);
     }
     cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device);
     *out = eng.release();

@@ -38,6 +38,9 @@ struct TcProblem {
     int n_tiles;
     int k_blocks;
     int tile_begin;  // first global tile index of this problem
+    int tma_out;     // h / c of whole 32-row warp slices leave through bulk tensor stores
+    alignas(64) CUtensorMap mh;  // fp32 [M][H] views of h_out / c_out, box 32 rows x 8 units
+    alignas(64) CUtensorMap mc;
 };
 
 // alpha-block mode: K-blocks of one tile.  The B operand's P^T columns start at
@@ -87,7 +90,9 @@ struct TcCfg {
     static constexpr int ACC_COLS = BN;                        // fp32 TMEM columns per accumulator
     static constexpr int ACC_STAGES = 512 / ACC_COLS >= 2 ? 2 : 1;
     static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+    // output staging for the bulk h / c stores: 8 epilogue warps x 2 buffers x (h, c) x 32 rows x 8 units
+    static constexpr int OUT_STAGE = 8 * 2 * 2 * 32 * 8 * 4;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */ + OUT_STAGE;
     // instruction descriptor: fp32 accumulate (bits 4-5 = 1), A/B fp16 (0) or bf16 (1) at
     // bits 7-9 / 10-12, both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
     static constexpr uint32_t IDESC = (1u << 4) | ((SPLIT ? 0u : 1u) << 7) | ((SPLIT ? 0u : 1u) << 10) |
@@ -123,7 +128,8 @@ __device__ __forceinline__ void lstm_cell_fast(float zi, float zf, float zo, flo
 template <int UNITS, bool SPLIT, int CG>
 __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars, uint32_t tmem_base, int acc,
                                                uint32_t acc_phase, int row0, int TRp, int nt, int q, int half,
-                                               int lane, int tfull, int tempty, int acc_cols, bool leader) {
+                                               int lane, int tfull, int tempty, int acc_cols, bool leader,
+                                               const TcProblem& pr, float* stg, int& stg_buf) {
     constexpr int HU = UNITS / 2;
     constexpr int NCH = HU / 8;
     const int tq = lane >> 2, tcol = 2 * (lane & 3);
@@ -138,7 +144,9 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
         crows[i] = valid[i] ? (p.parent ? p.parent[rows[i]] : rows[i]) : -1;
     }
     const bool have_cprev = p.c_prev != nullptr;
-    // G[slot] (4 gates) and c_prev of the chunk's 2 units per row, prefetched a chunk ahead
+    // bulk stores only for warp slices whose 32 rows all belong to this tile
+    const bool bulk = pr.tma_out && row0 + q * 32 + 31 < p.M && (CG == 2 || q * 32 + 31 < TRp);
+    // G[slot] and c_prev of the chunk's 2 units per row, prefetched a chunk ahead
     float2 gn[4][4], cn[4];
     auto load_bc = [&](int c, float2 (&gx)[4][4], float2 (&cx)[4]) {
         const int u0 = nt * UNITS + half * HU + c * 8 + tcol;
@@ -201,16 +209,40 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
             lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[i].x, cv[i][0], hv[i][0]);
             lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[i].y, cv[i][1], hv[i][1]);
         }
+        if (bulk) {
+            // the warp's 32 x 8 slice of h and c through shared memory and two bulk tensor
+            // stores (one engine transaction per slice instead of 64 row-segment stores)
+            float* sh = stg + stg_buf * 512;
+            float* scb = sh + 256;
+            if (lane == 0) tc::bulk_wait_read<1>();  // the group that last read this buffer is done
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int lr = 16 * (i >> 1) + tq + 8 * (i & 1);
+                *reinterpret_cast<float2*>(sh + lr * 8 + tcol) = make_float2(hv[i][0], hv[i][1]);
+                *reinterpret_cast<float2*>(scb + lr * 8 + tcol) = make_float2(cv[i][0], cv[i][1]);
+            }
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tc::tma_store_2d(&pr.mh, tc::smem_u32(sh), nt * UNITS + uc, row0 + q * 32);
+                tc::tma_store_2d(&pr.mc, tc::smem_u32(scb), nt * UNITS + uc, row0 + q * 32);
+                tc::bulk_commit();
+            }
+            stg_buf ^= 1;
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             if (!valid[i]) continue;
             const long long r = rows[i];
-            // streaming (evict-first) stores: h and c are re-read once, by the next kernels,
-            // and would otherwise push the GEMM's reused operands (W, P^T) out of L2
-            __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[i][0], hv[i][1]));
+            if (!bulk) {
+                // streaming (evict-first) stores: h and c are re-read once, by the next kernels,
+                // and would otherwise push the GEMM's reused operands (W, P^T) out of L2
+                __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[i][0], hv[i][1]));
+                __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[i][0], cv[i][1]));
+            }
             if (p.h_out2 != nullptr)
                 __stcs(reinterpret_cast<float2*>(p.h_out2 + r * p.ldh2 + u0), make_float2(hv[i][0], hv[i][1]));
-            __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[i][0], cv[i][1]));
             if (p.hA_hi != nullptr && p.ha_bf16) {
                 *reinterpret_cast<__nv_bfloat162*>(p.hA_hi + r * p.ldha + u0) =
                     __floats2bfloat162_rn(hv[i][0], hv[i][1]);
@@ -498,6 +530,8 @@ __global__ void __launch_bounds__(384, 1)
         const int q = warp & 3;
         const int half = (warp - 4) >> 2;
         constexpr int HU = UNITS / 2;
+        float* stg = reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES + 256) + (warp - 4) * 1024;
+        int stg_buf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = cid; t < P.total_tiles; t += ncl) {
@@ -517,7 +551,8 @@ __global__ void __launch_bounds__(384, 1)
                                                    2 * S, 2 * S + AS, Cfg::ACC_COLS, leader);
                 else
                     epilogue_cells<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half,
-                                                     lane, 2 * S, 2 * S + AS, Cfg::ACC_COLS, leader);
+                                                     lane, 2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, pr, stg,
+                                                     stg_buf);
                 if (++acc == AS) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -574,6 +609,7 @@ __global__ void __launch_bounds__(384, 1)
                 acc_phase ^= 1;
             }
         }
+        if (lane == 0) tc::bulk_wait_all();  // this warp's bulk stores are complete
     }
     __syncthreads();
     if (CG == 2) tc::cluster_sync();  // no CTA leaves while its peer may still signal it
@@ -622,6 +658,20 @@ bool tc_make_map(CUtensorMap* m, const void* base, long long rows, long long col
 
 namespace {
 
+// fp32 [rows][cols] output view (row stride ld elements), box 32 rows x 8 columns,
+// no swizzle: the bulk h / c stores of the cell epilogue
+bool make_out_map(CUtensorMap* m, const float* base, long long rows, long long cols, long long ld) {
+    EncodeTiledFn fn = tc_encode_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || (ld & 3)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {8, 32};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, long long row_stride_elems,
               int box_rows) {
     return tc_make_map(m, base, rows, cols, row_stride_elems, box_rows);
@@ -666,6 +716,17 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         }
         // the fan-out epilogue writes only h and c of the children
         if (a.fan > 1 && (a.h_out2 != nullptr || a.hA_hi != nullptr || a.raw)) return false;
+        {
+            static const bool bulk_out = [] {
+                const char* e = std::getenv("KS_BULK_OUT");
+                return !(e && e[0] == '0');
+            }();
+            pr.tma_out = bulk_out && !a.raw && a.fan <= 1 && a.h_out && a.c_out &&
+                         make_out_map(&pr.mh, a.h_out, a.M, a.H, a.ldh) &&
+                         make_out_map(&pr.mc, a.c_out, a.M, a.H, a.ldc)
+                             ? 1
+                             : 0;
+        }
         if (a.kb_alpha > 0 && (CG == 2 ? a.alpha_tile != 2 * TC_BM : (a.alpha_tile < 1 || a.alpha_tile > TC_BM)))
             return false;  // operand laid out for another tile
         const int tr = (CG == 1 && a.kb_alpha > 0) ? a.alpha_tile : TC_BM;
