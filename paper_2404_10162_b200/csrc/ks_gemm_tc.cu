@@ -264,7 +264,8 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
 template <int UNITS, bool SPLIT, int CG>
 __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, uint32_t tmem_base, int acc,
                                              uint32_t acc_phase, int row0, int TRp, int nt, int q, int half,
-                                             int lane, int tfull, int tempty, int acc_cols, bool leader) {
+                                             int lane, int tfull, int tempty, int acc_cols, bool leader,
+                                             const TcProblem& pr, float* stg, int& stg_buf) {
     constexpr int HU = UNITS / 2;
     constexpr int NCH = HU / 8;
     const int tq = lane >> 2, tcol = 2 * (lane & 3);
@@ -278,6 +279,7 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
         valid[i] = rows[i] < p.M && (CG == 2 || lr < TRp);
     }
     const bool have_cprev = p.c_prev != nullptr;
+    const bool bulk = pr.tma_out && row0 + q * 32 + 31 < p.M && (CG == 2 || q * 32 + 31 < TRp);
     float2 cn[4];
     auto load_c = [&](int c, float2 (&cx)[4]) {
         const int u0 = nt * UNITS + half * HU + c * 8 + tcol;
@@ -340,6 +342,29 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
                     z[gt] = __ffma2_rn(make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]), sc2, gz[i][gt]);
                 lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[i].x, cv[i][0], hv[i][0]);
                 lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[i].y, cv[i][1], hv[i][1]);
+            }
+            if (bulk) {
+                // child f of the warp's 32 parents: rows (row0 + q*32 + j) * fan + f, one box
+                // of the [parents][fan][H] view per array
+                float* sh = stg + stg_buf * 512;
+                float* scb = sh + 256;
+                if (lane == 0) tc::bulk_wait_read<1>();
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int lr = 16 * (i >> 1) + tq + 8 * (i & 1);
+                    *reinterpret_cast<float2*>(sh + lr * 8 + tcol) = make_float2(hv[i][0], hv[i][1]);
+                    *reinterpret_cast<float2*>(scb + lr * 8 + tcol) = make_float2(cv[i][0], cv[i][1]);
+                }
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tc::tma_store_3d(&pr.mh, tc::smem_u32(sh), nt * UNITS + uc, f, row0 + q * 32);
+                    tc::tma_store_3d(&pr.mc, tc::smem_u32(scb), nt * UNITS + uc, f, row0 + q * 32);
+                    tc::bulk_commit();
+                }
+                stg_buf ^= 1;
+                continue;
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -548,7 +573,7 @@ __global__ void __launch_bounds__(384, 1)
                 // writes whole 32-byte row segments (half the L1 wavefronts of row-per-lane)
                 if (p.fan > 1)
                     epilogue_fan<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half, lane,
-                                                   2 * S, 2 * S + AS, Cfg::ACC_COLS, leader);
+                                                   2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, pr, stg, stg_buf);
                 else
                     epilogue_cells<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half,
                                                      lane, 2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, pr, stg,
@@ -660,16 +685,30 @@ namespace {
 
 // fp32 [rows][cols] output view (row stride ld elements), box 32 rows x 8 columns,
 // no swizzle: the bulk h / c stores of the cell epilogue
-bool make_out_map(CUtensorMap* m, const float* base, long long rows, long long cols, long long ld) {
+// fan > 1: a 3D [rows][fan][cols] view of the children's rows (child f of parent r is
+// row r*fan + f), box 32 parents x 1 child x 8 columns
+bool make_out_map(CUtensorMap* m, const float* base, long long rows, int fan, long long cols, long long ld) {
     EncodeTiledFn fn = tc_encode_fn();
     if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || (ld & 3)) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    cuuint32_t box[2] = {8, 32};
-    cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    CUresult r;
+    if (fan <= 1) {
+        cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+        cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+        cuuint32_t box[2] = {8, 32};
+        cuuint32_t estr[2] = {1, 1};
+        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)fan, (cuuint64_t)rows};
+        cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)ld * 4 * fan};
+        cuuint32_t box[3] = {8, 1, 32};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    return r == CUDA_SUCCESS;
 }
 
 bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, long long row_stride_elems,
@@ -721,9 +760,10 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
                 const char* e = std::getenv("KS_BULK_OUT");
                 return !(e && e[0] == '0');
             }();
-            pr.tma_out = bulk_out && !a.raw && a.fan <= 1 && a.h_out && a.c_out &&
-                         make_out_map(&pr.mh, a.h_out, a.M, a.H, a.ldh) &&
-                         make_out_map(&pr.mc, a.c_out, a.M, a.H, a.ldc)
+            const int fan = a.fan > 1 ? a.fan : 1;
+            pr.tma_out = bulk_out && !a.raw && a.h_out && a.c_out &&
+                         make_out_map(&pr.mh, a.h_out, a.M, fan, a.H, a.ldh) &&
+                         make_out_map(&pr.mc, a.c_out, a.M, fan, a.H, a.ldc)
                              ? 1
                              : 0;
         }
