@@ -239,37 +239,89 @@ __device__ __forceinline__ void store_planes(float v, float sc, __half* hi, __ha
     lo[i] = __float2half_rn(x - __half2float(h));
 }
 
+// four consecutive units of one row per thread (128-bit loads / stores along the
+// units) when H and the row strides allow it, else one unit per thread
+template <int VEC>
 __global__ void k_cell_fwd(CellFwd a) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= (long long)a.M * a.H) return;
-    const int r = (int)(tid / a.H), j = (int)(tid % a.H);
+    const int HV = a.H / VEC;
+    if (tid >= (long long)a.M * HV) return;
+    const int r = (int)(tid / HV), j0 = (int)(tid % HV) * VEC;
     const int H = a.H;
     const float* bias = a.Ws + (long long)a.S * 4 * H;
     const int slot = a.slot ? a.slot[r] : -1;
     const float val = a.val ? a.val[r] : 1.0f;
-    float z[4];
     float* Zr = a.Z + (long long)r * 4 * H;
+    float z[4][VEC];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-        float v = a.zero_z ? 0.0f : Zr[g * H + j];
-        if (slot >= 0) v += val * a.Ws[(long long)slot * 4 * H + g * H + j];
-        z[g] = v + bias[g * H + j];
+        float zz[VEC], bb[VEC], ww[VEC];
+        if (VEC == 4) {
+            const float4 zv = a.zero_z ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(Zr + g * H + j0);
+            const float4 bv = *reinterpret_cast<const float4*>(bias + g * H + j0);
+            const float4 wv = slot >= 0 ? *reinterpret_cast<const float4*>(a.Ws + (long long)slot * 4 * H + g * H + j0)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            zz[0] = zv.x; zz[1] = zv.y; zz[2] = zv.z; zz[3] = zv.w;
+            bb[0] = bv.x; bb[1] = bv.y; bb[2] = bv.z; bb[3] = bv.w;
+            ww[0] = wv.x; ww[1] = wv.y; ww[2] = wv.z; ww[3] = wv.w;
+        } else {
+            zz[0] = a.zero_z ? 0.0f : Zr[g * H + j0];
+            bb[0] = bias[g * H + j0];
+            ww[0] = slot >= 0 ? a.Ws[(long long)slot * 4 * H + g * H + j0] : 0.0f;
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+            float v = zz[e];
+            if (slot >= 0) v += val * ww[e];
+            z[g][e] = v + bb[e];
+        }
     }
-    const float i = sigm(z[0]), f = sigm(z[1]), o = sigm(z[2]), g = tanhf(z[3]);
-    const float cp = a.c_prev ? a.c_prev[(long long)r * H + j] : 0.0f;
-    const float c = f * cp + i * g;
-    const float h = o * tanhf(c);
-    Zr[j] = i;
-    Zr[H + j] = f;
-    Zr[2 * H + j] = o;
-    Zr[3 * H + j] = g;
-    a.c_out[(long long)r * H + j] = c;
-    a.h_out[(long long)r * a.ldh + j] = h;
-    if (a.h_out2) {
-        const float h2 = a.mr ? h * a.mr[(long long)r * H + j] : h;
-        a.h_out2[(long long)r * a.ldh2 + j] = h2;
-        if (a.q_hi) store_planes(h2, exp2f((float)ksb::f16_scale_exp(*a.qamax)), a.q_hi, a.q_lo, (long long)r * a.ldq + j);
+    float act[4][VEC], c[VEC], h[VEC], h2[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+        const int j = j0 + e;
+        const float i = sigm(z[0][e]), f = sigm(z[1][e]), o = sigm(z[2][e]), g = tanhf(z[3][e]);
+        const float cp = a.c_prev ? a.c_prev[(long long)r * H + j] : 0.0f;
+        c[e] = f * cp + i * g;
+        h[e] = o * tanhf(c[e]);
+        act[0][e] = i;
+        act[1][e] = f;
+        act[2][e] = o;
+        act[3][e] = g;
+        h2[e] = a.mr ? h[e] * a.mr[(long long)r * H + j] : h[e];
     }
+    if (VEC == 4) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+            *reinterpret_cast<float4*>(Zr + g * H + j0) = make_float4(act[g][0], act[g][1], act[g][2], act[g][3]);
+        *reinterpret_cast<float4*>(a.c_out + (long long)r * H + j0) = make_float4(c[0], c[1], c[2], c[3]);
+        *reinterpret_cast<float4*>(a.h_out + (long long)r * a.ldh + j0) = make_float4(h[0], h[1], h[2], h[3]);
+        if (a.h_out2)
+            *reinterpret_cast<float4*>(a.h_out2 + (long long)r * a.ldh2 + j0) = make_float4(h2[0], h2[1], h2[2], h2[3]);
+    } else {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) Zr[g * H + j0] = act[g][0];
+        a.c_out[(long long)r * H + j0] = c[0];
+        a.h_out[(long long)r * a.ldh + j0] = h[0];
+        if (a.h_out2) a.h_out2[(long long)r * a.ldh2 + j0] = h2[0];
+    }
+    if (a.h_out2 && a.q_hi) {
+        const float qs = exp2f((float)ksb::f16_scale_exp(*a.qamax));
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) store_planes(h2[e], qs, a.q_hi, a.q_lo, (long long)r * a.ldq + j0 + e);
+    }
+}
+
+bool cell_fwd_vec_ok(const CellFwd& c) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return c.H % 4 == 0 && c.ldh % 4 == 0 && (!c.h_out2 || (c.ldh2 % 4 == 0 && al(c.h_out2))) && al(c.Z) &&
+           al(c.Ws) && al(c.c_out) && al(c.h_out);
+}
+void launch_cell_fwd(const CellFwd& c, cudaStream_t s) {
+    if (cell_fwd_vec_ok(c))
+        k_cell_fwd<4><<<(unsigned)(((long long)c.M * (c.H / 4) + 255) / 256), 256, 0, s>>>(c);
+    else
+        k_cell_fwd<1><<<(unsigned)(((long long)c.M * c.H + 255) / 256), 256, 0, s>>>(c);
 }
 
 // Fused LSTM cell backward: dh = dh1 + dh2 (* mask2); writes dZ (pre-activation
@@ -584,10 +636,14 @@ __global__ void k_head(HeadArgs a) {
     extern __shared__ float sh[];
     const int warps = blockDim.x >> 5;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* Wsm = sh;                          // ns * V
-    float* hrow = sh + a.ns * a.V + w * (a.ns + 32);
+    // W rows padded to V + 1 floats: lanes read rows j = lane + 32 i, so an odd row
+    // stride keeps the 32 reads of a step in 32 different banks (stride V was a
+    // V-way conflict)
+    const int VS = a.V + 1;
+    float* Wsm = sh;                          // ns * (V + 1)
+    float* hrow = sh + a.ns * VS + w * (a.ns + 32);
     float* dsm = hrow + a.ns;                 // this warp's dlogits (32)
-    for (int i = threadIdx.x; i < a.ns * a.V; i += blockDim.x) Wsm[i] = a.W[i];
+    for (int i = threadIdx.x; i < a.ns * a.V; i += blockDim.x) Wsm[(i / a.V) * VS + i % a.V] = a.W[i];
     __syncthreads();
     // persistent: the head weights are staged once per block, warps loop over rows
     for (long long r = (long long)blockIdx.x * warps + w; r < a.M; r += (long long)gridDim.x * warps) {
@@ -596,7 +652,7 @@ __global__ void k_head(HeadArgs a) {
         float lg = 0.0f;  // lane v holds logit v
         for (int v = 0; v < a.V; ++v) {
             float part = 0.0f;
-            for (int j = lane; j < a.ns; j += 32) part += hrow[j] * Wsm[j * a.V + v];
+            for (int j = lane; j < a.ns; j += 32) part += hrow[j] * Wsm[j * VS + v];
             for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
             if (lane == v) lg = part + a.b[v];
         }
@@ -624,7 +680,7 @@ __global__ void k_head(HeadArgs a) {
             __syncwarp();
             for (int j = lane; j < a.ns; j += 32) {
                 float v = 0.0f;
-                for (int q = 0; q < a.V; ++q) v += dsm[q] * Wsm[j * a.V + q];
+                for (int q = 0; q < a.V; ++q) v += dsm[q] * Wsm[j * VS + q];
                 a.dh[r * a.ns + j] = v;
             }
         }
@@ -1173,7 +1229,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
                     }
                 }
             }
-            k_cell_fwd<<<blocks(m * H, 256), 256, 0, s>>>(c);
+            launch_cell_fwd(c, s);
             ++t.launches;
         }
     }
@@ -1254,7 +1310,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
             c.qamax = act_amax;
         }
         c.mr = mr;
-        k_cell_fwd<<<blocks(m * Hd, 256), 256, 0, s>>>(c);
+        launch_cell_fwd(c, s);
         ++t.launches;
         // head + cross entropy
         HeadArgs ha{};
@@ -1272,7 +1328,7 @@ ks_status run_batch(ks_trainer& t, int M, const int* d_tok, const int* d_tgt, co
         ha.dlog = t.dlog.as<float>() + (long long)p * m * t.vmax;
         ha.dh = grads ? t.DHh.as<float>() + (long long)p * m * Hd : nullptr;
         const int hw = 8;
-        const size_t smem = ((size_t)Hd * ha.V + (size_t)hw * (Hd + 32)) * 4;
+        const size_t smem = ((size_t)Hd * (ha.V + 1) + (size_t)hw * (Hd + 32)) * 4;
         if (smem > 200 * 1024) return set_error(KS_ERR_UNSUPPORTED, "head too large for the head kernel");
         // function attributes are per device: each trainer sets it on its own device
         if (smem > 48 * 1024 && smem > t.head_attr) {
