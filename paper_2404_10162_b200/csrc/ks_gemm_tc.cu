@@ -187,14 +187,6 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
                     tc::mbar_arrive(tc::smem_u32(&bars[tempty + acc]));
             }
         }
-        float2 gb[4][4], cp[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            cp[i] = cn[i];
-#pragma unroll
-            for (int gt = 0; gt < 4; ++gt) gb[i][gt] = gn[i][gt];
-        }
-        if (c + 1 < NCH) load_bc(c + 1, gn, cn);
         const int u0 = nt * UNITS + uc + tcol;
         // the 8 cells of the chunk (4 rows x 2 units) computed unconditionally and
         // interleaved (independent dependency chains), stores predicated per row
@@ -205,10 +197,13 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
             float2 z[4];
 #pragma unroll
             for (int gt = 0; gt < 4; ++gt)
-                z[gt] = __ffma2_rn(make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]), sc2, gb[i][gt]);
-            lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[i].x, cv[i][0], hv[i][0]);
-            lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[i].y, cv[i][1], hv[i][1]);
+                z[gt] = __ffma2_rn(make_float2(v[g][gt][2 * j], v[g][gt][2 * j + 1]), sc2, gn[i][gt]);
+            lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cn[i].x, cv[i][0], hv[i][0]);
+            lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cn[i].y, cv[i][1], hv[i][1]);
         }
+        // the next chunk's G[slot] / c_prev, in flight during this chunk's stores and the
+        // next chunk's TMEM loads (one register set: these loads reuse gn / cn)
+        if (c + 1 < NCH) load_bc(c + 1, gn, cn);
         if (bulk) {
             // the warp's 32 x 8 slice of h and c through shared memory and two bulk tensor
             // stores (one engine transaction per slice instead of 64 row-segment stores)
