@@ -605,8 +605,37 @@ __global__ void __launch_bounds__(384, 1)
                             tc::mbar_arrive(tc::smem_u32(&bars[2 * S + AS + acc]));
                     }
                 }
-                if (!valid) continue;
                 const float sc = SPLIT ? kSplitUnscale : 1.0f;
+                if (SPLIT && pr.tma_out) {
+                    // P^T through shared memory: per gate block, the warp's 32 rows x 8
+                    // columns of each plane, one bulk tensor store into the [4H][7C] view
+                    __half* sp = reinterpret_cast<__half*>(stg);  // [gate][plane][8 n][32 rows]
+                    if (lane == 0) tc::bulk_wait_read<0>();      // the previous chunk's stores read it
+                    __syncwarp();
+#pragma unroll
+                    for (int gt = 0; gt < 4; ++gt) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            __half hi, lo;
+                            split_f16s(g[gt][j] * sc, kPScale, hi, lo);
+                            sp[((gt * 2 + 0) * 8 + j) * 32 + lane] = hi;
+                            sp[((gt * 2 + 1) * 8 + j) * 32 + lane] = lo;
+                        }
+                    }
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int gt = 0; gt < 4; ++gt) {
+                            const int n0 = nt * Cfg::BN + gt * UNITS + uc;
+                            tc::tma_store_2d(&pr.mh, tc::smem_u32(sp + (gt * 2 + 0) * 256), row0 + q * 32, n0);
+                            tc::tma_store_2d(&pr.mc, tc::smem_u32(sp + (gt * 2 + 1) * 256), row0 + q * 32, n0);
+                        }
+                        tc::bulk_commit();
+                    }
+                    continue;
+                }
+                if (!valid) continue;
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt) {
 #pragma unroll
@@ -706,6 +735,19 @@ bool make_out_map(CUtensorMap* m, const float* base, long long rows, int fan, lo
     return r == CUDA_SUCCESS;
 }
 
+// fp16 [n][rows] transposed P planes (row stride ld elements): box 32 rows x 8 n
+bool make_pt_out_map(CUtensorMap* m, const __half* base, long long rows, long long n, long long ld) {
+    EncodeTiledFn fn = tc_encode_fn();
+    if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15) || (ld & 7)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {32, 8};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols, long long row_stride_elems,
               int box_rows) {
     return tc_make_map(m, base, rows, cols, row_stride_elems, box_rows);
@@ -756,11 +798,17 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
                 return !(e && e[0] == '0');
             }();
             const int fan = a.fan > 1 ? a.fan : 1;
-            pr.tma_out = bulk_out && !a.raw && a.h_out && a.c_out &&
-                         make_out_map(&pr.mh, a.h_out, a.M, fan, a.H, a.ldh) &&
-                         make_out_map(&pr.mc, a.c_out, a.M, fan, a.H, a.ldc)
-                             ? 1
-                             : 0;
+            if (a.raw)  // P^T planes [4H][ldt] fp16: box 32 rows (inner) x 8 gate columns
+                pr.tma_out = bulk_out && SPLIT && CG == 1 && make_pt_out_map(&pr.mh, a.pt_hi, a.M, 4LL * a.H, a.ldt) &&
+                                     make_pt_out_map(&pr.mc, a.pt_lo, a.M, 4LL * a.H, a.ldt)
+                                 ? 1
+                                 : 0;
+            else
+                pr.tma_out = bulk_out && a.h_out && a.c_out &&
+                                     make_out_map(&pr.mh, a.h_out, a.M, fan, a.H, a.ldh) &&
+                                     make_out_map(&pr.mc, a.c_out, a.M, fan, a.H, a.ldc)
+                                 ? 1
+                                 : 0;
         }
         if (a.kb_alpha > 0 && (CG == 2 ? a.alpha_tile != 2 * TC_BM : (a.alpha_tile < 1 || a.alpha_tile > TC_BM)))
             return false;  // operand laid out for another tile
