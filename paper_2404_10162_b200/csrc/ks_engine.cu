@@ -198,6 +198,11 @@ struct ks_engine {
     // parameters bake in (KS_GRAPHS=0 disables)
     bool use_graphs = true;
     bool pt_valid = false;  // the workspace's P^T belongs to the last encoded chunk
+    // launches without an alpha block (encoder, context projection, position 0) run on
+    // CTA pairs (M = 256 tcgen05.mma.cta_group::2: half the B operand traffic per SM);
+    // alpha-block positions keep single-CTA tiles (a 256-row tile would double the
+    // alpha columns) and so does the epilogue-bound position-1 fan-out
+    bool pair_auto = true;
     struct GraphEntry {
         std::vector<long long> key;
         cudaGraphExec_t exec = nullptr;
@@ -594,6 +599,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.pair = tp && tp[0] == '1' && E.tc_units == 64;
         const char* kg = std::getenv("KS_GRAPHS");
         E.use_graphs = !(kg && kg[0] == '0');
+        const char* pr = std::getenv("KS_TC_PAIR_AUTO");
+        E.pair_auto = !(pr && pr[0] == '0');
         const char* kc = std::getenv("KS_CHUNK");
         if (kc && std::atoll(kc) > 0) E.chunk = std::atoll(kc);
     }
@@ -866,7 +873,9 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
         auto whi = [&](DevLstm& L) { return (u32 ? L.Whi32 : L.Whi).as<__half>(); };
         auto wlo = [&](DevLstm& L) { return (u32 ? L.Wlo32 : L.Wlo).as<__half>(); };
         done = launch_lstm_tc(a0, a1, E.precision, whi(L0), wlo(L0), L1 ? whi(*L1) : nullptr,
-                              L1 ? wlo(*L1) : nullptr, E.stream, &n, E.units_now, E.pair_now());
+                              L1 ? wlo(*L1) : nullptr, E.stream, &n, E.units_now,
+                              E.pair_now() || (E.pair_auto && E.units_now == 64 && a0.kb_alpha == 0 &&
+                                               a0.fan <= 1 && (!a1 || a1->kb_alpha == 0)));
         if (!done) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
     }
     if (!done && a0.K == 0 && launch_lstm_k0(a0, a1, E.num_sms, E.stream)) {

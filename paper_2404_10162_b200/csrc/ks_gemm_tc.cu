@@ -799,7 +799,7 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
             }();
             const int fan = a.fan > 1 ? a.fan : 1;
             if (a.raw)  // P^T planes [4H][ldt] fp16: box 32 rows (inner) x 8 gate columns
-                pr.tma_out = bulk_out && SPLIT && CG == 1 && make_pt_out_map(&pr.mh, a.pt_hi, a.M, 4LL * a.H, a.ldt) &&
+                pr.tma_out = bulk_out && SPLIT && make_pt_out_map(&pr.mh, a.pt_hi, a.M, 4LL * a.H, a.ldt) &&
                                      make_pt_out_map(&pr.mc, a.pt_lo, a.M, 4LL * a.H, a.ldt)
                                  ? 1
                                  : 0;
