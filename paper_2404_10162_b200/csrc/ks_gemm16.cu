@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ks_common.cuh"
 #include "ks_tc.cuh"
@@ -48,10 +49,10 @@ namespace {
 constexpr int G_BM = 128;
 constexpr int G_BK = kTcBK;  // 64 fp16 = one 128-byte swizzled row
 
-template <int BN>
+template <int BN, int CG>
 struct GCfg {
-    static constexpr int A_BYTES = G_BM * G_BK * 2;  // one plane
-    static constexpr int B_BYTES = BN * G_BK * 2;
+    static constexpr int A_BYTES = G_BM * G_BK * 2;        // one plane
+    static constexpr int B_BYTES = (BN / CG) * G_BK * 2;   // this CTA's share (CTA pair: half the N rows)
     static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
     static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
     static constexpr int ACC_COLS = BN;
@@ -59,10 +60,10 @@ struct GCfg {
 };
 // fp32 accumulate, fp16 A/B, a_major (bit 15) / b_major (bit 16): 1 = MN-major,
 // N >> 3 at bits 17-22, M >> 4 at bits 24-28
-template <int BN, bool AMN, bool BMN>
+template <int BN, bool AMN, bool BMN, int CG>
 constexpr uint32_t g_idesc() {
     return (1u << 4) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-           ((uint32_t)(G_BM >> 4) << 24);
+           ((uint32_t)((CG * G_BM) >> 4) << 24);
 }
 // MN-major SW128 descriptor: LBO = 8 KB (next 64 MN), SBO = 1 KB (next 8 K rows)
 __device__ __forceinline__ uint64_t desc_mn(uint32_t addr) {
@@ -82,14 +83,19 @@ struct GParams {
     float* part;              // [splits][M][N] when splits > 1
 };
 
-template <int BN, bool AMN, bool BMN>
+// CG = 2: a CTA pair (cluster of 2) runs M = 256 tcgen05.mma.cta_group::2 tiles, each
+// CTA holding its 128 A rows and half of the B tile (as the decode GEMM's pair mode)
+template <int BN, bool AMN, bool BMN, int CG>
 __global__ void __launch_bounds__(384, 1)
     gemm16_tc(const __grid_constant__ GParams P, const __grid_constant__ CUtensorMap mAh,
               const __grid_constant__ CUtensorMap mAl, const __grid_constant__ CUtensorMap mBh,
               const __grid_constant__ CUtensorMap mBl) {
-    using Cfg = GCfg<BN>;
+    using Cfg = GCfg<BN, CG>;
     constexpr int S = Cfg::STAGES;
-    constexpr uint32_t IDESC = g_idesc<BN, AMN, BMN>();
+    constexpr uint32_t IDESC = g_idesc<BN, AMN, BMN, CG>();
+    const int rank = CG == 2 ? (int)tc::cluster_rank() : 0;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(tc::smem_u32(&bars[2 * S + a]), 1);
-            tc::mbar_init(tc::smem_u32(&bars[2 * S + 2 + a]), 8);  // one arrive per epilogue warp
+            tc::mbar_init(tc::smem_u32(&bars[2 * S + 2 + a]), 8 * CG);  // one arrive per epilogue warp (of the pair)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -116,13 +122,21 @@ __global__ void __launch_bounds__(384, 1)
         tc::tma_prefetch(&mBl);
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         tc::smem_u32(tmem_slot)), "n"(2 * BN)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             tc::smem_u32(tmem_slot)), "n"(2 * BN)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             tc::smem_u32(tmem_slot)), "n"(2 * BN)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc::fence_before();
     __syncthreads();
+    if (CG == 2) tc::cluster_sync();  // the peer's barriers are initialised before any remote arrive
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -138,13 +152,21 @@ __global__ void __launch_bounds__(384, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int w = blockIdx.x; w < P.total; w += gridDim.x) {
+            auto load = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int x, int y) {
+                if (CG == 2)
+                    tc::tma_load_2d_pair(dst, m, bar, x, y);  // completes on the leader's barrier
+                else
+                    tc::tma_load_2d(dst, m, bar, x, y);
+            };
+            for (int w = cid; w < P.total; w += ncl) {
                 int mt, nt, kb0, kb1;
                 work(w, mt, nt, kb0, kb1);
+                const int arow = (mt * CG + rank) * G_BM;         // this CTA's A rows
+                const int bn0 = nt * BN + rank * (BN / CG);      // this CTA's B rows / columns
                 for (int kb = kb0; kb < kb1; ++kb) {
                     tc::mbar_wait(tc::smem_u32(&bars[S + stage]), phase ^ 1);
                     const uint32_t full = tc::smem_u32(&bars[stage]);
-                    tc::mbar_expect_tx(full, Cfg::STAGE_BYTES);
+                    if (leader) tc::mbar_expect_tx(full, CG * Cfg::STAGE_BYTES);  // both CTAs' bytes
                     const uint32_t st = tc::smem_u32(smem + stage * Cfg::STAGE_BYTES);
                     // stage: A_hi | A_lo | B_hi | B_lo
 #pragma unroll
@@ -153,19 +175,17 @@ __global__ void __launch_bounds__(384, 1)
                         const CUtensorMap* ma = pl ? &mAl : &mAh;
                         if (AMN) {
 #pragma unroll
-                            for (int j = 0; j < G_BM / 64; ++j)
-                                tc::tma_load_2d(da + j * 8192, ma, full, mt * G_BM + j * 64, kb * G_BK);
+                            for (int j = 0; j < G_BM / 64; ++j) load(da + j * 8192, ma, full, arow + j * 64, kb * G_BK);
                         } else {
-                            tc::tma_load_2d(da, ma, full, kb * G_BK, mt * G_BM);
+                            load(da, ma, full, kb * G_BK, arow);
                         }
                         const uint32_t db = st + 2 * Cfg::A_BYTES + pl * Cfg::B_BYTES;
                         const CUtensorMap* mb = pl ? &mBl : &mBh;
                         if (BMN) {
 #pragma unroll
-                            for (int j = 0; j < BN / 64; ++j)
-                                tc::tma_load_2d(db + j * 8192, mb, full, nt * BN + j * 64, kb * G_BK);
+                            for (int j = 0; j < BN / CG / 64; ++j) load(db + j * 8192, mb, full, bn0 + j * 64, kb * G_BK);
                         } else {
-                            tc::tma_load_2d(db, mb, full, kb * G_BK, nt * BN);
+                            load(db, mb, full, kb * G_BK, bn0);
                         }
                     }
                     if (++stage == S) {
@@ -176,10 +196,22 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && leader) {
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int w = blockIdx.x; w < P.total; w += gridDim.x) {
+            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t f) {
+                if (CG == 2)
+                    tc::mma_f16_pair(d, a, b, IDESC, f);
+                else
+                    tc::mma_f16(d, a, b, IDESC, f);
+            };
+            auto commit = [&](uint32_t bar) {
+                if (CG == 2)
+                    tc::mma_commit_pair(bar);  // arrives on the barrier in both CTAs
+                else
+                    tc::mma_commit(bar);
+            };
+            for (int w = cid; w < P.total; w += ncl) {
                 int mt, nt, kb0, kb1;
                 work(w, mt, nt, kb0, kb1);
                 tc::mbar_wait(tc::smem_u32(&bars[2 * S + 2 + acc]), acc_phase ^ 1);
@@ -197,17 +229,17 @@ __global__ void __launch_bounds__(384, 1)
                         // K = 16: 32 bytes along a K-major row, or 16 rows (2 KB) of an MN-major box
                         auto da = [&](uint32_t a) { return AMN ? desc_mn(a + k * 2048) : tc::smem_desc(a + k * 32); };
                         auto db = [&](uint32_t b) { return BMN ? desc_mn(b + k * 2048) : tc::smem_desc(b + k * 32); };
-                        tc::mma_f16(d, da(ah), db(bh), IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
-                        tc::mma_f16(d, da(ah), db(bl), IDESC, 1u);
-                        tc::mma_f16(d, da(al), db(bh), IDESC, 1u);
+                        mma(d, da(ah), db(bh), (kb > kb0 || k > 0) ? 1u : 0u);
+                        mma(d, da(ah), db(bl), 1u);
+                        mma(d, da(al), db(bh), 1u);
                     }
-                    tc::mma_commit(tc::smem_u32(&bars[S + stage]));
+                    commit(tc::smem_u32(&bars[S + stage]));
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc::mma_commit(tc::smem_u32(&bars[2 * S + acc]));
+                commit(tc::smem_u32(&bars[2 * S + acc]));
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -223,11 +255,11 @@ __global__ void __launch_bounds__(384, 1)
         const bool vec = (P.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(P.C) & 15) == 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int w = blockIdx.x; w < P.total; w += gridDim.x) {
+        for (int w = cid; w < P.total; w += ncl) {
             int mt, nt, kb0, kb1;
             work(w, mt, nt, kb0, kb1);
             const int sp = w % P.splits;
-            const int row = mt * G_BM + q * 32 + lane;
+            const int row = (mt * CG + rank) * G_BM + q * 32 + lane;
             tc::mbar_wait(tc::smem_u32(&bars[2 * S + acc]), acc_phase);
             tc::fence_after();
             const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * Cfg::ACC_COLS + half * HC;
@@ -240,7 +272,12 @@ __global__ void __launch_bounds__(384, 1)
                 if (c + 16 >= HC) {  // this warp's reads of the accumulator are done
                     tc::fence_before();
                     __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(tc::smem_u32(&bars[2 * S + 2 + acc]));
+                    if (lane == 0) {
+                        if (CG == 2 && !leader)
+                            tc::mbar_arrive_remote(tc::smem_u32(&bars[2 * S + 2 + acc]), 0);
+                        else
+                            tc::mbar_arrive(tc::smem_u32(&bars[2 * S + 2 + acc]));
+                    }
                 }
                 const int col = nt * BN + half * HC + c;
                 if (row >= P.M || col >= P.N) continue;
@@ -288,10 +325,15 @@ __global__ void __launch_bounds__(384, 1)
         }
     }
     __syncthreads();
+    if (CG == 2) tc::cluster_sync();  // no CTA leaves while its peer may still signal it
     if (warp == 2) {
         tc::fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN)
-                     : "memory");
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN)
+                         : "memory");
     }
 }
 
@@ -321,28 +363,29 @@ __global__ void gemm16_reduce(const float* part, int splits, int M, int N, float
     }
 }
 
-template <int BN, bool AMN, bool BMN>
+template <int BN, bool AMN, bool BMN, int CG>
 bool launch_t(const GemmF16Args& g, int splits, cudaStream_t stream) {
-    using Cfg = GCfg<BN>;
+    using Cfg = GCfg<BN, CG>;
     static std::atomic<unsigned long long> attr{0};
-    if (first_on_device(attr) && cudaFuncSetAttribute(gemm16_tc<BN, AMN, BMN>,
+    if (first_on_device(attr) && cudaFuncSetAttribute(gemm16_tc<BN, AMN, BMN, CG>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       Cfg::SMEM) != cudaSuccess)
         return false;
-    // K-major planes: [rows = M|N][cols = K], box [rows][64];  MN-major: [rows = K][cols = M|N], box [64][64]
+    // K-major planes: [rows = M|N][cols = K], box [rows][64];  MN-major: [rows = K][cols = M|N],
+    // box [64][64].  A CTA pair loads half of each B tile per CTA.
     CUtensorMap m[4];
     for (int pl = 0; pl < 2; ++pl) {
         const __half* a = pl ? g.A_lo : g.A_hi;
         const __half* b = pl ? g.B_lo : g.B_hi;
         const bool oka = AMN ? tc_make_map(&m[pl], a, g.K, g.M, g.lda, 64) : tc_make_map(&m[pl], a, g.M, g.K, g.lda, G_BM);
         const bool okb = BMN ? tc_make_map(&m[2 + pl], b, g.K, g.N, g.ldb, 64)
-                             : tc_make_map(&m[2 + pl], b, g.N, g.K, g.ldb, BN);
+                             : tc_make_map(&m[2 + pl], b, g.N, g.K, g.ldb, BN / CG);
         if (!oka || !okb) return false;
     }
     GParams P{};
     P.M = g.M;
     P.N = g.N;
-    P.m_tiles = (g.M + G_BM - 1) / G_BM;
+    P.m_tiles = (g.M + CG * G_BM - 1) / (CG * G_BM);
     P.n_tiles = (g.N + BN - 1) / BN;
     P.k_blocks = (int)((g.K + G_BK - 1) / G_BK);
     P.kb_per_split = (P.k_blocks + splits - 1) / splits;
@@ -354,9 +397,26 @@ bool launch_t(const GemmF16Args& g, int splits, cudaStream_t stream) {
     P.amaxB = g.amaxB;
     P.beta = g.beta;
     P.part = g.part;
-    const int grid = std::min(P.total, g.sms);
-    gemm16_tc<BN, AMN, BMN><<<grid, 384, Cfg::SMEM, stream>>>(P, m[0], m[1], m[2], m[3]);
-    if (cudaGetLastError() != cudaSuccess) return false;
+    const int grid = CG * std::min(P.total, g.sms / CG);
+    if (CG == 1) {
+        gemm16_tc<BN, AMN, BMN, CG><<<grid, 384, Cfg::SMEM, stream>>>(P, m[0], m[1], m[2], m[3]);
+        if (cudaGetLastError() != cudaSuccess) return false;
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(384);
+        cfg.dynamicSmemBytes = Cfg::SMEM;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, gemm16_tc<BN, AMN, BMN, CG>, P, m[0], m[1], m[2], m[3]) != cudaSuccess)
+            return false;
+    }
     if (P.splits > 1) {
         const long long n = (long long)g.M * ((g.N + 3) / 4);
         const int blocks = (int)std::min<long long>((n + 255) / 256, 8LL * g.sms);
@@ -366,40 +426,52 @@ bool launch_t(const GemmF16Args& g, int splits, cudaStream_t stream) {
     return true;
 }
 
-template <int BN>
+template <int BN, int CG>
 bool launch_bn(const GemmF16Args& g, int splits, cudaStream_t stream) {
     if (g.a_mn)
-        return g.b_mn ? launch_t<BN, true, true>(g, splits, stream) : launch_t<BN, true, false>(g, splits, stream);
-    return g.b_mn ? launch_t<BN, false, true>(g, splits, stream) : launch_t<BN, false, false>(g, splits, stream);
+        return g.b_mn ? launch_t<BN, true, true, CG>(g, splits, stream) : launch_t<BN, true, false, CG>(g, splits, stream);
+    return g.b_mn ? launch_t<BN, false, true, CG>(g, splits, stream) : launch_t<BN, false, false, CG>(g, splits, stream);
 }
 
 }  // namespace
 
 namespace {
-// modelled time of a (BN, splits) choice: the tensor-core makespan (waves of work
-// items; a full-K 128 x BN tile = 3 x 2 x 128 x BN x K FLOP at ~9 TFLOP/s per SM,
-// BN = 128 tiles ~10% slower per FLOP: A is re-staged per N tile) plus, when split,
-// the reduction pass ((splits + 2) x M x N x 4 bytes at ~2.5 TB/s, plus a launch)
-double gemm16_cost(int M, int N, long long K, int sms, int bn, int s) {
-    const long long tiles = (long long)((M + G_BM - 1) / G_BM) * ((N + bn - 1) / bn);
-    const double tile_s = 6.0 * G_BM * bn * (double)K / 9.0e12 * (bn == 128 ? 1.1 : 1.0);
-    double c = (double)((tiles * s + sms - 1) / sms) * tile_s / (double)s;
+// modelled time of a (BN, CTA group, splits) choice: the tensor-core makespan (waves
+// of work items over the SMs / CTA pairs; a full-K 128 x BN tile = 3 x 2 x 128 x BN x
+// K FLOP at ~9 TFLOP/s per SM, BN = 128 tiles ~10% slower per FLOP: A is re-staged
+// per N tile; a CTA pair runs a 256-row tile in the time of a 128-row one at ~15%
+// higher issue rate: half the B operand traffic per SM) plus, when split, the
+// reduction pass ((splits + 2) x M x N x 4 bytes at ~2.5 TB/s, plus a launch)
+double gemm16_cost(int M, int N, long long K, int sms, int bn, int cg, int s) {
+    const long long tiles = (long long)((M + cg * G_BM - 1) / (cg * G_BM)) * ((N + bn - 1) / bn);
+    const double tile_s = 6.0 * G_BM * bn * (double)K / 9.0e12 * (bn == 128 ? 1.1 : 1.0) * (cg == 2 ? 0.87 : 1.0);
+    const long long slots = sms / cg;
+    double c = (double)((tiles * s + slots - 1) / slots) * tile_s / (double)s;
     if (s > 1) c += (s + 2.0) * (double)M * N * 4.0 / 2.5e12 + 5e-6;
     return c;
 }
-void gemm16_plan(int M, int N, long long K, int sms, int& bn, int& splits) {
+void gemm16_plan(int M, int N, long long K, int sms, int& bn, int& cg, int& splits) {
+    static const bool pairs = [] {
+        const char* e = std::getenv("KS_TRAIN_PAIR");
+        return !(e && e[0] == '0');
+    }();
     const long long kb = (K + G_BK - 1) / G_BK;
     bn = N <= 128 ? 128 : 256;
+    cg = 1;
     splits = 1;
-    double best = gemm16_cost(M, N, K, sms, bn, 1);
-    for (int b : {128, 256}) {
-        if (b == 256 && N <= 128) continue;
-        for (long long s = 1; s <= 64 && (s == 1 || s * 4 <= kb); ++s) {
-            const double c = gemm16_cost(M, N, K, sms, b, (int)s);
-            if (c < best * 0.999) {
-                best = c;
-                bn = b;
-                splits = (int)s;
+    double best = gemm16_cost(M, N, K, sms, bn, 1, 1);
+    for (int c2 : {1, 2}) {
+        if (c2 == 2 && (!pairs || M <= G_BM)) continue;
+        for (int b : {128, 256}) {
+            if (b == 256 && N <= 128) continue;
+            for (long long s = 1; s <= 64 && (s == 1 || s * 4 <= kb); ++s) {
+                const double c = gemm16_cost(M, N, K, sms, b, c2, (int)s);
+                if (c < best * 0.999) {
+                    best = c;
+                    bn = b;
+                    cg = c2;
+                    splits = (int)s;
+                }
             }
         }
     }
@@ -407,18 +479,22 @@ void gemm16_plan(int M, int N, long long K, int sms, int& bn, int& splits) {
 }  // namespace
 
 int gemm16_splits(int M, int N, long long K, int sms) {
-    int bn, s;
-    gemm16_plan(M, N, K, sms, bn, s);
+    int bn, cg, s;
+    gemm16_plan(M, N, K, sms, bn, cg, s);
     return s;
 }
 
 bool launch_gemm16(const GemmF16Args& g, cudaStream_t stream, int* launches) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return false;
     if ((g.lda % 8) != 0 || (g.ldb % 8) != 0) return false;  // TMA: 16-byte row strides
-    int bn, splits;
-    gemm16_plan(g.M, g.N, g.K, g.sms, bn, splits);
+    int bn, cg, splits;
+    gemm16_plan(g.M, g.N, g.K, g.sms, bn, cg, splits);
     if (splits > 1 && g.part == nullptr) return false;
-    const bool ok = bn == 128 ? launch_bn<128>(g, splits, stream) : launch_bn<256>(g, splits, stream);
+    bool ok;
+    if (cg == 2)
+        ok = bn == 128 ? launch_bn<128, 2>(g, splits, stream) : launch_bn<256, 2>(g, splits, stream);
+    else
+        ok = bn == 128 ? launch_bn<128, 1>(g, splits, stream) : launch_bn<256, 1>(g, splits, stream);
     if (ok && launches) *launches += splits > 1 ? 2 : 1;
     return ok;
 }
