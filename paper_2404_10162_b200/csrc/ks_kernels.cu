@@ -883,7 +883,7 @@ __device__ __forceinline__ int src_lane(int v) {
 }
 
 template <int VP>
-__global__ void __launch_bounds__(256, VP == 32 ? 1 : VP == 16 ? 2 : 3) beam_step_t(BeamArgs a, PosMeta m) {
+__global__ void __launch_bounds__(256, VP == 32 ? 1 : VP == 16 ? 2 : 4) beam_step_t(BeamArgs a, PosMeta m) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int WS = VP == 4 ? 12 : VP + 4;  // padded W row: conflict-free 128-bit loads
     const int V = m.vsize[a.pos];
