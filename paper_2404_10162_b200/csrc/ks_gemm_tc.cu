@@ -41,6 +41,9 @@ struct TcProblem {
     int tma_out;     // h / c of whole 32-row warp slices leave through bulk tensor stores
     alignas(64) CUtensorMap mh;  // fp32 [M][H] views of h_out / c_out, box 32 rows x 8 units
     alignas(64) CUtensorMap mc;
+    int tma_a;                   // the split copy of h (hA_hi / hA_lo) through bulk stores too
+    alignas(64) CUtensorMap mah; // fp16 [M][H] views of hA_hi / hA_lo, box 32 rows x 8 units
+    alignas(64) CUtensorMap mal;
 };
 
 // alpha-block mode: K-blocks of one tile.  The B operand's P^T columns start at
@@ -204,27 +207,47 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
         // the next chunk's G[slot] / c_prev, in flight during this chunk's stores and the
         // next chunk's TMEM loads (one register set: these loads reuse gn / cn)
         if (c + 1 < NCH) load_bc(c + 1, gn, cn);
+        const bool bulk_a = bulk && pr.tma_a;
         if (bulk) {
-            // the warp's 32 x 8 slice of h and c through shared memory and two bulk tensor
-            // stores (one engine transaction per slice instead of 64 row-segment stores)
-            float* sh = stg + stg_buf * 512;
+            // the warp's 32 x 8 slice of h and c (and of the split h, the encoder's next
+            // operand) through shared memory and bulk tensor stores (one engine
+            // transaction per slice instead of 64 row-segment stores); with the split
+            // planes the 3 KB slice set is single-buffered
+            float* sh = bulk_a ? stg : stg + stg_buf * 512;
             float* scb = sh + 256;
-            if (lane == 0) tc::bulk_wait_read<1>();  // the group that last read this buffer is done
+            __half* sah = reinterpret_cast<__half*>(sh + 512);
+            __half* sal = sah + 256;
+            if (lane == 0) {
+                if (bulk_a)
+                    tc::bulk_wait_read<0>();
+                else
+                    tc::bulk_wait_read<1>();  // the group that last read this buffer is done
+            }
             __syncwarp();
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int lr = 16 * (i >> 1) + tq + 8 * (i & 1);
                 *reinterpret_cast<float2*>(sh + lr * 8 + tcol) = make_float2(hv[i][0], hv[i][1]);
                 *reinterpret_cast<float2*>(scb + lr * 8 + tcol) = make_float2(cv[i][0], cv[i][1]);
+                if (bulk_a) {
+                    __half2 hh, hl;
+                    split_f16x2(hv[i][0], hv[i][1], hh, hl);
+                    *reinterpret_cast<__half2*>(sah + lr * 8 + tcol) = hh;
+                    *reinterpret_cast<__half2*>(sal + lr * 8 + tcol) = hl;
+                }
             }
             tc::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
                 tc::tma_store_2d(&pr.mh, tc::smem_u32(sh), nt * UNITS + uc, row0 + q * 32);
                 tc::tma_store_2d(&pr.mc, tc::smem_u32(scb), nt * UNITS + uc, row0 + q * 32);
+                if (bulk_a) {
+                    tc::tma_store_2d(&pr.mah, tc::smem_u32(sah), nt * UNITS + uc, row0 + q * 32);
+                    tc::tma_store_2d(&pr.mal, tc::smem_u32(sal), nt * UNITS + uc, row0 + q * 32);
+                }
                 tc::bulk_commit();
             }
-            stg_buf ^= 1;
+            if (!bulk_a) stg_buf ^= 1;
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -238,6 +261,7 @@ __device__ __forceinline__ void epilogue_cells(const LstmArgs& p, uint64_t* bars
             }
             if (p.h_out2 != nullptr)
                 __stcs(reinterpret_cast<float2*>(p.h_out2 + r * p.ldh2 + u0), make_float2(hv[i][0], hv[i][1]));
+            if (bulk_a) continue;  // the split h went out with the bulk stores
             if (p.hA_hi != nullptr && p.ha_bf16) {
                 *reinterpret_cast<__nv_bfloat162*>(p.hA_hi + r * p.ldha + u0) =
                     __floats2bfloat162_rn(hv[i][0], hv[i][1]);
@@ -735,6 +759,19 @@ bool make_out_map(CUtensorMap* m, const float* base, long long rows, int fan, lo
     return r == CUDA_SUCCESS;
 }
 
+// fp16 [rows][cols] split-h planes (row stride ld elements): box 32 rows x 8 columns
+bool make_half_out_map(CUtensorMap* m, const __half* base, long long rows, long long cols, long long ld) {
+    EncodeTiledFn fn = tc_encode_fn();
+    if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15) || (ld & 7)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {8, 32};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // fp16 [n][rows] transposed P planes (row stride ld elements): box 32 rows x 8 n
 bool make_pt_out_map(CUtensorMap* m, const __half* base, long long rows, long long n, long long ld) {
     EncodeTiledFn fn = tc_encode_fn();
@@ -809,6 +846,15 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
                                      make_out_map(&pr.mc, a.c_out, a.M, fan, a.H, a.ldc)
                                  ? 1
                                  : 0;
+            static const bool bulk_a_env = [] {
+                const char* e = std::getenv("KS_BULK_A");
+                return !(e && e[0] == '0');
+            }();
+            pr.tma_a = bulk_a_env && pr.tma_out && !a.raw && fan == 1 && SPLIT && a.hA_hi && a.hA_lo && !a.ha_bf16 &&
+                               make_half_out_map(&pr.mah, a.hA_hi, a.M, a.H, a.ldha) &&
+                               make_half_out_map(&pr.mal, a.hA_lo, a.M, a.H, a.ldha)
+                           ? 1
+                           : 0;
         }
         if (a.kb_alpha > 0 && (CG == 2 ? a.alpha_tile != 2 * TC_BM : (a.alpha_tile < 1 || a.alpha_tile > TC_BM)))
             return false;  // operand laid out for another tile
