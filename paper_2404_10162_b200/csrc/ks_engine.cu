@@ -238,6 +238,19 @@ struct ks_engine {
     // N-tile width of the current chunk's gate GEMMs: tc_units, or 32 when 64-unit
     // tiles would leave SMs idle (small batches; needs the 32-unit weight planes)
     int units_now = 64;
+    // encoder prefix tables (attn / attn-2 with the a_t operand planes): the state of
+    // encoder step s of a direction depends only on the first s+1 input fields that
+    // direction reads, and those take few values -- every prefix's h, c and split h is
+    // computed once per engine, and a decode gathers the covered steps instead of
+    // running them (KS_ENC_TABLE=0 disables)
+    struct EncTable {
+        int S = -1;                 // steps 0..S covered (-1: none)
+        int order[7] = {};          // field read at step j (fwd t = j, bwd t = 6 - j)
+        long long stride[7] = {};   // mixed-radix weight of step j's field in a table row
+        int64_t rows = 0;           // table rows: every digit combination of steps 0..S
+        DevMem h, c, hA;            // [S+1][rows][He] fp32, fp32, and the split planes [2][S+1][rows][He]
+    };
+    EncTable etab[2];
     bool pair_now() const { return pair && units_now == 64; }
     bool proj_at(int pos, int H) const {
         return ctxproj && pos > 0 && (ctxproj_force || alpha_cols_of(H) < 2 * NA);
@@ -383,6 +396,7 @@ ks_status upload(DevMem& m, const void* src, size_t bytes) {
     return KS_OK;
 }
 
+ks_status build_enc_tables(ks_engine& E);
 }  // namespace
 
 extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, int32_t precision,
@@ -605,6 +619,7 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         if (kc && std::atoll(kc) > 0) E.chunk = std::atoll(kc);
     }
     cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (ks_status st = build_enc_tables(E)) return st;
     *out = eng.release();
     return KS_OK;
 }
@@ -1057,6 +1072,141 @@ ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
 }
 
 // Decodes one chunk of C configs already resident on the device.
+// ---- encoder prefix tables
+// Table rows enumerate every digit combination of a direction's first S+1 fields
+// (mixed radix, step 0's field least significant).  Step s's state of a row depends
+// only on digits 0..s, so a config's step-s state is the row whose digits 0..s are its
+// tokens and whose later digits are 0.  The rows are computed by the decode's own
+// encoder launches (same kernels, same per-row arithmetic), so a gathered state is
+// bit-identical to the one the loop would have produced.
+ks_status build_enc_tables(ks_engine& E) {
+    const char* env = std::getenv("KS_ENC_TABLE");
+    const bool on = E.ctxproj && E.precision != KS_PREC_FP32 && !(env && env[0] == '0');
+    if (!on) return KS_OK;
+    const int He = E.NA;
+    const int64_t kCapRows = 8192;
+    const double kCapBytes = 96.0 * (1 << 20);
+    const int units_saved = E.units_now;
+    E.units_now = E.tc_units;
+    for (int dir = 0; dir < 2; ++dir) {
+        ks_engine::EncTable& T = E.etab[dir];
+        T.S = -1;
+        int64_t r = 1;
+        for (int j = 0; j < 7; ++j) {
+            const int t = dir == 0 ? j : 6 - j;
+            const int64_t r2 = r * E.in_sizes[(size_t)t];
+            if (r2 > kCapRows || (double)r2 * (j + 1) * He * 12.0 > kCapBytes) break;
+            T.order[j] = t;
+            T.stride[j] = r;
+            r = r2;
+            T.S = j;
+        }
+        if (T.S < 0) continue;
+        T.rows = r;
+        const int S = T.S;
+        std::vector<int> tok((size_t)r * 7, 0);
+        for (int64_t row = 0; row < r; ++row)
+            for (int j = 0; j <= S; ++j)
+                tok[(size_t)row * 7 + T.order[j]] = (int)((row / T.stride[j]) % E.in_sizes[(size_t)T.order[j]]);
+        DevMem dtok;
+        const size_t plane = (size_t)(S + 1) * r * He;
+        if (dtok.ensure(tok.size() * 4) || T.h.ensure(plane * 4) || T.c.ensure(plane * 4) ||
+            T.hA.ensure(2 * plane * 2))
+            return set_error(KS_ERR_CUDA, "encoder table allocation failed");
+        KS_CUDA(cudaMemcpyAsync(dtok.p, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, E.stream));
+        KS_CUDA(cudaMemsetAsync(T.hA.p, 0, 2 * plane * 2, E.stream));
+        float* th = T.h.as<float>();
+        float* tc = T.c.as<float>();
+        __half* thi = T.hA.as<__half>();
+        __half* tlo = thi + plane;
+        const size_t step = (size_t)r * He;
+        for (int s = 0; s <= S; ++s) {
+            LstmArgs p;
+            std::memset(&p, 0, sizeof p);
+            p.M = (int)r;
+            p.H = He;
+            p.K = s == 0 ? 0 : He;
+            p.A = s == 0 ? nullptr : th + (s - 1) * step;
+            p.lda = He;
+            p.A_hi = s == 0 ? nullptr : thi + (s - 1) * step;
+            p.A_lo = s == 0 ? nullptr : tlo + (s - 1) * step;
+            p.ldah = He;
+            p.W = E.enc[dir].W.as<float>();
+            p.G = E.enc[dir].G.as<float>();
+            p.slot_ptr = dtok.as<int>() + T.order[s];
+            p.slot_stride = 7;
+            p.slot_base = E.in_offset[(size_t)T.order[s]];
+            p.c_prev = s == 0 ? nullptr : tc + (s - 1) * step;
+            p.ldc_prev = He;
+            p.c_out = tc + s * step;
+            p.ldc = He;
+            p.h_out = th + s * step;
+            p.ldh = He;
+            p.hA_hi = thi + s * step;
+            p.hA_lo = tlo + s * step;
+            p.ldha = He;
+            p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
+            ks_status st = launch_lstm(E, p, nullptr, E.enc[dir], nullptr, 0.0);
+            if (st) return st;
+        }
+        KS_CUDA(cudaStreamSynchronize(E.stream));  // dtok is freed on return
+    }
+    E.units_now = units_saved;
+    E.launches = 0;
+    return KS_OK;
+}
+
+struct EncGatherArgs {
+    const int* tok;              // [C][7]
+    int C, He, S[2];
+    int order[2][7];
+    long long stride[2][7];
+    long long rows[2];
+    const float* h[2];
+    const float* c[2];
+    const __half* hi[2];
+    const __half* lo[2];
+    float* act;                  // a_t fp32, row stride act_ld, step t at t*NA2 + dir*NA
+    __half* ahi;                 // a_t operand planes (same layout)
+    __half* alo;
+    long long act_ld, NA2, NA;
+    float* c_last[2];            // encoder c of step S_dir (the loop's ping-pong slot)
+};
+
+// one thread per (config, covered direction-step, 8 units)
+__global__ void __launch_bounds__(256) enc_table_gather(EncGatherArgs a) {
+    const int q8 = a.He / 8;
+    const int steps = a.S[0] + 1 + a.S[1] + 1;
+    const long long n = (long long)a.C * steps * q8;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(i % q8);
+        const long long bj = i / q8;
+        const int j = (int)(bj % steps);
+        const int b = (int)(bj / steps);
+        const int d = j <= a.S[0] ? 0 : 1;
+        const int s = d == 0 ? j : j - (a.S[0] + 1);
+        const int* tk = a.tok + (size_t)b * 7;
+        long long row = 0;
+        for (int x = 0; x <= s; ++x) row += (long long)__ldg(tk + a.order[d][x]) * a.stride[d][x];
+        const size_t src = ((size_t)s * a.rows[d] + row) * a.He + q * 8;
+        const int t = a.order[d][s];
+        const size_t dst = (size_t)b * a.act_ld + t * a.NA2 + d * a.NA + q * 8;
+        const float4* hs = reinterpret_cast<const float4*>(a.h[d] + src);
+        float4* hd = reinterpret_cast<float4*>(a.act + dst);
+        hd[0] = __ldg(hs);
+        hd[1] = __ldg(hs + 1);
+        *reinterpret_cast<uint4*>(a.ahi + dst) = __ldg(reinterpret_cast<const uint4*>(a.hi[d] + src));
+        *reinterpret_cast<uint4*>(a.alo + dst) = __ldg(reinterpret_cast<const uint4*>(a.lo[d] + src));
+        if (s == a.S[d]) {
+            const float4* cs = reinterpret_cast<const float4*>(a.c[d] + src);
+            float4* cd = reinterpret_cast<float4*>(a.c_last[d] + (size_t)b * a.He + q * 8);
+            cd[0] = __ldg(cs);
+            cd[1] = __ldg(cs + 1);
+        }
+    }
+}
+
 // reuse_encoder: the chunk's encoder outputs (a_t, encoder state, P^T, hybrid
 // features) from the previous run_chunk on the SAME tokens are still in the
 // workspace -- decode again at another beam width without re-encoding
@@ -1093,6 +1243,41 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     if (!reuse_encoder && hybrid && (st = encode_hybrid(E, C, d_tok))) return st;
     // ---- encoder (bi-LSTM over the 7 one-hot input steps, zero initial state)
     const int dirs = enc_dec ? 1 : 2;
+    // covered steps of each direction come from the prefix tables (to_actA engines)
+    int covered[2] = {-1, -1};
+    if (!reuse_encoder && !hybrid && !enc_dec && split && E.ctxproj &&
+        (E.etab[0].S >= 0 || E.etab[1].S >= 0)) {
+        EncGatherArgs g;
+        std::memset(&g, 0, sizeof g);
+        g.tok = d_tok;
+        g.C = (int)C;
+        g.He = He;
+        for (int d = 0; d < 2; ++d) {
+            const ks_engine::EncTable& T = E.etab[d];
+            g.S[d] = covered[d] = T.S;
+            for (int j = 0; j < 7; ++j) {
+                g.order[d][j] = T.order[j];
+                g.stride[d][j] = T.stride[j];
+            }
+            g.rows[d] = T.rows;
+            const size_t plane = (size_t)(T.S + 1) * T.rows * He;
+            g.h[d] = T.h.as<float>();
+            g.c[d] = T.c.as<float>();
+            g.hi[d] = T.hA.as<__half>();
+            g.lo[d] = T.hA.as<__half>() + plane;
+            g.c_last[d] = T.S >= 0 ? encc_at(d, T.S & 1) : nullptr;
+        }
+        g.act = act;
+        g.ahi = E.actA.as<__half>();
+        g.alo = g.ahi + (size_t)C * 7 * NA2;
+        g.act_ld = act_ld;
+        g.NA2 = NA2;
+        g.NA = E.NA;
+        const long long n = C * (long long)(g.S[0] + 1 + g.S[1] + 1) * (He / 8);
+        enc_table_gather<<<(unsigned)std::min<long long>((n + 255) / 256, 16LL * E.num_sms), 256, 0, s>>>(g);
+        E.launches++;
+        KS_CUDA(cudaGetLastError());
+    }
     for (int sidx = 0; sidx < ((hybrid || reuse_encoder) ? 0 : 7); ++sidx) {
         LstmArgs a[2];
         for (int dir = 0; dir < dirs; ++dir) {
@@ -1152,8 +1337,13 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
                 p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
             }
         }
-        const double fl = sidx == 0 ? 0.0 : 2.0 * dirs * (double)C * He * 4.0 * He;
-        if ((st = launch_lstm(E, a[0], dirs == 2 ? &a[1] : nullptr, E.enc[0], dirs == 2 ? &E.enc[1] : nullptr, fl)))
+        int act_dirs[2], na = 0;
+        for (int dir = 0; dir < dirs; ++dir)
+            if (sidx > covered[dir]) act_dirs[na++] = dir;
+        if (na == 0) continue;
+        const double fl = sidx == 0 ? 0.0 : 2.0 * na * (double)C * He * 4.0 * He;
+        const int d0 = act_dirs[0];
+        if ((st = launch_lstm(E, a[d0], na == 2 ? &a[1] : nullptr, E.enc[d0], na == 2 ? &E.enc[1] : nullptr, fl)))
             return st;
     }
     bool any_proj = false;

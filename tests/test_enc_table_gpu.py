@@ -1,0 +1,63 @@
+"""Encoder prefix tables (ks_engine.cu build_enc_tables / enc_table_gather): the
+covered encoder steps gathered from the per-engine tables must give decodes
+bit-identical to running every encoder step (KS_ENC_TABLE=0), on the BASELINE
+model and on random models whose vocabularies cover different step counts."""
+import os
+
+import numpy as np
+import pytest
+
+from tests.util import have_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a GPU")]
+
+
+def _decode(path, prec, tok, k, preds, table, chunk=None):
+    from paper_2404_10162_b200._cabi import Engine
+
+    old = os.environ.get("KS_ENC_TABLE")
+    os.environ["KS_ENC_TABLE"] = "1" if table else "0"
+    try:
+        e = Engine(path, 0, prec)
+    finally:
+        if old is None:
+            os.environ.pop("KS_ENC_TABLE")
+        else:
+            os.environ["KS_ENC_TABLE"] = old
+    if chunk:
+        e.set_chunk(chunk)
+    return e.beam(tok, k, None, preds)
+
+
+def _same(a, b):
+    for key in ("tokens", "log_prob", "count", "status"):
+        assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.parametrize("prec", ["f16x3", "bf16"])
+def test_tables_bit_identical_default_model(prec):
+    from paper_2404_10162_b200 import workloads as W
+    from paper_2404_10162_b200._cabi import Engine
+
+    path = W.DEFAULT_CKPT
+    e = Engine(path, 0, prec)
+    tok = e.encode(e.synthetic(6000, W.SEED, 123))
+    preds = W.predicate_dicts(path)
+    _same(_decode(path, prec, tok, 5, preds, True, 2500), _decode(path, prec, tok, 5, preds, False, 2500))
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_tables_bit_identical_random_models(case, tmp_path):
+    import paper_2404_10162_b200 as ks
+    from oracle.oracle import OracleModel
+    from tests.test_fuzz_gpu import _model
+
+    variant, n_a, spec = [("attn", 64, "ConvAsm1x1U"), ("attn-2", 128, "ConvOclDirectFwd1x1"),
+                          ("attn", 192, "ConvAsmBwdWrW3x3")][case]
+    path = _model(ks, variant, n_a, 128, 2, spec, 300 + case, str(tmp_path / "m.ckpt"))
+    o = OracleModel(path)
+    rng = np.random.default_rng(case)
+    B = 700
+    tok = np.stack([rng.integers(0, len(o.input_values[f]), B) for f in range(7)], 1).astype(np.int32)
+    preds = [o.membership()]
+    _same(_decode(path, "f16x3", tok, 4, preds, True), _decode(path, "f16x3", tok, 4, preds, False))
