@@ -247,8 +247,9 @@ struct ks_engine {
         int S = -1;                 // steps 0..S covered (-1: none)
         int order[7] = {};          // field read at step j (fwd t = j, bwd t = 6 - j)
         long long stride[7] = {};   // mixed-radix weight of step j's field in a table row
-        int64_t rows = 0;           // table rows: every digit combination of steps 0..S
-        DevMem h, c, hA;            // [S+1][rows][He] fp32, fp32, and the split planes [2][S+1][rows][He]
+        long long off[7] = {};      // first row of step j in the compact table (R_j rows each)
+        int64_t rows = 0;           // compact table rows: sum over steps of R_j = prod_{i<=j} |field_i|
+        DevMem h, c, hA;            // h [rows][He] fp32, c of step S [R_S][He], split planes [2][rows][He]
     };
     EncTable etab[2];
     bool pair_now() const { return pair && units_now == 64; }
@@ -1075,81 +1076,97 @@ ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
 // ---- encoder prefix tables
 // Table rows enumerate every digit combination of a direction's first S+1 fields
 // (mixed radix, step 0's field least significant).  Step s's state of a row depends
-// only on digits 0..s, so a config's step-s state is the row whose digits 0..s are its
-// tokens and whose later digits are 0.  The rows are computed by the decode's own
-// encoder launches (same kernels, same per-row arithmetic), so a gathered state is
-// bit-identical to the one the loop would have produced.
+// only on digits 0..s, so a config's step-s state is the one of the row whose digits
+// 0..s are its tokens and whose later digits are 0 -- one of the first R_s =
+// prod_{j<=s} |field_j| rows, which is all the compact table keeps of step s.  The
+// rows are computed by the decode's own encoder launches (same kernels, same per-row
+// arithmetic), so a gathered state is bit-identical to the one the loop produces.
 ks_status build_enc_tables(ks_engine& E) {
     const char* env = std::getenv("KS_ENC_TABLE");
     const bool on = E.ctxproj && E.precision != KS_PREC_FP32 && !(env && env[0] == '0');
     if (!on) return KS_OK;
     const int He = E.NA;
-    const int64_t kCapRows = 8192;
-    const double kCapBytes = 96.0 * (1 << 20);
+    // enumeration rows x units (12 B each, twice, while building) and compact table
+    // elements (12 B each): every step of the BASELINE model (46,656 x 256) fits
+    const char* ce = std::getenv("KS_ENC_TABLE_ELEMS");
+    const int64_t kCapElems = ce ? std::atoll(ce) : (1LL << 24);
+    const int64_t kCapTable = 6 * kCapElems;
     const int units_saved = E.units_now;
     E.units_now = E.tc_units;
     for (int dir = 0; dir < 2; ++dir) {
         ks_engine::EncTable& T = E.etab[dir];
         T.S = -1;
-        int64_t r = 1;
+        int64_t r = 1, total = 0;
         for (int j = 0; j < 7; ++j) {
             const int t = dir == 0 ? j : 6 - j;
             const int64_t r2 = r * E.in_sizes[(size_t)t];
-            if (r2 > kCapRows || (double)r2 * (j + 1) * He * 12.0 > kCapBytes) break;
+            if (r2 * He > kCapElems || (total + r2) * He > kCapTable) break;
             T.order[j] = t;
             T.stride[j] = r;
+            T.off[j] = total;
+            total += r2;
             r = r2;
             T.S = j;
         }
         if (T.S < 0) continue;
-        T.rows = r;
+        T.rows = total;
         const int S = T.S;
         std::vector<int> tok((size_t)r * 7, 0);
         for (int64_t row = 0; row < r; ++row)
             for (int j = 0; j <= S; ++j)
                 tok[(size_t)row * 7 + T.order[j]] = (int)((row / T.stride[j]) % E.in_sizes[(size_t)T.order[j]]);
-        DevMem dtok;
-        const size_t plane = (size_t)(S + 1) * r * He;
-        if (dtok.ensure(tok.size() * 4) || T.h.ensure(plane * 4) || T.c.ensure(plane * 4) ||
-            T.hA.ensure(2 * plane * 2))
+        DevMem dtok, scratch;
+        const size_t step = (size_t)r * He;
+        const size_t plane = (size_t)total * He;
+        if (dtok.ensure(tok.size() * 4) || scratch.ensure(2 * step * 12) || T.h.ensure(plane * 4) ||
+            T.c.ensure(step * 4) || T.hA.ensure(2 * plane * 2))
             return set_error(KS_ERR_CUDA, "encoder table allocation failed");
         KS_CUDA(cudaMemcpyAsync(dtok.p, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, E.stream));
-        KS_CUDA(cudaMemsetAsync(T.hA.p, 0, 2 * plane * 2, E.stream));
-        float* th = T.h.as<float>();
-        float* tc = T.c.as<float>();
-        __half* thi = T.hA.as<__half>();
-        __half* tlo = thi + plane;
-        const size_t step = (size_t)r * He;
+        KS_CUDA(cudaMemsetAsync(scratch.p, 0, 2 * step * 12, E.stream));
+        // scratch ping-pong: h [2][r][He] fp32, c [2][r][He] fp32, hi / lo [2][r][He]
+        float* sh = scratch.as<float>();
+        float* sc = sh + 2 * step;
+        __half* shi = reinterpret_cast<__half*>(sc + 2 * step);
+        __half* slo = shi + 2 * step;
         for (int s = 0; s <= S; ++s) {
+            const size_t cur = (size_t)(s & 1) * step, prv = (size_t)((s + 1) & 1) * step;
             LstmArgs p;
             std::memset(&p, 0, sizeof p);
             p.M = (int)r;
             p.H = He;
             p.K = s == 0 ? 0 : He;
-            p.A = s == 0 ? nullptr : th + (s - 1) * step;
+            p.A = s == 0 ? nullptr : sh + prv;
             p.lda = He;
-            p.A_hi = s == 0 ? nullptr : thi + (s - 1) * step;
-            p.A_lo = s == 0 ? nullptr : tlo + (s - 1) * step;
+            p.A_hi = s == 0 ? nullptr : shi + prv;
+            p.A_lo = s == 0 ? nullptr : slo + prv;
             p.ldah = He;
             p.W = E.enc[dir].W.as<float>();
             p.G = E.enc[dir].G.as<float>();
             p.slot_ptr = dtok.as<int>() + T.order[s];
             p.slot_stride = 7;
             p.slot_base = E.in_offset[(size_t)T.order[s]];
-            p.c_prev = s == 0 ? nullptr : tc + (s - 1) * step;
+            p.c_prev = s == 0 ? nullptr : sc + prv;
             p.ldc_prev = He;
-            p.c_out = tc + s * step;
+            p.c_out = sc + cur;
             p.ldc = He;
-            p.h_out = th + s * step;
+            p.h_out = sh + cur;
             p.ldh = He;
-            p.hA_hi = thi + s * step;
-            p.hA_lo = tlo + s * step;
+            p.hA_hi = shi + cur;
+            p.hA_lo = slo + cur;
             p.ldha = He;
             p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
             ks_status st = launch_lstm(E, p, nullptr, E.enc[dir], nullptr, 0.0);
             if (st) return st;
+            // keep the first R_s rows of step s (R_S = r: the last step's c too)
+            const size_t keep = (size_t)(s == S ? r : T.off[s + 1] - T.off[s]) * He;
+            const size_t at = (size_t)T.off[s] * He;
+            __half* thi = T.hA.as<__half>();
+            KS_CUDA(cudaMemcpyAsync(T.h.as<float>() + at, sh + cur, keep * 4, cudaMemcpyDeviceToDevice, E.stream));
+            KS_CUDA(cudaMemcpyAsync(thi + at, shi + cur, keep * 2, cudaMemcpyDeviceToDevice, E.stream));
+            KS_CUDA(cudaMemcpyAsync(thi + plane + at, slo + cur, keep * 2, cudaMemcpyDeviceToDevice, E.stream));
+            if (s == S) KS_CUDA(cudaMemcpyAsync(T.c.p, sc + cur, keep * 4, cudaMemcpyDeviceToDevice, E.stream));
         }
-        KS_CUDA(cudaStreamSynchronize(E.stream));  // dtok is freed on return
+        KS_CUDA(cudaStreamSynchronize(E.stream));  // dtok and scratch are freed on return
     }
     E.units_now = units_saved;
     E.launches = 0;
@@ -1161,7 +1178,7 @@ struct EncGatherArgs {
     int C, He, S[2];
     int order[2][7];
     long long stride[2][7];
-    long long rows[2];
+    long long off[2][7];
     const float* h[2];
     const float* c[2];
     const __half* hi[2];
@@ -1189,7 +1206,7 @@ __global__ void __launch_bounds__(256) enc_table_gather(EncGatherArgs a) {
         const int* tk = a.tok + (size_t)b * 7;
         long long row = 0;
         for (int x = 0; x <= s; ++x) row += (long long)__ldg(tk + a.order[d][x]) * a.stride[d][x];
-        const size_t src = ((size_t)s * a.rows[d] + row) * a.He + q * 8;
+        const size_t src = ((size_t)a.off[d][s] + row) * a.He + q * 8;
         const int t = a.order[d][s];
         const size_t dst = (size_t)b * a.act_ld + t * a.NA2 + d * a.NA + q * 8;
         const float4* hs = reinterpret_cast<const float4*>(a.h[d] + src);
@@ -1199,7 +1216,7 @@ __global__ void __launch_bounds__(256) enc_table_gather(EncGatherArgs a) {
         *reinterpret_cast<uint4*>(a.ahi + dst) = __ldg(reinterpret_cast<const uint4*>(a.hi[d] + src));
         *reinterpret_cast<uint4*>(a.alo + dst) = __ldg(reinterpret_cast<const uint4*>(a.lo[d] + src));
         if (s == a.S[d]) {
-            const float4* cs = reinterpret_cast<const float4*>(a.c[d] + src);
+            const float4* cs = reinterpret_cast<const float4*>(a.c[d] + (size_t)row * a.He + q * 8);
             float4* cd = reinterpret_cast<float4*>(a.c_last[d] + (size_t)b * a.He + q * 8);
             cd[0] = __ldg(cs);
             cd[1] = __ldg(cs + 1);
@@ -1258,9 +1275,9 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             for (int j = 0; j < 7; ++j) {
                 g.order[d][j] = T.order[j];
                 g.stride[d][j] = T.stride[j];
+                g.off[d][j] = T.off[j];
             }
-            g.rows[d] = T.rows;
-            const size_t plane = (size_t)(T.S + 1) * T.rows * He;
+            const size_t plane = (size_t)T.rows * He;
             g.h[d] = T.h.as<float>();
             g.c[d] = T.c.as<float>();
             g.hi[d] = T.hA.as<__half>();
