@@ -233,23 +233,28 @@ struct ks_engine {
     bool ctxproj = false;
     bool ctxproj_force = false;   // KS_CTXPROJ=force: alpha blocks even where wider than ctx (tests)
     DevMem Pt, actA;
+    DevMem encp;  // shared-prefix encoder tables of the current chunk
     // KS_TC_PAIR=1: gate GEMMs on CTA pairs (M = 256 tiles, tcgen05 cta_group::2)
     bool pair = false;
     // N-tile width of the current chunk's gate GEMMs: tc_units, or 32 when 64-unit
     // tiles would leave SMs idle (small batches; needs the 32-unit weight planes)
     int units_now = 64;
-    // encoder prefix tables (attn / attn-2 with the a_t operand planes): the state of
+    // shared-prefix encoder (attn / attn-2 with the a_t operand planes): the state of
     // encoder step s of a direction depends only on the first s+1 input fields that
-    // direction reads, and those take few values -- every prefix's h, c and split h is
-    // computed once per engine, and a decode gathers the covered steps instead of
-    // running them (KS_ENC_TABLE=0 disables)
+    // direction reads.  When a chunk holds more configs than a step has token
+    // prefixes, the step runs once per PREFIX (all of them, a static shape) instead of
+    // once per config -- a GEMM over the previous step's prefixes whose epilogue fans
+    // each parent out to its children -- and a gather hands every config its states
+    // (KS_ENC_PREFIX=0 disables)
     struct EncTable {
-        int S = -1;                 // steps 0..S covered (-1: none)
+        int S = -1;                 // steps 0..S can run per prefix (-1: none)
         int order[7] = {};          // field read at step j (fwd t = j, bwd t = 6 - j)
-        long long stride[7] = {};   // mixed-radix weight of step j's field in a table row
-        long long off[7] = {};      // first row of step j in the compact table (R_j rows each)
-        int64_t rows = 0;           // compact table rows: sum over steps of R_j = prod_{i<=j} |field_i|
-        DevMem h, c, hA;            // h [rows][He] fp32, c of step S [R_S][He], split planes [2][rows][He]
+        int size[7] = {};           // |field| of step j
+        long long R[7] = {};        // prefixes of step j: prod_{i<=j} size[i]
+        long long off[7] = {};      // first row of step j in the prefix tables (sum_{i<j} R[i])
+        DevMem digits;              // [2][sum R]: step j's new digit of prefix r (r % size[j]) at
+                                    // off[j] + r, then its parent prefix (r / size[j])
+        long long total = 0;        // sum R
     };
     EncTable etab[2];
     bool pair_now() const { return pair && units_now == 64; }
@@ -397,7 +402,7 @@ ks_status upload(DevMem& m, const void* src, size_t bytes) {
     return KS_OK;
 }
 
-ks_status build_enc_tables(ks_engine& E);
+ks_status plan_enc_prefix(ks_engine& E);
 }  // namespace
 
 extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, int32_t precision,
@@ -620,7 +625,7 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         if (kc && std::atoll(kc) > 0) E.chunk = std::atoll(kc);
     }
     cudaDeviceGetAttribute(&E.num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (ks_status st = build_enc_tables(E)) return st;
+    if (ks_status st = plan_enc_prefix(E)) return st;
     *out = eng.release();
     return KS_OK;
 }
@@ -811,6 +816,32 @@ ks_status upload_preds(ks_engine& E, const ks_pred* preds, int n, PredDev& pd) {
     return KS_OK;
 }
 
+// shared-prefix encoder tables of a C-config chunk: covered[d] = the last step of
+// direction d that runs per prefix (steps with no more prefixes than configs), byte
+// offsets of h fp32 / hi / lo [sum R][He], the c ping-pong [2][maxr][He] fp32 and
+// the replicated parent planes [2][maxr][He] fp16
+size_t prefix_layout(const ks_engine& E, int64_t C, int covered[2], size_t at[2][5], size_t maxr[2]) {
+    const int He = E.NA;
+    size_t bytes = 0;
+    for (int d = 0; d < 2; ++d) {
+        const ks_engine::EncTable& T = E.etab[d];
+        int S = -1;
+        while (S < T.S && T.R[S + 1] <= C) ++S;
+        covered[d] = S;
+        maxr[d] = 0;
+        for (int i = 0; i < 5; ++i) at[d][i] = bytes;
+        if (S < 0) continue;
+        const size_t rows = (size_t)(T.off[S] + T.R[S]);
+        for (int j = 0; j <= S; ++j) maxr[d] = std::max(maxr[d], (size_t)T.R[j]);
+        at[d][1] = at[d][0] + rows * He * 4;
+        at[d][2] = at[d][1] + rows * He * 2;
+        at[d][3] = at[d][2] + rows * He * 2;
+        at[d][4] = at[d][3] + 2 * maxr[d] * He * 4;  // replicated parent planes [2][maxr][He]
+        bytes = at[d][4] + 2 * maxr[d] * He * 2;
+    }
+    return bytes;
+}
+
 ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
     const int64_t R = C * k;
     const bool enc_dec = E.variant == KS_VARIANT_ENC_DEC;
@@ -841,6 +872,11 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
         ENS(E.act, C * 7 * (enc_dec ? E.NE : NA2) * 4);
         ENS(E.uatt, C * 7 * E.n_d * 4 + 16);
         ENS(E.encc, 2 * 2 * C * He * 4);
+        if (E.etab[0].S >= 0 || E.etab[1].S >= 0) {
+            int cov[2];
+            size_t at[2][5], maxr[2];
+            ENS(E.encp, prefix_layout(E, C, cov, at, maxr));
+        }
         ENS(E.encA, 2 * 2 * 2 * C * He * 2);   // [dir][pingpong][hi/lo][C][He] fp16
         if (E.precision == KS_PREC_FP32) {
             ENS(E.Abuf, R * Kd * 4);
@@ -891,7 +927,7 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
         done = launch_lstm_tc(a0, a1, E.precision, whi(L0), wlo(L0), L1 ? whi(*L1) : nullptr,
                               L1 ? wlo(*L1) : nullptr, E.stream, &n, E.units_now,
                               E.pair_now() || (E.pair_auto && E.units_now == 64 && a0.kb_alpha == 0 &&
-                                               a0.fan <= 1 && (!a1 || a1->kb_alpha == 0)));
+                                               a0.fan <= 1 && (!a1 || (a1->kb_alpha == 0 && a1->fan <= 1))));
         if (!done) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
     }
     if (!done && a0.K == 0 && launch_lstm_k0(a0, a1, E.num_sms, E.stream)) {
@@ -1073,26 +1109,23 @@ ks_status encode_hybrid(ks_engine& E, int64_t C, const int* d_tok) {
 }
 
 // Decodes one chunk of C configs already resident on the device.
-// ---- encoder prefix tables
-// Table rows enumerate every digit combination of a direction's first S+1 fields
-// (mixed radix, step 0's field least significant).  Step s's state of a row depends
-// only on digits 0..s, so a config's step-s state is the one of the row whose digits
-// 0..s are its tokens and whose later digits are 0 -- one of the first R_s =
-// prod_{j<=s} |field_j| rows, which is all the compact table keeps of step s.  The
-// rows are computed by the decode's own encoder launches (same kernels, same per-row
-// arithmetic), so a gathered state is bit-identical to the one the loop produces.
-ks_status build_enc_tables(ks_engine& E) {
-    const char* env = std::getenv("KS_ENC_TABLE");
+// ---- shared-prefix encoder
+// Prefix r of step j (0 <= r < R_j) is numbered with the newest digit least
+// significant: r = parent * size_j + digit_j, parent = the step-(j-1) prefix, so a
+// config's row at step j is Horner's ((tok_0 * size_1 + tok_1) * size_2 + ...) over
+// the fields it has read.  Step j is one gate-GEMM launch over its R_j prefixes:
+// A row r = the split h of parent r / size_j (the parent planes replicated by
+// enc_prefix_replicate), c_prev through the parent index, slot = digit_j.  (A
+// fan-out epilogue over the R_{j-1} parents does fewer MMAs but its per-child loop is
+// latency-bound: 2-4x slower at these sizes, tools/tiny_gemm.cu.)  The digit and
+// parent arrays depend on the vocabulary sizes only; the states are computed per chunk.
+ks_status plan_enc_prefix(ks_engine& E) {
+    const char* env = std::getenv("KS_ENC_PREFIX");
     const bool on = E.ctxproj && E.precision != KS_PREC_FP32 && !(env && env[0] == '0');
     if (!on) return KS_OK;
     const int He = E.NA;
-    // enumeration rows x units (12 B each, twice, while building) and compact table
-    // elements (12 B each): every step of the BASELINE model (46,656 x 256) fits
-    const char* ce = std::getenv("KS_ENC_TABLE_ELEMS");
-    const int64_t kCapElems = ce ? std::atoll(ce) : (1LL << 24);
-    const int64_t kCapTable = 6 * kCapElems;
-    const int units_saved = E.units_now;
-    E.units_now = E.tc_units;
+    // prefix table elements (h fp32 + split h: 8 B each) and per-step rows x units
+    const int64_t kCapStep = 1LL << 24, kCapTotal = 6LL << 24;
     for (int dir = 0; dir < 2; ++dir) {
         ks_engine::EncTable& T = E.etab[dir];
         T.S = -1;
@@ -1100,76 +1133,26 @@ ks_status build_enc_tables(ks_engine& E) {
         for (int j = 0; j < 7; ++j) {
             const int t = dir == 0 ? j : 6 - j;
             const int64_t r2 = r * E.in_sizes[(size_t)t];
-            if (r2 * He > kCapElems || (total + r2) * He > kCapTable) break;
+            if (r2 * He > kCapStep || (total + r2) * He > kCapTotal) break;
             T.order[j] = t;
-            T.stride[j] = r;
+            T.size[j] = E.in_sizes[(size_t)t];
+            T.R[j] = r2;
             T.off[j] = total;
             total += r2;
             r = r2;
             T.S = j;
         }
         if (T.S < 0) continue;
-        T.rows = total;
-        const int S = T.S;
-        std::vector<int> tok((size_t)r * 7, 0);
-        for (int64_t row = 0; row < r; ++row)
-            for (int j = 0; j <= S; ++j)
-                tok[(size_t)row * 7 + T.order[j]] = (int)((row / T.stride[j]) % E.in_sizes[(size_t)T.order[j]]);
-        DevMem dtok, scratch;
-        const size_t step = (size_t)r * He;
-        const size_t plane = (size_t)total * He;
-        if (dtok.ensure(tok.size() * 4) || scratch.ensure(2 * step * 12) || T.h.ensure(plane * 4) ||
-            T.c.ensure(step * 4) || T.hA.ensure(2 * plane * 2))
-            return set_error(KS_ERR_CUDA, "encoder table allocation failed");
-        KS_CUDA(cudaMemcpyAsync(dtok.p, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, E.stream));
-        KS_CUDA(cudaMemsetAsync(scratch.p, 0, 2 * step * 12, E.stream));
-        // scratch ping-pong: h [2][r][He] fp32, c [2][r][He] fp32, hi / lo [2][r][He]
-        float* sh = scratch.as<float>();
-        float* sc = sh + 2 * step;
-        __half* shi = reinterpret_cast<__half*>(sc + 2 * step);
-        __half* slo = shi + 2 * step;
-        for (int s = 0; s <= S; ++s) {
-            const size_t cur = (size_t)(s & 1) * step, prv = (size_t)((s + 1) & 1) * step;
-            LstmArgs p;
-            std::memset(&p, 0, sizeof p);
-            p.M = (int)r;
-            p.H = He;
-            p.K = s == 0 ? 0 : He;
-            p.A = s == 0 ? nullptr : sh + prv;
-            p.lda = He;
-            p.A_hi = s == 0 ? nullptr : shi + prv;
-            p.A_lo = s == 0 ? nullptr : slo + prv;
-            p.ldah = He;
-            p.W = E.enc[dir].W.as<float>();
-            p.G = E.enc[dir].G.as<float>();
-            p.slot_ptr = dtok.as<int>() + T.order[s];
-            p.slot_stride = 7;
-            p.slot_base = E.in_offset[(size_t)T.order[s]];
-            p.c_prev = s == 0 ? nullptr : sc + prv;
-            p.ldc_prev = He;
-            p.c_out = sc + cur;
-            p.ldc = He;
-            p.h_out = sh + cur;
-            p.ldh = He;
-            p.hA_hi = shi + cur;
-            p.hA_lo = slo + cur;
-            p.ldha = He;
-            p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
-            ks_status st = launch_lstm(E, p, nullptr, E.enc[dir], nullptr, 0.0);
-            if (st) return st;
-            // keep the first R_s rows of step s (R_S = r: the last step's c too)
-            const size_t keep = (size_t)(s == S ? r : T.off[s + 1] - T.off[s]) * He;
-            const size_t at = (size_t)T.off[s] * He;
-            __half* thi = T.hA.as<__half>();
-            KS_CUDA(cudaMemcpyAsync(T.h.as<float>() + at, sh + cur, keep * 4, cudaMemcpyDeviceToDevice, E.stream));
-            KS_CUDA(cudaMemcpyAsync(thi + at, shi + cur, keep * 2, cudaMemcpyDeviceToDevice, E.stream));
-            KS_CUDA(cudaMemcpyAsync(thi + plane + at, slo + cur, keep * 2, cudaMemcpyDeviceToDevice, E.stream));
-            if (s == S) KS_CUDA(cudaMemcpyAsync(T.c.p, sc + cur, keep * 4, cudaMemcpyDeviceToDevice, E.stream));
-        }
-        KS_CUDA(cudaStreamSynchronize(E.stream));  // dtok and scratch are freed on return
+        T.total = total;
+        std::vector<int> dg((size_t)total * 2);
+        for (int j = 0; j <= T.S; ++j)
+            for (int64_t x = 0; x < T.R[j]; ++x) {
+                dg[(size_t)(T.off[j] + x)] = (int)(x % T.size[j]);
+                dg[(size_t)(total + T.off[j] + x)] = (int)(x / T.size[j]);
+            }
+        if (T.digits.ensure(dg.size() * 4)) return set_error(KS_ERR_CUDA, "prefix digit allocation failed");
+        KS_CUDA(cudaMemcpy(T.digits.p, dg.data(), dg.size() * 4, cudaMemcpyHostToDevice));
     }
-    E.units_now = units_saved;
-    E.launches = 0;
     return KS_OK;
 }
 
@@ -1177,51 +1160,186 @@ struct EncGatherArgs {
     const int* tok;              // [C][7]
     int C, He, S[2];
     int order[2][7];
-    long long stride[2][7];
+    int size[2][7];
     long long off[2][7];
-    const float* h[2];
-    const float* c[2];
+    const float* h[2];           // prefix tables [sum R][He] per direction
     const __half* hi[2];
     const __half* lo[2];
+    const float* c[2];           // c of step S[dir] [R_S][He]
     float* act;                  // a_t fp32, row stride act_ld, step t at t*NA2 + dir*NA
     __half* ahi;                 // a_t operand planes (same layout)
     __half* alo;
     long long act_ld, NA2, NA;
-    float* c_last[2];            // encoder c of step S_dir (the loop's ping-pong slot)
+    float* c_last[2];            // the encoder loop's c slot of step S[dir]
 };
 
-// one thread per (config, covered direction-step, 8 units)
-__global__ void __launch_bounds__(256) enc_table_gather(EncGatherArgs a) {
+// one warp per (config, prefix-computed direction-step); lanes stride over 8-unit groups
+__global__ void __launch_bounds__(256) enc_prefix_gather(EncGatherArgs a) {
     const int q8 = a.He / 8;
     const int steps = a.S[0] + 1 + a.S[1] + 1;
-    const long long n = (long long)a.C * steps * q8;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int q = (int)(i % q8);
-        const long long bj = i / q8;
-        const int j = (int)(bj % steps);
-        const int b = (int)(bj / steps);
+    const int lane = threadIdx.x & 31;
+    const unsigned n = (unsigned)a.C * steps;
+    for (unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += (gridDim.x * blockDim.x) >> 5) {
+        const int j = (int)(w % steps);
+        const int b = (int)(w / steps);
         const int d = j <= a.S[0] ? 0 : 1;
         const int s = d == 0 ? j : j - (a.S[0] + 1);
         const int* tk = a.tok + (size_t)b * 7;
         long long row = 0;
-        for (int x = 0; x <= s; ++x) row += (long long)__ldg(tk + a.order[d][x]) * a.stride[d][x];
-        const size_t src = ((size_t)a.off[d][s] + row) * a.He + q * 8;
+        for (int x = 0; x <= s; ++x) row = row * a.size[d][x] + __ldg(tk + a.order[d][x]);
         const int t = a.order[d][s];
-        const size_t dst = (size_t)b * a.act_ld + t * a.NA2 + d * a.NA + q * 8;
-        const float4* hs = reinterpret_cast<const float4*>(a.h[d] + src);
-        float4* hd = reinterpret_cast<float4*>(a.act + dst);
-        hd[0] = __ldg(hs);
-        hd[1] = __ldg(hs + 1);
-        *reinterpret_cast<uint4*>(a.ahi + dst) = __ldg(reinterpret_cast<const uint4*>(a.hi[d] + src));
-        *reinterpret_cast<uint4*>(a.alo + dst) = __ldg(reinterpret_cast<const uint4*>(a.lo[d] + src));
-        if (s == a.S[d]) {
-            const float4* cs = reinterpret_cast<const float4*>(a.c[d] + (size_t)row * a.He + q * 8);
-            float4* cd = reinterpret_cast<float4*>(a.c_last[d] + (size_t)b * a.He + q * 8);
-            cd[0] = __ldg(cs);
-            cd[1] = __ldg(cs + 1);
+        const size_t src0 = ((size_t)a.off[d][s] + row) * a.He;
+        const size_t dst0 = (size_t)b * a.act_ld + t * a.NA2 + d * a.NA;
+        for (int q = lane; q < q8; q += 32) {
+            const size_t src = src0 + q * 8, dst = dst0 + q * 8;
+            const float4* hs = reinterpret_cast<const float4*>(a.h[d] + src);
+            float4* hd = reinterpret_cast<float4*>(a.act + dst);
+            hd[0] = __ldg(hs);
+            hd[1] = __ldg(hs + 1);
+            *reinterpret_cast<uint4*>(a.ahi + dst) = __ldg(reinterpret_cast<const uint4*>(a.hi[d] + src));
+            *reinterpret_cast<uint4*>(a.alo + dst) = __ldg(reinterpret_cast<const uint4*>(a.lo[d] + src));
+            if (s == a.S[d]) {
+                const float4* cs = reinterpret_cast<const float4*>(a.c[d] + (size_t)row * a.He + q * 8);
+                float4* cd = reinterpret_cast<float4*>(a.c_last[d] + (size_t)b * a.He + q * 8);
+                cd[0] = __ldg(cs);
+                cd[1] = __ldg(cs + 1);
+            }
         }
     }
+}
+
+// A operand of a prefix step: row r of the step = the split h of parent r / fan
+struct RepJob {
+    const __half* src_hi;
+    const __half* src_lo;
+    __half* dst_hi;
+    __half* dst_lo;
+    long long rows;
+    int fan;
+};
+
+__global__ void __launch_bounds__(256) enc_prefix_replicate(RepJob j0, RepJob j1, int He) {
+    const RepJob& j = blockIdx.y == 0 ? j0 : j1;
+    const int q8 = He / 8;
+    const long long n = j.rows * q8;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / q8;
+        const int q = (int)(i - r * q8);
+        const size_t src = (size_t)(r / j.fan) * He + q * 8, dst = (size_t)r * He + q * 8;
+        *reinterpret_cast<uint4*>(j.dst_hi + dst) = __ldg(reinterpret_cast<const uint4*>(j.src_hi + src));
+        *reinterpret_cast<uint4*>(j.dst_lo + dst) = __ldg(reinterpret_cast<const uint4*>(j.src_lo + src));
+    }
+}
+
+// Runs the prefix steps of both directions (step s of every direction that covers
+// it in one launch) and gathers every config's states of those steps into a_t, its
+// operand planes and the encoder loop's c slot.  covered[d] = the last such step.
+ks_status encode_prefix(ks_engine& E, int64_t C, const int* d_tok, float* act, __half* ahi, __half* alo,
+                        long long act_ld, int NA2, float* c_slot0, float* c_slot1, int covered[2]) {
+    const int He = E.NA;
+    size_t at[2][5], maxr[2];
+    const size_t bytes = prefix_layout(E, C, covered, at, maxr);
+    if (covered[0] < 0 && covered[1] < 0) return KS_OK;
+    if (E.encp.ensure(bytes)) return set_error(KS_ERR_CUDA, "prefix table allocation failed");
+    char* base = E.encp.as<char>();
+    auto H = [&](int d) { return reinterpret_cast<float*>(base + at[d][0]); };
+    auto HI = [&](int d) { return reinterpret_cast<__half*>(base + at[d][1]); };
+    auto LO = [&](int d) { return reinterpret_cast<__half*>(base + at[d][2]); };
+    auto CB = [&](int d, int s) { return reinterpret_cast<float*>(base + at[d][3]) + (size_t)(s & 1) * maxr[d] * He; };
+    auto REP = [&](int d) { return reinterpret_cast<__half*>(base + at[d][4]); };
+    ks_status st;
+    for (int s = 0; s <= std::max(covered[0], covered[1]); ++s) {
+        LstmArgs a[2];
+        int na = 0, dd[2];
+        RepJob rj[2];
+        int nr = 0;
+        for (int d = 0; d < 2; ++d) {
+            if (s > covered[d]) continue;
+            const ks_engine::EncTable& T = E.etab[d];
+            LstmArgs& p = a[na];
+            dd[na++] = d;
+            std::memset(&p, 0, sizeof p);
+            const size_t prev = s ? (size_t)T.off[s - 1] * He : 0, cur = (size_t)T.off[s] * He;
+            const bool rep = s > 0 && T.size[s] > 1;
+            if (rep) {
+                RepJob& j = rj[nr++];
+                j.src_hi = HI(d) + prev;
+                j.src_lo = LO(d) + prev;
+                j.dst_hi = REP(d);
+                j.dst_lo = REP(d) + maxr[d] * He;
+                j.rows = T.R[s];
+                j.fan = T.size[s];
+            }
+            p.M = (int)T.R[s];
+            p.H = He;
+            p.K = s == 0 ? 0 : He;
+            p.A = s == 0 ? nullptr : H(d) + prev;
+            p.lda = He;
+            p.A_hi = s == 0 ? nullptr : rep ? REP(d) : HI(d) + prev;
+            p.A_lo = s == 0 ? nullptr : rep ? REP(d) + maxr[d] * He : LO(d) + prev;
+            p.ldah = He;
+            p.W = E.enc[d].W.as<float>();
+            p.G = E.enc[d].G.as<float>();
+            p.slot_ptr = T.digits.as<int>() + T.off[s];
+            p.slot_stride = 1;
+            p.slot_base = E.in_offset[(size_t)T.order[s]];
+            p.c_prev = s == 0 ? nullptr : CB(d, s - 1);
+            p.ldc_prev = He;
+            p.parent = rep ? T.digits.as<int>() + T.total + T.off[s] : nullptr;
+            p.c_out = CB(d, s);
+            p.ldc = He;
+            p.h_out = H(d) + cur;
+            p.ldh = He;
+            p.hA_hi = HI(d) + cur;
+            p.hA_lo = LO(d) + cur;
+            p.ldha = He;
+            p.ha_bf16 = E.precision == KS_PREC_BF16 ? 1 : 0;
+        }
+        if (na == 0) continue;
+        if (nr) {
+            long long n = 0;
+            for (int i = 0; i < nr; ++i) n = std::max(n, rj[i].rows * (long long)(He / 8));
+            enc_prefix_replicate<<<dim3((unsigned)std::min<long long>((n + 255) / 256, 8LL * E.num_sms), (unsigned)nr),
+                                   256, 0, E.stream>>>(rj[0], rj[1], He);
+            E.launches++;
+            KS_CUDA(cudaGetLastError());
+        }
+        double fl = 0.0;
+        for (int i = 0; i < na; ++i) fl += s == 0 ? 0.0 : 2.0 * (double)a[i].M * He * 4.0 * He;
+        if ((st = launch_lstm(E, a[0], na == 2 ? &a[1] : nullptr, E.enc[dd[0]], na == 2 ? &E.enc[1] : nullptr, fl)))
+            return st;
+    }
+    EncGatherArgs g;
+    std::memset(&g, 0, sizeof g);
+    g.tok = d_tok;
+    g.C = (int)C;
+    g.He = He;
+    for (int d = 0; d < 2; ++d) {
+        const ks_engine::EncTable& T = E.etab[d];
+        g.S[d] = covered[d];
+        for (int j = 0; j < 7; ++j) {
+            g.order[d][j] = T.order[j];
+            g.size[d][j] = T.size[j];
+            g.off[d][j] = T.off[j];
+        }
+        if (covered[d] < 0) continue;
+        g.h[d] = H(d);
+        g.hi[d] = HI(d);
+        g.lo[d] = LO(d);
+        g.c[d] = CB(d, covered[d]);
+        g.c_last[d] = (covered[d] & 1) ? c_slot1 + (size_t)d * 2 * C * He : c_slot0 + (size_t)d * 2 * C * He;
+    }
+    g.act = act;
+    g.ahi = ahi;
+    g.alo = alo;
+    g.act_ld = act_ld;
+    g.NA2 = NA2;
+    g.NA = E.NA;
+    const long long warps = C * (long long)(g.S[0] + 1 + g.S[1] + 1);
+    enc_prefix_gather<<<(unsigned)std::min<long long>((warps + 7) / 8, 16LL * E.num_sms), 256, 0, E.stream>>>(g);
+    E.launches++;
+    KS_CUDA(cudaGetLastError());
+    return KS_OK;
 }
 
 // reuse_encoder: the chunk's encoder outputs (a_t, encoder state, P^T, hybrid
@@ -1260,41 +1378,12 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
     if (!reuse_encoder && hybrid && (st = encode_hybrid(E, C, d_tok))) return st;
     // ---- encoder (bi-LSTM over the 7 one-hot input steps, zero initial state)
     const int dirs = enc_dec ? 1 : 2;
-    // covered steps of each direction come from the prefix tables (to_actA engines)
+    // steps with fewer token prefixes than the chunk has configs run per prefix
     int covered[2] = {-1, -1};
-    if (!reuse_encoder && !hybrid && !enc_dec && split && E.ctxproj &&
-        (E.etab[0].S >= 0 || E.etab[1].S >= 0)) {
-        EncGatherArgs g;
-        std::memset(&g, 0, sizeof g);
-        g.tok = d_tok;
-        g.C = (int)C;
-        g.He = He;
-        for (int d = 0; d < 2; ++d) {
-            const ks_engine::EncTable& T = E.etab[d];
-            g.S[d] = covered[d] = T.S;
-            for (int j = 0; j < 7; ++j) {
-                g.order[d][j] = T.order[j];
-                g.stride[d][j] = T.stride[j];
-                g.off[d][j] = T.off[j];
-            }
-            const size_t plane = (size_t)T.rows * He;
-            g.h[d] = T.h.as<float>();
-            g.c[d] = T.c.as<float>();
-            g.hi[d] = T.hA.as<__half>();
-            g.lo[d] = T.hA.as<__half>() + plane;
-            g.c_last[d] = T.S >= 0 ? encc_at(d, T.S & 1) : nullptr;
-        }
-        g.act = act;
-        g.ahi = E.actA.as<__half>();
-        g.alo = g.ahi + (size_t)C * 7 * NA2;
-        g.act_ld = act_ld;
-        g.NA2 = NA2;
-        g.NA = E.NA;
-        const long long n = C * (long long)(g.S[0] + 1 + g.S[1] + 1) * (He / 8);
-        enc_table_gather<<<(unsigned)std::min<long long>((n + 255) / 256, 16LL * E.num_sms), 256, 0, s>>>(g);
-        E.launches++;
-        KS_CUDA(cudaGetLastError());
-    }
+    if (!reuse_encoder && !hybrid && !enc_dec && split && E.ctxproj && (E.etab[0].S >= 0 || E.etab[1].S >= 0) &&
+        (st = encode_prefix(E, C, d_tok, act, E.actA.as<__half>(), E.actA.as<__half>() + (size_t)C * 7 * NA2, act_ld,
+                            NA2, encc_at(0, 0), encc_at(0, 1), covered)))
+        return st;
     for (int sidx = 0; sidx < ((hybrid || reuse_encoder) ? 0 : 7); ++sidx) {
         LstmArgs a[2];
         for (int dir = 0; dir < dirs; ++dir) {

@@ -339,17 +339,28 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
         for (int i = 0; i < 4; ++i) cp[i] = cn[i];
         if (c + 1 < NCH) load_c(c + 1, cn);
         const int u0 = nt * UNITS + uc + tcol;
-        // child f of the thread's 4 rows at a time: their slot and G loads are independent
+        // child f of the thread's 4 rows at a time.  The 4 slots of child f+1 load while
+        // child f computes, and child f's 16 G loads issue together: one load latency per
+        // child instead of a slot -> G chain per row
+        int sl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            sl[i] = (valid[i] && p.slot_ptr) ? __ldg(p.slot_ptr + (long long)rows[i] * fan * p.slot_stride) : 0;
 #pragma unroll 1
         for (int f = 0; f < fan; ++f) {
             float2 gz[4][4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const long long r = (long long)rows[i] * fan + f;
-                const int slot = valid[i] ? p.slot_base + (p.slot_ptr ? p.slot_ptr[r * p.slot_stride] : 0) : 0;
-                const float* G = p.G + (long long)slot * 4 * p.H;
+                const float* G = p.G + ((long long)(p.slot_base + sl[i]) * 4 * p.H + u0);
 #pragma unroll
-                for (int gt = 0; gt < 4; ++gt) gz[i][gt] = *reinterpret_cast<const float2*>(G + gt * p.H + u0);
+                for (int gt = 0; gt < 4; ++gt) gz[i][gt] = __ldg(reinterpret_cast<const float2*>(G + gt * p.H));
+            }
+            if (f + 1 < fan) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    sl[i] = (valid[i] && p.slot_ptr)
+                                ? __ldg(p.slot_ptr + ((long long)rows[i] * fan + f + 1) * p.slot_stride)
+                                : 0;
             }
             float hv[4][2], cv[4][2];
 #pragma unroll
@@ -383,14 +394,26 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
                     tc::bulk_commit();
                 }
                 stg_buf ^= 1;
-                continue;
+                if (p.hA_hi == nullptr) continue;
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 if (!valid[i]) continue;
                 const long long r = (long long)rows[i] * fan + f;
-                __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[i][0], hv[i][1]));
-                __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[i][0], cv[i][1]));
+                if (!bulk) {
+                    __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv[i][0], hv[i][1]));
+                    __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv[i][0], cv[i][1]));
+                }
+                // split h (the shared-prefix encoder's next operand)
+                if (p.hA_hi != nullptr && p.ha_bf16) {
+                    *reinterpret_cast<__nv_bfloat162*>(p.hA_hi + r * p.ldha + u0) =
+                        __floats2bfloat162_rn(hv[i][0], hv[i][1]);
+                } else if (p.hA_hi != nullptr) {
+                    __half2 hh, hl;
+                    split_f16x2(hv[i][0], hv[i][1], hh, hl);
+                    *reinterpret_cast<__half2*>(p.hA_hi + r * p.ldha + u0) = hh;
+                    *reinterpret_cast<__half2*>(p.hA_lo + r * p.ldha + u0) = hl;
+                }
             }
         }
     }
@@ -827,8 +850,8 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
             }();
             pr.p.drop_pass = drop;
         }
-        // the fan-out epilogue writes only h and c of the children
-        if (a.fan > 1 && (a.h_out2 != nullptr || a.hA_hi != nullptr || a.raw)) return false;
+        // the fan-out epilogue writes h, c and the split h of the children
+        if (a.fan > 1 && (a.h_out2 != nullptr || a.raw)) return false;
         {
             static const bool bulk_out = [] {
                 const char* e = std::getenv("KS_BULK_OUT");

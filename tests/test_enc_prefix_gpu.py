@@ -1,7 +1,9 @@
-"""Encoder prefix tables (ks_engine.cu build_enc_tables / enc_table_gather): the
-covered encoder steps gathered from the per-engine tables must give decodes
-bit-identical to running every encoder step (KS_ENC_TABLE=0), on the BASELINE
-model and on random models whose vocabularies cover different step counts."""
+"""Shared-prefix encoder (ks_engine.cu encode_prefix / enc_prefix_gather): encoder
+steps run once per token prefix (fan-out epilogue over the previous step's
+prefixes) and gathered per config must give decodes bit-identical to running every
+encoder step per config (KS_ENC_PREFIX=0) -- on the BASELINE model at chunk sizes
+that cover different step counts (all 7 steps of both directions at 60,000 configs)
+and on random models."""
 import os
 
 import numpy as np
@@ -15,15 +17,15 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs 
 def _decode(path, prec, tok, k, preds, table, chunk=None):
     from paper_2404_10162_b200._cabi import Engine
 
-    old = os.environ.get("KS_ENC_TABLE")
-    os.environ["KS_ENC_TABLE"] = "1" if table else "0"
+    old = os.environ.get("KS_ENC_PREFIX")
+    os.environ["KS_ENC_PREFIX"] = "1" if table else "0"
     try:
         e = Engine(path, 0, prec)
     finally:
         if old is None:
-            os.environ.pop("KS_ENC_TABLE")
+            os.environ.pop("KS_ENC_PREFIX")
         else:
-            os.environ["KS_ENC_TABLE"] = old
+            os.environ["KS_ENC_PREFIX"] = old
     if chunk:
         e.set_chunk(chunk)
     return e.beam(tok, k, None, preds)
@@ -34,16 +36,17 @@ def _same(a, b):
         assert np.array_equal(a[key], b[key]), key
 
 
-@pytest.mark.parametrize("prec", ["f16x3", "bf16"])
-def test_tables_bit_identical_default_model(prec):
+@pytest.mark.parametrize("prec,B,chunk", [("f16x3", 6000, 2500), ("bf16", 6000, 2500), ("f16x3", 60000, None),
+                                          ("f16x3", 3000, 700)])
+def test_tables_bit_identical_default_model(prec, B, chunk):
     from paper_2404_10162_b200 import workloads as W
     from paper_2404_10162_b200._cabi import Engine
 
     path = W.DEFAULT_CKPT
     e = Engine(path, 0, prec)
-    tok = e.encode(e.synthetic(6000, W.SEED, 123))
+    tok = e.encode(e.synthetic(B, W.SEED, 123))
     preds = W.predicate_dicts(path)
-    _same(_decode(path, prec, tok, 5, preds, True, 2500), _decode(path, prec, tok, 5, preds, False, 2500))
+    _same(_decode(path, prec, tok, 5, preds, True, chunk), _decode(path, prec, tok, 5, preds, False, chunk))
 
 
 @pytest.mark.parametrize("case", range(3))
