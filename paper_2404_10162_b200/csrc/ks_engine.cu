@@ -256,6 +256,9 @@ struct ks_engine {
                                     // off[j] + r, then its parent prefix (r / size[j])
         long long total = 0;        // sum R
     };
+    // chunks below this many configs encode per config: their launches are latency-bound,
+    // so the prefix steps' extra launches (replicate, gather) cost more than they save
+    int64_t prefix_min = 16384;
     EncTable etab[2];
     bool pair_now() const { return pair && units_now == 64; }
     bool proj_at(int pos, int H) const {
@@ -826,7 +829,7 @@ size_t prefix_layout(const ks_engine& E, int64_t C, int covered[2], size_t at[2]
     for (int d = 0; d < 2; ++d) {
         const ks_engine::EncTable& T = E.etab[d];
         int S = -1;
-        while (S < T.S && T.R[S + 1] <= C) ++S;
+        while (C >= E.prefix_min && S < T.S && T.R[S + 1] <= C) ++S;
         covered[d] = S;
         maxr[d] = 0;
         for (int i = 0; i < 5; ++i) at[d][i] = bytes;
@@ -1124,6 +1127,7 @@ ks_status plan_enc_prefix(ks_engine& E) {
     const bool on = E.ctxproj && E.precision != KS_PREC_FP32 && !(env && env[0] == '0');
     if (!on) return KS_OK;
     const int He = E.NA;
+    if (const char* pm = std::getenv("KS_ENC_PREFIX_MIN")) E.prefix_min = std::atoll(pm);
     // prefix table elements (h fp32 + split h: 8 B each) and per-step rows x units
     const int64_t kCapStep = 1LL << 24, kCapTotal = 6LL << 24;
     for (int dir = 0; dir < 2; ++dir) {

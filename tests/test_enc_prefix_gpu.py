@@ -17,15 +17,18 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs 
 def _decode(path, prec, tok, k, preds, table, chunk=None):
     from paper_2404_10162_b200._cabi import Engine
 
-    old = os.environ.get("KS_ENC_PREFIX")
-    os.environ["KS_ENC_PREFIX"] = "1" if table else "0"
+    # KS_ENC_PREFIX_MIN=0: the prefix steps also at the small chunks of these cases
+    env = {"KS_ENC_PREFIX": "1" if table else "0", "KS_ENC_PREFIX_MIN": "0"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         e = Engine(path, 0, prec)
     finally:
-        if old is None:
-            os.environ.pop("KS_ENC_PREFIX")
-        else:
-            os.environ["KS_ENC_PREFIX"] = old
+        for name, val in old.items():
+            if val is None:
+                os.environ.pop(name)
+            else:
+                os.environ[name] = val
     if chunk:
         e.set_chunk(chunk)
     return e.beam(tok, k, None, preds)
