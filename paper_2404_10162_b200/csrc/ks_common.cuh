@@ -103,6 +103,18 @@ struct LstmArgs {
     const __half* PT_lo;
     long long ldpt;
     long long pt_rows;     // K extent of P^T (C * 7); reads beyond are zero-filled
+    // compacted alpha-block positions (cp_M != null): rows are the DISTINCT live parents
+    // of the position, *cp_M of them (M is the bound); row r belongs to config
+    // cp_cfg[r] (the alpha-block tile spans configs cp_cfg[first row .. last row]), its
+    // c_prev row is cp_prow[r], and its children are cp_child[cp_cstart[r] ..
+    // + cp_ccount[r]) = {child row, slot} pairs (epilogue_compact)
+    const int* cp_M;
+    const int* cp_cfg;
+    const int* cp_prow;
+    const int* cp_cstart;
+    const int* cp_ccount;
+    const int2* cp_child;
+    int g_first, g_count;  // G rows the children's slots fall in (staged in shared memory)
 };
 
 struct AttnArgs {
@@ -132,6 +144,11 @@ struct AttnArgs {
     int kalpha;
     int alpha_tile;        // rows of the GEMM tile the alpha block is laid out for (128 / 256)
     int alpha_sparse;      // alpha-block layout unchanged since the last position: write the 7 values only
+    // compacted rows (LstmArgs::cp_M): row r = config cp_cfg[r], h_prev row cp_prow[r];
+    // the alpha block follows the 128-row GEMM tile of r
+    const int* cp_M;
+    const int* cp_cfg;
+    const int* cp_prow;
 };
 
 // Scales of the alpha-block MMA (F16X3): alpha in [0, 1] carries 2^12, P carries

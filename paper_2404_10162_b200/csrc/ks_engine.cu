@@ -234,6 +234,12 @@ struct ks_engine {
     bool ctxproj_force = false;   // KS_CTXPROJ=force: alpha blocks even where wider than ctx (tests)
     DevMem Pt, actA;
     DevMem encp;  // shared-prefix encoder tables of the current chunk
+    // compacted alpha-block positions: the GEMM and attention run on each
+    // config's distinct live parents, the epilogue writes their children
+    // (auto: decoders of >= 1024 units, whose h-part MMA hides the longer fan-out
+    // epilogue; KS_COMPACT=0 / 1 forces it off / on)
+    bool compact = false;
+    DevMem cpbuf;  // [C] counts, [C + 1] bases (last = rows), [R] cfg, prow, cstart, ccount, [R] int2 children
     // KS_TC_PAIR=1: gate GEMMs on CTA pairs (M = 256 tiles, tcgen05 cta_group::2)
     bool pair = false;
     // N-tile width of the current chunk's gate GEMMs: tc_units, or 32 when 64-unit
@@ -243,9 +249,9 @@ struct ks_engine {
     // encoder step s of a direction depends only on the first s+1 input fields that
     // direction reads.  When a chunk holds more configs than a step has token
     // prefixes, the step runs once per PREFIX (all of them, a static shape) instead of
-    // once per config -- a GEMM over the previous step's prefixes whose epilogue fans
-    // each parent out to its children -- and a gather hands every config its states
-    // (KS_ENC_PREFIX=0 disables)
+    // once per config -- one gate-GEMM launch over the step's prefixes, the parents'
+    // split h replicated as its A operand -- and a gather hands every config its
+    // states (KS_ENC_PREFIX=0 disables)
     struct EncTable {
         int S = -1;                 // steps 0..S can run per prefix (-1: none)
         int order[7] = {};          // field read at step j (fwd t = j, bwd t = 6 - j)
@@ -624,6 +630,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.use_graphs = !(kg && kg[0] == '0');
         const char* pr = std::getenv("KS_TC_PAIR_AUTO");
         E.pair_auto = !(pr && pr[0] == '0');
+        const char* kcp = std::getenv("KS_COMPACT");
+        E.compact = kcp ? kcp[0] == '1' : E.NS >= 1024;
         const char* kc = std::getenv("KS_CHUNK");
         if (kc && std::atoll(kc) > 0) E.chunk = std::atoll(kc);
     }
@@ -891,6 +899,7 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
         ENS(E.hbuf, 2 * R * Hd * 4);
         ENS(E.cbuf, 2 * R * Hd * 4);
         if (E.ctxproj) {
+            ENS(E.cpbuf, (2 * C + 2 + 4 * R) * 4 + R * 8 + 16);
             const int64_t ldt = (C * 7 + 7) / 8 * 8;
             ENS(E.Pt, 2 * 4 * (int64_t)Hd * ldt * 2);   // [hi/lo][4NS][ldt] fp16
             ENS(E.actA, 2 * C * 7 * (int64_t)NA2 * 2);
@@ -1235,6 +1244,124 @@ __global__ void __launch_bounds__(256) enc_prefix_replicate(RepJob j0, RepJob j1
     }
 }
 
+// ---- parent compaction (alpha-block positions)
+// Row b*H + i of a position is child i of config b; siblings (same parent) share the
+// gate GEMM's A row ([alpha | h_prev]: attention runs on the parent's h) and c_prev.
+// cp_count: distinct live parents per config (>= 1: a config without live rows keeps
+// one dummy row, so a 128-row GEMM tile spans at most 128 configs and the alpha block
+// stays within alpha_cols_for(128, 1) columns), and each block's total.
+__device__ __forceinline__ int cp_distinct(const int* pa, const unsigned char* lv, int H) {
+    int n = 0;
+    for (int i = 0; i < H; ++i) {
+        if (!lv[i]) continue;
+        bool seen = false;
+        for (int j = 0; j < i && !seen; ++j) seen = lv[j] && pa[j] == pa[i];
+        n += !seen;
+    }
+    return n > 0 ? n : 1;
+}
+
+__global__ void __launch_bounds__(256) cp_count(const int* __restrict__ parent, const unsigned char* __restrict__ live,
+                                                int C, int H, int* __restrict__ cnt, int* __restrict__ part) {
+    __shared__ int ws[8];
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    int n = 0;
+    if (b < C) {
+        n = cp_distinct(parent + (size_t)b * H, live + (size_t)b * H, H);
+        cnt[b] = n;
+    }
+    int x = n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < 8; ++w) t += ws[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+// compacted rows of config b from base_b = (totals of the previous blocks) + (the
+// block's exclusive scan); parents in first-occurrence order, each row's children
+// {row, slot} grouped in child[b*H ..]; the last block writes the row count
+__global__ void __launch_bounds__(256) cp_fill(const int* __restrict__ parent, const unsigned char* __restrict__ live,
+                                               const int* __restrict__ slot, int C, int H,
+                                               const int* __restrict__ cnt, const int* __restrict__ part,
+                                               int* __restrict__ total, int* __restrict__ cfg,
+                                               int* __restrict__ prow, int* __restrict__ cstart,
+                                               int* __restrict__ ccount, int2* __restrict__ child) {
+    __shared__ int ws[8];
+    __shared__ int off_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        int t = 0;
+        for (int j = lane; j < (int)blockIdx.x; j += 32) t += part[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) off_s = t;
+    }
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = b < C ? cnt[b] : 0;
+    int x = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    int pre = off_s;
+    for (int w = 0; w < warp; ++w) pre += ws[w];
+    int rc = pre + x - n;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) *total = rc + n;
+    if (b >= C) return;
+    const int* pa = parent + (size_t)b * H;
+    const unsigned char* lv = live + (size_t)b * H;
+    int q = b * H;
+    bool any = false;
+    for (int i = 0; i < H; ++i) {
+        if (!lv[i]) continue;
+        bool seen = false;
+        for (int j = 0; j < i && !seen; ++j) seen = lv[j] && pa[j] == pa[i];
+        if (seen) continue;
+        any = true;
+        cfg[rc] = b;
+        prow[rc] = pa[i];
+        cstart[rc] = q;
+        int m = 0;
+        for (int j = i; j < H; ++j)
+            if (lv[j] && pa[j] == pa[i]) {
+                child[q++] = make_int2(b * H + j, slot ? slot[(size_t)b * H + j] : 0);
+                ++m;
+            }
+        ccount[rc] = m;
+        ++rc;
+    }
+    if (!any) {  // the dummy row of a config without live rows
+        cfg[rc] = b;
+        prow[rc] = -1;
+        cstart[rc] = q;
+        ccount[rc] = 0;
+    }
+}
+
+__global__ void dbg_parents(const int* parent, const unsigned char* live, int C, int H, unsigned long long* acc) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= C) return;
+    int n = 0, nl = 0;
+    for (int i = 0; i < H; ++i) {
+        if (!live[(size_t)b * H + i]) continue;
+        ++nl;
+        bool seen = false;
+        for (int j = 0; j < i; ++j)
+            if (live[(size_t)b * H + j] && parent[(size_t)b * H + j] == parent[(size_t)b * H + i]) seen = true;
+        n += !seen;
+    }
+    atomicAdd(acc, (unsigned long long)n);
+    atomicAdd(acc + 1, (unsigned long long)nl);
+}
+
 // Runs the prefix steps of both directions (step s of every direction that covers
 // it in one launch) and gathers every config's states of those steps into a_t, its
 // operand planes and the encoder loop's c slot.  covered[d] = the last such step.
@@ -1547,6 +1674,35 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         const bool fan = pos == 1 && H > 1 && !enc_dec && !hybrid && E.precision != KS_PREC_FP32 &&
                          E.ctxproj && !E.pair_now();
         const int Mg = fan ? (int)C : M;  // rows of this position's attention and gate GEMM
+        // positions >= 2 (alpha blocks): attention and the gate GEMM run on each config's
+        // distinct live parents (compacted rows, 128-row tiles), the GEMM epilogue writes
+        // their children
+        const int g_first = E.variant == KS_VARIANT_ATTN2 ? 0 : (pos > 0 ? E.meta.fb_offset[pos - 1] : 0);
+        const int g_count = E.variant == KS_VARIANT_ATTN2 ? 1 : (pos > 0 ? E.vsize[(size_t)pos - 1] : 1);
+        const bool compact = E.compact && pos >= 2 && !fan && H > 1 && !enc_dec && !hybrid &&
+                             E.precision != KS_PREC_FP32 && E.proj_at(pos, H) && !E.pair_now() &&
+                             g_count * (4 * E.units_now + 8) * 4 <= 32768;  // staged G (epilogue_compact)
+        int *cp_cnt = nullptr, *cp_base = nullptr, *cp_cfg = nullptr, *cp_prow = nullptr, *cp_cst = nullptr,
+            *cp_ccn = nullptr;
+        int2* cp_child = nullptr;
+        const int kal_c = E.alpha_cols_for(128, 1);  // <= 128 configs per 128-row tile
+        if (compact) {
+            cp_cnt = E.cpbuf.as<int>();
+            cp_base = cp_cnt + C;
+            cp_cfg = cp_base + C + 2;
+            cp_prow = cp_cfg + M;
+            cp_cst = cp_prow + M;
+            cp_ccn = cp_cst + M;
+            cp_child = reinterpret_cast<int2*>(
+                (reinterpret_cast<uintptr_t>(cp_ccn + M) + 7) & ~static_cast<uintptr_t>(7));
+            const unsigned g = (unsigned)((C + 255) / 256);
+            const int* slots = E.variant == KS_VARIANT_ATTN2 ? nullptr : E.slot[cur].as<int>();
+            cp_count<<<g, 256, 0, s>>>(par, E.live[cur].as<unsigned char>(), (int)C, H, cp_cnt, cp_base);
+            cp_fill<<<g, 256, 0, s>>>(par, E.live[cur].as<unsigned char>(), slots, (int)C, H, cp_cnt, cp_base,
+                                      cp_base + C, cp_cfg, cp_prow, cp_cst, cp_ccn, cp_child);
+            E.launches += 2;
+            KS_CUDA(cudaGetLastError());
+        }
         AttnArgs aa{};
         aa.M = Mg;
         aa.H_rows = fan ? 1 : H;
@@ -1573,6 +1729,15 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         // same rows and layout as the previous alpha-block position: its zeros are still in place
         aa.alpha_sparse = (aa.kalpha && alpha_fill_H == H) ? 1 : 0;
         alpha_fill_H = aa.kalpha ? H : -1;
+        if (compact) {
+            aa.kalpha = kal_c;
+            aa.alpha_tile = 128;
+            aa.alpha_sparse = 0;
+            alpha_fill_H = -1;  // the next position rewrites its layout in full
+            aa.cp_M = cp_base + C;
+            aa.cp_cfg = cp_cfg;
+            aa.cp_prow = cp_prow;
+        }
         if (enc_dec) aa.nd = 0;
         if (!hybrid) {
             if (!launch_attention(aa, pos == 0 && !enc_dec, s))
@@ -1630,6 +1795,20 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.ldpt = (C * 7 + 7) / 8 * 8;
             p.PT_lo = p.PT_hi + (size_t)4 * Hd * p.ldpt;
             p.pt_rows = C * 7;
+            if (compact) {
+                p.K = kal_c + Hd;
+                p.kb_alpha = kal_c / kTcBK;
+                p.alpha_tile = 128;
+                p.parent = nullptr;
+                p.cp_M = cp_base + C;
+                p.cp_cfg = cp_cfg;
+                p.cp_prow = cp_prow;
+                p.cp_cstart = cp_cst;
+                p.cp_ccount = cp_ccn;
+                p.cp_child = cp_child;
+                p.g_first = g_first;
+                p.g_count = g_count;
+            }
         }
         const double useful = 2.0 * (double)M * (double)(2 * E.n_a * (enc_dec ? 0 : 1) + (enc_dec ? E.e : E.n_s)) *
                               4.0 * (enc_dec ? E.e : E.n_s);
@@ -1733,6 +1912,17 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         E.launches++;
         const cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("beam launch: ") + cudaGetErrorString(err));
+        if (std::getenv("KS_DEBUG_PARENTS") && pos + 1 < E.T) {
+            static DevMem acc;
+            acc.ensure(16);
+            cudaMemsetAsync(acc.p, 0, 16, s);
+            dbg_parents<<<(unsigned)((C + 255) / 256), 256, 0, s>>>(E.parent[nxt].as<int>(), E.live[nxt].as<unsigned char>(), (int)C, Hn, acc.as<unsigned long long>());
+            unsigned long long hv[2];
+            cudaMemcpyAsync(hv, acc.p, 16, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            fprintf(stderr, "pos %d -> %d: rows/config %d, live %.3f, distinct parents %.3f\n", pos, pos + 1, Hn,
+                    (double)hv[1] / C, (double)hv[0] / C);
+        }
         H = Hn;
     }
     if (keys_ready) {

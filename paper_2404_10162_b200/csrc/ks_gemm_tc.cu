@@ -56,12 +56,20 @@ struct TileK {
     int nkb;    // total K-blocks of the tile
 };
 // mt indexes alpha tiles of TR rows (<= 128 -- config-aligned tiles hold whole
-// configs -- or 256 = one CTA pair)
-__device__ __forceinline__ TileK tile_k(const LstmArgs& p, int k_blocks, int mt, int TR) {
+// configs -- or 256 = one CTA pair); compacted rows (cp_cfg): the tile's first and
+// last configs come from the row -> config map, Mv = the rows of the launch
+__device__ __forceinline__ TileK tile_k(const LstmArgs& p, int k_blocks, int mt, int TR, int Mv) {
     TileK r{0, 0, k_blocks};
     if (p.kb_alpha > 0) {
-        const int b0 = (mt * TR) / p.rows_per_cfg;
-        const int b1 = (mt * TR + TR - 1) / p.rows_per_cfg;
+        int b0, b1;
+        if (p.cp_cfg) {
+            const int last = (mt * TR + TR < Mv ? mt * TR + TR : Mv) - 1;
+            b0 = p.cp_cfg[mt * TR];
+            b1 = p.cp_cfg[last];
+        } else {
+            b0 = (mt * TR) / p.rows_per_cfg;
+            b1 = (mt * TR + TR - 1) / p.rows_per_cfg;
+        }
         r.x0 = (7 * b0) & ~7;
         r.kba_t = (7 * (b1 + 1) - r.x0 + kTcBK - 1) / kTcBK;
         if (r.kba_t > p.kb_alpha) r.kba_t = p.kb_alpha;
@@ -419,6 +427,136 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
     }
 }
 
+// Compacted-row cell epilogue: row r of the tile is a distinct live parent
+// (epilogue_fan's sharing, with a variable number of children per parent): each
+// child gets gates = D(r) + G[slot(child)], c_prev = c(cp_prow[r]), and its h / c at
+// its own (uncompacted) row.  Children of the thread's 4 rows are visited together;
+// the {row, slot} pairs of child f+1 load while child f computes.
+template <int UNITS, bool SPLIT, int CG>
+__device__ __forceinline__ void epilogue_compact(const LstmArgs& p, int Mv, uint64_t* bars, uint32_t tmem_base,
+                                                 int acc, uint32_t acc_phase, int row0, int nt, int q, int half,
+                                                 int lane, int tfull, int tempty, int acc_cols, bool leader,
+                                                 float* gst) {
+    constexpr int HU = UNITS / 2;
+    constexpr int NCH = HU / 8;
+    constexpr int GS = 4 * UNITS + 8;  // staged G row stride (floats): slots 8 banks apart
+    const int tq = lane >> 2, tcol = 2 * (lane & 3);
+    // the tile's N slice of the G rows the children can use, staged once per tile by the
+    // 8 epilogue warps (the bulk-store staging area is free in this mode); the first
+    // barrier keeps the previous tile's readers ahead of the overwrite
+    {
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int et = threadIdx.x - 128;
+        const int n4 = p.g_count * UNITS;  // float4 per staged slot: 4 gates x UNITS / 4
+        for (int i = et; i < n4; i += 256) {
+            const int sl = i / UNITS, rem = i - sl * UNITS, gt = rem / (UNITS / 4), u4 = rem - gt * (UNITS / 4);
+            const float4 g = __ldg(reinterpret_cast<const float4*>(p.G + (long long)(p.g_first + sl) * 4 * p.H +
+                                                                   gt * p.H + nt * UNITS) + u4);
+            *reinterpret_cast<float4*>(gst + sl * GS + gt * UNITS + 4 * u4) = g;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+    int cst[4], ccnt[4], prow[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = row0 + q * 32 + 16 * (i >> 1) + tq + 8 * (i & 1);
+        const bool v = row < Mv;
+        cst[i] = v ? p.cp_cstart[row] : 0;
+        ccnt[i] = v ? p.cp_ccount[row] : 0;
+        prow[i] = v ? p.cp_prow[row] : -1;
+    }
+    const int e1 = ccnt[0], e2 = e1 + ccnt[1], e3 = e2 + ccnt[2], tot = e3 + ccnt[3];
+    const int tmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)tot);
+    const bool have_cprev = p.c_prev != nullptr;
+    float2 cn[4];
+    auto load_c = [&](int c, float2 (&cx)[4]) {
+        const int u0 = nt * UNITS + half * HU + c * 8 + tcol;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            cx[i] = (prow[i] >= 0 && have_cprev)
+                        ? *reinterpret_cast<const float2*>(p.c_prev + (long long)prow[i] * p.ldc_prev + u0)
+                        : make_float2(0.f, 0.f);
+    };
+    load_c(0, cn);
+    tc::mbar_wait(tc::smem_u32(&bars[tfull + acc]), acc_phase);
+    tc::fence_after();
+    const uint32_t tq_base = tmem_base + ((uint32_t)(q * 32) << 16) + acc * acc_cols;
+    constexpr float sc = SPLIT ? kSplitUnscale : 1.0f;
+    const float2 sc2 = make_float2(sc, sc);
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+        const int uc = half * HU + c * 8;
+        float v[2][4][4];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt)
+                tc::tmem_ld16x256(tq_base + ((uint32_t)(16 * g) << 16) + gt * UNITS + uc, v[g][gt]);
+        tc::tmem_wait_ld();
+        if (c == NCH - 1) {
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2 && !leader)
+                    tc::mbar_arrive_remote(tc::smem_u32(&bars[tempty + acc]), 0);
+                else
+                    tc::mbar_arrive(tc::smem_u32(&bars[tempty + acc]));
+            }
+        }
+        float2 cp[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp[i] = cn[i];
+        if (c + 1 < NCH) load_c(c + 1, cn);
+        const int u0 = nt * UNITS + uc + tcol;
+        // the children of the thread's 4 rows in one flat loop (j -> row i, its child
+        // j - e_i): a warp iterates max_lanes(sum of children) times, not 4 x max fan
+        auto child_of = [&](int j) -> int2 {
+            if (j >= tot) return make_int2(-1, p.g_first);
+            const int base = j < e1 ? cst[0] : j < e2 ? cst[1] - e1 : j < e3 ? cst[2] - e2 : cst[3] - e3;
+            return __ldg(p.cp_child + base + j);
+        };
+        // four children per iteration (8 cells in flight); the next four children's
+        // {row, slot} loads are issued before this group's math
+        int2 nx[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nx[k] = child_of(k);
+#pragma unroll 1
+        for (int j = 0; j < tmax; j += 4) {
+            int2 cur[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                cur[k] = nx[k];
+                nx[k] = child_of(j + 4 + k);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int jj = j + k;
+                const int i = jj < e1 ? 0 : jj < e2 ? 1 : jj < e3 ? 2 : 3;
+                const float* G = gst + (cur[k].y - p.g_first) * GS + uc + tcol;
+                float2 z[4];
+#pragma unroll
+                for (int gt = 0; gt < 4; ++gt) {
+                    const float2 gz = *reinterpret_cast<const float2*>(G + gt * UNITS);
+                    const float a0 =
+                        i == 0 ? v[0][gt][0] : i == 1 ? v[0][gt][2] : i == 2 ? v[1][gt][0] : v[1][gt][2];
+                    const float a1 =
+                        i == 0 ? v[0][gt][1] : i == 1 ? v[0][gt][3] : i == 2 ? v[1][gt][1] : v[1][gt][3];
+                    z[gt] = __ffma2_rn(make_float2(a0, a1), sc2, gz);
+                }
+                const float2 cpi = i == 0 ? cp[0] : i == 1 ? cp[1] : i == 2 ? cp[2] : cp[3];
+                float hv0, hv1, cv0, cv1;
+                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cpi.x, cv0, hv0);
+                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cpi.y, cv1, hv1);
+                if (cur[k].x >= 0) {
+                    const long long r = cur[k].x;
+                    __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv0, hv1));
+                    __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv0, cv1));
+                }
+            }
+        }
+    }
+}
+
 template <int UNITS, bool SPLIT, int CG>
 __global__ void __launch_bounds__(384, 1)
     lstm_gemm_tc(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap mA0,
@@ -481,13 +619,22 @@ __global__ void __launch_bounds__(384, 1)
     if (CG == 2) tc::cluster_sync();  // the peer's barriers are initialised before any remote arrive
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // compacted rows (one problem): the row count is device data written by the
+    // compaction before this launch; the tile loop covers ceil(Mv / TR) row tiles
+    const int Mv = P.prob[0].p.cp_M ? *P.prob[0].p.cp_M : P.prob[0].p.M;
+    int total_tiles = P.total_tiles;
+    if (P.prob[0].p.cp_M) {
+        const int tr = tile_rows(P.prob[0].p);
+        const int dyn = (Mv + tr - 1) / tr * P.prob[0].n_tiles;
+        total_tiles = dyn < total_tiles ? dyn : total_tiles;
+    }
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cid; t < P.total_tiles; t += ncl) {
+            for (int t = cid; t < total_tiles; t += ncl) {
                 const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
                 const TcProblem& pr = P.prob[pi];
                 const int lt = t - pr.tile_begin;
@@ -501,7 +648,7 @@ __global__ void __launch_bounds__(384, 1)
                 const CUtensorMap* mbl = pi ? &mBl1 : &mBl0;
                 // alpha-block mode: B K-blocks [0, kba_t) come from P^T (held in the
                 // second problem's map slots) from column x0 on (see tile_k)
-                const TileK tk = tile_k(pr.p, pr.k_blocks, mt, TRp);
+                const TileK tk = tile_k(pr.p, pr.k_blocks, mt, TRp, Mv);
                 for (int kb = 0; kb < tk.nkb; ++kb) {
                     tc::mbar_wait(tc::smem_u32(&bars[S + stage]), phase ^ 1);
                     const uint32_t full = tc::smem_u32(&bars[stage]);
@@ -540,11 +687,11 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = cid; t < P.total_tiles; t += ncl) {
+            for (int t = cid; t < total_tiles; t += ncl) {
                 const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
                 const TcProblem& pr = P.prob[pi];
                 const int mt_i = (t - pr.tile_begin) / pr.n_tiles;
-                const int nkb = tile_k(pr.p, pr.k_blocks, mt_i, tile_rows(pr.p)).nkb;
+                const int nkb = tile_k(pr.p, pr.k_blocks, mt_i, tile_rows(pr.p), Mv).nkb;
                 tc::mbar_wait(tc::smem_u32(&bars[2 * S + AS + acc]), acc_phase ^ 1);
                 tc::fence_after();
                 const uint32_t d1 = tmem_base + acc * Cfg::ACC_COLS;
@@ -601,7 +748,7 @@ __global__ void __launch_bounds__(384, 1)
         int stg_buf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = cid; t < P.total_tiles; t += ncl) {
+        for (int t = cid; t < total_tiles; t += ncl) {
             const int pi = (P.n_prob > 1 && t >= P.prob[1].tile_begin) ? 1 : 0;
             const TcProblem& pr = P.prob[pi];
             const LstmArgs& p = pr.p;
@@ -613,7 +760,11 @@ __global__ void __launch_bounds__(384, 1)
                 // cell mode: 16x256b TMEM loads, so the 4 lanes of a quad hold 2 consecutive
                 // units each of the same row -- every h / c / split-h store instruction
                 // writes whole 32-byte row segments (half the L1 wavefronts of row-per-lane)
-                if (p.fan > 1)
+                if (p.cp_M)
+                    epilogue_compact<UNITS, SPLIT, CG>(
+                        p, Mv, bars, tmem_base, acc, acc_phase, row0, nt, q, half, lane, 2 * S, 2 * S + AS,
+                        Cfg::ACC_COLS, leader, reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES + 256));
+                else if (p.fan > 1)
                     epilogue_fan<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half, lane,
                                                    2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, pr, stg, stg_buf);
                 else
@@ -852,6 +1003,11 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         }
         // the fan-out epilogue writes h, c and the split h of the children
         if (a.fan > 1 && (a.h_out2 != nullptr || a.raw)) return false;
+        // compacted rows: one alpha-block problem on single-CTA 128-row tiles, h / c only
+        if (a.cp_M && (a1 || CG == 2 || a.kb_alpha == 0 || a.alpha_tile != TC_BM || a.fan > 1 || a.raw ||
+                       a.hA_hi || a.h_out2 || a.g_count < 1 ||
+                       (size_t)a.g_count * (4 * UNITS + 8) * 4 > (size_t)Cfg::OUT_STAGE))
+            return false;
         {
             static const bool bulk_out = [] {
                 const char* e = std::getenv("KS_BULK_OUT");
@@ -864,7 +1020,7 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
                                  ? 1
                                  : 0;
             else
-                pr.tma_out = bulk_out && a.h_out && a.c_out &&
+                pr.tma_out = bulk_out && !a.cp_M && a.h_out && a.c_out &&
                                      make_out_map(&pr.mh, a.h_out, a.M, fan, a.H, a.ldh) &&
                                      make_out_map(&pr.mc, a.c_out, a.M, fan, a.H, a.ldc)
                                  ? 1

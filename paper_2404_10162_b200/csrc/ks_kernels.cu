@@ -258,7 +258,17 @@ template <int SPLIT>
 __device__ __forceinline__ void write_alpha_block(const AttnArgs& p, int r, int b, const float (&al)[kTin],
                                                   int lane) {
     // column of alpha_0 = 7 * b - x0, x0 = 7 * b0 rounded down to 8 (see tile_k, ks_gemm_tc.cu)
-    const int b0 = (r / p.alpha_tile * p.alpha_tile) / p.H_rows;
+    int b0 = (r / p.alpha_tile * p.alpha_tile) / p.H_rows;
+    int width = p.kalpha;
+    if (p.cp_cfg) {  // compacted rows: the tile's configs from the row -> config map
+        const int Mv = *p.cp_M;
+        const int t0 = r / p.alpha_tile * p.alpha_tile;
+        const int last = (t0 + p.alpha_tile < Mv ? t0 + p.alpha_tile : Mv) - 1;
+        b0 = p.cp_cfg[t0];
+        const int cols = kTin * (p.cp_cfg[last] + 1) - ((kTin * b0) & ~7);
+        width = (cols + 63) / 64 * 64;  // the K-blocks the GEMM contracts for this tile
+        width = width < p.kalpha ? width : p.kalpha;
+    }
     const int c0 = kTin * b - ((kTin * b0) & ~7);
     const long long base = (long long)r * (p.kalpha + p.NS);
     if (p.alpha_sparse) {  // the previous position left this layout's zeros in place
@@ -277,7 +287,7 @@ __device__ __forceinline__ void write_alpha_block(const AttnArgs& p, int r, int 
         }
         return;
     }
-    for (int c = lane; c < p.kalpha / 8; c += 32) {
+    for (int c = lane; c < width / 8; c += 32) {
         float v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -304,8 +314,8 @@ __device__ __forceinline__ void write_alpha_block(const AttnArgs& p, int r, int 
 
 template <int ND, int SPLIT, bool FIRST>
 __device__ __forceinline__ void attention_row(const AttnArgs& p, int r, int lane) {
-    const int b = r / p.H_rows;
-    const int par = p.parent ? p.parent[r] : r;
+    const int b = p.cp_cfg ? p.cp_cfg[r] : r / p.H_rows;
+    const int par = p.cp_prow ? p.cp_prow[r] : p.parent ? p.parent[r] : r;
     const float* s = (p.h_prev != nullptr && par >= 0) ? p.h_prev + (long long)par * p.ldh : nullptr;
     const int Kd = p.kalpha ? p.kalpha + p.NS : p.NA2 + p.NS;
     const int hc = p.kalpha ? p.kalpha : p.NA2;  // column of h_prev in the operand
@@ -425,8 +435,10 @@ __device__ __forceinline__ void attention_row(const AttnArgs& p, int r, int lane
 template <int ND, int SPLIT, bool FIRST>
 __global__ void __launch_bounds__(256) attention_pack_t(AttnArgs p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // persistent: one warp per row, grid-strided (the grid is sized to one resident wave)
-    for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < p.M; r += gridDim.x * (blockDim.x >> 5))
+    // persistent: one warp per row, grid-strided (the grid is sized to one resident wave);
+    // compacted rows: *cp_M of them
+    const int M = p.cp_M ? *p.cp_M : p.M;
+    for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < M; r += gridDim.x * (blockDim.x >> 5))
         attention_row<ND, SPLIT, FIRST>(p, r, lane);
 }
 
@@ -621,9 +633,9 @@ void launch_attention_nd(const AttnArgs& p, bool first, cudaStream_t s) {
     };
     if (first) {
         attention_pack_t<ND, SPLIT, true><<<wave(attention_pack_t<ND, SPLIT, true>, (p.M + 7) / 8), 256, 0, s>>>(p);
-    } else if (mode == 0 && p.H_rows > 1 && p.H_rows <= 64 && p.kalpha == 0) {
+    } else if (mode == 0 && p.H_rows > 1 && p.H_rows <= 64 && p.kalpha == 0 && !p.cp_M) {
         attention_cta_t<ND, SPLIT><<<(unsigned)(p.M / p.H_rows), 128, 0, s>>>(p);
-    } else if (mode == 2 && p.H_rows > 1) {
+    } else if (mode == 2 && p.H_rows > 1 && !p.cp_M) {
         const int C = p.M / p.H_rows;
         attention_cfg_t<ND, SPLIT><<<(unsigned)((C + 7) / 8), 256, 0, s>>>(p);
     } else {
