@@ -107,14 +107,14 @@ struct LstmArgs {
     // of the position, *cp_M of them (M is the bound); row r belongs to config
     // cp_cfg[r] (the alpha-block tile spans configs cp_cfg[first row .. last row]), its
     // c_prev row is cp_prow[r], and its children are cp_child[cp_cstart[r] ..
-    // + cp_ccount[r]) = {child row, slot} pairs (epilogue_compact)
+    // + cp_ccount[r]) = {child row, slot, r, cp_prow[r]} (epilogue_compact); the
+    // children of consecutive rows are consecutive entries
     const int* cp_M;
     const int* cp_cfg;
     const int* cp_prow;
     const int* cp_cstart;
     const int* cp_ccount;
-    const int2* cp_child;
-    int g_first, g_count;  // G rows the children's slots fall in (staged in shared memory)
+    const int4* cp_child;
 };
 
 struct AttnArgs {

@@ -899,7 +899,7 @@ ks_status ensure_workspace(ks_engine& E, int64_t C, int k) {
         ENS(E.hbuf, 2 * R * Hd * 4);
         ENS(E.cbuf, 2 * R * Hd * 4);
         if (E.ctxproj) {
-            ENS(E.cpbuf, (2 * C + 2 + 4 * R) * 4 + R * 8 + 16);
+            ENS(E.cpbuf, (2 * C + 2 + 4 * R) * 4 + R * 16 + 16);
             const int64_t ldt = (C * 7 + 7) / 8 * 8;
             ENS(E.Pt, 2 * 4 * (int64_t)Hd * ldt * 2);   // [hi/lo][4NS][ldt] fp16
             ENS(E.actA, 2 * C * 7 * (int64_t)NA2 * 2);
@@ -1290,7 +1290,7 @@ __global__ void __launch_bounds__(256) cp_fill(const int* __restrict__ parent, c
                                                const int* __restrict__ cnt, const int* __restrict__ part,
                                                int* __restrict__ total, int* __restrict__ cfg,
                                                int* __restrict__ prow, int* __restrict__ cstart,
-                                               int* __restrict__ ccount, int2* __restrict__ child) {
+                                               int* __restrict__ ccount, int4* __restrict__ child) {
     __shared__ int ws[8];
     __shared__ int off_s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1332,7 +1332,7 @@ __global__ void __launch_bounds__(256) cp_fill(const int* __restrict__ parent, c
         int m = 0;
         for (int j = i; j < H; ++j)
             if (lv[j] && pa[j] == pa[i]) {
-                child[q++] = make_int2(b * H + j, slot ? slot[(size_t)b * H + j] : 0);
+                child[q++] = make_int4(b * H + j, slot ? slot[(size_t)b * H + j] : 0, rc, pa[i]);
                 ++m;
             }
         ccount[rc] = m;
@@ -1344,6 +1344,8 @@ __global__ void __launch_bounds__(256) cp_fill(const int* __restrict__ parent, c
         cstart[rc] = q;
         ccount[rc] = 0;
     }
+    // entries of dead children: skipped by the epilogue (it walks entry ranges)
+    for (; q < (b + 1) * H; ++q) child[q] = make_int4(-1, 0, -1, -1);
 }
 
 __global__ void dbg_parents(const int* parent, const unsigned char* live, int C, int H, unsigned long long* acc) {
@@ -1677,14 +1679,11 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         // positions >= 2 (alpha blocks): attention and the gate GEMM run on each config's
         // distinct live parents (compacted rows, 128-row tiles), the GEMM epilogue writes
         // their children
-        const int g_first = E.variant == KS_VARIANT_ATTN2 ? 0 : (pos > 0 ? E.meta.fb_offset[pos - 1] : 0);
-        const int g_count = E.variant == KS_VARIANT_ATTN2 ? 1 : (pos > 0 ? E.vsize[(size_t)pos - 1] : 1);
         const bool compact = E.compact && pos >= 2 && !fan && H > 1 && !enc_dec && !hybrid &&
-                             E.precision != KS_PREC_FP32 && E.proj_at(pos, H) && !E.pair_now() &&
-                             g_count * (4 * E.units_now + 8) * 4 <= 32768;  // staged G (epilogue_compact)
+                             E.precision != KS_PREC_FP32 && E.proj_at(pos, H) && !E.pair_now();
         int *cp_cnt = nullptr, *cp_base = nullptr, *cp_cfg = nullptr, *cp_prow = nullptr, *cp_cst = nullptr,
             *cp_ccn = nullptr;
-        int2* cp_child = nullptr;
+        int4* cp_child = nullptr;
         const int kal_c = E.alpha_cols_for(128, 1);  // <= 128 configs per 128-row tile
         if (compact) {
             cp_cnt = E.cpbuf.as<int>();
@@ -1693,8 +1692,8 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             cp_prow = cp_cfg + M;
             cp_cst = cp_prow + M;
             cp_ccn = cp_cst + M;
-            cp_child = reinterpret_cast<int2*>(
-                (reinterpret_cast<uintptr_t>(cp_ccn + M) + 7) & ~static_cast<uintptr_t>(7));
+            cp_child = reinterpret_cast<int4*>(
+                (reinterpret_cast<uintptr_t>(cp_ccn + M) + 15) & ~static_cast<uintptr_t>(15));
             const unsigned g = (unsigned)((C + 255) / 256);
             const int* slots = E.variant == KS_VARIANT_ATTN2 ? nullptr : E.slot[cur].as<int>();
             cp_count<<<g, 256, 0, s>>>(par, E.live[cur].as<unsigned char>(), (int)C, H, cp_cnt, cp_base);
@@ -1806,8 +1805,6 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
                 p.cp_cstart = cp_cst;
                 p.cp_ccount = cp_ccn;
                 p.cp_child = cp_child;
-                p.g_first = g_first;
-                p.g_count = g_count;
             }
         }
         const double useful = 2.0 * (double)M * (double)(2 * E.n_a * (enc_dec ? 0 : 1) + (enc_dec ? E.e : E.n_s)) *

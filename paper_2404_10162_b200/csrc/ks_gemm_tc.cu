@@ -428,56 +428,31 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
 }
 
 // Compacted-row cell epilogue: row r of the tile is a distinct live parent
-// (epilogue_fan's sharing, with a variable number of children per parent): each
-// child gets gates = D(r) + G[slot(child)], c_prev = c(cp_prow[r]), and its h / c at
-// its own (uncompacted) row.  Children of the thread's 4 rows are visited together;
-// the {row, slot} pairs of child f+1 load while child f computes.
+// (epilogue_fan's sharing, with a variable number of children per parent).  Per
+// 8-unit chunk the warp stages its 32 parents' pre-activations in shared memory
+// (4 KB, the bulk-store staging area, unused in this mode), then its 8 lane quads
+// take the warp's children round-robin -- the children of consecutive rows are
+// consecutive cp_child entries, so the load is balanced whatever the fan-outs --
+// each child: gates = D(parent) + G[slot], c_prev = c(cp_prow[parent]), h / c at the
+// child's own row.  The next round's entry, G and c_prev loads are in flight during
+// a round's math.
 template <int UNITS, bool SPLIT, int CG>
 __device__ __forceinline__ void epilogue_compact(const LstmArgs& p, int Mv, uint64_t* bars, uint32_t tmem_base,
                                                  int acc, uint32_t acc_phase, int row0, int nt, int q, int half,
                                                  int lane, int tfull, int tempty, int acc_cols, bool leader,
-                                                 float* gst) {
+                                                 float* sp) {
     constexpr int HU = UNITS / 2;
     constexpr int NCH = HU / 8;
-    constexpr int GS = 4 * UNITS + 8;  // staged G row stride (floats): slots 8 banks apart
     const int tq = lane >> 2, tcol = 2 * (lane & 3);
-    // the tile's N slice of the G rows the children can use, staged once per tile by the
-    // 8 epilogue warps (the bulk-store staging area is free in this mode); the first
-    // barrier keeps the previous tile's readers ahead of the overwrite
-    {
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const int et = threadIdx.x - 128;
-        const int n4 = p.g_count * UNITS;  // float4 per staged slot: 4 gates x UNITS / 4
-        for (int i = et; i < n4; i += 256) {
-            const int sl = i / UNITS, rem = i - sl * UNITS, gt = rem / (UNITS / 4), u4 = rem - gt * (UNITS / 4);
-            const float4 g = __ldg(reinterpret_cast<const float4*>(p.G + (long long)(p.g_first + sl) * 4 * p.H +
-                                                                   gt * p.H + nt * UNITS) + u4);
-            *reinterpret_cast<float4*>(gst + sl * GS + gt * UNITS + 4 * u4) = g;
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+    // the warp's parents: rows wr0 .. wr1-1; their children: entries [e0, e1)
+    const int wr0 = row0 + q * 32;
+    const int wr1 = wr0 + 32 < Mv ? wr0 + 32 : Mv;
+    int e0 = 0, e1 = 0;
+    if (wr0 < wr1) {
+        e0 = p.cp_cstart[wr0];
+        e1 = p.cp_cstart[wr1 - 1] + p.cp_ccount[wr1 - 1];
     }
-    int cst[4], ccnt[4], prow[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int row = row0 + q * 32 + 16 * (i >> 1) + tq + 8 * (i & 1);
-        const bool v = row < Mv;
-        cst[i] = v ? p.cp_cstart[row] : 0;
-        ccnt[i] = v ? p.cp_ccount[row] : 0;
-        prow[i] = v ? p.cp_prow[row] : -1;
-    }
-    const int e1 = ccnt[0], e2 = e1 + ccnt[1], e3 = e2 + ccnt[2], tot = e3 + ccnt[3];
-    const int tmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)tot);
     const bool have_cprev = p.c_prev != nullptr;
-    float2 cn[4];
-    auto load_c = [&](int c, float2 (&cx)[4]) {
-        const int u0 = nt * UNITS + half * HU + c * 8 + tcol;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            cx[i] = (prow[i] >= 0 && have_cprev)
-                        ? *reinterpret_cast<const float2*>(p.c_prev + (long long)prow[i] * p.ldc_prev + u0)
-                        : make_float2(0.f, 0.f);
-    };
-    load_c(0, cn);
     tc::mbar_wait(tc::smem_u32(&bars[tfull + acc]), acc_phase);
     tc::fence_after();
     const uint32_t tq_base = tmem_base + ((uint32_t)(q * 32) << 16) + acc * acc_cols;
@@ -503,55 +478,58 @@ __device__ __forceinline__ void epilogue_compact(const LstmArgs& p, int Mv, uint
                     tc::mbar_arrive(tc::smem_u32(&bars[tempty + acc]));
             }
         }
-        float2 cp[4];
+        // parents' scaled pre-activations: sp[row][gate][8 units]
+        __syncwarp();  // the previous chunk's readers are done
 #pragma unroll
-        for (int i = 0; i < 4; ++i) cp[i] = cn[i];
-        if (c + 1 < NCH) load_c(c + 1, cn);
+        for (int i = 0; i < 4; ++i) {
+            const int g = i >> 1, j = i & 1;
+            const int lr = 16 * g + tq + 8 * j;
+#pragma unroll
+            for (int gt = 0; gt < 4; ++gt)
+                *reinterpret_cast<float2*>(sp + (lr * 4 + gt) * 8 + tcol) =
+                    make_float2(v[g][gt][2 * j] * sc, v[g][gt][2 * j + 1] * sc);
+        }
+        __syncwarp();
         const int u0 = nt * UNITS + uc + tcol;
-        // the children of the thread's 4 rows in one flat loop (j -> row i, its child
-        // j - e_i): a warp iterates max_lanes(sum of children) times, not 4 x max fan
-        auto child_of = [&](int j) -> int2 {
-            if (j >= tot) return make_int2(-1, p.g_first);
-            const int base = j < e1 ? cst[0] : j < e2 ? cst[1] - e1 : j < e3 ? cst[2] - e2 : cst[3] - e3;
-            return __ldg(p.cp_child + base + j);
-        };
-        // four children per iteration (8 cells in flight); the next four children's
-        // {row, slot} loads are issued before this group's math
-        int2 nx[4];
+        auto fetch = [&](int e, int4& en, float2 (&gz)[4], float2& cpv) {
+            if (e < e1) {
+                en = __ldg(p.cp_child + e);
+                const float* G = p.G + ((long long)(p.slot_base + (en.x >= 0 ? en.y : 0)) * 4 * p.H + u0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) nx[k] = child_of(k);
-#pragma unroll 1
-        for (int j = 0; j < tmax; j += 4) {
-            int2 cur[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                cur[k] = nx[k];
-                nx[k] = child_of(j + 4 + k);
+                for (int gt = 0; gt < 4; ++gt) gz[gt] = __ldg(reinterpret_cast<const float2*>(G + gt * p.H));
+                cpv = (have_cprev && en.w >= 0)
+                          ? *reinterpret_cast<const float2*>(p.c_prev + (long long)en.w * p.ldc_prev + u0)
+                          : make_float2(0.f, 0.f);
+            } else {
+                en = make_int4(-1, 0, wr0, -1);
             }
+        };
+        int4 en;
+        float2 gz[4], cpv = make_float2(0.f, 0.f);
+        fetch(e0 + tq, en, gz, cpv);
+#pragma unroll 1
+        for (int e = e0 + tq; e < e1; e += 8) {
+            const int4 cur = en;
+            float2 g4[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int jj = j + k;
-                const int i = jj < e1 ? 0 : jj < e2 ? 1 : jj < e3 ? 2 : 3;
-                const float* G = gst + (cur[k].y - p.g_first) * GS + uc + tcol;
-                float2 z[4];
+            for (int gt = 0; gt < 4; ++gt) g4[gt] = gz[gt];
+            const float2 cp = cpv;
+            fetch(e + 8, en, gz, cpv);
+            const int lp = (unsigned)(cur.z - wr0) < 32u ? cur.z - wr0 : 0;  // dead-child entries: no store
+            const float* d = sp + (lp * 4) * 8 + tcol;
+            float2 z[4];
 #pragma unroll
-                for (int gt = 0; gt < 4; ++gt) {
-                    const float2 gz = *reinterpret_cast<const float2*>(G + gt * UNITS);
-                    const float a0 =
-                        i == 0 ? v[0][gt][0] : i == 1 ? v[0][gt][2] : i == 2 ? v[1][gt][0] : v[1][gt][2];
-                    const float a1 =
-                        i == 0 ? v[0][gt][1] : i == 1 ? v[0][gt][3] : i == 2 ? v[1][gt][1] : v[1][gt][3];
-                    z[gt] = __ffma2_rn(make_float2(a0, a1), sc2, gz);
-                }
-                const float2 cpi = i == 0 ? cp[0] : i == 1 ? cp[1] : i == 2 ? cp[2] : cp[3];
-                float hv0, hv1, cv0, cv1;
-                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cpi.x, cv0, hv0);
-                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cpi.y, cv1, hv1);
-                if (cur[k].x >= 0) {
-                    const long long r = cur[k].x;
-                    __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv0, hv1));
-                    __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv0, cv1));
-                }
+            for (int gt = 0; gt < 4; ++gt) {
+                const float2 dv = *reinterpret_cast<const float2*>(d + gt * 8);
+                z[gt] = make_float2(dv.x + g4[gt].x, dv.y + g4[gt].y);
+            }
+            float hv0, hv1, cv0, cv1;
+            lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp.x, cv0, hv0);
+            lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp.y, cv1, hv1);
+            if (cur.x >= 0) {
+                const long long r = cur.x;
+                __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv0, hv1));
+                __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv0, cv1));
             }
         }
     }
@@ -761,9 +739,8 @@ __global__ void __launch_bounds__(384, 1)
                 // units each of the same row -- every h / c / split-h store instruction
                 // writes whole 32-byte row segments (half the L1 wavefronts of row-per-lane)
                 if (p.cp_M)
-                    epilogue_compact<UNITS, SPLIT, CG>(
-                        p, Mv, bars, tmem_base, acc, acc_phase, row0, nt, q, half, lane, 2 * S, 2 * S + AS,
-                        Cfg::ACC_COLS, leader, reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES + 256));
+                    epilogue_compact<UNITS, SPLIT, CG>(p, Mv, bars, tmem_base, acc, acc_phase, row0, nt, q, half,
+                                                       lane, 2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, stg);
                 else if (p.fan > 1)
                     epilogue_fan<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half, lane,
                                                    2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, pr, stg, stg_buf);
@@ -1005,8 +982,7 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         if (a.fan > 1 && (a.h_out2 != nullptr || a.raw)) return false;
         // compacted rows: one alpha-block problem on single-CTA 128-row tiles, h / c only
         if (a.cp_M && (a1 || CG == 2 || a.kb_alpha == 0 || a.alpha_tile != TC_BM || a.fan > 1 || a.raw ||
-                       a.hA_hi || a.h_out2 || a.g_count < 1 ||
-                       (size_t)a.g_count * (4 * UNITS + 8) * 4 > (size_t)Cfg::OUT_STAGE))
+                       a.hA_hi || a.h_out2))
             return false;
         {
             static const bool bulk_out = [] {
