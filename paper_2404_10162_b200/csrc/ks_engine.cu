@@ -962,6 +962,23 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
             if (a.K <= 0) return 0.0;
             const double passes = E.precision == KS_PREC_F16X3 ? 3.0 : 1.0;
             double rowk = (double)a.M * a.K;
+            if (a.cp_M) {
+                // compacted rows: the row count and the tiles' configs are device data
+                // (profiling runs only: a synchronous read-back)
+                int mc = 0;
+                cudaMemcpyAsync(&mc, a.cp_M, 4, cudaMemcpyDeviceToHost, E.stream);
+                cudaStreamSynchronize(E.stream);
+                std::vector<int> cfg((size_t)std::max(mc, 1));
+                cudaMemcpy(cfg.data(), a.cp_cfg, (size_t)mc * 4, cudaMemcpyDeviceToHost);
+                rowk = 0.0;
+                for (int r0 = 0; r0 < mc; r0 += a.alpha_tile) {
+                    const int r1 = std::min(mc, r0 + a.alpha_tile);
+                    const int x0 = (7 * cfg[(size_t)r0]) & ~7;
+                    const int kba = std::min(a.kb_alpha, (7 * (cfg[(size_t)r1 - 1] + 1) - x0 + kTcBK - 1) / kTcBK);
+                    rowk += (double)(r1 - r0) * (a.K - (double)kTcBK * (a.kb_alpha - kba));
+                }
+                return 2.0 * rowk * 4.0 * a.H * passes;
+            }
             if (a.kb_alpha > 0) {
                 rowk = 0.0;
                 const int TR = a.alpha_tile;
