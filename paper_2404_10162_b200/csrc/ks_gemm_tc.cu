@@ -504,38 +504,54 @@ __device__ __forceinline__ void epilogue_compact(const LstmArgs& p, int Mv, uint
                 en = make_int4(-1, 0, wr0, -1);
             }
         };
-        int4 en;
-        float2 gz[4], cpv = make_float2(0.f, 0.f);
-        fetch(e0 + tq, en, gz, cpv);
+        // two children per quad per round (entries e and e + 8), the next round's two
+        // in flight during this round's math
+        constexpr int KC = 2;
+        int4 en[KC];
+        float2 gz[KC][4], cpv[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            cpv[k] = make_float2(0.f, 0.f);
+            fetch(e0 + tq + 8 * k, en[k], gz[k], cpv[k]);
+        }
 #pragma unroll 1
-        for (int e = e0 + tq; e < e1; e += 8) {
-            const int4 cur = en;
-            float2 g4[4];
+        for (int e = e0 + tq; e < e1; e += 8 * KC) {
+            int4 cur[KC];
+            float2 g4[KC][4], cp[KC];
 #pragma unroll
-            for (int gt = 0; gt < 4; ++gt) g4[gt] = gz[gt];
-            const float2 cp = cpv;
-            fetch(e + 8, en, gz, cpv);
-            const int lp = (unsigned)(cur.z - wr0) < 32u ? cur.z - wr0 : 0;  // dead-child entries: no store
-            const float* d = sp + (lp * 4) * 8 + tcol;
-            float2 z[4];
+            for (int k = 0; k < KC; ++k) {
+                cur[k] = en[k];
 #pragma unroll
-            for (int gt = 0; gt < 4; ++gt) {
-                const float2 dv = *reinterpret_cast<const float2*>(d + gt * 8);
-                z[gt] = make_float2(dv.x + g4[gt].x, dv.y + g4[gt].y);
+                for (int gt = 0; gt < 4; ++gt) g4[k][gt] = gz[k][gt];
+                cp[k] = cpv[k];
+                fetch(e + 8 * (KC + k), en[k], gz[k], cpv[k]);
             }
-            float hv0, hv1, cv0, cv1;
-            lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp.x, cv0, hv0);
-            lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp.y, cv1, hv1);
-            if (cur.x >= 0) {
-                const long long r = cur.x;
-                __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv0, hv1));
-                __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv0, cv1));
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const int lp = (unsigned)(cur[k].z - wr0) < 32u ? cur[k].z - wr0 : 0;  // dead-child entries: no store
+                const float* d = sp + (lp * 4) * 8 + tcol;
+                float2 z[4];
+#pragma unroll
+                for (int gt = 0; gt < 4; ++gt) {
+                    const float2 dv = *reinterpret_cast<const float2*>(d + gt * 8);
+                    z[gt] = make_float2(dv.x + g4[k][gt].x, dv.y + g4[k][gt].y);
+                }
+                float hv0, hv1, cv0, cv1;
+                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[k].x, cv0, hv0);
+                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[k].y, cv1, hv1);
+                if (cur[k].x >= 0) {
+                    const long long r = cur[k].x;
+                    __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv0, hv1));
+                    __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv0, cv1));
+                }
             }
         }
     }
 }
 
-template <int UNITS, bool SPLIT, int CG>
+// CPT: the compacted-row instantiation (LstmArgs::cp_M launches only), so the
+// register allocation of the other launches is not shaped by epilogue_compact
+template <int UNITS, bool SPLIT, int CG, bool CPT = false>
 __global__ void __launch_bounds__(384, 1)
     lstm_gemm_tc(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap mA0,
                  const __grid_constant__ CUtensorMap mAl0, const __grid_constant__ CUtensorMap mB0,
@@ -599,9 +615,9 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem_base = *tmem_slot;
     // compacted rows (one problem): the row count is device data written by the
     // compaction before this launch; the tile loop covers ceil(Mv / TR) row tiles
-    const int Mv = P.prob[0].p.cp_M ? *P.prob[0].p.cp_M : P.prob[0].p.M;
+    const int Mv = CPT ? *P.prob[0].p.cp_M : P.prob[0].p.M;
     int total_tiles = P.total_tiles;
-    if (P.prob[0].p.cp_M) {
+    if (CPT) {
         const int tr = tile_rows(P.prob[0].p);
         const int dyn = (Mv + tr - 1) / tr * P.prob[0].n_tiles;
         total_tiles = dyn < total_tiles ? dyn : total_tiles;
@@ -734,14 +750,16 @@ __global__ void __launch_bounds__(384, 1)
             const int mt = lt / pr.n_tiles, nt = lt - mt * pr.n_tiles;
             const int TRp = tile_rows(p);
             const int row0 = CG == 1 ? mt * TRp : (mt * CG + rank) * TC_BM;  // first row of this CTA's tile
-            if (!p.raw) {
+            if (CPT || !p.raw) {
                 // cell mode: 16x256b TMEM loads, so the 4 lanes of a quad hold 2 consecutive
                 // units each of the same row -- every h / c / split-h store instruction
                 // writes whole 32-byte row segments (half the L1 wavefronts of row-per-lane)
-                if (p.cp_M)
+                // each instantiation compiles only the epilogues its launches use (fan-out
+                // launches run on single CTAs, compacted ones on the CPT instantiation)
+                if constexpr (CPT)
                     epilogue_compact<UNITS, SPLIT, CG>(p, Mv, bars, tmem_base, acc, acc_phase, row0, nt, q, half,
                                                        lane, 2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, stg);
-                else if (p.fan > 1)
+                else if (CG == 1 && p.fan > 1)
                     epilogue_fan<UNITS, SPLIT, CG>(p, bars, tmem_base, acc, acc_phase, row0, TRp, nt, q, half, lane,
                                                    2 * S, 2 * S + AS, Cfg::ACC_COLS, leader, pr, stg, stg_buf);
                 else
@@ -957,6 +975,9 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         if (cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::SMEM) != cudaSuccess)
             return false;
+        if (CG == 1 && cudaFuncSetAttribute(lstm_gemm_tc<UNITS, SPLIT, 1, true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
+            return false;
     }
     constexpr int BROWS = Cfg::BN / CG;  // B rows each CTA loads
     TcParams P{};
@@ -978,8 +999,8 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
             }();
             pr.p.drop_pass = drop;
         }
-        // the fan-out epilogue writes h, c and the split h of the children
-        if (a.fan > 1 && (a.h_out2 != nullptr || a.raw)) return false;
+        // the fan-out epilogue writes h, c and the split h of the children (single CTAs)
+        if (a.fan > 1 && (a.h_out2 != nullptr || a.raw || CG == 2)) return false;
         // compacted rows: one alpha-block problem on single-CTA 128-row tiles, h / c only
         if (a.cp_M && (a1 || CG == 2 || a.kb_alpha == 0 || a.alpha_tile != TC_BM || a.fan > 1 || a.raw ||
                        a.hA_hi || a.h_out2))
@@ -1046,8 +1067,12 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
     const int units = sm_count() / CG;  // persistent: one CTA (pair) per SM (pair)
     const int grid = CG * (tiles < units ? tiles : units);
     if (CG == 1) {
-        lstm_gemm_tc<UNITS, SPLIT, CG><<<grid, 384, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3],
-                                                                          maps[4], maps[5], maps[6], maps[7]);
+        if (a0.cp_M)
+            lstm_gemm_tc<UNITS, SPLIT, 1, true><<<grid, 384, Cfg::SMEM, stream>>>(
+                P, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7]);
+        else
+            lstm_gemm_tc<UNITS, SPLIT, CG><<<grid, 384, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3],
+                                                                              maps[4], maps[5], maps[6], maps[7]);
         return cudaGetLastError() == cudaSuccess;
     }
     cudaLaunchConfig_t cfg{};
