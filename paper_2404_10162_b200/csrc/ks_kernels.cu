@@ -979,7 +979,17 @@ __global__ void __launch_bounds__(256, VP == 32 ? 1 : VP == 16 ? 2 : 4) beam_ste
                     }
                 };
                 if (v4) {
-                    // 128-bit loads, both rows' loads in flight together
+                    // 128-bit loads, both rows' loads in flight together; the next pair's
+                    // rows (or the warp's next config's first pair) are prefetched into L2
+                    // meanwhile
+                    if (!a.h_per_config) {
+                        const long long rn = j0 + 2 < a.H_cur ? r0 + 2
+                                             : (long long)(b + gridDim.x * nwarps) * a.H_cur;
+                        const int nrows = j0 + 2 < a.H_cur ? (j0 + 3 < a.H_cur ? 2 : 1)
+                                          : (b + gridDim.x * nwarps < a.B ? (a.H_cur > 1 ? 2 : 1) : 0);
+                        for (int q = lane; q < NQ * nrows; q += 32)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.h + rn * a.NS + 4 * q));
+                    }
                     const float4* h04 = reinterpret_cast<const float4*>(h0);
                     const float4* h14 = reinterpret_cast<const float4*>(h1);
                     const float4 z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
