@@ -239,6 +239,8 @@ struct ks_engine {
     // (auto: decoders of >= 1024 units, whose h-part MMA hides the longer fan-out
     // epilogue; KS_COMPACT=0 / 1 forces it off / on)
     bool compact = false;
+    bool debug_parents = false;  // KS_DEBUG_PARENTS=1: print distinct parents per position (not with graphs)
+    DevMem dbg;
     DevMem cpbuf;  // [C] counts, [C + 1] bases (last = rows), [R] cfg, prow, cstart, ccount, [R] int2 children
     // KS_TC_PAIR=1: gate GEMMs on CTA pairs (M = 256 tiles, tcgen05 cta_group::2)
     bool pair = false;
@@ -630,6 +632,9 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.use_graphs = !(kg && kg[0] == '0');
         const char* pr = std::getenv("KS_TC_PAIR_AUTO");
         E.pair_auto = !(pr && pr[0] == '0');
+        const char* kdp = std::getenv("KS_DEBUG_PARENTS");
+        E.debug_parents = kdp && kdp[0] == '1';
+        if (E.debug_parents) E.use_graphs = false;
         const char* kcp = std::getenv("KS_COMPACT");
         E.compact = kcp ? kcp[0] == '1' : E.NS >= 1024;
         const char* kc = std::getenv("KS_CHUNK");
@@ -1926,13 +1931,14 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         E.launches++;
         const cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return set_error(KS_ERR_CUDA, std::string("beam launch: ") + cudaGetErrorString(err));
-        if (std::getenv("KS_DEBUG_PARENTS") && pos + 1 < E.T) {
-            static DevMem acc;
-            acc.ensure(16);
-            cudaMemsetAsync(acc.p, 0, 16, s);
-            dbg_parents<<<(unsigned)((C + 255) / 256), 256, 0, s>>>(E.parent[nxt].as<int>(), E.live[nxt].as<unsigned char>(), (int)C, Hn, acc.as<unsigned long long>());
+        if (E.debug_parents && pos + 1 < E.T) {  // diagnostic (KS_DEBUG_PARENTS=1): synchronous
+            if (E.dbg.ensure(16)) return set_error(KS_ERR_CUDA, "debug counter allocation failed");
+            cudaMemsetAsync(E.dbg.p, 0, 16, s);
+            dbg_parents<<<(unsigned)((C + 255) / 256), 256, 0, s>>>(E.parent[nxt].as<int>(),
+                                                                    E.live[nxt].as<unsigned char>(), (int)C, Hn,
+                                                                    E.dbg.as<unsigned long long>());
             unsigned long long hv[2];
-            cudaMemcpyAsync(hv, acc.p, 16, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(hv, E.dbg.p, 16, cudaMemcpyDeviceToHost, s);
             cudaStreamSynchronize(s);
             fprintf(stderr, "pos %d -> %d: rows/config %d, live %.3f, distinct parents %.3f\n", pos, pos + 1, Hn,
                     (double)hv[1] / C, (double)hv[0] / C);
