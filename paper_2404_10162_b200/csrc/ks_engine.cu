@@ -236,9 +236,8 @@ struct ks_engine {
     DevMem encp;  // shared-prefix encoder tables of the current chunk
     // compacted alpha-block positions: the GEMM and attention run on each
     // config's distinct live parents, the epilogue writes their children
-    // (auto: decoders of >= 1024 units, whose h-part MMA hides the longer fan-out
-    // epilogue; KS_COMPACT=0 / 1 forces it off / on)
-    bool compact = false;
+    // (KS_COMPACT=0 disables)
+    bool compact = true;
     bool debug_parents = false;  // KS_DEBUG_PARENTS=1: print distinct parents per position (not with graphs)
     DevMem dbg;
     DevMem cpbuf;  // [C] counts, [C + 1] bases (last = rows), [R] cfg, prow, cstart, ccount, [R] int2 children
@@ -636,7 +635,7 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         E.debug_parents = kdp && kdp[0] == '1';
         if (E.debug_parents) E.use_graphs = false;
         const char* kcp = std::getenv("KS_COMPACT");
-        E.compact = kcp ? kcp[0] == '1' : E.NS >= 1024;
+        E.compact = !(kcp && kcp[0] == '0');
         const char* kc = std::getenv("KS_CHUNK");
         if (kc && std::atoll(kc) > 0) E.chunk = std::atoll(kc);
     }

@@ -438,29 +438,32 @@ __device__ __forceinline__ void epilogue_fan(const LstmArgs& p, uint64_t* bars, 
 // a round's math.
 template <int UNITS, bool SPLIT, int CG>
 __device__ __forceinline__ void epilogue_compact(const LstmArgs& p, int Mv, uint64_t* bars, uint32_t tmem_base,
-                                                 int acc, uint32_t acc_phase, int row0, int nt, int q, int half,
+                                                 int acc, uint32_t acc_phase, int row0, int nt, int q, int grp,
                                                  int lane, int tfull, int tempty, int acc_cols, bool leader,
                                                  float* sp) {
-    constexpr int HU = UNITS / 2;
-    constexpr int NCH = HU / 8;
+    // 16 epilogue warps: warp (q, grp) owns TMEM lane quarter q (32 parents) and units
+    // [grp * UPW, + UPW) of the tile; per 8-unit chunk and per 16-parent half (2 KB of
+    // shared memory per warp) it stages the parents' scaled pre-activations, then its 8
+    // lane quads take those parents' children round-robin
+    constexpr int UPW = UNITS / 4;
+    constexpr int NCH = UPW / 8;
     const int tq = lane >> 2, tcol = 2 * (lane & 3);
-    // the warp's parents: rows wr0 .. wr1-1; their children: entries [e0, e1)
     const int wr0 = row0 + q * 32;
-    const int wr1 = wr0 + 32 < Mv ? wr0 + 32 : Mv;
-    int e0 = 0, e1 = 0;
-    if (wr0 < wr1) {
-        e0 = p.cp_cstart[wr0];
-        e1 = p.cp_cstart[wr1 - 1] + p.cp_ccount[wr1 - 1];
+    int eb[3];  // children entries of the warp's parents [wr0, +16) and [wr0 + 16, +16)
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+        const int r = wr0 + 16 * g;
+        eb[g] = r < Mv ? p.cp_cstart[r] : (Mv > wr0 ? p.cp_cstart[Mv - 1] + p.cp_ccount[Mv - 1] : 0);
     }
+    if (wr0 >= Mv) eb[0] = eb[1] = eb[2] = 0;
     const bool have_cprev = p.c_prev != nullptr;
     tc::mbar_wait(tc::smem_u32(&bars[tfull + acc]), acc_phase);
     tc::fence_after();
     const uint32_t tq_base = tmem_base + ((uint32_t)(q * 32) << 16) + acc * acc_cols;
     constexpr float sc = SPLIT ? kSplitUnscale : 1.0f;
-    const float2 sc2 = make_float2(sc, sc);
 #pragma unroll 1
     for (int c = 0; c < NCH; ++c) {
-        const int uc = half * HU + c * 8;
+        const int uc = grp * UPW + c * 8;
         float v[2][4][4];
 #pragma unroll
         for (int g = 0; g < 2; ++g)
@@ -478,69 +481,59 @@ __device__ __forceinline__ void epilogue_compact(const LstmArgs& p, int Mv, uint
                     tc::mbar_arrive(tc::smem_u32(&bars[tempty + acc]));
             }
         }
-        // parents' scaled pre-activations: sp[row][gate][8 units]
-        __syncwarp();  // the previous chunk's readers are done
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int g = i >> 1, j = i & 1;
-            const int lr = 16 * g + tq + 8 * j;
-#pragma unroll
-            for (int gt = 0; gt < 4; ++gt)
-                *reinterpret_cast<float2*>(sp + (lr * 4 + gt) * 8 + tcol) =
-                    make_float2(v[g][gt][2 * j] * sc, v[g][gt][2 * j + 1] * sc);
-        }
-        __syncwarp();
         const int u0 = nt * UNITS + uc + tcol;
-        auto fetch = [&](int e, int4& en, float2 (&gz)[4], float2& cpv) {
-            if (e < e1) {
-                en = __ldg(p.cp_child + e);
-                const float* G = p.G + ((long long)(p.slot_base + (en.x >= 0 ? en.y : 0)) * 4 * p.H + u0);
 #pragma unroll
-                for (int gt = 0; gt < 4; ++gt) gz[gt] = __ldg(reinterpret_cast<const float2*>(G + gt * p.H));
-                cpv = (have_cprev && en.w >= 0)
-                          ? *reinterpret_cast<const float2*>(p.c_prev + (long long)en.w * p.ldc_prev + u0)
-                          : make_float2(0.f, 0.f);
-            } else {
-                en = make_int4(-1, 0, wr0, -1);
+        for (int g = 0; g < 2; ++g) {
+            // parents wr0 + 16 g + [0, 16): sp[parent][gate][8 units]
+            __syncwarp();  // the previous phase's readers are done
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int lr = tq + 8 * j;
+#pragma unroll
+                for (int gt = 0; gt < 4; ++gt)
+                    *reinterpret_cast<float2*>(sp + (lr * 4 + gt) * 8 + tcol) =
+                        make_float2(v[g][gt][2 * j] * sc, v[g][gt][2 * j + 1] * sc);
             }
-        };
-        // two children per quad per round (entries e and e + 8), the next round's two
-        // in flight during this round's math
-        constexpr int KC = 2;
-        int4 en[KC];
-        float2 gz[KC][4], cpv[KC];
+            __syncwarp();
+            const int e0 = eb[g], e1 = eb[g + 1];
+            const int pr0 = wr0 + 16 * g;
+            auto fetch = [&](int e, int4& en, float2 (&gz)[4], float2& cpv) {
+                if (e < e1) {
+                    en = __ldg(p.cp_child + e);
+                    const float* G = p.G + ((long long)(p.slot_base + (en.x >= 0 ? en.y : 0)) * 4 * p.H + u0);
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            cpv[k] = make_float2(0.f, 0.f);
-            fetch(e0 + tq + 8 * k, en[k], gz[k], cpv[k]);
-        }
+                    for (int gt = 0; gt < 4; ++gt) gz[gt] = __ldg(reinterpret_cast<const float2*>(G + gt * p.H));
+                    cpv = (have_cprev && en.w >= 0)
+                              ? *reinterpret_cast<const float2*>(p.c_prev + (long long)en.w * p.ldc_prev + u0)
+                              : make_float2(0.f, 0.f);
+                } else {
+                    en = make_int4(-1, 0, pr0, -1);
+                }
+            };
+            int4 en;
+            float2 gz[4], cpv = make_float2(0.f, 0.f);
+            fetch(e0 + tq, en, gz, cpv);
 #pragma unroll 1
-        for (int e = e0 + tq; e < e1; e += 8 * KC) {
-            int4 cur[KC];
-            float2 g4[KC][4], cp[KC];
+            for (int e = e0 + tq; e < e1; e += 8) {
+                const int4 cur = en;
+                float2 g4[4];
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                cur[k] = en[k];
-#pragma unroll
-                for (int gt = 0; gt < 4; ++gt) g4[k][gt] = gz[k][gt];
-                cp[k] = cpv[k];
-                fetch(e + 8 * (KC + k), en[k], gz[k], cpv[k]);
-            }
-#pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const int lp = (unsigned)(cur[k].z - wr0) < 32u ? cur[k].z - wr0 : 0;  // dead-child entries: no store
+                for (int gt = 0; gt < 4; ++gt) g4[gt] = gz[gt];
+                const float2 cp = cpv;
+                fetch(e + 8, en, gz, cpv);
+                const int lp = (unsigned)(cur.z - pr0) < 16u ? cur.z - pr0 : 0;  // dead-child entries: no store
                 const float* d = sp + (lp * 4) * 8 + tcol;
                 float2 z[4];
 #pragma unroll
                 for (int gt = 0; gt < 4; ++gt) {
                     const float2 dv = *reinterpret_cast<const float2*>(d + gt * 8);
-                    z[gt] = make_float2(dv.x + g4[k][gt].x, dv.y + g4[k][gt].y);
+                    z[gt] = make_float2(dv.x + g4[gt].x, dv.y + g4[gt].y);
                 }
                 float hv0, hv1, cv0, cv1;
-                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp[k].x, cv0, hv0);
-                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp[k].y, cv1, hv1);
-                if (cur[k].x >= 0) {
-                    const long long r = cur[k].x;
+                lstm_cell_fast(z[0].x, z[1].x, z[2].x, z[3].x, cp.x, cv0, hv0);
+                lstm_cell_fast(z[0].y, z[1].y, z[2].y, z[3].y, cp.y, cv1, hv1);
+                if (cur.x >= 0) {
+                    const long long r = cur.x;
                     __stcs(reinterpret_cast<float2*>(p.h_out + r * p.ldh + u0), make_float2(hv0, hv1));
                     __stcs(reinterpret_cast<float2*>(p.c_out + r * p.ldc + u0), make_float2(cv0, cv1));
                 }
@@ -552,7 +545,7 @@ __device__ __forceinline__ void epilogue_compact(const LstmArgs& p, int Mv, uint
 // CPT: the compacted-row instantiation (LstmArgs::cp_M launches only), so the
 // register allocation of the other launches is not shaped by epilogue_compact
 template <int UNITS, bool SPLIT, int CG, bool CPT = false>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(CPT ? 640 : 384, 1)
     lstm_gemm_tc(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap mA0,
                  const __grid_constant__ CUtensorMap mAl0, const __grid_constant__ CUtensorMap mB0,
                  const __grid_constant__ CUtensorMap mBl0, const __grid_constant__ CUtensorMap mA1,
@@ -583,7 +576,8 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int a = 0; a < AS; ++a) {
             tc::mbar_init(tc::smem_u32(&bars[2 * S + a]), 1);
-            tc::mbar_init(tc::smem_u32(&bars[2 * S + AS + a]), 8 * CG);  // one arrive per epilogue warp (of the pair)
+            // one arrive per epilogue warp (of the pair): 8, or 16 in the compacted instantiation
+            tc::mbar_init(tc::smem_u32(&bars[2 * S + AS + a]), (CPT ? 16 : 8) * CG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -738,7 +732,7 @@ __global__ void __launch_bounds__(384, 1)
         const int q = warp & 3;
         const int half = (warp - 4) >> 2;
         constexpr int HU = UNITS / 2;
-        float* stg = reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES + 256) + (warp - 4) * 1024;
+        float* stg = reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES + 256) + (warp - 4) * (CPT ? 512 : 1024);
         int stg_buf = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -1068,7 +1062,7 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
     const int grid = CG * (tiles < units ? tiles : units);
     if (CG == 1) {
         if (a0.cp_M)
-            lstm_gemm_tc<UNITS, SPLIT, 1, true><<<grid, 384, Cfg::SMEM, stream>>>(
+            lstm_gemm_tc<UNITS, SPLIT, 1, true><<<grid, 640, Cfg::SMEM, stream>>>(
                 P, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7]);
         else
             lstm_gemm_tc<UNITS, SPLIT, CG><<<grid, 384, Cfg::SMEM, stream>>>(P, maps[0], maps[1], maps[2], maps[3],
