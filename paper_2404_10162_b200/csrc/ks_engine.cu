@@ -238,6 +238,8 @@ struct ks_engine {
     // config's distinct live parents, the epilogue writes their children
     // (KS_COMPACT=0 disables)
     bool compact = true;
+    bool compact_pos1 = false;   // KS_COMPACT_POS1=1: position 1 compacted too instead of the fan-out
+                                 // epilogue (measured slower: 1.37 vs 1.12 ms at cfg2)
     bool debug_parents = false;  // KS_DEBUG_PARENTS=1: print distinct parents per position (not with graphs)
     DevMem dbg;
     DevMem cpbuf;  // [C] counts, [C + 1] bases (last = rows), [R] cfg, prow, cstart, ccount, [R] int2 children
@@ -636,6 +638,8 @@ extern "C" ks_status ks_engine_create(const ks_model_desc* d, int32_t device, in
         if (E.debug_parents) E.use_graphs = false;
         const char* kcp = std::getenv("KS_COMPACT");
         E.compact = !(kcp && kcp[0] == '0');
+        const char* kc1 = std::getenv("KS_COMPACT_POS1");
+        E.compact_pos1 = kc1 && kc1[0] == '1';
         const char* kc = std::getenv("KS_CHUNK");
         if (kc && std::atoll(kc) > 0) E.chunk = std::atoll(kc);
     }
@@ -943,7 +947,7 @@ ks_status launch_lstm(ks_engine& E, const LstmArgs& a0, const LstmArgs* a1, DevL
         done = launch_lstm_tc(a0, a1, E.precision, whi(L0), wlo(L0), L1 ? whi(*L1) : nullptr,
                               L1 ? wlo(*L1) : nullptr, E.stream, &n, E.units_now,
                               E.pair_now() || (E.pair_auto && E.units_now == 64 && a0.kb_alpha == 0 &&
-                                               a0.fan <= 1 && (!a1 || (a1->kb_alpha == 0 && a1->fan <= 1))));
+                                               a0.fan <= 1 && !a0.cp_M && (!a1 || (a1->kb_alpha == 0 && a1->fan <= 1))));
         if (!done) return set_error(KS_ERR_CUDA, "tensor-core GEMM launch failed");
     }
     if (!done && a0.K == 0 && launch_lstm_k0(a0, a1, E.num_sms, E.stream)) {
@@ -1694,14 +1698,18 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         // siblings share [ctx | h_prev] and c_prev -- attention and the gate GEMM run
         // once per config (classic ctx operand) and the GEMM epilogue fans each
         // parent row's gates out to its H children (gates + G[slot(child)])
-        const bool fan = pos == 1 && H > 1 && !enc_dec && !hybrid && E.precision != KS_PREC_FP32 &&
-                         E.ctxproj && !E.pair_now();
+        const bool fan_ok = pos == 1 && H > 1 && !enc_dec && !hybrid && E.precision != KS_PREC_FP32 &&
+                            E.ctxproj && !E.pair_now();
+        // with compaction on, position 1 runs as a compacted position (one parent per
+        // config, classic [ctx | h] operand) on the 16-warp compacted epilogue
+        const bool cp1 = fan_ok && E.compact && E.compact_pos1;
+        const bool fan = fan_ok && !cp1;
         const int Mg = fan ? (int)C : M;  // rows of this position's attention and gate GEMM
         // positions >= 2 (alpha blocks): attention and the gate GEMM run on each config's
         // distinct live parents (compacted rows, 128-row tiles), the GEMM epilogue writes
         // their children
-        const bool compact = E.compact && pos >= 2 && !fan && H > 1 && !enc_dec && !hybrid &&
-                             E.precision != KS_PREC_FP32 && E.proj_at(pos, H) && !E.pair_now();
+        const bool compact = cp1 || (E.compact && pos >= 2 && !fan && H > 1 && !enc_dec && !hybrid &&
+                                     E.precision != KS_PREC_FP32 && E.proj_at(pos, H) && !E.pair_now());
         int *cp_cnt = nullptr, *cp_base = nullptr, *cp_cfg = nullptr, *cp_prow = nullptr, *cp_cst = nullptr,
             *cp_ccn = nullptr;
         int4* cp_child = nullptr;
@@ -1750,7 +1758,7 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
         aa.alpha_sparse = (aa.kalpha && alpha_fill_H == H) ? 1 : 0;
         alpha_fill_H = aa.kalpha ? H : -1;
         if (compact) {
-            aa.kalpha = kal_c;
+            aa.kalpha = cp1 ? 0 : kal_c;
             aa.alpha_tile = 128;
             aa.alpha_sparse = 0;
             alpha_fill_H = -1;  // the next position rewrites its layout in full
@@ -1801,6 +1809,16 @@ ks_status run_chunk(ks_engine& E, int64_t C, int64_t cfg_base, int k, bool greed
             p.ldah = Kd;
             p.ldw = Kd;
             p.wcol = 0;
+        } else if (cp1) {
+            // position 1 compacted: classic [ctx | h_prev] rows of the roots
+            p.parent = nullptr;
+            p.alpha_tile = 128;
+            p.cp_M = cp_base + C;
+            p.cp_cfg = cp_cfg;
+            p.cp_prow = cp_prow;
+            p.cp_cstart = cp_cst;
+            p.cp_ccount = cp_ccn;
+            p.cp_child = cp_child;
         } else if (!fan && E.proj_at(pos, H)) {
             // [alpha block | h_prev] . [P^T | W_h]  (ctx . W_ctx = sum_t alpha_t P_t)
             const int kal = E.alpha_cols_of(H);

@@ -996,7 +996,7 @@ bool launch_impl(const LstmArgs& a0, const LstmArgs* a1, const __half* Wh0, cons
         // the fan-out epilogue writes h, c and the split h of the children (single CTAs)
         if (a.fan > 1 && (a.h_out2 != nullptr || a.raw || CG == 2)) return false;
         // compacted rows: one alpha-block problem on single-CTA 128-row tiles, h / c only
-        if (a.cp_M && (a1 || CG == 2 || a.kb_alpha == 0 || a.alpha_tile != TC_BM || a.fan > 1 || a.raw ||
+        if (a.cp_M && (a1 || CG == 2 || (a.kb_alpha > 0 && a.alpha_tile != TC_BM) || a.fan > 1 || a.raw ||
                        a.hA_hi || a.h_out2))
             return false;
         {

@@ -2,9 +2,9 @@
 ks_gemm_tc.cu epilogue_compact): attention and the gate GEMM on each config's
 distinct live parents, the epilogue writing their children.  The decodes are
 checked against the REFERENCE's decodes (tests/golden/baseline_parity.npz) with
-compaction forced on and off, whatever the engine's auto rule picks for the
-model, and against the fp64 oracle on random models (small chunks, exhaustion,
-beam widths 2..16)."""
+compaction on (the default) and off, and with position 1 compacted too
+(KS_COMPACT_POS1=1), and against the fp64 oracle on random models (small
+chunks, exhaustion, beam widths 2..16)."""
 import os
 
 import numpy as np
@@ -18,18 +18,20 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs 
 FX = os.path.join(ROOT, "tests", "golden", "baseline_parity.npz")
 
 
-def _engine(path, prec, compact):
+def _engine(path, prec, compact, pos1=False):
     from paper_2404_10162_b200._cabi import Engine
 
-    old = os.environ.get("KS_COMPACT")
-    os.environ["KS_COMPACT"] = "1" if compact else "0"
+    env = {"KS_COMPACT": "1" if compact else "0", "KS_COMPACT_POS1": "1" if pos1 else "0"}
+    old = {name: os.environ.get(name) for name in env}
+    os.environ.update(env)
     try:
         return Engine(path, 0, prec)
     finally:
-        if old is None:
-            os.environ.pop("KS_COMPACT")
-        else:
-            os.environ["KS_COMPACT"] = old
+        for name, val in old.items():
+            if val is None:
+                os.environ.pop(name)
+            else:
+                os.environ[name] = val
 
 
 def _ref(cfg):
@@ -37,11 +39,11 @@ def _ref(cfg):
     return {k.split("/", 1)[1]: fx[k] for k in fx.files if k.startswith(cfg + "/")}
 
 
-@pytest.mark.parametrize("compact", [True, False])
+@pytest.mark.parametrize("compact,pos1", [(True, False), (True, True), (False, False)])
 @pytest.mark.parametrize("prec", ["f16x3", "bf16"])
-def test_cfg2_fixtures(compact, prec):
+def test_cfg2_fixtures(compact, pos1, prec):
     r = _ref("cfg2")
-    e = _engine(W.DEFAULT_CKPT, prec, compact)
+    e = _engine(W.DEFAULT_CKPT, prec, compact, pos1)
     g = e.beam(r["tok"], 5, r["desc"], W.predicate_dicts(W.DEFAULT_CKPT))
     if prec == "bf16":  # reduced precision: agreement floor only
         assert (g["tokens"][:, 0] == r["tokens"][:, 0]).all(axis=1).mean() >= 0.97
@@ -61,8 +63,8 @@ def test_cfg5_fixtures(compact):
     assert not bad, f"{len(bad)} mismatching of {n} compared ({ties} tie-adjacent); first {bad[:8]}"
 
 
-@pytest.mark.parametrize("case", [0, 1, 3, 4, 7])
-def test_random_models_compacted(case, tmp_path):
+@pytest.mark.parametrize("case,pos1", [(0, False), (1, True), (3, False), (4, True), (7, False)])
+def test_random_models_compacted(case, pos1, tmp_path):
     import paper_2404_10162_b200 as ks
     from oracle.oracle import OracleModel
     from tests.test_fuzz_gpu import CASES, _model
@@ -75,7 +77,7 @@ def test_random_models_compacted(case, tmp_path):
     budget = float(sum(np.median(v) for v in o.values))
     preds = [o.membership(), o.budget({nm: 1.0 for nm in o.names}, budget)]
     a = o.beam(tok, k, None, preds, threads=8)
-    e = _engine(path, prec, True)
+    e = _engine(path, prec, True, pos1)
     e.set_chunk(97)
     g = e.beam(tok, k, None, preds)
     n, ties, bad = compare_beams(g, a)
