@@ -477,7 +477,10 @@ def run_b200(args):
                          "kernel": ("lstm_gemm_tc (gate GEMMs + fused LSTM cell, incl. the context projection), "
                                     "all launches of one step" if args.precision != "fp32" else "lstm_step_simt"),
                          "peak_kind": f"{peak_kind} bf16 dense, sustained (MEASURED_PEAKS.json; burst {bf16_burst:g})",
-                         "algorithmic": "reference formula (SURVEY 8(d)) FLOPs / summed launch time",
+                         "algorithmic": "reference formula (SURVEY 8(d)) FLOPs / summed launch time; the engine "
+                                        "skips part of those FLOPs (projected context, position-1 fan-out, parent "
+                                        "compaction: DESIGN 5.1-5.1d), so frac can exceed what the tensor pipe "
+                                        "issues (mma_issued_frac, 3 MMA passes per F16X3 product)",
                          "useful_flops_per_launch": launch_flops, "launch_ms": launch_ms,
                          "launches_averaged": int(len(each_ms)),
                          "mma_issued_tflops": issued, "mma_issued_frac": issued / bf16_peak,
